@@ -1,0 +1,166 @@
+/*
+ * hlq_b200.h -- C ABI of the B200 (sm_100a) HLQ backward path.
+ *
+ * This is the drop-in boundary for the reference's HLQ hot path
+ * (/root/reference/pkg/src/hlq).  The reference is a pure-Python/numpy package
+ * with no FFI; its interface for this path is a set of Python functions.  Each
+ * entry point below replaces one of them (file:line cited per function) and is
+ * what a ctypes / cffi binding of that function would call -- see
+ * INTEGRATION.md for the binding a maintainer would add.
+ *
+ * Conventions
+ *  - every pointer is a DEVICE pointer unless stated otherwise; the caller
+ *    allocates every output and workspace (the library never allocates device
+ *    memory, so every call is CUDA-graph-capture safe);
+ *  - all work is enqueued on `stream` (a cudaStream_t passed as void*);
+ *  - shapes / strides are int64_t element counts, row-major;
+ *  - return value is an hlq_status; hlq_last_error() gives a message
+ *    (thread-local).  Status codes map onto the reference's exception classes
+ *    (errors.py:4-13): DIMENSION -> DimensionError, PARAMETER -> ParameterError,
+ *    STATE -> StateError, NONFINITE -> ValueError.
+ *  - "codes" are int8 quantizer outputs; operand layouts are K-major (each row
+ *    holds one output row/column's contraction axis), which is the layout
+ *    tcgen05 consumes directly.
+ *  - block size is 16 (hadamard.py:19, the HLQ design point); `bitmap` has bit
+ *    i set iff Walsh basis i is kept (hadamard.py:97-106).
+ */
+#ifndef HLQ_B200_H
+#define HLQ_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#if defined(__GNUC__)
+#define HLQ_API __attribute__((visibility("default")))
+#else
+#define HLQ_API
+#endif
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum {
+  HLQ_OK = 0,
+  HLQ_ERR_DIMENSION = 1, /* errors.py:4  DimensionError */
+  HLQ_ERR_PARAMETER = 2, /* errors.py:8  ParameterError */
+  HLQ_ERR_STATE = 3,     /* errors.py:12 StateError */
+  HLQ_ERR_NONFINITE = 4, /* quantize.py:138-139 ValueError */
+  HLQ_ERR_CUDA = 5
+} hlq_status;
+
+typedef enum { HLQ_F32 = 0, HLQ_BF16 = 1 } hlq_dtype;
+
+typedef enum {
+  HLQ_EPI_EXACT = 0, /* out = f32(f64(acc) * (f64(f32(sa*sb)) * extra)), quantize.py:181-187 */
+  HLQ_EPI_FAST = 1   /* out = f32(acc) * f32(sa*sb*extra); training path, fp32 or bf16 out */
+} hlq_epilogue;
+
+/* Library identification. */
+HLQ_API const char* hlq_version(void);
+/* Message of the last failing call on this thread ("" if none). */
+HLQ_API const char* hlq_last_error(void);
+/* 1 when a sm_100 device and the driver entry points are usable, else 0. */
+HLQ_API int hlq_device_ok(void);
+
+/* ---------------------------------------------------------------------------
+ * Stage primitives
+ * ------------------------------------------------------------------------- */
+
+/* Q_bits( block-FWHT along the contiguous axis of src (rows x cols) ).
+ * Replaces `_block_axis(gy, 2, plan)` + `quant_pseudo_stochastic` on the gx
+ * left operand (backprop.py:212-220,362,367; quantize.py:128-145).
+ * Writes codes (rows x pad16(cols), leading dim ld_dst >= pad16(cols), a
+ * multiple of 16) and the fp32 scale.  amax_ws: 4-byte device scratch that
+ * also carries the per-tensor amax bits out.  bits in {4, 8}. */
+HLQ_API int hlq_quantize_ht_cols(const void* src, int dtype, int64_t rows, int64_t cols, int64_t ld_src,
+                         int bits, uint32_t* amax_ws, int8_t* dst, int64_t ld_dst,
+                         float* scale_out, void* stream);
+
+/* Q_bits( rank-r block projection along the ROW axis of src ), codes written
+ * transposed: dst[c * ld_dst + (s * nblk + blk) * r + j], nblk = ceil(rows/16).
+ * src is `segs` segments of (rows x cols) with row stride ld_src and segment
+ * stride seg_src.  Replaces `_project_axis` + `quant_pseudo_stochastic`
+ * (backprop.py:223-234; acbp_compress :373-385; hlq_grad_weight :401-407) and,
+ * with bitmap 0xFFFF, `_block_axis(w, 0, plan)` (:363). */
+HLQ_API int hlq_quantize_proj_rows(const void* src, int dtype, int64_t segs, int64_t rows, int64_t cols,
+                           int64_t ld_src, int64_t seg_src, uint32_t bitmap, int bits,
+                           uint32_t* amax_ws, int8_t* dst, int64_t ld_dst, float* scale_out,
+                           void* stream);
+
+/* The two passes of hlq_quantize_proj_rows, separately, for the data-parallel
+ * global-scale mode: _amax accumulates (atomic max, no reset) the transformed
+ * amax into *amax_bits; callers all-reduce(MAX) it across ranks, then _quant
+ * quantizes with scale = amax / qmax (quantize.py:94-100). */
+HLQ_API int hlq_proj_rows_amax(const void* src, int dtype, int64_t segs, int64_t rows, int64_t cols,
+                       int64_t ld_src, int64_t seg_src, uint32_t bitmap, uint32_t* amax_bits,
+                       void* stream);
+HLQ_API int hlq_proj_rows_quant(const void* src, int dtype, int64_t segs, int64_t rows, int64_t cols,
+                        int64_t ld_src, int64_t seg_src, uint32_t bitmap, int bits,
+                        const uint32_t* amax_bits, int8_t* dst, int64_t ld_dst, float* scale_out,
+                        void* stream);
+
+/* D[m, n] = sum_k A[m, k] * B[n, k] on int8 codes (tcgen05 kind::i8, int32 in
+ * TMEM), dequantized with the fused epilogue.  Replaces `int_matmul` +
+ * `int_matmul_dequant` (quantize.py:152-187).  lda/ldb are byte strides,
+ * multiples of 16; sa/sb are device fp32 scales.  out may be NULL; acc_out
+ * (int32, M x N, ld_acc) may be NULL -- it exposes the exact accumulator for
+ * parity checks.  Fails with PARAMETER if K * qmax_a * qmax_b could overflow
+ * int32 (pass the operands' bit widths). */
+HLQ_API int hlq_gemm_i8(const int8_t* A, int64_t lda, const int8_t* B, int64_t ldb, int64_t M, int64_t N,
+                int64_t K, int bits_a, int bits_b, const float* sa, const float* sb, double extra,
+                int epilogue, void* out, int out_dtype, int64_t ldo, int32_t* acc_out,
+                int64_t ld_acc, void* stream);
+
+/* Grouped form: the contraction runs over `groups` stacked K panels,
+ * D[m, n] = sum_g sum_k A[g][m, k] * B[g][n, k], panel g of A at byte offset
+ * g * a_gstride (likewise B).  This is the batch-axis projection with L > 1,
+ * whose reference K index is (block, basis, l) (backprop.py:223-234,402-403). */
+HLQ_API int hlq_gemm_i8_grouped(const int8_t* A, int64_t lda, int64_t a_gstride, const int8_t* B,
+                        int64_t ldb, int64_t b_gstride, int64_t M, int64_t N, int64_t K,
+                        int64_t groups, int bits_a, int bits_b, const float* sa, const float* sb,
+                        double extra, int epilogue, void* out, int out_dtype, int64_t ldo,
+                        int32_t* acc_out, int64_t ld_acc, void* stream);
+
+/* ---------------------------------------------------------------------------
+ * Reference-function equivalents (whole calls)
+ * ------------------------------------------------------------------------- */
+
+/* Payload geometry of acbp_compress for x of shape (B, L, I):
+ *   axis 1 (tokens): I rows of K = B * ceil(L/16) * r codes;
+ *   axis 0 (batch):  L*I rows (row l*I + i) of K = ceil(B/16) * r codes.
+ * hlq_acbp_k returns K (per row), hlq_acbp_rows the row count. */
+HLQ_API int64_t hlq_acbp_k(int64_t B, int64_t L, int axis, int rank);
+HLQ_API int64_t hlq_acbp_rows(int64_t L, int64_t I, int axis);
+
+/* backprop.py:373-385  acbp_compress(x, plan, bits, pad_small_axes).
+ * x is (B, L, I); axis from ht_axis_for (0 = batch, 1 = tokens).  Payload is
+ * written K-major, payload[row * ld_payload + k] (the reference's (K, I)
+ * payload, transposed; see hlq_acbp_k).  amax_ws: 4-byte scratch. */
+HLQ_API int hlq_acbp_compress(const void* x, int dtype, int64_t B, int64_t L, int64_t I, int axis,
+                      uint32_t bitmap, int bits, int8_t* payload, int64_t ld_payload,
+                      float* scale_out, uint32_t* amax_ws, void* stream);
+
+/* Workspace bytes needed by hlq_hq_grad_input / hlq_grad_weight. */
+HLQ_API size_t hlq_hq_grad_input_ws(int64_t T, int64_t O, int64_t I);
+HLQ_API size_t hlq_grad_weight_ws(int64_t B, int64_t L, int64_t O, int axis, int rank);
+
+/* backprop.py:350-370  hq_grad_input(gy, w, bits): dX (T x I) from gy (T x O)
+ * and the fp32 weight W (O x I).  dx_dtype HLQ_F32 with HLQ_EPI_EXACT
+ * reproduces the reference bit for bit. */
+HLQ_API int hlq_hq_grad_input(const void* gy, int gy_dtype, int64_t T, int64_t O, const float* w, int64_t I,
+                      int bits, void* dx, int dx_dtype, int epilogue, void* ws, size_t ws_bytes,
+                      void* stream);
+
+/* backprop.py:388-410  hlq_grad_weight(acbp, gy, bits): dW (O x I) from the
+ * ACBP payload (K-major, as written by hlq_acbp_compress) and gy (B, L, O).
+ * extra is the reference's 1/B (pass 1.0 under a torch mean loss). */
+HLQ_API int hlq_grad_weight(const int8_t* payload, int64_t ld_payload, const float* x_scale,
+                    const void* gy, int gy_dtype, int64_t B, int64_t L, int64_t O, int64_t I,
+                    int axis, uint32_t bitmap, int bits, double extra, void* dw, int dw_dtype,
+                    int epilogue, void* ws, size_t ws_bytes, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* HLQ_B200_H */

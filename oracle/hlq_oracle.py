@@ -1,0 +1,271 @@
+"""CPU oracle for the HLQ backward path -- TEST INFRASTRUCTURE, NOT PRODUCT CODE.
+
+This module is a numpy restatement of the reference's algorithm for the one hot
+path this repository accelerates (HLQ backward for Linear / Conv2d plus the
+forward-time ACBP compression).  It exists only to *check* the CUDA path:
+
+* only ``tests/``, ``__graft_entry__.smoke()`` and ``bench.py``'s
+  ``cpu_baseline`` / ``--impl reference`` leg may import it;
+* nothing under ``paper_2406_15102_b200/`` imports it -- the product path has
+  no CPU fallback and fails loudly when its CUDA library is missing.
+
+Parity pinning: every function below is validated bit-for-bit against golden
+vectors produced by the reference itself (``tests/golden/make_golden.py``
+imports ``/root/reference/pkg/src/hlq`` in the build container and stores the
+outputs under ``tests/golden/*.npz``; ``tests/test_oracle_golden.py`` checks
+this module against them).
+
+Reference anchors (paths relative to ``/root/reference/pkg/src/hlq``):
+  hadamard.py:24-49    sequency ordering / default basis sets
+  hadamard.py:121-134  orthonormal radix-2 FWHT, stage order h = 1, 2, 4, ...
+  tensor.py:91-95,125-135  zero padding to a block multiple
+  backprop.py:179-190  projection-axis rule
+  backprop.py:212-234  block transform / low-rank projection along one axis
+  quantize.py:94-100   per-tensor symmetric scale
+  quantize.py:128-145  pseudo-stochastic rounding (low 11 bits as the draw)
+  quantize.py:152-187  exact integer GEMM + fp64 dequant epilogue
+  backprop.py:350-447  hq_grad_input / acbp_compress / hlq_grad_weight / hlq_backward
+  harness/layers.py:96-158  conv lowering (im2col / col2im)
+"""
+from __future__ import annotations
+
+import numpy as np
+
+F32 = np.float32
+QMAX = {4: 7, 8: 127}
+
+
+class OracleError(ValueError):
+    pass
+
+
+# ---------------------------------------------------------------------------
+# basis sets (hadamard.py:24-49)
+# ---------------------------------------------------------------------------
+
+def sequency_of_row(i: int, n: int) -> int:
+    """Sign changes of natural-order Walsh row ``i``: Gray-decode of the
+    bit-reversed index (hadamard.py:34-43)."""
+    k = n.bit_length() - 1
+    rev = 0
+    for b in range(k):
+        if i >> b & 1:
+            rev |= 1 << (k - 1 - b)
+    g, shift = rev, 1
+    while shift < 32:
+        g ^= g >> shift
+        shift <<= 1
+    return g
+
+
+def lowest_sequency_bases(n: int, r: int) -> tuple:
+    order = sorted(range(n), key=lambda i: (sequency_of_row(i, n), i))
+    return tuple(sorted(order[:r]))
+
+
+# ---------------------------------------------------------------------------
+# transforms (hadamard.py:121-134, backprop.py:212-234)
+# ---------------------------------------------------------------------------
+
+def fwht_blocks(a: np.ndarray) -> np.ndarray:
+    """Orthonormal FWHT over the last axis (length n, power of two), fp32.
+
+    Stage order h = 1, 2, 4, ... with (lower, upper) = (a + b, a - b) for
+    every pair (i, i + h), i & h == 0, then one multiply by fp32(1/sqrt(n)).
+    The stage order is part of the bit-exact contract (hadamard.py:125-133).
+    """
+    x = np.array(a, dtype=F32, copy=True)
+    n = x.shape[-1]
+    h = 1
+    while h < n:
+        lo = np.array([i for i in range(n) if not i & h])
+        hi = lo + h
+        a_, b_ = x[..., lo], x[..., hi]
+        x[..., lo] = a_ + b_
+        x[..., hi] = a_ - b_
+        h <<= 1
+    return x * F32(1.0 / np.sqrt(n))
+
+
+def pad_to(a: np.ndarray, axis: int, n: int) -> np.ndarray:
+    ext = a.shape[axis]
+    tgt = -(-ext // n) * n
+    if tgt == ext:
+        return a
+    widths = [(0, 0)] * a.ndim
+    widths[axis] = (0, tgt - ext)
+    return np.pad(a, widths)
+
+
+def transform_axis(a: np.ndarray, axis: int, n: int, bases=None) -> np.ndarray:
+    """Pad ``axis`` to a multiple of n, block-FWHT it, and (when ``bases`` is
+    given) keep only those coefficient rows of every block."""
+    p = pad_to(np.asarray(a, dtype=F32), axis, n)
+    m = np.moveaxis(p, axis, -1)
+    lead = m.shape[:-1]
+    nb = m.shape[-1] // n
+    c = fwht_blocks(m.reshape(*lead, nb, n))
+    if bases is not None and len(bases) != n:
+        c = c[..., list(bases)]
+    out = c.reshape(*lead, nb * c.shape[-1])
+    return np.ascontiguousarray(np.moveaxis(out, -1, axis))
+
+
+def proj_axis_rule(B: int, L: int, n: int, pad_small_axes: bool = False) -> int:
+    """backprop.py:179-190: L when L >= n, else B when B >= n."""
+    if L >= n:
+        return 1
+    if B >= n:
+        return 0
+    if not pad_small_axes:
+        raise OracleError(f"L={L} and B={B} both below block {n}")
+    return 1 if L >= B else 0
+
+
+# ---------------------------------------------------------------------------
+# quantizer + integer GEMM (quantize.py:94-187)
+# ---------------------------------------------------------------------------
+
+def quantize(v: np.ndarray, bits: int):
+    """Per-tensor symmetric pseudo-stochastic quantizer -> (int8 codes, f32 scale)."""
+    qmax = QMAX[bits]
+    v = np.ascontiguousarray(v, dtype=F32)
+    if not np.isfinite(v).all():
+        raise OracleError("non-finite input")
+    amax = F32(np.abs(v).max()) if v.size else F32(0)
+    scale = F32(amax / F32(qmax))
+    if scale == 0:
+        scale = F32(1.0)
+    q = v / scale
+    lo = np.floor(q)
+    draw = (v.view(np.uint32) & np.uint32(0x7FF)).astype(F32)
+    bump = ((q - lo) * F32(2048.0)) > draw
+    codes = np.clip(lo + bump.astype(F32), -qmax, qmax).astype(np.int8)
+    return codes, scale
+
+
+def int_gemm(a: np.ndarray, b: np.ndarray) -> np.ndarray:
+    """Exact sum of int8 products; fp64 BLAS is exact below 2**53."""
+    return (a.astype(np.float64) @ b.astype(np.float64)).astype(np.int64)
+
+
+def dequant(acc: np.ndarray, sa, sb, extra: float = 1.0) -> np.ndarray:
+    comb = F32(F32(sa) * F32(sb))
+    return (acc.astype(np.float64) * (np.float64(comb) * float(extra))).astype(F32)
+
+
+# ---------------------------------------------------------------------------
+# the HLQ path (backprop.py:350-447)
+# ---------------------------------------------------------------------------
+
+def hq_grad_input(gy3: np.ndarray, w: np.ndarray, bits: int = 4, n: int = 16,
+                  stages: dict | None = None) -> np.ndarray:
+    B, L, O = gy3.shape
+    I = w.shape[1]
+    ghat = transform_axis(gy3, 2, n).reshape(B * L, -1)
+    what = transform_axis(w, 0, n)
+    cg, sg = quantize(ghat, bits)
+    cw, sw = quantize(what, bits)
+    acc = int_gemm(cg, cw)
+    out = dequant(acc, sg, sw).reshape(B, L, I)
+    if stages is not None:
+        stages.update(gx_codes_g=cg, gx_scale_g=sg, gx_codes_w=cw, gx_scale_w=sw, gx_acc=acc)
+    return out
+
+
+def acbp_compress(x3: np.ndarray, bases, bits: int = 8, n: int = 16,
+                  pad_small_axes: bool = False):
+    """Forward-time projection + quantization of X -> (payload (K, I), scale, axis)."""
+    B, L, I = x3.shape
+    axis = proj_axis_rule(B, L, n, pad_small_axes)
+    proj = transform_axis(x3, axis, n, bases)
+    codes, scale = quantize(proj, bits)
+    return codes.reshape(-1, I), scale, axis
+
+
+def hlq_grad_weight(payload: np.ndarray, x_scale, axis: int, gy3: np.ndarray,
+                    bases, bits: int = 8, n: int = 16, extra: float | None = None,
+                    stages: dict | None = None) -> np.ndarray:
+    B, L, O = gy3.shape
+    gproj = transform_axis(gy3, axis, n, bases).reshape(-1, O)
+    if gproj.shape[0] != payload.shape[0]:
+        raise OracleError("projected extents differ")
+    cg, sg = quantize(np.ascontiguousarray(gproj.T), bits)
+    acc = int_gemm(cg, payload)
+    out = dequant(acc, sg, x_scale, 1.0 / B if extra is None else extra)
+    if stages is not None:
+        stages.update(gw_codes_g=cg, gw_scale_g=sg, gw_acc=acc)
+    return out
+
+
+def hlq_backward(x3: np.ndarray, w: np.ndarray, gy3: np.ndarray, rank: int = 8,
+                 bits_gx: int = 4, bits_gw: int = 8, n: int = 16, bases=None,
+                 pad_small_axes: bool = False, extra: float | None = None,
+                 stages: dict | None = None):
+    """ACBP branch of strategy_backward (backprop.py:416-430): gw then gx."""
+    bases = lowest_sequency_bases(n, rank) if bases is None else tuple(bases)
+    payload, sx, axis = acbp_compress(x3, bases, bits_gw, n, pad_small_axes)
+    if stages is not None:
+        stages.update(x_codes=payload, x_scale=sx, axis=axis)
+    gw = hlq_grad_weight(payload, sx, axis, gy3, bases, bits_gw, n, extra, stages)
+    gx = hq_grad_input(gy3, w, bits_gx, n, stages)
+    return gx, gw
+
+
+# ---------------------------------------------------------------------------
+# conv lowering (harness/layers.py:96-158)
+# ---------------------------------------------------------------------------
+
+def conv_out_hw(H: int, W: int, k: int, s: int, p: int):
+    return (H + 2 * p - k) // s + 1, (W + 2 * p - k) // s + 1
+
+
+def im2col(x: np.ndarray, k: int, s: int, p: int) -> np.ndarray:
+    """(B, C, H, W) -> (B, Ho*Wo, C*k*k); column index c*k*k + i*k + j."""
+    B, C, H, W = x.shape
+    Ho, Wo = conv_out_hw(H, W, k, s, p)
+    xp = np.pad(x, ((0, 0), (0, 0), (p, p), (p, p)))
+    taps = np.stack([np.stack([xp[:, :, i:i + s * Ho:s, j:j + s * Wo:s] for j in range(k)], 2)
+                     for i in range(k)], 2)          # (B, C, k, k, Ho, Wo)
+    return np.ascontiguousarray(taps.transpose(0, 4, 5, 1, 2, 3)).reshape(B, Ho * Wo, C * k * k)
+
+
+def col2im(cols: np.ndarray, x_shape, k: int, s: int, p: int) -> np.ndarray:
+    """Scatter-add inverse of im2col, taps accumulated in (i, j) order in the
+    column dtype (fp32 for the dequantized path, int64 for accumulators)."""
+    B, C, H, W = x_shape
+    Ho, Wo = conv_out_hw(H, W, k, s, p)
+    c6 = cols.reshape(B, Ho, Wo, C, k, k)
+    acc = np.zeros((B, C, H + 2 * p, W + 2 * p), dtype=cols.dtype)
+    for i in range(k):
+        for j in range(k):
+            acc[:, :, i:i + s * Ho:s, j:j + s * Wo:s] += c6[..., i, j].transpose(0, 3, 1, 2)
+    return np.ascontiguousarray(acc[:, :, p:p + H, p:p + W])
+
+
+def conv2d_hlq_backward(x: np.ndarray, w4: np.ndarray, gy: np.ndarray, stride: int, pad: int,
+                        rank: int = 8, bits_gx: int = 4, bits_gw: int = 8, n: int = 16,
+                        extra: float | None = None, stages: dict | None = None):
+    """Conv2d.forward's ACBP + Conv2d.backward (layers.py:141-158)."""
+    O, C, k, _ = w4.shape
+    B = x.shape[0]
+    cols = im2col(x, k, stride, pad)
+    gy3 = np.ascontiguousarray(gy.transpose(0, 2, 3, 1).reshape(B, -1, O))
+    gcols, gw = hlq_backward(cols, w4.reshape(O, -1), gy3, rank, bits_gx, bits_gw, n,
+                             extra=extra, stages=stages)
+    gx = col2im(gcols, x.shape, k, stride, pad)
+    return gx, gw.reshape(O, C, k, k)
+
+
+# ---------------------------------------------------------------------------
+# synthetic inputs
+# ---------------------------------------------------------------------------
+
+def make_inputs(seed: int, x_shape, w_shape, gy_shape):
+    rng = np.random.default_rng(seed)
+    x = rng.standard_normal(x_shape).astype(F32)
+    fan_in = int(np.prod(w_shape[1:]))
+    w = (rng.standard_normal(w_shape) * np.sqrt(2.0 / fan_in)).astype(F32)
+    gy = (rng.lognormal(0.0, 1.4, size=gy_shape) * rng.choice([-1.0, 1.0], size=gy_shape)
+          * 1e-3).astype(F32)
+    return x, w, gy

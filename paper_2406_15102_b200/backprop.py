@@ -1,0 +1,321 @@
+"""HLQ backward for linear (or im2col'd convolution) layers on B200.
+
+Same public surface as the reference module
+/root/reference/pkg/src/hlq/backprop.py (names, argument meaning, error
+classes), over torch CUDA tensors:
+
+    acbp_compress(x, plan, bits=8, rng=None, pad_small_axes=False) -> ACBPActivation
+    hq_grad_input(gy, w, bits, rng=None, block=16) -> Tensor (B, L, I)
+    hlq_grad_weight(acbp, gy, bits=8, rng=None) -> Tensor (O, I)
+    strategy_backward(x_or_acbp, w, gy, strategy, rng=None) -> GradPair
+    hlq_backward(x_or_acbp, w, gy, strategy=None, rng=None) -> GradPair
+
+Every quantized stage runs in libhlq_b200.so (sm_100a): block-Hadamard /
+projection + amax + pseudo-stochastic quantizer kernels and the tcgen05
+int8 GEMM with the fused dequant epilogue.  Outputs are fp32 and, with the
+exact epilogue used here, bit-identical to the reference on the same inputs.
+
+Differences from the reference, by design:
+  * ``rng`` (true stochastic rounding, quantize.py:114-125) is not implemented
+    on the GPU yet: passing one raises ParameterError.
+  * the ACBP payload is stored K-major ((I, K) instead of (K, I)), which is
+    the tcgen05 operand layout; ``ACBPActivation.reference_payload()``
+    returns the reference layout.
+"""
+from __future__ import annotations
+
+from dataclasses import dataclass, field, replace
+
+import torch
+
+from . import ops
+from .errors import DimensionError, ParameterError, StateError
+from .hadamard import DEFAULT_BLOCK, DEFAULT_RANK, HadamardPlan, lowest_sequency_bases
+
+GX_MODES = ("fp", "quant", "ht_quant", "lowrank")
+GW_MODES = ("fp", "quant", "ht_quant", "lowrank", "lowrank_quant")
+
+
+@dataclass(frozen=True)
+class GradPair:
+    grad_input: torch.Tensor
+    grad_weight: torch.Tensor
+
+
+@dataclass(frozen=True)
+class PathSpec:
+    mode: str
+    bits: int | None = None
+
+
+@dataclass(frozen=True)
+class BackwardStrategy:
+    """Per-layer backward configuration (backprop.py:66-155)."""
+
+    name: str
+    grad_input_path: PathSpec
+    grad_weight_path: PathSpec
+    plan: HadamardPlan = field(default_factory=HadamardPlan)
+    pad_small_axes: bool = False
+    store_compressed: bool = True
+
+    def __post_init__(self):
+        gx, gw = self.grad_input_path, self.grad_weight_path
+        if gx.mode not in GX_MODES:
+            raise ParameterError(f"unknown grad_input mode {gx.mode!r}")
+        if gw.mode not in GW_MODES:
+            raise ParameterError(f"unknown grad_weight mode {gw.mode!r}")
+        for spec in (gx, gw):
+            if spec.mode in ("fp", "lowrank") and spec.bits is not None:
+                raise ParameterError(f"mode {spec.mode!r} does not quantize; bits must be None")
+            if spec.bits is not None and spec.bits not in (4, 8):
+                raise ParameterError(f"bits must be 4 or 8, got {spec.bits}")
+
+    @classmethod
+    def vanilla(cls) -> "BackwardStrategy":
+        return cls("vanilla", PathSpec("fp"), PathSpec("fp"))
+
+    @classmethod
+    def hlq(cls, bits_gx: int = 4, bits_gw: int = 8, rank: int = DEFAULT_RANK,
+            block: int = DEFAULT_BLOCK) -> "BackwardStrategy":
+        plan = HadamardPlan(block_size=block, basis_indices=lowest_sequency_bases(block, rank))
+        return cls("hlq", PathSpec("ht_quant", bits_gx), PathSpec("lowrank_quant", bits_gw), plan)
+
+    def with_warmup_bits(self, bits: int = 8) -> "BackwardStrategy":
+        def widen(spec: PathSpec) -> PathSpec:
+            return spec if spec.bits is None else replace(spec, bits=bits)
+        return replace(self, name=f"{self.name}[warmup-int{bits}]",
+                       grad_input_path=widen(self.grad_input_path),
+                       grad_weight_path=widen(self.grad_weight_path))
+
+    def with_plan(self, plan: HadamardPlan) -> "BackwardStrategy":
+        return replace(self, plan=plan)
+
+    @property
+    def uses_compressed_activation(self) -> bool:
+        return self.grad_weight_path.mode == "lowrank_quant" and self.store_compressed
+
+
+@dataclass(frozen=True)
+class QuantizedTensor:
+    """int8 codes (kernel layout) + bit width + per-tensor fp32 scale on the device."""
+
+    payload: torch.Tensor
+    bits: int
+    scale: torch.Tensor
+    per_axis: int | None = None
+
+    @property
+    def qmax(self) -> int:
+        return (1 << (self.bits - 1)) - 1
+
+
+@dataclass(frozen=True)
+class ACBPActivation:
+    """Forward-time compressed activation (backprop.py:158-176).
+
+    ``quantized.payload`` is (rows, ld) int8, K-major: rows = I (token axis) or
+    L*I (batch axis, row l*I + i); the first ``k`` codes of each row are valid.
+    """
+
+    quantized: QuantizedTensor
+    orig_shape: tuple
+    axis: int
+    plan: HadamardPlan
+    k: int
+
+    @property
+    def payload_nbytes(self) -> int:
+        n = self.k * self.quantized.payload.shape[0]
+        return n if self.quantized.bits == 8 else (n + 1) // 2
+
+    def reference_payload(self) -> torch.Tensor:
+        """The payload in the reference's (K_ref, I) layout (backprop.py:383-385)."""
+        B, L, I = self.orig_shape
+        p = self.quantized.payload[:, : self.k]
+        if self.axis == 1:
+            return p.t().contiguous()
+        return p.reshape(L, I, self.k).permute(2, 0, 1).reshape(self.k * L, I).contiguous()
+
+
+def ht_axis_for(B: int, L: int, block: int, pad_small_axes: bool = False) -> int:
+    """backprop.py:179-190."""
+    if L >= block:
+        return 1
+    if B >= block:
+        return 0
+    if not pad_small_axes:
+        raise DimensionError(
+            f"both L={L} and B={B} are below the block size {block}; set pad_small_axes to zero-pad")
+    return 1 if L >= B else 0
+
+
+def _no_rng(rng):
+    if rng is not None:
+        raise ParameterError("true stochastic rounding (rng) is not implemented on the B200 path; "
+                             "use the default pseudo-stochastic mode (rng=None)")
+
+
+def _as3(t: torch.Tensor, what: str) -> torch.Tensor:
+    if t.dim() != 3:
+        raise DimensionError(f"expected {what} (B,L,C), got {tuple(t.shape)}")
+    return t
+
+
+def _proj_view(B: int, L: int, C: int, axis: int):
+    """(segs, rows, cols, ld_src, seg_src) of the projection along `axis`."""
+    if axis == 1:
+        return B, L, C, C, L * C
+    return 1, B, L * C, L * C, B * L * C
+
+
+def acbp_compress(x: torch.Tensor, plan: HadamardPlan, bits: int = 8, rng=None,
+                  pad_small_axes: bool = False, check_finite: bool = True) -> ACBPActivation:
+    """backprop.py:373-385 on the GPU: project X along ht_axis_for's axis,
+    quantize (int8 by default), keep only the payload."""
+    _no_rng(rng)
+    x = _as3(x, "x")
+    B, L, I = x.shape
+    axis = ht_axis_for(B, L, plan.block_size, pad_small_axes)
+    segs, rows, cols, ld_src, seg_src = _proj_view(B, L, I, axis)
+    codes, k, scale, amax = ops.quant_proj_rows(x, segs, rows, cols, plan.gpu_bitmap(), bits,
+                                                ld_src, seg_src)
+    if check_finite:
+        ops.check_finite(amax)
+    q = QuantizedTensor(payload=codes, bits=bits, scale=scale)
+    return ACBPActivation(quantized=q, orig_shape=(B, L, I), axis=axis, plan=plan, k=k)
+
+
+def hq_grad_input(gy: torch.Tensor, w: torch.Tensor, bits: int | None, rng=None,
+                  block: int = DEFAULT_BLOCK, out_dtype=torch.float32, exact: bool = True,
+                  check_finite: bool = True, stages: dict | None = None) -> torch.Tensor:
+    """backprop.py:350-370: dX = deq(Q(HT_O(gy)) . Q(HT_O(W))), full rank, no inverse HT."""
+    _no_rng(rng)
+    if gy.dim() != 3 or w.dim() != 2:
+        raise DimensionError(f"expected gy (B,L,O) and w (O,I), got {tuple(gy.shape)}, {tuple(w.shape)}")
+    if gy.shape[2] != w.shape[0]:
+        raise DimensionError(f"output channels differ: gy {tuple(gy.shape)} vs w {tuple(w.shape)}")
+    if bits is None:
+        raise ParameterError("bits=None (float debug pipeline) is not implemented on the B200 path")
+    if block != 16:
+        raise ParameterError(f"the B200 kernels implement block 16 only, got {block}")
+    B, L, O = gy.shape
+    I = w.shape[1]
+    cg, sg, ag = ops.quant_ht_cols(gy.reshape(B * L, O), bits)
+    w32 = w if w.dtype == torch.float32 else w.float()
+    cw, kw, sw, aw = ops.quant_proj_rows(w32, 1, O, I, 0xFFFF, bits)
+    if check_finite:
+        ops.check_finite(ag, aw)
+    out, acc = ops.gemm_i8(cg, cw, B * L, I, ops.pad16(O), bits, bits, sg, sw, 1.0, exact=exact,
+                           out_dtype=out_dtype, want_acc=stages is not None)
+    if stages is not None:
+        stages.update(gx_codes_g=cg[:, :ops.pad16(O)], gx_scale_g=sg, gx_codes_w=cw[:, :kw],
+                      gx_scale_w=sw, gx_acc=acc)
+    return out.reshape(B, L, I)
+
+
+def _gy_projection(gy: torch.Tensor, axis: int, plan: HadamardPlan, bits: int):
+    B, L, O = gy.shape
+    segs, rows, cols, ld_src, seg_src = _proj_view(B, L, O, axis)
+    return ops.quant_proj_rows(gy, segs, rows, cols, plan.gpu_bitmap(), bits, ld_src, seg_src)
+
+
+def hlq_grad_weight(acbp: ACBPActivation, gy: torch.Tensor, bits: int = 8, rng=None,
+                    extra_scale: float | None = None, out_dtype=torch.float32, exact: bool = True,
+                    check_finite: bool = True, stages: dict | None = None) -> torch.Tensor:
+    """backprop.py:388-410: project gy onto the ACBP bases, quantize, int8 GEMM
+    against the stored payload, dequantize with s_g * s_x * extra (1/B by default)."""
+    _no_rng(rng)
+    B, L, I = acbp.orig_shape
+    if gy.dim() != 3 or gy.shape[0] != B or gy.shape[1] != L:
+        raise StateError(f"gy shape {tuple(gy.shape)} does not match the compressed activation ({B}, {L}, ...)")
+    if acbp.quantized.bits != bits:
+        raise StateError(f"compressed activation is {acbp.quantized.bits}-bit but backward wants {bits}-bit")
+    O = gy.shape[2]
+    cg, k, sg, ag = _gy_projection(gy, acbp.axis, acbp.plan, bits)
+    if k != acbp.k:
+        raise StateError("projected extents differ between forward and backward; the plans do not match")
+    if check_finite:
+        ops.check_finite(ag)
+    extra = 1.0 / B if extra_scale is None else extra_scale
+    groups = L if acbp.axis == 0 else 1
+    xp = acbp.quantized.payload
+    out, acc = ops.gemm_i8(cg, xp, O, I, k, bits, bits, sg, acbp.quantized.scale, extra,
+                           exact=exact, out_dtype=out_dtype, want_acc=stages is not None,
+                           groups=groups, a_gstride=cg.stride(0) * O, b_gstride=xp.stride(0) * I)
+    if stages is not None:
+        stages.update(gw_codes_g=cg[:, :k], gw_scale_g=sg, gw_acc=acc)
+    return out
+
+
+def _vanilla_gx(gy, w):
+    B, L, O = gy.shape
+    return (gy.reshape(-1, O).float() @ w.float()).reshape(B, L, -1)
+
+
+def _vanilla_gw(x, gy):
+    B, L, I = x.shape
+    return (gy.reshape(-1, gy.shape[2]).float().t() @ x.reshape(-1, I).float()) * (1.0 / B)
+
+
+def _grad_input(gy, w, strategy: BackwardStrategy, rng, stages=None):
+    spec = strategy.grad_input_path
+    if spec.mode == "fp":
+        return _vanilla_gx(gy, w)
+    if spec.mode == "ht_quant":
+        return hq_grad_input(gy, w, spec.bits, rng=rng, block=strategy.plan.block_size, stages=stages)
+    raise ParameterError(f"grad_input mode {spec.mode!r} is a baseline without a B200 kernel "
+                         "(SURVEY.md 8(f) f4)")
+
+
+def strategy_backward(x_or_acbp, w: torch.Tensor, gy: torch.Tensor, strategy: BackwardStrategy,
+                      rng=None, stages: dict | None = None) -> GradPair:
+    """backprop.py:413-435."""
+    if isinstance(x_or_acbp, ACBPActivation):
+        acbp = x_or_acbp
+        if strategy.grad_weight_path.mode != "lowrank_quant":
+            raise StateError(f"strategy {strategy.name!r} expects the raw activation, not a compressed one")
+        if (acbp.plan.block_size != strategy.plan.block_size
+                or acbp.plan.basis_indices != strategy.plan.basis_indices):
+            raise StateError("compressed activation was built with a different plan")
+        B, L, I = acbp.orig_shape
+        if gy.dim() != 3 or tuple(gy.shape[:2]) != (B, L) or w.shape[1] != I:
+            raise DimensionError(f"gy {tuple(gy.shape)} / w {tuple(w.shape)} do not match activation {acbp.orig_shape}")
+        gw = hlq_grad_weight(acbp, gy, bits=strategy.grad_weight_path.bits or 8, rng=rng, stages=stages)
+        gx = _grad_input(gy, w, strategy, rng, stages)
+        return GradPair(gx, gw)
+    x = x_or_acbp
+    if x.dim() != 3 or gy.dim() != 3 or w.dim() != 2:
+        raise DimensionError(
+            f"expected x (B,L,I), w (O,I), gy (B,L,O); got {tuple(x.shape)}, {tuple(w.shape)}, {tuple(gy.shape)}")
+    B, L, I = x.shape
+    O = w.shape[0]
+    if w.shape[1] != I:
+        raise DimensionError(f"weight {tuple(w.shape)} does not match input channels {I}")
+    if tuple(gy.shape) != (B, L, O):
+        raise DimensionError(f"gy shape {tuple(gy.shape)} does not match ({B}, {L}, {O})")
+    gx = _grad_input(gy, w, strategy, rng, stages)
+    spec = strategy.grad_weight_path
+    if spec.mode == "fp":
+        gw = _vanilla_gw(x, gy)
+    elif spec.mode == "lowrank_quant":
+        # raw branch == ACBP branch bit for bit in pseudo mode (test_backprop.py:338-345)
+        acbp = acbp_compress(x, strategy.plan, bits=spec.bits or 8, rng=rng,
+                             pad_small_axes=strategy.pad_small_axes)
+        if stages is not None:
+            stages.update(x_codes=acbp.reference_payload(), x_scale=acbp.quantized.scale, axis=acbp.axis)
+        gw = hlq_grad_weight(acbp, gy, bits=spec.bits or 8, rng=rng, stages=stages)
+    else:
+        raise ParameterError(f"grad_weight mode {spec.mode!r} is a baseline without a B200 kernel "
+                             "(SURVEY.md 8(f) f4)")
+    return GradPair(gx, gw)
+
+
+def hlq_backward(x_or_acbp, w: torch.Tensor, gy: torch.Tensor,
+                 strategy: BackwardStrategy | None = None, rng=None,
+                 stages: dict | None = None) -> GradPair:
+    """backprop.py:438-447: int4 HQ input gradient + int8 low-rank weight gradient."""
+    strategy = strategy or BackwardStrategy.hlq()
+    if strategy.grad_weight_path.mode != "lowrank_quant" or strategy.grad_input_path.mode != "ht_quant":
+        raise ParameterError(f"hlq_backward requires the combined strategy, got {strategy.name!r}")
+    return strategy_backward(x_or_acbp, w, gy, strategy, rng=rng, stages=stages)

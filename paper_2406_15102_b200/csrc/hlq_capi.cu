@@ -1,0 +1,302 @@
+// extern "C" boundary of libhlq_b200.so (declared in include/hlq_b200.h).
+// Validation happens here so every failure maps onto one of the reference's
+// exception classes; kernels are enqueued on the caller's stream and the
+// library never allocates device memory.
+#include <cuda.h>
+#include <cuda_runtime.h>
+#include <cstdarg>
+#include <cstdint>
+#include <cstdio>
+#include <cstring>
+
+#include "../../include/hlq_b200.h"
+#include "hlq_internal.h"
+
+#define HLQ_VERSION_STRING "hlq_b200 0.1.0 (sm_100a, tcgen05 kind::i8)"
+
+namespace hlq {
+
+int num_sms() {
+  static thread_local int dev_cached = -1;
+  static thread_local int sms = 148;
+  int dev = 0;
+  cudaGetDevice(&dev);
+  if (dev != dev_cached) {
+    int v = 0;
+    if (cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev) == cudaSuccess && v > 0) sms = v;
+    dev_cached = dev;
+  }
+  return sms;
+}
+
+}  // namespace hlq
+
+namespace {
+
+thread_local char g_err[512] = {0};
+
+int fail(int code, const char* fmt, ...) {
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(g_err, sizeof(g_err), fmt, ap);
+  va_end(ap);
+  return code;
+}
+
+int cuda_status(const char* where) {
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) return fail(HLQ_ERR_CUDA, "%s: %s", where, cudaGetErrorString(e));
+  return HLQ_OK;
+}
+
+inline int64_t pad16(int64_t v) { return (v + 15) & ~int64_t(15); }
+inline size_t align256(size_t v) { return (v + 255) & ~size_t(255); }
+inline int qmax_of(int bits) { return (1 << (bits - 1)) - 1; }
+
+int check_bits(int bits) {
+  if (bits != 4 && bits != 8) return fail(HLQ_ERR_PARAMETER, "bits must be 4 or 8, got %d", bits);
+  return HLQ_OK;
+}
+int check_dtype(int dtype) {
+  if (dtype != HLQ_F32 && dtype != HLQ_BF16)
+    return fail(HLQ_ERR_PARAMETER, "dtype must be HLQ_F32 or HLQ_BF16, got %d", dtype);
+  return HLQ_OK;
+}
+int check_bitmap(uint32_t bitmap) {
+  if (bitmap == 0 || bitmap > 0xFFFFu)
+    return fail(HLQ_ERR_PARAMETER, "basis bitmap must select 1..16 of 16 bases, got 0x%x", bitmap);
+  return HLQ_OK;
+}
+int check_ld16(int64_t ld, const char* what) {
+  if (ld <= 0 || ld % 16 != 0)
+    return fail(HLQ_ERR_PARAMETER, "%s leading dimension must be a positive multiple of 16, got %lld",
+                what, (long long)ld);
+  return HLQ_OK;
+}
+
+#define HLQ_TRY(expr)          \
+  do {                         \
+    int _s = (expr);           \
+    if (_s != HLQ_OK) return _s; \
+  } while (0)
+
+int proj_rows_checked(const void* src, int dtype, int64_t segs, int64_t rows, int64_t cols,
+                      int64_t ld_src, int64_t seg_src, uint32_t bitmap, int bits, int8_t* dst,
+                      int64_t ld_dst) {
+  HLQ_TRY(check_dtype(dtype));
+  HLQ_TRY(check_bits(bits));
+  HLQ_TRY(check_bitmap(bitmap));
+  if (segs < 0 || rows < 0 || cols < 0 || ld_src < cols || (segs > 1 && seg_src < rows * ld_src))
+    return fail(HLQ_ERR_DIMENSION, "bad projection view segs=%lld rows=%lld cols=%lld ld=%lld",
+                (long long)segs, (long long)rows, (long long)cols, (long long)ld_src);
+  const int64_t k = segs * ((rows + 15) / 16) * __builtin_popcount(bitmap);
+  if (dst) {
+    HLQ_TRY(check_ld16(ld_dst, "projection output"));
+    if (ld_dst < k)
+      return fail(HLQ_ERR_DIMENSION, "projection output ld %lld < K %lld", (long long)ld_dst,
+                  (long long)k);
+  }
+  if (!src && segs * rows * cols > 0) return fail(HLQ_ERR_PARAMETER, "null source");
+  return HLQ_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* hlq_version(void) { return HLQ_VERSION_STRING; }
+const char* hlq_last_error(void) { return g_err; }
+
+int hlq_device_ok(void) {
+  int n = 0;
+  if (cudaGetDeviceCount(&n) != cudaSuccess || n == 0) {
+    cudaGetLastError();
+    return 0;
+  }
+  int dev = 0, major = 0;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&major, cudaDevAttrComputeCapabilityMajor, dev);
+  return major == 10 ? 1 : 0;
+}
+
+int hlq_quantize_ht_cols(const void* src, int dtype, int64_t rows, int64_t cols, int64_t ld_src,
+                         int bits, uint32_t* amax_ws, int8_t* dst, int64_t ld_dst,
+                         float* scale_out, void* stream) {
+  HLQ_TRY(check_dtype(dtype));
+  HLQ_TRY(check_bits(bits));
+  HLQ_TRY(check_ld16(ld_dst, "codes"));
+  if (rows < 0 || cols < 0 || ld_src < cols || ld_dst < pad16(cols))
+    return fail(HLQ_ERR_DIMENSION, "bad ht_cols view rows=%lld cols=%lld ld_src=%lld ld_dst=%lld",
+                (long long)rows, (long long)cols, (long long)ld_src, (long long)ld_dst);
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  cudaMemsetAsync(amax_ws, 0, sizeof(uint32_t), st);
+  hlq::launch_ht_cols_any(src, dtype, rows, cols, ld_src, bits, hlq::kStats, amax_ws, nullptr, 0,
+                          nullptr, st);
+  hlq::launch_ht_cols_any(src, dtype, rows, cols, ld_src, bits, hlq::kQuant, amax_ws, dst, ld_dst,
+                          scale_out, st);
+  return cuda_status("hlq_quantize_ht_cols");
+}
+
+int hlq_proj_rows_amax(const void* src, int dtype, int64_t segs, int64_t rows, int64_t cols,
+                       int64_t ld_src, int64_t seg_src, uint32_t bitmap, uint32_t* amax_bits,
+                       void* stream) {
+  HLQ_TRY(proj_rows_checked(src, dtype, segs, rows, cols, ld_src, seg_src, bitmap, 8, nullptr, 0));
+  hlq::launch_proj_rows_any(src, dtype, segs, rows, cols, ld_src, seg_src, bitmap, 8, hlq::kStats,
+                            amax_bits, nullptr, 0, nullptr, static_cast<cudaStream_t>(stream));
+  return cuda_status("hlq_proj_rows_amax");
+}
+
+int hlq_proj_rows_quant(const void* src, int dtype, int64_t segs, int64_t rows, int64_t cols,
+                        int64_t ld_src, int64_t seg_src, uint32_t bitmap, int bits,
+                        const uint32_t* amax_bits, int8_t* dst, int64_t ld_dst, float* scale_out,
+                        void* stream) {
+  HLQ_TRY(proj_rows_checked(src, dtype, segs, rows, cols, ld_src, seg_src, bitmap, bits, dst, ld_dst));
+  hlq::launch_proj_rows_any(src, dtype, segs, rows, cols, ld_src, seg_src, bitmap, bits, hlq::kQuant,
+                            const_cast<uint32_t*>(amax_bits), dst, ld_dst, scale_out,
+                            static_cast<cudaStream_t>(stream));
+  return cuda_status("hlq_proj_rows_quant");
+}
+
+int hlq_quantize_proj_rows(const void* src, int dtype, int64_t segs, int64_t rows, int64_t cols,
+                           int64_t ld_src, int64_t seg_src, uint32_t bitmap, int bits,
+                           uint32_t* amax_ws, int8_t* dst, int64_t ld_dst, float* scale_out,
+                           void* stream) {
+  HLQ_TRY(proj_rows_checked(src, dtype, segs, rows, cols, ld_src, seg_src, bitmap, bits, dst, ld_dst));
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  cudaMemsetAsync(amax_ws, 0, sizeof(uint32_t), st);
+  hlq::launch_proj_rows_any(src, dtype, segs, rows, cols, ld_src, seg_src, bitmap, bits, hlq::kStats,
+                            amax_ws, nullptr, 0, nullptr, st);
+  hlq::launch_proj_rows_any(src, dtype, segs, rows, cols, ld_src, seg_src, bitmap, bits, hlq::kQuant,
+                            amax_ws, dst, ld_dst, scale_out, st);
+  return cuda_status("hlq_quantize_proj_rows");
+}
+
+int hlq_gemm_i8(const int8_t* A, int64_t lda, const int8_t* B, int64_t ldb, int64_t M, int64_t N,
+                int64_t K, int bits_a, int bits_b, const float* sa, const float* sb, double extra,
+                int epilogue, void* out, int out_dtype, int64_t ldo, int32_t* acc_out,
+                int64_t ld_acc, void* stream) {
+  return hlq_gemm_i8_grouped(A, lda, lda * M, B, ldb, ldb * N, M, N, K, 1, bits_a, bits_b, sa, sb,
+                             extra, epilogue, out, out_dtype, ldo, acc_out, ld_acc, stream);
+}
+
+int hlq_gemm_i8_grouped(const int8_t* A, int64_t lda, int64_t a_gstride, const int8_t* B,
+                        int64_t ldb, int64_t b_gstride, int64_t M, int64_t N, int64_t K,
+                        int64_t groups, int bits_a, int bits_b, const float* sa, const float* sb,
+                        double extra, int epilogue, void* out, int out_dtype, int64_t ldo,
+                        int32_t* acc_out, int64_t ld_acc, void* stream) {
+  if (groups < 1 || groups > 65535 || (groups > 1 && (a_gstride % 16 || b_gstride % 16 ||
+                                                      a_gstride < lda * M || b_gstride < ldb * N)))
+    return fail(HLQ_ERR_PARAMETER, "bad K-group layout groups=%lld", (long long)groups);
+  HLQ_TRY(check_bits(bits_a));
+  HLQ_TRY(check_bits(bits_b));
+  HLQ_TRY(check_dtype(out_dtype));
+  HLQ_TRY(check_ld16(lda, "A"));
+  HLQ_TRY(check_ld16(ldb, "B"));
+  if (M < 0 || N < 0 || K <= 0 || lda < K || ldb < K || (out && ldo < N) || (acc_out && ld_acc < N))
+    return fail(HLQ_ERR_DIMENSION, "bad GEMM shape M=%lld N=%lld K=%lld", (long long)M, (long long)N,
+                (long long)K);
+  if (M > INT32_MAX || N > INT32_MAX || K > INT32_MAX)
+    return fail(HLQ_ERR_DIMENSION, "GEMM extent exceeds int32");
+  const long double worst = (long double)K * groups * qmax_of(bits_a) * qmax_of(bits_b);
+  if (worst >= 2147483648.0L)
+    return fail(HLQ_ERR_PARAMETER,
+                "contraction extent %lld exceeds the int32-exact bound for %dx%d-bit operands",
+                (long long)K, bits_a, bits_b);
+  if (epilogue != HLQ_EPI_EXACT && epilogue != HLQ_EPI_FAST)
+    return fail(HLQ_ERR_PARAMETER, "unknown epilogue %d", epilogue);
+  if (M == 0 || N == 0) return HLQ_OK;
+  int e = hlq::launch_gemm_i8(A, lda, B, ldb, M, N, K, groups, a_gstride, b_gstride, sa, sb, extra,
+                              epilogue, out, out_dtype, ldo, acc_out, ld_acc,
+                              static_cast<cudaStream_t>(stream));
+  if (e == -1) return fail(HLQ_ERR_CUDA, "cuTensorMapEncodeTiled unavailable or rejected the operands");
+  if (e != 0) return fail(HLQ_ERR_CUDA, "hlq_gemm_i8: %s", cudaGetErrorString(cudaError_t(e)));
+  return HLQ_OK;
+}
+
+int64_t hlq_acbp_k(int64_t B, int64_t L, int axis, int rank) {
+  return axis == 1 ? B * ((L + 15) / 16) * rank : ((B + 15) / 16) * rank;
+}
+int64_t hlq_acbp_rows(int64_t L, int64_t I, int axis) { return axis == 1 ? I : L * I; }
+
+int hlq_acbp_compress(const void* x, int dtype, int64_t B, int64_t L, int64_t I, int axis,
+                      uint32_t bitmap, int bits, int8_t* payload, int64_t ld_payload,
+                      float* scale_out, uint32_t* amax_ws, void* stream) {
+  if (axis != 0 && axis != 1) return fail(HLQ_ERR_PARAMETER, "axis must be 0 or 1, got %d", axis);
+  // axis 1: B segments of (L x I); axis 0: one segment of (B x L*I) -- the
+  // reference's (B_p r/16, L, I) payload flattens to rows (blk*r + j)*L + l,
+  // which is exactly column (l*I + i) of the transposed projection.
+  if (axis == 1)
+    return hlq_quantize_proj_rows(x, dtype, B, L, I, I, L * I, bitmap, bits, amax_ws, payload,
+                                  ld_payload, scale_out, stream);
+  return hlq_quantize_proj_rows(x, dtype, 1, B, L * I, L * I, B * L * I, bitmap, bits, amax_ws,
+                                payload, ld_payload, scale_out, stream);
+}
+
+size_t hlq_hq_grad_input_ws(int64_t T, int64_t O, int64_t I) {
+  const int64_t op = pad16(O);
+  return align256(size_t(T * op)) + align256(size_t(I * op)) + 256;
+}
+
+int hlq_hq_grad_input(const void* gy, int gy_dtype, int64_t T, int64_t O, const float* w, int64_t I,
+                      int bits, void* dx, int dx_dtype, int epilogue, void* ws, size_t ws_bytes,
+                      void* stream) {
+  HLQ_TRY(check_bits(bits));
+  if (T < 0 || O <= 0 || I <= 0) return fail(HLQ_ERR_DIMENSION, "bad hq_grad_input shape");
+  if (ws_bytes < hlq_hq_grad_input_ws(T, O, I))
+    return fail(HLQ_ERR_PARAMETER, "workspace too small: %zu < %zu", ws_bytes,
+                hlq_hq_grad_input_ws(T, O, I));
+  const int64_t op = pad16(O);
+  uint8_t* p = static_cast<uint8_t*>(ws);
+  int8_t* cg = reinterpret_cast<int8_t*>(p);
+  p += align256(size_t(T * op));
+  int8_t* cw = reinterpret_cast<int8_t*>(p);
+  p += align256(size_t(I * op));
+  uint32_t* amax = reinterpret_cast<uint32_t*>(p);  // [0] gy, [1] w
+  float* scales = reinterpret_cast<float*>(p + 64);  // [0] gy, [1] w
+  HLQ_TRY(hlq_quantize_ht_cols(gy, gy_dtype, T, O, O, bits, amax, cg, op, scales, stream));
+  HLQ_TRY(hlq_quantize_proj_rows(w, HLQ_F32, 1, O, I, I, O * I, 0xFFFFu, bits, amax + 1, cw, op,
+                                 scales + 1, stream));
+  return hlq_gemm_i8(cg, op, cw, op, T, I, op, bits, bits, scales, scales + 1, 1.0, epilogue, dx,
+                     dx_dtype, I, nullptr, 0, stream);
+}
+
+size_t hlq_grad_weight_ws(int64_t B, int64_t L, int64_t O, int axis, int rank) {
+  const int64_t k = hlq_acbp_k(B, L, axis, rank);
+  return align256(size_t(hlq_acbp_rows(L, O, axis) * pad16(k))) + 256;
+}
+
+int hlq_grad_weight(const int8_t* payload, int64_t ld_payload, const float* x_scale,
+                    const void* gy, int gy_dtype, int64_t B, int64_t L, int64_t O, int64_t I,
+                    int axis, uint32_t bitmap, int bits, double extra, void* dw, int dw_dtype,
+                    int epilogue, void* ws, size_t ws_bytes, void* stream) {
+  HLQ_TRY(check_bits(bits));
+  HLQ_TRY(check_bitmap(bitmap));
+  if (axis != 0 && axis != 1) return fail(HLQ_ERR_PARAMETER, "axis must be 0 or 1, got %d", axis);
+  const int rank = __builtin_popcount(bitmap);
+  const int64_t k = hlq_acbp_k(B, L, axis, rank);
+  if (ld_payload < k)
+    return fail(HLQ_ERR_STATE, "payload extent %lld < projected extent %lld", (long long)ld_payload,
+                (long long)k);
+  if (ws_bytes < hlq_grad_weight_ws(B, L, O, axis, rank))
+    return fail(HLQ_ERR_PARAMETER, "workspace too small");
+  const int64_t ldk = pad16(k);
+  uint8_t* p = static_cast<uint8_t*>(ws);
+  int8_t* cg = reinterpret_cast<int8_t*>(p);
+  p += align256(size_t(hlq_acbp_rows(L, O, axis) * ldk));
+  uint32_t* amax = reinterpret_cast<uint32_t*>(p);
+  float* scale = reinterpret_cast<float*>(p + 64);
+  if (axis == 1)
+    HLQ_TRY(hlq_quantize_proj_rows(gy, gy_dtype, B, L, O, O, L * O, bitmap, bits, amax, cg, ldk, scale,
+                                   stream));
+  else
+    HLQ_TRY(hlq_quantize_proj_rows(gy, gy_dtype, 1, B, L * O, L * O, B * L * O, bitmap, bits, amax, cg,
+                                   ldk, scale, stream));
+  // axis 0: the transposed projections have L*O rows (l, o) and L*I rows
+  // (l, i); the reference's K index (blk, j, l) becomes L stacked K panels.
+  const int64_t groups = axis == 0 ? L : 1;
+  return hlq_gemm_i8_grouped(cg, ldk, ldk * O, payload, ld_payload, ld_payload * I, O, I, k, groups,
+                             bits, bits, scale, x_scale, extra, epilogue, dw, dw_dtype, I, nullptr, 0,
+                             stream);
+}
+
+}  // extern "C"

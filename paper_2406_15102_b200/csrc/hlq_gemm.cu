@@ -1,0 +1,312 @@
+// Integer GEMM with fused dequantization for both HLQ products:
+//
+//   dX  = deq( Q4(H.gy) [T x O_p]  . Q4(H.W)^T [I x O_p]^T )          (backprop.py:367-369)
+//   dW  = deq( Q8(P.gy)^T [O x K]  . Q8(P.X)^T  [I x K]^T ) * extra   (backprop.py:407-410)
+//
+// Both operands are int8 codes stored K-major (row = M or N index, K contiguous),
+// so the same kernel serves both products:  D[m, n] = sum_k A[m, k] * B[n, k].
+//
+// sm_100a structure (one persistent CTA per SM, 8 warps):
+//   warp 0      TMA producer: 128x128 A tile + BNx128 B tile per stage (SWIZZLE_128B)
+//   warp 1      MMA issuer: tcgen05.mma.cta_group::1.kind::i8, M=128, N=BN, K=32 per op,
+//               int32 accumulators in TMEM, two accumulator buffers (2*BN columns)
+//   warp 2      TMEM allocator
+//   warps 4..7  epilogue: tcgen05.ld 32x32b -> registers -> dequant -> global
+// Exact epilogue (quantize.py:181-187): out = f32( f64(acc) * (f64(f32(sa*sb)) * extra) ).
+// Fast epilogue (training): out = f32(acc) * f32(sa*sb*extra), fp32 or bf16 output.
+// int32 accumulation is exact while K * qmax_a * qmax_b < 2^31 (checked by the caller).
+#include <cuda.h>
+#include <cuda_bf16.h>
+#include <cuda_runtime.h>
+#include <cstdint>
+#include <cstdio>
+#include <mutex>
+
+#include "hlq_internal.h"
+#include "hlq_ptx.cuh"
+
+namespace hlq {
+
+namespace {
+
+constexpr int kBM = 128;
+constexpr int kBK = 128;  // bytes of K per stage = one 128B swizzle row
+constexpr int kThreads = 256;
+
+template <int BN, int STAGES>
+struct GemmCfg {
+  static constexpr uint32_t kABytes = kBM * kBK;
+  static constexpr uint32_t kBBytes = BN * kBK;
+  static constexpr uint32_t kStageBytes = kABytes + kBBytes;
+  static constexpr uint32_t kTmemCols = 2 * BN;  // 256 or 512: power of two
+  static constexpr size_t kSmem = size_t(STAGES) * kStageBytes + 1024 /*align*/ + 256 /*barriers*/;
+};
+
+__device__ __forceinline__ void store_row_chunk(const uint32_t (&acc)[32], int64_t row, int64_t col0,
+                                                int64_t N, int epilogue, double dscale, float fscale,
+                                                void* out, int out_dtype, int64_t ldo, bool vec_ok,
+                                                int32_t* acc_out, int64_t ld_acc) {
+  const int64_t nvalid = N - col0;
+  if (acc_out) {
+    int32_t* a = acc_out + row * ld_acc + col0;
+    if (nvalid >= 32 && (ld_acc % 4 == 0) && ((reinterpret_cast<uintptr_t>(acc_out) & 15) == 0)) {
+#pragma unroll
+      for (int j = 0; j < 32; j += 4)
+        *reinterpret_cast<int4*>(a + j) =
+            make_int4(int(acc[j]), int(acc[j + 1]), int(acc[j + 2]), int(acc[j + 3]));
+    } else {
+#pragma unroll
+      for (int j = 0; j < 32; ++j)
+        if (j < nvalid) a[j] = int(acc[j]);
+    }
+  }
+  if (!out) return;
+  float v[32];
+  if (epilogue == kEpiExact) {
+#pragma unroll
+    for (int j = 0; j < 32; ++j) v[j] = __double2float_rn(__dmul_rn(double(int(acc[j])), dscale));
+  } else {
+#pragma unroll
+    for (int j = 0; j < 32; ++j) v[j] = __fmul_rn(__int2float_rn(int(acc[j])), fscale);
+  }
+  if (out_dtype == kF32) {
+    float* o = static_cast<float*>(out) + row * ldo + col0;
+    if (nvalid >= 32 && vec_ok) {
+#pragma unroll
+      for (int j = 0; j < 32; j += 4)
+        *reinterpret_cast<float4*>(o + j) = make_float4(v[j], v[j + 1], v[j + 2], v[j + 3]);
+    } else {
+#pragma unroll
+      for (int j = 0; j < 32; ++j)
+        if (j < nvalid) o[j] = v[j];
+    }
+  } else {
+    __nv_bfloat16* o = static_cast<__nv_bfloat16*>(out) + row * ldo + col0;
+    if (nvalid >= 32 && vec_ok) {
+#pragma unroll
+      for (int j = 0; j < 32; j += 8) {
+        uint4 p;
+        __nv_bfloat162 t0 = __floats2bfloat162_rn(v[j], v[j + 1]);
+        __nv_bfloat162 t1 = __floats2bfloat162_rn(v[j + 2], v[j + 3]);
+        __nv_bfloat162 t2 = __floats2bfloat162_rn(v[j + 4], v[j + 5]);
+        __nv_bfloat162 t3 = __floats2bfloat162_rn(v[j + 6], v[j + 7]);
+        p.x = *reinterpret_cast<uint32_t*>(&t0);
+        p.y = *reinterpret_cast<uint32_t*>(&t1);
+        p.z = *reinterpret_cast<uint32_t*>(&t2);
+        p.w = *reinterpret_cast<uint32_t*>(&t3);
+        *reinterpret_cast<uint4*>(o + j) = p;
+      }
+    } else {
+#pragma unroll
+      for (int j = 0; j < 32; ++j)
+        if (j < nvalid) o[j] = __float2bfloat16_rn(v[j]);
+    }
+  }
+}
+
+template <int BN, int STAGES>
+__global__ void __launch_bounds__(kThreads, 1)
+    gemm_i8_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant__ CUtensorMap map_b,
+                   int M, int N, int K, int groups, const float* __restrict__ sa, const float* __restrict__ sb,
+                   double extra, int epilogue, void* out, int out_dtype, int64_t ldo,
+                   int32_t* acc_out, int64_t ld_acc) {
+  using Cfg = GemmCfg<BN, STAGES>;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
+                                             ~uintptr_t(1023));
+  uint8_t* sA = smem;
+  uint8_t* sB = smem + STAGES * Cfg::kABytes;
+  uint64_t* full = reinterpret_cast<uint64_t*>(sB + STAGES * Cfg::kBBytes);
+  uint64_t* empty = full + STAGES;
+  uint64_t* tfull = empty + STAGES;
+  uint64_t* tempty = tfull + 2;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+
+  const uint32_t warp = ptx::warp_id();
+  const uint32_t lane = ptx::lane_id();
+
+  if (warp == 0 && lane == 0) {
+    ptx::tma_prefetch_desc(&map_a);
+    ptx::tma_prefetch_desc(&map_b);
+  }
+  if (warp == 1 && lane == 0) {
+    for (int s = 0; s < STAGES; ++s) {
+      ptx::mbar_init(&full[s], 1);
+      ptx::mbar_init(&empty[s], 1);
+    }
+    for (int a = 0; a < 2; ++a) {
+      ptx::mbar_init(&tfull[a], 1);
+      ptx::mbar_init(&tempty[a], 128);
+    }
+    ptx::fence_mbar_init();
+  }
+  if (warp == 2) ptx::tmem_alloc(tmem_slot, Cfg::kTmemCols);
+  ptx::tc_fence_before();
+  __syncthreads();
+  ptx::tc_fence_after();
+  const uint32_t tmem_base = *tmem_slot;
+
+  const int num_m = (M + kBM - 1) / kBM;
+  const int num_n = (N + BN - 1) / BN;
+  const int tiles = num_m * num_n;
+  const int nk_g = (K + kBK - 1) / kBK;  // K blocks per group
+  const int nk = nk_g * groups;           // groups accumulate into the same tile
+
+  if (warp == 0) {
+    if (ptx::elect_one()) {
+      int stage = 0;
+      uint32_t phase = 0;
+      for (int t = blockIdx.x; t < tiles; t += gridDim.x) {
+        const int mb = t / num_n, nb = t - mb * num_n;
+        int g = 0, kg = 0;
+        for (int kb = 0; kb < nk; ++kb) {
+          ptx::mbar_wait(&empty[stage], phase ^ 1);
+          ptx::mbar_arrive_expect_tx(&full[stage], Cfg::kStageBytes);
+          ptx::tma_load_3d(sA + stage * Cfg::kABytes, &map_a, &full[stage], kg * kBK, mb * kBM, g);
+          ptx::tma_load_3d(sB + stage * Cfg::kBBytes, &map_b, &full[stage], kg * kBK, nb * BN, g);
+          if (++kg == nk_g) { kg = 0; ++g; }
+          if (++stage == STAGES) { stage = 0; phase ^= 1; }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    constexpr uint32_t idesc = ptx::idesc_i8(kBM, BN);
+    int stage = 0;
+    uint32_t phase = 0;
+    int acc = 0;
+    uint32_t acc_phase = 0;
+    for (int t = blockIdx.x; t < tiles; t += gridDim.x) {
+      ptx::mbar_wait(&tempty[acc], acc_phase ^ 1);
+      ptx::tc_fence_after();
+      const uint32_t d_tmem = tmem_base + uint32_t(acc * BN);
+      for (int kb = 0; kb < nk; ++kb) {
+        ptx::mbar_wait(&full[stage], phase);
+        ptx::tc_fence_after();
+        if (ptx::elect_one()) {
+          const uint64_t a_desc = ptx::desc_kmajor_sw128(ptx::smem_u32(sA + stage * Cfg::kABytes));
+          const uint64_t b_desc = ptx::desc_kmajor_sw128(ptx::smem_u32(sB + stage * Cfg::kBBytes));
+#pragma unroll
+          for (int k = 0; k < kBK / 32; ++k) {
+            // advance the start address by 32 bytes of K inside the swizzle atom
+            ptx::mma_i8(d_tmem, a_desc + uint64_t((k * 32) >> 4), b_desc + uint64_t((k * 32) >> 4),
+                        idesc, (kb | k) != 0 ? 1u : 0u);
+          }
+          ptx::mma_commit(&empty[stage]);
+          if (kb == nk - 1) ptx::mma_commit(&tfull[acc]);
+        }
+        __syncwarp();
+        if (++stage == STAGES) { stage = 0; phase ^= 1; }
+      }
+      if (++acc == 2) { acc = 0; acc_phase ^= 1; }
+    }
+  } else if (warp >= 4) {
+    const uint32_t quarter = warp & 3;  // TMEM lanes [32*quarter, 32*quarter+32)
+    const float comb = __fmul_rn(*sa, *sb);
+    const double dscale = __dmul_rn(double(comb), extra);
+    const float fscale = float(dscale);
+    const bool vec_ok = (ldo % 8 == 0) && ((reinterpret_cast<uintptr_t>(out) & 15) == 0);
+    int acc = 0;
+    uint32_t acc_phase = 0;
+    for (int t = blockIdx.x; t < tiles; t += gridDim.x) {
+      const int mb = t / num_n, nb = t - mb * num_n;
+      ptx::mbar_wait(&tfull[acc], acc_phase);
+      ptx::tc_fence_after();
+      const int64_t row = int64_t(mb) * kBM + quarter * 32 + lane;
+#pragma unroll 1
+      for (int c = 0; c < BN / 32; ++c) {
+        const int64_t col0 = int64_t(nb) * BN + c * 32;
+        uint32_t r[32];
+        ptx::tmem_ld_32x32b_x32(tmem_base + ((quarter * 32) << 16) + uint32_t(acc * BN + c * 32), r);
+        ptx::tmem_ld_wait();
+        if (row < M && col0 < N)
+          store_row_chunk(r, row, col0, N, epilogue, dscale, fscale, out, out_dtype, ldo, vec_ok,
+                          acc_out, ld_acc);
+      }
+      ptx::tc_fence_before();
+      ptx::mbar_arrive(&tempty[acc]);
+      if (++acc == 2) { acc = 0; acc_phase ^= 1; }
+    }
+  }
+
+  ptx::tc_fence_before();
+  __syncthreads();
+  ptx::tc_fence_after();
+  if (warp == 2) ptx::tmem_dealloc(tmem_base, Cfg::kTmemCols);
+}
+
+// ---------------------------------------------------------------- host side
+
+typedef CUresult (*EncodeTiledFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*,
+                                  const cuuint64_t*, const cuuint64_t*, const cuuint32_t*,
+                                  const cuuint32_t*, CUtensorMapInterleave, CUtensorMapSwizzle,
+                                  CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+EncodeTiledFn encode_fn() {
+  static EncodeTiledFn fn = nullptr;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<EncodeTiledFn>(p);
+  });
+  return fn;
+}
+
+// 3-D map (K, rows, groups): OOB rows / K columns of a group are zero-filled,
+// so ragged tiles never read a neighbouring group's data.
+bool make_map(CUtensorMap* map, const int8_t* ptr, int64_t rows, int64_t k, int64_t ld,
+              int64_t groups, int64_t gstride, uint32_t box_rows) {
+  EncodeTiledFn fn = encode_fn();
+  if (!fn) return false;
+  cuuint64_t dims[3] = {cuuint64_t(k), cuuint64_t(rows), cuuint64_t(groups)};
+  cuuint64_t strides[2] = {cuuint64_t(ld), cuuint64_t(groups > 1 ? gstride : ld * rows)};
+  cuuint32_t box[3] = {uint32_t(kBK), box_rows, 1};
+  cuuint32_t estr[3] = {1, 1, 1};
+  return fn(map, CU_TENSOR_MAP_DATA_TYPE_UINT8, 3, const_cast<int8_t*>(ptr), dims, strides, box, estr,
+            CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+            CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
+template <int BN, int STAGES>
+int run(const int8_t* A, int64_t lda, const int8_t* B, int64_t ldb, int64_t M, int64_t N, int64_t K,
+        int64_t groups, int64_t a_gstride, int64_t b_gstride, const float* sa, const float* sb, double extra, int epilogue, void* out, int out_dtype,
+        int64_t ldo, int32_t* acc_out, int64_t ld_acc, cudaStream_t stream) {
+  using Cfg = GemmCfg<BN, STAGES>;
+  CUtensorMap ma, mb;
+  if (!make_map(&ma, A, M, K, lda, groups, a_gstride, kBM) ||
+      !make_map(&mb, B, N, K, ldb, groups, b_gstride, BN))
+    return -1;
+  static bool attr_set = false;  // per template instance
+  if (!attr_set) {
+    cudaError_t e = cudaFuncSetAttribute(gemm_i8_kernel<BN, STAGES>,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize, int(Cfg::kSmem));
+    if (e != cudaSuccess) return int(e);
+    attr_set = true;
+  }
+  const int64_t tiles = ((M + kBM - 1) / kBM) * ((N + BN - 1) / BN);
+  const int grid = int(tiles < num_sms() ? tiles : num_sms());
+  gemm_i8_kernel<BN, STAGES><<<grid, kThreads, Cfg::kSmem, stream>>>(
+      ma, mb, int(M), int(N), int(K), int(groups), sa, sb, extra, epilogue, out, out_dtype, ldo, acc_out, ld_acc);
+  return int(cudaGetLastError());
+}
+
+}  // namespace
+
+int launch_gemm_i8(const int8_t* A, int64_t lda, const int8_t* B, int64_t ldb, int64_t M, int64_t N,
+                   int64_t K, int64_t groups, int64_t a_gstride, int64_t b_gstride,
+                   const float* sa, const float* sb, double extra, int epilogue,
+                   void* out, int out_dtype, int64_t ldo, int32_t* acc_out, int64_t ld_acc,
+                   cudaStream_t stream) {
+  // Wide N tiles amortise the A stream; narrow ones keep >= ~1 wave of CTAs busy.
+  const int64_t m_tiles = (M + kBM - 1) / kBM;
+  const int64_t wide_tiles = m_tiles * ((N + 255) / 256);
+  if (N > 128 && wide_tiles >= num_sms())
+    return run<256, 4>(A, lda, B, ldb, M, N, K, groups, a_gstride, b_gstride, sa, sb, extra, epilogue, out, out_dtype, ldo,
+                       acc_out, ld_acc, stream);
+  return run<128, 6>(A, lda, B, ldb, M, N, K, groups, a_gstride, b_gstride, sa, sb, extra, epilogue, out, out_dtype, ldo, acc_out,
+                     ld_acc, stream);
+}
+
+}  // namespace hlq

@@ -1,0 +1,133 @@
+"""Drop-in torch modules whose backward is the HLQ path on B200.
+
+Mirror of the reference's GEMM-layer hooks (harness/layers.py:22-93):
+forward = stock ``F.linear`` plus ACBP compression of the input
+(``GemmLayer._store_forward``, layers.py:46-55); backward = HLQ
+(``GemmLayer._strategy_backward``, layers.py:57-69): the int8 low-rank weight
+gradient from the compressed activation and the int4 Hadamard-quantized input
+gradient, both on the sm_100a kernels.  The raw input is not kept.
+
+Conventions:
+  * 2-D input (N, I) is viewed as (N, 1, I) (layers.py:87) -> projection along N;
+    >3-D input uses B = shape[0], L = prod(shape[1:-1]);
+  * torch's mean-loss gradient already carries 1/B, so the dW dequant uses
+    extra = 1 (the reference applies 1/B inside hlq_grad_weight, layers.py:239-250);
+  * dX is produced in the input's dtype (bf16 under autocast) with the fp32
+    epilogue; dW is fp32 (the master weight's dtype); the bias gradient is a
+    plain torch reduction.
+"""
+from __future__ import annotations
+
+import torch
+import torch.nn as nn
+import torch.nn.functional as F
+
+from . import ops
+from .backprop import BackwardStrategy, ht_axis_for, _proj_view
+from .errors import ParameterError
+
+
+def _blv(shape):
+    if len(shape) == 2:
+        return shape[0], 1, shape[1]
+    if len(shape) < 2:
+        raise ParameterError(f"HLQ linear needs at least 2-D input, got {tuple(shape)}")
+    L = 1
+    for s in shape[1:-1]:
+        L *= s
+    return shape[0], L, shape[-1]
+
+
+class HLQLinearFunction(torch.autograd.Function):
+    """y = x W^T + b forward; HLQ backward (ACBP payload saved, raw x dropped)."""
+
+    @staticmethod
+    def forward(ctx, x, weight, bias, strategy: BackwardStrategy):
+        y = F.linear(x, weight.to(x.dtype) if x.dtype != weight.dtype else weight,
+                     None if bias is None else bias.to(x.dtype))
+        B, L, I = _blv(x.shape)
+        plan = strategy.plan
+        bits_gw = strategy.grad_weight_path.bits or 8
+        axis = ht_axis_for(B, L, plan.block_size, strategy.pad_small_axes)
+        segs, rows, cols, ld_src, seg_src = _proj_view(B, L, I, axis)
+        if ctx.needs_input_grad[1]:
+            payload, k, sx, _ = ops.quant_proj_rows(x.detach().contiguous(), segs, rows, cols,
+                                                    plan.gpu_bitmap(), bits_gw, ld_src, seg_src)
+        else:
+            payload, k, sx = None, 0, None
+        ctx.save_for_backward(weight, payload, sx)
+        ctx.meta = (B, L, I, axis, k, x.dtype, tuple(x.shape), bias is not None, strategy)
+        return y
+
+    @staticmethod
+    def backward(ctx, gy):
+        weight, payload, sx = ctx.saved_tensors
+        B, L, I, axis, k, x_dtype, x_shape, has_bias, strategy = ctx.meta
+        O = weight.shape[0]
+        gy3 = gy.reshape(B, L, O)
+        if gy3.dtype not in (torch.float32, torch.bfloat16):
+            gy3 = gy3.float()
+        gy3 = gy3.contiguous()
+        gx = gw = gb = None
+        if ctx.needs_input_grad[1]:
+            bits = strategy.grad_weight_path.bits or 8
+            segs, rows, cols, ld_src, seg_src = _proj_view(B, L, O, axis)
+            cg, kg, sg, _ = ops.quant_proj_rows(gy3, segs, rows, cols, strategy.plan.gpu_bitmap(),
+                                                bits, ld_src, seg_src)
+            groups = L if axis == 0 else 1
+            gw, _ = ops.gemm_i8(cg, payload, O, I, k, bits, bits, sg, sx, 1.0, exact=False,
+                                out_dtype=torch.float32, groups=groups,
+                                a_gstride=cg.stride(0) * O, b_gstride=payload.stride(0) * I)
+            if weight.dtype != torch.float32:
+                gw = gw.to(weight.dtype)
+        if ctx.needs_input_grad[0]:
+            bits = strategy.grad_input_path.bits or 4
+            cgx, sgx, _ = ops.quant_ht_cols(gy3.reshape(B * L, O), bits)
+            w32 = weight.detach() if weight.dtype == torch.float32 else weight.detach().float()
+            cw, _, sw, _ = ops.quant_proj_rows(w32, 1, O, I, 0xFFFF, bits)
+            out_dtype = x_dtype if x_dtype in (torch.float32, torch.bfloat16) else torch.float32
+            gx, _ = ops.gemm_i8(cgx, cw, B * L, I, ops.pad16(O), bits, bits, sgx, sw, 1.0,
+                                exact=False, out_dtype=out_dtype)
+            gx = gx.reshape(x_shape)
+            if gx.dtype != x_dtype:
+                gx = gx.to(x_dtype)
+        if has_bias and ctx.needs_input_grad[2]:
+            gb = gy.reshape(-1, O).sum(0, dtype=torch.float32)
+        return gx, gw, gb, None
+
+
+class HLQLinear(nn.Linear):
+    """nn.Linear with the HLQ backward (reference harness/layers.py:72-93)."""
+
+    def __init__(self, in_features: int, out_features: int, bias: bool = True,
+                 strategy: BackwardStrategy | None = None, device=None, dtype=None):
+        super().__init__(in_features, out_features, bias=bias, device=device, dtype=dtype)
+        self.strategy = strategy or BackwardStrategy.hlq()
+
+    def forward(self, x):
+        if not (self.training and torch.is_grad_enabled()):
+            return F.linear(x, self.weight.to(x.dtype), None if self.bias is None else self.bias.to(x.dtype))
+        if torch.is_autocast_enabled("cuda"):
+            x = x.to(torch.get_autocast_dtype("cuda"))
+        with torch.autocast("cuda", enabled=False):
+            return HLQLinearFunction.apply(x, self.weight, self.bias, self.strategy)
+
+    @classmethod
+    def from_linear(cls, lin: nn.Linear, strategy: BackwardStrategy | None = None) -> "HLQLinear":
+        m = cls(lin.in_features, lin.out_features, bias=lin.bias is not None, strategy=strategy,
+                device=lin.weight.device, dtype=lin.weight.dtype)
+        with torch.no_grad():
+            m.weight.copy_(lin.weight)
+            if lin.bias is not None:
+                m.bias.copy_(lin.bias)
+        return m
+
+
+def convert_linears(module: nn.Module, strategy: BackwardStrategy | None = None) -> nn.Module:
+    """Swap every nn.Linear under `module` for HLQLinear (in place)."""
+    for name, child in list(module.named_children()):
+        if isinstance(child, nn.Linear) and not isinstance(child, HLQLinear):
+            setattr(module, name, HLQLinear.from_linear(child, strategy))
+        else:
+            convert_linears(child, strategy)
+    return module

@@ -1,0 +1,152 @@
+"""Torch-facing wrappers over the C-ABI stage primitives.
+
+Every function takes / returns CUDA tensors, allocates outputs with the torch
+caching allocator, and enqueues work on torch's current stream.  There is no
+CPU path: a CPU tensor raises ParameterError and a missing library raises
+HLQLibraryError.
+"""
+from __future__ import annotations
+
+import ctypes
+
+import torch
+
+from . import _lib
+from .errors import DimensionError, ParameterError
+
+QMAX = {4: 7, 8: 127}
+
+
+def pad16(n: int) -> int:
+    return (int(n) + 15) & ~15
+
+
+def _stream():
+    return ctypes.c_void_p(torch.cuda.current_stream().cuda_stream)
+
+
+def _p(t):
+    return ctypes.c_void_p(0 if t is None else t.data_ptr())
+
+
+def dtype_code(t: torch.Tensor) -> int:
+    if t.dtype == torch.float32:
+        return _lib.HLQ_F32
+    if t.dtype == torch.bfloat16:
+        return _lib.HLQ_BF16
+    raise ParameterError(f"HLQ kernels take float32 or bfloat16 inputs, got {t.dtype}")
+
+
+def _cuda(t: torch.Tensor, what: str) -> torch.Tensor:
+    if not t.is_cuda:
+        raise ParameterError(f"{what} must be a CUDA tensor (the HLQ path has no CPU fallback)")
+    return t if t.is_contiguous() else t.contiguous()
+
+
+def _check_bits(bits):
+    if bits not in (4, 8):
+        raise ParameterError(f"bits must be 4 or 8, got {bits}")
+
+
+def quant_ht_cols(src: torch.Tensor, bits: int):
+    """Q_bits(block-FWHT of every row of a (rows, cols) matrix along cols).
+    Returns (codes (rows, pad16(cols)) int8, scale (1,) fp32, amax_bits (1,) int32)."""
+    _check_bits(bits)
+    src = _cuda(src, "src")
+    rows, cols = src.shape
+    ld = pad16(cols)
+    codes = torch.empty((rows, ld), dtype=torch.int8, device=src.device)
+    scale = torch.empty(1, dtype=torch.float32, device=src.device)
+    amax = torch.empty(1, dtype=torch.int32, device=src.device)
+    _lib.call("hlq_quantize_ht_cols", _p(src), dtype_code(src), rows, cols, cols, bits, _p(amax),
+              _p(codes), ld, _p(scale), _stream())
+    return codes, scale, amax
+
+
+def proj_rows_k(segs: int, rows: int, rank: int) -> int:
+    return segs * ((rows + 15) // 16) * rank
+
+
+def quant_proj_rows(src: torch.Tensor, segs: int, rows: int, cols: int, bitmap: int, bits: int,
+                    ld_src: int | None = None, seg_src: int | None = None):
+    """Q_bits(rank-r block projection along rows), written transposed.
+    Returns (codes (cols, pad16(K)) int8, K, scale (1,), amax_bits (1,))."""
+    _check_bits(bits)
+    src = _cuda(src, "src")
+    ld_src = cols if ld_src is None else ld_src
+    seg_src = rows * ld_src if seg_src is None else seg_src
+    k = proj_rows_k(segs, rows, bin(bitmap).count("1"))
+    ld = max(pad16(k), 16)
+    codes = torch.empty((cols, ld), dtype=torch.int8, device=src.device)
+    if ld != k:
+        codes[:, k:].zero_()  # keep the alignment tail deterministic (never read by the GEMM)
+    scale = torch.empty(1, dtype=torch.float32, device=src.device)
+    amax = torch.empty(1, dtype=torch.int32, device=src.device)
+    _lib.call("hlq_quantize_proj_rows", _p(src), dtype_code(src), segs, rows, cols, ld_src, seg_src,
+              bitmap, bits, _p(amax), _p(codes), ld, _p(scale), _stream())
+    return codes, k, scale, amax
+
+
+def proj_rows_amax(src: torch.Tensor, segs: int, rows: int, cols: int, bitmap: int,
+                   amax: torch.Tensor, ld_src: int | None = None, seg_src: int | None = None):
+    """Accumulate the transformed amax (IEEE bits, atomic max) into `amax`."""
+    src = _cuda(src, "src")
+    ld_src = cols if ld_src is None else ld_src
+    seg_src = rows * ld_src if seg_src is None else seg_src
+    _lib.call("hlq_proj_rows_amax", _p(src), dtype_code(src), segs, rows, cols, ld_src, seg_src,
+              bitmap, _p(amax), _stream())
+
+
+def proj_rows_quant(src: torch.Tensor, segs: int, rows: int, cols: int, bitmap: int, bits: int,
+                    amax: torch.Tensor, ld_src: int | None = None, seg_src: int | None = None):
+    src = _cuda(src, "src")
+    ld_src = cols if ld_src is None else ld_src
+    seg_src = rows * ld_src if seg_src is None else seg_src
+    k = proj_rows_k(segs, rows, bin(bitmap).count("1"))
+    ld = max(pad16(k), 16)
+    codes = torch.empty((cols, ld), dtype=torch.int8, device=src.device)
+    if ld != k:
+        codes[:, k:].zero_()
+    scale = torch.empty(1, dtype=torch.float32, device=src.device)
+    _lib.call("hlq_proj_rows_quant", _p(src), dtype_code(src), segs, rows, cols, ld_src, seg_src,
+              bitmap, bits, _p(amax), _p(codes), ld, _p(scale), _stream())
+    return codes, k, scale
+
+
+def gemm_i8(a: torch.Tensor, b: torch.Tensor, m: int, n: int, k: int, bits_a: int, bits_b: int,
+            sa: torch.Tensor, sb: torch.Tensor, extra: float = 1.0, exact: bool = True,
+            out_dtype=torch.float32, want_acc: bool = False, want_out: bool = True,
+            groups: int = 1, a_gstride: int | None = None, b_gstride: int | None = None):
+    """D[m, n] = sum_(g,k) A[g][m, k] B[g][n, k] on K-major int8 codes, fused dequant.
+    Returns (out or None, acc or None)."""
+    if a.dtype != torch.int8 or b.dtype != torch.int8:
+        raise ParameterError("GEMM operands must be int8 codes")
+    dev = a.device
+    out = torch.empty((m, n), dtype=out_dtype, device=dev) if want_out else None
+    acc = torch.empty((m, n), dtype=torch.int32, device=dev) if want_acc else None
+    lda, ldb = a.stride(0), b.stride(0)
+    a_gs = lda * m if a_gstride is None else a_gstride
+    b_gs = ldb * n if b_gstride is None else b_gstride
+    _lib.call("hlq_gemm_i8_grouped", _p(a), lda, a_gs, _p(b), ldb, b_gs, m, n, k, groups, bits_a,
+              bits_b, _p(sa), _p(sb), float(extra),
+              _lib.HLQ_EPI_EXACT if exact else _lib.HLQ_EPI_FAST, _p(out),
+              _lib.HLQ_BF16 if out_dtype == torch.bfloat16 else _lib.HLQ_F32, n, _p(acc), n,
+              _stream())
+    return out, acc
+
+
+def amax_to_float(amax_bits: torch.Tensor) -> torch.Tensor:
+    return amax_bits.view(torch.float32)
+
+
+def check_finite(*amax_bits: torch.Tensor) -> None:
+    """Raise ValueError (quantize.py:138-139) if a transformed operand held NaN/Inf.
+    Synchronizes; used by the reference-mirroring API, not by the training path."""
+    for a in amax_bits:
+        if int(a.item()) & 0xFFFFFFFF >= 0x7F800000:
+            raise ValueError("cannot quantize non-finite values")
+
+
+def require_dims(cond: bool, msg: str):
+    if not cond:
+        raise DimensionError(msg)
