@@ -71,10 +71,11 @@ HLQ_API int hlq_device_ok(void);
  * Replaces `_block_axis(gy, 2, plan)` + `quant_pseudo_stochastic` on the gx
  * left operand (backprop.py:212-220,362,367; quantize.py:128-145).
  * Writes codes (rows x pad16(cols), leading dim ld_dst >= pad16(cols), a
- * multiple of 16) and the fp32 scale.  amax_ws: 4-byte device scratch that
- * also carries the per-tensor amax bits out.  bits in {4, 8}. */
+ * multiple of 16) and the fp32 scale.  stats_ws: 16-byte (4 x uint32) device
+ * scratch; on return stats_ws[0] holds the bits of max|4v| (>= 0x7F800000
+ * means a NaN/Inf was present, the reference's ValueError).  bits in {4, 8}. */
 HLQ_API int hlq_quantize_ht_cols(const void* src, int dtype, int64_t rows, int64_t cols, int64_t ld_src,
-                         int bits, uint32_t* amax_ws, int8_t* dst, int64_t ld_dst,
+                         int bits, uint32_t* stats_ws, int8_t* dst, int64_t ld_dst,
                          float* scale_out, void* stream);
 
 /* Q_bits( rank-r block projection along the ROW axis of src ), codes written
@@ -82,22 +83,36 @@ HLQ_API int hlq_quantize_ht_cols(const void* src, int dtype, int64_t rows, int64
  * src is `segs` segments of (rows x cols) with row stride ld_src and segment
  * stride seg_src.  Replaces `_project_axis` + `quant_pseudo_stochastic`
  * (backprop.py:223-234; acbp_compress :373-385; hlq_grad_weight :401-407) and,
- * with bitmap 0xFFFF, `_block_axis(w, 0, plan)` (:363). */
+ * with bitmap 0xFFFF, `_block_axis(w, 0, plan)` (:363).  stats_ws: 16-byte
+ * scratch, the amax bits land in stats_ws[2]. */
 HLQ_API int hlq_quantize_proj_rows(const void* src, int dtype, int64_t segs, int64_t rows, int64_t cols,
                            int64_t ld_src, int64_t seg_src, uint32_t bitmap, int bits,
-                           uint32_t* amax_ws, int8_t* dst, int64_t ld_dst, float* scale_out,
+                           uint32_t* stats_ws, int8_t* dst, int64_t ld_dst, float* scale_out,
                            void* stream);
+
+/* Both gy operands in ONE read of gy per pass (the fused "dual" transform):
+ * the gx codes Q_bits_gx(HT along cols) exactly as hlq_quantize_ht_cols and
+ * the gw codes Q_bits_gw(projection along rows) exactly as
+ * hlq_quantize_proj_rows, over the same (segs x rows x cols) view.  Valid when
+ * the token axis is the projection axis (reference axis rule L >= 16, or
+ * L == 1 with projection along the batch).  stats_ws: 16 bytes. */
+HLQ_API int hlq_quantize_dual(const void* src, int dtype, int64_t segs, int64_t rows, int64_t cols,
+                              int64_t ld_src, int64_t seg_src, uint32_t bitmap, int bits_gx,
+                              int bits_gw, uint32_t* stats_ws, int8_t* dst_gx, int64_t ld_gx,
+                              int8_t* dst_gw, int64_t ld_gw, float* scale_gx, float* scale_gw,
+                              void* stream);
 
 /* The two passes of hlq_quantize_proj_rows, separately, for the data-parallel
  * global-scale mode: _amax accumulates (atomic max, no reset) the transformed
- * amax into *amax_bits; callers all-reduce(MAX) it across ranks, then _quant
+ * statistics into stats[2..3] (stats: 4 x uint32, zero-initialised by the
+ * caller); callers all-reduce(MAX) the 4 words across ranks, then _quant
  * quantizes with scale = amax / qmax (quantize.py:94-100). */
 HLQ_API int hlq_proj_rows_amax(const void* src, int dtype, int64_t segs, int64_t rows, int64_t cols,
-                       int64_t ld_src, int64_t seg_src, uint32_t bitmap, uint32_t* amax_bits,
+                       int64_t ld_src, int64_t seg_src, uint32_t bitmap, uint32_t* stats,
                        void* stream);
 HLQ_API int hlq_proj_rows_quant(const void* src, int dtype, int64_t segs, int64_t rows, int64_t cols,
                         int64_t ld_src, int64_t seg_src, uint32_t bitmap, int bits,
-                        const uint32_t* amax_bits, int8_t* dst, int64_t ld_dst, float* scale_out,
+                        const uint32_t* stats, int8_t* dst, int64_t ld_dst, float* scale_out,
                         void* stream);
 
 /* D[m, n] = sum_k A[m, k] * B[n, k] on int8 codes (tcgen05 kind::i8, int32 in
@@ -136,10 +151,10 @@ HLQ_API int64_t hlq_acbp_rows(int64_t L, int64_t I, int axis);
 /* backprop.py:373-385  acbp_compress(x, plan, bits, pad_small_axes).
  * x is (B, L, I); axis from ht_axis_for (0 = batch, 1 = tokens).  Payload is
  * written K-major, payload[row * ld_payload + k] (the reference's (K, I)
- * payload, transposed; see hlq_acbp_k).  amax_ws: 4-byte scratch. */
+ * payload, transposed; see hlq_acbp_k).  stats_ws: 16-byte scratch. */
 HLQ_API int hlq_acbp_compress(const void* x, int dtype, int64_t B, int64_t L, int64_t I, int axis,
                       uint32_t bitmap, int bits, int8_t* payload, int64_t ld_payload,
-                      float* scale_out, uint32_t* amax_ws, void* stream);
+                      float* scale_out, uint32_t* stats_ws, void* stream);
 
 /* Workspace bytes needed by hlq_hq_grad_input / hlq_grad_weight. */
 HLQ_API size_t hlq_hq_grad_input_ws(int64_t T, int64_t O, int64_t I);

@@ -209,7 +209,7 @@ def hq_grad_input(gy: torch.Tensor, w: torch.Tensor, bits: int | None, rng=None,
     out, acc = ops.gemm_i8(cg, cw, B * L, I, ops.pad16(O), bits, bits, sg, sw, 1.0, exact=exact,
                            out_dtype=out_dtype, want_acc=stages is not None)
     if stages is not None:
-        stages.update(gx_codes_g=cg[:, :ops.pad16(O)], gx_scale_g=sg, gx_codes_w=cw[:, :kw],
+        stages.update(gx_codes_g=cg[:, :ops.pad16(O)], gx_scale_g=sg, gx_codes_w=cw[:, :kw].t(),
                       gx_scale_w=sw, gx_acc=acc)
     return out.reshape(B, L, I)
 
@@ -248,6 +248,43 @@ def hlq_grad_weight(acbp: ACBPActivation, gy: torch.Tensor, bits: int = 8, rng=N
     return out
 
 
+def dual_ok(B: int, L: int, axis: int) -> bool:
+    """The fused gy transform needs the projection view's rows to be the HT
+    view's rows: projection along tokens, or along the batch with L == 1."""
+    return axis == 1 or L == 1
+
+
+def hlq_pair(acbp: ACBPActivation, w: torch.Tensor, gy: torch.Tensor, bits_gx: int, bits_gw: int,
+             extra_scale: float, exact: bool = True, gx_dtype=torch.float32,
+             check_finite: bool = True, stages: dict | None = None):
+    """Both HLQ products with ONE fused transform of gy (two passes instead of
+    four): returns (gx (B, L, I), gw (O, I)).  Same numerics as calling
+    hlq_grad_weight and hq_grad_input separately."""
+    B, L, I = acbp.orig_shape
+    O = gy.shape[2]
+    if acbp.quantized.bits != bits_gw:
+        raise StateError(f"compressed activation is {acbp.quantized.bits}-bit but backward wants {bits_gw}-bit")
+    segs, rows, cols, ld_src, seg_src = _proj_view(B, L, O, acbp.axis)
+    cgx, sgx, cgw, k, sgw, st = ops.quant_dual(gy, segs, rows, cols, acbp.plan.gpu_bitmap(),
+                                               bits_gx, bits_gw, ld_src, seg_src)
+    if k != acbp.k:
+        raise StateError("projected extents differ between forward and backward; the plans do not match")
+    w32 = w if w.dtype == torch.float32 else w.float()
+    cw, kw, sw, aw = ops.quant_proj_rows(w32, 1, O, I, 0xFFFF, bits_gx)
+    if check_finite:
+        ops.check_finite(st[0:1], st[2:3], aw)
+    xp = acbp.quantized.payload
+    want = stages is not None
+    gw, accw = ops.gemm_i8(cgw, xp, O, I, k, bits_gw, bits_gw, sgw, acbp.quantized.scale, extra_scale,
+                           exact=exact, want_acc=want)
+    gx, accx = ops.gemm_i8(cgx, cw, B * L, I, ops.pad16(O), bits_gx, bits_gx, sgx, sw, 1.0,
+                           exact=exact, out_dtype=gx_dtype, want_acc=want)
+    if want:
+        stages.update(gx_codes_g=cgx, gx_scale_g=sgx, gx_codes_w=cw[:, :kw].t(), gx_scale_w=sw,
+                      gx_acc=accx, gw_codes_g=cgw[:, :k], gw_scale_g=sgw, gw_acc=accw)
+    return gx.reshape(B, L, I), gw
+
+
 def _vanilla_gx(gy, w):
     B, L, O = gy.shape
     return (gy.reshape(-1, O).float() @ w.float()).reshape(B, L, -1)
@@ -281,7 +318,13 @@ def strategy_backward(x_or_acbp, w: torch.Tensor, gy: torch.Tensor, strategy: Ba
         B, L, I = acbp.orig_shape
         if gy.dim() != 3 or tuple(gy.shape[:2]) != (B, L) or w.shape[1] != I:
             raise DimensionError(f"gy {tuple(gy.shape)} / w {tuple(w.shape)} do not match activation {acbp.orig_shape}")
-        gw = hlq_grad_weight(acbp, gy, bits=strategy.grad_weight_path.bits or 8, rng=rng, stages=stages)
+        bits_gw = strategy.grad_weight_path.bits or 8
+        if (strategy.grad_input_path.mode == "ht_quant" and strategy.grad_input_path.bits
+                and rng is None and dual_ok(B, L, acbp.axis)):
+            gx, gw = hlq_pair(acbp, w, gy, strategy.grad_input_path.bits, bits_gw, 1.0 / B,
+                              stages=stages)
+            return GradPair(gx, gw)
+        gw = hlq_grad_weight(acbp, gy, bits=bits_gw, rng=rng, stages=stages)
         gx = _grad_input(gy, w, strategy, rng, stages)
         return GradPair(gx, gw)
     x = x_or_acbp
@@ -294,17 +337,17 @@ def strategy_backward(x_or_acbp, w: torch.Tensor, gy: torch.Tensor, strategy: Ba
         raise DimensionError(f"weight {tuple(w.shape)} does not match input channels {I}")
     if tuple(gy.shape) != (B, L, O):
         raise DimensionError(f"gy shape {tuple(gy.shape)} does not match ({B}, {L}, {O})")
-    gx = _grad_input(gy, w, strategy, rng, stages)
     spec = strategy.grad_weight_path
-    if spec.mode == "fp":
-        gw = _vanilla_gw(x, gy)
-    elif spec.mode == "lowrank_quant":
+    if spec.mode == "lowrank_quant":
         # raw branch == ACBP branch bit for bit in pseudo mode (test_backprop.py:338-345)
         acbp = acbp_compress(x, strategy.plan, bits=spec.bits or 8, rng=rng,
                              pad_small_axes=strategy.pad_small_axes)
         if stages is not None:
             stages.update(x_codes=acbp.reference_payload(), x_scale=acbp.quantized.scale, axis=acbp.axis)
-        gw = hlq_grad_weight(acbp, gy, bits=spec.bits or 8, rng=rng, stages=stages)
+        return strategy_backward(acbp, w, gy, strategy, rng=rng, stages=stages)
+    gx = _grad_input(gy, w, strategy, rng, stages)
+    if spec.mode == "fp":
+        gw = _vanilla_gw(x, gy)
     else:
         raise ParameterError(f"grad_weight mode {spec.mode!r} is a baseline without a B200 kernel "
                              "(SURVEY.md 8(f) f4)")

@@ -120,7 +120,7 @@ int hlq_device_ok(void) {
 }
 
 int hlq_quantize_ht_cols(const void* src, int dtype, int64_t rows, int64_t cols, int64_t ld_src,
-                         int bits, uint32_t* amax_ws, int8_t* dst, int64_t ld_dst,
+                         int bits, uint32_t* stats_ws, int8_t* dst, int64_t ld_dst,
                          float* scale_out, void* stream) {
   HLQ_TRY(check_dtype(dtype));
   HLQ_TRY(check_bits(bits));
@@ -128,47 +128,82 @@ int hlq_quantize_ht_cols(const void* src, int dtype, int64_t rows, int64_t cols,
   if (rows < 0 || cols < 0 || ld_src < cols || ld_dst < pad16(cols))
     return fail(HLQ_ERR_DIMENSION, "bad ht_cols view rows=%lld cols=%lld ld_src=%lld ld_dst=%lld",
                 (long long)rows, (long long)cols, (long long)ld_src, (long long)ld_dst);
+  if (!src && rows * cols > 0) return fail(HLQ_ERR_PARAMETER, "null source");
   cudaStream_t st = static_cast<cudaStream_t>(stream);
-  cudaMemsetAsync(amax_ws, 0, sizeof(uint32_t), st);
-  hlq::launch_ht_cols_any(src, dtype, rows, cols, ld_src, bits, hlq::kStats, amax_ws, nullptr, 0,
-                          nullptr, st);
-  hlq::launch_ht_cols_any(src, dtype, rows, cols, ld_src, bits, hlq::kQuant, amax_ws, dst, ld_dst,
-                          scale_out, st);
+  hlq::TransformArgs t{};
+  t.src = src; t.dtype = dtype; t.segs = 1; t.rows = rows; t.cols = cols; t.ld_src = ld_src;
+  t.seg_src = rows * ld_src; t.do_gx = true; t.do_gw = false; t.bitmap = 0xFFFF;
+  t.bits_gx = bits; t.bits_gw = bits; t.stats = stats_ws; t.dst_gx = dst; t.ld_gx = ld_dst;
+  t.scale_gx = scale_out;
+  cudaMemsetAsync(stats_ws, 0, 4 * sizeof(uint32_t), st);
+  hlq::launch_transform(t, hlq::kStats, st);
+  hlq::launch_transform(t, hlq::kQuant, st);
   return cuda_status("hlq_quantize_ht_cols");
 }
 
+static hlq::TransformArgs proj_args(const void* src, int dtype, int64_t segs, int64_t rows,
+                                    int64_t cols, int64_t ld_src, int64_t seg_src, uint32_t bitmap,
+                                    int bits, uint32_t* stats, int8_t* dst, int64_t ld_dst,
+                                    float* scale_out) {
+  hlq::TransformArgs t{};
+  t.src = src; t.dtype = dtype; t.segs = segs; t.rows = rows; t.cols = cols; t.ld_src = ld_src;
+  t.seg_src = seg_src; t.do_gx = false; t.do_gw = true; t.bitmap = bitmap; t.bits_gx = bits;
+  t.bits_gw = bits; t.stats = stats; t.dst_gw = dst; t.ld_gw = ld_dst; t.scale_gw = scale_out;
+  return t;
+}
+
 int hlq_proj_rows_amax(const void* src, int dtype, int64_t segs, int64_t rows, int64_t cols,
-                       int64_t ld_src, int64_t seg_src, uint32_t bitmap, uint32_t* amax_bits,
+                       int64_t ld_src, int64_t seg_src, uint32_t bitmap, uint32_t* stats,
                        void* stream) {
   HLQ_TRY(proj_rows_checked(src, dtype, segs, rows, cols, ld_src, seg_src, bitmap, 8, nullptr, 0));
-  hlq::launch_proj_rows_any(src, dtype, segs, rows, cols, ld_src, seg_src, bitmap, 8, hlq::kStats,
-                            amax_bits, nullptr, 0, nullptr, static_cast<cudaStream_t>(stream));
+  hlq::launch_transform(proj_args(src, dtype, segs, rows, cols, ld_src, seg_src, bitmap, 8, stats,
+                                  nullptr, 0, nullptr),
+                        hlq::kStats, static_cast<cudaStream_t>(stream));
   return cuda_status("hlq_proj_rows_amax");
 }
 
 int hlq_proj_rows_quant(const void* src, int dtype, int64_t segs, int64_t rows, int64_t cols,
                         int64_t ld_src, int64_t seg_src, uint32_t bitmap, int bits,
-                        const uint32_t* amax_bits, int8_t* dst, int64_t ld_dst, float* scale_out,
+                        const uint32_t* stats, int8_t* dst, int64_t ld_dst, float* scale_out,
                         void* stream) {
   HLQ_TRY(proj_rows_checked(src, dtype, segs, rows, cols, ld_src, seg_src, bitmap, bits, dst, ld_dst));
-  hlq::launch_proj_rows_any(src, dtype, segs, rows, cols, ld_src, seg_src, bitmap, bits, hlq::kQuant,
-                            const_cast<uint32_t*>(amax_bits), dst, ld_dst, scale_out,
-                            static_cast<cudaStream_t>(stream));
+  hlq::launch_transform(proj_args(src, dtype, segs, rows, cols, ld_src, seg_src, bitmap, bits,
+                                  const_cast<uint32_t*>(stats), dst, ld_dst, scale_out),
+                        hlq::kQuant, static_cast<cudaStream_t>(stream));
   return cuda_status("hlq_proj_rows_quant");
 }
 
 int hlq_quantize_proj_rows(const void* src, int dtype, int64_t segs, int64_t rows, int64_t cols,
                            int64_t ld_src, int64_t seg_src, uint32_t bitmap, int bits,
-                           uint32_t* amax_ws, int8_t* dst, int64_t ld_dst, float* scale_out,
+                           uint32_t* stats_ws, int8_t* dst, int64_t ld_dst, float* scale_out,
                            void* stream) {
   HLQ_TRY(proj_rows_checked(src, dtype, segs, rows, cols, ld_src, seg_src, bitmap, bits, dst, ld_dst));
   cudaStream_t st = static_cast<cudaStream_t>(stream);
-  cudaMemsetAsync(amax_ws, 0, sizeof(uint32_t), st);
-  hlq::launch_proj_rows_any(src, dtype, segs, rows, cols, ld_src, seg_src, bitmap, bits, hlq::kStats,
-                            amax_ws, nullptr, 0, nullptr, st);
-  hlq::launch_proj_rows_any(src, dtype, segs, rows, cols, ld_src, seg_src, bitmap, bits, hlq::kQuant,
-                            amax_ws, dst, ld_dst, scale_out, st);
+  const hlq::TransformArgs t = proj_args(src, dtype, segs, rows, cols, ld_src, seg_src, bitmap, bits,
+                                         stats_ws, dst, ld_dst, scale_out);
+  cudaMemsetAsync(stats_ws, 0, 4 * sizeof(uint32_t), st);
+  hlq::launch_transform(t, hlq::kStats, st);
+  hlq::launch_transform(t, hlq::kQuant, st);
   return cuda_status("hlq_quantize_proj_rows");
+}
+
+int hlq_quantize_dual(const void* src, int dtype, int64_t segs, int64_t rows, int64_t cols,
+                      int64_t ld_src, int64_t seg_src, uint32_t bitmap, int bits_gx, int bits_gw,
+                      uint32_t* stats_ws, int8_t* dst_gx, int64_t ld_gx, int8_t* dst_gw,
+                      int64_t ld_gw, float* scale_gx, float* scale_gw, void* stream) {
+  HLQ_TRY(check_bits(bits_gx));
+  HLQ_TRY(proj_rows_checked(src, dtype, segs, rows, cols, ld_src, seg_src, bitmap, bits_gw, dst_gw,
+                            ld_gw));
+  HLQ_TRY(check_ld16(ld_gx, "gx codes"));
+  if (ld_gx < pad16(cols)) return fail(HLQ_ERR_DIMENSION, "gx codes ld < pad16(cols)");
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  hlq::TransformArgs t = proj_args(src, dtype, segs, rows, cols, ld_src, seg_src, bitmap, bits_gw,
+                                   stats_ws, dst_gw, ld_gw, scale_gw);
+  t.do_gx = true; t.bits_gx = bits_gx; t.dst_gx = dst_gx; t.ld_gx = ld_gx; t.scale_gx = scale_gx;
+  cudaMemsetAsync(stats_ws, 0, 4 * sizeof(uint32_t), st);
+  hlq::launch_transform(t, hlq::kStats, st);
+  hlq::launch_transform(t, hlq::kQuant, st);
+  return cuda_status("hlq_quantize_dual");
 }
 
 int hlq_gemm_i8(const int8_t* A, int64_t lda, const int8_t* B, int64_t ldb, int64_t M, int64_t N,
@@ -220,15 +255,15 @@ int64_t hlq_acbp_rows(int64_t L, int64_t I, int axis) { return axis == 1 ? I : L
 
 int hlq_acbp_compress(const void* x, int dtype, int64_t B, int64_t L, int64_t I, int axis,
                       uint32_t bitmap, int bits, int8_t* payload, int64_t ld_payload,
-                      float* scale_out, uint32_t* amax_ws, void* stream) {
+                      float* scale_out, uint32_t* stats_ws, void* stream) {
   if (axis != 0 && axis != 1) return fail(HLQ_ERR_PARAMETER, "axis must be 0 or 1, got %d", axis);
   // axis 1: B segments of (L x I); axis 0: one segment of (B x L*I) -- the
   // reference's (B_p r/16, L, I) payload flattens to rows (blk*r + j)*L + l,
   // which is exactly column (l*I + i) of the transposed projection.
   if (axis == 1)
-    return hlq_quantize_proj_rows(x, dtype, B, L, I, I, L * I, bitmap, bits, amax_ws, payload,
+    return hlq_quantize_proj_rows(x, dtype, B, L, I, I, L * I, bitmap, bits, stats_ws, payload,
                                   ld_payload, scale_out, stream);
-  return hlq_quantize_proj_rows(x, dtype, 1, B, L * I, L * I, B * L * I, bitmap, bits, amax_ws,
+  return hlq_quantize_proj_rows(x, dtype, 1, B, L * I, L * I, B * L * I, bitmap, bits, stats_ws,
                                 payload, ld_payload, scale_out, stream);
 }
 
@@ -251,10 +286,10 @@ int hlq_hq_grad_input(const void* gy, int gy_dtype, int64_t T, int64_t O, const 
   p += align256(size_t(T * op));
   int8_t* cw = reinterpret_cast<int8_t*>(p);
   p += align256(size_t(I * op));
-  uint32_t* amax = reinterpret_cast<uint32_t*>(p);  // [0] gy, [1] w
+  uint32_t* stats = reinterpret_cast<uint32_t*>(p);    // [0..3] gy, [4..7] w
   float* scales = reinterpret_cast<float*>(p + 64);  // [0] gy, [1] w
-  HLQ_TRY(hlq_quantize_ht_cols(gy, gy_dtype, T, O, O, bits, amax, cg, op, scales, stream));
-  HLQ_TRY(hlq_quantize_proj_rows(w, HLQ_F32, 1, O, I, I, O * I, 0xFFFFu, bits, amax + 1, cw, op,
+  HLQ_TRY(hlq_quantize_ht_cols(gy, gy_dtype, T, O, O, bits, stats, cg, op, scales, stream));
+  HLQ_TRY(hlq_quantize_proj_rows(w, HLQ_F32, 1, O, I, I, O * I, 0xFFFFu, bits, stats + 4, cw, op,
                                  scales + 1, stream));
   return hlq_gemm_i8(cg, op, cw, op, T, I, op, bits, bits, scales, scales + 1, 1.0, epilogue, dx,
                      dx_dtype, I, nullptr, 0, stream);
@@ -283,14 +318,14 @@ int hlq_grad_weight(const int8_t* payload, int64_t ld_payload, const float* x_sc
   uint8_t* p = static_cast<uint8_t*>(ws);
   int8_t* cg = reinterpret_cast<int8_t*>(p);
   p += align256(size_t(hlq_acbp_rows(L, O, axis) * ldk));
-  uint32_t* amax = reinterpret_cast<uint32_t*>(p);
+  uint32_t* stats = reinterpret_cast<uint32_t*>(p);
   float* scale = reinterpret_cast<float*>(p + 64);
   if (axis == 1)
-    HLQ_TRY(hlq_quantize_proj_rows(gy, gy_dtype, B, L, O, O, L * O, bitmap, bits, amax, cg, ldk, scale,
-                                   stream));
+    HLQ_TRY(hlq_quantize_proj_rows(gy, gy_dtype, B, L, O, O, L * O, bitmap, bits, stats, cg, ldk,
+                                   scale, stream));
   else
-    HLQ_TRY(hlq_quantize_proj_rows(gy, gy_dtype, 1, B, L * O, L * O, B * L * O, bitmap, bits, amax, cg,
-                                   ldk, scale, stream));
+    HLQ_TRY(hlq_quantize_proj_rows(gy, gy_dtype, 1, B, L * O, L * O, B * L * O, bitmap, bits, stats,
+                                   cg, ldk, scale, stream));
   // axis 0: the transposed projections have L*O rows (l, o) and L*I rows
   // (l, i); the reference's K index (blk, j, l) becomes L stacked K panels.
   const int64_t groups = axis == 0 ? L : 1;

@@ -11,14 +11,30 @@ enum : int { kEpiExact = 0, kEpiFast = 1 };
 
 int num_sms();
 
-void launch_ht_cols_any(const void* src, int dtype, int64_t rows, int64_t cols, int64_t ld_src,
-                        int bits, int mode, uint32_t* amax_bits, int8_t* dst, int64_t ld_dst,
-                        float* scale_out, cudaStream_t stream);
+// One pass (STATS or QUANT) of the transform kernels over a (segs x rows x cols)
+// view.  do_gx: 16-point HT along cols, codes row-major into dst_gx (row index
+// seg*rows + row).  do_gw: projection along rows keeping `bitmap`'s bases,
+// codes transposed into dst_gw[col * ld_gw + (seg * nblk + blk) * rank + j].
+// stats: {amax_gx, ~minnz_gx, amax_gw, ~minnz_gw} (uint32 bits, max-reduced;
+// zero-initialised by the caller before the STATS pass).  When only do_gw is
+// set the gw statistics still live at stats[2..3].
+struct TransformArgs {
+  const void* src;
+  int dtype;
+  int64_t segs, rows, cols, ld_src, seg_src;
+  bool do_gx, do_gw;
+  uint32_t bitmap;
+  int bits_gx, bits_gw;
+  uint32_t* stats;
+  int8_t* dst_gx;
+  int64_t ld_gx;
+  int8_t* dst_gw;
+  int64_t ld_gw;
+  float* scale_gx;
+  float* scale_gw;
+};
 
-void launch_proj_rows_any(const void* src, int dtype, int64_t segs, int64_t rows, int64_t cols,
-                          int64_t ld_src, int64_t seg_src, uint32_t bitmap, int bits, int mode,
-                          uint32_t* amax_bits, int8_t* dst, int64_t ld_dst, float* scale_out,
-                          cudaStream_t stream);
+void launch_transform(const TransformArgs& t, int mode, cudaStream_t stream);
 
 // Returns a cudaError_t-compatible code (0 on success) or -1 if the tensor maps
 // could not be encoded.

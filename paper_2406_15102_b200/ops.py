@@ -48,6 +48,11 @@ def _check_bits(bits):
         raise ParameterError(f"bits must be 4 or 8, got {bits}")
 
 
+def new_stats(device) -> torch.Tensor:
+    """4 x uint32 statistics scratch: {amax, ~minnz} for the gx and gw operands."""
+    return torch.zeros(4, dtype=torch.int32, device=device)
+
+
 def quant_ht_cols(src: torch.Tensor, bits: int):
     """Q_bits(block-FWHT of every row of a (rows, cols) matrix along cols).
     Returns (codes (rows, pad16(cols)) int8, scale (1,) fp32, amax_bits (1,) int32)."""
@@ -57,10 +62,33 @@ def quant_ht_cols(src: torch.Tensor, bits: int):
     ld = pad16(cols)
     codes = torch.empty((rows, ld), dtype=torch.int8, device=src.device)
     scale = torch.empty(1, dtype=torch.float32, device=src.device)
-    amax = torch.empty(1, dtype=torch.int32, device=src.device)
-    _lib.call("hlq_quantize_ht_cols", _p(src), dtype_code(src), rows, cols, cols, bits, _p(amax),
+    stats = torch.empty(4, dtype=torch.int32, device=src.device)
+    _lib.call("hlq_quantize_ht_cols", _p(src), dtype_code(src), rows, cols, cols, bits, _p(stats),
               _p(codes), ld, _p(scale), _stream())
-    return codes, scale, amax
+    return codes, scale, stats[0:1]
+
+
+def quant_dual(src: torch.Tensor, segs: int, rows: int, cols: int, bitmap: int, bits_gx: int,
+               bits_gw: int, ld_src: int | None = None, seg_src: int | None = None):
+    """Both gy operands from one read per pass: HT along cols (gx) and the
+    rank-r projection along rows (gw).  Returns
+    (gx_codes (segs*rows, pad16(cols)), gx_scale, gw_codes (cols, pad16(K)), K, gw_scale, stats)."""
+    _check_bits(bits_gx)
+    _check_bits(bits_gw)
+    src = _cuda(src, "src")
+    ld_src = cols if ld_src is None else ld_src
+    seg_src = rows * ld_src if seg_src is None else seg_src
+    k = proj_rows_k(segs, rows, bin(bitmap).count("1"))
+    ldk = max(pad16(k), 16)
+    dev = src.device
+    cgx = torch.empty((segs * rows, pad16(cols)), dtype=torch.int8, device=dev)
+    cgw = torch.empty((cols, ldk), dtype=torch.int8, device=dev)
+    scales = torch.empty(2, dtype=torch.float32, device=dev)
+    stats = torch.empty(4, dtype=torch.int32, device=dev)
+    _lib.call("hlq_quantize_dual", _p(src), dtype_code(src), segs, rows, cols, ld_src, seg_src,
+              bitmap, bits_gx, bits_gw, _p(stats), _p(cgx), cgx.stride(0), _p(cgw), ldk,
+              _p(scales), _p(scales[1:]), _stream())
+    return cgx, scales[0:1], cgw, k, scales[1:2], stats
 
 
 def proj_rows_k(segs: int, rows: int, rank: int) -> int:
@@ -78,38 +106,35 @@ def quant_proj_rows(src: torch.Tensor, segs: int, rows: int, cols: int, bitmap: 
     k = proj_rows_k(segs, rows, bin(bitmap).count("1"))
     ld = max(pad16(k), 16)
     codes = torch.empty((cols, ld), dtype=torch.int8, device=src.device)
-    if ld != k:
-        codes[:, k:].zero_()  # keep the alignment tail deterministic (never read by the GEMM)
     scale = torch.empty(1, dtype=torch.float32, device=src.device)
-    amax = torch.empty(1, dtype=torch.int32, device=src.device)
+    stats = torch.empty(4, dtype=torch.int32, device=src.device)
     _lib.call("hlq_quantize_proj_rows", _p(src), dtype_code(src), segs, rows, cols, ld_src, seg_src,
-              bitmap, bits, _p(amax), _p(codes), ld, _p(scale), _stream())
-    return codes, k, scale, amax
+              bitmap, bits, _p(stats), _p(codes), ld, _p(scale), _stream())
+    return codes, k, scale, stats[2:3]
 
 
 def proj_rows_amax(src: torch.Tensor, segs: int, rows: int, cols: int, bitmap: int,
-                   amax: torch.Tensor, ld_src: int | None = None, seg_src: int | None = None):
-    """Accumulate the transformed amax (IEEE bits, atomic max) into `amax`."""
+                   stats: torch.Tensor, ld_src: int | None = None, seg_src: int | None = None):
+    """Accumulate the transformed statistics (IEEE bits, atomic max) into stats[2:4]
+    (`stats` from new_stats(); all-reduce(MAX) it across ranks for global scales)."""
     src = _cuda(src, "src")
     ld_src = cols if ld_src is None else ld_src
     seg_src = rows * ld_src if seg_src is None else seg_src
     _lib.call("hlq_proj_rows_amax", _p(src), dtype_code(src), segs, rows, cols, ld_src, seg_src,
-              bitmap, _p(amax), _stream())
+              bitmap, _p(stats), _stream())
 
 
 def proj_rows_quant(src: torch.Tensor, segs: int, rows: int, cols: int, bitmap: int, bits: int,
-                    amax: torch.Tensor, ld_src: int | None = None, seg_src: int | None = None):
+                    stats: torch.Tensor, ld_src: int | None = None, seg_src: int | None = None):
     src = _cuda(src, "src")
     ld_src = cols if ld_src is None else ld_src
     seg_src = rows * ld_src if seg_src is None else seg_src
     k = proj_rows_k(segs, rows, bin(bitmap).count("1"))
     ld = max(pad16(k), 16)
     codes = torch.empty((cols, ld), dtype=torch.int8, device=src.device)
-    if ld != k:
-        codes[:, k:].zero_()
     scale = torch.empty(1, dtype=torch.float32, device=src.device)
     _lib.call("hlq_proj_rows_quant", _p(src), dtype_code(src), segs, rows, cols, ld_src, seg_src,
-              bitmap, bits, _p(amax), _p(codes), ld, _p(scale), _stream())
+              bitmap, bits, _p(stats), _p(codes), ld, _p(scale), _stream())
     return codes, k, scale
 
 
@@ -143,8 +168,9 @@ def check_finite(*amax_bits: torch.Tensor) -> None:
     """Raise ValueError (quantize.py:138-139) if a transformed operand held NaN/Inf.
     Synchronizes; used by the reference-mirroring API, not by the training path."""
     for a in amax_bits:
-        if int(a.item()) & 0xFFFFFFFF >= 0x7F800000:
-            raise ValueError("cannot quantize non-finite values")
+        for v in a.reshape(-1).tolist():
+            if int(v) & 0xFFFFFFFF >= 0x7F800000:
+                raise ValueError("cannot quantize non-finite values")
 
 
 def require_dims(cond: bool, msg: str):
