@@ -9,32 +9,38 @@
 //
 // One kernel template (tile_kernel) covers all of them.  A CTA owns NB
 // consecutive 16-row projection blocks x 256 columns of a (S segments x R rows
-// x C cols) view.  Per block:
-//   phase 1: thread (row r, 16-col block b) loads 16 contiguous elements
-//            (128-bit loads), runs the column-direction FWHT in registers (gx
-//            operand) and parks the raw values in shared memory (swizzled);
-//   phase 2: thread c reads its column's 16 rows from shared memory, runs the
-//            row-direction FWHT and keeps the plan's bases (gw operand / W);
-//            codes are staged in shared memory and written as >=32-byte runs.
+// x C cols) view, one block ("step") at a time:
+//   phase 1: thread (row r, 16-col block b) holds 16 contiguous elements in
+//            registers (128-bit loads, issued two steps ahead), runs the
+//            column-direction FWHT (gx operand) and parks the raw bytes in a
+//            double-buffered, bank-swizzled shared tile;
+//   phase 2: thread c reads the 16 rows of columns (2c, 2c+1) from shared
+//            memory and runs the row-direction FWHT with packed f32x2 math,
+//            keeping only the plan's bases (dead butterflies are pruned for the
+//            common compile-time basis sets); codes are staged in shared
+//            memory and written as >= 32-byte runs per output row.
 // gy is therefore read once per pass for BOTH products (the "dual" mode).
 //
 // Two passes: STATS (max|w| and min nonzero |w| of the transformed values,
 // one atomicMax per CTA per statistic, on the IEEE bits) then QUANT.
 //
 // Bit-exactness (hadamard.py:121-134, quantize.py:94-145):
-//  * butterfly stages h = 1, 2, 4, 8, (lower, upper) = (a + b, a - b), fp32 RN;
-//  * the reference multiplies by 0.25 then divides by s; we keep w = 4v and
+//  * butterfly stages h = 1, 2, 4, 8, (lower, upper) = (a + b, a - b), fp32 RN
+//    (pairing two independent lanes in one f32x2 op changes nothing per lane);
+//  * the reference multiplies by 0.25 then divides by s.  We keep w = 4v and
 //    divide by d = s/512, i.e. compute Q = RN(w/d) = 2048 * RN(v/s) exactly
-//    (power-of-two rescalings are exact for normal numbers), with the
+//    (power-of-two rescalings are exact for normal numbers) with the
 //    reciprocal-FMA division Q = fma(fma(-Q0, d, w), r, Q0), r = RN(1/d),
 //    Q0 = RN(w r) -- verified equal to IEEE division on 2.8e9 pairs inside the
 //    guard |w| >= 2^-100, |Q| >= 2^-100, 2^-125 < d < 2^125
 //    (tools/verify_fast_div.c).  The STATS pass records min nonzero |w| so the
-//    QUANT pass can check the guard once per tensor and otherwise fall back to
+//    QUANT pass checks the guard once per tensor and otherwise falls back to
 //    the literal IEEE-division formula;
-//  * floor(q), frac(q) and the up-decision use no conversion instructions:
-//    F = floor(Q), C = ceil(Q) come from the bit patterns of Q + 1.5*2^23
-//    rounded down / up, lo = F >> 11, frac*2048 > u  <=>  C - 2048*lo > u;
+//  * code = lo + [frac*2048 > u] = ceil((Q - u) / 2048) exactly, evaluated as
+//    RU(RU(Q - u) * 2^-11 + 1.5*2^23): the low byte of that float's bit
+//    pattern IS the int8 code -- no conversion instructions anywhere.  Q is
+//    clamped to +-2048*qmax first, which yields the same codes as the
+//    reference's clip after rounding;
 //  * the draw u = bits(v) & 0x7FF equals bits(w) & 0x7FF (same mantissa).
 #include <cuda_bf16.h>
 #include <cstdint>
@@ -48,53 +54,156 @@ namespace {
 
 constexpr int kTileCols = 256;
 constexpr int kThreads = 256;
-constexpr float kMagic = 12582912.0f;  // 1.5 * 2^23
-constexpr int kMagicShift = 0x4B400000 >> 11;
+constexpr float kMagic = 12582912.0f;  // 1.5 * 2^23: ulp 1, integers in its low mantissa bits
 
-// ------------------------------------------------------------------ loads
-// 16 consecutive elements -> fp32.  `n` valid (0..16); vector path if aligned.
-__device__ __forceinline__ void load16(const float* p, int n, bool vec, float (&v)[16]) {
-  if (vec && n == 16) {
+// ------------------------------------------------------------------ packed fp32x2
+__device__ __forceinline__ float2 f2add(float2 a, float2 b) {
+  float2 d;
+  asm("{.reg .b64 ra, rb, rd;\n\tmov.b64 ra, {%2, %3};\n\tmov.b64 rb, {%4, %5};\n\t"
+      "add.rn.f32x2 rd, ra, rb;\n\tmov.b64 {%0, %1}, rd;}"
+      : "=f"(d.x), "=f"(d.y) : "f"(a.x), "f"(a.y), "f"(b.x), "f"(b.y));
+  return d;
+}
+__device__ __forceinline__ float2 f2sub(float2 a, float2 b) {
+  float2 d;
+  asm("{.reg .b64 ra, rb, rd;\n\tmov.b64 ra, {%2, %3};\n\tmov.b64 rb, {%4, %5};\n\t"
+      "sub.rn.f32x2 rd, ra, rb;\n\tmov.b64 {%0, %1}, rd;}"
+      : "=f"(d.x), "=f"(d.y) : "f"(a.x), "f"(a.y), "f"(b.x), "f"(b.y));
+  return d;
+}
+__device__ __forceinline__ float2 f2mul(float2 a, float2 b) {
+  float2 d;
+  asm("{.reg .b64 ra, rb, rd;\n\tmov.b64 ra, {%2, %3};\n\tmov.b64 rb, {%4, %5};\n\t"
+      "mul.rn.f32x2 rd, ra, rb;\n\tmov.b64 {%0, %1}, rd;}"
+      : "=f"(d.x), "=f"(d.y) : "f"(a.x), "f"(a.y), "f"(b.x), "f"(b.y));
+  return d;
+}
+__device__ __forceinline__ float2 f2fma(float2 a, float2 b, float2 c) {
+  float2 d;
+  asm("{.reg .b64 ra, rb, rc, rd;\n\tmov.b64 ra, {%2, %3};\n\tmov.b64 rb, {%4, %5};\n\t"
+      "mov.b64 rc, {%6, %7};\n\tfma.rn.f32x2 rd, ra, rb, rc;\n\tmov.b64 {%0, %1}, rd;}"
+      : "=f"(d.x), "=f"(d.y) : "f"(a.x), "f"(a.y), "f"(b.x), "f"(b.y), "f"(c.x), "f"(c.y));
+  return d;
+}
+__device__ __forceinline__ float2 f2add_rp(float2 a, float2 b) {
+  float2 d;
+  asm("{.reg .b64 ra, rb, rd;\n\tmov.b64 ra, {%2, %3};\n\tmov.b64 rb, {%4, %5};\n\t"
+      "add.rp.f32x2 rd, ra, rb;\n\tmov.b64 {%0, %1}, rd;}"
+      : "=f"(d.x), "=f"(d.y) : "f"(a.x), "f"(a.y), "f"(b.x), "f"(b.y));
+  return d;
+}
+__device__ __forceinline__ float2 f2fma_rp(float2 a, float2 b, float2 c) {
+  float2 d;
+  asm("{.reg .b64 ra, rb, rc, rd;\n\tmov.b64 ra, {%2, %3};\n\tmov.b64 rb, {%4, %5};\n\t"
+      "mov.b64 rc, {%6, %7};\n\tfma.rp.f32x2 rd, ra, rb, rc;\n\tmov.b64 {%0, %1}, rd;}"
+      : "=f"(d.x), "=f"(d.y) : "f"(a.x), "f"(a.y), "f"(b.x), "f"(b.y), "f"(c.x), "f"(c.y));
+  return d;
+}
+__device__ __forceinline__ float2 f2(float a) { return make_float2(a, a); }
+
+// ------------------------------------------------------------------ element types
+template <typename T>
+struct Traits;
+template <>
+struct Traits<float> {
+  static constexpr int kVec = 4;        // uint4 chunks per 16 elements
+  static constexpr int kRowBytes = 1024;  // one 256-col smem row
+};
+template <>
+struct Traits<__nv_bfloat16> {
+  static constexpr int kVec = 2;
+  static constexpr int kRowBytes = 512;
+};
+
+__device__ __forceinline__ float bf_lo(uint32_t w) { return __uint_as_float(w << 16); }
+__device__ __forceinline__ float bf_hi(uint32_t w) { return __uint_as_float(w & 0xFFFF0000u); }
+
+// raw chunks -> 16 fp32 values
+template <typename T>
+__device__ __forceinline__ void unpack16(const uint4 (&raw)[Traits<T>::kVec], float (&v)[16]);
+template <>
+__device__ __forceinline__ void unpack16<float>(const uint4 (&raw)[4], float (&v)[16]) {
 #pragma unroll
-    for (int q = 0; q < 4; ++q) {
-      const float4 t = __ldg(reinterpret_cast<const float4*>(p) + q);
-      v[4 * q] = t.x; v[4 * q + 1] = t.y; v[4 * q + 2] = t.z; v[4 * q + 3] = t.w;
-    }
-  } else {
-#pragma unroll
-    for (int i = 0; i < 16; ++i) v[i] = i < n ? __ldg(p + i) : 0.0f;
+  for (int q = 0; q < 4; ++q) {
+    v[4 * q] = __uint_as_float(raw[q].x); v[4 * q + 1] = __uint_as_float(raw[q].y);
+    v[4 * q + 2] = __uint_as_float(raw[q].z); v[4 * q + 3] = __uint_as_float(raw[q].w);
   }
 }
-__device__ __forceinline__ void load16(const __nv_bfloat16* p, int n, bool vec, float (&v)[16]) {
+template <>
+__device__ __forceinline__ void unpack16<__nv_bfloat16>(const uint4 (&raw)[2], float (&v)[16]) {
+#pragma unroll
+  for (int q = 0; q < 2; ++q) {
+    const uint32_t w[4] = {raw[q].x, raw[q].y, raw[q].z, raw[q].w};
+#pragma unroll
+    for (int k = 0; k < 4; ++k) { v[8 * q + 2 * k] = bf_lo(w[k]); v[8 * q + 2 * k + 1] = bf_hi(w[k]); }
+  }
+}
+
+// Load the 16 elements at p (n valid, zero-filled beyond) as raw 16-byte chunks.
+template <typename T>
+__device__ __forceinline__ void load_raw(const T* p, int n, bool vec, uint4 (&raw)[Traits<T>::kVec]) {
+  constexpr int V = Traits<T>::kVec;
   if (vec && n == 16) {
 #pragma unroll
-    for (int q = 0; q < 2; ++q) {
-      const uint4 t = __ldg(reinterpret_cast<const uint4*>(p) + q);
-      const uint32_t w[4] = {t.x, t.y, t.z, t.w};
+    for (int q = 0; q < V; ++q) raw[q] = __ldg(reinterpret_cast<const uint4*>(p) + q);
+    return;
+  }
+  uint32_t w[4 * V];
+  if (sizeof(T) == 4) {
+    const uint32_t* s = reinterpret_cast<const uint32_t*>(p);
 #pragma unroll
-      for (int k = 0; k < 4; ++k) {
-        v[8 * q + 2 * k] = __uint_as_float(w[k] << 16);
-        v[8 * q + 2 * k + 1] = __uint_as_float(w[k] & 0xFFFF0000u);
+    for (int i = 0; i < 16; ++i) w[i] = i < n ? __ldg(s + i) : 0u;
+  } else {
+    const unsigned short* s = reinterpret_cast<const unsigned short*>(p);
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+      const uint32_t lo = 2 * i < n ? uint32_t(__ldg(s + 2 * i)) : 0u;
+      const uint32_t hi = 2 * i + 1 < n ? uint32_t(__ldg(s + 2 * i + 1)) : 0u;
+      w[i] = lo | (hi << 16);
+    }
+  }
+#pragma unroll
+  for (int q = 0; q < V; ++q) raw[q] = make_uint4(w[4 * q], w[4 * q + 1], w[4 * q + 2], w[4 * q + 3]);
+}
+
+// ------------------------------------------------------------------ transforms
+// Un-normalised 16-point FWHT of one vector (the 0.25 is folded into the
+// quantizer divisor).  Register pairs (v[i], v[i+8]) run stages h = 1, 2, 4
+// as f32x2; stage 8 pairs the two lanes of each register pair.
+__device__ __forceinline__ void fwht16_raw(float (&v)[16]) {
+  float2 p[8];
+#pragma unroll
+  for (int i = 0; i < 8; ++i) p[i] = make_float2(v[i], v[i + 8]);
+#pragma unroll
+  for (int h = 1; h < 8; h <<= 1) {
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+      if (!(i & h)) {
+        const float2 a = p[i], b = p[i + h];
+        p[i] = f2add(a, b);
+        p[i + h] = f2sub(a, b);
       }
     }
-  } else {
-    const unsigned short* q = reinterpret_cast<const unsigned short*>(p);
+  }
 #pragma unroll
-    for (int i = 0; i < 16; ++i) v[i] = i < n ? __uint_as_float(uint32_t(__ldg(q + i)) << 16) : 0.0f;
+  for (int i = 0; i < 8; ++i) {
+    v[i] = __fadd_rn(p[i].x, p[i].y);
+    v[i + 8] = __fsub_rn(p[i].x, p[i].y);
   }
 }
 
-// ------------------------------------------------------------------ transform
-// Un-normalised 16-point FWHT (the 0.25 is folded into the quantizer divisor).
-__device__ __forceinline__ void fwht16_raw(float (&v)[16]) {
+// Two independent columns at once: FWHT of a[.] (lane x) and b[.] (lane y).
+// Only outputs selected by KEEP (compile-time bitmap, 0 = all) are guaranteed;
+// the compiler removes butterflies that feed nothing.
+__device__ __forceinline__ void fwht16_pair(float2 (&p)[16]) {
 #pragma unroll
   for (int h = 1; h < 16; h <<= 1) {
 #pragma unroll
     for (int i = 0; i < 16; ++i) {
       if (!(i & h)) {
-        const float a = v[i], b = v[i + h];
-        v[i] = __fadd_rn(a, b);
-        v[i + h] = __fsub_rn(a, b);
+        const float2 a = p[i], b = p[i + h];
+        p[i] = f2add(a, b);
+        p[i + h] = f2sub(a, b);
       }
     }
   }
@@ -158,21 +267,25 @@ __device__ __forceinline__ Quant make_quant(const uint32_t* g, int bits) {
   return q;
 }
 
-__device__ __forceinline__ int quant_fast(float w, const Quant& q) {
-  float Q = __fmul_rn(w, q.r);
-  const float e = __fmaf_rn(-Q, q.d, w);
-  Q = __fmaf_rn(e, q.r, Q);
-  Q = fminf(fmaxf(Q, -q.lim), q.lim);
-  const int Fb = __float_as_int(__fadd_rd(Q, kMagic));
-  const int Cb = __float_as_int(__fadd_ru(Q, kMagic));
-  const int u = __float_as_int(w) & 0x7FF;
-  const int up = (Cb - (Fb & ~2047)) > u ? 1 : 0;
-  return (Fb >> 11) - kMagicShift + up;
+// Two codes (low byte of each returned word).
+__device__ __forceinline__ uint2 quant_fast2(float2 w, const Quant& q) {
+  float2 Q = f2mul(w, f2(q.r));
+  const float2 e = f2fma(Q, f2(-q.d), w);
+  Q = f2fma(e, f2(q.r), Q);
+  Q.x = fminf(fmaxf(Q.x, -q.lim), q.lim);
+  Q.y = fminf(fmaxf(Q.y, -q.lim), q.lim);
+  // -u as an exact float: (2^23) - (2^23 + u)
+  const float2 ub = make_float2(__uint_as_float((__float_as_uint(w.x) & 0x7FFu) | 0x4B000000u),
+                                __uint_as_float((__float_as_uint(w.y) & 0x7FFu) | 0x4B000000u));
+  const float2 nu = f2sub(f2(8388608.0f), ub);
+  const float2 z = f2add_rp(Q, nu);
+  const float2 c = f2fma_rp(z, f2(1.0f / 2048.0f), f2(kMagic));
+  return make_uint2(__float_as_uint(c.x), __float_as_uint(c.y));
 }
 
 // Literal restatement of quantize.py:140-145 (IEEE division), used when the
 // fast path's guard fails for the tensor.
-__device__ __forceinline__ int quant_exact(float w, const Quant& q) {
+__device__ __forceinline__ uint32_t quant_exact(float w, const Quant& q) {
   const float v = __fmul_rn(w, 0.25f);
   const float qq = __fdiv_rn(v, q.s);
   const float lo = floorf(qq);
@@ -180,17 +293,20 @@ __device__ __forceinline__ int quant_exact(float w, const Quant& q) {
   const float frac = __fmul_rn(__fsub_rn(qq, lo), 2048.0f);
   float c = __fadd_rn(lo, frac > draw ? 1.0f : 0.0f);
   c = fminf(fmaxf(c, -q.qmax), q.qmax);
-  return static_cast<int>(c);
+  return uint32_t(static_cast<int>(c));
 }
 
 template <bool FAST>
-__device__ __forceinline__ int quant(float w, const Quant& q) {
-  return FAST ? quant_fast(w, q) : quant_exact(w, q);
+__device__ __forceinline__ uint2 quant2(float2 w, const Quant& q) {
+  if (FAST) return quant_fast2(w, q);
+  return make_uint2(quant_exact(w.x, q), quant_exact(w.y, q));
 }
 
-__device__ __forceinline__ uint32_t pack4(int a, int b, int c, int d) {
-  return (uint32_t(a) & 0xFFu) | ((uint32_t(b) & 0xFFu) << 8) | ((uint32_t(c) & 0xFFu) << 16) |
-         (uint32_t(d) << 24);
+// low bytes of a, b, c, d -> one word
+__device__ __forceinline__ uint32_t pack_bytes(uint32_t a, uint32_t b, uint32_t c, uint32_t d) {
+  const uint32_t ab = __byte_perm(a, b, 0x0040);   // [a0, b0, a0, a0] -> use bytes 0,1
+  const uint32_t cd = __byte_perm(c, d, 0x0040);
+  return __byte_perm(ab, cd, 0x5410);
 }
 
 // ------------------------------------------------------------------ the tile kernel
@@ -199,7 +315,7 @@ struct TileArgs {
   int64_t segs, rows, cols, ld_src, seg_src;
   int64_t nblk;          // ceil(rows / 16)
   int64_t total_blocks;  // segs * nblk
-  int nb;                // projection blocks per CTA
+  int nb;                // projection blocks per CTA work item
   uint32_t bitmap;
   int rank;
   int bits_gx, bits_gw;
@@ -213,154 +329,239 @@ struct TileArgs {
   bool vec;
 };
 
-__device__ __forceinline__ int phys_col(int c) {
-  // 16-float blocks split into 4 chunks, chunk index xor-swizzled by (block >> 1) & 3
-  return (c & ~15) | ((((c >> 2) & 3) ^ ((c >> 5) & 3)) << 2) | (c & 3);
+// byte offset of 16-byte chunk q of 16-col block b inside one smem row
+// (xor swizzle so the 8 threads of a store phase hit 8 distinct bank groups)
+template <typename T>
+__device__ __forceinline__ int chunk_off(int b, int q) {
+  if (Traits<T>::kVec == 2) return b * 32 + ((q ^ ((b >> 2) & 1)) << 4);
+  return b * 64 + ((q ^ ((b >> 1) & 3)) << 4);
 }
 
-template <typename T, int MODE, bool GX, bool GW, bool FAST_GX, bool FAST_GW>
-__device__ __forceinline__ void tile_body(const TileArgs& a, const Quant& qx, const Quant& qw,
-                                          float* tile, uint8_t* cbuf, int cstride, Stat& sx,
-                                          Stat& sw) {
-  const T* src = static_cast<const T*>(a.src);
+// One step = one 16-row block of the tile.  Precomputed per step:
+struct StepPos {
+  const void* ptr;  // this thread's 16 phase-1 elements
+  int n;            // valid elements for this thread
+  int64_t row;      // global row index (seg*rows + row) for gx output, -1 if invalid
+  int64_t col0;     // tile's first column
+  int bl;           // block index inside the work item
+  bool last;        // last block of the work item (flush codes after it)
+  int nbl;          // blocks in this work item
+  int64_t gb0;      // first global block of the work item
+  bool valid;
+};
+
+template <int BM, int MODE, bool GX, bool GW, bool FAST_GX, bool FAST_GW, typename T>
+__device__ __forceinline__ void run_tile(const TileArgs& a, const Quant& qx, const Quant& qw,
+                                         uint8_t* smem, Stat& sx, Stat& sw) {
+  constexpr int V = Traits<T>::kVec;
+  constexpr int kRow = Traits<T>::kRowBytes;
+  uint8_t* tiles = smem;                           // [2][16][kRow]
+  uint8_t* cbuf = smem + (GW ? 2 * 16 * kRow : 0);  // [256][cstride]
+  const uint32_t bitmap = BM ? uint32_t(BM) : a.bitmap;
+  const int rank = BM ? __builtin_popcount(uint32_t(BM)) : a.rank;
+  const int cstride = a.nb * rank + 16;
+  const int tid = threadIdx.x;
+  const int pr = tid >> 4, pb = tid & 15;
   const int64_t ncol_tiles = (a.cols + kTileCols - 1) / kTileCols;
   const int64_t ngroups = (a.total_blocks + a.nb - 1) / a.nb;
   const int64_t items = ngroups * ncol_tiles;
-  const int tid = threadIdx.x;
-  const int pr = tid >> 4, pb = tid & 15;  // phase-1 role: row within block, 16-col block
-  for (int64_t item = blockIdx.x; item < items; item += gridDim.x) {
+  const T* src = static_cast<const T*>(a.src);
+
+  // iterator over (item, block) steps of this CTA
+  int64_t it_item = blockIdx.x;
+  int it_bl = 0;
+  auto pos_of = [&](int64_t item, int bl) {
+    StepPos p;
+    p.valid = item < items;
+    if (!p.valid) { p.ptr = src; p.n = 0; p.row = -1; p.col0 = 0; p.bl = 0; p.last = false; p.nbl = 0; p.gb0 = 0; return p; }
     const int64_t g = item / ncol_tiles;
     const int64_t ct = item - g * ncol_tiles;
-    const int64_t col0 = ct * kTileCols;
+    p.col0 = ct * kTileCols;
+    p.gb0 = g * a.nb;
+    p.nbl = int(a.total_blocks - p.gb0 < a.nb ? a.total_blocks - p.gb0 : a.nb);
+    p.bl = bl;
+    p.last = bl == p.nbl - 1;
+    const int64_t gb = p.gb0 + bl;
+    const int64_t s = gb / a.nblk;
+    const int64_t blk = gb - s * a.nblk;
+    const int64_t row = blk * 16 + pr;
+    const int64_t c = p.col0 + pb * 16;
+    const int64_t cv = a.cols - c;
+    p.n = row < a.rows ? int(cv < 0 ? 0 : (cv > 16 ? 16 : cv)) : 0;
+    p.row = (row < a.rows && cv > 0) ? s * a.rows + row : -1;
+    p.ptr = p.n ? static_cast<const void*>(src + s * a.seg_src + row * a.ld_src + c) : static_cast<const void*>(src);
+    return p;
+  };
+  auto advance = [&]() {
+    if (it_item >= items) return;
+    const int64_t g = it_item / ncol_tiles;
     const int64_t gb0 = g * a.nb;
     const int nbl = int(a.total_blocks - gb0 < a.nb ? a.total_blocks - gb0 : a.nb);
-    for (int bl = 0; bl < nbl; ++bl) {
-      const int64_t gb = gb0 + bl;
-      const int64_t s = gb / a.nblk;
-      const int64_t blk = gb - s * a.nblk;
-      // ---------------- phase 1: row pieces
-      {
-        const int64_t row = blk * 16 + pr;
-        const int64_t c = col0 + pb * 16;
-        const bool row_ok = row < a.rows;
-        const int64_t cvalid = a.cols - c;
-        const int n = row_ok ? int(cvalid < 0 ? 0 : (cvalid > 16 ? 16 : cvalid)) : 0;
-        float v[16];
-        load16(src + (n ? s * a.seg_src + row * a.ld_src + c : 0), n, a.vec, v);
-        if (GW) {
-          float* dstp = tile + pr * kTileCols;
+    if (++it_bl == nbl) { it_bl = 0; it_item += gridDim.x; }
+  };
+
+  StepPos p0 = pos_of(it_item, it_bl); advance();
+  StepPos p1 = pos_of(it_item, it_bl); advance();
+  uint4 r0[V], r1[V], r2[V];
+  load_raw<T>(static_cast<const T*>(p0.ptr), p0.n, a.vec, r0);
+  load_raw<T>(static_cast<const T*>(p1.ptr), p1.n, a.vec, r1);
+  int buf = 0;
+
+  auto step = [&](const StepPos& p, const uint4 (&raw)[V]) {
+    uint8_t* tile = tiles + buf * 16 * kRow;
+    // ---------------- phase 1: this thread's row piece
+    if (GW) {
 #pragma unroll
-          for (int q = 0; q < 4; ++q) {
-            const int pc = phys_col(pb * 16 + 4 * q);
-            *reinterpret_cast<float4*>(dstp + pc) =
-                make_float4(v[4 * q], v[4 * q + 1], v[4 * q + 2], v[4 * q + 3]);
-          }
-        }
-        if (GX && row_ok && cvalid > 0) {
-          fwht16_raw(v);
-          if (MODE == kStats) {
+      for (int q = 0; q < V; ++q)
+        *reinterpret_cast<uint4*>(tile + pr * kRow + chunk_off<T>(pb, q)) = raw[q];
+    }
+    if (GX && p.row >= 0) {
+      float v[16];
+      unpack16<T>(raw, v);
+      fwht16_raw(v);
+      if (MODE == kStats) {
 #pragma unroll
-            for (int i = 0; i < 16; ++i) sx.add(v[i]);
-          } else {
-            uint4 p;
-            p.x = pack4(quant<FAST_GX>(v[0], qx), quant<FAST_GX>(v[1], qx),
-                        quant<FAST_GX>(v[2], qx), quant<FAST_GX>(v[3], qx));
-            p.y = pack4(quant<FAST_GX>(v[4], qx), quant<FAST_GX>(v[5], qx),
-                        quant<FAST_GX>(v[6], qx), quant<FAST_GX>(v[7], qx));
-            p.z = pack4(quant<FAST_GX>(v[8], qx), quant<FAST_GX>(v[9], qx),
-                        quant<FAST_GX>(v[10], qx), quant<FAST_GX>(v[11], qx));
-            p.w = pack4(quant<FAST_GX>(v[12], qx), quant<FAST_GX>(v[13], qx),
-                        quant<FAST_GX>(v[14], qx), quant<FAST_GX>(v[15], qx));
-            *reinterpret_cast<uint4*>(a.dst_gx + (s * a.rows + row) * a.ld_gx + c) = p;
-          }
+        for (int i = 0; i < 16; ++i) sx.add(v[i]);
+      } else {
+        uint32_t c[16];
+#pragma unroll
+        for (int i = 0; i < 16; i += 2) {
+          const uint2 cc = quant2<FAST_GX>(make_float2(v[i], v[i + 1]), qx);
+          c[i] = cc.x; c[i + 1] = cc.y;
         }
+        uint4 out;
+        out.x = pack_bytes(c[0], c[1], c[2], c[3]);
+        out.y = pack_bytes(c[4], c[5], c[6], c[7]);
+        out.z = pack_bytes(c[8], c[9], c[10], c[11]);
+        out.w = pack_bytes(c[12], c[13], c[14], c[15]);
+        *reinterpret_cast<uint4*>(a.dst_gx + p.row * a.ld_gx + p.col0 + pb * 16) = out;
       }
-      if (!GW) continue;
-      __syncthreads();
-      // ---------------- phase 2: column pieces (projection along rows)
-      {
-        const int64_t c = col0 + tid;
-        if (c < a.cols) {
-          float v[16];
-          const int pc = phys_col(tid);
+    }
+    if (!GW) return;
+    __syncthreads();
+    // ---------------- phase 2: columns (2t, 2t+1) of the tile, projection along rows
+    if (tid < kTileCols / 2) {
+      const int c = 2 * tid;
+      const int64_t gc = p.col0 + c;
+      if (gc < a.cols) {
+        float2 pv[16];
+        const int b = c >> 4, e = c & 15;
+        if (sizeof(T) == 2) {
+          const int off = chunk_off<T>(b, e >> 3) + 2 * (e & 7);
 #pragma unroll
-          for (int i = 0; i < 16; ++i) v[i] = tile[i * kTileCols + pc];
-          fwht16_raw(v);
-          if (MODE == kStats) {
+          for (int i = 0; i < 16; ++i) {
+            const uint32_t w = *reinterpret_cast<const uint32_t*>(tile + i * kRow + off);
+            pv[i] = make_float2(bf_lo(w), bf_hi(w));
+          }
+        } else {
+          const int off = chunk_off<T>(b, e >> 2) + 4 * (e & 3);
 #pragma unroll
-            for (int i = 0; i < 16; ++i)
-              if ((a.bitmap >> i) & 1u) sw.add(v[i]);
-          } else {
-            uint8_t* out = cbuf + tid * cstride + bl * a.rank;
-            uint32_t w4[4] = {0, 0, 0, 0};
+          for (int i = 0; i < 16; ++i) pv[i] = *reinterpret_cast<const float2*>(tile + i * kRow + off);
+        }
+        fwht16_pair(pv);
+        const bool has2 = gc + 1 < a.cols;
+        if (MODE == kStats) {
 #pragma unroll
-            for (int i = 0; i < 16; ++i) {
-              if ((a.bitmap >> i) & 1u) {
-                const int j = __popc(a.bitmap & ((1u << i) - 1u));
-                const uint32_t code = uint32_t(quant<FAST_GW>(v[i], qw)) & 0xFFu;
-                // j is uniform across the grid; the switch keeps w4 in registers
-                switch (j >> 2) {
-                  case 0: w4[0] |= code << (8 * (j & 3)); break;
-                  case 1: w4[1] |= code << (8 * (j & 3)); break;
-                  case 2: w4[2] |= code << (8 * (j & 3)); break;
-                  default: w4[3] |= code << (8 * (j & 3)); break;
-                }
+          for (int i = 0; i < 16; ++i) {
+            if ((bitmap >> i) & 1u) {
+              sw.add(pv[i].x);
+              if (has2) sw.add(pv[i].y);
+            }
+          }
+        } else {
+          uint32_t wx[4] = {0, 0, 0, 0}, wy[4] = {0, 0, 0, 0};
+#pragma unroll
+          for (int i = 0; i < 16; ++i) {
+            if ((bitmap >> i) & 1u) {
+              const int j = BM ? __builtin_popcount(uint32_t(BM) & ((1u << i) - 1u))
+                               : __popc(bitmap & ((1u << i) - 1u));
+              const uint2 cc = quant2<FAST_GW>(pv[i], qw);
+              const uint32_t bx = (cc.x & 0xFFu) << (8 * (j & 3));
+              const uint32_t by = (cc.y & 0xFFu) << (8 * (j & 3));
+              switch (j >> 2) {
+                case 0: wx[0] |= bx; wy[0] |= by; break;
+                case 1: wx[1] |= bx; wy[1] |= by; break;
+                case 2: wx[2] |= bx; wy[2] |= by; break;
+                default: wx[3] |= bx; wy[3] |= by; break;
               }
             }
-            if (a.rank == 16) {
-              *reinterpret_cast<uint4*>(out) = make_uint4(w4[0], w4[1], w4[2], w4[3]);
-            } else if (a.rank == 8) {
-              *reinterpret_cast<uint2*>(out) = make_uint2(w4[0], w4[1]);
-            } else if (a.rank == 4) {
-              *reinterpret_cast<uint32_t*>(out) = w4[0];
-            } else {
-              for (int j = 0; j < a.rank; ++j) out[j] = uint8_t(w4[j >> 2] >> (8 * (j & 3)));
+          }
+          uint8_t* ox = cbuf + c * cstride + p.bl * rank;
+          uint8_t* oy = ox + cstride;
+          if (rank == 16) {
+            *reinterpret_cast<uint4*>(ox) = make_uint4(wx[0], wx[1], wx[2], wx[3]);
+            *reinterpret_cast<uint4*>(oy) = make_uint4(wy[0], wy[1], wy[2], wy[3]);
+          } else if (rank == 8) {
+            *reinterpret_cast<uint2*>(ox) = make_uint2(wx[0], wx[1]);
+            *reinterpret_cast<uint2*>(oy) = make_uint2(wy[0], wy[1]);
+          } else if (rank == 4) {
+            *reinterpret_cast<uint32_t*>(ox) = wx[0];
+            *reinterpret_cast<uint32_t*>(oy) = wy[0];
+          } else {
+            for (int j = 0; j < rank; ++j) {
+              ox[j] = uint8_t(wx[j >> 2] >> (8 * (j & 3)));
+              oy[j] = uint8_t(wy[j >> 2] >> (8 * (j & 3)));
             }
           }
         }
       }
-      __syncthreads();
     }
-    // ---------------- write the staged projection codes: (cols, K) K-major
-    if (GW && MODE == kQuant) {
-      const int run = nbl * a.rank;  // contiguous bytes per column
-      const int64_t k0 = gb0 * a.rank;
-      const int ncols = int(a.cols - col0 < kTileCols ? a.cols - col0 : kTileCols);
+    // ---------------- flush the work item's codes: (cols, K) K-major, >= 32B runs
+    if (MODE == kQuant && p.last) {
+      __syncthreads();
+      const int run = p.nbl * rank;
+      const int64_t k0 = p.gb0 * rank;
+      const int ncols = int(a.cols - p.col0 < kTileCols ? a.cols - p.col0 : kTileCols);
       if ((run & 15) == 0 && (k0 & 15) == 0) {
         const int chunks = run >> 4;
         for (int i = tid; i < ncols * chunks; i += kThreads) {
-          const int c = i / chunks, p = i - c * chunks;
-          *reinterpret_cast<uint4*>(a.dst_gw + (col0 + c) * a.ld_gw + k0 + 16 * p) =
-              *reinterpret_cast<const uint4*>(cbuf + c * cstride + 16 * p);
+          const int c = i / chunks, q = i - c * chunks;
+          *reinterpret_cast<uint4*>(a.dst_gw + (p.col0 + c) * a.ld_gw + k0 + 16 * q) =
+              *reinterpret_cast<const uint4*>(cbuf + c * cstride + 16 * q);
         }
       } else if ((run & 7) == 0 && (k0 & 7) == 0) {
         const int chunks = run >> 3;
         for (int i = tid; i < ncols * chunks; i += kThreads) {
-          const int c = i / chunks, p = i - c * chunks;
-          *reinterpret_cast<uint2*>(a.dst_gw + (col0 + c) * a.ld_gw + k0 + 8 * p) =
-              *reinterpret_cast<const uint2*>(cbuf + c * cstride + 8 * p);
+          const int c = i / chunks, q = i - c * chunks;
+          *reinterpret_cast<uint2*>(a.dst_gw + (p.col0 + c) * a.ld_gw + k0 + 8 * q) =
+              *reinterpret_cast<const uint2*>(cbuf + c * cstride + 8 * q);
         }
       } else {
         for (int i = tid; i < ncols * run; i += kThreads) {
-          const int c = i / run, p = i - c * run;
-          a.dst_gw[(col0 + c) * a.ld_gw + k0 + p] = int8_t(cbuf[c * cstride + p]);
+          const int c = i / run, q = i - c * run;
+          a.dst_gw[(p.col0 + c) * a.ld_gw + k0 + q] = int8_t(cbuf[c * cstride + q]);
         }
       }
       __syncthreads();
     }
+    buf ^= 1;
+  };
+
+  // software pipeline: loads run two steps ahead of the math
+  while (p0.valid) {
+    StepPos p2 = pos_of(it_item, it_bl); advance();
+    load_raw<T>(static_cast<const T*>(p2.ptr), p2.n, a.vec, r2);
+    step(p0, r0);
+    if (!p1.valid) break;
+    StepPos p3 = pos_of(it_item, it_bl); advance();
+    load_raw<T>(static_cast<const T*>(p3.ptr), p3.n, a.vec, r0);
+    step(p1, r1);
+    if (!p2.valid) break;
+    StepPos p4 = pos_of(it_item, it_bl); advance();
+    load_raw<T>(static_cast<const T*>(p4.ptr), p4.n, a.vec, r1);
+    step(p2, r2);
+    p0 = p3;
+    p1 = p4;
   }
 }
 
-template <typename T, int MODE, bool GX, bool GW>
+template <typename T, int MODE, bool GX, bool GW, int BM>
 __global__ void __launch_bounds__(kThreads) tile_kernel(TileArgs a) {
   extern __shared__ __align__(16) uint8_t smem[];
-  float* tile = reinterpret_cast<float*>(smem);  // 16 x 256 fp32
-  uint8_t* cbuf = smem + (GW ? 16 * kTileCols * sizeof(float) : 0);
-  const int cstride = a.nb * a.rank + 16;
   Stat sx, sw;
   if (MODE == kStats) {
     Quant dummy{};
-    tile_body<T, MODE, GX, GW, true, true>(a, dummy, dummy, tile, cbuf, cstride, sx, sw);
+    run_tile<BM, MODE, GX, GW, true, true, T>(a, dummy, dummy, smem, sx, sw);
     if (GX) reduce_stat_to_global(sx, a.stats);
     if (GW) reduce_stat_to_global(sw, a.stats + 2);
     return;
@@ -374,52 +575,64 @@ __global__ void __launch_bounds__(kThreads) tile_kernel(TileArgs a) {
   }
   const bool fx = !GX || qx.fast, fw = !GW || qw.fast;  // uniform across the grid
   if (fx && fw)
-    tile_body<T, MODE, GX, GW, true, true>(a, qx, qw, tile, cbuf, cstride, sx, sw);
+    run_tile<BM, MODE, GX, GW, true, true, T>(a, qx, qw, smem, sx, sw);
   else if (fx)
-    tile_body<T, MODE, GX, GW, true, false>(a, qx, qw, tile, cbuf, cstride, sx, sw);
+    run_tile<BM, MODE, GX, GW, true, false, T>(a, qx, qw, smem, sx, sw);
   else if (fw)
-    tile_body<T, MODE, GX, GW, false, true>(a, qx, qw, tile, cbuf, cstride, sx, sw);
+    run_tile<BM, MODE, GX, GW, false, true, T>(a, qx, qw, smem, sx, sw);
   else
-    tile_body<T, MODE, GX, GW, false, false>(a, qx, qw, tile, cbuf, cstride, sx, sw);
+    run_tile<BM, MODE, GX, GW, false, false, T>(a, qx, qw, smem, sx, sw);
 }
 
-template <typename T, int MODE, bool GX, bool GW>
+template <typename T, int MODE, bool GX, bool GW, int BM>
 void launch_tile(const TileArgs& a, cudaStream_t stream) {
   const int64_t ncol_tiles = (a.cols + kTileCols - 1) / kTileCols;
   const int64_t ngroups = (a.total_blocks + a.nb - 1) / a.nb;
   const int64_t items = ngroups * ncol_tiles;
-  const size_t smem =
-      GW ? 16 * kTileCols * sizeof(float) + size_t(kTileCols) * (a.nb * a.rank + 16) : 0;
+  const int rank = GW ? a.rank : 0;
+  const size_t smem = GW ? size_t(2 * 16 * Traits<T>::kRowBytes) + size_t(kTileCols) * (a.nb * rank + 16) : 0;
   static bool attr = false;
   if (!attr) {
-    cudaFuncSetAttribute(tile_kernel<T, MODE, GX, GW>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         64 * 1024);
+    cudaFuncSetAttribute(tile_kernel<T, MODE, GX, GW, BM>,
+                         cudaFuncAttributeMaxDynamicSharedMemorySize, 96 * 1024);
     attr = true;
   }
-  const int64_t cap = int64_t(num_sms()) * 6;
+  const int64_t cap = int64_t(num_sms()) * 4;
   const int grid = int(items < 1 ? 1 : (items > cap ? cap : items));
-  tile_kernel<T, MODE, GX, GW><<<grid, kThreads, smem, stream>>>(a);
+  tile_kernel<T, MODE, GX, GW, BM><<<grid, kThreads, smem, stream>>>(a);
+}
+
+template <typename T, int MODE, bool GX, bool GW>
+void launch_bm(const TileArgs& a, cudaStream_t st) {
+  if (!GW) return launch_tile<T, MODE, GX, GW, 0>(a, st);
+  switch (a.bitmap) {
+    case 0x5555: return launch_tile<T, MODE, GX, GW, 0x5555>(a, st);  // rank 8 (default plan)
+    case 0x1111: return launch_tile<T, MODE, GX, GW, 0x1111>(a, st);  // rank 4
+    case 0x0101: return launch_tile<T, MODE, GX, GW, 0x0101>(a, st);  // rank 2
+    case 0xFFFF: return launch_tile<T, MODE, GX, GW, 0xFFFF>(a, st);  // full (H.W, rank 16)
+    default: return launch_tile<T, MODE, GX, GW, 0>(a, st);           // calibrated bases
+  }
 }
 
 template <typename T>
-void launch_tile_modes(const TileArgs& a, int mode, bool gx, bool gw, cudaStream_t st) {
+void launch_modes(const TileArgs& a, int mode, bool gx, bool gw, cudaStream_t st) {
   if (mode == kStats) {
-    if (gx && gw) launch_tile<T, kStats, true, true>(a, st);
-    else if (gx) launch_tile<T, kStats, true, false>(a, st);
-    else launch_tile<T, kStats, false, true>(a, st);
+    if (gx && gw) launch_bm<T, kStats, true, true>(a, st);
+    else if (gx) launch_bm<T, kStats, true, false>(a, st);
+    else launch_bm<T, kStats, false, true>(a, st);
   } else {
-    if (gx && gw) launch_tile<T, kQuant, true, true>(a, st);
-    else if (gx) launch_tile<T, kQuant, true, false>(a, st);
-    else launch_tile<T, kQuant, false, true>(a, st);
+    if (gx && gw) launch_bm<T, kQuant, true, true>(a, st);
+    else if (gx) launch_bm<T, kQuant, true, false>(a, st);
+    else launch_bm<T, kQuant, false, true>(a, st);
   }
 }
 
-// Blocks per CTA: >= 32-byte output runs per column when the problem is large,
-// while keeping >= ~4 CTAs per SM of work.
+// Blocks per work item: >= 32-byte output runs per column when the problem is
+// large, while keeping >= ~3 work items per SM.
 int choose_nb(int64_t total_blocks, int64_t cols, int rank) {
   int nb = rank >= 8 ? 4 : (rank >= 4 ? 8 : 16);
   const int64_t ncol_tiles = (cols + kTileCols - 1) / kTileCols;
-  while (nb > 1 && ((total_blocks + nb - 1) / nb) * ncol_tiles < int64_t(num_sms()) * 4) nb >>= 1;
+  while (nb > 1 && ((total_blocks + nb - 1) / nb) * ncol_tiles < int64_t(num_sms()) * 3) nb >>= 1;
   return nb;
 }
 
@@ -451,9 +664,9 @@ void launch_transform(const TransformArgs& t, int mode, cudaStream_t stream) {
           ((t.seg_src * esz) % 16 == 0);
   a.nb = t.do_gw ? choose_nb(a.total_blocks, t.cols, a.rank) : 4;
   if (t.dtype == kBF16)
-    launch_tile_modes<__nv_bfloat16>(a, mode, t.do_gx, t.do_gw, stream);
+    launch_modes<__nv_bfloat16>(a, mode, t.do_gx, t.do_gw, stream);
   else
-    launch_tile_modes<float>(a, mode, t.do_gx, t.do_gw, stream);
+    launch_modes<float>(a, mode, t.do_gx, t.do_gw, stream);
 }
 
 }  // namespace hlq

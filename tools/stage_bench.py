@@ -19,9 +19,17 @@ from paper_2406_15102_b200 import ops  # noqa: E402
 from paper_2406_15102_b200.backprop import _proj_view  # noqa: E402
 
 
-def timeit(fn, iters=20, warmup=5, flush=None):
+def timeit(fn, iters=20, warmup=3, flush=None):
+    """Median GPU time (us) of fn, captured in a CUDA graph so host overhead
+    (ctypes, allocator) is excluded; L2 flushed before every replay."""
     for _ in range(warmup):
         fn()
+    torch.cuda.synchronize()
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g):
+        fn()
+    for _ in range(2):
+        g.replay()
     torch.cuda.synchronize()
     ts = []
     for _ in range(iters):
@@ -30,7 +38,7 @@ def timeit(fn, iters=20, warmup=5, flush=None):
         s = torch.cuda.Event(enable_timing=True)
         e = torch.cuda.Event(enable_timing=True)
         s.record()
-        fn()
+        g.replay()
         e.record()
         e.synchronize()
         ts.append(s.elapsed_time(e) * 1e3)
@@ -75,7 +83,14 @@ def main():
                                                 exact=False, out_dtype=dt), flush=flush)
     res["gemm_dx_exact_f32"] = timeit(lambda: ops.gemm_i8(cgx, cw, T, I, ops.pad16(O), 4, 4, sgx, sw,
                                                           1.0, exact=True), flush=flush)
-    res["hlq_bwd_total"] = res["proj_gy"] + res["ht_gy"] + res["ht_w"] + res["gemm_dw"] + res["gemm_dx"]
+    if axis == 1 or L == 1:
+        res["dual_gy"] = timeit(lambda: ops.quant_dual(gy, segs, rows, cols, bitmap, 4, 8, ld, sgo),
+                                flush=flush)
+        res["dual_gy_GBps"] = (T * O * (2 if dt == torch.bfloat16 else 4) + T * ops.pad16(O) + O * kg) \
+            / res["dual_gy"] / 1e3
+        res["hlq_bwd_total"] = res["dual_gy"] + res["ht_w"] + res["gemm_dw"] + res["gemm_dx"]
+    else:
+        res["hlq_bwd_total"] = res["proj_gy"] + res["ht_gy"] + res["ht_w"] + res["gemm_dw"] + res["gemm_dx"]
     # dense bf16 backward of the same layer (cuBLAS): dX = gy W, dW = gy^T x
     xb, wb, gb = x.to(torch.bfloat16).reshape(T, I), w.to(torch.bfloat16), gy.to(torch.bfloat16).reshape(T, O)
     res["dense_dx"] = timeit(lambda: gb @ wb, flush=flush)
