@@ -1,0 +1,433 @@
+"""Benchmark for the HLQ backward path on B200 (driver contract in the task spec).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+                    [--workload vit_train|layers]
+
+Default workload (BASELINE.json metric, configs[3]): one ViT-B/16 fine-tune step
+on synthetic 224 px images, batch 128 PER GPU (weak scaling), bf16 autocast,
+every nn.Linear (48 block Linears + head) replaced by HLQLinear -- forward =
+stock F.linear + ACBP compression (sm_100a), backward = the HLQ kernels
+(fused Hadamard/projection quantizers + tcgen05 int8 GEMMs).  N > 1: one
+process per GPU, DDP all-reduce of the fp32 dW buckets over NCCL.
+
+The JSON line reports img/s for the whole job (value), the same step end to
+end with images in pinned host memory (e2e), the dominant HLQ kernel against
+its roofline (CUDA events on the launching stream), per-layer HLQ backward time
+vs the dense bf16 backward (the first half of the metric), a dense-bf16
+training step for context, and the CPU oracle's rate on a bounded sample.
+
+--impl reference times the reference's CPU algorithm for the path (the numpy
+restatement in oracle/, the reference itself cannot travel to the GPU box) on
+this host's cores, on the same workload and unit.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "HLQ backward time/layer vs dense bf16 bwd; ViT-B/16 train img/s at 1/2/4/8 GPU"
+IMG, TOKENS, BATCH = 224, 197, 128
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--workload", default="vit_train", choices=["vit_train"])
+    ap.add_argument("--batch", type=int, default=BATCH, help="images per GPU")
+    ap.add_argument("--no-extras", action="store_true", help="skip dense/layer/cpu side measurements")
+    return ap.parse_args()
+
+
+# ---------------------------------------------------------------------------
+# CPU side: the reference algorithm (oracle port) on a bounded sample
+# ---------------------------------------------------------------------------
+
+def vit_layer_list():
+    # (name, I, O, count per image-forward) for ViT-B/16; tokens 197 except the head (L = 1)
+    return [("qkv", 768, 2304, 12), ("proj", 768, 768, 12), ("fc1", 768, 3072, 12),
+            ("fc2", 3072, 768, 12)]
+
+
+def cpu_path_seconds_per_image(images: int = 1, seed: int = 0):
+    """Seconds of host time for the reference algorithm's HLQ path of one
+    image: ACBP compress + hlq_backward for every Linear of ViT-B/16 (48 block
+    layers at L = 197; the 1000-way head needs >= 16 images for its batch-axis
+    projection and is < 0.1 % of the work, so it is left out of the sample).
+    Sample: `images` images through one layer of each of the 4 block shapes,
+    times 12 blocks."""
+    import numpy as np
+    from oracle import hlq_oracle as orc
+    total = 0.0
+    for name, I, O, count in vit_layer_list():
+        x, w, gy = orc.make_inputs(seed, (images, TOKENS, I), (O, I), (images, TOKENS, O))
+        t0 = time.perf_counter()
+        orc.hlq_backward(x, w, gy, rank=8)
+        total += (time.perf_counter() - t0) * count
+    return total / images
+
+
+def cpu_threads():
+    try:
+        import numpy as np  # noqa: F401
+        from threadpoolctl import threadpool_info
+        n = max((d.get("num_threads", 1) for d in threadpool_info()), default=1)
+        return int(n)
+    except Exception:  # noqa: BLE001
+        return os.cpu_count() or 1
+
+
+def run_reference(args):
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return 0
+    for _ in range(args.warmup):
+        cpu_path_seconds_per_image(1)
+    ts = [cpu_path_seconds_per_image(1, seed=i) for i in range(args.steps)]
+    sec = sum(ts) / len(ts)
+    value = 1.0 / sec
+    line = {
+        "impl": "reference", "metric": METRIC, "value": round(value, 4), "unit": "img/s",
+        "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": round(sec * 1e3, 1), "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "fp32", "data": "synthetic",
+        "config": workload_config(args, args.gpus),
+        "cpu_baseline": {"value": round(value, 4), "unit": "img/s", "cores": cpu_threads(),
+                         "kind": "port",
+                         "sample": "1 image per step: ACBP compress + hlq_backward of one layer of each "
+                                   "ViT-B/16 block shape (qkv, proj, fc1, fc2) at L=197, x12 blocks; "
+                                   "numpy restatement of the reference (oracle/hlq_oracle.py), "
+                                   "BLAS threads as listed, elementwise stages single-threaded"},
+        "e2e": {"value": round(value, 4), "unit": "img/s", "h2d_bytes_per_step": 0,
+                "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+def workload_config(args, world):
+    return {"workload": "vit_b16_finetune_step (BASELINE configs[3])", "model": "ViT-B/16",
+            "global_batch": args.batch * world, "per_gpu_batch": args.batch, "seq_len": TOKENS,
+            "image": IMG, "parallelism": f"dp{world}", "amp": "bf16",
+            "hlq": "gx int4 HQ (block 16), gw int8 HLA rank 8, ACBP int8; 49 Linear layers",
+            "l2": "per-step working set (activations, codes) >> 126 MB L2; no flush needed"}
+
+
+# ---------------------------------------------------------------------------
+# GPU side
+# ---------------------------------------------------------------------------
+
+class ClockSampler:
+    def __init__(self, gpu_index: int):
+        self.gpu = gpu_index
+        self.samples = []
+        self._stop = threading.Event()
+        self._t = None
+
+    def __enter__(self):
+        def loop():
+            q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
+                 "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+                 "clocks_event_reasons.sw_power_cap")
+            while not self._stop.is_set():
+                try:
+                    out = subprocess.run(["nvidia-smi", "-i", str(self.gpu), f"--query-gpu={q}",
+                                          "--format=csv,noheader,nounits"], capture_output=True,
+                                         text=True, timeout=5).stdout.strip()
+                    if out:
+                        self.samples.append([v.strip() for v in out.split(",")])
+                except Exception:  # noqa: BLE001
+                    pass
+                self._stop.wait(0.2)
+        self._t = threading.Thread(target=loop, daemon=True)
+        self._t.start()
+        return self
+
+    def __exit__(self, *exc):
+        self._stop.set()
+        if self._t:
+            self._t.join(timeout=10)
+        return False
+
+    def summary(self):
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        sm = sorted(float(s[0]) for s in self.samples if s[0].replace(".", "").isdigit())
+        mx = max((float(s[1]) for s in self.samples if s[1].replace(".", "").isdigit()), default=None)
+        reasons = sorted({names[i] for s in self.samples for i in range(4)
+                          if len(s) > 2 + i and s[2 + i].lower() == "active"})
+        return {"sm_mhz": sm[len(sm) // 2] if sm else None, "sm_max_mhz": mx, "reasons": reasons,
+                "samples": len(self.samples)}
+
+
+def measured_peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        d = json.load(open(p))
+        return {"hbm_gbs": d.get("hbm_gbs", 6650.0), "bf16_tflops": d.get("bf16_tflops", 1590.0),
+                "bf16_tflops_sustained": d.get("bf16_tflops_sustained", 1400.0), "source": "measured"}
+    return {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0, "bf16_tflops_sustained": 1400.0,
+            "source": "fallback (B200_PROFILING.md)"}
+
+
+def int8_peak_tops(torch):
+    """cuBLASLt int8 GEMM at 8192^3, best of 10 (the int8 roofline denominator;
+    MEASURED_PEAKS.json carries no int8 figure)."""
+    a = torch.randint(-127, 127, (8192, 8192), dtype=torch.int8, device="cuda")
+    b = torch.randint(-127, 127, (8192, 8192), dtype=torch.int8, device="cuda").t()
+    for _ in range(3):
+        torch._int_mm(a, b)
+    best = 1e9
+    for _ in range(10):
+        s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        s.record()
+        torch._int_mm(a, b)
+        e.record()
+        e.synchronize()
+        best = min(best, s.elapsed_time(e))
+    del a, b
+    return 2 * 8192 ** 3 / (best * 1e-3) / 1e12
+
+
+def make_model(torch, hlq: bool):
+    from paper_2406_15102_b200.vit import vit_b16
+    from paper_2406_15102_b200.layers import convert_linears
+    torch.manual_seed(0)
+    m = vit_b16().cuda()
+    if hlq:
+        convert_linears(m)
+    return m
+
+
+def train_steps(torch, model, opt, x, y, n, host=None):
+    F = torch.nn.functional
+    loss = None
+    for _ in range(n):
+        if host is not None:
+            x.copy_(host[0], non_blocking=True)
+            y.copy_(host[1], non_blocking=True)
+        with torch.autocast("cuda", dtype=torch.bfloat16):
+            logits = model(x)
+        loss = F.cross_entropy(logits.float(), y)
+        loss.backward()
+        opt.step()
+        opt.zero_grad(set_to_none=True)
+        if host is not None:
+            loss.item()  # D2H of the step's result
+    return loss
+
+
+def timed(torch, dist, fn):
+    if dist is not None:
+        dist.barrier()
+    torch.cuda.synchronize()
+    s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    s.record()
+    fn()
+    e.record()
+    torch.cuda.synchronize()
+    ms = s.elapsed_time(e)
+    if dist is not None:
+        t = torch.tensor([ms], device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+        dist.barrier()
+    return ms
+
+
+def layer_bwd_table(torch):
+    """Per-layer backward (dX + dW) at the ViT-B/16 shapes, batch 128: the HLQ
+    kernels exactly as HLQLinearFunction.backward runs them vs the dense bf16
+    backward (two cuBLAS GEMMs).  CUDA-graph replays, L2 flushed before each."""
+    from paper_2406_15102_b200 import ops
+    flush = torch.empty(64 * 1024 * 1024, device="cuda")
+
+    def graph_us(fn, reps=10):
+        fn()
+        torch.cuda.synchronize()
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g):
+            fn()
+        ts = []
+        for _ in range(reps):
+            flush.zero_()
+            s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            s.record()
+            g.replay()
+            e.record()
+            e.synchronize()
+            ts.append(s.elapsed_time(e) * 1e3)
+        return sorted(ts)[len(ts) // 2]
+
+    out = {}
+    for name, B, L, I, O in [("qkv", BATCH, TOKENS, 768, 2304), ("proj", BATCH, TOKENS, 768, 768),
+                             ("fc1", BATCH, TOKENS, 768, 3072), ("fc2", BATCH, TOKENS, 3072, 768)]:
+        torch.manual_seed(1)
+        x = torch.randn(B, L, I, device="cuda", dtype=torch.bfloat16)
+        w = torch.randn(O, I, device="cuda") * (2.0 / I) ** 0.5
+        gy = (torch.randn(B, L, O, device="cuda") * 1e-3).to(torch.bfloat16)
+        xp, k, sx, _ = ops.quant_proj_rows(x, B, L, I, 0x5555, 8, I, L * I)
+
+        def hlq_bwd():
+            cgx, sgx, cg, kg, sg, _ = ops.quant_dual(gy, B, L, O, 0x5555, 4, 8, O, L * O)
+            cw, _, sw, _ = ops.quant_proj_rows(w, 1, O, I, 0xFFFF, 4)
+            ops.gemm_i8(cg, xp, O, I, k, 8, 8, sg, sx, 1.0, exact=False)
+            ops.gemm_i8(cgx, cw, B * L, I, ops.pad16(O), 4, 4, sgx, sw, 1.0, exact=False,
+                        out_dtype=torch.bfloat16)
+
+        wb, xb, gb = w.to(torch.bfloat16), x.reshape(-1, I), gy.reshape(-1, O)
+
+        def dense_bwd():
+            gb @ wb
+            gb.t() @ xb
+
+        h, d = graph_us(hlq_bwd), graph_us(dense_bwd)
+        out[name] = {"hlq_us": round(h, 1), "dense_bf16_us": round(d, 1), "speedup": round(d / h, 3)}
+    tot_h = sum(v["hlq_us"] for v in out.values())
+    tot_d = sum(v["dense_bf16_us"] for v in out.values())
+    out["block_total"] = {"hlq_us": round(tot_h, 1), "dense_bf16_us": round(tot_d, 1),
+                          "speedup": round(tot_d / tot_h, 3)}
+    del flush
+    return out
+
+
+def run_ours(args):
+    import torch
+    import torch.distributed as dist_mod
+    from paper_2406_15102_b200 import _lib, ops
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    dist = None
+    if world > 1:
+        dist_mod.init_process_group("nccl", device_id=torch.device("cuda", local))
+        dist = dist_mod
+    if _lib.load().hlq_device_ok() != 1:
+        raise RuntimeError("libhlq_b200 needs an sm_100 device")
+    torch.backends.cuda.matmul.allow_tf32 = True
+    torch.backends.cudnn.allow_tf32 = True
+
+    B = args.batch
+    model = make_model(torch, hlq=True)
+    if dist is not None:
+        model = torch.nn.parallel.DistributedDataParallel(model, device_ids=[local],
+                                                          gradient_as_bucket_view=True)
+    opt = torch.optim.SGD(model.parameters(), lr=1e-3, momentum=0.9, foreach=True)
+    g = torch.Generator(device="cuda").manual_seed(1234 + rank)
+    x = torch.randn(B, 3, IMG, IMG, device="cuda", generator=g)
+    y = torch.randint(0, 1000, (B,), device="cuda", generator=g)
+
+    train_steps(torch, model, opt, x, y, args.warmup)
+    launches0 = ops.LAUNCHES[0]
+    with ClockSampler(local) as clk, ops.trace() as tr:
+        ms = timed(torch, dist, lambda: train_steps(torch, model, opt, x, y, args.steps))
+    launches = ops.LAUNCHES[0] - launches0
+    kern = tr.summary()
+    ms_step = ms / args.steps
+    value = world * B * args.steps / (ms * 1e-3)
+
+    # end to end: images + labels from pinned host memory every step, loss read back
+    hx = x.cpu().pin_memory()
+    hy = y.cpu().pin_memory()
+    e2e_steps = max(3, min(args.steps, 10))
+    ms_e2e = timed(torch, dist, lambda: train_steps(torch, model, opt, x, y, e2e_steps, host=(hx, hy)))
+    e2e_value = world * B * e2e_steps / (ms_e2e * 1e-3)
+
+    peaks = measured_peaks()
+    line = None
+    if rank == 0:
+        int8_peak = int8_peak_tops(torch)
+        # dominant libhlq kernel class over the timed region
+        tr_us = kern.get("transform", {}).get("us", 0.0)
+        gm_us = kern.get("gemm", {}).get("us", 0.0)
+        if tr_us >= gm_us:
+            d = kern["transform"]
+            ach = d["bytes"] / (d["us"] * 1e-6) / 1e9
+            roof = {"kernel": "fused Hadamard/projection + amax + quantize (tile_kernel, 2 passes)",
+                    "bound": "hbm", "achieved": round(ach, 1), "peak": peaks["hbm_gbs"],
+                    "unit": "GB/s", "frac": round(ach / peaks["hbm_gbs"], 4),
+                    "traffic": None, "peak_source": peaks["source"],
+                    "per_launch_us": round(d["us"] / d["calls"], 2), "calls": d["calls"],
+                    "share_of_step": round(d["us"] / (ms * 1e3), 4)}
+        else:
+            d = kern["gemm"]
+            ach = d["ops"] / (d["us"] * 1e-6) / 1e12
+            roof = {"kernel": "tcgen05 kind::i8 GEMM + dequant epilogue (gemm_i8_kernel)",
+                    "bound": "tensor", "achieved": round(ach, 1), "peak": round(int8_peak, 1),
+                    "unit": "TFLOP/s", "frac": round(ach / int8_peak, 4), "traffic": None,
+                    "peak_source": "int8 ops/s of cuBLASLt torch._int_mm 8192^3, measured in this run",
+                    "per_launch_us": round(d["us"] / d["calls"], 2), "calls": d["calls"],
+                    "share_of_step": round(d["us"] / (ms * 1e3), 4)}
+        roof["kernels"] = {k: {"us_per_step": round(v["us"] / args.steps, 1), "calls": v["calls"]}
+                           for k, v in kern.items()}
+        line = {
+            "metric": METRIC, "value": round(value, 2), "unit": "img/s", "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms_step, 3),
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+            "dtype": "int8 (HLQ backward codes; bf16 autocast forward)", "data": "synthetic",
+            "config": workload_config(args, world),
+            "e2e": {"value": round(e2e_value, 2), "unit": "img/s",
+                    "h2d_bytes_per_step": int(hx.numel() * hx.element_size() + hy.numel() * hy.element_size()),
+                    "d2h_bytes_per_step": 4},
+            "roofline": roof,
+            "gpu_launches": int(launches),
+            "int8_peak_tops_measured": round(int8_peak, 1),
+        }
+    if not args.no_extras:
+        # dense bf16 training step of the same model for context (same GPUs, same batch)
+        del model, opt
+        torch.cuda.empty_cache()
+        dmodel = make_model(torch, hlq=False)
+        if dist is not None:
+            dmodel = torch.nn.parallel.DistributedDataParallel(dmodel, device_ids=[local],
+                                                               gradient_as_bucket_view=True)
+        dopt = torch.optim.SGD(dmodel.parameters(), lr=1e-3, momentum=0.9, foreach=True)
+        train_steps(torch, dmodel, dopt, x, y, args.warmup)
+        dsteps = max(3, min(args.steps, 10))
+        dms = timed(torch, dist, lambda: train_steps(torch, dmodel, dopt, x, y, dsteps))
+        if rank == 0:
+            line["dense_bf16_train"] = {"value": round(world * B * dsteps / (dms * 1e-3), 2),
+                                        "unit": "img/s", "ms_per_step": round(dms / dsteps, 3)}
+            line["hlq_vs_dense_train_speedup"] = round(line["value"] / line["dense_bf16_train"]["value"], 4)
+        del dmodel, dopt
+        torch.cuda.empty_cache()
+        if rank == 0:
+            line["layer_bwd"] = layer_bwd_table(torch)
+            if world == 1:
+                t0 = time.perf_counter()
+                sec = cpu_path_seconds_per_image(1)
+                line["cpu_baseline"] = {
+                    "value": round(1.0 / sec, 4), "unit": "img/s", "cores": cpu_threads(),
+                    "kind": "port",
+                    "sample": "1 image: ACBP compress + hlq_backward of one layer of each ViT-B/16 "
+                              "block shape at L=197 (x12 blocks), numpy restatement oracle/hlq_oracle.py",
+                    "wall_s": round(time.perf_counter() - t0, 2)}
+    if rank == 0:
+        line["clocks"] = clk.summary()
+        print(json.dumps(line), flush=True)
+    if dist is not None:
+        dist.barrier()
+        dist.destroy_process_group()
+    return 0
+
+
+def main():
+    args = parse()
+    if args.impl == "reference":
+        return run_reference(args)
+    return run_ours(args)
+
+
+if __name__ == "__main__":
+    sys.exit(main())

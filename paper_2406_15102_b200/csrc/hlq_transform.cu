@@ -342,12 +342,39 @@ struct StepPos {
   const void* ptr;  // this thread's 16 phase-1 elements
   int n;            // valid elements for this thread
   int64_t row;      // global row index (seg*rows + row) for gx output, -1 if invalid
-  int64_t col0;     // tile's first column
+  int col0;         // tile's first column
   int bl;           // block index inside the work item
   bool last;        // last block of the work item (flush codes after it)
   int nbl;          // blocks in this work item
-  int64_t gb0;      // first global block of the work item
+  int gb0;          // first global block of the work item
   bool valid;
+};
+
+// Walks this CTA's (work item, block) steps with 32-bit counters; the only
+// divisions happen once per work item.
+struct StepIter {
+  int item, items, ncol_tiles, nb, total_blocks, nblk;
+  int bl, nbl, gb0, col0, s, blk;
+  __device__ __forceinline__ void start_item() {
+    if (item >= items) return;
+    const int g = item / ncol_tiles;
+    col0 = (item - g * ncol_tiles) * kTileCols;
+    gb0 = g * nb;
+    nbl = min(nb, total_blocks - gb0);
+    bl = 0;
+    s = gb0 / nblk;
+    blk = gb0 - s * nblk;
+  }
+  __device__ __forceinline__ void advance() {
+    if (item >= items) return;
+    if (++bl == nbl) {
+      item += gridDim.x;
+      start_item();
+    } else if (++blk == nblk) {
+      blk = 0;
+      ++s;
+    }
+  }
 };
 
 template <int BM, int MODE, bool GX, bool GW, bool FAST_GX, bool FAST_GW, typename T>
@@ -362,46 +389,41 @@ __device__ __forceinline__ void run_tile(const TileArgs& a, const Quant& qx, con
   const int cstride = a.nb * rank + 16;
   const int tid = threadIdx.x;
   const int pr = tid >> 4, pb = tid & 15;
-  const int64_t ncol_tiles = (a.cols + kTileCols - 1) / kTileCols;
-  const int64_t ngroups = (a.total_blocks + a.nb - 1) / a.nb;
-  const int64_t items = ngroups * ncol_tiles;
   const T* src = static_cast<const T*>(a.src);
+  const int rows = int(a.rows), cols = int(a.cols);
 
   // iterator over (item, block) steps of this CTA
-  int64_t it_item = blockIdx.x;
-  int it_bl = 0;
-  auto pos_of = [&](int64_t item, int bl) {
+  StepIter it;
+  it.ncol_tiles = (cols + kTileCols - 1) / kTileCols;
+  it.nb = a.nb;
+  it.total_blocks = int(a.total_blocks);
+  it.nblk = int(a.nblk);
+  it.items = ((it.total_blocks + a.nb - 1) / a.nb) * it.ncol_tiles;
+  it.item = blockIdx.x;
+  it.start_item();
+  auto pos_of = [&]() {
     StepPos p;
-    p.valid = item < items;
+    p.valid = it.item < it.items;
     if (!p.valid) { p.ptr = src; p.n = 0; p.row = -1; p.col0 = 0; p.bl = 0; p.last = false; p.nbl = 0; p.gb0 = 0; return p; }
-    const int64_t g = item / ncol_tiles;
-    const int64_t ct = item - g * ncol_tiles;
-    p.col0 = ct * kTileCols;
-    p.gb0 = g * a.nb;
-    p.nbl = int(a.total_blocks - p.gb0 < a.nb ? a.total_blocks - p.gb0 : a.nb);
-    p.bl = bl;
-    p.last = bl == p.nbl - 1;
-    const int64_t gb = p.gb0 + bl;
-    const int64_t s = gb / a.nblk;
-    const int64_t blk = gb - s * a.nblk;
-    const int64_t row = blk * 16 + pr;
-    const int64_t c = p.col0 + pb * 16;
-    const int64_t cv = a.cols - c;
-    p.n = row < a.rows ? int(cv < 0 ? 0 : (cv > 16 ? 16 : cv)) : 0;
-    p.row = (row < a.rows && cv > 0) ? s * a.rows + row : -1;
-    p.ptr = p.n ? static_cast<const void*>(src + s * a.seg_src + row * a.ld_src + c) : static_cast<const void*>(src);
+    p.col0 = it.col0;
+    p.gb0 = it.gb0;
+    p.nbl = it.nbl;
+    p.bl = it.bl;
+    p.last = it.bl == it.nbl - 1;
+    const int row = it.blk * 16 + pr;
+    const int c = it.col0 + pb * 16;
+    const int cv = cols - c;
+    const bool rok = row < rows;
+    p.n = rok ? (cv < 0 ? 0 : (cv > 16 ? 16 : cv)) : 0;
+    p.row = (rok && cv > 0) ? int64_t(it.s) * rows + row : -1;
+    p.ptr = p.n ? static_cast<const void*>(src + int64_t(it.s) * a.seg_src + int64_t(row) * a.ld_src + c)
+                : static_cast<const void*>(src);
+    it.advance();
     return p;
   };
-  auto advance = [&]() {
-    if (it_item >= items) return;
-    const int64_t g = it_item / ncol_tiles;
-    const int64_t gb0 = g * a.nb;
-    const int nbl = int(a.total_blocks - gb0 < a.nb ? a.total_blocks - gb0 : a.nb);
-    if (++it_bl == nbl) { it_bl = 0; it_item += gridDim.x; }
-  };
 
-  StepPos p0 = pos_of(it_item, it_bl); advance();
-  StepPos p1 = pos_of(it_item, it_bl); advance();
+  StepPos p0 = pos_of();
+  StepPos p1 = pos_of();
   uint4 r0[V], r1[V], r2[V];
   load_raw<T>(static_cast<const T*>(p0.ptr), p0.n, a.vec, r0);
   load_raw<T>(static_cast<const T*>(p1.ptr), p1.n, a.vec, r1);
@@ -539,15 +561,15 @@ __device__ __forceinline__ void run_tile(const TileArgs& a, const Quant& qx, con
 
   // software pipeline: loads run two steps ahead of the math
   while (p0.valid) {
-    StepPos p2 = pos_of(it_item, it_bl); advance();
+    StepPos p2 = pos_of();
     load_raw<T>(static_cast<const T*>(p2.ptr), p2.n, a.vec, r2);
     step(p0, r0);
     if (!p1.valid) break;
-    StepPos p3 = pos_of(it_item, it_bl); advance();
+    StepPos p3 = pos_of();
     load_raw<T>(static_cast<const T*>(p3.ptr), p3.n, a.vec, r0);
     step(p1, r1);
     if (!p2.valid) break;
-    StepPos p4 = pos_of(it_item, it_bl); advance();
+    StepPos p4 = pos_of();
     load_raw<T>(static_cast<const T*>(p4.ptr), p4.n, a.vec, r1);
     step(p2, r2);
     p0 = p3;
@@ -597,7 +619,13 @@ void launch_tile(const TileArgs& a, cudaStream_t stream) {
                          cudaFuncAttributeMaxDynamicSharedMemorySize, 96 * 1024);
     attr = true;
   }
-  const int64_t cap = int64_t(num_sms()) * 4;
+  // persistent grid: exactly the resident CTAs, each walking several steps so
+  // the register prefetch always has the next two blocks in flight
+  int per_sm = 0;
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, tile_kernel<T, MODE, GX, GW, BM>,
+                                                    kThreads, smem) != cudaSuccess || per_sm < 1)
+    per_sm = 1;
+  const int64_t cap = int64_t(num_sms()) * per_sm;
   const int grid = int(items < 1 ? 1 : (items > cap ? cap : items));
   tile_kernel<T, MODE, GX, GW, BM><<<grid, kThreads, smem, stream>>>(a);
 }

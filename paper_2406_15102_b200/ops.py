@@ -16,6 +16,57 @@ from .errors import DimensionError, ParameterError
 
 QMAX = {4: 7, 8: 127}
 
+# ---------------------------------------------------------------------------
+# launch accounting / tracing (bench.py's gpu_launches and roofline inputs)
+# ---------------------------------------------------------------------------
+LAUNCHES = [0]  # number of libhlq kernels enqueued by this process
+_TRACE = [None]
+
+
+class Trace:
+    """Records a CUDA event pair around every libhlq call on the launching
+    stream, with the call's algorithmic bytes (transforms) or ops (GEMMs)."""
+
+    def __init__(self):
+        self.records = []  # (kind, start_event, end_event, bytes, ops, launches)
+
+    def summary(self):
+        torch.cuda.synchronize()
+        out = {}
+        for kind, s, e, nbytes, nops, nl in self.records:
+            d = out.setdefault(kind, {"calls": 0, "us": 0.0, "bytes": 0, "ops": 0, "launches": 0})
+            d["calls"] += 1
+            d["us"] += s.elapsed_time(e) * 1e3
+            d["bytes"] += nbytes
+            d["ops"] += nops
+            d["launches"] += nl
+        return out
+
+
+class trace:
+    def __enter__(self):
+        self.t = Trace()
+        _TRACE[0] = self.t
+        return self.t
+
+    def __exit__(self, *exc):
+        _TRACE[0] = None
+        return False
+
+
+def _traced(kind: str, nbytes: int, nops: int, launches: int, fn):
+    LAUNCHES[0] += launches
+    tr = _TRACE[0]
+    if tr is None:
+        return fn()
+    s = torch.cuda.Event(enable_timing=True)
+    e = torch.cuda.Event(enable_timing=True)
+    s.record()
+    r = fn()
+    e.record()
+    tr.records.append((kind, s, e, nbytes, nops, launches))
+    return r
+
 
 def pad16(n: int) -> int:
     return (int(n) + 15) & ~15
@@ -63,8 +114,9 @@ def quant_ht_cols(src: torch.Tensor, bits: int):
     codes = torch.empty((rows, ld), dtype=torch.int8, device=src.device)
     scale = torch.empty(1, dtype=torch.float32, device=src.device)
     stats = torch.empty(4, dtype=torch.int32, device=src.device)
-    _lib.call("hlq_quantize_ht_cols", _p(src), dtype_code(src), rows, cols, cols, bits, _p(stats),
-              _p(codes), ld, _p(scale), _stream())
+    _traced("transform", rows * cols * src.element_size() + rows * ld, 0, 2,
+            lambda: _lib.call("hlq_quantize_ht_cols", _p(src), dtype_code(src), rows, cols, cols,
+                              bits, _p(stats), _p(codes), ld, _p(scale), _stream()))
     return codes, scale, stats[0:1]
 
 
@@ -85,9 +137,11 @@ def quant_dual(src: torch.Tensor, segs: int, rows: int, cols: int, bitmap: int, 
     cgw = torch.empty((cols, ldk), dtype=torch.int8, device=dev)
     scales = torch.empty(2, dtype=torch.float32, device=dev)
     stats = torch.empty(4, dtype=torch.int32, device=dev)
-    _lib.call("hlq_quantize_dual", _p(src), dtype_code(src), segs, rows, cols, ld_src, seg_src,
-              bitmap, bits_gx, bits_gw, _p(stats), _p(cgx), cgx.stride(0), _p(cgw), ldk,
-              _p(scales), _p(scales[1:]), _stream())
+    nbytes = segs * rows * cols * src.element_size() + cgx.numel() + cols * k
+    _traced("transform", nbytes, 0, 2,
+            lambda: _lib.call("hlq_quantize_dual", _p(src), dtype_code(src), segs, rows, cols,
+                              ld_src, seg_src, bitmap, bits_gx, bits_gw, _p(stats), _p(cgx),
+                              cgx.stride(0), _p(cgw), ldk, _p(scales), _p(scales[1:]), _stream()))
     return cgx, scales[0:1], cgw, k, scales[1:2], stats
 
 
@@ -108,8 +162,10 @@ def quant_proj_rows(src: torch.Tensor, segs: int, rows: int, cols: int, bitmap: 
     codes = torch.empty((cols, ld), dtype=torch.int8, device=src.device)
     scale = torch.empty(1, dtype=torch.float32, device=src.device)
     stats = torch.empty(4, dtype=torch.int32, device=src.device)
-    _lib.call("hlq_quantize_proj_rows", _p(src), dtype_code(src), segs, rows, cols, ld_src, seg_src,
-              bitmap, bits, _p(stats), _p(codes), ld, _p(scale), _stream())
+    _traced("transform", segs * rows * cols * src.element_size() + cols * k, 0, 2,
+            lambda: _lib.call("hlq_quantize_proj_rows", _p(src), dtype_code(src), segs, rows, cols,
+                              ld_src, seg_src, bitmap, bits, _p(stats), _p(codes), ld, _p(scale),
+                              _stream()))
     return codes, k, scale, stats[2:3]
 
 
@@ -152,11 +208,12 @@ def gemm_i8(a: torch.Tensor, b: torch.Tensor, m: int, n: int, k: int, bits_a: in
     lda, ldb = a.stride(0), b.stride(0)
     a_gs = lda * m if a_gstride is None else a_gstride
     b_gs = ldb * n if b_gstride is None else b_gstride
-    _lib.call("hlq_gemm_i8_grouped", _p(a), lda, a_gs, _p(b), ldb, b_gs, m, n, k, groups, bits_a,
-              bits_b, _p(sa), _p(sb), float(extra),
-              _lib.HLQ_EPI_EXACT if exact else _lib.HLQ_EPI_FAST, _p(out),
-              _lib.HLQ_BF16 if out_dtype == torch.bfloat16 else _lib.HLQ_F32, n, _p(acc), n,
-              _stream())
+    _traced("gemm", 0, 2 * m * n * k * groups, 1,
+            lambda: _lib.call("hlq_gemm_i8_grouped", _p(a), lda, a_gs, _p(b), ldb, b_gs, m, n, k,
+                              groups, bits_a, bits_b, _p(sa), _p(sb), float(extra),
+                              _lib.HLQ_EPI_EXACT if exact else _lib.HLQ_EPI_FAST, _p(out),
+                              _lib.HLQ_BF16 if out_dtype == torch.bfloat16 else _lib.HLQ_F32, n,
+                              _p(acc), n, _stream()))
     return out, acc
 
 
