@@ -269,6 +269,31 @@ bool make_map(CUtensorMap* map, const int8_t* ptr, int64_t rows, int64_t k, int6
             CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
+}  // namespace
+
+bool encode_tensor_map(void* map, int dtype, int rank, const void* ptr, const uint64_t* dims,
+                       const uint64_t* strides_bytes, const uint32_t* box, int swizzle_128b) {
+  EncodeTiledFn fn = encode_fn();
+  if (!fn || rank < 1 || rank > 5) return false;
+  cuuint64_t d[5], s[4];
+  cuuint32_t b[5], e[5];
+  for (int i = 0; i < rank; ++i) {
+    d[i] = dims[i];
+    b[i] = box[i];
+    e[i] = 1;
+    if (i < rank - 1) s[i] = strides_bytes[i];
+  }
+  const CUtensorMapDataType t = dtype == 1 ? CU_TENSOR_MAP_DATA_TYPE_BFLOAT16
+                                : dtype == 2 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT32
+                                             : CU_TENSOR_MAP_DATA_TYPE_UINT8;
+  return fn(static_cast<CUtensorMap*>(map), t, cuuint32_t(rank), const_cast<void*>(ptr), d, s, b, e,
+            CU_TENSOR_MAP_INTERLEAVE_NONE,
+            swizzle_128b ? CU_TENSOR_MAP_SWIZZLE_128B : CU_TENSOR_MAP_SWIZZLE_NONE,
+            CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
+namespace {
+
 template <int BN, int STAGES>
 int run(const int8_t* A, int64_t lda, const int8_t* B, int64_t ldb, int64_t M, int64_t N, int64_t K,
         int64_t groups, int64_t a_gstride, int64_t b_gstride, const float* sa, const float* sb, double extra, int epilogue, void* out, int out_dtype,

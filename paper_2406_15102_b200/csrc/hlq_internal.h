@@ -35,6 +35,13 @@ struct TransformArgs {
 };
 
 void launch_transform(const TransformArgs& t, int mode, cudaStream_t stream);
+void launch_transform_fallback(const TransformArgs& t, int mode, cudaStream_t stream);
+
+// cuTensorMapEncodeTiled through the runtime's driver entry point (no libcuda
+// link dependency).  Returns false if the driver rejects the map.
+bool encode_tensor_map(void* map /* CUtensorMap* */, int dtype /* 0 u8, 1 bf16, 2 f32 */,
+                       int rank, const void* ptr, const uint64_t* dims, const uint64_t* strides_bytes,
+                       const uint32_t* box, int swizzle_128b);
 
 // Returns a cudaError_t-compatible code (0 on success) or -1 if the tensor maps
 // could not be encoded.

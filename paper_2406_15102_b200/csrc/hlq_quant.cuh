@@ -1,0 +1,208 @@
+// Device helpers shared by the transform kernels: packed fp32x2 arithmetic,
+// the 16-point Walsh-Hadamard butterflies, transformed-value statistics and
+// the bit-exact pseudo-stochastic quantizer (see hlq_transform.cu header for
+// the exactness argument).
+#pragma once
+#include <cuda_bf16.h>
+#include <cstdint>
+
+namespace hlq {
+namespace dev {
+
+constexpr float kMagic = 12582912.0f;  // 1.5 * 2^23: ulp 1, small integers in the low mantissa bits
+
+// ------------------------------------------------------------------ packed fp32x2
+__device__ __forceinline__ float2 f2add(float2 a, float2 b) {
+  float2 d;
+  asm("{.reg .b64 ra, rb, rd;\n\tmov.b64 ra, {%2, %3};\n\tmov.b64 rb, {%4, %5};\n\t"
+      "add.rn.f32x2 rd, ra, rb;\n\tmov.b64 {%0, %1}, rd;}"
+      : "=f"(d.x), "=f"(d.y) : "f"(a.x), "f"(a.y), "f"(b.x), "f"(b.y));
+  return d;
+}
+__device__ __forceinline__ float2 f2sub(float2 a, float2 b) {
+  float2 d;
+  asm("{.reg .b64 ra, rb, rd;\n\tmov.b64 ra, {%2, %3};\n\tmov.b64 rb, {%4, %5};\n\t"
+      "sub.rn.f32x2 rd, ra, rb;\n\tmov.b64 {%0, %1}, rd;}"
+      : "=f"(d.x), "=f"(d.y) : "f"(a.x), "f"(a.y), "f"(b.x), "f"(b.y));
+  return d;
+}
+__device__ __forceinline__ float2 f2mul(float2 a, float2 b) {
+  float2 d;
+  asm("{.reg .b64 ra, rb, rd;\n\tmov.b64 ra, {%2, %3};\n\tmov.b64 rb, {%4, %5};\n\t"
+      "mul.rn.f32x2 rd, ra, rb;\n\tmov.b64 {%0, %1}, rd;}"
+      : "=f"(d.x), "=f"(d.y) : "f"(a.x), "f"(a.y), "f"(b.x), "f"(b.y));
+  return d;
+}
+__device__ __forceinline__ float2 f2fma(float2 a, float2 b, float2 c) {
+  float2 d;
+  asm("{.reg .b64 ra, rb, rc, rd;\n\tmov.b64 ra, {%2, %3};\n\tmov.b64 rb, {%4, %5};\n\t"
+      "mov.b64 rc, {%6, %7};\n\tfma.rn.f32x2 rd, ra, rb, rc;\n\tmov.b64 {%0, %1}, rd;}"
+      : "=f"(d.x), "=f"(d.y) : "f"(a.x), "f"(a.y), "f"(b.x), "f"(b.y), "f"(c.x), "f"(c.y));
+  return d;
+}
+__device__ __forceinline__ float2 f2add_rp(float2 a, float2 b) {
+  float2 d;
+  asm("{.reg .b64 ra, rb, rd;\n\tmov.b64 ra, {%2, %3};\n\tmov.b64 rb, {%4, %5};\n\t"
+      "add.rp.f32x2 rd, ra, rb;\n\tmov.b64 {%0, %1}, rd;}"
+      : "=f"(d.x), "=f"(d.y) : "f"(a.x), "f"(a.y), "f"(b.x), "f"(b.y));
+  return d;
+}
+__device__ __forceinline__ float2 f2fma_rp(float2 a, float2 b, float2 c) {
+  float2 d;
+  asm("{.reg .b64 ra, rb, rc, rd;\n\tmov.b64 ra, {%2, %3};\n\tmov.b64 rb, {%4, %5};\n\t"
+      "mov.b64 rc, {%6, %7};\n\tfma.rp.f32x2 rd, ra, rb, rc;\n\tmov.b64 {%0, %1}, rd;}"
+      : "=f"(d.x), "=f"(d.y) : "f"(a.x), "f"(a.y), "f"(b.x), "f"(b.y), "f"(c.x), "f"(c.y));
+  return d;
+}
+__device__ __forceinline__ float2 f2(float a) { return make_float2(a, a); }
+
+__device__ __forceinline__ float bf_lo(uint32_t w) { return __uint_as_float(w << 16); }
+__device__ __forceinline__ float bf_hi(uint32_t w) { return __uint_as_float(w & 0xFFFF0000u); }
+
+// ------------------------------------------------------------------ transforms
+// Un-normalised 16-point FWHT of one vector (the 0.25 is folded into the
+// quantizer divisor).  Register pairs (v[i], v[i+8]) run stages h = 1, 2, 4
+// as f32x2; stage 8 pairs the two lanes of each register pair.  Stage order
+// h = 1, 2, 4, 8 is the reference's (hadamard.py:125-133).
+__device__ __forceinline__ void fwht16_raw(float (&v)[16]) {
+  float2 p[8];
+#pragma unroll
+  for (int i = 0; i < 8; ++i) p[i] = make_float2(v[i], v[i + 8]);
+#pragma unroll
+  for (int h = 1; h < 8; h <<= 1) {
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+      if (!(i & h)) {
+        const float2 a = p[i], b = p[i + h];
+        p[i] = f2add(a, b);
+        p[i + h] = f2sub(a, b);
+      }
+    }
+  }
+#pragma unroll
+  for (int i = 0; i < 8; ++i) {
+    v[i] = __fadd_rn(p[i].x, p[i].y);
+    v[i + 8] = __fsub_rn(p[i].x, p[i].y);
+  }
+}
+
+// Two independent vectors at once (lane x and lane y of each float2).  The
+// compiler drops butterflies whose outputs are never read (pruned projection).
+__device__ __forceinline__ void fwht16_pair(float2 (&p)[16]) {
+#pragma unroll
+  for (int h = 1; h < 16; h <<= 1) {
+#pragma unroll
+    for (int i = 0; i < 16; ++i) {
+      if (!(i & h)) {
+        const float2 a = p[i], b = p[i + h];
+        p[i] = f2add(a, b);
+        p[i + h] = f2sub(a, b);
+      }
+    }
+  }
+}
+
+// ------------------------------------------------------------------ statistics
+struct Stat {
+  uint32_t amax = 0;             // max |w| bits (NaN/Inf land >= 0x7F800000)
+  uint32_t minnz = 0xFFFFFFFFu;  // min (|w| bits - 1): the smallest nonzero magnitude
+  __device__ __forceinline__ void add(float w) {
+    const uint32_t a = __float_as_uint(w) & 0x7FFFFFFFu;
+    amax = max(amax, a);
+    minnz = min(minnz, a - 1u);
+  }
+  __device__ __forceinline__ void warp_reduce() {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      amax = max(amax, __shfl_xor_sync(0xffffffffu, amax, o));
+      minnz = min(minnz, __shfl_xor_sync(0xffffffffu, minnz, o));
+    }
+  }
+  // global layout {amax, ~minnz}, both max-reduced so a zero memset is the identity
+  __device__ __forceinline__ void commit(uint32_t* g) const {
+    if (amax) atomicMax(g, amax);
+    if (~minnz) atomicMax(g + 1, ~minnz);
+  }
+};
+
+// ------------------------------------------------------------------ quantizer
+struct Quant {
+  float s, d, r, lim, qmax;
+  uint32_t lim16;   // (qmax, qmax) as s16x2
+  uint32_t nlim16;  // (-qmax, -qmax) as s16x2
+  bool fast;
+};
+
+// scale = f32(amax_v) / f32(qmax), 0 -> 1 (quantize.py:94-100), amax_v = RN(0.25 * max|w|)
+// (= max|RN(0.25 w)| because rounding is monotone).
+__device__ __forceinline__ Quant make_quant(const uint32_t* g, int bits) {
+  Quant q;
+  const int qm = (1 << (bits - 1)) - 1;
+  q.qmax = float(qm);
+  q.lim16 = (uint32_t(qm) & 0xFFFFu) * 0x10001u;
+  q.nlim16 = (uint32_t(-qm) & 0xFFFFu) * 0x10001u;
+  const float amax_w = __uint_as_float(g[0]);
+  const float amax_v = __fmul_rn(amax_w, 0.25f);
+  float s = __fdiv_rn(amax_v, q.qmax);
+  if (s == 0.0f) s = 1.0f;
+  q.s = s;
+  q.d = __fmul_rn(s, 1.0f / 512.0f);
+  q.r = __frcp_rn(q.d);
+  q.lim = 2048.0f * q.qmax;
+  const uint32_t inv = g[1];
+  const float minnz = inv ? __uint_as_float(~inv + 1u) : 0.0f;  // 0: no nonzero value at all
+  q.fast = (g[0] < 0x7F800000u) && s > 0x1p-116f &&
+           (minnz == 0.0f || (minnz >= 0x1p-100f && minnz >= __fmul_rn(s, 0x1p-108f)));
+  return q;
+}
+
+// Unclamped codes of two values as two s16 lanes: code = ceil((Q - u) / 2048),
+// Q = RN(w / d) by reciprocal-FMA division, u = bits(w) & 0x7FF.
+__device__ __forceinline__ uint32_t quant_fast2(float2 w, const Quant& q) {
+  const float2 Q0 = f2mul(w, f2(q.r));
+  const float2 e = f2fma(Q0, f2(-q.d), w);
+  const float2 Q = f2fma(e, f2(q.r), Q0);
+  uint32_t ux, uy;
+  const uint32_t magic = 0x4B000000u;  // 2^23: (2^23 + u) as a float, one LOP3 each
+  asm("lop3.b32 %0, %1, 0x7FF, %2, 0xEA;" : "=r"(ux) : "r"(__float_as_uint(w.x)), "r"(magic));
+  asm("lop3.b32 %0, %1, 0x7FF, %2, 0xEA;" : "=r"(uy) : "r"(__float_as_uint(w.y)), "r"(magic));
+  const float2 nu = f2sub(f2(8388608.0f), make_float2(__uint_as_float(ux), __uint_as_float(uy)));
+  const float2 z = f2add_rp(Q, nu);                                   // RU(Q - u)
+  const float2 c = f2fma_rp(z, f2(1.0f / 2048.0f), f2(kMagic));       // M + ceil(z / 2048)
+  return __byte_perm(__float_as_uint(c.x), __float_as_uint(c.y), 0x5410);
+}
+
+// Literal restatement of quantize.py:140-145 (IEEE division), used when the
+// fast path's guard fails for the tensor.  Returns the clamped code.
+__device__ __forceinline__ int quant_exact(float w, const Quant& q) {
+  const float v = __fmul_rn(w, 0.25f);
+  const float qq = __fdiv_rn(v, q.s);
+  const float lo = floorf(qq);
+  const float draw = __uint2float_rn(__float_as_uint(v) & 0x7FFu);
+  const float frac = __fmul_rn(__fsub_rn(qq, lo), 2048.0f);
+  float c = __fadd_rn(lo, frac > draw ? 1.0f : 0.0f);
+  c = fminf(fmaxf(c, -q.qmax), q.qmax);
+  return static_cast<int>(c);
+}
+
+__device__ __forceinline__ uint32_t clamp_s16x2(uint32_t p, const Quant& q) {
+  uint32_t r;
+  asm("max.s16x2 %0, %1, %2;" : "=r"(r) : "r"(p), "r"(q.nlim16));
+  asm("min.s16x2 %0, %1, %2;" : "=r"(r) : "r"(r), "r"(q.lim16));
+  return r;
+}
+
+// Two clamped codes as s16x2.
+template <bool FAST>
+__device__ __forceinline__ uint32_t quant2(float2 w, const Quant& q) {
+  if (FAST) return clamp_s16x2(quant_fast2(w, q), q);
+  return (uint32_t(quant_exact(w.x, q)) & 0xFFFFu) | (uint32_t(quant_exact(w.y, q)) << 16);
+}
+
+// Four codes (two s16x2 words) -> four int8 bytes.
+__device__ __forceinline__ uint32_t pack4(uint32_t p01, uint32_t p23) {
+  return __byte_perm(p01, p23, 0x6420);
+}
+
+}  // namespace dev
+}  // namespace hlq
