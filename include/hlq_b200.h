@@ -156,6 +156,23 @@ HLQ_API int hlq_acbp_compress(const void* x, int dtype, int64_t B, int64_t L, in
                       uint32_t bitmap, int bits, int8_t* payload, int64_t ld_payload,
                       float* scale_out, uint32_t* stats_ws, void* stream);
 
+/* Conv2d (harness/layers.py:96-158).  ACBP of the im2col'd input without
+ * materialising it: x is channels-last (B, H, W, C); the payload row for
+ * column (c, i, j) of cols is c*k*k + i*k + j (torch's weight flattening);
+ * K = B * ceil(Ho*Wo/16) * rank.  Replaces Conv2d.forward's im2col +
+ * acbp_compress (layers.py:141-151,46-55).  Requires Ho*Wo >= 16. */
+HLQ_API int hlq_conv_acbp_compress(const void* x_nhwc, int dtype, int64_t B, int64_t H, int64_t W,
+                                   int64_t C, int k, int stride, int pad, uint32_t bitmap,
+                                   int bits, int8_t* payload, int64_t ld_payload, float* scale_out,
+                                   uint32_t* stats_ws, void* stream);
+
+/* col2im (layers.py:109-121): dx[b, h, w, c] (channels-last) = sum over taps
+ * in the reference's (i, j) order of dcols[b*L + l, c*k*k + i*k + j]
+ * (fp32 accumulation; bit-exact vs the reference for fp32 dcols). */
+HLQ_API int hlq_col2im(const void* dcols, int dtype, int64_t ld, int64_t B, int64_t H, int64_t W,
+                       int64_t C, int k, int stride, int pad, void* dx_nhwc, int out_dtype,
+                       void* stream);
+
 /* Workspace bytes needed by hlq_hq_grad_input / hlq_grad_weight. */
 HLQ_API size_t hlq_hq_grad_input_ws(int64_t T, int64_t O, int64_t I);
 HLQ_API size_t hlq_grad_weight_ws(int64_t B, int64_t L, int64_t O, int axis, int rank);

@@ -248,6 +248,44 @@ int hlq_gemm_i8_grouped(const int8_t* A, int64_t lda, int64_t a_gstride, const i
   return HLQ_OK;
 }
 
+int hlq_conv_acbp_compress(const void* x_nhwc, int dtype, int64_t B, int64_t H, int64_t W,
+                           int64_t C, int k, int stride, int pad, uint32_t bitmap, int bits,
+                           int8_t* payload, int64_t ld_payload, float* scale_out,
+                           uint32_t* stats_ws, void* stream) {
+  HLQ_TRY(check_dtype(dtype));
+  HLQ_TRY(check_bits(bits));
+  HLQ_TRY(check_bitmap(bitmap));
+  HLQ_TRY(check_ld16(ld_payload, "payload"));
+  if (B <= 0 || H <= 0 || W <= 0 || C <= 0 || k <= 0 || stride <= 0 || pad < 0 ||
+      H + 2 * pad < k || W + 2 * pad < k || B * H * W * C >= (int64_t(1) << 40))
+    return fail(HLQ_ERR_DIMENSION, "bad conv geometry");
+  const int64_t Ho = (H + 2 * pad - k) / stride + 1, Wo = (W + 2 * pad - k) / stride + 1;
+  if (Ho * Wo < 16)
+    return fail(HLQ_ERR_DIMENSION,
+                "conv output has L=Ho*Wo=%lld < 16; the batch-axis projection needs the Python layer",
+                (long long)(Ho * Wo));
+  const int64_t kk = B * ((Ho * Wo + 15) / 16) * __builtin_popcount(bitmap);
+  if (ld_payload < kk) return fail(HLQ_ERR_DIMENSION, "payload ld %lld < K %lld", (long long)ld_payload, (long long)kk);
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  cudaMemsetAsync(stats_ws, 0, 4 * sizeof(uint32_t), st);
+  hlq::launch_im2col_proj(x_nhwc, dtype, int(B), int(H), int(W), int(C), k, stride, pad, bitmap, bits,
+                          hlq::kStats, stats_ws, nullptr, 0, nullptr, st);
+  hlq::launch_im2col_proj(x_nhwc, dtype, int(B), int(H), int(W), int(C), k, stride, pad, bitmap, bits,
+                          hlq::kQuant, stats_ws, payload, ld_payload, scale_out, st);
+  return cuda_status("hlq_conv_acbp_compress");
+}
+
+int hlq_col2im(const void* dcols, int dtype, int64_t ld, int64_t B, int64_t H, int64_t W, int64_t C,
+               int k, int stride, int pad, void* dx_nhwc, int out_dtype, void* stream) {
+  HLQ_TRY(check_dtype(dtype));
+  HLQ_TRY(check_dtype(out_dtype));
+  if (B <= 0 || H <= 0 || W <= 0 || C <= 0 || k <= 0 || stride <= 0 || pad < 0 || ld < C * k * k)
+    return fail(HLQ_ERR_DIMENSION, "bad col2im geometry");
+  hlq::launch_col2im(dcols, dtype, ld, int(B), int(H), int(W), int(C), k, stride, pad, dx_nhwc,
+                     out_dtype, static_cast<cudaStream_t>(stream));
+  return cuda_status("hlq_col2im");
+}
+
 int64_t hlq_acbp_k(int64_t B, int64_t L, int axis, int rank) {
   return axis == 1 ? B * ((L + 15) / 16) * rank : ((B + 15) / 16) * rank;
 }

@@ -37,6 +37,13 @@ struct TransformArgs {
 void launch_transform(const TransformArgs& t, int mode, cudaStream_t stream);
 void launch_transform_fallback(const TransformArgs& t, int mode, cudaStream_t stream);
 
+// Conv lowering (hlq_conv.cu).  x is channels-last (B, H, W, C).
+void launch_im2col_proj(const void* x, int dtype, int B, int H, int W, int C, int k, int stride,
+                        int pad, uint32_t bitmap, int bits, int mode, uint32_t* stats, int8_t* dst,
+                        int64_t ld_dst, float* scale, cudaStream_t st);
+void launch_col2im(const void* dcols, int in_dtype, int64_t ld, int B, int H, int W, int C, int k,
+                   int stride, int pad, void* dx, int out_dtype, cudaStream_t st);
+
 // cuTensorMapEncodeTiled through the runtime's driver entry point (no libcuda
 // link dependency).  Returns false if the driver rejects the map.
 bool encode_tensor_map(void* map /* CUtensorMap* */, int dtype /* 0 u8, 1 bf16, 2 f32 */,

@@ -217,6 +217,43 @@ def gemm_i8(a: torch.Tensor, b: torch.Tensor, m: int, n: int, k: int, bits_a: in
     return out, acc
 
 
+def conv_out_hw(H: int, W: int, k: int, stride: int, pad: int):
+    return (H + 2 * pad - k) // stride + 1, (W + 2 * pad - k) // stride + 1
+
+
+def conv_acbp(x_nhwc: torch.Tensor, k: int, stride: int, pad: int, bitmap: int, bits: int):
+    """ACBP of im2col(x) along the output-pixel axis, from channels-last x
+    (B, H, W, C) viewed as a contiguous tensor.  Returns (codes (C*k*k, pad16(K)), K, scale, amax)."""
+    _check_bits(bits)
+    x_nhwc = _cuda(x_nhwc, "x")
+    B, H, W, C = x_nhwc.shape
+    Ho, Wo = conv_out_hw(H, W, k, stride, pad)
+    kk = B * ((Ho * Wo + 15) // 16) * bin(bitmap).count("1")
+    ld = max(pad16(kk), 16)
+    codes = torch.empty((C * k * k, ld), dtype=torch.int8, device=x_nhwc.device)
+    scale = torch.empty(1, dtype=torch.float32, device=x_nhwc.device)
+    stats = torch.empty(4, dtype=torch.int32, device=x_nhwc.device)
+    nbytes = x_nhwc.numel() * x_nhwc.element_size() + C * k * k * kk
+    _traced("transform", nbytes, 0, 2,
+            lambda: _lib.call("hlq_conv_acbp_compress", _p(x_nhwc), dtype_code(x_nhwc), B, H, W, C, k,
+                              stride, pad, bitmap, bits, _p(codes), ld, _p(scale), _p(stats),
+                              _stream()))
+    return codes, kk, scale, stats[2:3]
+
+
+def col2im(dcols: torch.Tensor, B: int, H: int, W: int, C: int, k: int, stride: int, pad: int,
+           out_dtype=torch.float32) -> torch.Tensor:
+    """dX (B, H, W, C) contiguous (= channels-last NCHW) from dcols (B*L, C*k*k)."""
+    dcols = _cuda(dcols, "dcols")
+    dx = torch.empty((B, H, W, C), dtype=out_dtype, device=dcols.device)
+    _traced("col2im", dcols.numel() * dcols.element_size() + dx.numel() * dx.element_size(), 0, 1,
+            lambda: _lib.call("hlq_col2im", _p(dcols), dtype_code(dcols), dcols.stride(0), B, H, W, C,
+                              k, stride, pad, _p(dx),
+                              _lib.HLQ_BF16 if out_dtype == torch.bfloat16 else _lib.HLQ_F32,
+                              _stream()))
+    return dx
+
+
 def amax_to_float(amax_bits: torch.Tensor) -> torch.Tensor:
     return amax_bits.view(torch.float32)
 

@@ -1,0 +1,100 @@
+"""GPU parity for the Conv2d lowering (reference harness/layers.py:96-158):
+ACBP of im2col(x) straight from channels-last x, dW through the int8 GEMM,
+dX through the int8 GEMM + col2im in the reference's tap order."""
+import json
+import os
+
+import numpy as np
+import pytest
+import torch
+
+from oracle import hlq_oracle as orc
+
+from .conftest import GOLDEN
+
+pytestmark = pytest.mark.gpu
+
+MANIFEST = json.load(open(os.path.join(GOLDEN, "MANIFEST.json")))
+CONV = [c for c in MANIFEST["cases"] if c.startswith("conv")]
+DEV = "cuda"
+
+
+def t(a):
+    return torch.from_numpy(np.ascontiguousarray(a)).to(DEV)
+
+
+def n(x):
+    return x.detach().cpu().numpy()
+
+
+@pytest.fixture(scope="module")
+def conv():
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    from paper_2406_15102_b200 import conv as c
+    return c
+
+
+def check(got_st, dx, dw, ref):
+    for key in ("x_codes", "gx_codes_g", "gx_codes_w", "gw_codes_g"):
+        g = n(got_st[key])
+        assert g.shape == ref[key].shape, (key, g.shape, ref[key].shape)
+        assert np.count_nonzero(g != ref[key]) == 0, key
+    assert np.array_equal(n(got_st["gx_acc"]).astype(np.int64), ref["gx_acc"])
+    assert np.array_equal(n(got_st["gw_acc"]).astype(np.int64), ref["gw_acc"])
+    assert np.array_equal(n(dw), ref["gw"]), "dW not bit-exact"
+    assert np.array_equal(n(dx), ref["gx"]), "dX not bit-exact"
+
+
+@pytest.mark.parametrize("case", CONV)
+def test_golden_conv(conv, case):
+    g = dict(np.load(os.path.join(GOLDEN, case + ".npz")))
+    st = {}
+    dx, dw = conv.conv2d_hlq_backward(t(g["x"]), t(g["w"]), t(g["gy"]), int(g["stride"]), int(g["pad"]),
+                                      stages=st)
+    torch.cuda.synchronize()
+    check(st, dx, dw, g)
+
+
+@pytest.mark.parametrize("B,C,H,O,k,s,p", [
+    (16, 256, 14, 256, 3, 1, 1),   # BASELINE config (b) geometry, 16 of its 128 images
+    (8, 64, 32, 64, 3, 1, 1),      # ResNet-18 CIFAR stage 1
+    (8, 64, 32, 128, 3, 2, 1),     # stage-2 downsampling conv
+    (8, 64, 32, 128, 1, 2, 0),     # 1x1 shortcut
+    (4, 3, 32, 64, 3, 1, 1),       # stem (C = 3: unaligned channel rows)
+])
+def test_seeded_conv_vs_oracle(conv, B, C, H, O, k, s, p):
+    x, w, gy0 = orc.make_inputs(B + C + k, (B, C, H, H), (O, C, k, k), (1,))
+    Ho, _ = orc.conv_out_hw(H, H, k, s, p)
+    rng = np.random.default_rng(7)
+    gy = (rng.lognormal(0.0, 1.4, size=(B, O, Ho, Ho)) * rng.choice([-1.0, 1.0], size=(B, O, Ho, Ho))
+          * 1e-3).astype(np.float32)
+    st = {}
+    rst = {}
+    dx, dw = conv.conv2d_hlq_backward(t(x), t(w), t(gy), s, p, stages=st)
+    rdx, rdw = orc.conv2d_hlq_backward(x, w, gy, s, p, stages=rst)
+    rst["gx"], rst["gw"] = rdx, rdw
+    check(st, dx, dw, rst)
+
+
+def test_hlq_conv2d_module_autograd(conv):
+    from paper_2406_15102_b200.conv import HLQConv2d
+    B, C, H, O = 8, 32, 16, 64
+    x, w, _ = orc.make_inputs(3, (B, C, H, H), (O, C, 3, 3), (1,))
+    rng = np.random.default_rng(4)
+    gy = (rng.standard_normal((B, O, H, H)) * 1e-2).astype(np.float32)
+    m = HLQConv2d(C, O, 3, padding=1, bias=True).to(DEV)
+    with torch.no_grad():
+        m.weight.copy_(t(w))
+        m.bias.zero_()
+    xt = t(x).contiguous(memory_format=torch.channels_last).requires_grad_(True)
+    y = m(xt)
+    ref_y = torch.nn.functional.conv2d(t(x), t(w), padding=1)
+    assert torch.allclose(y, ref_y, rtol=1e-4, atol=1e-4)
+    y.backward(t(gy))
+    rdx, rdw = orc.conv2d_hlq_backward(x, w, gy, 1, 1, extra=1.0)
+    ex = np.linalg.norm(n(xt.grad) - rdx) / np.linalg.norm(rdx)
+    ew = np.linalg.norm(n(m.weight.grad) - rdw) / np.linalg.norm(rdw)
+    # training path: fast fp32 epilogue, bf16 dcols -> within the 1e-3 contract
+    assert ex < 1e-2 and ew < 1e-5, (ex, ew)
+    assert np.allclose(n(m.bias.grad), gy.sum(axis=(0, 2, 3)), rtol=1e-4, atol=1e-5)
