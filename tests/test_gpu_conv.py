@@ -88,8 +88,13 @@ def test_hlq_conv2d_module_autograd(conv):
         m.weight.copy_(t(w))
         m.bias.zero_()
     xt = t(x).contiguous(memory_format=torch.channels_last).requires_grad_(True)
-    y = m(xt)
-    ref_y = torch.nn.functional.conv2d(t(x), t(w), padding=1)
+    tf32 = torch.backends.cudnn.allow_tf32
+    torch.backends.cudnn.allow_tf32 = False
+    try:
+        y = m(xt)
+        ref_y = torch.nn.functional.conv2d(t(x), t(w), padding=1)
+    finally:
+        torch.backends.cudnn.allow_tf32 = tf32
     assert torch.allclose(y, ref_y, rtol=1e-4, atol=1e-4)
     y.backward(t(gy))
     rdx, rdw = orc.conv2d_hlq_backward(x, w, gy, 1, 1, extra=1.0)
