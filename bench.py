@@ -46,6 +46,7 @@ def parse():
     ap.add_argument("--workload", default="vit_train", choices=["vit_train"])
     ap.add_argument("--batch", type=int, default=BATCH, help="images per GPU")
     ap.add_argument("--no-extras", action="store_true", help="skip dense/layer/cpu side measurements")
+    ap.add_argument("--dist-backend", default="nccl", choices=["nccl", "gloo"])
     return ap.parse_args()
 
 
@@ -307,11 +308,16 @@ def run_ours(args):
 
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
-    local = int(os.environ.get("LOCAL_RANK", "0"))
+    # one process per GPU; (--dist-backend gloo lets several ranks share a GPU
+    # to exercise the N > 1 code path on a single-GPU box)
+    local = int(os.environ.get("LOCAL_RANK", "0")) % max(1, torch.cuda.device_count())
     torch.cuda.set_device(local)
     dist = None
     if world > 1:
-        dist_mod.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if args.dist_backend == "nccl":
+            dist_mod.init_process_group("nccl", device_id=torch.device("cuda", local))
+        else:
+            dist_mod.init_process_group(args.dist_backend)
         dist = dist_mod
     if _lib.load().hlq_device_ok() != 1:
         raise RuntimeError("libhlq_b200 needs an sm_100 device")

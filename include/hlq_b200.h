@@ -115,6 +115,20 @@ HLQ_API int hlq_proj_rows_quant(const void* src, int dtype, int64_t segs, int64_
                         const uint32_t* stats, int8_t* dst, int64_t ld_dst, float* scale_out,
                         void* stream);
 
+/* One pass of the general transform (the building block of every call above):
+ * mode 0 = STATS (max-accumulates {amax, ~minnz} of the gx operand into
+ * stats[0..1] and of the gw operand into stats[2..3]; the caller zeroes
+ * stats first, or all-reduces(MAX) them across ranks in between), mode 1 =
+ * QUANT with the scales implied by `stats`.  This is what the exact
+ * data-parallel mode uses: STATS on the local shard, all-reduce(MAX) of the 4
+ * words, QUANT -- every rank then quantizes with the scale the single-process
+ * reference computes. */
+HLQ_API int hlq_transform_pass(const void* src, int dtype, int64_t segs, int64_t rows, int64_t cols,
+                               int64_t ld_src, int64_t seg_src, int do_gx, int do_gw,
+                               uint32_t bitmap, int bits_gx, int bits_gw, int mode, uint32_t* stats,
+                               int8_t* dst_gx, int64_t ld_gx, int8_t* dst_gw, int64_t ld_gw,
+                               float* scale_gx, float* scale_gw, void* stream);
+
 /* D[m, n] = sum_k A[m, k] * B[n, k] on int8 codes (tcgen05 kind::i8, int32 in
  * TMEM), dequantized with the fused epilogue.  Replaces `int_matmul` +
  * `int_matmul_dequant` (quantize.py:152-187).  lda/ldb are byte strides,

@@ -144,6 +144,22 @@ def quantize(v: np.ndarray, bits: int):
     return codes, scale
 
 
+def quantize_with_amax(v: np.ndarray, bits: int, amax) -> tuple:
+    """quantize() with the per-tensor amax supplied (e.g. reduced over data-
+    parallel shards): the codes the single-process quantizer produces for this
+    slice of a larger tensor."""
+    qmax = QMAX[bits]
+    v = np.ascontiguousarray(v, dtype=F32)
+    scale = F32(F32(amax) / F32(qmax))
+    if scale == 0:
+        scale = F32(1.0)
+    q = v / scale
+    lo = np.floor(q)
+    draw = (v.view(np.uint32) & np.uint32(0x7FF)).astype(F32)
+    bump = ((q - lo) * F32(2048.0)) > draw
+    return np.clip(lo + bump.astype(F32), -qmax, qmax).astype(np.int8), scale
+
+
 def int_gemm(a: np.ndarray, b: np.ndarray) -> np.ndarray:
     """Exact sum of int8 products; fp64 BLAS is exact below 2**53."""
     return (a.astype(np.float64) @ b.astype(np.float64)).astype(np.int64)

@@ -36,6 +36,8 @@ SIGNATURES = {
                                     _P, _P]),
     "hlq_quantize_dual": (_I, [_P, _I, _I64, _I64, _I64, _I64, _I64, _U32, _I, _I, _P, _P, _I64, _P,
                                _I64, _P, _P, _P]),
+    "hlq_transform_pass": (_I, [_P, _I, _I64, _I64, _I64, _I64, _I64, _I, _I, _U32, _I, _I, _I, _P,
+                                _P, _I64, _P, _I64, _P, _P, _P]),
     "hlq_proj_rows_amax": (_I, [_P, _I, _I64, _I64, _I64, _I64, _I64, _U32, _P, _P]),
     "hlq_proj_rows_quant": (_I, [_P, _I, _I64, _I64, _I64, _I64, _I64, _U32, _I, _P, _P, _I64, _P,
                                  _P]),

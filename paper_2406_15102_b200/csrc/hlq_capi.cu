@@ -187,6 +187,28 @@ int hlq_quantize_proj_rows(const void* src, int dtype, int64_t segs, int64_t row
   return cuda_status("hlq_quantize_proj_rows");
 }
 
+int hlq_transform_pass(const void* src, int dtype, int64_t segs, int64_t rows, int64_t cols,
+                       int64_t ld_src, int64_t seg_src, int do_gx, int do_gw, uint32_t bitmap,
+                       int bits_gx, int bits_gw, int mode, uint32_t* stats, int8_t* dst_gx,
+                       int64_t ld_gx, int8_t* dst_gw, int64_t ld_gw, float* scale_gx,
+                       float* scale_gw, void* stream) {
+  if (!do_gx && !do_gw) return fail(HLQ_ERR_PARAMETER, "transform pass with neither operand");
+  if (mode != 0 && mode != 1) return fail(HLQ_ERR_PARAMETER, "mode must be 0 (stats) or 1 (quant)");
+  HLQ_TRY(check_bits(bits_gx));
+  HLQ_TRY(proj_rows_checked(src, dtype, segs, rows, cols, ld_src, seg_src, do_gw ? bitmap : 0xFFFF,
+                            bits_gw, mode == 1 && do_gw ? dst_gw : nullptr, ld_gw));
+  if (do_gx && mode == 1) {
+    HLQ_TRY(check_ld16(ld_gx, "gx codes"));
+    if (ld_gx < pad16(cols)) return fail(HLQ_ERR_DIMENSION, "gx codes ld < pad16(cols)");
+  }
+  hlq::TransformArgs t = proj_args(src, dtype, segs, rows, cols, ld_src, seg_src, bitmap, bits_gw,
+                                   stats, dst_gw, ld_gw, scale_gw);
+  t.do_gx = do_gx != 0; t.do_gw = do_gw != 0; t.bits_gx = bits_gx; t.dst_gx = dst_gx;
+  t.ld_gx = ld_gx; t.scale_gx = scale_gx;
+  hlq::launch_transform(t, mode, static_cast<cudaStream_t>(stream));
+  return cuda_status("hlq_transform_pass");
+}
+
 int hlq_quantize_dual(const void* src, int dtype, int64_t segs, int64_t rows, int64_t cols,
                       int64_t ld_src, int64_t seg_src, uint32_t bitmap, int bits_gx, int bits_gw,
                       uint32_t* stats_ws, int8_t* dst_gx, int64_t ld_gx, int8_t* dst_gw,

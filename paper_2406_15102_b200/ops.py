@@ -145,6 +145,21 @@ def quant_dual(src: torch.Tensor, segs: int, rows: int, cols: int, bitmap: int, 
     return cgx, scales[0:1], cgw, k, scales[1:2], stats
 
 
+def transform_pass(src: torch.Tensor, segs: int, rows: int, cols: int, ld_src: int, seg_src: int,
+                   do_gx: bool, do_gw: bool, bitmap: int, bits_gx: int, bits_gw: int, mode: int,
+                   stats: torch.Tensor, dst_gx=None, dst_gw=None, scale_gx=None, scale_gw=None):
+    """One STATS (mode 0) or QUANT (mode 1) pass of the general transform
+    (hlq_transform_pass); stats is a 4-word int32 tensor (see new_stats)."""
+    src = _cuda(src, "src")
+    nbytes = segs * rows * cols * src.element_size()
+    _traced("transform", nbytes, 0, 1,
+            lambda: _lib.call("hlq_transform_pass", _p(src), dtype_code(src), segs, rows, cols, ld_src,
+                              seg_src, int(do_gx), int(do_gw), bitmap, bits_gx, bits_gw, mode,
+                              _p(stats), _p(dst_gx), 0 if dst_gx is None else dst_gx.stride(0),
+                              _p(dst_gw), 0 if dst_gw is None else dst_gw.stride(0), _p(scale_gx),
+                              _p(scale_gw), _stream()))
+
+
 def proj_rows_k(segs: int, rows: int, rank: int) -> int:
     return segs * ((rows + 15) // 16) * rank
 
