@@ -13,6 +13,9 @@ GOLDEN = os.path.join(ROOT, "tests", "golden")
 def pytest_configure(config):
     config.addinivalue_line("markers", "gpu: needs a CUDA device (B200, sm_100a)")
     config.addinivalue_line("markers", "slow: long-running CPU test")
+    # (re)build libhlq_b200.so in-tree if any CUDA source is newer than it
+    from paper_2406_15102_b200 import build
+    build.build()
 
 
 @pytest.fixture(scope="session")
