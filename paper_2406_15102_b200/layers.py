@@ -38,30 +38,61 @@ def _blv(shape):
     return shape[0], L, shape[-1]
 
 
+_SIDE = {}
+
+
+def side_stream(device) -> torch.cuda.Stream:
+    """Per-device auxiliary stream: the memory-bound HLQ work overlaps the
+    compute-bound forward GEMM / the other backward GEMM on it."""
+    key = torch.device(device).index
+    if key not in _SIDE:
+        _SIDE[key] = torch.cuda.Stream(device=device)
+    return _SIDE[key]
+
+
 class HLQLinearFunction(torch.autograd.Function):
-    """y = x W^T + b forward; HLQ backward (ACBP payload saved, raw x dropped)."""
+    """y = x W^T + b forward; HLQ backward (ACBP payload saved, raw x dropped).
+
+    Forward enqueues ACBP(X) and the W codes of the dX product on a side
+    stream so they run under the cuBLAS forward GEMM; W codes taken at forward
+    time are the codes of the W the backward differentiates (an in-place
+    update in between trips autograd's version check on the saved weight)."""
 
     @staticmethod
     def forward(ctx, x, weight, bias, strategy: BackwardStrategy):
-        y = F.linear(x, weight.to(x.dtype) if x.dtype != weight.dtype else weight,
-                     None if bias is None else bias.to(x.dtype))
         B, L, I = _blv(x.shape)
+        O = weight.shape[0]
         plan = strategy.plan
         bits_gw = strategy.grad_weight_path.bits or 8
+        bits_gx = strategy.grad_input_path.bits or 4
         axis = ht_axis_for(B, L, plan.block_size, strategy.pad_small_axes)
         segs, rows, cols, ld_src, seg_src = _proj_view(B, L, I, axis)
-        if ctx.needs_input_grad[1]:
-            payload, k, sx, _ = ops.quant_proj_rows(x.detach().contiguous(), segs, rows, cols,
-                                                    plan.gpu_bitmap(), bits_gw, ld_src, seg_src)
-        else:
-            payload, k, sx = None, 0, None
-        ctx.save_for_backward(weight, payload, sx)
+        main = torch.cuda.current_stream()
+        side = side_stream(x.device)
+        side.wait_stream(main)
+        payload = sx = cw = sw = None
+        k = 0
+        with torch.cuda.stream(side):
+            if ctx.needs_input_grad[1]:
+                payload, k, sx, _ = ops.quant_proj_rows(x.detach().contiguous(), segs, rows, cols,
+                                                        plan.gpu_bitmap(), bits_gw, ld_src, seg_src)
+            if ctx.needs_input_grad[0]:
+                w32 = weight.detach() if weight.dtype == torch.float32 else weight.detach().float()
+                cw, _, sw, _ = ops.quant_proj_rows(w32, 1, O, I, 0xFFFF, bits_gx)
+        y = F.linear(x, weight.to(x.dtype) if x.dtype != weight.dtype else weight,
+                     None if bias is None else bias.to(x.dtype))
+        main.wait_stream(side)
+        for t in (payload, sx, cw, sw):
+            if t is not None:
+                t.record_stream(main)
+        x.record_stream(side)
+        ctx.save_for_backward(weight, payload, sx, cw, sw)
         ctx.meta = (B, L, I, axis, k, x.dtype, tuple(x.shape), bias is not None, strategy)
         return y
 
     @staticmethod
     def backward(ctx, gy):
-        weight, payload, sx = ctx.saved_tensors
+        weight, payload, sx, cw_saved, sw_saved = ctx.saved_tensors
         B, L, I, axis, k, x_dtype, x_shape, has_bias, strategy = ctx.meta
         O = weight.shape[0]
         gy3 = gy.reshape(B, L, O)
@@ -78,11 +109,19 @@ class HLQLinearFunction(torch.autograd.Function):
             cgx, sgx, cg, kg, sg, _ = ops.quant_dual(gy3, segs, rows, cols,
                                                      strategy.plan.gpu_bitmap(), bits_gx, bits_gw,
                                                      ld_src, seg_src)
-            w32 = weight.detach() if weight.dtype == torch.float32 else weight.detach().float()
-            cw, _, sw, _ = ops.quant_proj_rows(w32, 1, O, I, 0xFFFF, bits_gx)
-            gw, _ = ops.gemm_i8(cg, payload, O, I, k, bits_gw, bits_gw, sg, sx, 1.0, exact=False)
+            cw, sw = cw_saved, sw_saved
+            # the two products are independent: dW on the side stream, dX here
+            main = torch.cuda.current_stream()
+            side = side_stream(gy.device)
+            side.wait_stream(main)
+            with torch.cuda.stream(side):
+                gw, _ = ops.gemm_i8(cg, payload, O, I, k, bits_gw, bits_gw, sg, sx, 1.0, exact=False)
             gx, _ = ops.gemm_i8(cgx, cw, B * L, I, ops.pad16(O), bits_gx, bits_gx, sgx, sw, 1.0,
                                 exact=False, out_dtype=out_dtype)
+            main.wait_stream(side)
+            gw.record_stream(main)
+            for t in (cg, sg, payload, sx):
+                t.record_stream(side)
             if weight.dtype != torch.float32:
                 gw = gw.to(weight.dtype)
             gx = gx.reshape(x_shape).to(x_dtype)
@@ -103,8 +142,7 @@ class HLQLinearFunction(torch.autograd.Function):
         if ctx.needs_input_grad[0]:
             bits = strategy.grad_input_path.bits or 4
             cgx, sgx, _ = ops.quant_ht_cols(gy3.reshape(B * L, O), bits)
-            w32 = weight.detach() if weight.dtype == torch.float32 else weight.detach().float()
-            cw, _, sw, _ = ops.quant_proj_rows(w32, 1, O, I, 0xFFFF, bits)
+            cw, sw = cw_saved, sw_saved
             out_dtype = x_dtype if x_dtype in (torch.float32, torch.bfloat16) else torch.float32
             gx, _ = ops.gemm_i8(cgx, cw, B * L, I, ops.pad16(O), bits, bits, sgx, sw, 1.0,
                                 exact=False, out_dtype=out_dtype)
