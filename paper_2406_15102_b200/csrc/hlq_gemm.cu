@@ -160,7 +160,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         const int mb = t / num_n, nb = t - mb * num_n;
         int g = 0, kg = 0;
         for (int kb = 0; kb < nk; ++kb) {
-          ptx::mbar_wait(&empty[stage], phase ^ 1);
+          ptx::mbar_wait_sleep(&empty[stage], phase ^ 1);
           ptx::mbar_arrive_expect_tx(&full[stage], Cfg::kStageBytes);
           ptx::tma_load_3d(sA + stage * Cfg::kABytes, &map_a, &full[stage], kg * kBK, mb * kBM, g);
           ptx::tma_load_3d(sB + stage * Cfg::kBBytes, &map_b, &full[stage], kg * kBK, nb * BN, g);
@@ -176,7 +176,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     int acc = 0;
     uint32_t acc_phase = 0;
     for (int t = blockIdx.x; t < tiles; t += gridDim.x) {
-      ptx::mbar_wait(&tempty[acc], acc_phase ^ 1);
+      ptx::mbar_wait_sleep(&tempty[acc], acc_phase ^ 1);
       ptx::tc_fence_after();
       const uint32_t d_tmem = tmem_base + uint32_t(acc * BN);
       for (int kb = 0; kb < nk; ++kb) {
@@ -209,7 +209,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     uint32_t acc_phase = 0;
     for (int t = blockIdx.x; t < tiles; t += gridDim.x) {
       const int mb = t / num_n, nb = t - mb * num_n;
-      ptx::mbar_wait(&tfull[acc], acc_phase);
+      ptx::mbar_wait_sleep(&tfull[acc], acc_phase);
       ptx::tc_fence_after();
       const int64_t row = int64_t(mb) * kBM + quarter * 32 + lane;
 #pragma unroll 1

@@ -115,11 +115,11 @@ struct StepIter {
 
 // 16 elements of one row piece from the staged tile -> fp32
 template <typename T>
-__device__ __forceinline__ void read16(const uint8_t* p, float (&v)[16]) {
+__device__ __forceinline__ void read16(uint32_t p, float (&v)[16]) {
   if (sizeof(T) == 2) {
 #pragma unroll
     for (int q = 0; q < 2; ++q) {
-      const uint4 t = *reinterpret_cast<const uint4*>(p + 16 * q);
+      const uint4 t = ptx::lds128(p + 16 * q);
       const uint32_t w[4] = {t.x, t.y, t.z, t.w};
 #pragma unroll
       for (int k = 0; k < 4; ++k) { v[8 * q + 2 * k] = bf_lo(w[k]); v[8 * q + 2 * k + 1] = bf_hi(w[k]); }
@@ -127,8 +127,9 @@ __device__ __forceinline__ void read16(const uint8_t* p, float (&v)[16]) {
   } else {
 #pragma unroll
     for (int q = 0; q < 4; ++q) {
-      const float4 t = *reinterpret_cast<const float4*>(p + 16 * q);
-      v[4 * q] = t.x; v[4 * q + 1] = t.y; v[4 * q + 2] = t.z; v[4 * q + 3] = t.w;
+      const uint4 t = ptx::lds128(p + 16 * q);
+      v[4 * q] = __uint_as_float(t.x); v[4 * q + 1] = __uint_as_float(t.y);
+      v[4 * q + 2] = __uint_as_float(t.z); v[4 * q + 3] = __uint_as_float(t.w);
     }
   }
 }
@@ -149,7 +150,7 @@ __device__ __forceinline__ void consume(const Args& a, const Quant& qx, const Qu
   uint32_t phase = 0;
   while (it.item < a.items) {
     ptx::mbar_wait(&full[slot], phase);
-    const uint8_t* tile = tiles + slot * (16 * kRow);
+    const uint32_t tile = ptx::smem_u32(tiles) + slot * (16 * kRow);
     const int rvalid = a.rows - it.blk * 16;  // rows of this block inside the segment
     // ---------------- phase 1: (row, 16-col block) pieces -> gx operand
     if (GX) {
@@ -185,10 +186,11 @@ __device__ __forceinline__ void consume(const Args& a, const Quant& qx, const Qu
 #pragma unroll
         for (int i = 0; i < 16; ++i) {
           if (sizeof(T) == 2) {
-            const uint32_t w = *reinterpret_cast<const uint32_t*>(tile + i * kRow + 2 * c);
+            const uint32_t w = ptx::lds32(tile + i * kRow + 2 * c);
             pv[i] = make_float2(bf_lo(w), bf_hi(w));
           } else {
-            pv[i] = *reinterpret_cast<const float2*>(tile + i * kRow + 4 * c);
+            const uint2 w = ptx::lds64(tile + i * kRow + 4 * c);
+            pv[i] = make_float2(__uint_as_float(w.x), __uint_as_float(w.y));
           }
         }
         fwht16_pair(pv);
@@ -276,10 +278,13 @@ __global__ void __launch_bounds__(kThreads) tma_tile_kernel(const __grid_constan
                                                            Args a) {
   constexpr int kRow = Tr<T>::kRow;
   extern __shared__ __align__(128) uint8_t smem_raw[];
-  uint8_t* tiles = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 127) & ~uintptr_t(127));
+  // pointer arithmetic only (no integer round trip) so the compiler keeps the
+  // shared address space and emits LDS/STS rather than generic LD/ST
+  uint8_t* tiles = smem_raw + ((128u - (ptx::smem_u32(smem_raw) & 127u)) & 127u);
   uint8_t* cbuf = tiles + kStages * 16 * kRow;
-  uint64_t* full = reinterpret_cast<uint64_t*>(cbuf + (GW && MODE == kQuant ? kCols * a.cstride : 0));
-  full = reinterpret_cast<uint64_t*>((reinterpret_cast<uintptr_t>(full) + 7) & ~uintptr_t(7));
+  uint8_t* bars = cbuf + (GW && MODE == kQuant ? kCols * a.cstride : 0);
+  bars += (8u - (ptx::smem_u32(bars) & 7u)) & 7u;
+  uint64_t* full = reinterpret_cast<uint64_t*>(bars);
   uint64_t* empty = full + kStages;
 
   const int warp = threadIdx.x >> 5;
@@ -302,7 +307,7 @@ __global__ void __launch_bounds__(kThreads) tma_tile_kernel(const __grid_constan
       int slot = 0;
       uint32_t phase = 0;
       while (it.item < a.items) {
-        ptx::mbar_wait(&empty[slot], phase ^ 1);
+        ptx::mbar_wait_sleep(&empty[slot], phase ^ 1);
         ptx::mbar_arrive_expect_tx(&full[slot], 16 * kRow);
         ptx::tma_load_3d(tiles + slot * 16 * kRow, &map, &full[slot], it.col0, it.blk * 16, it.s);
         if (++slot == kStages) { slot = 0; phase ^= 1; }
