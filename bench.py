@@ -351,11 +351,17 @@ def run_ours(args):
 
     train_steps(torch, model, opt, x, y, args.warmup)
     launches0 = ops.LAUNCHES[0]
-    with ClockSampler(local) as clk, ops.trace() as tr:
+    with ClockSampler(local) as clk:
         ms = timed(torch, dist, lambda: train_steps(torch, model, opt, x, y, args.steps))
     launches = ops.LAUNCHES[0] - launches0
-    kern = tr.summary()
     ms_step = ms / args.steps
+    # kernel breakdown for the roofline: a separate pass of the same step with a
+    # CUDA event pair around every libhlq call on its launching stream (the
+    # events perturb the step, so the headline number above is taken untraced)
+    tr_steps = max(1, min(args.steps, 3))
+    with ops.trace() as tr:
+        ms_tr = timed(torch, dist, lambda: train_steps(torch, model, opt, x, y, tr_steps))
+    kern = tr.summary()
     value = world * B * args.steps / (ms * 1e-3)
 
     # end to end: images + labels from pinned host memory every step, loss read back
@@ -380,7 +386,7 @@ def run_ours(args):
                     "unit": "GB/s", "frac": round(ach / peaks["hbm_gbs"], 4),
                     "traffic": None, "peak_source": peaks["source"],
                     "per_launch_us": round(d["us"] / d["calls"], 2), "calls": d["calls"],
-                    "share_of_step": round(d["us"] / (ms * 1e3), 4)}
+                    "share_of_step": round(d["us"] / (ms_tr * 1e3), 4)}
         else:
             d = kern["gemm"]
             ach = d["ops"] / (d["us"] * 1e-6) / 1e12
@@ -389,8 +395,8 @@ def run_ours(args):
                     "unit": "TFLOP/s", "frac": round(ach / int8_peak, 4), "traffic": None,
                     "peak_source": "int8 ops/s of cuBLASLt torch._int_mm 8192^3, measured in this run",
                     "per_launch_us": round(d["us"] / d["calls"], 2), "calls": d["calls"],
-                    "share_of_step": round(d["us"] / (ms * 1e3), 4)}
-        roof["kernels"] = {k: {"us_per_step": round(v["us"] / args.steps, 1), "calls": v["calls"]}
+                    "share_of_step": round(d["us"] / (ms_tr * 1e3), 4)}
+        roof["kernels"] = {k: {"us_per_step": round(v["us"] / tr_steps, 1), "calls": v["calls"]}
                            for k, v in kern.items()}
         line = {
             "metric": METRIC, "value": round(value, 2), "unit": "img/s", "n_gpus": world,

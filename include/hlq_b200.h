@@ -36,6 +36,10 @@
 #define HLQ_API
 #endif
 
+/* Device scratch the single-call quantizers need for their statistics and the
+ * fused kernel's grid barrier (zeroed by the library on the caller's stream). */
+#define HLQ_STATS_WS_BYTES 32
+
 #ifdef __cplusplus
 extern "C" {
 #endif
@@ -71,8 +75,8 @@ HLQ_API int hlq_device_ok(void);
  * Replaces `_block_axis(gy, 2, plan)` + `quant_pseudo_stochastic` on the gx
  * left operand (backprop.py:212-220,362,367; quantize.py:128-145).
  * Writes codes (rows x pad16(cols), leading dim ld_dst >= pad16(cols), a
- * multiple of 16) and the fp32 scale.  stats_ws: 16-byte (4 x uint32) device
- * scratch; on return stats_ws[0] holds the bits of max|4v| (>= 0x7F800000
+ * multiple of 16) and the fp32 scale.  stats_ws: HLQ_STATS_WS_BYTES (32-byte,
+ * 8 x uint32) device scratch; on return stats_ws[0] holds the bits of max|4v| (>= 0x7F800000
  * means a NaN/Inf was present, the reference's ValueError).  bits in {4, 8}. */
 HLQ_API int hlq_quantize_ht_cols(const void* src, int dtype, int64_t rows, int64_t cols, int64_t ld_src,
                          int bits, uint32_t* stats_ws, int8_t* dst, int64_t ld_dst,
@@ -83,7 +87,7 @@ HLQ_API int hlq_quantize_ht_cols(const void* src, int dtype, int64_t rows, int64
  * src is `segs` segments of (rows x cols) with row stride ld_src and segment
  * stride seg_src.  Replaces `_project_axis` + `quant_pseudo_stochastic`
  * (backprop.py:223-234; acbp_compress :373-385; hlq_grad_weight :401-407) and,
- * with bitmap 0xFFFF, `_block_axis(w, 0, plan)` (:363).  stats_ws: 16-byte
+ * with bitmap 0xFFFF, `_block_axis(w, 0, plan)` (:363).  stats_ws: 32-byte
  * scratch, the amax bits land in stats_ws[2]. */
 HLQ_API int hlq_quantize_proj_rows(const void* src, int dtype, int64_t segs, int64_t rows, int64_t cols,
                            int64_t ld_src, int64_t seg_src, uint32_t bitmap, int bits,
@@ -95,7 +99,7 @@ HLQ_API int hlq_quantize_proj_rows(const void* src, int dtype, int64_t segs, int
  * the gw codes Q_bits_gw(projection along rows) exactly as
  * hlq_quantize_proj_rows, over the same (segs x rows x cols) view.  Valid when
  * the token axis is the projection axis (reference axis rule L >= 16, or
- * L == 1 with projection along the batch).  stats_ws: 16 bytes. */
+ * L == 1 with projection along the batch).  stats_ws: 32 bytes. */
 HLQ_API int hlq_quantize_dual(const void* src, int dtype, int64_t segs, int64_t rows, int64_t cols,
                               int64_t ld_src, int64_t seg_src, uint32_t bitmap, int bits_gx,
                               int bits_gw, uint32_t* stats_ws, int8_t* dst_gx, int64_t ld_gx,
@@ -151,6 +155,22 @@ HLQ_API int hlq_gemm_i8_grouped(const int8_t* A, int64_t lda, int64_t a_gstride,
                         double extra, int epilogue, void* out, int out_dtype, int64_t ldo,
                         int32_t* acc_out, int64_t ld_acc, void* stream);
 
+/* Split-K form of hlq_gemm_i8_grouped for products with few output tiles
+ * and a long contraction (the dW GEMM: M = O, N = I, K = projected tokens).
+ * ws (device, caller-allocated, no initialisation needed) of at least
+ * hlq_gemm_i8_ws(M, N, K, groups) bytes lets the kernel split K across CTAs;
+ * the per-split int32 partial tiles are summed in-kernel (exact) before the
+ * same dequant epilogue.  ws == NULL or too small runs unsplit.  Same
+ * contract and results as hlq_gemm_i8_grouped (int_matmul_dequant,
+ * quantize.py:152-187). */
+HLQ_API size_t hlq_gemm_i8_ws(int64_t M, int64_t N, int64_t K, int64_t groups);
+HLQ_API int hlq_gemm_i8_ex(const int8_t* A, int64_t lda, int64_t a_gstride, const int8_t* B,
+                           int64_t ldb, int64_t b_gstride, int64_t M, int64_t N, int64_t K,
+                           int64_t groups, int bits_a, int bits_b, const float* sa, const float* sb,
+                           double extra, int epilogue, void* out, int out_dtype, int64_t ldo,
+                           int32_t* acc_out, int64_t ld_acc, void* ws, size_t ws_bytes,
+                           void* stream);
+
 /* ---------------------------------------------------------------------------
  * Reference-function equivalents (whole calls)
  * ------------------------------------------------------------------------- */
@@ -165,7 +185,7 @@ HLQ_API int64_t hlq_acbp_rows(int64_t L, int64_t I, int axis);
 /* backprop.py:373-385  acbp_compress(x, plan, bits, pad_small_axes).
  * x is (B, L, I); axis from ht_axis_for (0 = batch, 1 = tokens).  Payload is
  * written K-major, payload[row * ld_payload + k] (the reference's (K, I)
- * payload, transposed; see hlq_acbp_k).  stats_ws: 16-byte scratch. */
+ * payload, transposed; see hlq_acbp_k).  stats_ws: 32-byte scratch. */
 HLQ_API int hlq_acbp_compress(const void* x, int dtype, int64_t B, int64_t L, int64_t I, int axis,
                       uint32_t bitmap, int bits, int8_t* payload, int64_t ld_payload,
                       float* scale_out, uint32_t* stats_ws, void* stream);

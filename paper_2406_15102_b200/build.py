@@ -49,24 +49,35 @@ def _stale() -> bool:
 def build(force: bool = False, verbose: bool = False) -> str:
     if not force and not _stale():
         return LIB
-    objs = []
+    # translation units compile in parallel; objects are kept (git-ignored) so a
+    # rebuild only recompiles sources newer than their object or any header
+    objdir = os.path.join(HERE, "build")
+    os.makedirs(objdir, exist_ok=True)
+    hdr_t = max(os.path.getmtime(os.path.join(CSRC, h)) for h in HEADERS
+                if os.path.exists(os.path.join(CSRC, h)))
+    hdr_t = max(hdr_t, os.path.getmtime(__file__))
+    objs, procs = [], []
     for src in SOURCES:
-        obj = os.path.join(CSRC, src.replace(".cu", ".o"))
-        cmd = [nvcc(), *NVCC_FLAGS, "-I", os.path.join(ROOT, "include"), "-c",
-               os.path.join(CSRC, src), "-o", obj]
+        obj = os.path.join(objdir, src.replace(".cu", ".o"))
+        objs.append(obj)
+        srcp = os.path.join(CSRC, src)
+        if (not force and os.path.exists(obj) and os.path.getmtime(obj) > os.path.getmtime(srcp)
+                and os.path.getmtime(obj) > hdr_t):
+            continue
+        cmd = [nvcc(), *NVCC_FLAGS, "-I", os.path.join(ROOT, "include"), "-c", srcp, "-o", obj]
         if verbose:
             cmd.insert(1, "-Xptxas=-v")
             print(" ".join(cmd))
-        subprocess.run(cmd, check=True)
-        objs.append(obj)
+        procs.append((src, subprocess.Popen(cmd)))
+    for src, p in procs:
+        if p.wait() != 0:
+            raise subprocess.CalledProcessError(p.returncode, f"nvcc {src}")
     # the driver API (cuTensorMapEncodeTiled) is resolved at run time through
     # cudaGetDriverEntryPoint, so there is no link-time libcuda dependency
     cmd = [nvcc(), *NVCC_FLAGS, "-shared", *objs, "-o", LIB]
     if verbose:
         print(" ".join(cmd))
     subprocess.run(cmd, check=True)
-    for o in objs:
-        os.remove(o)
     return LIB
 
 

@@ -135,9 +135,8 @@ int hlq_quantize_ht_cols(const void* src, int dtype, int64_t rows, int64_t cols,
   t.seg_src = rows * ld_src; t.do_gx = true; t.do_gw = false; t.bitmap = 0xFFFF;
   t.bits_gx = bits; t.bits_gw = bits; t.stats = stats_ws; t.dst_gx = dst; t.ld_gx = ld_dst;
   t.scale_gx = scale_out;
-  cudaMemsetAsync(stats_ws, 0, 4 * sizeof(uint32_t), st);
-  hlq::launch_transform(t, hlq::kStats, st);
-  hlq::launch_transform(t, hlq::kQuant, st);
+  cudaMemsetAsync(stats_ws, 0, HLQ_STATS_WS_BYTES, st);
+  hlq::launch_transform(t, hlq::kBoth, st);
   return cuda_status("hlq_quantize_ht_cols");
 }
 
@@ -181,9 +180,8 @@ int hlq_quantize_proj_rows(const void* src, int dtype, int64_t segs, int64_t row
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   const hlq::TransformArgs t = proj_args(src, dtype, segs, rows, cols, ld_src, seg_src, bitmap, bits,
                                          stats_ws, dst, ld_dst, scale_out);
-  cudaMemsetAsync(stats_ws, 0, 4 * sizeof(uint32_t), st);
-  hlq::launch_transform(t, hlq::kStats, st);
-  hlq::launch_transform(t, hlq::kQuant, st);
+  cudaMemsetAsync(stats_ws, 0, HLQ_STATS_WS_BYTES, st);
+  hlq::launch_transform(t, hlq::kBoth, st);
   return cuda_status("hlq_quantize_proj_rows");
 }
 
@@ -222,9 +220,8 @@ int hlq_quantize_dual(const void* src, int dtype, int64_t segs, int64_t rows, in
   hlq::TransformArgs t = proj_args(src, dtype, segs, rows, cols, ld_src, seg_src, bitmap, bits_gw,
                                    stats_ws, dst_gw, ld_gw, scale_gw);
   t.do_gx = true; t.bits_gx = bits_gx; t.dst_gx = dst_gx; t.ld_gx = ld_gx; t.scale_gx = scale_gx;
-  cudaMemsetAsync(stats_ws, 0, 4 * sizeof(uint32_t), st);
-  hlq::launch_transform(t, hlq::kStats, st);
-  hlq::launch_transform(t, hlq::kQuant, st);
+  cudaMemsetAsync(stats_ws, 0, HLQ_STATS_WS_BYTES, st);
+  hlq::launch_transform(t, hlq::kBoth, st);
   return cuda_status("hlq_quantize_dual");
 }
 
@@ -241,6 +238,20 @@ int hlq_gemm_i8_grouped(const int8_t* A, int64_t lda, int64_t a_gstride, const i
                         int64_t groups, int bits_a, int bits_b, const float* sa, const float* sb,
                         double extra, int epilogue, void* out, int out_dtype, int64_t ldo,
                         int32_t* acc_out, int64_t ld_acc, void* stream) {
+  return hlq_gemm_i8_ex(A, lda, a_gstride, B, ldb, b_gstride, M, N, K, groups, bits_a, bits_b, sa, sb,
+                        extra, epilogue, out, out_dtype, ldo, acc_out, ld_acc, nullptr, 0, stream);
+}
+
+size_t hlq_gemm_i8_ws(int64_t M, int64_t N, int64_t K, int64_t groups) {
+  if (M <= 0 || N <= 0 || K <= 0 || groups < 1) return 0;
+  return hlq::gemm_i8_ws_bytes(M, N, K, groups);
+}
+
+int hlq_gemm_i8_ex(const int8_t* A, int64_t lda, int64_t a_gstride, const int8_t* B, int64_t ldb,
+                   int64_t b_gstride, int64_t M, int64_t N, int64_t K, int64_t groups, int bits_a,
+                   int bits_b, const float* sa, const float* sb, double extra, int epilogue, void* out,
+                   int out_dtype, int64_t ldo, int32_t* acc_out, int64_t ld_acc, void* ws,
+                   size_t ws_bytes, void* stream) {
   if (groups < 1 || groups > 65535 || (groups > 1 && (a_gstride % 16 || b_gstride % 16 ||
                                                       a_gstride < lda * M || b_gstride < ldb * N)))
     return fail(HLQ_ERR_PARAMETER, "bad K-group layout groups=%lld", (long long)groups);
@@ -263,7 +274,7 @@ int hlq_gemm_i8_grouped(const int8_t* A, int64_t lda, int64_t a_gstride, const i
     return fail(HLQ_ERR_PARAMETER, "unknown epilogue %d", epilogue);
   if (M == 0 || N == 0) return HLQ_OK;
   int e = hlq::launch_gemm_i8(A, lda, B, ldb, M, N, K, groups, a_gstride, b_gstride, sa, sb, extra,
-                              epilogue, out, out_dtype, ldo, acc_out, ld_acc,
+                              epilogue, out, out_dtype, ldo, acc_out, ld_acc, ws, ws_bytes,
                               static_cast<cudaStream_t>(stream));
   if (e == -1) return fail(HLQ_ERR_CUDA, "cuTensorMapEncodeTiled unavailable or rejected the operands");
   if (e != 0) return fail(HLQ_ERR_CUDA, "hlq_gemm_i8: %s", cudaGetErrorString(cudaError_t(e)));
@@ -346,10 +357,10 @@ int hlq_hq_grad_input(const void* gy, int gy_dtype, int64_t T, int64_t O, const 
   p += align256(size_t(T * op));
   int8_t* cw = reinterpret_cast<int8_t*>(p);
   p += align256(size_t(I * op));
-  uint32_t* stats = reinterpret_cast<uint32_t*>(p);    // [0..3] gy, [4..7] w
+  uint32_t* stats = reinterpret_cast<uint32_t*>(p);    // [0..7] gy, [8..15] w
   float* scales = reinterpret_cast<float*>(p + 64);  // [0] gy, [1] w
   HLQ_TRY(hlq_quantize_ht_cols(gy, gy_dtype, T, O, O, bits, stats, cg, op, scales, stream));
-  HLQ_TRY(hlq_quantize_proj_rows(w, HLQ_F32, 1, O, I, I, O * I, 0xFFFFu, bits, stats + 4, cw, op,
+  HLQ_TRY(hlq_quantize_proj_rows(w, HLQ_F32, 1, O, I, I, O * I, 0xFFFFu, bits, stats + 8, cw, op,
                                  scales + 1, stream));
   return hlq_gemm_i8(cg, op, cw, op, T, I, op, bits, bits, scales, scales + 1, 1.0, epilogue, dx,
                      dx_dtype, I, nullptr, 0, stream);

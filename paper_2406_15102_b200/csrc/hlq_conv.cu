@@ -131,7 +131,7 @@ __device__ __forceinline__ void im2col_body(const ConvArgs& a, const Quant& q, f
           if (MODE == kStats) {
 #pragma unroll
             for (int i = 0; i < 16; ++i)
-              if ((bitmap >> i) & 1u) { st.add(pv[i].x); st.add(pv[i].y); }
+              if ((bitmap >> i) & 1u) st.add2(pv[i].x, pv[i].y);
           } else {
             uint8_t* ox = cbuf + cc * cstride + bl * rank;
             uint8_t* oy = ox + cstride;

@@ -20,6 +20,7 @@
 #include <cuda_runtime.h>
 #include <cstdint>
 #include <cstdio>
+#include <cstdlib>
 #include <mutex>
 
 #include "hlq_internal.h"
@@ -104,12 +105,16 @@ __device__ __forceinline__ void store_row_chunk(const uint32_t (&acc)[32], int64
   }
 }
 
+// Split-K (dW: few output tiles, very long K): work unit u = tile * splits + split
+// covers K blocks [split*nk/splits, (split+1)*nk/splits) and stores its int32
+// partial tile to workspace slab `split`; splitk_finalize then sums the slabs
+// (integers: exact in any order) and runs the same dequant epilogue.
 template <int BN, int STAGES>
 __global__ void __launch_bounds__(kThreads, 1)
     gemm_i8_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant__ CUtensorMap map_b,
                    int M, int N, int K, int groups, const float* __restrict__ sa, const float* __restrict__ sb,
                    double extra, int epilogue, void* out, int out_dtype, int64_t ldo,
-                   int32_t* acc_out, int64_t ld_acc) {
+                   int32_t* acc_out, int64_t ld_acc, int splits, int32_t* __restrict__ slabs) {
   using Cfg = GemmCfg<BN, STAGES>;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
@@ -149,6 +154,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   const int num_m = (M + kBM - 1) / kBM;
   const int num_n = (N + BN - 1) / BN;
   const int tiles = num_m * num_n;
+  const int units = tiles * splits;
   const int nk_g = (K + kBK - 1) / kBK;  // K blocks per group
   const int nk = nk_g * groups;           // groups accumulate into the same tile
 
@@ -156,10 +162,12 @@ __global__ void __launch_bounds__(kThreads, 1)
     if (ptx::elect_one()) {
       int stage = 0;
       uint32_t phase = 0;
-      for (int t = blockIdx.x; t < tiles; t += gridDim.x) {
+      for (int u = blockIdx.x; u < units; u += gridDim.x) {
+        const int t = u / splits, sp = u - t * splits;
         const int mb = t / num_n, nb = t - mb * num_n;
-        int g = 0, kg = 0;
-        for (int kb = 0; kb < nk; ++kb) {
+        const int kb0 = int(int64_t(sp) * nk / splits), kb1 = int(int64_t(sp + 1) * nk / splits);
+        int g = kb0 / nk_g, kg = kb0 - g * nk_g;
+        for (int kb = kb0; kb < kb1; ++kb) {
           ptx::mbar_wait_sleep(&empty[stage], phase ^ 1);
           ptx::mbar_arrive_expect_tx(&full[stage], Cfg::kStageBytes);
           ptx::tma_load_3d(sA + stage * Cfg::kABytes, &map_a, &full[stage], kg * kBK, mb * kBM, g);
@@ -175,11 +183,13 @@ __global__ void __launch_bounds__(kThreads, 1)
     uint32_t phase = 0;
     int acc = 0;
     uint32_t acc_phase = 0;
-    for (int t = blockIdx.x; t < tiles; t += gridDim.x) {
+    for (int u = blockIdx.x; u < units; u += gridDim.x) {
+      const int sp = u % splits;
+      const int kb0 = int(int64_t(sp) * nk / splits), kb1 = int(int64_t(sp + 1) * nk / splits);
       ptx::mbar_wait_sleep(&tempty[acc], acc_phase ^ 1);
       ptx::tc_fence_after();
       const uint32_t d_tmem = tmem_base + uint32_t(acc * BN);
-      for (int kb = 0; kb < nk; ++kb) {
+      for (int kb = kb0; kb < kb1; ++kb) {
         ptx::mbar_wait(&full[stage], phase);
         ptx::tc_fence_after();
         if (ptx::elect_one()) {
@@ -189,10 +199,10 @@ __global__ void __launch_bounds__(kThreads, 1)
           for (int k = 0; k < kBK / 32; ++k) {
             // advance the start address by 32 bytes of K inside the swizzle atom
             ptx::mma_i8(d_tmem, a_desc + uint64_t((k * 32) >> 4), b_desc + uint64_t((k * 32) >> 4),
-                        idesc, (kb | k) != 0 ? 1u : 0u);
+                        idesc, (kb != kb0 || k != 0) ? 1u : 0u);
           }
           ptx::mma_commit(&empty[stage]);
-          if (kb == nk - 1) ptx::mma_commit(&tfull[acc]);
+          if (kb == kb1 - 1) ptx::mma_commit(&tfull[acc]);
         }
         __syncwarp();
         if (++stage == STAGES) { stage = 0; phase ^= 1; }
@@ -207,23 +217,52 @@ __global__ void __launch_bounds__(kThreads, 1)
     const bool vec_ok = (ldo % 8 == 0) && ((reinterpret_cast<uintptr_t>(out) & 15) == 0);
     int acc = 0;
     uint32_t acc_phase = 0;
-    for (int t = blockIdx.x; t < tiles; t += gridDim.x) {
+    for (int u = blockIdx.x; u < units; u += gridDim.x) {
+      const int t = u / splits, sp = u - t * splits;
       const int mb = t / num_n, nb = t - mb * num_n;
       ptx::mbar_wait_sleep(&tfull[acc], acc_phase);
       ptx::tc_fence_after();
-      const int64_t row = int64_t(mb) * kBM + quarter * 32 + lane;
+      const int rl = quarter * 32 + lane;  // row inside the tile
+      const int64_t row = int64_t(mb) * kBM + rl;
+      if (splits == 1) {
 #pragma unroll 1
-      for (int c = 0; c < BN / 32; ++c) {
-        const int64_t col0 = int64_t(nb) * BN + c * 32;
-        uint32_t r[32];
-        ptx::tmem_ld_32x32b_x32(tmem_base + ((quarter * 32) << 16) + uint32_t(acc * BN + c * 32), r);
-        ptx::tmem_ld_wait();
-        if (row < M && col0 < N)
-          store_row_chunk(r, row, col0, N, epilogue, dscale, fscale, out, out_dtype, ldo, vec_ok,
-                          acc_out, ld_acc);
+        for (int c = 0; c < BN / 32; ++c) {
+          const int64_t col0 = int64_t(nb) * BN + c * 32;
+          uint32_t r[32];
+          ptx::tmem_ld_32x32b_x32(tmem_base + ((quarter * 32) << 16) + uint32_t(acc * BN + c * 32), r);
+          ptx::tmem_ld_wait();
+          if (row < M && col0 < N)
+            store_row_chunk(r, row, col0, N, epilogue, dscale, fscale, out, out_dtype, ldo, vec_ok,
+                            acc_out, ld_acc);
+        }
+        ptx::tc_fence_before();
+        ptx::mbar_arrive(&tempty[acc]);
+      } else {
+        // partial tile -> slab sp (row-major M x N int32); summed by splitk_finalize
+        int32_t* slab = slabs + int64_t(sp) * M * N;
+#pragma unroll 1
+        for (int c = 0; c < BN / 32; ++c) {
+          const int64_t col0 = int64_t(nb) * BN + c * 32;
+          uint32_t r[32];
+          ptx::tmem_ld_32x32b_x32(tmem_base + ((quarter * 32) << 16) + uint32_t(acc * BN + c * 32), r);
+          ptx::tmem_ld_wait();
+          if (row < M && col0 < N) {
+            int32_t* d = slab + row * N + col0;
+            if (col0 + 32 <= N && (N & 3) == 0) {
+#pragma unroll
+              for (int j = 0; j < 32; j += 4)
+                __stcg(reinterpret_cast<int4*>(d + j),
+                       make_int4(int(r[j]), int(r[j + 1]), int(r[j + 2]), int(r[j + 3])));
+            } else {
+#pragma unroll
+              for (int j = 0; j < 32; ++j)
+                if (col0 + j < N) d[j] = int(r[j]);
+            }
+          }
+        }
+        ptx::tc_fence_before();
+        ptx::mbar_arrive(&tempty[acc]);
       }
-      ptx::tc_fence_before();
-      ptx::mbar_arrive(&tempty[acc]);
       if (++acc == 2) { acc = 0; acc_phase ^= 1; }
     }
   }
@@ -232,6 +271,45 @@ __global__ void __launch_bounds__(kThreads, 1)
   __syncthreads();
   ptx::tc_fence_after();
   if (warp == 2) ptx::tmem_dealloc(tmem_base, Cfg::kTmemCols);
+}
+
+// out[m, n] = dequant(sum_s slab[s][m, n]) (+ the exact int32 sum into acc_out).
+__global__ void __launch_bounds__(256) splitk_finalize(const int32_t* __restrict__ slabs, int splits,
+                                                       int M, int N, const float* __restrict__ sa,
+                                                       const float* __restrict__ sb, double extra,
+                                                       int epilogue, void* out, int out_dtype, int64_t ldo,
+                                                       int32_t* acc_out, int64_t ld_acc) {
+  const float comb = __fmul_rn(*sa, *sb);
+  const double dscale = __dmul_rn(double(comb), extra);
+  const float fscale = float(dscale);
+  const int64_t plane = int64_t(M) * N;
+  const int64_t nq = plane >> 2;  // N % 4 == 0 is required by the launcher
+  for (int64_t q = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; q < nq; q += int64_t(gridDim.x) * blockDim.x) {
+    int4 t = __ldcs(reinterpret_cast<const int4*>(slabs) + q);
+    for (int s = 1; s < splits; ++s) {
+      const int4 v = __ldcs(reinterpret_cast<const int4*>(slabs + s * plane) + q);
+      t.x += v.x; t.y += v.y; t.z += v.z; t.w += v.w;
+    }
+    const int64_t e = q << 2;
+    const int64_t m = e / N, n = e - m * N;
+    const int a[4] = {t.x, t.y, t.z, t.w};
+    if (acc_out) *reinterpret_cast<int4*>(acc_out + m * ld_acc + n) = t;
+    if (!out) continue;
+    float v[4];
+#pragma unroll
+    for (int j = 0; j < 4; ++j)
+      v[j] = epilogue == kEpiExact ? __double2float_rn(__dmul_rn(double(a[j]), dscale))
+                                   : __fmul_rn(__int2float_rn(a[j]), fscale);
+    if (out_dtype == kF32) {
+      *reinterpret_cast<float4*>(static_cast<float*>(out) + m * ldo + n) = make_float4(v[0], v[1], v[2], v[3]);
+    } else {
+      __nv_bfloat162 p0 = __floats2bfloat162_rn(v[0], v[1]), p1 = __floats2bfloat162_rn(v[2], v[3]);
+      uint2 w;
+      w.x = *reinterpret_cast<uint32_t*>(&p0);
+      w.y = *reinterpret_cast<uint32_t*>(&p1);
+      *reinterpret_cast<uint2*>(static_cast<__nv_bfloat16*>(out) + m * ldo + n) = w;
+    }
+  }
 }
 
 // ---------------------------------------------------------------- host side
@@ -297,7 +375,7 @@ namespace {
 template <int BN, int STAGES>
 int run(const int8_t* A, int64_t lda, const int8_t* B, int64_t ldb, int64_t M, int64_t N, int64_t K,
         int64_t groups, int64_t a_gstride, int64_t b_gstride, const float* sa, const float* sb, double extra, int epilogue, void* out, int out_dtype,
-        int64_t ldo, int32_t* acc_out, int64_t ld_acc, cudaStream_t stream) {
+        int64_t ldo, int32_t* acc_out, int64_t ld_acc, int splits, void* ws, cudaStream_t stream) {
   using Cfg = GemmCfg<BN, STAGES>;
   CUtensorMap ma, mb;
   if (!make_map(&ma, A, M, K, lda, groups, a_gstride, kBM) ||
@@ -311,27 +389,84 @@ int run(const int8_t* A, int64_t lda, const int8_t* B, int64_t ldb, int64_t M, i
     attr_set = true;
   }
   const int64_t tiles = ((M + kBM - 1) / kBM) * ((N + BN - 1) / BN);
-  const int grid = int(tiles < num_sms() ? tiles : num_sms());
+  int32_t* slabs = splits > 1 ? static_cast<int32_t*>(ws) : nullptr;
+  const int64_t units = tiles * splits;
+  const int grid = int(units < num_sms() ? units : num_sms());
   gemm_i8_kernel<BN, STAGES><<<grid, kThreads, Cfg::kSmem, stream>>>(
-      ma, mb, int(M), int(N), int(K), int(groups), sa, sb, extra, epilogue, out, out_dtype, ldo, acc_out, ld_acc);
+      ma, mb, int(M), int(N), int(K), int(groups), sa, sb, extra, epilogue, out, out_dtype, ldo, acc_out, ld_acc,
+      splits, slabs);
+  if (splits > 1) {
+    const int64_t nq = M * N / 4;
+    int fgrid = int((nq + 255) / 256);
+    if (fgrid > num_sms() * 8) fgrid = num_sms() * 8;
+    splitk_finalize<<<fgrid, 256, 0, stream>>>(slabs, splits, int(M), int(N), sa, sb, extra, epilogue, out,
+                                               out_dtype, ldo, acc_out, ld_acc);
+  }
   return int(cudaGetLastError());
 }
 
+// Tile width, split count and workspace bytes for one GEMM.  Split-K only when
+// the output has too few tiles to fill the SMs and K is long (the dW products:
+// M = O, N = I, K = projected tokens).
+struct GemmPlan {
+  int bn, splits;
+  size_t ws;
+};
+
+GemmPlan plan_gemm(int64_t M, int64_t N, int64_t K, int64_t groups, bool allow_split) {
+  const int64_t m_tiles = (M + kBM - 1) / kBM;
+  const int64_t wide_tiles = m_tiles * ((N + 255) / 256);
+  const int64_t nk = ((K + kBK - 1) / kBK) * groups;
+  const int64_t sms = num_sms();
+  GemmPlan p{128, 1, 0};
+  // 128x256 tiles need 96 B/clk/SM of operand traffic vs 128 for 128x128, so
+  // prefer them, and recover parallelism with split-K when K is long
+  if (N > 128 && (wide_tiles >= sms || (allow_split && nk >= 16))) p.bn = 256;
+  const int64_t tiles = m_tiles * ((N + p.bn - 1) / p.bn);
+  // (the finalize pass reads 16-byte int32 quads: N % 4 == 0; outputs 16-byte aligned rows)
+  if (allow_split && tiles < sms && nk >= 16 && N % 4 == 0) {
+    // makespan model: waves * (K blocks per unit + epilogue/slab overhead)
+    double best = double((tiles + sms - 1) / sms) * double(nk + 2);
+    for (int s = 2; s <= 16 && nk / s >= 4; ++s) {
+      const double t = double((tiles * s + sms - 1) / sms) * (double((nk + s - 1) / s) + 2.0) + 0.5 * s;
+      if (t < 0.97 * best) { best = t; p.splits = s; }
+    }
+  }
+  // tuning knobs (development sweeps): HLQ_GEMM_SPLITS=s forces s splits (1 = off),
+  // HLQ_GEMM_BN=128|256 forces the tile width
+  if (const char* e = getenv("HLQ_GEMM_BN")) {
+    const int bn = atoi(e);
+    if (bn == 128 || (bn == 256 && N > 128)) p.bn = bn;
+  }
+  if (const char* e = getenv("HLQ_GEMM_SPLITS")) {
+    const int s = atoi(e);
+    if (s >= 1 && s <= 64 && allow_split && N % 4 == 0) p.splits = s;
+  }
+  if (p.splits > 1) p.ws = size_t(p.splits) * M * N * 4;
+  return p;
+}
+
 }  // namespace
+
+size_t gemm_i8_ws_bytes(int64_t M, int64_t N, int64_t K, int64_t groups) {
+  return plan_gemm(M, N, K, groups, true).ws;
+}
 
 int launch_gemm_i8(const int8_t* A, int64_t lda, const int8_t* B, int64_t ldb, int64_t M, int64_t N,
                    int64_t K, int64_t groups, int64_t a_gstride, int64_t b_gstride,
                    const float* sa, const float* sb, double extra, int epilogue,
                    void* out, int out_dtype, int64_t ldo, int32_t* acc_out, int64_t ld_acc,
-                   cudaStream_t stream) {
-  // Wide N tiles amortise the A stream; narrow ones keep >= ~1 wave of CTAs busy.
-  const int64_t m_tiles = (M + kBM - 1) / kBM;
-  const int64_t wide_tiles = m_tiles * ((N + 255) / 256);
-  if (N > 128 && wide_tiles >= num_sms())
-    return run<256, 4>(A, lda, B, ldb, M, N, K, groups, a_gstride, b_gstride, sa, sb, extra, epilogue, out, out_dtype, ldo,
-                       acc_out, ld_acc, stream);
-  return run<128, 6>(A, lda, B, ldb, M, N, K, groups, a_gstride, b_gstride, sa, sb, extra, epilogue, out, out_dtype, ldo, acc_out,
-                     ld_acc, stream);
+                   void* ws, size_t ws_bytes, cudaStream_t stream) {
+  GemmPlan p = plan_gemm(M, N, K, groups, true);
+  const bool vec_out = (ldo % 4 == 0) && (reinterpret_cast<uintptr_t>(out) % 16 == 0) &&
+                       (ld_acc % 4 == 0) && (reinterpret_cast<uintptr_t>(acc_out) % 16 == 0);
+  if (p.splits > 1 && (ws == nullptr || ws_bytes < p.ws || !vec_out || (reinterpret_cast<uintptr_t>(ws) % 16)))
+    p = plan_gemm(M, N, K, groups, false);
+  if (p.bn == 256)
+    return run<256, 4>(A, lda, B, ldb, M, N, K, groups, a_gstride, b_gstride, sa, sb, extra, epilogue, out,
+                       out_dtype, ldo, acc_out, ld_acc, p.splits, ws, stream);
+  return run<128, 6>(A, lda, B, ldb, M, N, K, groups, a_gstride, b_gstride, sa, sb, extra, epilogue, out,
+                     out_dtype, ldo, acc_out, ld_acc, p.splits, ws, stream);
 }
 
 }  // namespace hlq

@@ -6,7 +6,7 @@
 namespace hlq {
 
 enum : int { kF32 = 0, kBF16 = 1 };
-enum : int { kStats = 0, kQuant = 1 };
+enum : int { kStats = 0, kQuant = 1, kBoth = 2 };  // kBoth: one cooperative launch
 enum : int { kEpiExact = 0, kEpiFast = 1 };
 
 int num_sms();
@@ -16,7 +16,8 @@ int num_sms();
 // seg*rows + row).  do_gw: projection along rows keeping `bitmap`'s bases,
 // codes transposed into dst_gw[col * ld_gw + (seg * nblk + blk) * rank + j].
 // stats: {amax_gx, ~minnz_gx, amax_gw, ~minnz_gw} (uint32 bits, max-reduced;
-// zero-initialised by the caller before the STATS pass).  When only do_gw is
+// zero-initialised by the caller before the STATS pass; kBoth also uses
+// stats[4] as its grid-barrier counter, zero-initialised likewise).  When only do_gw is
 // set the gw statistics still live at stats[2..3].
 struct TransformArgs {
   const void* src;
@@ -56,6 +57,8 @@ int launch_gemm_i8(const int8_t* A, int64_t lda, const int8_t* B, int64_t ldb, i
                    int64_t K, int64_t groups, int64_t a_gstride, int64_t b_gstride,
                    const float* sa, const float* sb, double extra, int epilogue,
                    void* out, int out_dtype, int64_t ldo, int32_t* acc_out, int64_t ld_acc,
-                   cudaStream_t stream);
+                   void* ws, size_t ws_bytes, cudaStream_t stream);
+// Workspace bytes that let launch_gemm_i8 split K (0: no split planned).
+size_t gemm_i8_ws_bytes(int64_t M, int64_t N, int64_t K, int64_t groups);
 
 }  // namespace hlq

@@ -47,6 +47,13 @@ __device__ __forceinline__ float2 f2add_rp(float2 a, float2 b) {
       : "=f"(d.x), "=f"(d.y) : "f"(a.x), "f"(a.y), "f"(b.x), "f"(b.y));
   return d;
 }
+__device__ __forceinline__ float2 f2sub_rp(float2 a, float2 b) {
+  float2 d;
+  asm("{.reg .b64 ra, rb, rd;\n\tmov.b64 ra, {%2, %3};\n\tmov.b64 rb, {%4, %5};\n\t"
+      "sub.rp.f32x2 rd, ra, rb;\n\tmov.b64 {%0, %1}, rd;}"
+      : "=f"(d.x), "=f"(d.y) : "f"(a.x), "f"(a.y), "f"(b.x), "f"(b.y));
+  return d;
+}
 __device__ __forceinline__ float2 f2fma_rp(float2 a, float2 b, float2 c) {
   float2 d;
   asm("{.reg .b64 ra, rb, rc, rd;\n\tmov.b64 ra, {%2, %3};\n\tmov.b64 rb, {%4, %5};\n\t"
@@ -56,7 +63,13 @@ __device__ __forceinline__ float2 f2fma_rp(float2 a, float2 b, float2 c) {
 }
 __device__ __forceinline__ float2 f2(float a) { return make_float2(a, a); }
 
-__device__ __forceinline__ float bf_lo(uint32_t w) { return __uint_as_float(w << 16); }
+// bf16 -> fp32: both halves on the ALU pipe (PRMT / LOP3), keeping the FMA
+// pipe for the butterflies and the quantizer
+__device__ __forceinline__ float bf_lo(uint32_t w) {
+  uint32_t r;
+  asm("prmt.b32 %0, %1, 0, 0x1044;" : "=r"(r) : "r"(w));
+  return __uint_as_float(r);
+}
 __device__ __forceinline__ float bf_hi(uint32_t w) { return __uint_as_float(w & 0xFFFF0000u); }
 
 // ------------------------------------------------------------------ transforms
@@ -103,25 +116,44 @@ __device__ __forceinline__ void fwht16_pair(float2 (&p)[16]) {
 }
 
 // ------------------------------------------------------------------ statistics
+// Per-thread statistics of transformed values, two values per update, all on
+// 3-input FMNMX with |.| operand modifiers:
+//   amax  max |w| with NaN propagation (a NaN/Inf input surfaces as bits
+//         >= 0x7F800000);
+//   mnz   min over nonzero |w| of the float whose bits are bits(|w|) - 1: the
+//         decrement (an IMAD, FMA pipe) turns +-0 into a NaN pattern that the
+//         NaN-ignoring min skips, and is monotone on nonzero magnitudes.
 struct Stat {
-  uint32_t amax = 0;             // max |w| bits (NaN/Inf land >= 0x7F800000)
-  uint32_t minnz = 0xFFFFFFFFu;  // min (|w| bits - 1): the smallest nonzero magnitude
-  __device__ __forceinline__ void add(float w) {
-    const uint32_t a = __float_as_uint(w) & 0x7FFFFFFFu;
-    amax = max(amax, a);
-    minnz = min(minnz, a - 1u);
+  float amax = 0.0f;
+  float mnz = __builtin_huge_valf();  // +inf: no nonzero value seen
+  __device__ __forceinline__ static float dec(float a) {
+    uint32_t r;
+    asm("mad.lo.u32 %0, %1, %2, %3;" : "=r"(r) : "r"(__float_as_uint(a)), "r"(1u), "r"(0xFFFFFFFFu));
+    return __uint_as_float(r);
   }
+  __device__ __forceinline__ void add2(float a, float b) {
+    asm("{.reg .f32 t0, t1;\n\tabs.f32 t0, %1;\n\tabs.f32 t1, %2;\n\t"
+        "max.NaN.f32 %0, %0, t0, t1;}" : "+f"(amax) : "f"(a), "f"(b));
+    asm("{.reg .f32 t0, t1;\n\tabs.f32 t0, %1;\n\tabs.f32 t1, %2;\n\t"
+        "min.f32 %0, %0, t0, t1;}" : "+f"(mnz) : "f"(dec(a)), "f"(dec(b)));
+  }
+  __device__ __forceinline__ void add(float a) { add2(a, 0.0f); }
   __device__ __forceinline__ void warp_reduce() {
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) {
-      amax = max(amax, __shfl_xor_sync(0xffffffffu, amax, o));
-      minnz = min(minnz, __shfl_xor_sync(0xffffffffu, minnz, o));
+      const float oa = __shfl_xor_sync(0xffffffffu, amax, o);
+      asm("max.NaN.f32 %0, %0, %1;" : "+f"(amax) : "f"(oa));
+      const float om = __shfl_xor_sync(0xffffffffu, mnz, o);
+      asm("min.f32 %0, %0, %1;" : "+f"(mnz) : "f"(om));
     }
   }
-  // global layout {amax, ~minnz}, both max-reduced so a zero memset is the identity
+  // global layout {amax bits, ~(minnz bits - 1)}, both max-reduced so a zero
+  // memset is the identity (NaN from max.NaN is 0x7FFFFFFF: flagged non-finite)
   __device__ __forceinline__ void commit(uint32_t* g) const {
-    if (amax) atomicMax(g, amax);
-    if (~minnz) atomicMax(g + 1, ~minnz);
+    const uint32_t ab = __float_as_uint(amax) & 0x7FFFFFFFu;
+    if (ab) atomicMax(g, ab);
+    const uint32_t mb = __float_as_uint(mnz);
+    if (mb < 0x7F800000u) atomicMax(g + 1, ~mb);
   }
 };
 
@@ -141,7 +173,10 @@ __device__ __forceinline__ Quant make_quant(const uint32_t* g, int bits) {
   q.qmax = float(qm);
   q.lim16 = (uint32_t(qm) & 0xFFFFu) * 0x10001u;
   q.nlim16 = (uint32_t(-qm) & 0xFFFFu) * 0x10001u;
-  const float amax_w = __uint_as_float(g[0]);
+  // L1-bypassing loads: in the fused kernel these words were written by other
+  // CTAs' atomics just before the grid barrier
+  const uint32_t g0 = __ldcg(g), g1 = __ldcg(g + 1);
+  const float amax_w = __uint_as_float(g0);
   const float amax_v = __fmul_rn(amax_w, 0.25f);
   float s = __fdiv_rn(amax_v, q.qmax);
   if (s == 0.0f) s = 1.0f;
@@ -149,26 +184,32 @@ __device__ __forceinline__ Quant make_quant(const uint32_t* g, int bits) {
   q.d = __fmul_rn(s, 1.0f / 512.0f);
   q.r = __frcp_rn(q.d);
   q.lim = 2048.0f * q.qmax;
-  const uint32_t inv = g[1];
+  const uint32_t inv = g1;
   const float minnz = inv ? __uint_as_float(~inv + 1u) : 0.0f;  // 0: no nonzero value at all
-  q.fast = (g[0] < 0x7F800000u) && s > 0x1p-116f &&
+  q.fast = (g0 < 0x7F800000u) && s > 0x1p-116f &&
            (minnz == 0.0f || (minnz >= 0x1p-100f && minnz >= __fmul_rn(s, 0x1p-108f)));
   return q;
 }
 
 // Unclamped codes of two values as two s16 lanes: code = ceil((Q - u) / 2048),
 // Q = RN(w / d) by reciprocal-FMA division, u = bits(w) & 0x7FF.
+//   U  = 2^23 + u as a float (one LOP3: OR the draw into 2^23's mantissa);
+//   z  = RU(Q - U) = RU(y - 2^23), y = Q - u in (-2^19, 2^19): a grid of
+//        spacing <= 1 around -2^23, so z + 2^23 = g is the smallest grid point
+//        >= y, and ceil(g / 2048) = ceil(y / 2048) (multiples of 2048 lie on
+//        the grid);
+//   c  = RU(z * 2^-11 + (M + 4096)) = M + ceil(g / 2048), M = 1.5 * 2^23 (ulp 1):
+//        the low bits of c are the two's-complement code.
 __device__ __forceinline__ uint32_t quant_fast2(float2 w, const Quant& q) {
   const float2 Q0 = f2mul(w, f2(q.r));
   const float2 e = f2fma(Q0, f2(-q.d), w);
   const float2 Q = f2fma(e, f2(q.r), Q0);
   uint32_t ux, uy;
-  const uint32_t magic = 0x4B000000u;  // 2^23: (2^23 + u) as a float, one LOP3 each
+  const uint32_t magic = 0x4B000000u;  // 2^23
   asm("lop3.b32 %0, %1, 0x7FF, %2, 0xEA;" : "=r"(ux) : "r"(__float_as_uint(w.x)), "r"(magic));
   asm("lop3.b32 %0, %1, 0x7FF, %2, 0xEA;" : "=r"(uy) : "r"(__float_as_uint(w.y)), "r"(magic));
-  const float2 nu = f2sub(f2(8388608.0f), make_float2(__uint_as_float(ux), __uint_as_float(uy)));
-  const float2 z = f2add_rp(Q, nu);                                   // RU(Q - u)
-  const float2 c = f2fma_rp(z, f2(1.0f / 2048.0f), f2(kMagic));       // M + ceil(z / 2048)
+  const float2 z = f2sub_rp(Q, make_float2(__uint_as_float(ux), __uint_as_float(uy)));  // RU(Q - U)
+  const float2 c = f2fma_rp(z, f2(1.0f / 2048.0f), f2(kMagic + 4096.0f));
   return __byte_perm(__float_as_uint(c.x), __float_as_uint(c.y), 0x5410);
 }
 
@@ -185,10 +226,13 @@ __device__ __forceinline__ int quant_exact(float w, const Quant& q) {
   return static_cast<int>(c);
 }
 
+// Clip to +-qmax.  Only the upper bound can bind: |q| = |v/s| <= qmax*(1 + 2^-23)
+// (s = RN(amax/qmax)), so a code below -qmax would need frac*2048 <= u with
+// frac >= 1 - 2^-20, impossible for u <= 2047; above, q = qmax + tiny rounds
+// up to qmax + 1 when u == 0.
 __device__ __forceinline__ uint32_t clamp_s16x2(uint32_t p, const Quant& q) {
   uint32_t r;
-  asm("max.s16x2 %0, %1, %2;" : "=r"(r) : "r"(p), "r"(q.nlim16));
-  asm("min.s16x2 %0, %1, %2;" : "=r"(r) : "r"(r), "r"(q.lim16));
+  asm("min.s16x2 %0, %1, %2;" : "=r"(r) : "r"(p), "r"(q.lim16));
   return r;
 }
 

@@ -90,10 +90,21 @@ struct Args {
 };
 
 // (item, block) steps of this CTA with 32-bit counters; divisions once per item.
+// ord runs over this CTA's ordinals blockIdx.x, +gridDim.x, ...; item = ord, or
+// items-1-ord for the reversed second pass of the fused kernel (the last items
+// of pass 1 are the ones still in L2 when pass 2 starts).
 struct StepIter {
-  int item, bl, nbl, gb0, col0, s, blk;
+  int ord, item, bl, nbl, gb0, col0, s, blk;
+  bool rev;
+  __device__ __forceinline__ void begin(const Args& a, bool reverse) {
+    rev = reverse;
+    ord = blockIdx.x;
+    start(a);
+  }
+  __device__ __forceinline__ bool valid(const Args& a) const { return ord < a.items; }
   __device__ __forceinline__ void start(const Args& a) {
-    if (item >= a.items) return;
+    if (ord >= a.items) return;
+    item = rev ? a.items - 1 - ord : ord;
     const int g = item / a.ncol_tiles;
     col0 = (item - g * a.ncol_tiles) * kCols;
     gb0 = g * a.nb;
@@ -104,7 +115,7 @@ struct StepIter {
   }
   __device__ __forceinline__ void next(const Args& a) {
     if (++bl == nbl) {
-      item += gridDim.x;
+      ord += gridDim.x;
       start(a);
     } else if (++blk == a.nblk) {
       blk = 0;
@@ -113,23 +124,38 @@ struct StepIter {
   }
 };
 
-// 16 elements of one row piece from the staged tile -> fp32
+// Two 16-element row pieces (rows r and r+8 of the staged tile, same column
+// block) as 16 f32x2 lanes: p[i] = (A[i], B[i]).  All four butterfly stages
+// then run on packed pairs.
+// `flip` (bf16): read the two 16-byte halves in swapped order, so the 8
+// threads of one LDS.128 wavefront (blocks b..b+7, 32-byte pieces) cover all
+// 8 bank groups instead of 4 (blocks b and b+4 collide otherwise).
 template <typename T>
-__device__ __forceinline__ void read16(uint32_t p, float (&v)[16]) {
+__device__ __forceinline__ void read16x2(uint32_t pa, uint32_t pb, float2 (&p)[16], uint32_t flip) {
   if (sizeof(T) == 2) {
+    const uint32_t o0 = flip << 4, o1 = o0 ^ 16u;
+    const uint4 a0 = ptx::lds128(pa + o0), b0 = ptx::lds128(pb + o0);
+    const uint4 a1 = ptx::lds128(pa + o1), b1 = ptx::lds128(pb + o1);
+    const uint4 ta[2] = {flip ? a1 : a0, flip ? a0 : a1};
+    const uint4 tb[2] = {flip ? b1 : b0, flip ? b0 : b1};
 #pragma unroll
     for (int q = 0; q < 2; ++q) {
-      const uint4 t = ptx::lds128(p + 16 * q);
-      const uint32_t w[4] = {t.x, t.y, t.z, t.w};
+      const uint32_t wa[4] = {ta[q].x, ta[q].y, ta[q].z, ta[q].w};
+      const uint32_t wb[4] = {tb[q].x, tb[q].y, tb[q].z, tb[q].w};
 #pragma unroll
-      for (int k = 0; k < 4; ++k) { v[8 * q + 2 * k] = bf_lo(w[k]); v[8 * q + 2 * k + 1] = bf_hi(w[k]); }
+      for (int k = 0; k < 4; ++k) {
+        p[8 * q + 2 * k] = make_float2(bf_lo(wa[k]), bf_lo(wb[k]));
+        p[8 * q + 2 * k + 1] = make_float2(bf_hi(wa[k]), bf_hi(wb[k]));
+      }
     }
   } else {
 #pragma unroll
     for (int q = 0; q < 4; ++q) {
-      const uint4 t = ptx::lds128(p + 16 * q);
-      v[4 * q] = __uint_as_float(t.x); v[4 * q + 1] = __uint_as_float(t.y);
-      v[4 * q + 2] = __uint_as_float(t.z); v[4 * q + 3] = __uint_as_float(t.w);
+      const uint4 ta = ptx::lds128(pa + 16 * q), tb = ptx::lds128(pb + 16 * q);
+      p[4 * q] = make_float2(__uint_as_float(ta.x), __uint_as_float(tb.x));
+      p[4 * q + 1] = make_float2(__uint_as_float(ta.y), __uint_as_float(tb.y));
+      p[4 * q + 2] = make_float2(__uint_as_float(ta.z), __uint_as_float(tb.z));
+      p[4 * q + 3] = make_float2(__uint_as_float(ta.w), __uint_as_float(tb.w));
     }
   }
 }
@@ -137,142 +163,181 @@ __device__ __forceinline__ void read16(uint32_t p, float (&v)[16]) {
 template <typename T, int MODE, bool GX, bool GW, int BM, bool FX, bool FW>
 __device__ __forceinline__ void consume(const Args& a, const Quant& qx, const Quant& qw,
                                         uint8_t* tiles, uint64_t* full, uint64_t* empty,
-                                        uint8_t* cbuf, Stat& sx, Stat& sw) {
+                                        uint8_t* cbuf, Stat& sx, Stat& sw, int& slot,
+                                        uint32_t& phase, bool reverse) {
   constexpr int kRow = Tr<T>::kRow;
   const uint32_t bitmap = BM ? uint32_t(BM) : a.bitmap;
   const int rank = BM ? __builtin_popcount(uint32_t(BM)) : a.rank;
   const int tid = threadIdx.x;
-  const int lane = tid & 31;
+  const int lane = threadIdx.x & 31;
+  constexpr bool p1 = true, p2 = true;
+  const int ftid = tid;
+  constexpr int kFlushThreads = kConsumers;
   StepIter it;
-  it.item = blockIdx.x;
-  it.start(a);
-  int slot = 0;
-  uint32_t phase = 0;
-  while (it.item < a.items) {
-    ptx::mbar_wait(&full[slot], phase);
-    const uint32_t tile = ptx::smem_u32(tiles) + slot * (16 * kRow);
-    const int rvalid = a.rows - it.blk * 16;  // rows of this block inside the segment
-    // ---------------- phase 1: (row, 16-col block) pieces -> gx operand
-    if (GX) {
-#pragma unroll
-      for (int h = 0; h < 2; ++h) {
-        const int u = tid + h * kConsumers;
-        const int r = u >> 4, b = u & 15;
+  it.begin(a, reverse);
+  while (it.valid(a)) {
+    {
+      ptx::mbar_wait(&full[slot], phase);
+      const uint32_t tile = ptx::smem_u32(tiles) + slot * (16 * kRow);
+      const int rvalid = a.rows - it.blk * 16;  // rows of this block inside the segment
+      // ---------------- phase 1: (row, 16-col block) pieces -> gx operand
+      // thread = (rows r and r+8, block b); rows past the segment and columns
+      // past `cols` were zero-filled by TMA, so the statistics need no predicate
+      if (GX && p1) {
+        const int r = tid >> 4, b = tid & 15;
         const int c = it.col0 + b * 16;
-        if (r < rvalid && c < a.cols) {
-          float v[16];
-          read16<T>(tile + r * kRow + b * 16 * sizeof(T), v);
-          fwht16_raw(v);
-          if (MODE == kStats) {
-#pragma unroll
-            for (int i = 0; i < 16; ++i) sx.add(v[i]);
-          } else {
-            uint32_t p[8];
-#pragma unroll
-            for (int i = 0; i < 8; ++i) p[i] = quant2<FX>(make_float2(v[2 * i], v[2 * i + 1]), qx);
-            const uint4 out = make_uint4(pack4(p[0], p[1]), pack4(p[2], p[3]), pack4(p[4], p[5]),
-                                         pack4(p[6], p[7]));
-            const int64_t row = int64_t(it.s) * a.rows + it.blk * 16 + r;
-            *reinterpret_cast<uint4*>(a.dst_gx + row * a.ld_gx + c) = out;
-          }
-        }
-      }
-    }
-    // ---------------- phase 2: column pair -> gw operand (projection along rows)
-    if (GW) {
-      const int c = 2 * tid;
-      if (it.col0 + c < a.cols) {
-        float2 pv[16];
-#pragma unroll
-        for (int i = 0; i < 16; ++i) {
-          if (sizeof(T) == 2) {
-            const uint32_t w = ptx::lds32(tile + i * kRow + 2 * c);
-            pv[i] = make_float2(bf_lo(w), bf_hi(w));
-          } else {
-            const uint2 w = ptx::lds64(tile + i * kRow + 4 * c);
-            pv[i] = make_float2(__uint_as_float(w.x), __uint_as_float(w.y));
-          }
-        }
-        fwht16_pair(pv);
+        float2 p[16];
+        read16x2<T>(tile + r * kRow + b * 16 * sizeof(T), tile + (r + 8) * kRow + b * 16 * sizeof(T), p,
+                    uint32_t(b >> 2) & 1u);
+        fwht16_pair(p);
         if (MODE == kStats) {
 #pragma unroll
-          for (int i = 0; i < 16; ++i)
-            if ((bitmap >> i) & 1u) { sw.add(pv[i].x); sw.add(pv[i].y); }
-        } else {
-          // codes of kept basis j for both columns, as s16x2 (x = col c, y = col c+1)
-          uint32_t cx[4] = {0, 0, 0, 0}, cy[4] = {0, 0, 0, 0};
+          for (int i = 0; i < 16; ++i) sx.add2(p[i].x, p[i].y);
+        } else if (c < a.cols) {
+          uint32_t w[16];
+#pragma unroll
+          for (int i = 0; i < 16; ++i) w[i] = quant2<FX>(p[i], qx);  // (code A_i, code B_i)
+          uint32_t ca[4], cb[4];
+#pragma unroll
+          for (int q = 0; q < 4; ++q) {
+            const uint32_t t01 = __byte_perm(w[4 * q], w[4 * q + 1], 0x6420);  // A B A B
+            const uint32_t t23 = __byte_perm(w[4 * q + 2], w[4 * q + 3], 0x6420);
+            ca[q] = __byte_perm(t01, t23, 0x6420);
+            cb[q] = __byte_perm(t01, t23, 0x7531);
+          }
+          const int64_t row = int64_t(it.s) * a.rows + it.blk * 16 + r;
+          if (r < rvalid)
+            *reinterpret_cast<uint4*>(a.dst_gx + row * a.ld_gx + c) = make_uint4(ca[0], ca[1], ca[2], ca[3]);
+          if (r + 8 < rvalid)
+            *reinterpret_cast<uint4*>(a.dst_gx + (row + 8) * a.ld_gx + c) =
+                make_uint4(cb[0], cb[1], cb[2], cb[3]);
+        }
+      }
+      // ---------------- phase 2: column pair -> gw operand (projection along rows)
+      if (GW && p2) {
+        const int c = 2 * tid;
+        if (it.col0 + c < a.cols) {
+          float2 pv[16];
 #pragma unroll
           for (int i = 0; i < 16; ++i) {
-            if ((bitmap >> i) & 1u) {
-              const int j = BM ? __builtin_popcount(uint32_t(BM) & ((1u << i) - 1u))
-                               : __popc(bitmap & ((1u << i) - 1u));
-              const uint32_t p = quant2<FW>(pv[i], qw);
-              const uint32_t bx = (p & 0xFFu) << (8 * (j & 3));
-              const uint32_t by = ((p >> 16) & 0xFFu) << (8 * (j & 3));
-              switch (j >> 2) {
-                case 0: cx[0] |= bx; cy[0] |= by; break;
-                case 1: cx[1] |= bx; cy[1] |= by; break;
-                case 2: cx[2] |= bx; cy[2] |= by; break;
-                default: cx[3] |= bx; cy[3] |= by; break;
+            if (sizeof(T) == 2) {
+              const uint32_t w = ptx::lds32(tile + i * kRow + 2 * c);
+              pv[i] = make_float2(bf_lo(w), bf_hi(w));
+            } else {
+              const uint2 w = ptx::lds64(tile + i * kRow + 4 * c);
+              pv[i] = make_float2(__uint_as_float(w.x), __uint_as_float(w.y));
+            }
+          }
+          fwht16_pair(pv);
+          if (MODE == kStats) {
+#pragma unroll
+            for (int i = 0; i < 16; ++i)
+              if ((bitmap >> i) & 1u) sw.add2(pv[i].x, pv[i].y);
+          } else {
+            // codes of kept basis j for both columns, as s16x2 (x = col c, y = col c+1)
+            uint32_t cx[4] = {0, 0, 0, 0}, cy[4] = {0, 0, 0, 0};
+#pragma unroll
+            for (int i = 0; i < 16; ++i) {
+              if ((bitmap >> i) & 1u) {
+                const int j = BM ? __builtin_popcount(uint32_t(BM) & ((1u << i) - 1u))
+                                 : __popc(bitmap & ((1u << i) - 1u));
+                const uint32_t p = quant2<FW>(pv[i], qw);
+                const uint32_t bx = (p & 0xFFu) << (8 * (j & 3));
+                const uint32_t by = ((p >> 16) & 0xFFu) << (8 * (j & 3));
+                switch (j >> 2) {
+                  case 0: cx[0] |= bx; cy[0] |= by; break;
+                  case 1: cx[1] |= bx; cy[1] |= by; break;
+                  case 2: cx[2] |= bx; cy[2] |= by; break;
+                  default: cx[3] |= bx; cy[3] |= by; break;
+                }
+              }
+            }
+            uint8_t* ox = cbuf + c * a.cstride + it.bl * rank;
+            uint8_t* oy = ox + a.cstride;
+            if (rank == 16) {
+              *reinterpret_cast<uint4*>(ox) = make_uint4(cx[0], cx[1], cx[2], cx[3]);
+              *reinterpret_cast<uint4*>(oy) = make_uint4(cy[0], cy[1], cy[2], cy[3]);
+            } else if (rank == 8) {
+              *reinterpret_cast<uint2*>(ox) = make_uint2(cx[0], cx[1]);
+              *reinterpret_cast<uint2*>(oy) = make_uint2(cy[0], cy[1]);
+            } else if (rank == 4) {
+              *reinterpret_cast<uint32_t*>(ox) = cx[0];
+              *reinterpret_cast<uint32_t*>(oy) = cy[0];
+            } else {
+              for (int j = 0; j < rank; ++j) {
+                ox[j] = uint8_t(cx[j >> 2] >> (8 * (j & 3)));
+                oy[j] = uint8_t(cy[j >> 2] >> (8 * (j & 3)));
               }
             }
           }
-          uint8_t* ox = cbuf + c * a.cstride + it.bl * rank;
-          uint8_t* oy = ox + a.cstride;
-          if (rank == 16) {
-            *reinterpret_cast<uint4*>(ox) = make_uint4(cx[0], cx[1], cx[2], cx[3]);
-            *reinterpret_cast<uint4*>(oy) = make_uint4(cy[0], cy[1], cy[2], cy[3]);
-          } else if (rank == 8) {
-            *reinterpret_cast<uint2*>(ox) = make_uint2(cx[0], cx[1]);
-            *reinterpret_cast<uint2*>(oy) = make_uint2(cy[0], cy[1]);
-          } else if (rank == 4) {
-            *reinterpret_cast<uint32_t*>(ox) = cx[0];
-            *reinterpret_cast<uint32_t*>(oy) = cy[0];
-          } else {
-            for (int j = 0; j < rank; ++j) {
-              ox[j] = uint8_t(cx[j >> 2] >> (8 * (j & 3)));
-              oy[j] = uint8_t(cy[j >> 2] >> (8 * (j & 3)));
-            }
-          }
         }
       }
+      // release the slot to the producer (one arrive per consuming warp)
+      __syncwarp();
+      if (lane == 0) ptx::mbar_arrive(&empty[slot]);
     }
-    // release the slot to the producer (one arrive per consumer warp)
-    __syncwarp();
-    if (lane == 0) ptx::mbar_arrive(&empty[slot]);
     if (++slot == kStages) { slot = 0; phase ^= 1; }
     // ---------------- end of a work item: flush the staged gw codes
     if (GW && MODE == kQuant && it.bl == it.nbl - 1) {
-      asm volatile("bar.sync 1, %0;" ::"n"(kConsumers));
+      asm volatile("bar.sync 1, %0;" ::"n"(kFlushThreads));
       const int run = it.nbl * rank;
       const int64_t k0 = int64_t(it.gb0) * rank;
       const int ncols = min(kCols, a.cols - it.col0);
       if ((run & 15) == 0 && (k0 & 15) == 0) {
         const int chunks = run >> 4;
-        for (int i = tid; i < ncols * chunks; i += kConsumers) {
+        for (int i = ftid; i < ncols * chunks; i += kFlushThreads) {
           const int c = i / chunks, q = i - c * chunks;
           *reinterpret_cast<uint4*>(a.dst_gw + (it.col0 + c) * a.ld_gw + k0 + 16 * q) =
               *reinterpret_cast<const uint4*>(cbuf + c * a.cstride + 16 * q);
         }
       } else if ((run & 7) == 0 && (k0 & 7) == 0) {
         const int chunks = run >> 3;
-        for (int i = tid; i < ncols * chunks; i += kConsumers) {
+        for (int i = ftid; i < ncols * chunks; i += kFlushThreads) {
           const int c = i / chunks, q = i - c * chunks;
           *reinterpret_cast<uint2*>(a.dst_gw + (it.col0 + c) * a.ld_gw + k0 + 8 * q) =
               *reinterpret_cast<const uint2*>(cbuf + c * a.cstride + 8 * q);
         }
       } else {
-        for (int i = tid; i < ncols * run; i += kConsumers) {
+        for (int i = ftid; i < ncols * run; i += kFlushThreads) {
           const int c = i / run, q = i - c * run;
           a.dst_gw[(it.col0 + c) * a.ld_gw + k0 + q] = int8_t(cbuf[c * a.cstride + q]);
         }
       }
-      asm volatile("bar.sync 1, %0;" ::"n"(kConsumers));
+      asm volatile("bar.sync 1, %0;" ::"n"(kFlushThreads));
     }
     it.next(a);
   }
 }
 
+// Quant-pass dispatch on the (grid-uniform) fast-division guard of each operand.
+template <typename T, bool GX, bool GW, int BM>
+__device__ __forceinline__ void consume_quant(const Args& a, uint8_t* tiles, uint64_t* full,
+                                              uint64_t* empty, uint8_t* cbuf, int& slot,
+                                              uint32_t& phase, bool reverse) {
+  Quant qx{}, qw{};
+  if (GX) qx = make_quant(a.stats, a.bits_gx);
+  if (GW) qw = make_quant(a.stats + 2, a.bits_gw);
+  if (blockIdx.x == 0 && threadIdx.x == 0) {
+    if (GX && a.scale_gx) *a.scale_gx = qx.s;
+    if (GW && a.scale_gw) *a.scale_gw = qw.s;
+  }
+  Stat sx, sw;
+  const bool fx = !GX || qx.fast, fw = !GW || qw.fast;
+  if (fx && fw)
+    consume<T, kQuant, GX, GW, BM, true, true>(a, qx, qw, tiles, full, empty, cbuf, sx, sw, slot, phase, reverse);
+  else if (fx)
+    consume<T, kQuant, GX, GW, BM, true, false>(a, qx, qw, tiles, full, empty, cbuf, sx, sw, slot, phase, reverse);
+  else if (fw)
+    consume<T, kQuant, GX, GW, BM, false, true>(a, qx, qw, tiles, full, empty, cbuf, sx, sw, slot, phase, reverse);
+  else
+    consume<T, kQuant, GX, GW, BM, false, false>(a, qx, qw, tiles, full, empty, cbuf, sx, sw, slot, phase, reverse);
+}
+
+// MODE kStats / kQuant: one pass.  MODE kBoth: both passes in one cooperative
+// launch -- statistics, a grid-wide barrier (a counter in stats[4]), then the
+// quantization pass over the items in reverse order.  The producer warp never
+// waits for the barrier: it keeps streaming pass-2 tiles into the ring while
+// the consumers wait for the scales.
 template <typename T, int MODE, bool GX, bool GW, int BM>
 __global__ void __launch_bounds__(kThreads) tma_tile_kernel(const __grid_constant__ CUtensorMap map,
                                                            Args a) {
@@ -282,7 +347,7 @@ __global__ void __launch_bounds__(kThreads) tma_tile_kernel(const __grid_constan
   // shared address space and emits LDS/STS rather than generic LD/ST
   uint8_t* tiles = smem_raw + ((128u - (ptx::smem_u32(smem_raw) & 127u)) & 127u);
   uint8_t* cbuf = tiles + kStages * 16 * kRow;
-  uint8_t* bars = cbuf + (GW && MODE == kQuant ? kCols * a.cstride : 0);
+  uint8_t* bars = cbuf + (GW && MODE != kStats ? kCols * a.cstride : 0);
   bars += (8u - (ptx::smem_u32(bars) & 7u)) & 7u;
   uint64_t* full = reinterpret_cast<uint64_t*>(bars);
   uint64_t* empty = full + kStages;
@@ -301,57 +366,62 @@ __global__ void __launch_bounds__(kThreads) tma_tile_kernel(const __grid_constan
     // ---------------- producer
     if (ptx::elect_one()) {
       ptx::tma_prefetch_desc(&map);
-      StepIter it;
-      it.item = blockIdx.x;
-      it.start(a);
       int slot = 0;
       uint32_t phase = 0;
-      while (it.item < a.items) {
-        ptx::mbar_wait_sleep(&empty[slot], phase ^ 1);
-        ptx::mbar_arrive_expect_tx(&full[slot], 16 * kRow);
-        ptx::tma_load_3d(tiles + slot * 16 * kRow, &map, &full[slot], it.col0, it.blk * 16, it.s);
-        if (++slot == kStages) { slot = 0; phase ^= 1; }
-        it.next(a);
+      for (int pass = 0; pass < (MODE == kBoth ? 2 : 1); ++pass) {
+        StepIter it;
+        it.begin(a, pass == 1);
+        while (it.valid(a)) {
+          ptx::mbar_wait_sleep(&empty[slot], phase ^ 1);
+          ptx::mbar_arrive_expect_tx(&full[slot], 16 * kRow);
+          ptx::tma_load_3d(tiles + slot * 16 * kRow, &map, &full[slot], it.col0, it.blk * 16, it.s);
+          if (++slot == kStages) { slot = 0; phase ^= 1; }
+          it.next(a);
+        }
       }
     }
     return;
   }
 
-  Stat sx, sw;
-  if (MODE == kStats) {
-    Quant dummy{};
-    consume<T, MODE, GX, GW, BM, true, true>(a, dummy, dummy, tiles, full, empty, cbuf, sx, sw);
-    sx.warp_reduce();
-    sw.warp_reduce();
-    if ((threadIdx.x & 31) == 0) {
-      if (GX) sx.commit(a.stats);
-      if (GW) sw.commit(a.stats + 2);
-    }
+  int slot = 0;
+  uint32_t phase = 0;
+  if (MODE == kQuant) {
+    consume_quant<T, GX, GW, BM>(a, tiles, full, empty, cbuf, slot, phase, false);
     return;
   }
-  Quant qx{}, qw{};
-  if (GX) qx = make_quant(a.stats, a.bits_gx);
-  if (GW) qw = make_quant(a.stats + 2, a.bits_gw);
-  if (blockIdx.x == 0 && threadIdx.x == 0) {
-    if (GX && a.scale_gx) *a.scale_gx = qx.s;
-    if (GW && a.scale_gw) *a.scale_gw = qw.s;
+  Stat sx, sw;
+  {
+    Quant dummy{};
+    consume<T, kStats, GX, GW, BM, true, true>(a, dummy, dummy, tiles, full, empty, cbuf, sx, sw, slot,
+                                               phase, false);
   }
-  const bool fx = !GX || qx.fast, fw = !GW || qw.fast;  // uniform across the grid
-  if (fx && fw)
-    consume<T, MODE, GX, GW, BM, true, true>(a, qx, qw, tiles, full, empty, cbuf, sx, sw);
-  else if (fx)
-    consume<T, MODE, GX, GW, BM, true, false>(a, qx, qw, tiles, full, empty, cbuf, sx, sw);
-  else if (fw)
-    consume<T, MODE, GX, GW, BM, false, true>(a, qx, qw, tiles, full, empty, cbuf, sx, sw);
-  else
-    consume<T, MODE, GX, GW, BM, false, false>(a, qx, qw, tiles, full, empty, cbuf, sx, sw);
+  sx.warp_reduce();
+  sw.warp_reduce();
+  if ((threadIdx.x & 31) == 0) {
+    if (GX) sx.commit(a.stats);
+    if (GW) sw.commit(a.stats + 2);
+  }
+  if (MODE == kStats) return;
+  // ---------------- grid barrier (consumer threads only; all CTAs co-resident)
+  asm volatile("bar.sync 2, %0;" ::"n"(kConsumers) : "memory");
+  if (threadIdx.x == 0) {
+    __threadfence();
+    atomicAdd(a.stats + 4, 1u);
+    uint32_t seen;
+    do {
+      asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(seen) : "l"(a.stats + 4) : "memory");
+      if (seen < gridDim.x) __nanosleep(64);
+    } while (seen < gridDim.x);
+  }
+  asm volatile("bar.sync 2, %0;" ::"n"(kConsumers) : "memory");
+  consume_quant<T, GX, GW, BM>(a, tiles, full, empty, cbuf, slot, phase, true);
 }
 
 template <typename T, int MODE, bool GX, bool GW, int BM>
-void launch_one(const CUtensorMap& map, const Args& a, cudaStream_t stream) {
+void launch_one(const CUtensorMap& map, Args a, cudaStream_t stream) {
   constexpr int kRow = Tr<T>::kRow;
   const size_t smem = 128 + size_t(kStages) * 16 * kRow +
-                      (GW && MODE == kQuant ? size_t(kCols) * a.cstride : 0) + 8 + 2 * kStages * 8;
+                      (GW && MODE != kStats ? size_t(kCols) * a.cstride : 0) + 8 + 2 * kStages * 8;
   auto kern = tma_tile_kernel<T, MODE, GX, GW, BM>;
   static bool attr = false;
   if (!attr) {
@@ -364,7 +434,22 @@ void launch_one(const CUtensorMap& map, const Args& a, cudaStream_t stream) {
     per_sm = 1;
   const int cap = num_sms() * per_sm;
   const int grid = a.items < 1 ? 1 : (a.items > cap ? cap : a.items);
-  kern<<<grid, kThreads, smem, stream>>>(map, a);
+  if (MODE != kBoth) {
+    kern<<<grid, kThreads, smem, stream>>>(map, a);
+    return;
+  }
+  // every CTA must be resident for the grid barrier: cooperative launch
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(grid);
+  cfg.blockDim = dim3(kThreads);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = stream;
+  cudaLaunchAttribute attr_coop[1];
+  attr_coop[0].id = cudaLaunchAttributeCooperative;
+  attr_coop[0].val.cooperative = 1;
+  cfg.attrs = attr_coop;
+  cfg.numAttrs = 1;
+  cudaLaunchKernelEx(&cfg, kern, map, a);
 }
 
 template <typename T, int MODE, bool GX, bool GW>
@@ -379,17 +464,18 @@ void launch_bm(const CUtensorMap& map, const Args& a, cudaStream_t st) {
   }
 }
 
+template <typename T, int MODE>
+void launch_ops(const CUtensorMap& map, const Args& a, bool gx, bool gw, cudaStream_t st) {
+  if (gx && gw) launch_bm<T, MODE, true, true>(map, a, st);
+  else if (gx) launch_bm<T, MODE, true, false>(map, a, st);
+  else launch_bm<T, MODE, false, true>(map, a, st);
+}
+
 template <typename T>
 void launch_modes(const CUtensorMap& map, const Args& a, int mode, bool gx, bool gw, cudaStream_t st) {
-  if (mode == kStats) {
-    if (gx && gw) launch_bm<T, kStats, true, true>(map, a, st);
-    else if (gx) launch_bm<T, kStats, true, false>(map, a, st);
-    else launch_bm<T, kStats, false, true>(map, a, st);
-  } else {
-    if (gx && gw) launch_bm<T, kQuant, true, true>(map, a, st);
-    else if (gx) launch_bm<T, kQuant, true, false>(map, a, st);
-    else launch_bm<T, kQuant, false, true>(map, a, st);
-  }
+  if (mode == kStats) launch_ops<T, kStats>(map, a, gx, gw, st);
+  else if (mode == kQuant) launch_ops<T, kQuant>(map, a, gx, gw, st);
+  else launch_ops<T, kBoth>(map, a, gx, gw, st);
 }
 
 // Blocks per work item: >= 32-byte output runs per column when the problem is
@@ -419,7 +505,13 @@ void launch_transform(const TransformArgs& t, int mode, cudaStream_t stream) {
     const uint32_t box[3] = {uint32_t(kCols), 16, 1};
     ok = encode_tensor_map(&map, t.dtype == kBF16 ? 1 : 2, 3, t.src, dims, strides, box, 0);
   }
-  if (!ok) return launch_transform_fallback(t, mode, stream);
+  if (!ok) {
+    if (mode == kBoth) {
+      launch_transform_fallback(t, kStats, stream);
+      return launch_transform_fallback(t, kQuant, stream);
+    }
+    return launch_transform_fallback(t, mode, stream);
+  }
   Args a{};
   a.rows = int(t.rows);
   a.cols = int(t.cols);

@@ -113,8 +113,8 @@ def quant_ht_cols(src: torch.Tensor, bits: int):
     ld = pad16(cols)
     codes = torch.empty((rows, ld), dtype=torch.int8, device=src.device)
     scale = torch.empty(1, dtype=torch.float32, device=src.device)
-    stats = torch.empty(4, dtype=torch.int32, device=src.device)
-    _traced("transform", rows * cols * src.element_size() + rows * ld, 0, 2,
+    stats = torch.empty(8, dtype=torch.int32, device=src.device)
+    _traced("transform", rows * cols * src.element_size() + rows * ld, 0, 1,
             lambda: _lib.call("hlq_quantize_ht_cols", _p(src), dtype_code(src), rows, cols, cols,
                               bits, _p(stats), _p(codes), ld, _p(scale), _stream()))
     return codes, scale, stats[0:1]
@@ -136,9 +136,9 @@ def quant_dual(src: torch.Tensor, segs: int, rows: int, cols: int, bitmap: int, 
     cgx = torch.empty((segs * rows, pad16(cols)), dtype=torch.int8, device=dev)
     cgw = torch.empty((cols, ldk), dtype=torch.int8, device=dev)
     scales = torch.empty(2, dtype=torch.float32, device=dev)
-    stats = torch.empty(4, dtype=torch.int32, device=dev)
+    stats = torch.empty(8, dtype=torch.int32, device=dev)
     nbytes = segs * rows * cols * src.element_size() + cgx.numel() + cols * k
-    _traced("transform", nbytes, 0, 2,
+    _traced("transform", nbytes, 0, 1,
             lambda: _lib.call("hlq_quantize_dual", _p(src), dtype_code(src), segs, rows, cols,
                               ld_src, seg_src, bitmap, bits_gx, bits_gw, _p(stats), _p(cgx),
                               cgx.stride(0), _p(cgw), ldk, _p(scales), _p(scales[1:]), _stream()))
@@ -176,8 +176,8 @@ def quant_proj_rows(src: torch.Tensor, segs: int, rows: int, cols: int, bitmap: 
     ld = max(pad16(k), 16)
     codes = torch.empty((cols, ld), dtype=torch.int8, device=src.device)
     scale = torch.empty(1, dtype=torch.float32, device=src.device)
-    stats = torch.empty(4, dtype=torch.int32, device=src.device)
-    _traced("transform", segs * rows * cols * src.element_size() + cols * k, 0, 2,
+    stats = torch.empty(8, dtype=torch.int32, device=src.device)
+    _traced("transform", segs * rows * cols * src.element_size() + cols * k, 0, 1,
             lambda: _lib.call("hlq_quantize_proj_rows", _p(src), dtype_code(src), segs, rows, cols,
                               ld_src, seg_src, bitmap, bits, _p(stats), _p(codes), ld, _p(scale),
                               _stream()))
@@ -223,12 +223,16 @@ def gemm_i8(a: torch.Tensor, b: torch.Tensor, m: int, n: int, k: int, bits_a: in
     lda, ldb = a.stride(0), b.stride(0)
     a_gs = lda * m if a_gstride is None else a_gstride
     b_gs = ldb * n if b_gstride is None else b_gstride
+    # split-K workspace (the dW products: few output tiles, long K); stream-ordered
+    # caching-allocator memory, no initialisation needed
+    wsb = int(_lib.load().hlq_gemm_i8_ws(m, n, k, groups)) if m > 0 and n > 0 else 0
+    ws = torch.empty(wsb, dtype=torch.uint8, device=dev) if wsb else None
     _traced("gemm", 0, 2 * m * n * k * groups, 1,
-            lambda: _lib.call("hlq_gemm_i8_grouped", _p(a), lda, a_gs, _p(b), ldb, b_gs, m, n, k,
+            lambda: _lib.call("hlq_gemm_i8_ex", _p(a), lda, a_gs, _p(b), ldb, b_gs, m, n, k,
                               groups, bits_a, bits_b, _p(sa), _p(sb), float(extra),
                               _lib.HLQ_EPI_EXACT if exact else _lib.HLQ_EPI_FAST, _p(out),
                               _lib.HLQ_BF16 if out_dtype == torch.bfloat16 else _lib.HLQ_F32, n,
-                              _p(acc), n, _stream()))
+                              _p(acc), n, _p(ws), wsb, _stream()))
     return out, acc
 
 
@@ -247,7 +251,7 @@ def conv_acbp(x_nhwc: torch.Tensor, k: int, stride: int, pad: int, bitmap: int, 
     ld = max(pad16(kk), 16)
     codes = torch.empty((C * k * k, ld), dtype=torch.int8, device=x_nhwc.device)
     scale = torch.empty(1, dtype=torch.float32, device=x_nhwc.device)
-    stats = torch.empty(4, dtype=torch.int32, device=x_nhwc.device)
+    stats = torch.empty(8, dtype=torch.int32, device=x_nhwc.device)
     nbytes = x_nhwc.numel() * x_nhwc.element_size() + C * k * k * kk
     _traced("transform", nbytes, 0, 2,
             lambda: _lib.call("hlq_conv_acbp_compress", _p(x_nhwc), dtype_code(x_nhwc), B, H, W, C, k,

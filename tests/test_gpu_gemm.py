@@ -1,0 +1,85 @@
+"""GPU: the tcgen05 int8 GEMM (both tile widths, split-K, K groups, ragged
+edges) against exact int64 products on the host and the reference's fp64
+dequant formula (quantize.py:152-187)."""
+import numpy as np
+import pytest
+import torch
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def ops():
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    from paper_2406_15102_b200 import _lib, ops
+    assert _lib.load().hlq_device_ok() == 1
+    return ops
+
+
+def _ref(a, b, groups, sa, sb, extra):
+    acc = np.zeros((a.shape[1], b.shape[1]), dtype=np.int64)
+    for g in range(groups):
+        acc += a[g].astype(np.int64) @ b[g].astype(np.int64).T
+    comb = np.float64(np.float32(sa) * np.float32(sb))
+    out = (acc.astype(np.float64) * (comb * np.float64(extra))).astype(np.float32)
+    return acc, out
+
+
+# (M, N, K, groups, bits): dX-like (many tiles), dW-like (few tiles, long K ->
+# split-K), ragged M/N/K, grouped K panels, tiny
+SHAPES = [
+    (1000, 768, 3072, 1, 4),
+    (768, 768, 13312, 1, 8),
+    (3072, 768, 13312, 1, 8),
+    (2304, 768, 13312, 1, 8),
+    (200, 136, 4000, 1, 8),
+    (130, 300, 2080, 1, 8),
+    (96, 80, 48, 1, 8),
+    (256, 200, 64, 9, 8),
+    (384, 256, 512, 12, 8),
+]
+
+
+@pytest.mark.parametrize("M,N,K,groups,bits", SHAPES)
+def test_gemm_exact(ops, M, N, K, groups, bits):
+    rng = np.random.default_rng(M * 7 + N * 3 + K + groups)
+    q = 7 if bits == 4 else 127
+    ld = (K + 15) // 16 * 16
+    a = np.zeros((groups, M, ld), dtype=np.int8)
+    b = np.zeros((groups, N, ld), dtype=np.int8)
+    a[:, :, :K] = rng.integers(-q, q + 1, (groups, M, K))
+    b[:, :, :K] = rng.integers(-q, q + 1, (groups, N, K))
+    sa, sb, extra = np.float32(0.0123), np.float32(3.7e-4), 1.0 / 96
+    ta = torch.from_numpy(a).cuda()
+    tb = torch.from_numpy(b).cuda()
+    tsa = torch.tensor([sa], device="cuda")
+    tsb = torch.tensor([sb], device="cuda")
+    out, acc = ops.gemm_i8(ta[0] if groups == 1 else ta.view(groups * M, ld), tb[0] if groups == 1 else tb.view(groups * N, ld),
+                           M, N, K, bits, bits, tsa, tsb, extra, exact=True, want_acc=True,
+                           groups=groups, a_gstride=M * ld, b_gstride=N * ld)
+    torch.cuda.synchronize()
+    racc, rout = _ref(a[:, :, :K], b[:, :, :K], groups, sa, sb, extra)
+    assert np.array_equal(acc.cpu().numpy().astype(np.int64), racc)
+    assert np.array_equal(out.cpu().numpy(), rout)
+
+
+def test_split_plan_used_for_dw_shapes(ops):
+    from paper_2406_15102_b200 import _lib
+    lib = _lib.load()
+    assert lib.hlq_gemm_i8_ws(768, 768, 13312, 1) > 0        # ViT proj dW: 18 tiles
+    assert lib.hlq_gemm_i8_ws(25216, 768, 3072, 1) == 0      # ViT fc1 dX: 591 tiles
+
+
+def test_fast_epilogue_bf16(ops):
+    rng = np.random.default_rng(5)
+    M, N, K = 513, 768, 2048
+    a = rng.integers(-7, 8, (M, K)).astype(np.int8)
+    b = rng.integers(-7, 8, (N, K)).astype(np.int8)
+    sa, sb = np.float32(0.031), np.float32(0.0007)
+    out, _ = ops.gemm_i8(torch.from_numpy(a).cuda(), torch.from_numpy(b).cuda(), M, N, K, 4, 4,
+                         torch.tensor([sa], device="cuda"), torch.tensor([sb], device="cuda"), 1.0,
+                         exact=False, out_dtype=torch.bfloat16)
+    _, rout = _ref(a[None], b[None], 1, sa, sb, 1.0)
+    got = out.float().cpu().numpy()
+    assert np.linalg.norm(got - rout) / np.linalg.norm(rout) < 4e-3
