@@ -25,7 +25,6 @@ from __future__ import annotations
 import argparse
 import json
 import os
-import subprocess
 import sys
 import threading
 import time
@@ -129,24 +128,41 @@ def workload_config(args, world):
 # ---------------------------------------------------------------------------
 
 class ClockSampler:
+    """SM clock and throttle reasons sampled every 200 ms during the timed
+    region, in-process through NVML (nvidia-ml-py): spawning nvidia-smi from
+    the training process forks a multi-GB Python image and stalls the
+    launch-heavy step loop, which showed up as a 10 % slower step."""
+
+    REASONS = {"hw_slowdown": 0x8, "sw_thermal_slowdown": 0x20, "hw_thermal_slowdown": 0x40,
+               "sw_power_cap": 0x4}
+
     def __init__(self, gpu_index: int):
         self.gpu = gpu_index
         self.samples = []
         self._stop = threading.Event()
         self._t = None
+        self._nvml = None
 
     def __enter__(self):
+        if os.environ.get("HLQ_BENCH_NO_CLOCKS"):
+            return self
+        try:
+            import pynvml
+            pynvml.nvmlInit()
+            self._nvml = pynvml
+            h = pynvml.nvmlDeviceGetHandleByIndex(self.gpu)
+            self._max = pynvml.nvmlDeviceGetMaxClockInfo(h, pynvml.NVML_CLOCK_SM)
+        except Exception:  # noqa: BLE001
+            self._nvml = None
+            return self
+
         def loop():
-            q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
-                 "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
-                 "clocks_event_reasons.sw_power_cap")
+            nv = self._nvml
             while not self._stop.is_set():
                 try:
-                    out = subprocess.run(["nvidia-smi", "-i", str(self.gpu), f"--query-gpu={q}",
-                                          "--format=csv,noheader,nounits"], capture_output=True,
-                                         text=True, timeout=5).stdout.strip()
-                    if out:
-                        self.samples.append([v.strip() for v in out.split(",")])
+                    sm = nv.nvmlDeviceGetClockInfo(h, nv.NVML_CLOCK_SM)
+                    rs = nv.nvmlDeviceGetCurrentClocksEventReasons(h)
+                    self.samples.append((sm, rs))
                 except Exception:  # noqa: BLE001
                     pass
                 self._stop.wait(0.2)
@@ -161,13 +177,12 @@ class ClockSampler:
         return False
 
     def summary(self):
-        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        sm = sorted(float(s[0]) for s in self.samples if s[0].replace(".", "").isdigit())
-        mx = max((float(s[1]) for s in self.samples if s[1].replace(".", "").isdigit()), default=None)
-        reasons = sorted({names[i] for s in self.samples for i in range(4)
-                          if len(s) > 2 + i and s[2 + i].lower() == "active"})
-        return {"sm_mhz": sm[len(sm) // 2] if sm else None, "sm_max_mhz": mx, "reasons": reasons,
-                "samples": len(self.samples)}
+        if not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": [], "samples": 0}
+        sm = sorted(s[0] for s in self.samples)
+        reasons = sorted({n for _, rs in self.samples for n, bit in self.REASONS.items() if rs & bit})
+        return {"sm_mhz": float(sm[len(sm) // 2]), "sm_max_mhz": float(self._max), "reasons": reasons,
+                "samples": len(self.samples), "source": "nvml"}
 
 
 def measured_peaks():
@@ -227,6 +242,27 @@ def train_steps(torch, model, opt, x, y, n, host=None):
     return loss
 
 
+def warmup(torch, step_fn, min_steps: int, dist, min_seconds: float = 4.0) -> int:
+    """At least `min_steps` untimed steps, continued until `min_seconds` of
+    stepping have passed: on a freshly leased box the first seconds of load run
+    ~20 % slower (clock / power-state ramp), which a 3-step warm-up does not
+    absorb.  All ranks run the same number of steps."""
+    n = 0
+    t0 = time.perf_counter()
+    while True:
+        step_fn(1)
+        n += 1
+        if n >= min_steps:
+            torch.cuda.synchronize()
+            done = time.perf_counter() - t0 >= min_seconds
+            if dist is not None:
+                flag = torch.tensor([1 if done else 0], device="cuda")
+                dist.all_reduce(flag, op=dist.ReduceOp.MIN)
+                done = bool(flag.item())
+            if done:
+                return n
+
+
 def timed(torch, dist, fn):
     if dist is not None:
         dist.barrier()
@@ -245,29 +281,32 @@ def timed(torch, dist, fn):
     return ms
 
 
+def graph_us(torch, fn, flush, reps=10):
+    """Median device time (us) of fn captured in a CUDA graph (no host
+    overhead), L2 flushed (a 256 MB write) before every replay."""
+    fn()
+    torch.cuda.synchronize()
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g):
+        fn()
+    ts = []
+    for _ in range(reps):
+        flush.zero_()
+        s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        s.record()
+        g.replay()
+        e.record()
+        e.synchronize()
+        ts.append(s.elapsed_time(e) * 1e3)
+    return sorted(ts)[len(ts) // 2]
+
+
 def layer_bwd_table(torch):
     """Per-layer backward (dX + dW) at the ViT-B/16 shapes, batch 128: the HLQ
     kernels exactly as HLQLinearFunction.backward runs them vs the dense bf16
     backward (two cuBLAS GEMMs).  CUDA-graph replays, L2 flushed before each."""
     from paper_2406_15102_b200 import ops
     flush = torch.empty(64 * 1024 * 1024, device="cuda")
-
-    def graph_us(fn, reps=10):
-        fn()
-        torch.cuda.synchronize()
-        g = torch.cuda.CUDAGraph()
-        with torch.cuda.graph(g):
-            fn()
-        ts = []
-        for _ in range(reps):
-            flush.zero_()
-            s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-            s.record()
-            g.replay()
-            e.record()
-            e.synchronize()
-            ts.append(s.elapsed_time(e) * 1e3)
-        return sorted(ts)[len(ts) // 2]
 
     out = {}
     for name, B, L, I, O in [("qkv", BATCH, TOKENS, 768, 2304), ("proj", BATCH, TOKENS, 768, 768),
@@ -302,7 +341,8 @@ def layer_bwd_table(torch):
             gb @ wb
             gb.t() @ xb
 
-        h, d, f = graph_us(hlq_bwd), graph_us(dense_bwd), graph_us(hlq_fwd_extra)
+        h, d, f = (graph_us(torch, hlq_bwd, flush), graph_us(torch, dense_bwd, flush),
+                   graph_us(torch, hlq_fwd_extra, flush))
         out[name] = {"hlq_us": round(h, 1), "dense_bf16_us": round(d, 1), "speedup": round(d / h, 3),
                      "fwd_overhead_us": round(f, 1)}
     tot_h = sum(v["hlq_us"] for v in out.values())
@@ -312,6 +352,61 @@ def layer_bwd_table(torch):
                           "speedup": round(tot_d / tot_h, 3), "fwd_overhead_us": round(tot_f, 1)}
     out["note"] = ("hlq_us = backward as run by HLQLinearFunction (fused gy transform, dW || dX); "
                    "fwd_overhead_us = ACBP(X) + W codes, enqueued on a side stream under the forward GEMM")
+    del flush
+    return out
+
+
+def config_table(torch):
+    """The other BASELINE single-layer configs, HLQ backward vs dense bf16
+    backward on the same GPU (CUDA graphs, L2 flushed):
+      (a) configs[0]: Linear 4096 tokens x 1024 -> 1024, fp32 I/O, HLA rank 2
+          (r = tokens/8: K = 512) and the paper-default rank 8;
+      (b) configs[1]: Conv2d 256 -> 256, 3x3, 14x14, batch 128, rank 8 --
+          HLQConv2dFunction.backward's kernels (fused gy transform, W codes,
+          dW / dX int8 GEMMs, col2im) vs cuDNN dgrad + wgrad, channels_last bf16."""
+    from paper_2406_15102_b200 import ops
+    flush = torch.empty(64 * 1024 * 1024, device="cuda")
+    out = {}
+    torch.manual_seed(2)
+    T, I, O = 4096, 1024, 1024
+    x = torch.randn(T, 1, I, device="cuda")
+    w = torch.randn(O, I, device="cuda") * (2.0 / I) ** 0.5
+    gy = torch.randn(T, 1, O, device="cuda") * 1e-3
+    wb, xb, gb = w.to(torch.bfloat16), x.reshape(T, I).to(torch.bfloat16), gy.reshape(T, O).to(torch.bfloat16)
+    dense = graph_us(torch, lambda: (gb @ wb, gb.t() @ xb), flush)
+    cw, _, sw, _ = ops.quant_proj_rows(w, 1, O, I, 0xFFFF, 4)
+    for rank, bm in ((2, 0x0101), (8, 0x5555)):
+        # 2-D Linear convention: projection along the token (batch) axis, one segment
+        xp, k, sx, _ = ops.quant_proj_rows(x.reshape(T, I), 1, T, I, bm, 8)
+
+        def hlq_bwd():
+            cgx, sgx, cg, kg, sg, _ = ops.quant_dual(gy.reshape(T, O), 1, T, O, bm, 4, 8)
+            ops.gemm_i8(cg, xp, O, I, k, 8, 8, sg, sx, 1.0, exact=False)
+            ops.gemm_i8(cgx, cw, T, I, ops.pad16(O), 4, 4, sgx, sw, 1.0, exact=False)
+        h = graph_us(torch, hlq_bwd, flush)
+        out[f"a_linear_4096x1024_fp32_r{rank}"] = {"hlq_us": round(h, 1), "dense_bf16_us": round(dense, 1),
+                                                   "speedup": round(dense / h, 3), "K": k}
+    # (b) conv
+    B, C, H, W, k = 128, 256, 14, 14, 3
+    xc = torch.randn(B, C, H, W, device="cuda").to(memory_format=torch.channels_last).to(torch.bfloat16)
+    w4 = torch.randn(C, C, k, k, device="cuda") * (2.0 / (C * k * k)) ** 0.5
+    gyc = (torch.randn(B, C, H, W, device="cuda") * 1e-3).to(torch.bfloat16).to(
+        memory_format=torch.channels_last)
+    from paper_2406_15102_b200.backprop import BackwardStrategy
+    from paper_2406_15102_b200.conv import _conv_backward, conv_acbp_compress
+    strat = BackwardStrategy.hlq()
+    acbp, _ = conv_acbp_compress(xc, k, 1, 1, strat)
+    hc = graph_us(torch, lambda: _conv_backward(acbp, w4, gyc, xc.shape, 1, 1, strat, 1.0, False,
+                                                torch.bfloat16), flush)
+    w4b = w4.to(torch.bfloat16).to(memory_format=torch.channels_last)
+
+    def dense_conv():
+        torch.nn.grad.conv2d_input(xc.shape, w4b, gyc, stride=1, padding=1)
+        torch.nn.grad.conv2d_weight(xc, w4b.shape, gyc, stride=1, padding=1)
+    dc = graph_us(torch, dense_conv, flush)
+    fwd = graph_us(torch, lambda: conv_acbp_compress(xc, k, 1, 1, strat), flush)
+    out["b_conv_256x256_3x3_14x14_b128"] = {"hlq_us": round(hc, 1), "dense_bf16_us": round(dc, 1),
+                                            "speedup": round(dc / hc, 3), "fwd_acbp_us": round(fwd, 1)}
     del flush
     return out
 
@@ -349,7 +444,7 @@ def run_ours(args):
     x = torch.randn(B, 3, IMG, IMG, device="cuda", generator=g)
     y = torch.randint(0, 1000, (B,), device="cuda", generator=g)
 
-    train_steps(torch, model, opt, x, y, args.warmup)
+    warm_steps = warmup(torch, lambda n: train_steps(torch, model, opt, x, y, n), args.warmup, dist)
     launches0 = ops.LAUNCHES[0]
     with ClockSampler(local) as clk:
         ms = timed(torch, dist, lambda: train_steps(torch, model, opt, x, y, args.steps))
@@ -409,6 +504,7 @@ def run_ours(args):
                     "d2h_bytes_per_step": 4},
             "roofline": roof,
             "gpu_launches": int(launches),
+            "warmup_steps_run": int(warm_steps),
             "int8_peak_tops_measured": round(int8_peak, 1),
         }
     if not args.no_extras:
@@ -420,7 +516,7 @@ def run_ours(args):
             dmodel = torch.nn.parallel.DistributedDataParallel(dmodel, device_ids=[local],
                                                                gradient_as_bucket_view=True)
         dopt = torch.optim.SGD(dmodel.parameters(), lr=1e-3, momentum=0.9, foreach=True)
-        train_steps(torch, dmodel, dopt, x, y, args.warmup)
+        warmup(torch, lambda n: train_steps(torch, dmodel, dopt, x, y, n), args.warmup, dist, 2.0)
         dsteps = max(3, min(args.steps, 10))
         dms = timed(torch, dist, lambda: train_steps(torch, dmodel, dopt, x, y, dsteps))
         if rank == 0:
@@ -431,6 +527,7 @@ def run_ours(args):
         torch.cuda.empty_cache()
         if rank == 0:
             line["layer_bwd"] = layer_bwd_table(torch)
+            line["config_bwd"] = config_table(torch)
             if world == 1:
                 t0 = time.perf_counter()
                 sec = cpu_path_seconds_per_image(1)

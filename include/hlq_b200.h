@@ -200,6 +200,21 @@ HLQ_API int hlq_conv_acbp_compress(const void* x_nhwc, int dtype, int64_t B, int
                                    int bits, int8_t* payload, int64_t ld_payload, float* scale_out,
                                    uint32_t* stats_ws, void* stream);
 
+/* Conv2d dX as ONE implicit GEMM (stride 1): dx[b, h, w, c] (channels-last)
+ * = deq( sum over taps (i, j) and o of gcodes[b, h + pad - i, w + pad - j, o]
+ *        * wcodes[c*k*k + i*k + j, o] ), zero outside the gy extent.  gcodes is
+ * the gx operand of the conv backward (B, Ho, Wo, O) with pixel stride ld_g
+ * (= hlq_quantize_dual's gx codes), wcodes the W codes (C*k*k rows of ld_w).
+ * The taps accumulate in int32 before the dequant, so acc_out (B*H*W x C,
+ * optional) equals col2im of the reference's per-tap int64 accumulators and dx
+ * matches the reference's fp32 col2im (layers.py:109-121,153-158) to fp32
+ * rounding rather than bit for bit.  Replaces GEMM -> dcols -> col2im. */
+HLQ_API int hlq_conv_dgrad_i8(const int8_t* gcodes, int64_t ld_g, int64_t B, int64_t Ho, int64_t Wo,
+                              int64_t O, const int8_t* wcodes, int64_t ld_w, int64_t C, int k,
+                              int stride, int pad, int bits, const float* sg, const float* sw,
+                              int epilogue, void* dx_nhwc, int dx_dtype, int32_t* acc_out,
+                              void* stream);
+
 /* col2im (layers.py:109-121): dx[b, h, w, c] (channels-last) = sum over taps
  * in the reference's (i, j) order of dcols[b*L + l, c*k*k + i*k + j]
  * (fp32 accumulation; bit-exact vs the reference for fp32 dcols). */

@@ -54,7 +54,12 @@ def conv_acbp_compress(x: torch.Tensor, k: int, stride: int, pad: int, strategy:
 
 def _conv_backward(acbp: ACBPActivation, w4: torch.Tensor, gy: torch.Tensor, x_shape, stride: int,
                    pad: int, strategy: BackwardStrategy, extra: float, exact: bool, dx_dtype,
-                   need_dx: bool = True, need_dw: bool = True, stages: dict | None = None):
+                   need_dx: bool = True, need_dw: bool = True, stages: dict | None = None,
+                   implicit: bool | None = None):
+    """implicit (default: stride 1 and not exact): dX as one implicit GEMM over
+    the taps (hlq_conv_dgrad_i8; taps summed in int32, matches the reference to
+    fp32 rounding); otherwise the reference's lowering, GEMM -> dcols -> col2im
+    in tap order (bit-exact with the exact epilogue)."""
     B, C, H, W = x_shape
     O, _, k, _ = w4.shape
     Ho, Wo = gy.shape[2], gy.shape[3]
@@ -86,7 +91,19 @@ def _conv_backward(acbp: ACBPActivation, w4: torch.Tensor, gy: torch.Tensor, x_s
         dw = dw2.reshape(O, C, k, k)
         if want:
             stages.update(gw_codes_g=cg[:, :kg], gw_scale_g=sg, gw_acc=accw)
-    if need_dx:
+    if implicit is None:
+        implicit = stride == 1 and not exact and pad <= k - 1
+    if need_dx and implicit:
+        w2 = w4.detach().reshape(O, I)
+        w2 = w2 if w2.dtype == torch.float32 else w2.float()
+        cw, kw, sw, _ = ops.quant_proj_rows(w2.contiguous(), 1, O, I, 0xFFFF, bits_gx)
+        dx_nhwc, accx = ops.conv_dgrad_i8(cgx, B, Ho, Wo, O, cw, C, k, pad, bits_gx, sgx, sw, exact=exact,
+                                          out_dtype=dx_dtype, want_acc=want)
+        dx = dx_nhwc.permute(0, 3, 1, 2)  # NCHW shape, channels_last memory
+        if want:
+            stages.update(gx_codes_g=cgx, gx_scale_g=sgx, gx_codes_w=cw[:, :kw].t(), gx_scale_w=sw,
+                          dx_acc=accx)
+    elif need_dx:
         w2 = w4.detach().reshape(O, I)
         w2 = w2 if w2.dtype == torch.float32 else w2.float()
         cw, kw, sw, _ = ops.quant_proj_rows(w2.contiguous(), 1, O, I, 0xFFFF, bits_gx)

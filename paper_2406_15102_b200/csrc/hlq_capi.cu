@@ -281,6 +281,34 @@ int hlq_gemm_i8_ex(const int8_t* A, int64_t lda, int64_t a_gstride, const int8_t
   return HLQ_OK;
 }
 
+int hlq_conv_dgrad_i8(const int8_t* gcodes, int64_t ld_g, int64_t B, int64_t Ho, int64_t Wo, int64_t O,
+                      const int8_t* wcodes, int64_t ld_w, int64_t C, int k, int stride, int pad,
+                      int bits, const float* sg, const float* sw, int epilogue, void* dx_nhwc,
+                      int dx_dtype, int32_t* acc_out, void* stream) {
+  HLQ_TRY(check_bits(bits));
+  HLQ_TRY(check_dtype(dx_dtype));
+  HLQ_TRY(check_ld16(ld_g, "gy codes"));
+  HLQ_TRY(check_ld16(ld_w, "W codes"));
+  if (stride != 1)
+    return fail(HLQ_ERR_PARAMETER, "implicit-GEMM dgrad needs stride 1 (use the GEMM + col2im path)");
+  if (B <= 0 || Ho <= 0 || Wo <= 0 || O <= 0 || C <= 0 || k <= 0 || pad < 0 || pad > k - 1 ||
+      ld_g < pad16(O) || ld_w < pad16(O) || k > 15)
+    return fail(HLQ_ERR_DIMENSION, "bad conv dgrad geometry");
+  const int64_t H = Ho + k - 1 - 2 * pad, W = Wo + k - 1 - 2 * pad;
+  if (H <= 0 || W <= 0 || B * H * W > INT32_MAX)
+    return fail(HLQ_ERR_DIMENSION, "bad conv dgrad geometry");
+  const long double worst = (long double)k * k * pad16(O) * qmax_of(bits) * qmax_of(bits);
+  if (worst >= 2147483648.0L)
+    return fail(HLQ_ERR_PARAMETER, "contraction k*k*O exceeds the int32-exact bound");
+  if (epilogue != HLQ_EPI_EXACT && epilogue != HLQ_EPI_FAST)
+    return fail(HLQ_ERR_PARAMETER, "unknown epilogue %d", epilogue);
+  int e = hlq::launch_conv_dgrad_i8(gcodes, ld_g, B, Ho, Wo, O, wcodes, ld_w, C, k, pad, sg, sw, epilogue,
+                                    dx_nhwc, dx_dtype, C, acc_out, C, static_cast<cudaStream_t>(stream));
+  if (e == -1) return fail(HLQ_ERR_CUDA, "im2col tensor map rejected");
+  if (e != 0) return fail(HLQ_ERR_CUDA, "hlq_conv_dgrad_i8: %s", cudaGetErrorString(cudaError_t(e)));
+  return HLQ_OK;
+}
+
 int hlq_conv_acbp_compress(const void* x_nhwc, int dtype, int64_t B, int64_t H, int64_t W,
                            int64_t C, int k, int stride, int pad, uint32_t bitmap, int bits,
                            int8_t* payload, int64_t ld_payload, float* scale_out,
@@ -300,7 +328,10 @@ int hlq_conv_acbp_compress(const void* x_nhwc, int dtype, int64_t B, int64_t H, 
   const int64_t kk = B * ((Ho * Wo + 15) / 16) * __builtin_popcount(bitmap);
   if (ld_payload < kk) return fail(HLQ_ERR_DIMENSION, "payload ld %lld < K %lld", (long long)ld_payload, (long long)kk);
   cudaStream_t st = static_cast<cudaStream_t>(stream);
-  cudaMemsetAsync(stats_ws, 0, 4 * sizeof(uint32_t), st);
+  cudaMemsetAsync(stats_ws, 0, HLQ_STATS_WS_BYTES, st);
+  if (hlq::launch_conv_acbp_tma(x_nhwc, dtype, int(B), int(H), int(W), int(C), k, stride, pad, bitmap, bits,
+                                hlq::kBoth, stats_ws, payload, ld_payload, scale_out, st))
+    return cuda_status("hlq_conv_acbp_compress");
   hlq::launch_im2col_proj(x_nhwc, dtype, int(B), int(H), int(W), int(C), k, stride, pad, bitmap, bits,
                           hlq::kStats, stats_ws, nullptr, 0, nullptr, st);
   hlq::launch_im2col_proj(x_nhwc, dtype, int(B), int(H), int(W), int(C), k, stride, pad, bitmap, bits,

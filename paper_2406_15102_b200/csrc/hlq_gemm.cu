@@ -109,12 +109,24 @@ __device__ __forceinline__ void store_row_chunk(const uint32_t (&acc)[32], int64
 // covers K blocks [split*nk/splits, (split+1)*nk/splits) and stores its int32
 // partial tile to workspace slab `split`; splitk_finalize then sums the slabs
 // (integers: exact in any order) and runs the same dequant epilogue.
+// Implicit-GEMM conv dgrad (stride 1): A[m, (tap, o)] = G codes at output pixel
+// m shifted by the flipped tap, read by im2col-mode TMA (zero padding from the
+// map's bounding box); B[c, (tap, o)] = W codes row c*k*k + tap, a 3-D tiled
+// map (o, tap, c).  K loop = taps x channel chunks of 128.
+struct ConvGeo {
+  int conv;       // 0: plain GEMM
+  int Ho, Wo;     // gy spatial extent (= the im2col box traversal)
+  int k, padp;    // kernel size, im2col padding k-1-pad
+  int nkc;        // 128-byte channel chunks per tap
+};
+
 template <int BN, int STAGES>
 __global__ void __launch_bounds__(kThreads, 1)
     gemm_i8_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant__ CUtensorMap map_b,
                    int M, int N, int K, int groups, const float* __restrict__ sa, const float* __restrict__ sb,
                    double extra, int epilogue, void* out, int out_dtype, int64_t ldo,
-                   int32_t* acc_out, int64_t ld_acc, int splits, int32_t* __restrict__ slabs) {
+                   int32_t* acc_out, int64_t ld_acc, int splits, int32_t* __restrict__ slabs,
+                   const ConvGeo geo) {
   using Cfg = GemmCfg<BN, STAGES>;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
@@ -156,7 +168,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   const int tiles = num_m * num_n;
   const int units = tiles * splits;
   const int nk_g = (K + kBK - 1) / kBK;  // K blocks per group
-  const int nk = nk_g * groups;           // groups accumulate into the same tile
+  const int nk = geo.conv ? geo.k * geo.k * geo.nkc : nk_g * groups;  // groups / taps accumulate
 
   if (warp == 0) {
     if (ptx::elect_one()) {
@@ -167,11 +179,30 @@ __global__ void __launch_bounds__(kThreads, 1)
         const int mb = t / num_n, nb = t - mb * num_n;
         const int kb0 = int(int64_t(sp) * nk / splits), kb1 = int(int64_t(sp + 1) * nk / splits);
         int g = kb0 / nk_g, kg = kb0 - g * nk_g;
+        // conv: first output pixel of this M tile, as im2col box coordinates
+        int pw = 0, ph = 0, pn = 0;
+        if (geo.conv) {
+          const int p0 = mb * kBM, hw = geo.Ho * geo.Wo;
+          pn = p0 / hw;
+          const int rem = p0 - pn * hw;
+          ph = rem / geo.Wo;
+          pw = rem - ph * geo.Wo;
+        }
         for (int kb = kb0; kb < kb1; ++kb) {
           ptx::mbar_wait_sleep(&empty[stage], phase ^ 1);
           ptx::mbar_arrive_expect_tx(&full[stage], Cfg::kStageBytes);
-          ptx::tma_load_3d(sA + stage * Cfg::kABytes, &map_a, &full[stage], kg * kBK, mb * kBM, g);
-          ptx::tma_load_3d(sB + stage * Cfg::kBBytes, &map_b, &full[stage], kg * kBK, nb * BN, g);
+          if (geo.conv) {
+            const int tap = kb / geo.nkc, oc = kb - tap * geo.nkc;
+            const int ti = tap / geo.k, tj = tap - ti * geo.k;
+            // flipped tap (k-1-i, k-1-j): dX[h, w] += G[h + pad - i, w + pad - j] W[i, j]
+            ptx::tma_load_im2col_4d(sA + stage * Cfg::kABytes, &map_a, &full[stage], oc * kBK,
+                                    pw - geo.padp, ph - geo.padp, pn, uint16_t(geo.k - 1 - tj),
+                                    uint16_t(geo.k - 1 - ti));
+            ptx::tma_load_3d(sB + stage * Cfg::kBBytes, &map_b, &full[stage], oc * kBK, tap, nb * BN);
+          } else {
+            ptx::tma_load_3d(sA + stage * Cfg::kABytes, &map_a, &full[stage], kg * kBK, mb * kBM, g);
+            ptx::tma_load_3d(sB + stage * Cfg::kBBytes, &map_b, &full[stage], kg * kBK, nb * BN, g);
+          }
           if (++kg == nk_g) { kg = 0; ++g; }
           if (++stage == STAGES) { stage = 0; phase ^= 1; }
         }
@@ -373,14 +404,11 @@ bool encode_tensor_map(void* map, int dtype, int rank, const void* ptr, const ui
 namespace {
 
 template <int BN, int STAGES>
-int run(const int8_t* A, int64_t lda, const int8_t* B, int64_t ldb, int64_t M, int64_t N, int64_t K,
-        int64_t groups, int64_t a_gstride, int64_t b_gstride, const float* sa, const float* sb, double extra, int epilogue, void* out, int out_dtype,
-        int64_t ldo, int32_t* acc_out, int64_t ld_acc, int splits, void* ws, cudaStream_t stream) {
+int run_maps(const CUtensorMap& ma, const CUtensorMap& mb, int64_t M, int64_t N, int64_t K, int64_t groups,
+             const float* sa, const float* sb, double extra, int epilogue, void* out, int out_dtype,
+             int64_t ldo, int32_t* acc_out, int64_t ld_acc, int splits, void* ws, const ConvGeo& geo,
+             cudaStream_t stream) {
   using Cfg = GemmCfg<BN, STAGES>;
-  CUtensorMap ma, mb;
-  if (!make_map(&ma, A, M, K, lda, groups, a_gstride, kBM) ||
-      !make_map(&mb, B, N, K, ldb, groups, b_gstride, BN))
-    return -1;
   static bool attr_set = false;  // per template instance
   if (!attr_set) {
     cudaError_t e = cudaFuncSetAttribute(gemm_i8_kernel<BN, STAGES>,
@@ -394,7 +422,7 @@ int run(const int8_t* A, int64_t lda, const int8_t* B, int64_t ldb, int64_t M, i
   const int grid = int(units < num_sms() ? units : num_sms());
   gemm_i8_kernel<BN, STAGES><<<grid, kThreads, Cfg::kSmem, stream>>>(
       ma, mb, int(M), int(N), int(K), int(groups), sa, sb, extra, epilogue, out, out_dtype, ldo, acc_out, ld_acc,
-      splits, slabs);
+      splits, slabs, geo);
   if (splits > 1) {
     const int64_t nq = M * N / 4;
     int fgrid = int((nq + 255) / 256);
@@ -403,6 +431,37 @@ int run(const int8_t* A, int64_t lda, const int8_t* B, int64_t ldb, int64_t M, i
                                                out_dtype, ldo, acc_out, ld_acc);
   }
   return int(cudaGetLastError());
+}
+
+template <int BN, int STAGES>
+int run(const int8_t* A, int64_t lda, const int8_t* B, int64_t ldb, int64_t M, int64_t N, int64_t K,
+        int64_t groups, int64_t a_gstride, int64_t b_gstride, const float* sa, const float* sb, double extra, int epilogue, void* out, int out_dtype,
+        int64_t ldo, int32_t* acc_out, int64_t ld_acc, int splits, void* ws, cudaStream_t stream) {
+  CUtensorMap ma, mb;
+  if (!make_map(&ma, A, M, K, lda, groups, a_gstride, kBM) ||
+      !make_map(&mb, B, N, K, ldb, groups, b_gstride, BN))
+    return -1;
+  const ConvGeo geo{0, 0, 0, 0, 0, 0};
+  return run_maps<BN, STAGES>(ma, mb, M, N, K, groups, sa, sb, extra, epilogue, out, out_dtype, ldo, acc_out,
+                              ld_acc, splits, ws, geo, stream);
+}
+
+typedef CUresult (*EncodeIm2colFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                                   const cuuint64_t*, const int*, const int*, cuuint32_t, cuuint32_t,
+                                   const cuuint32_t*, CUtensorMapInterleave, CUtensorMapSwizzle,
+                                   CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+EncodeIm2colFn encode_im2col_fn() {
+  static EncodeIm2colFn fn = nullptr;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeIm2col", &p, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<EncodeIm2colFn>(p);
+  });
+  return fn;
 }
 
 // Tile width, split count and workspace bytes for one GEMM.  Split-K only when
@@ -419,18 +478,18 @@ GemmPlan plan_gemm(int64_t M, int64_t N, int64_t K, int64_t groups, bool allow_s
   const int64_t nk = ((K + kBK - 1) / kBK) * groups;
   const int64_t sms = num_sms();
   GemmPlan p{128, 1, 0};
-  // 128x256 tiles need 96 B/clk/SM of operand traffic vs 128 for 128x128, so
-  // prefer them, and recover parallelism with split-K when K is long
-  if (N > 128 && (wide_tiles >= sms || (allow_split && nk >= 16))) p.bn = 256;
+  if (N > 128 && wide_tiles >= sms) p.bn = 256;
   const int64_t tiles = m_tiles * ((N + p.bn - 1) / p.bn);
-  // (the finalize pass reads 16-byte int32 quads: N % 4 == 0; outputs 16-byte aligned rows)
-  if (allow_split && tiles < sms && nk >= 16 && N % 4 == 0) {
-    // makespan model: waves * (K blocks per unit + epilogue/slab overhead)
-    double best = double((tiles + sms - 1) / sms) * double(nk + 2);
-    for (int s = 2; s <= 16 && nk / s >= 4; ++s) {
-      const double t = double((tiles * s + sms - 1) / sms) * (double((nk + s - 1) / s) + 2.0) + 0.5 * s;
-      if (t < 0.97 * best) { best = t; p.splits = s; }
-    }
+  // Split-K only for products that fill less than half the SMs (e.g. the ViT
+  // proj dW, 36 tiles of K = 13312): the slab round trip costs ~6 us per split
+  // at fc1 size, which outweighs the wave gain once >= half the SMs are busy
+  // (tools/gemm_sweep.py, B200).  (the finalize pass reads 16-byte int32 quads:
+  // N % 4 == 0)
+  if (allow_split && 2 * tiles <= sms && nk >= 16 && N % 4 == 0) {
+    int64_t sp = sms / tiles;
+    if (sp > 4) sp = 4;
+    while (sp > 1 && nk / sp < 8) --sp;
+    p.splits = int(sp);
   }
   // tuning knobs (development sweeps): HLQ_GEMM_SPLITS=s forces s splits (1 = off),
   // HLQ_GEMM_BN=128|256 forces the tile width
@@ -467,6 +526,52 @@ int launch_gemm_i8(const int8_t* A, int64_t lda, const int8_t* B, int64_t ldb, i
                        out_dtype, ldo, acc_out, ld_acc, p.splits, ws, stream);
   return run<128, 6>(A, lda, B, ldb, M, N, K, groups, a_gstride, b_gstride, sa, sb, extra, epilogue, out,
                      out_dtype, ldo, acc_out, ld_acc, p.splits, ws, stream);
+}
+
+int launch_conv_dgrad_i8(const int8_t* G, int64_t ldg, int64_t B, int64_t Ho, int64_t Wo, int64_t O,
+                         const int8_t* Wc, int64_t ldw, int64_t C, int k, int pad, const float* sa,
+                         const float* sb, int epilogue, void* out, int out_dtype, int64_t ldo,
+                         int32_t* acc_out, int64_t ld_acc, cudaStream_t stream) {
+  EncodeIm2colFn enc = encode_im2col_fn();
+  EncodeTiledFn tenc = encode_fn();
+  if (!enc || !tenc) return -1;
+  const int padp = k - 1 - pad;  // dgrad of a stride-1 conv = conv of gy, flipped taps, padding k-1-pad
+  O = (O + 15) & ~int64_t(15);    // the contraction runs over the padded HT blocks (codes of pad16(O))
+  const int64_t H = Ho + 2 * padp - k + 1, W = Wo + 2 * padp - k + 1;
+  CUtensorMap ma, mb;
+  {
+    // gy codes as NHWC int8: dims (O, Wo, Ho, B), pixel stride ldg bytes
+    cuuint64_t dims[4] = {cuuint64_t(O), cuuint64_t(Wo), cuuint64_t(Ho), cuuint64_t(B)};
+    cuuint64_t strides[3] = {cuuint64_t(ldg), cuuint64_t(ldg * Wo), cuuint64_t(ldg * Wo * Ho)};
+    const int lower[2] = {-padp, -padp};
+    const int upper[2] = {padp - (k - 1), padp - (k - 1)};
+    cuuint32_t es[4] = {1, 1, 1, 1};
+    if (enc(&ma, CU_TENSOR_MAP_DATA_TYPE_UINT8, 4, const_cast<int8_t*>(G), dims, strides, lower, upper,
+            cuuint32_t(kBK), cuuint32_t(kBM), es, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+            CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
+      return -1;
+  }
+  const int64_t taps = int64_t(k) * k;
+  const int bn = (C > 128 && ((B * H * W + kBM - 1) / kBM) * ((C + 255) / 256) >= num_sms()) ? 256 : 128;
+  {
+    // W codes (C*k*k rows of ldw bytes, K = o): dims (O, taps, C)
+    cuuint64_t dims[3] = {cuuint64_t(O), cuuint64_t(taps), cuuint64_t(C)};
+    cuuint64_t strides[2] = {cuuint64_t(ldw), cuuint64_t(ldw * taps)};
+    cuuint32_t box[3] = {cuuint32_t(kBK), 1, cuuint32_t(bn)};
+    cuuint32_t es[3] = {1, 1, 1};
+    if (tenc(&mb, CU_TENSOR_MAP_DATA_TYPE_UINT8, 3, const_cast<int8_t*>(Wc), dims, strides, box, es,
+             CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+             CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
+      return -1;
+  }
+  const ConvGeo geo{1, int(H), int(W), k, padp, int((O + kBK - 1) / kBK)};
+  // the im2col box walks the OUTPUT (dX) pixel grid H x W of every image
+  const int64_t M = B * H * W;
+  if (bn == 256)
+    return run_maps<256, 4>(ma, mb, M, C, O, 1, sa, sb, 1.0, epilogue, out, out_dtype, ldo, acc_out, ld_acc, 1,
+                            nullptr, geo, stream);
+  return run_maps<128, 6>(ma, mb, M, C, O, 1, sa, sb, 1.0, epilogue, out, out_dtype, ldo, acc_out, ld_acc, 1,
+                          nullptr, geo, stream);
 }
 
 }  // namespace hlq

@@ -42,6 +42,12 @@ void launch_transform_fallback(const TransformArgs& t, int mode, cudaStream_t st
 void launch_im2col_proj(const void* x, int dtype, int B, int H, int W, int C, int k, int stride,
                         int pad, uint32_t bitmap, int bits, int mode, uint32_t* stats, int8_t* dst,
                         int64_t ld_dst, float* scale, cudaStream_t st);
+// The same ACBP on the TMA transform kernel: x read by im2col-mode TMA (one
+// 16-pixel x 256-channel tile per tap and step).  Returns false (nothing
+// launched) when a tensor map cannot describe x; mode may be kBoth.
+bool launch_conv_acbp_tma(const void* x, int dtype, int B, int H, int W, int C, int k, int stride, int pad,
+                          uint32_t bitmap, int bits, int mode, uint32_t* stats, int8_t* dst, int64_t ld_dst,
+                          float* scale, cudaStream_t stream);
 void launch_col2im(const void* dcols, int in_dtype, int64_t ld, int B, int H, int W, int C, int k,
                    int stride, int pad, void* dx, int out_dtype, cudaStream_t st);
 
@@ -58,6 +64,14 @@ int launch_gemm_i8(const int8_t* A, int64_t lda, const int8_t* B, int64_t ldb, i
                    const float* sa, const float* sb, double extra, int epilogue,
                    void* out, int out_dtype, int64_t ldo, int32_t* acc_out, int64_t ld_acc,
                    void* ws, size_t ws_bytes, cudaStream_t stream);
+// Implicit-GEMM dgrad of a stride-1 conv (k x k, padding pad): dX (B, H, W, C)
+// channels-last = sum over taps and o of G codes (B, Ho, Wo, O; pixel stride
+// ldg) at the shifted pixel x W codes (row c*k*k + tap, ld ldw), int32 in TMEM,
+// then the dequant epilogue.
+int launch_conv_dgrad_i8(const int8_t* G, int64_t ldg, int64_t B, int64_t Ho, int64_t Wo, int64_t O,
+                         const int8_t* Wc, int64_t ldw, int64_t C, int k, int pad, const float* sa,
+                         const float* sb, int epilogue, void* out, int out_dtype, int64_t ldo,
+                         int32_t* acc_out, int64_t ld_acc, cudaStream_t stream);
 // Workspace bytes that let launch_gemm_i8 split K (0: no split planned).
 size_t gemm_i8_ws_bytes(int64_t M, int64_t N, int64_t K, int64_t groups);
 

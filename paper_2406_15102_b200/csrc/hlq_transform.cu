@@ -87,6 +87,10 @@ struct Args {
   float* scale_gx;
   float* scale_gw;
   int cstride;  // bytes per column in the code staging buffer
+  // conv ACBP (taps > 0): the source is channels-last x read by im2col-mode TMA,
+  // one 16-output-pixel block x 256 channels per step and tap; segments =
+  // images, rows = output pixels l = ho*Wo + wo, payload row = c*taps + tap
+  int taps, kconv, cstr, cpad, wo_n;
 };
 
 // (item, block) steps of this CTA with 32-bit counters; divisions once per item.
@@ -94,7 +98,7 @@ struct Args {
 // items-1-ord for the reversed second pass of the fused kernel (the last items
 // of pass 1 are the ones still in L2 when pass 2 starts).
 struct StepIter {
-  int ord, item, bl, nbl, gb0, col0, s, blk;
+  int ord, item, bl, nbl, gb0, col0, s, blk, tap;
   bool rev;
   __device__ __forceinline__ void begin(const Args& a, bool reverse) {
     rev = reverse;
@@ -105,8 +109,14 @@ struct StepIter {
   __device__ __forceinline__ void start(const Args& a) {
     if (ord >= a.items) return;
     item = rev ? a.items - 1 - ord : ord;
-    const int g = item / a.ncol_tiles;
-    col0 = (item - g * a.ncol_tiles) * kCols;
+    int rest = item;
+    tap = 0;
+    if (a.taps) {  // taps innermost: concurrent CTAs reuse the same x pixels through L2
+      rest = item / a.taps;
+      tap = item - rest * a.taps;
+    }
+    const int g = rest / a.ncol_tiles;
+    col0 = (rest - g * a.ncol_tiles) * kCols;
     gb0 = g * a.nb;
     nbl = min(a.nb, a.total_blocks - gb0);
     bl = 0;
@@ -228,6 +238,13 @@ __device__ __forceinline__ void consume(const Args& a, const Quant& qx, const Qu
               pv[i] = make_float2(__uint_as_float(w.x), __uint_as_float(w.y));
             }
           }
+          // conv: the im2col walk runs on into the next image after the last
+          // pixel of this one; the reference zero-pads L (tensor.py:125-135)
+          if (a.taps && rvalid < 16) {
+#pragma unroll
+            for (int i = 0; i < 16; ++i)
+              if (i >= rvalid) pv[i] = make_float2(0.0f, 0.0f);
+          }
           fwht16_pair(pv);
           if (MODE == kStats) {
 #pragma unroll
@@ -282,25 +299,26 @@ __device__ __forceinline__ void consume(const Args& a, const Quant& qx, const Qu
       asm volatile("bar.sync 1, %0;" ::"n"(kFlushThreads));
       const int run = it.nbl * rank;
       const int64_t k0 = int64_t(it.gb0) * rank;
+      const int orow = a.taps ? a.taps : 1;  // payload row of column c: c (Linear) or c*taps + tap (conv)
       const int ncols = min(kCols, a.cols - it.col0);
       if ((run & 15) == 0 && (k0 & 15) == 0) {
         const int chunks = run >> 4;
         for (int i = ftid; i < ncols * chunks; i += kFlushThreads) {
           const int c = i / chunks, q = i - c * chunks;
-          *reinterpret_cast<uint4*>(a.dst_gw + (it.col0 + c) * a.ld_gw + k0 + 16 * q) =
+          *reinterpret_cast<uint4*>(a.dst_gw + int64_t((it.col0 + c) * orow + it.tap) * a.ld_gw + k0 + 16 * q) =
               *reinterpret_cast<const uint4*>(cbuf + c * a.cstride + 16 * q);
         }
       } else if ((run & 7) == 0 && (k0 & 7) == 0) {
         const int chunks = run >> 3;
         for (int i = ftid; i < ncols * chunks; i += kFlushThreads) {
           const int c = i / chunks, q = i - c * chunks;
-          *reinterpret_cast<uint2*>(a.dst_gw + (it.col0 + c) * a.ld_gw + k0 + 8 * q) =
+          *reinterpret_cast<uint2*>(a.dst_gw + int64_t((it.col0 + c) * orow + it.tap) * a.ld_gw + k0 + 8 * q) =
               *reinterpret_cast<const uint2*>(cbuf + c * a.cstride + 8 * q);
         }
       } else {
         for (int i = ftid; i < ncols * run; i += kFlushThreads) {
           const int c = i / run, q = i - c * run;
-          a.dst_gw[(it.col0 + c) * a.ld_gw + k0 + q] = int8_t(cbuf[c * a.cstride + q]);
+          a.dst_gw[int64_t((it.col0 + c) * orow + it.tap) * a.ld_gw + k0 + q] = int8_t(cbuf[c * a.cstride + q]);
         }
       }
       asm volatile("bar.sync 1, %0;" ::"n"(kFlushThreads));
@@ -374,7 +392,15 @@ __global__ void __launch_bounds__(kThreads) tma_tile_kernel(const __grid_constan
         while (it.valid(a)) {
           ptx::mbar_wait_sleep(&empty[slot], phase ^ 1);
           ptx::mbar_arrive_expect_tx(&full[slot], 16 * kRow);
-          ptx::tma_load_3d(tiles + slot * 16 * kRow, &map, &full[slot], it.col0, it.blk * 16, it.s);
+          if (a.taps) {
+            const int l0 = it.blk * 16, ho = l0 / a.wo_n, wo = l0 - ho * a.wo_n;
+            const int ti = it.tap / a.kconv, tj = it.tap - ti * a.kconv;
+            ptx::tma_load_im2col_4d(tiles + slot * 16 * kRow, &map, &full[slot], it.col0,
+                                    wo * a.cstr - a.cpad, ho * a.cstr - a.cpad, it.s, uint16_t(tj),
+                                    uint16_t(ti));
+          } else {
+            ptx::tma_load_3d(tiles + slot * 16 * kRow, &map, &full[slot], it.col0, it.blk * 16, it.s);
+          }
           if (++slot == kStages) { slot = 0; phase ^= 1; }
           it.next(a);
         }
@@ -488,6 +514,71 @@ int choose_nb(int total_blocks, int cols, int rank) {
 }
 
 }  // namespace
+
+typedef CUresult (*EncodeIm2colFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                                   const cuuint64_t*, const int*, const int*, cuuint32_t, cuuint32_t,
+                                   const cuuint32_t*, CUtensorMapInterleave, CUtensorMapSwizzle,
+                                   CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+bool launch_conv_acbp_tma(const void* x, int dtype, int B, int H, int W, int C, int k, int stride, int pad,
+                          uint32_t bitmap, int bits, int mode, uint32_t* stats, int8_t* dst, int64_t ld_dst,
+                          float* scale, cudaStream_t stream) {
+  static EncodeIm2colFn enc = [] {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeIm2col", &p, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      return reinterpret_cast<EncodeIm2colFn>(p);
+    return EncodeIm2colFn(nullptr);
+  }();
+  const size_t esz = dtype == kBF16 ? 2 : 4;
+  const int Ho = (H + 2 * pad - k) / stride + 1, Wo = (W + 2 * pad - k) / stride + 1;
+  if (!enc || (reinterpret_cast<uintptr_t>(x) % 16) || (size_t(C) * esz) % 16 || stride > 8 || pad > 127 ||
+      k - 1 - pad > 127 || k > 16 || Ho * Wo < 16)
+    return false;
+  CUtensorMap map;
+  const cuuint64_t dims[4] = {cuuint64_t(C), cuuint64_t(W), cuuint64_t(H), cuuint64_t(B)};
+  const cuuint64_t strides[3] = {cuuint64_t(C) * esz, cuuint64_t(C) * esz * W, cuuint64_t(C) * esz * W * H};
+  const int lower[2] = {-pad, -pad};
+  const int upper[2] = {pad - (k - 1), pad - (k - 1)};
+  const cuuint32_t es[4] = {1, cuuint32_t(stride), cuuint32_t(stride), 1};
+  if (enc(&map, dtype == kBF16 ? CU_TENSOR_MAP_DATA_TYPE_BFLOAT16 : CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4,
+          const_cast<void*>(x), dims, strides, lower, upper, cuuint32_t(kCols), 16, es,
+          CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+          CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
+    return false;
+  Args a{};
+  a.rows = Ho * Wo;
+  a.cols = C;
+  a.nblk = (a.rows + 15) / 16;
+  a.total_blocks = B * a.nblk;
+  a.rank = __builtin_popcount(bitmap);
+  a.taps = k * k;
+  a.kconv = k;
+  a.cstr = stride;
+  a.cpad = pad;
+  a.wo_n = Wo;
+  a.ncol_tiles = (C + kCols - 1) / kCols;
+  {
+    int nb = a.rank >= 8 ? 4 : (a.rank >= 4 ? 8 : 16);
+    while (nb > 1 && ((a.total_blocks + nb - 1) / nb) * a.ncol_tiles * a.taps < num_sms() * 3) nb >>= 1;
+    a.nb = nb;
+  }
+  a.items = ((a.total_blocks + a.nb - 1) / a.nb) * a.ncol_tiles * a.taps;
+  a.bitmap = bitmap;
+  a.bits_gx = bits;
+  a.bits_gw = bits;
+  a.stats = stats;
+  a.dst_gw = dst;
+  a.ld_gw = ld_dst;
+  a.scale_gw = scale;
+  a.cstride = a.nb * a.rank + 16;
+  if (dtype == kBF16)
+    launch_modes<__nv_bfloat16>(map, a, mode, false, true, stream);
+  else
+    launch_modes<float>(map, a, mode, false, true, stream);
+  return true;
+}
 
 void launch_transform(const TransformArgs& t, int mode, cudaStream_t stream) {
   const size_t esz = t.dtype == kBF16 ? 2 : 4;
