@@ -35,12 +35,57 @@ constexpr int kBK = 128;  // bytes of K per stage = one 128B swizzle row
 constexpr int kThreads = 256;
 
 template <int BN, int STAGES>
+struct GemmCfg;
+
+// Per-warp staging for the TMA-store epilogue: 2 buffers x 32 rows x 128 B.
+constexpr uint32_t kStgBytes = 2 * 32 * 128;
+constexpr uint32_t kStgAll = 4 * kStgBytes;
+
+// Fast epilogue of one 32 x 32 chunk (this warp's 32 TMEM lanes = rows) through
+// shared memory and one TMA tile store: rows are written swizzled (SW64 for
+// bf16 / SW128 for fp32, matching the store map) so the row-per-thread 16-byte
+// writes are bank-conflict free; TMA clips rows / columns outside the output.
+__device__ __forceinline__ void store_chunk_tma(const uint32_t (&acc)[32], float fscale, int out_dtype,
+                                                uint8_t* buf, uint32_t lane, const CUtensorMap* map_o,
+                                                int32_t col0, int32_t row0) {
+  float v[32];
+#pragma unroll
+  for (int j = 0; j < 32; ++j) v[j] = __fmul_rn(__int2float_rn(int(acc[j])), fscale);
+  if (out_dtype == kBF16) {
+    uint8_t* rowp = buf + lane * 64;
+    const uint32_t sw = (lane >> 1) & 3;
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      uint32_t w[4];
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        __nv_bfloat162 t = __floats2bfloat162_rn(v[8 * q + 2 * k], v[8 * q + 2 * k + 1]);
+        w[k] = *reinterpret_cast<uint32_t*>(&t);
+      }
+      *reinterpret_cast<uint4*>(rowp + 16 * (q ^ sw)) = make_uint4(w[0], w[1], w[2], w[3]);
+    }
+  } else {
+    uint8_t* rowp = buf + lane * 128;
+    const uint32_t sw = lane & 7;
+#pragma unroll
+    for (int q = 0; q < 8; ++q)
+      *reinterpret_cast<float4*>(rowp + 16 * (q ^ sw)) = make_float4(v[4 * q], v[4 * q + 1], v[4 * q + 2], v[4 * q + 3]);
+  }
+  ptx::fence_proxy_async_smem();
+  __syncwarp();
+  if (lane == 0) {
+    ptx::tma_store_2d(map_o, buf, col0, row0);
+    ptx::bulk_commit();
+  }
+}
+
+template <int BN, int STAGES>
 struct GemmCfg {
   static constexpr uint32_t kABytes = kBM * kBK;
   static constexpr uint32_t kBBytes = BN * kBK;
   static constexpr uint32_t kStageBytes = kABytes + kBBytes;
   static constexpr uint32_t kTmemCols = 2 * BN;  // 256 or 512: power of two
-  static constexpr size_t kSmem = size_t(STAGES) * kStageBytes + 1024 /*align*/ + 256 /*barriers*/;
+  static constexpr size_t kSmem = size_t(STAGES) * kStageBytes + kStgAll + 1024 /*align*/ + 256 /*barriers*/;
 };
 
 __device__ __forceinline__ void store_row_chunk(const uint32_t (&acc)[32], int64_t row, int64_t col0,
@@ -123,6 +168,7 @@ struct ConvGeo {
 template <int BN, int STAGES>
 __global__ void __launch_bounds__(kThreads, 1)
     gemm_i8_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant__ CUtensorMap map_b,
+                   const __grid_constant__ CUtensorMap map_o, int tma_out,
                    int M, int N, int K, int groups, const float* __restrict__ sa, const float* __restrict__ sb,
                    double extra, int epilogue, void* out, int out_dtype, int64_t ldo,
                    int32_t* acc_out, int64_t ld_acc, int splits, int32_t* __restrict__ slabs,
@@ -133,7 +179,8 @@ __global__ void __launch_bounds__(kThreads, 1)
                                              ~uintptr_t(1023));
   uint8_t* sA = smem;
   uint8_t* sB = smem + STAGES * Cfg::kABytes;
-  uint64_t* full = reinterpret_cast<uint64_t*>(sB + STAGES * Cfg::kBBytes);
+  uint8_t* stg = sB + STAGES * Cfg::kBBytes;  // 1024-aligned: stage bytes are multiples of 1 KB
+  uint64_t* full = reinterpret_cast<uint64_t*>(stg + kStgAll);
   uint64_t* empty = full + STAGES;
   uint64_t* tfull = empty + STAGES;
   uint64_t* tempty = tfull + 2;
@@ -255,7 +302,23 @@ __global__ void __launch_bounds__(kThreads, 1)
       ptx::tc_fence_after();
       const int rl = quarter * 32 + lane;  // row inside the tile
       const int64_t row = int64_t(mb) * kBM + rl;
-      if (splits == 1) {
+      if (splits == 1 && tma_out) {
+        uint8_t* wbuf = stg + quarter * kStgBytes;
+        const int32_t row0 = mb * kBM + int32_t(quarter) * 32;
+#pragma unroll 1
+        for (int c = 0; c < BN / 32; ++c) {
+          const int32_t col0 = nb * BN + c * 32;
+          uint32_t r[32];
+          ptx::tmem_ld_32x32b_x32(tmem_base + ((quarter * 32) << 16) + uint32_t(acc * BN + c * 32), r);
+          ptx::tmem_ld_wait();
+          if (lane == 0) ptx::bulk_wait_read<1>();  // the store that used this buffer 2 chunks ago
+          __syncwarp();
+          if (row0 < M && col0 < N)
+            store_chunk_tma(r, fscale, out_dtype, wbuf + (c & 1) * (kStgBytes / 2), lane, &map_o, col0, row0);
+        }
+        ptx::tc_fence_before();
+        ptx::mbar_arrive(&tempty[acc]);
+      } else if (splits == 1) {
 #pragma unroll 1
         for (int c = 0; c < BN / 32; ++c) {
           const int64_t col0 = int64_t(nb) * BN + c * 32;
@@ -298,10 +361,194 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
   }
 
+  if (warp >= 4 && lane == 0) ptx::bulk_wait_read<0>();  // staging reads done before the CTA exits
   ptx::tc_fence_before();
   __syncthreads();
   ptx::tc_fence_after();
   if (warp == 2) ptx::tmem_dealloc(tmem_base, Cfg::kTmemCols);
+}
+
+// CTA-pair variant (tcgen05 cta_group::2): a cluster of 2 CTAs on one TPC
+// computes a 256 x BN tile.  CTA r stages A rows [128 r, 128 r + 128) and B
+// rows [BN/2 r, BN/2 r + BN/2) of every K block in its own shared memory, and
+// its TMEM holds its 128 accumulator rows; only the leader (rank 0) issues the
+// MMAs.  Per SM that is 16 + BN/2*128/1024 KB of operands per 128-byte K block
+// for 128 x BN MACs -- a third less L2->SM traffic than the 128 x BN single-CTA
+// tile, which is what bounds the dX / dW products (~46 B/clk/SM measured).
+// Pipelines: both producers wait on their own `empty` (the leader's MMA commit
+// multicasts to both CTAs) and complete bytes on the LEADER's `full`; the MMA
+// commit multicasts `tfull` to both CTAs; every epilogue warp of both CTAs
+// arrives on the leader's `tempty`.
+template <int BN, int STAGES>
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
+    gemm_i8_2sm_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant__ CUtensorMap map_b,
+                       const __grid_constant__ CUtensorMap map_o, int tma_out, int M, int N, int K, int groups, const float* __restrict__ sa,
+                       const float* __restrict__ sb, double extra, int epilogue, void* out, int out_dtype,
+                       int64_t ldo, int32_t* acc_out, int64_t ld_acc, int splits,
+                       int32_t* __restrict__ slabs) {
+  constexpr uint32_t kABytes = kBM * kBK;             // this CTA's 128 rows of A
+  constexpr uint32_t kBBytes = (BN / 2) * kBK;        // this CTA's BN/2 rows of B
+  constexpr uint32_t kStageBytes = kABytes + kBBytes;
+  constexpr uint32_t kTmemCols = 2 * BN;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
+                                             ~uintptr_t(1023));
+  uint8_t* sA = smem;
+  uint8_t* sB = smem + STAGES * kABytes;
+  uint8_t* stg = sB + STAGES * kBBytes;
+  uint64_t* full = reinterpret_cast<uint64_t*>(stg + kStgAll);
+  uint64_t* empty = full + STAGES;
+  uint64_t* tfull = empty + STAGES;
+  uint64_t* tempty = tfull + 2;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+
+  const uint32_t warp = ptx::warp_id();
+  const uint32_t lane = ptx::lane_id();
+  const uint32_t rank = ptx::cluster_rank();
+  const bool leader = rank == 0;
+
+  if (warp == 0 && lane == 0) {
+    ptx::tma_prefetch_desc(&map_a);
+    ptx::tma_prefetch_desc(&map_b);
+  }
+  if (warp == 1 && lane == 0) {
+    for (int s = 0; s < STAGES; ++s) {
+      ptx::mbar_init(&full[s], 1);
+      ptx::mbar_init(&empty[s], 1);
+    }
+    for (int a = 0; a < 2; ++a) {
+      ptx::mbar_init(&tfull[a], 1);
+      ptx::mbar_init(&tempty[a], 8);  // 4 epilogue warps x 2 CTAs
+    }
+    ptx::fence_mbar_init();
+  }
+  if (warp == 2) ptx::tmem_alloc_2sm(tmem_slot, kTmemCols);
+  ptx::tc_fence_before();
+  ptx::cluster_sync();  // barrier inits visible to the peer before any remote arrive / TMA
+  ptx::tc_fence_after();
+  const uint32_t tmem_base = *tmem_slot;
+
+  const int num_m = (M + 2 * kBM - 1) / (2 * kBM);
+  const int num_n = (N + BN - 1) / BN;
+  const int tiles = num_m * num_n;
+  const int units = tiles * splits;
+  const int nk_g = (K + kBK - 1) / kBK;
+  const int nk = nk_g * groups;
+  const int cid = blockIdx.x >> 1, ncl = gridDim.x >> 1;
+  const uint32_t full_leader = ptx::mapa(ptx::smem_u32(full), 0);
+  const uint32_t tempty_leader = ptx::mapa(ptx::smem_u32(tempty), 0);
+
+  if (warp == 0) {
+    if (ptx::elect_one()) {
+      int stage = 0;
+      uint32_t phase = 0;
+      for (int u = cid; u < units; u += ncl) {
+        const int t = u / splits, sp = u - t * splits;
+        const int mb = t / num_n, nb = t - mb * num_n;
+        const int kb0 = int(int64_t(sp) * nk / splits), kb1 = int(int64_t(sp + 1) * nk / splits);
+        int g = kb0 / nk_g, kg = kb0 - g * nk_g;
+        for (int kb = kb0; kb < kb1; ++kb) {
+          ptx::mbar_wait_sleep(&empty[stage], phase ^ 1);
+          if (leader) ptx::mbar_arrive_expect_tx(&full[stage], 2 * kStageBytes);
+          const uint32_t fb = full_leader + uint32_t(stage) * 8u;
+          ptx::tma_load_3d_2sm(sA + stage * kABytes, &map_a, fb, kg * kBK, mb * 2 * kBM + int(rank) * kBM, g);
+          ptx::tma_load_3d_2sm(sB + stage * kBBytes, &map_b, fb, kg * kBK, nb * BN + int(rank) * (BN / 2), g);
+          if (++kg == nk_g) { kg = 0; ++g; }
+          if (++stage == STAGES) { stage = 0; phase ^= 1; }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    if (leader) {
+      constexpr uint32_t idesc = ptx::idesc_i8(2 * kBM, BN);
+      int stage = 0;
+      uint32_t phase = 0;
+      int acc = 0;
+      uint32_t acc_phase = 0;
+      for (int u = cid; u < units; u += ncl) {
+        const int sp = u % splits;
+        const int kb0 = int(int64_t(sp) * nk / splits), kb1 = int(int64_t(sp + 1) * nk / splits);
+        ptx::mbar_wait_sleep(&tempty[acc], acc_phase ^ 1);
+        ptx::tc_fence_after();
+        const uint32_t d_tmem = tmem_base + uint32_t(acc * BN);
+        for (int kb = kb0; kb < kb1; ++kb) {
+          ptx::mbar_wait(&full[stage], phase);
+          ptx::tc_fence_after();
+          if (ptx::elect_one()) {
+            const uint64_t a_desc = ptx::desc_kmajor_sw128(ptx::smem_u32(sA + stage * kABytes));
+            const uint64_t b_desc = ptx::desc_kmajor_sw128(ptx::smem_u32(sB + stage * kBBytes));
+#pragma unroll
+            for (int k = 0; k < kBK / 32; ++k)
+              ptx::mma_i8_2sm(d_tmem, a_desc + uint64_t((k * 32) >> 4), b_desc + uint64_t((k * 32) >> 4), idesc,
+                              (kb != kb0 || k != 0) ? 1u : 0u);
+            ptx::mma_commit_2sm(&empty[stage], 0x3);
+            if (kb == kb1 - 1) ptx::mma_commit_2sm(&tfull[acc], 0x3);
+          }
+          __syncwarp();
+          if (++stage == STAGES) { stage = 0; phase ^= 1; }
+        }
+        if (++acc == 2) { acc = 0; acc_phase ^= 1; }
+      }
+    }
+  } else if (warp >= 4) {
+    const uint32_t quarter = warp & 3;
+    const float comb = __fmul_rn(*sa, *sb);
+    const double dscale = __dmul_rn(double(comb), extra);
+    const float fscale = float(dscale);
+    const bool vec_ok = (ldo % 8 == 0) && ((reinterpret_cast<uintptr_t>(out) & 15) == 0);
+    int acc = 0;
+    uint32_t acc_phase = 0;
+    for (int u = cid; u < units; u += ncl) {
+      const int t = u / splits, sp = u - t * splits;
+      const int mb = t / num_n, nb = t - mb * num_n;
+      ptx::mbar_wait_sleep(&tfull[acc], acc_phase);
+      ptx::tc_fence_after();
+      const int64_t row = int64_t(mb) * 2 * kBM + int64_t(rank) * kBM + quarter * 32 + lane;
+      const int32_t row0 = mb * 2 * kBM + int32_t(rank) * kBM + int32_t(quarter) * 32;
+      uint8_t* wbuf = stg + quarter * kStgBytes;
+#pragma unroll 1
+      for (int c = 0; c < BN / 32; ++c) {
+        const int64_t col0 = int64_t(nb) * BN + c * 32;
+        uint32_t r[32];
+        ptx::tmem_ld_32x32b_x32(tmem_base + ((quarter * 32) << 16) + uint32_t(acc * BN + c * 32), r);
+        ptx::tmem_ld_wait();
+        if (splits == 1 && tma_out) {
+          if (lane == 0) ptx::bulk_wait_read<1>();
+          __syncwarp();
+          if (row0 < M && col0 < N)
+            store_chunk_tma(r, fscale, out_dtype, wbuf + (c & 1) * (kStgBytes / 2), lane, &map_o, int32_t(col0),
+                            row0);
+        } else if (row < M && col0 < N) {
+          if (splits == 1) {
+            store_row_chunk(r, row, col0, N, epilogue, dscale, fscale, out, out_dtype, ldo, vec_ok, acc_out,
+                            ld_acc);
+          } else {
+            int32_t* d = slabs + int64_t(sp) * M * N + row * N + col0;
+            if (col0 + 32 <= N && (N & 3) == 0) {
+#pragma unroll
+              for (int j = 0; j < 32; j += 4)
+                __stcg(reinterpret_cast<int4*>(d + j),
+                       make_int4(int(r[j]), int(r[j + 1]), int(r[j + 2]), int(r[j + 3])));
+            } else {
+#pragma unroll
+              for (int j = 0; j < 32; ++j)
+                if (col0 + j < N) d[j] = int(r[j]);
+            }
+          }
+        }
+      }
+      ptx::tc_fence_before();
+      __syncwarp();
+      if (lane == 0) ptx::mbar_arrive_cluster(tempty_leader + uint32_t(acc) * 8u);
+      if (++acc == 2) { acc = 0; acc_phase ^= 1; }
+    }
+  }
+
+  if (warp >= 4 && lane == 0) ptx::bulk_wait_read<0>();
+  ptx::tc_fence_before();
+  ptx::cluster_sync();
+  ptx::tc_fence_after();
+  if (warp == 2) ptx::tmem_dealloc_2sm(tmem_base, kTmemCols);
 }
 
 // out[m, n] = dequant(sum_s slab[s][m, n]) (+ the exact int32 sum into acc_out).
@@ -378,6 +625,27 @@ bool make_map(CUtensorMap* map, const int8_t* ptr, int64_t rows, int64_t k, int6
             CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
+// Store map of the output for the TMA epilogue: (N, M) with row stride ldo,
+// 32 x 32 boxes, swizzle matching store_chunk_tma.  False = use the direct
+// store epilogue (exact fp64 dequant, int32 accumulator dump, split-K slabs or
+// an output TMA cannot describe).
+bool make_out_map(CUtensorMap* map, void* out, int out_dtype, int64_t M, int64_t N, int64_t ldo, int epilogue,
+                  const int32_t* acc_out, int splits) {
+  if (!out || acc_out || splits != 1 || epilogue != kEpiFast) return false;
+  const int64_t esz = out_dtype == kBF16 ? 2 : 4;
+  if ((reinterpret_cast<uintptr_t>(out) % 16) || (ldo * esz) % 16 || M <= 0 || N <= 0) return false;
+  EncodeTiledFn fn = encode_fn();
+  if (!fn) return false;
+  cuuint64_t dims[2] = {cuuint64_t(N), cuuint64_t(M)};
+  cuuint64_t strides[1] = {cuuint64_t(ldo * esz)};
+  cuuint32_t box[2] = {32, 32};
+  cuuint32_t es[2] = {1, 1};
+  return fn(map, out_dtype == kBF16 ? CU_TENSOR_MAP_DATA_TYPE_BFLOAT16 : CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, out,
+            dims, strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
+            out_dtype == kBF16 ? CU_TENSOR_MAP_SWIZZLE_64B : CU_TENSOR_MAP_SWIZZLE_128B,
+            CU_TENSOR_MAP_L2_PROMOTION_NONE, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
 }  // namespace
 
 bool encode_tensor_map(void* map, int dtype, int rank, const void* ptr, const uint64_t* dims,
@@ -420,9 +688,12 @@ int run_maps(const CUtensorMap& ma, const CUtensorMap& mb, int64_t M, int64_t N,
   int32_t* slabs = splits > 1 ? static_cast<int32_t*>(ws) : nullptr;
   const int64_t units = tiles * splits;
   const int grid = int(units < num_sms() ? units : num_sms());
+  CUtensorMap mo;
+  const int tma_out = make_out_map(&mo, out, out_dtype, M, N, ldo, epilogue, acc_out, splits) ? 1 : 0;
+  if (!tma_out) mo = ma;  // unused
   gemm_i8_kernel<BN, STAGES><<<grid, kThreads, Cfg::kSmem, stream>>>(
-      ma, mb, int(M), int(N), int(K), int(groups), sa, sb, extra, epilogue, out, out_dtype, ldo, acc_out, ld_acc,
-      splits, slabs, geo);
+      ma, mb, mo, tma_out, int(M), int(N), int(K), int(groups), sa, sb, extra, epilogue, out, out_dtype, ldo,
+      acc_out, ld_acc, splits, slabs, geo);
   if (splits > 1) {
     const int64_t nq = M * N / 4;
     int fgrid = int((nq + 255) / 256);
@@ -444,6 +715,44 @@ int run(const int8_t* A, int64_t lda, const int8_t* B, int64_t ldb, int64_t M, i
   const ConvGeo geo{0, 0, 0, 0, 0, 0};
   return run_maps<BN, STAGES>(ma, mb, M, N, K, groups, sa, sb, extra, epilogue, out, out_dtype, ldo, acc_out,
                               ld_acc, splits, ws, geo, stream);
+}
+
+template <int BN, int STAGES>
+int run_2sm(const int8_t* A, int64_t lda, const int8_t* B, int64_t ldb, int64_t M, int64_t N, int64_t K,
+            int64_t groups, int64_t a_gstride, int64_t b_gstride, const float* sa, const float* sb, double extra,
+            int epilogue, void* out, int out_dtype, int64_t ldo, int32_t* acc_out, int64_t ld_acc, int splits,
+            void* ws, cudaStream_t stream) {
+  constexpr size_t kSmem = size_t(STAGES) * (kBM * kBK + (BN / 2) * kBK) + kStgAll + 1024 + 256;
+  CUtensorMap ma, mb;
+  if (!make_map(&ma, A, M, K, lda, groups, a_gstride, kBM) ||
+      !make_map(&mb, B, N, K, ldb, groups, b_gstride, BN / 2))
+    return -1;
+  static bool attr_set = false;
+  if (!attr_set) {
+    cudaError_t e = cudaFuncSetAttribute(gemm_i8_2sm_kernel<BN, STAGES>,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize, int(kSmem));
+    if (e != cudaSuccess) return int(e);
+    attr_set = true;
+  }
+  const int64_t tiles = ((M + 2 * kBM - 1) / (2 * kBM)) * ((N + BN - 1) / BN);
+  const int64_t units = tiles * splits;
+  const int64_t pairs = num_sms() / 2;
+  const int grid = 2 * int(units < pairs ? units : pairs);
+  int32_t* slabs = splits > 1 ? static_cast<int32_t*>(ws) : nullptr;
+  CUtensorMap mo;
+  const int tma_out = make_out_map(&mo, out, out_dtype, M, N, ldo, epilogue, acc_out, splits) ? 1 : 0;
+  if (!tma_out) mo = ma;  // unused
+  gemm_i8_2sm_kernel<BN, STAGES><<<grid, kThreads, kSmem, stream>>>(
+      ma, mb, mo, tma_out, int(M), int(N), int(K), int(groups), sa, sb, extra, epilogue, out, out_dtype, ldo,
+      acc_out, ld_acc, splits, slabs);
+  if (splits > 1) {
+    const int64_t nq = M * N / 4;
+    int fgrid = int((nq + 255) / 256);
+    if (fgrid > num_sms() * 8) fgrid = num_sms() * 8;
+    splitk_finalize<<<fgrid, 256, 0, stream>>>(slabs, splits, int(M), int(N), sa, sb, extra, epilogue, out,
+                                               out_dtype, ldo, acc_out, ld_acc);
+  }
+  return int(cudaGetLastError());
 }
 
 typedef CUresult (*EncodeIm2colFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
@@ -470,16 +779,35 @@ EncodeIm2colFn encode_im2col_fn() {
 struct GemmPlan {
   int bn, splits;
   size_t ws;
+  bool pair;  // CTA-pair (cta_group::2) 256 x bn tiles
 };
+
+GemmPlan finish_plan(GemmPlan p, int64_t M, int64_t N, bool allow_split);
 
 GemmPlan plan_gemm(int64_t M, int64_t N, int64_t K, int64_t groups, bool allow_split) {
   const int64_t m_tiles = (M + kBM - 1) / kBM;
   const int64_t wide_tiles = m_tiles * ((N + 255) / 256);
   const int64_t nk = ((K + kBK - 1) / kBK) * groups;
   const int64_t sms = num_sms();
-  GemmPlan p{128, 1, 0};
+  GemmPlan p{128, 1, 0, false};
   if (N > 128 && wide_tiles >= sms) p.bn = 256;
   const int64_t tiles = m_tiles * ((N + p.bn - 1) / p.bn);
+  // Long contractions with enough rows run as CTA pairs (cta_group::2, 256-row
+  // tiles: a third less operand traffic per MAC).  Tile width by a makespan
+  // model: rounds of pair units x relative unit cost (a 256 x 128 unit costs
+  // ~0.6 of a 256 x 256 one; tools/gemm_sweep.py, B200).  Short K (e.g. the
+  // fc2 dX, K = 768) stays single-CTA: its epilogue, not the operand stream,
+  // dominates.
+  const int64_t tiles128 = m_tiles * ((N + 127) / 128);
+  const bool split_case = allow_split && 2 * tiles128 <= sms && nk >= 16 && N % 4 == 0;
+  if (!split_case && nk >= 16 && M >= 2 * kBM && sms >= 2) {
+    const int64_t pairs = sms / 2, pm = (M + 2 * kBM - 1) / (2 * kBM);
+    const int64_t u256 = pm * ((N + 255) / 256), u128 = pm * ((N + 127) / 128);
+    const double t256 = double((u256 + pairs - 1) / pairs), t128 = 0.6 * double((u128 + pairs - 1) / pairs);
+    p.pair = true;
+    p.bn = (N > 128 && t256 <= t128) ? 256 : 128;
+    return finish_plan(p, M, N, allow_split);
+  }
   // Split-K only for products that fill less than half the SMs (e.g. the ViT
   // proj dW, 36 tiles of K = 13312): the slab round trip costs ~6 us per split
   // at fc1 size, which outweighs the wave gain once >= half the SMs are busy
@@ -491,8 +819,12 @@ GemmPlan plan_gemm(int64_t M, int64_t N, int64_t K, int64_t groups, bool allow_s
     while (sp > 1 && nk / sp < 8) --sp;
     p.splits = int(sp);
   }
-  // tuning knobs (development sweeps): HLQ_GEMM_SPLITS=s forces s splits (1 = off),
-  // HLQ_GEMM_BN=128|256 forces the tile width
+  return finish_plan(p, M, N, allow_split);
+}
+
+// tuning knobs (development sweeps): HLQ_GEMM_SPLITS=s forces s splits (1 = off),
+// HLQ_GEMM_BN=128|256 forces the tile width, HLQ_GEMM_PAIR=0|1 the CTA-pair kernel
+GemmPlan finish_plan(GemmPlan p, int64_t M, int64_t N, bool allow_split) {
   if (const char* e = getenv("HLQ_GEMM_BN")) {
     const int bn = atoi(e);
     if (bn == 128 || (bn == 256 && N > 128)) p.bn = bn;
@@ -501,6 +833,7 @@ GemmPlan plan_gemm(int64_t M, int64_t N, int64_t K, int64_t groups, bool allow_s
     const int s = atoi(e);
     if (s >= 1 && s <= 64 && allow_split && N % 4 == 0) p.splits = s;
   }
+  if (const char* e = getenv("HLQ_GEMM_PAIR")) p.pair = atoi(e) != 0;
   if (p.splits > 1) p.ws = size_t(p.splits) * M * N * 4;
   return p;
 }
@@ -521,6 +854,13 @@ int launch_gemm_i8(const int8_t* A, int64_t lda, const int8_t* B, int64_t ldb, i
                        (ld_acc % 4 == 0) && (reinterpret_cast<uintptr_t>(acc_out) % 16 == 0);
   if (p.splits > 1 && (ws == nullptr || ws_bytes < p.ws || !vec_out || (reinterpret_cast<uintptr_t>(ws) % 16)))
     p = plan_gemm(M, N, K, groups, false);
+  if (p.pair) {
+    if (p.bn == 256)
+      return run_2sm<256, 6>(A, lda, B, ldb, M, N, K, groups, a_gstride, b_gstride, sa, sb, extra, epilogue, out,
+                             out_dtype, ldo, acc_out, ld_acc, p.splits, ws, stream);
+    return run_2sm<128, 8>(A, lda, B, ldb, M, N, K, groups, a_gstride, b_gstride, sa, sb, extra, epilogue, out,
+                           out_dtype, ldo, acc_out, ld_acc, p.splits, ws, stream);
+  }
   if (p.bn == 256)
     return run<256, 4>(A, lda, B, ldb, M, N, K, groups, a_gstride, b_gstride, sa, sb, extra, epilogue, out,
                        out_dtype, ldo, acc_out, ld_acc, p.splits, ws, stream);

@@ -23,19 +23,25 @@ def main():
         a = torch.randint(-127, 128, (M, K), dtype=torch.int8, device="cuda")
         b = torch.randint(-127, 128, (N, K), dtype=torch.int8, device="cuda")
         res = {}
-        for bn in ("128", "256"):
-            for s in ("1", "2", "3", "4", "6", "8", "12"):
+        for pair in ("0", "1"):
+          for bn in ("128", "256"):
+            for s in ("1", "2", "4"):
                 if name.endswith("dx") and s != "1":
                     continue
                 os.environ["HLQ_GEMM_BN"], os.environ["HLQ_GEMM_SPLITS"] = bn, s
+                os.environ["HLQ_GEMM_PAIR"] = pair
                 us = timeit(lambda: ops.gemm_i8(a, b, M, N, K, 8, 8, sa, sa, 1.0, exact=False,
                                                 out_dtype=torch.bfloat16 if name.endswith("dx") else torch.float32),
                             iters=10, flush=flush)
-                res[f"bn{bn}_s{s}"] = round(us, 1)
+                res[f"{'p' if pair == '1' else 'c'}{bn}_s{s}"] = round(us, 1)
         os.environ.pop("HLQ_GEMM_BN")
         os.environ.pop("HLQ_GEMM_SPLITS")
-        res["auto"] = round(timeit(lambda: ops.gemm_i8(a, b, M, N, K, 8, 8, sa, sa, 1.0, exact=False),
+        os.environ.pop("HLQ_GEMM_PAIR")
+        res["auto"] = round(timeit(lambda: ops.gemm_i8(a, b, M, N, K, 8, 8, sa, sa, 1.0, exact=False,
+                                                       out_dtype=torch.bfloat16 if name.endswith("dx") else torch.float32),
                                    iters=10, flush=flush), 1)
+        res["torch_int_mm"] = round(timeit(lambda: torch._int_mm(a, b.t()), iters=10, flush=flush), 1) \
+            if M % 8 == 0 and N % 8 == 0 and K % 8 == 0 else None
         best = min(res, key=res.get)
         print(json.dumps({"gemm": name, "MNK": [M, N, K], "tops_best": round(2 * M * N * K / res[best] / 1e6, 1),
                           "best": best, **res}), flush=True)
