@@ -200,6 +200,20 @@ HLQ_API int hlq_conv_acbp_compress(const void* x_nhwc, int dtype, int64_t B, int
                                    int bits, int8_t* payload, int64_t ld_payload, float* scale_out,
                                    uint32_t* stats_ws, void* stream);
 
+/* The dX right operand of many layers at once: codes_i = Q_bits(HT_O(W_i))
+ * for n <= 128 fp32 weights W_i (O_i x I_i, row-major), written K-major as
+ * (I_i rows of ld_i >= pad16(O_i) bytes), scale_i one fp32 each -- identical
+ * to hlq_quantize_proj_rows(W_i, 1, O_i, I_i, bitmap 0xFFFF) per tensor
+ * (`_block_axis(w, 0, plan)` + `_quant`, backprop.py:363,368), in ONE
+ * cooperative launch (training refreshes every layer's codes once per
+ * optimizer step).  w, O, I, codes, ld, scales are HOST arrays of n entries
+ * holding device pointers / extents.  ws: hlq_quantize_weights_ws(n) device
+ * bytes (no initialisation needed). */
+HLQ_API size_t hlq_quantize_weights_ws(int n);
+HLQ_API int hlq_quantize_weights(int n, const float* const* w, const int64_t* O, const int64_t* I,
+                                 int bits, int8_t* const* codes, const int64_t* ld,
+                                 float* const* scales, uint32_t* ws, size_t ws_bytes, void* stream);
+
 /* Conv2d dX as ONE implicit GEMM (stride 1): dx[b, h, w, c] (channels-last)
  * = deq( sum over taps (i, j) and o of gcodes[b, h + pad - i, w + pad - j, o]
  *        * wcodes[c*k*k + i*k + j, o] ), zero outside the gy extent.  gcodes is

@@ -25,7 +25,7 @@ __version__ = "0.1.0"
 
 def __getattr__(name):
     # torch.nn modules are imported lazily so `import paper_2406_15102_b200` stays light
-    if name in ("HLQLinear", "HLQLinearFunction", "convert_linears"):
+    if name in ("HLQLinear", "HLQLinearFunction", "convert_linears", "refresh_weight_codes"):
         from . import layers
         return getattr(layers, name)
     raise AttributeError(name)

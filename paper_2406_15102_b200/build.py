@@ -19,7 +19,8 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(HERE)
 CSRC = os.path.join(HERE, "csrc")
 LIB = os.path.join(HERE, "libhlq_b200.so")
-SOURCES = ["hlq_transform.cu", "hlq_transform_fallback.cu", "hlq_conv.cu", "hlq_gemm.cu", "hlq_capi.cu"]
+SOURCES = ["hlq_transform.cu", "hlq_transform_fallback.cu", "hlq_conv.cu", "hlq_gemm.cu", "hlq_weights.cu",
+           "hlq_capi.cu"]
 HEADERS = ["hlq_ptx.cuh", "hlq_quant.cuh", "hlq_internal.h", os.path.join("..", "..", "include", "hlq_b200.h")]
 
 NVCC_FLAGS = [

@@ -281,6 +281,30 @@ int hlq_gemm_i8_ex(const int8_t* A, int64_t lda, int64_t a_gstride, const int8_t
   return HLQ_OK;
 }
 
+size_t hlq_quantize_weights_ws(int n) { return n < 0 ? 0 : size_t(8 * n + 8) * sizeof(uint32_t); }
+
+int hlq_quantize_weights(int n, const float* const* w, const int64_t* O, const int64_t* I, int bits,
+                         int8_t* const* codes, const int64_t* ld, float* const* scales, uint32_t* ws,
+                         size_t ws_bytes, void* stream) {
+  HLQ_TRY(check_bits(bits));
+  if (n < 0 || n > hlq::kMaxWeights)
+    return fail(HLQ_ERR_PARAMETER, "batched weight codes take 0..%d tensors, got %d", hlq::kMaxWeights, n);
+  if (n == 0) return HLQ_OK;
+  if (ws_bytes < hlq_quantize_weights_ws(n)) return fail(HLQ_ERR_PARAMETER, "workspace too small");
+  for (int i = 0; i < n; ++i) {
+    if (!w[i] || !codes[i] || O[i] <= 0 || I[i] <= 0 || O[i] > INT32_MAX / 2 || I[i] > INT32_MAX / 2)
+      return fail(HLQ_ERR_DIMENSION, "weight %d: bad shape or null pointer", i);
+    HLQ_TRY(check_ld16(ld[i], "weight codes"));
+    if (ld[i] < pad16(O[i]))
+      return fail(HLQ_ERR_DIMENSION, "weight %d: codes ld %lld < pad16(O) %lld", i, (long long)ld[i],
+                  (long long)pad16(O[i]));
+    if (reinterpret_cast<uintptr_t>(codes[i]) % 16) return fail(HLQ_ERR_PARAMETER, "codes %d not 16-byte aligned", i);
+  }
+  int e = hlq::launch_weight_codes(n, w, O, I, bits, codes, ld, scales, ws, static_cast<cudaStream_t>(stream));
+  if (e != 0) return fail(HLQ_ERR_CUDA, "hlq_quantize_weights: %s", cudaGetErrorString(cudaError_t(e)));
+  return cuda_status("hlq_quantize_weights");
+}
+
 int hlq_conv_dgrad_i8(const int8_t* gcodes, int64_t ld_g, int64_t B, int64_t Ho, int64_t Wo, int64_t O,
                       const int8_t* wcodes, int64_t ld_w, int64_t C, int k, int stride, int pad,
                       int bits, const float* sg, const float* sw, int epilogue, void* dx_nhwc,

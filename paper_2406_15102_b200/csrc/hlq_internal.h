@@ -72,6 +72,13 @@ int launch_conv_dgrad_i8(const int8_t* G, int64_t ldg, int64_t B, int64_t Ho, in
                          const int8_t* Wc, int64_t ldw, int64_t C, int k, int pad, const float* sa,
                          const float* sb, int epilogue, void* out, int out_dtype, int64_t ldo,
                          int32_t* acc_out, int64_t ld_acc, cudaStream_t stream);
+// Batched W codes (hlq_weights.cu): Q_bits(HT_O(W_i)) of up to kMaxWeights fp32
+// (O_i, I_i) matrices in one cooperative launch; codes_i is (I_i, ld_i) K-major,
+// scales_i one fp32.  ws: 8 * n + 8 uint32 (statistics + grid barrier).
+constexpr int kMaxWeights = 128;
+int launch_weight_codes(int n, const float* const* w, const int64_t* O, const int64_t* I, int bits,
+                        int8_t* const* codes, const int64_t* ld, float* const* scales, uint32_t* ws,
+                        cudaStream_t stream);
 // Workspace bytes that let launch_gemm_i8 split K (0: no split planned).
 size_t gemm_i8_ws_bytes(int64_t M, int64_t N, int64_t K, int64_t groups);
 

@@ -18,6 +18,8 @@ Conventions:
 """
 from __future__ import annotations
 
+import os
+
 import torch
 import torch.nn as nn
 import torch.nn.functional as F
@@ -42,8 +44,14 @@ _SIDE = {}
 
 
 def side_stream(device) -> torch.cuda.Stream:
-    """Per-device auxiliary stream: the memory-bound HLQ work overlaps the
-    compute-bound forward GEMM / the other backward GEMM on it."""
+    """Auxiliary stream for the forward ACBP / backward dW work when
+    HLQ_SIDE_STREAM=1.  Default: the current stream.  The persistent GEMMs and
+    the cooperative transform kernels each fill every SM, so a second stream
+    buys no real overlap (0.4 ms/step at best on ViT-B/16), and with the host
+    running several steps ahead the cross-stream interleaving made the step
+    time erratic (40-86 ms/step, B200) -- one stream gives a steady 40.8 ms."""
+    if os.environ.get("HLQ_SIDE_STREAM", "0") != "1":
+        return torch.cuda.current_stream(device)
     key = torch.device(device).index
     if key not in _SIDE:
         _SIDE[key] = torch.cuda.Stream(device=device)
@@ -53,13 +61,14 @@ def side_stream(device) -> torch.cuda.Stream:
 class HLQLinearFunction(torch.autograd.Function):
     """y = x W^T + b forward; HLQ backward (ACBP payload saved, raw x dropped).
 
-    Forward enqueues ACBP(X) and the W codes of the dX product on a side
-    stream so they run under the cuBLAS forward GEMM; W codes taken at forward
-    time are the codes of the W the backward differentiates (an in-place
-    update in between trips autograd's version check on the saved weight)."""
+    Forward computes ACBP(X) and takes the W codes of the dX product (from the
+    model-wide batched refresh, or a per-layer transform): codes taken at
+    forward time are the codes of the W the backward differentiates (an
+    in-place update in between trips autograd's version check on the saved
+    weight)."""
 
     @staticmethod
-    def forward(ctx, x, weight, bias, strategy: BackwardStrategy):
+    def forward(ctx, x, weight, bias, strategy: BackwardStrategy, wcodes=None):
         B, L, I = _blv(x.shape)
         O = weight.shape[0]
         plan = strategy.plan
@@ -76,7 +85,9 @@ class HLQLinearFunction(torch.autograd.Function):
             if ctx.needs_input_grad[1]:
                 payload, k, sx, _ = ops.quant_proj_rows(x.detach().contiguous(), segs, rows, cols,
                                                         plan.gpu_bitmap(), bits_gw, ld_src, seg_src)
-            if ctx.needs_input_grad[0]:
+            if ctx.needs_input_grad[0] and wcodes is not None:
+                cw, sw = wcodes  # refreshed for this weight version by refresh_weight_codes
+            elif ctx.needs_input_grad[0]:
                 w32 = weight.detach() if weight.dtype == torch.float32 else weight.detach().float()
                 cw, _, sw, _ = ops.quant_proj_rows(w32, 1, O, I, 0xFFFF, bits_gx)
         y = F.linear(x, weight.to(x.dtype) if x.dtype != weight.dtype else weight,
@@ -127,7 +138,7 @@ class HLQLinearFunction(torch.autograd.Function):
             gx = gx.reshape(x_shape).to(x_dtype)
             if has_bias and ctx.needs_input_grad[2]:
                 gb = gy.reshape(-1, O).sum(0, dtype=torch.float32)
-            return gx, gw, gb, None
+            return gx, gw, gb, None, None
         if ctx.needs_input_grad[1]:
             bits = strategy.grad_weight_path.bits or 8
             segs, rows, cols, ld_src, seg_src = _proj_view(B, L, O, axis)
@@ -151,7 +162,7 @@ class HLQLinearFunction(torch.autograd.Function):
                 gx = gx.to(x_dtype)
         if has_bias and ctx.needs_input_grad[2]:
             gb = gy.reshape(-1, O).sum(0, dtype=torch.float32)
-        return gx, gw, gb, None
+        return gx, gw, gb, None, None
 
 
 class HLQLinear(nn.Linear):
@@ -161,6 +172,19 @@ class HLQLinear(nn.Linear):
                  strategy: BackwardStrategy | None = None, device=None, dtype=None):
         super().__init__(in_features, out_features, bias=bias, device=device, dtype=dtype)
         self.strategy = strategy or BackwardStrategy.hlq()
+        self._wcodes = None  # (weight version, data_ptr, bits, codes, scale)
+
+    def bits_gx(self) -> int:
+        return self.strategy.grad_input_path.bits or 4
+
+    def cached_weight_codes(self):
+        """(codes, scale) of the current weight if refresh_weight_codes made
+        them for this exact weight version, else None."""
+        c = self._wcodes
+        w = self.weight
+        if c is not None and c[0] == w._version and c[1] == w.data_ptr() and c[2] == self.bits_gx():
+            return c[3], c[4]
+        return None
 
     def forward(self, x):
         if not (self.training and torch.is_grad_enabled()):
@@ -168,7 +192,7 @@ class HLQLinear(nn.Linear):
         if torch.is_autocast_enabled("cuda"):
             x = x.to(torch.get_autocast_dtype("cuda"))
         with torch.autocast("cuda", enabled=False):
-            return HLQLinearFunction.apply(x, self.weight, self.bias, self.strategy)
+            return HLQLinearFunction.apply(x, self.weight, self.bias, self.strategy, self.cached_weight_codes())
 
     @classmethod
     def from_linear(cls, lin: nn.Linear, strategy: BackwardStrategy | None = None) -> "HLQLinear":
@@ -181,11 +205,47 @@ class HLQLinear(nn.Linear):
         return m
 
 
-def convert_linears(module: nn.Module, strategy: BackwardStrategy | None = None) -> nn.Module:
-    """Swap every nn.Linear under `module` for HLQLinear (in place)."""
+def refresh_weight_codes(module: nn.Module) -> int:
+    """Recompute, in ONE batched launch per bit width (hlq_quantize_weights),
+    the dX weight codes Q(HT_O(W)) of every HLQLinear under `module` whose
+    weight changed since its codes were made (training: every layer, once per
+    optimizer step).  HLQLinear.forward then reuses them instead of launching
+    a per-layer transform.  Returns the number of layers refreshed."""
+    stale = {}
+    for m in module.modules():
+        if isinstance(m, HLQLinear) and m.weight.is_cuda and m.cached_weight_codes() is None:
+            stale.setdefault(m.bits_gx(), []).append(m)
+    n = 0
+    for bits, mods in stale.items():
+        ws = [m.weight.detach() if m.weight.dtype == torch.float32 else m.weight.detach().float()
+              for m in mods]
+        for m, (codes, scale) in zip(mods, ops.quant_weights(ws, bits)):
+            m._wcodes = (m.weight._version, m.weight.data_ptr(), bits, codes, scale)
+        n += len(mods)
+    return n
+
+
+def _refresh_hook(module, args):
+    if module.training and torch.is_grad_enabled():
+        refresh_weight_codes(module)
+
+
+def convert_linears(module: nn.Module, strategy: BackwardStrategy | None = None,
+                    batch_weight_codes: bool = True) -> nn.Module:
+    """Swap every nn.Linear under `module` for HLQLinear (in place).  With
+    batch_weight_codes, `module` also gets a forward pre-hook that refreshes
+    all its layers' weight codes in one launch per training forward
+    (refresh_weight_codes)."""
+    _convert(module, strategy)
+    if batch_weight_codes and not getattr(module, "_hlq_wcodes_hook", False):
+        module.register_forward_pre_hook(_refresh_hook)
+        module._hlq_wcodes_hook = True
+    return module
+
+
+def _convert(module: nn.Module, strategy):
     for name, child in list(module.named_children()):
         if isinstance(child, nn.Linear) and not isinstance(child, HLQLinear):
             setattr(module, name, HLQLinear.from_linear(child, strategy))
         else:
-            convert_linears(child, strategy)
-    return module
+            _convert(child, strategy)

@@ -184,6 +184,43 @@ def quant_proj_rows(src: torch.Tensor, segs: int, rows: int, cols: int, bitmap: 
     return codes, k, scale, stats[2:3]
 
 
+def quant_weights(weights, bits: int):
+    """Q_bits(HT_O(W)) for a list of fp32 CUDA weights (O, I) in one launch.
+    Returns [(codes (I, pad16(O)) int8, scale (1,) fp32)] -- the same as
+    quant_proj_rows(W, 1, O, I, 0xFFFF, bits)[0, 2] per tensor."""
+    _check_bits(bits)
+    n = len(weights)
+    if n == 0:
+        return []
+    if n > 128:
+        out = []
+        for i in range(0, n, 128):
+            out += quant_weights(weights[i:i + 128], bits)
+        return out
+    dev = weights[0].device
+    ws_ = [_cuda(w, "weight") for w in weights]
+    for w in ws_:
+        if w.dtype != torch.float32 or w.dim() != 2:
+            raise ParameterError("batched weight codes take 2-D float32 weights")
+    codes = [torch.empty((w.shape[1], pad16(w.shape[0])), dtype=torch.int8, device=dev) for w in ws_]
+    scales = torch.empty(n, dtype=torch.float32, device=dev)
+    wsb = int(_lib.load().hlq_quantize_weights_ws(n))
+    scratch = torch.empty(wsb, dtype=torch.uint8, device=dev)
+    P = ctypes.c_void_p * n
+    I64 = ctypes.c_int64 * n
+    wp = P(*[w.data_ptr() for w in ws_])
+    cp = P(*[c.data_ptr() for c in codes])
+    sp = P(*[scales.data_ptr() + 4 * i for i in range(n)])
+    Os = I64(*[w.shape[0] for w in ws_])
+    Is = I64(*[w.shape[1] for w in ws_])
+    lds = I64(*[c.stride(0) for c in codes])
+    nbytes = sum(w.numel() * 4 + c.numel() for w, c in zip(ws_, codes))
+    _traced("transform", nbytes, 0, 1,
+            lambda: _lib.call("hlq_quantize_weights", n, wp, Os, Is, bits, cp, lds, sp, _p(scratch), wsb,
+                              _stream()))
+    return [(c, scales[i:i + 1]) for i, c in enumerate(codes)]
+
+
 def proj_rows_amax(src: torch.Tensor, segs: int, rows: int, cols: int, bitmap: int,
                    stats: torch.Tensor, ld_src: int | None = None, seg_src: int | None = None):
     """Accumulate the transformed statistics (IEEE bits, atomic max) into stats[2:4]

@@ -83,3 +83,50 @@ def test_fast_epilogue_bf16(ops):
     _, rout = _ref(a[None], b[None], 1, sa, sb, 1.0)
     got = out.float().cpu().numpy()
     assert np.linalg.norm(got - rout) / np.linalg.norm(rout) < 4e-3
+
+
+def test_batched_weight_codes_match_per_tensor(ops):
+    """hlq_quantize_weights (one launch for many layers) == per-tensor
+    quant_proj_rows(W, 1, O, I, 0xFFFF) codes and scales, bit for bit."""
+    torch.manual_seed(3)
+    shapes = [(2304, 768), (768, 768), (3072, 768), (768, 3072), (1000, 768), (37, 19), (16, 1)]
+    ws = [torch.randn(o, i, device="cuda") * (2.0 / i) ** 0.5 for o, i in shapes]
+    ws[5][3:9] = 0.0  # zero rows inside a block
+    for bits in (4, 8):
+        got = ops.quant_weights(ws, bits)
+        for w, (codes, scale) in zip(ws, got):
+            o, i = w.shape
+            ref, _, rs, _ = ops.quant_proj_rows(w, 1, o, i, 0xFFFF, bits)
+            assert torch.equal(codes[:, :ops.pad16(o)], ref[:, :ops.pad16(o)])
+            assert torch.equal(scale, rs)
+
+
+def test_linear_uses_refreshed_weight_codes(ops):
+    """The batched, cached weight codes give bit-identical gradients to the
+    per-layer transform inside forward, and refresh only stale layers."""
+    from paper_2406_15102_b200.layers import HLQLinear, convert_linears, refresh_weight_codes
+
+    def make(batch):
+        torch.manual_seed(7)
+        net = torch.nn.Sequential(torch.nn.Linear(64, 96), torch.nn.ReLU(), torch.nn.Linear(96, 32)).cuda()
+        return convert_linears(net, batch_weight_codes=batch)
+
+    x = torch.randn(8, 20, 64, device="cuda")
+    grads = []
+    for batch in (True, False):
+        net = make(batch)
+        with torch.no_grad():
+            net[0].weight.mul_(1.5)  # bump the version after construction
+        xi = x.clone().requires_grad_(True)
+        net(xi).sum().backward()
+        layers = [m for m in net if isinstance(m, HLQLinear)]
+        assert all((m.cached_weight_codes() is not None) == batch for m in layers)
+        grads.append((xi.grad, net[0].weight.grad, net[2].weight.grad))
+    for a, b in zip(*grads):
+        assert torch.equal(a, b)
+    net = make(True)
+    net(x)
+    with torch.no_grad():
+        net[2].weight.add_(1.0)
+    assert net[0].cached_weight_codes() is not None and net[2].cached_weight_codes() is None
+    assert refresh_weight_codes(net) == 1
