@@ -46,6 +46,7 @@
 #include <cuda.h>
 #include <cuda_bf16.h>
 #include <cstdint>
+#include <cstdlib>
 
 #include "hlq_internal.h"
 #include "hlq_ptx.cuh"
@@ -137,17 +138,12 @@ struct StepIter {
 // Two 16-element row pieces (rows r and r+8 of the staged tile, same column
 // block) as 16 f32x2 lanes: p[i] = (A[i], B[i]).  All four butterfly stages
 // then run on packed pairs.
-// `flip` (bf16): read the two 16-byte halves in swapped order, so the 8
-// threads of one LDS.128 wavefront (blocks b..b+7, 32-byte pieces) cover all
-// 8 bank groups instead of 4 (blocks b and b+4 collide otherwise).
 template <typename T>
 __device__ __forceinline__ void read16x2(uint32_t pa, uint32_t pb, float2 (&p)[16], uint32_t flip) {
   if (sizeof(T) == 2) {
-    const uint32_t o0 = flip << 4, o1 = o0 ^ 16u;
-    const uint4 a0 = ptx::lds128(pa + o0), b0 = ptx::lds128(pb + o0);
-    const uint4 a1 = ptx::lds128(pa + o1), b1 = ptx::lds128(pb + o1);
-    const uint4 ta[2] = {flip ? a1 : a0, flip ? a0 : a1};
-    const uint4 tb[2] = {flip ? b1 : b0, flip ? b0 : b1};
+    (void)flip;  // swapping the halves per thread costs more SELs than the 2-way conflict
+    const uint4 ta[2] = {ptx::lds128(pa), ptx::lds128(pa + 16)};
+    const uint4 tb[2] = {ptx::lds128(pb), ptx::lds128(pb + 16)};
 #pragma unroll
     for (int q = 0; q < 2; ++q) {
       const uint32_t wa[4] = {ta[q].x, ta[q].y, ta[q].z, ta[q].w};
@@ -253,6 +249,22 @@ __device__ __forceinline__ void consume(const Args& a, const Quant& qx, const Qu
           } else {
             // codes of kept basis j for both columns, as s16x2 (x = col c, y = col c+1)
             uint32_t cx[4] = {0, 0, 0, 0}, cy[4] = {0, 0, 0, 0};
+            constexpr int kRankC = BM ? __builtin_popcount(uint32_t(BM)) : 0;
+            if (BM && (kRankC & 3) == 0) {
+              // compile-time bases, rank 4/8/16: byte-pack 4 codes per column with 4 PRMTs
+              uint32_t w[16];
+              int j = 0;
+#pragma unroll
+              for (int i = 0; i < 16; ++i)
+                if ((uint32_t(BM) >> i) & 1u) w[j++] = quant2<FW>(pv[i], qw);
+#pragma unroll
+              for (int g = 0; g < kRankC / 4; ++g) {
+                const uint32_t t01 = __byte_perm(w[4 * g], w[4 * g + 1], 0x6420);
+                const uint32_t t23 = __byte_perm(w[4 * g + 2], w[4 * g + 3], 0x6420);
+                cx[g] = __byte_perm(t01, t23, 0x6420);
+                cy[g] = __byte_perm(t01, t23, 0x7531);
+              }
+            } else {
 #pragma unroll
             for (int i = 0; i < 16; ++i) {
               if ((bitmap >> i) & 1u) {
@@ -268,6 +280,7 @@ __device__ __forceinline__ void consume(const Args& a, const Quant& qx, const Qu
                   default: cx[3] |= bx; cy[3] |= by; break;
                 }
               }
+            }
             }
             uint8_t* ox = cbuf + c * a.cstride + it.bl * rank;
             uint8_t* oy = ox + a.cstride;
@@ -458,6 +471,10 @@ void launch_one(const CUtensorMap& map, Args a, cudaStream_t stream) {
   if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kThreads, smem) != cudaSuccess ||
       per_sm < 1)
     per_sm = 1;
+  if (const char* e = getenv("HLQ_TR_CTAS_PER_SM")) {  // development sweeps
+    const int v = atoi(e);
+    if (v >= 1 && v < per_sm) per_sm = v;
+  }
   const int cap = num_sms() * per_sm;
   const int grid = a.items < 1 ? 1 : (a.items > cap ? cap : a.items);
   if (MODE != kBoth) {

@@ -28,13 +28,16 @@ class Trace:
     stream, with the call's algorithmic bytes (transforms) or ops (GEMMs)."""
 
     def __init__(self):
-        self.records = []  # (kind, start_event, end_event, bytes, ops, launches)
+        self.records = []  # (kind, key, start_event, end_event, bytes, ops, launches)
 
-    def summary(self):
+    def summary(self, by: str = "kind"):
+        """Aggregate per kind ("transform", "gemm", ...) or per key (kind plus
+        the call's operation and shape, e.g. "transform:dual:25216x3072")."""
         torch.cuda.synchronize()
         out = {}
-        for kind, s, e, nbytes, nops, nl in self.records:
-            d = out.setdefault(kind, {"calls": 0, "us": 0.0, "bytes": 0, "ops": 0, "launches": 0})
+        for kind, key, s, e, nbytes, nops, nl in self.records:
+            d = out.setdefault(kind if by == "kind" else key,
+                               {"calls": 0, "us": 0.0, "bytes": 0, "ops": 0, "launches": 0})
             d["calls"] += 1
             d["us"] += s.elapsed_time(e) * 1e3
             d["bytes"] += nbytes
@@ -54,7 +57,7 @@ class trace:
         return False
 
 
-def _traced(kind: str, nbytes: int, nops: int, launches: int, fn):
+def _traced(kind: str, nbytes: int, nops: int, launches: int, fn, key: str | None = None):
     LAUNCHES[0] += launches
     tr = _TRACE[0]
     if tr is None:
@@ -64,7 +67,7 @@ def _traced(kind: str, nbytes: int, nops: int, launches: int, fn):
     s.record()
     r = fn()
     e.record()
-    tr.records.append((kind, s, e, nbytes, nops, launches))
+    tr.records.append((kind, key or kind, s, e, nbytes, nops, launches))
     return r
 
 
@@ -141,7 +144,8 @@ def quant_dual(src: torch.Tensor, segs: int, rows: int, cols: int, bitmap: int, 
     _traced("transform", nbytes, 0, 1,
             lambda: _lib.call("hlq_quantize_dual", _p(src), dtype_code(src), segs, rows, cols,
                               ld_src, seg_src, bitmap, bits_gx, bits_gw, _p(stats), _p(cgx),
-                              cgx.stride(0), _p(cgw), ldk, _p(scales), _p(scales[1:]), _stream()))
+                              cgx.stride(0), _p(cgw), ldk, _p(scales), _p(scales[1:]), _stream()),
+            key=f"transform:dual:{segs * rows}x{cols}:{src.dtype}".replace("torch.", ""))
     return cgx, scales[0:1], cgw, k, scales[1:2], stats
 
 
@@ -180,7 +184,8 @@ def quant_proj_rows(src: torch.Tensor, segs: int, rows: int, cols: int, bitmap: 
     _traced("transform", segs * rows * cols * src.element_size() + cols * k, 0, 1,
             lambda: _lib.call("hlq_quantize_proj_rows", _p(src), dtype_code(src), segs, rows, cols,
                               ld_src, seg_src, bitmap, bits, _p(stats), _p(codes), ld, _p(scale),
-                              _stream()))
+                              _stream()),
+            key=f"transform:proj:{segs * rows}x{cols}:{src.dtype}".replace("torch.", ""))
     return codes, k, scale, stats[2:3]
 
 
@@ -217,7 +222,8 @@ def quant_weights(weights, bits: int):
     nbytes = sum(w.numel() * 4 + c.numel() for w, c in zip(ws_, codes))
     _traced("transform", nbytes, 0, 1,
             lambda: _lib.call("hlq_quantize_weights", n, wp, Os, Is, bits, cp, lds, sp, _p(scratch), wsb,
-                              _stream()))
+                              _stream()),
+            key=f"transform:weights:{n}")
     return [(c, scales[i:i + 1]) for i, c in enumerate(codes)]
 
 
@@ -269,7 +275,8 @@ def gemm_i8(a: torch.Tensor, b: torch.Tensor, m: int, n: int, k: int, bits_a: in
                               groups, bits_a, bits_b, _p(sa), _p(sb), float(extra),
                               _lib.HLQ_EPI_EXACT if exact else _lib.HLQ_EPI_FAST, _p(out),
                               _lib.HLQ_BF16 if out_dtype == torch.bfloat16 else _lib.HLQ_F32, n,
-                              _p(acc), n, _p(ws), wsb, _stream()))
+                              _p(acc), n, _p(ws), wsb, _stream()),
+            key=f"gemm:{m}x{n}x{k * groups}")
     return out, acc
 
 
