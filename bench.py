@@ -435,6 +435,71 @@ def config_table(torch):
     return out
 
 
+def graphed_step(torch, model, opt, x, y, warm: int = 3):
+    """The whole training step (forward, backward, optimizer) captured in one
+    CUDA graph -- the standard static-input whole-network capture.  Returns a
+    replay function.  The HLQ kernels are graph-safe (no host syncs, caller-
+    allocated memory, cooperative launches are capturable)."""
+    F = torch.nn.functional
+
+    def body():
+        with torch.autocast("cuda", dtype=torch.bfloat16):
+            loss = F.cross_entropy(model(x).float(), y)
+        loss.backward()
+        opt.step()
+        return loss
+
+    s = torch.cuda.Stream()
+    s.wait_stream(torch.cuda.current_stream())
+    with torch.cuda.stream(s):
+        for _ in range(warm):
+            opt.zero_grad(set_to_none=True)
+            body()
+    torch.cuda.current_stream().wait_stream(s)
+    g = torch.cuda.CUDAGraph()
+    opt.zero_grad(set_to_none=True)
+    with torch.cuda.graph(g):
+        body()
+
+    def replay(n):
+        for _ in range(n):
+            g.replay()
+    return replay
+
+
+def resnet_table(torch, batch: int = 256, steps: int = 20):
+    """BASELINE configs[2]: ResNet-18 CIFAR-10 training step, synthetic batch of
+    32x32 images, every conv / linear HLQ (HLQConv2d, HLQLinear) vs the dense
+    bf16 step of the same model; channels_last, bf16 autocast, SGD momentum.
+    Both arms run as one CUDA graph per step (the step is ~800 small kernels:
+    eager launching is host-bound); img/s from CUDA events around `steps`
+    replays after a >= 2 s warm-up."""
+    from paper_2406_15102_b200.resnet import convert_resnet, resnet18_cifar
+    out = {}
+    g = torch.Generator(device="cuda").manual_seed(5)
+    x = torch.randn(batch, 3, 32, 32, device="cuda", generator=g).to(memory_format=torch.channels_last)
+    y = torch.randint(0, 10, (batch,), device="cuda", generator=g)
+    for name, hlq in (("hlq", True), ("dense_bf16", False)):
+        torch.manual_seed(0)
+        m = resnet18_cifar().cuda().to(memory_format=torch.channels_last)
+        if hlq:
+            convert_resnet(m)
+        opt = torch.optim.SGD(m.parameters(), lr=1e-2, momentum=0.9, foreach=True, capturable=True) \
+            if "capturable" in torch.optim.SGD.__init__.__code__.co_varnames else \
+            torch.optim.SGD(m.parameters(), lr=1e-2, momentum=0.9, foreach=True)
+        step = graphed_step(torch, m, opt, x, y)
+        warmup(torch, step, 3, None, 2.0)
+        ms = timed(torch, None, lambda: step(steps))
+        out[name] = {"img_s": round(batch * steps / (ms * 1e-3), 1), "ms_per_step": round(ms / steps, 3)}
+        del m, opt, step
+        torch.cuda.empty_cache()
+    out["speedup"] = round(out["hlq"]["img_s"] / out["dense_bf16"]["img_s"], 3)
+    out["config"] = {"model": "ResNet-18 (CIFAR stem)", "batch": batch, "image": 32, "amp": "bf16",
+                     "hlq": "all 20 Conv2d (HLQConv2d) + fc (HLQLinear)", "data": "synthetic",
+                     "execution": "one CUDA graph per training step, both arms"}
+    return out
+
+
 def run_ours(args):
     import torch
     import torch.distributed as dist_mod
@@ -559,6 +624,10 @@ def run_ours(args):
         if rank == 0:
             line["layer_bwd"] = layer_bwd_table(torch)
             line["config_bwd"] = config_table(torch)
+            try:
+                line["resnet18_cifar_train"] = resnet_table(torch)
+            except Exception as exc:  # noqa: BLE001  (side measurement: never sink the bench line)
+                line["resnet18_cifar_train"] = {"error": f"{type(exc).__name__}: {exc}"[:300]}
             if world == 1:
                 t0 = time.perf_counter()
                 sec = cpu_path_seconds_per_image(1)

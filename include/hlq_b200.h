@@ -236,6 +236,14 @@ HLQ_API int hlq_col2im(const void* dcols, int dtype, int64_t ld, int64_t B, int6
                        int64_t C, int k, int stride, int pad, void* dx_nhwc, int out_dtype,
                        void* stream);
 
+/* col2im with a choice of dcols column order: 0 = (c, tap) (= hlq_col2im),
+ * 1 = (tap, c) -- what the dX GEMM produces when the W codes rows are
+ * permuted tap-major; channels are then contiguous per tap (16-byte loads,
+ * C % 8 == 0).  Same fp32 summation order over taps, same result. */
+HLQ_API int hlq_col2im_ex(const void* dcols, int dtype, int64_t ld, int64_t B, int64_t H, int64_t W,
+                          int64_t C, int k, int stride, int pad, int col_order, void* dx_nhwc,
+                          int out_dtype, void* stream);
+
 /* Workspace bytes needed by hlq_hq_grad_input / hlq_grad_weight. */
 HLQ_API size_t hlq_hq_grad_input_ws(int64_t T, int64_t O, int64_t I);
 HLQ_API size_t hlq_grad_weight_ws(int64_t B, int64_t L, int64_t O, int axis, int rank);

@@ -55,6 +55,7 @@ SIGNATURES = {
     "hlq_conv_acbp_compress": (_I, [_P, _I, _I64, _I64, _I64, _I64, _I, _I, _I, _U32, _I, _P, _I64,
                                     _P, _P, _P]),
     "hlq_col2im": (_I, [_P, _I, _I64, _I64, _I64, _I64, _I64, _I, _I, _I, _P, _I, _P]),
+    "hlq_col2im_ex": (_I, [_P, _I, _I64, _I64, _I64, _I64, _I64, _I, _I, _I, _I, _P, _I, _P]),
     "hlq_acbp_k": (_I64, [_I64, _I64, _I, _I]),
     "hlq_acbp_rows": (_I64, [_I64, _I64, _I]),
     "hlq_acbp_compress": (_I, [_P, _I, _I64, _I64, _I64, _I, _U32, _I, _P, _I64, _P, _P, _P]),

@@ -40,7 +40,22 @@ def conv_acbp_compress(x: torch.Tensor, k: int, stride: int, pad: int, strategy:
     plan = strategy.plan
     bits = strategy.grad_weight_path.bits or 8
     axis = ht_axis_for(B, L, plan.block_size, strategy.pad_small_axes)
-    if axis == 1:
+    if axis == 1 and C * k * k <= 256 and (C * x.element_size()) % 16 != 0:
+        # few input channels (e.g. an RGB stem): materialise the small cols tensor and run
+        # the TMA projection on it -- the im2col producer's 256-channel tiles would be
+        # almost empty and the gather fallback handles 16-byte-unaligned pixels slowly
+        I = C * k * k
+        ldc = (I + 7) // 8 * 8
+        Ho, Wo = ops.conv_out_hw(H, W, k, stride, pad)
+        xp = F.pad(x, (pad, pad, pad, pad))
+        sb, sc, sh, sw = xp.stride()
+        # cols[b, (ho, wo), (c, i, j)] = xp[b, c, ho*s + i, wo*s + j] -- one strided copy
+        # (F.unfold runs one kernel per image)
+        win = xp.as_strided((B, Ho, Wo, C, k, k), (sb, stride * sh, stride * sw, sc, sh, sw))
+        cols = torch.zeros((B, L, ldc), dtype=x.dtype, device=x.device)
+        cols[:, :, :I] = win.reshape(B, L, I)
+        codes, kk, scale, amax = ops.quant_proj_rows(cols, B, L, I, plan.gpu_bitmap(), bits, ldc, L * ldc)
+    elif axis == 1:
         codes, kk, scale, amax = ops.conv_acbp(_to_nhwc(x), k, stride, pad, plan.gpu_bitmap(), bits)
     else:
         # L < 16: projection along the batch axis needs the lowered tensor itself
@@ -107,10 +122,17 @@ def _conv_backward(acbp: ACBPActivation, w4: torch.Tensor, gy: torch.Tensor, x_s
         w2 = w4.detach().reshape(O, I)
         w2 = w2 if w2.dtype == torch.float32 else w2.float()
         cw, kw, sw, _ = ops.quant_proj_rows(w2.contiguous(), 1, O, I, 0xFFFF, bits_gx)
-        cols_dtype = torch.float32 if exact else torch.bfloat16
-        dcols, accx = ops.gemm_i8(cgx, cw, B * L, I, ops.pad16(O), bits_gx, bits_gx, sgx, sw, 1.0,
+        # fp32 dcols even for training: rounding every tap's partial to bf16 before the
+        # col2im sum costs ~1.6e-3 relative error on dX, over the 1e-3 contract
+        cols_dtype = torch.float32
+        # training path: W codes rows tap-major, so dcols columns are (tap, c) and the
+        # col2im reads each tap's channels contiguously (same per-element sum order);
+        # the reference-mirroring path keeps the reference's (c, tap) column order
+        tap_major = not want and C % 8 == 0
+        cwg = cw.view(C, k * k, cw.shape[1]).transpose(0, 1).reshape(I, cw.shape[1]) if tap_major else cw
+        dcols, accx = ops.gemm_i8(cgx, cwg, B * L, I, ops.pad16(O), bits_gx, bits_gx, sgx, sw, 1.0,
                                   exact=exact, out_dtype=cols_dtype, want_acc=want)
-        dx_nhwc = ops.col2im(dcols, B, H, W, C, k, stride, pad, out_dtype=dx_dtype)
+        dx_nhwc = ops.col2im(dcols, B, H, W, C, k, stride, pad, out_dtype=dx_dtype, tap_major=tap_major)
         dx = dx_nhwc.permute(0, 3, 1, 2)  # NCHW shape, channels_last memory
         if want:
             stages.update(gx_codes_g=cgx, gx_scale_g=sgx, gx_codes_w=cw[:, :kw].t(), gx_scale_w=sw,

@@ -374,6 +374,21 @@ int hlq_col2im(const void* dcols, int dtype, int64_t ld, int64_t B, int64_t H, i
   return cuda_status("hlq_col2im");
 }
 
+int hlq_col2im_ex(const void* dcols, int dtype, int64_t ld, int64_t B, int64_t H, int64_t W, int64_t C,
+                  int k, int stride, int pad, int col_order, void* dx_nhwc, int out_dtype, void* stream) {
+  if (col_order == 0)
+    return hlq_col2im(dcols, dtype, ld, B, H, W, C, k, stride, pad, dx_nhwc, out_dtype, stream);
+  if (col_order != 1) return fail(HLQ_ERR_PARAMETER, "col_order must be 0 (c, tap) or 1 (tap, c)");
+  HLQ_TRY(check_dtype(dtype));
+  HLQ_TRY(check_dtype(out_dtype));
+  if (B <= 0 || H <= 0 || W <= 0 || C <= 0 || k <= 0 || stride <= 0 || pad < 0 || ld < C * k * k)
+    return fail(HLQ_ERR_DIMENSION, "bad col2im geometry");
+  if (!hlq::launch_col2im_tapmajor(dcols, dtype, ld, int(B), int(H), int(W), int(C), k, stride, pad, dx_nhwc,
+                                   out_dtype, static_cast<cudaStream_t>(stream)))
+    return fail(HLQ_ERR_PARAMETER, "tap-major col2im needs C %% 8 == 0 and 16-byte aligned rows");
+  return cuda_status("hlq_col2im_ex");
+}
+
 int64_t hlq_acbp_k(int64_t B, int64_t L, int axis, int rank) {
   return axis == 1 ? B * ((L + 15) / 16) * rank : ((B + 15) / 16) * rank;
 }

@@ -244,7 +244,103 @@ __global__ void __launch_bounds__(256) col2im_kernel(const TIn* __restrict__ dco
   }
 }
 
+// Tap-major variant: dcols columns ordered (tap, c) (the W codes rows permuted
+// tap-major before the dX GEMM), so each tap's C channels are contiguous: a
+// thread owns 8 channels of one output pixel, 16-byte loads per tap, fp32 sums
+// in the reference's (i, j) order (the per-element summation order, and so the
+// result, is the same as col2im_kernel's).
+template <typename TIn, typename TOut>
+__global__ void __launch_bounds__(256) col2im_tapmajor_kernel(const TIn* __restrict__ dcols, int64_t ld, int B,
+                                                              int H, int W, int C, int k, int stride, int pad,
+                                                              int Ho, int Wo, TOut* __restrict__ dx) {
+  const int groups = C >> 3;
+  const int64_t total = int64_t(B) * H * W * groups;
+  for (int64_t e = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; e < total;
+       e += int64_t(gridDim.x) * blockDim.x) {
+    const int c0 = int(e % groups) * 8;
+    int64_t r = e / groups;
+    const int w = int(r % W);
+    r /= W;
+    const int h = int(r % H);
+    const int b = int(r / H);
+    float acc[8];
+#pragma unroll
+    for (int q = 0; q < 8; ++q) acc[q] = 0.0f;
+    for (int i = 0; i < k; ++i) {
+      const int hh = h + pad - i;
+      if (hh < 0 || hh % stride) continue;
+      const int ho = hh / stride;
+      if (ho >= Ho) continue;
+      for (int j = 0; j < k; ++j) {
+        const int ww = w + pad - j;
+        if (ww < 0 || ww % stride) continue;
+        const int wo = ww / stride;
+        if (wo >= Wo) continue;
+        const int64_t row = int64_t(b) * Ho * Wo + ho * Wo + wo;
+        const TIn* src = dcols + row * ld + int64_t(i * k + j) * C + c0;
+        float v[8];
+        if (sizeof(TIn) == 2) {
+          const uint4 t = __ldg(reinterpret_cast<const uint4*>(src));
+          const uint32_t u[4] = {t.x, t.y, t.z, t.w};
+#pragma unroll
+          for (int q = 0; q < 4; ++q) {
+            v[2 * q] = __uint_as_float(u[q] << 16);
+            v[2 * q + 1] = __uint_as_float(u[q] & 0xFFFF0000u);
+          }
+        } else {
+          const float4 t0 = __ldg(reinterpret_cast<const float4*>(src));
+          const float4 t1 = __ldg(reinterpret_cast<const float4*>(src) + 1);
+          v[0] = t0.x; v[1] = t0.y; v[2] = t0.z; v[3] = t0.w;
+          v[4] = t1.x; v[5] = t1.y; v[6] = t1.z; v[7] = t1.w;
+        }
+#pragma unroll
+        for (int q = 0; q < 8; ++q) acc[q] = __fadd_rn(acc[q], v[q]);
+      }
+    }
+    const int64_t o = ((int64_t(b) * H + h) * W + w) * C + c0;
+    if (sizeof(TOut) == 2) {
+      uint32_t u[4];
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        __nv_bfloat162 t = __floats2bfloat162_rn(acc[2 * q], acc[2 * q + 1]);
+        u[q] = *reinterpret_cast<uint32_t*>(&t);
+      }
+      *reinterpret_cast<uint4*>(reinterpret_cast<__nv_bfloat16*>(dx) + o) = make_uint4(u[0], u[1], u[2], u[3]);
+    } else {
+      float* d = reinterpret_cast<float*>(dx) + o;
+      *reinterpret_cast<float4*>(d) = make_float4(acc[0], acc[1], acc[2], acc[3]);
+      *reinterpret_cast<float4*>(d + 4) = make_float4(acc[4], acc[5], acc[6], acc[7]);
+    }
+  }
+}
+
 }  // namespace
+
+bool launch_col2im_tapmajor(const void* dcols, int in_dtype, int64_t ld, int B, int H, int W, int C, int k,
+                            int stride, int pad, void* dx, int out_dtype, cudaStream_t st) {
+  const size_t ein = in_dtype == kBF16 ? 2 : 4, eout = out_dtype == kBF16 ? 2 : 4;
+  if (C % 8 || (reinterpret_cast<uintptr_t>(dcols) % 16) || (ld * ein) % 16 ||
+      (reinterpret_cast<uintptr_t>(dx) % 16) || (size_t(C) * eout) % 16)
+    return false;
+  const int Ho = (H + 2 * pad - k) / stride + 1, Wo = (W + 2 * pad - k) / stride + 1;
+  const int64_t total = int64_t(B) * H * W * (C / 8);
+  const int64_t want = (total + 255) / 256;
+  const int grid = int(want < num_sms() * 16 ? want : num_sms() * 16);
+  if (in_dtype == kBF16 && out_dtype == kBF16)
+    col2im_tapmajor_kernel<__nv_bfloat16, __nv_bfloat16><<<grid, 256, 0, st>>>(
+        static_cast<const __nv_bfloat16*>(dcols), ld, B, H, W, C, k, stride, pad, Ho, Wo,
+        static_cast<__nv_bfloat16*>(dx));
+  else if (in_dtype == kBF16)
+    col2im_tapmajor_kernel<__nv_bfloat16, float><<<grid, 256, 0, st>>>(
+        static_cast<const __nv_bfloat16*>(dcols), ld, B, H, W, C, k, stride, pad, Ho, Wo, static_cast<float*>(dx));
+  else if (out_dtype == kBF16)
+    col2im_tapmajor_kernel<float, __nv_bfloat16><<<grid, 256, 0, st>>>(
+        static_cast<const float*>(dcols), ld, B, H, W, C, k, stride, pad, Ho, Wo, static_cast<__nv_bfloat16*>(dx));
+  else
+    col2im_tapmajor_kernel<float, float><<<grid, 256, 0, st>>>(static_cast<const float*>(dcols), ld, B, H, W, C, k,
+                                                                stride, pad, Ho, Wo, static_cast<float*>(dx));
+  return true;
+}
 
 void launch_im2col_proj(const void* x, int dtype, int B, int H, int W, int C, int k, int stride,
                         int pad, uint32_t bitmap, int bits, int mode, uint32_t* stats, int8_t* dst,

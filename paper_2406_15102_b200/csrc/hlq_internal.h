@@ -48,6 +48,10 @@ void launch_im2col_proj(const void* x, int dtype, int B, int H, int W, int C, in
 bool launch_conv_acbp_tma(const void* x, int dtype, int B, int H, int W, int C, int k, int stride, int pad,
                           uint32_t bitmap, int bits, int mode, uint32_t* stats, int8_t* dst, int64_t ld_dst,
                           float* scale, cudaStream_t stream);
+// col2im for dcols with (tap, c) column order; false if C % 8 or alignment
+// rule out its 16-byte accesses (nothing launched).
+bool launch_col2im_tapmajor(const void* dcols, int in_dtype, int64_t ld, int B, int H, int W, int C, int k,
+                            int stride, int pad, void* dx, int out_dtype, cudaStream_t st);
 void launch_col2im(const void* dcols, int in_dtype, int64_t ld, int B, int H, int W, int C, int k,
                    int stride, int pad, void* dx, int out_dtype, cudaStream_t st);
 

@@ -212,8 +212,11 @@ def refresh_weight_codes(module: nn.Module) -> int:
     optimizer step).  HLQLinear.forward then reuses them instead of launching
     a per-layer transform.  Returns the number of layers refreshed."""
     stale = {}
+    # under CUDA-graph capture the refresh must be part of the captured step whatever
+    # the cache says (replays re-run the kernels, not this Python check)
+    force = torch.cuda.is_available() and torch.cuda.is_current_stream_capturing()
     for m in module.modules():
-        if isinstance(m, HLQLinear) and m.weight.is_cuda and m.cached_weight_codes() is None:
+        if isinstance(m, HLQLinear) and m.weight.is_cuda and (force or m.cached_weight_codes() is None):
             stale.setdefault(m.bits_gx(), []).append(m)
     n = 0
     for bits, mods in stale.items():

@@ -323,13 +323,13 @@ def conv_dgrad_i8(gcodes: torch.Tensor, B: int, Ho: int, Wo: int, O: int, wcodes
 
 
 def col2im(dcols: torch.Tensor, B: int, H: int, W: int, C: int, k: int, stride: int, pad: int,
-           out_dtype=torch.float32) -> torch.Tensor:
+           out_dtype=torch.float32, tap_major: bool = False) -> torch.Tensor:
     """dX (B, H, W, C) contiguous (= channels-last NCHW) from dcols (B*L, C*k*k)."""
     dcols = _cuda(dcols, "dcols")
     dx = torch.empty((B, H, W, C), dtype=out_dtype, device=dcols.device)
     _traced("col2im", dcols.numel() * dcols.element_size() + dx.numel() * dx.element_size(), 0, 1,
-            lambda: _lib.call("hlq_col2im", _p(dcols), dtype_code(dcols), dcols.stride(0), B, H, W, C,
-                              k, stride, pad, _p(dx),
+            lambda: _lib.call("hlq_col2im_ex", _p(dcols), dtype_code(dcols), dcols.stride(0), B, H, W, C,
+                              k, stride, pad, 1 if tap_major else 0, _p(dx),
                               _lib.HLQ_BF16 if out_dtype == torch.bfloat16 else _lib.HLQ_F32,
                               _stream()))
     return dx

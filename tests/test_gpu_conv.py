@@ -150,3 +150,28 @@ def test_implicit_gemm_dgrad_matches_col2im(conv, B, C, H, O, k, p):
     # and against the CPU oracle (reference Conv2d.backward, 1/B not applied to dX)
     rdx, _ = orc.conv2d_hlq_backward(x, w, gy, 1, p)
     assert np.linalg.norm(a - rdx) / np.linalg.norm(rdx) < 1e-6
+
+
+@pytest.mark.parametrize("B,C,H,O,k,s,p", [(4, 64, 16, 128, 3, 2, 1), (4, 64, 16, 128, 1, 2, 0),
+                                           (2, 3, 32, 64, 3, 1, 1)])
+def test_training_path_conv_matches_oracle(conv, B, C, H, O, k, s, p):
+    """HLQConv2dFunction's training path: tap-major col2im for strided convs,
+    the unfold ACBP for an RGB stem -- dW bit-for-bit the reference's codes path
+    (fast epilogue: <= 1e-5), dX within fp32 rounding of the oracle."""
+    from paper_2406_15102_b200.backprop import BackwardStrategy
+    x, w, _ = orc.make_inputs(21 + k + s, (B, C, H, H), (O, C, k, k), (1,))
+    Ho, _ = orc.conv_out_hw(H, H, k, s, p)
+    rng = np.random.default_rng(9)
+    gy = (rng.lognormal(0.0, 1.4, (B, O, Ho, Ho)) * rng.choice([-1.0, 1.0], (B, O, Ho, Ho)) * 1e-3)
+    gy = gy.astype(np.float32)
+    strat = BackwardStrategy.hlq()
+    xt = t(x).contiguous(memory_format=torch.channels_last)
+    acbp, _ = conv.conv_acbp_compress(xt, k, s, p, strat)
+    st = {}
+    acbp_ref, _ = conv.conv_acbp_compress(t(x), k, s, p, strat)
+    conv._conv_backward(acbp_ref, t(w), t(gy), xt.shape, s, p, strat, 1.0, True, torch.float32, stages=st)
+    assert np.array_equal(n(acbp.reference_payload()), n(acbp_ref.reference_payload()))
+    dx, dw = conv._conv_backward(acbp, t(w), t(gy), xt.shape, s, p, strat, 1.0, False, torch.float32)
+    rdx, rdw = orc.conv2d_hlq_backward(x, w, gy, s, p, extra=1.0)
+    assert np.linalg.norm(n(dx) - rdx) / np.linalg.norm(rdx) < 1e-5
+    assert np.linalg.norm(n(dw) - rdw) / np.linalg.norm(rdw) < 1e-5
