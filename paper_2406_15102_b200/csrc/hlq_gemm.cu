@@ -389,7 +389,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
   constexpr uint32_t kABytes = kBM * kBK;             // this CTA's 128 rows of A
   constexpr uint32_t kBBytes = (BN / 2) * kBK;        // this CTA's BN/2 rows of B
   constexpr uint32_t kStageBytes = kABytes + kBBytes;
-  constexpr uint32_t kTmemCols = 2 * BN;
+  constexpr uint32_t kTmemCols = 2 * BN <= 256 ? 256 : 512;  // power of two >= 2*BN
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
                                              ~uintptr_t(1023));
@@ -802,10 +802,14 @@ GemmPlan plan_gemm(int64_t M, int64_t N, int64_t K, int64_t groups, bool allow_s
   const bool split_case = allow_split && 2 * tiles128 <= sms && nk >= 16 && N % 4 == 0;
   if (!split_case && nk >= 16 && M >= 2 * kBM && sms >= 2) {
     const int64_t pairs = sms / 2, pm = (M + 2 * kBM - 1) / (2 * kBM);
-    const int64_t u256 = pm * ((N + 255) / 256), u128 = pm * ((N + 127) / 128);
-    const double t256 = double((u256 + pairs - 1) / pairs), t128 = 0.6 * double((u128 + pairs - 1) / pairs);
+    const int64_t u256 = pm * ((N + 255) / 256), u192 = pm * ((N + 191) / 192), u128 = pm * ((N + 127) / 128);
+    const double t256 = double((u256 + pairs - 1) / pairs), t192 = 0.9 * double((u192 + pairs - 1) / pairs),
+                 t128 = 0.6 * double((u128 + pairs - 1) / pairs);
     p.pair = true;
-    p.bn = (N > 128 && t256 <= t128) ? 256 : 128;
+    p.bn = 128;
+    double best = t128;
+    if (N > 128 && t192 < best) { best = t192; p.bn = 192; }
+    if (N > 128 && t256 <= best) p.bn = 256;
     return finish_plan(p, M, N, allow_split);
   }
   // Split-K only for products that fill less than half the SMs (e.g. the ViT
@@ -827,7 +831,7 @@ GemmPlan plan_gemm(int64_t M, int64_t N, int64_t K, int64_t groups, bool allow_s
 GemmPlan finish_plan(GemmPlan p, int64_t M, int64_t N, bool allow_split) {
   if (const char* e = getenv("HLQ_GEMM_BN")) {
     const int bn = atoi(e);
-    if (bn == 128 || (bn == 256 && N > 128)) p.bn = bn;
+    if (bn == 128 || ((bn == 256 || bn == 192) && N > 128)) p.bn = bn;
   }
   if (const char* e = getenv("HLQ_GEMM_SPLITS")) {
     const int s = atoi(e);
@@ -857,6 +861,9 @@ int launch_gemm_i8(const int8_t* A, int64_t lda, const int8_t* B, int64_t ldb, i
   if (p.pair) {
     if (p.bn == 256)
       return run_2sm<256, 6>(A, lda, B, ldb, M, N, K, groups, a_gstride, b_gstride, sa, sb, extra, epilogue, out,
+                             out_dtype, ldo, acc_out, ld_acc, p.splits, ws, stream);
+    if (p.bn == 192)
+      return run_2sm<192, 6>(A, lda, B, ldb, M, N, K, groups, a_gstride, b_gstride, sa, sb, extra, epilogue, out,
                              out_dtype, ldo, acc_out, ld_acc, p.splits, ws, stream);
     return run_2sm<128, 8>(A, lda, B, ldb, M, N, K, groups, a_gstride, b_gstride, sa, sb, extra, epilogue, out,
                            out_dtype, ldo, acc_out, ld_acc, p.splits, ws, stream);

@@ -24,7 +24,7 @@ def main():
         b = torch.randint(-127, 128, (N, K), dtype=torch.int8, device="cuda")
         res = {}
         for pair in ("0", "1"):
-          for bn in ("128", "256"):
+          for bn in ("128", "192", "256") if pair == "1" else ("128", "256"):
             for s in ("1", "2", "4"):
                 if name.endswith("dx") and s != "1":
                     continue
