@@ -333,18 +333,13 @@ def layer_bwd_table(torch):
         gy = (torch.randn(B, L, O, device="cuda") * 1e-3).to(torch.bfloat16)
         xp, k, sx, _ = ops.quant_proj_rows(x, B, L, I, 0x5555, 8, I, L * I)
         cw, _, sw, _ = ops.quant_proj_rows(w, 1, O, I, 0xFFFF, 4)
-        side = torch.cuda.Stream()
-
         def hlq_bwd():
-            # exactly HLQLinearFunction.backward: fused gy transform, then dW || dX
+            # exactly HLQLinearFunction.backward: fused gy transform, then dW and dX
+            # (one CTA-pair launch over both when both contractions are long)
             cgx, sgx, cg, kg, sg, _ = ops.quant_dual(gy, B, L, O, 0x5555, 4, 8, O, L * O)
-            main = torch.cuda.current_stream()
-            side.wait_stream(main)
-            with torch.cuda.stream(side):
-                ops.gemm_i8(cg, xp, O, I, k, 8, 8, sg, sx, 1.0, exact=False)
-            ops.gemm_i8(cgx, cw, B * L, I, ops.pad16(O), 4, 4, sgx, sw, 1.0, exact=False,
-                        out_dtype=torch.bfloat16)
-            main.wait_stream(side)
+            ops.gemm_i8_pair(dict(a=cg, b=xp, m=O, n=I, k=k, bits_a=8, bits_b=8, sa=sg, sb=sx),
+                             dict(a=cgx, b=cw, m=B * L, n=I, k=ops.pad16(O), bits_a=4, bits_b=4, sa=sgx, sb=sw,
+                                  out_dtype=torch.bfloat16))
 
         def hlq_fwd_extra():
             # forward-time work (on a side stream under the forward GEMM in training); the
@@ -373,8 +368,8 @@ def layer_bwd_table(torch):
     out["weight_codes_refresh"] = {"us_per_step": round(graph_us(torch, lambda: ops.quant_weights(ws, 4), flush), 1),
                                    "layers": len(ws), "launches": 1}
     del ws
-    out["note"] = ("hlq_us = backward as run by HLQLinearFunction (fused gy transform, dW || dX); "
-                   "fwd_overhead_us = ACBP(X), enqueued on a side stream under the forward GEMM; "
+    out["note"] = ("hlq_us = backward as run by HLQLinearFunction (fused gy transform, then dW + dX via "
+                   "hlq_gemm_i8_multi); fwd_overhead_us = ACBP(X) in the forward; "
                    "weight_codes_refresh = the dX weight codes of every layer, batched once per step")
     del flush
     return out

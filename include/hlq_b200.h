@@ -171,6 +171,33 @@ HLQ_API int hlq_gemm_i8_ex(const int8_t* A, int64_t lda, int64_t a_gstride, cons
                            int32_t* acc_out, int64_t ld_acc, void* ws, size_t ws_bytes,
                            void* stream);
 
+/* One product for hlq_gemm_i8_multi (fields as in hlq_gemm_i8_grouped). */
+typedef struct {
+  const int8_t* A;
+  int64_t lda, a_gstride;
+  const int8_t* B;
+  int64_t ldb, b_gstride;
+  int64_t M, N, K, groups;
+  int bits_a, bits_b;
+  const float* sa;
+  const float* sb;
+  double extra;
+  int epilogue;
+  void* out;
+  int out_dtype;
+  int64_t ldo;
+  int32_t* acc_out;
+  int64_t ld_acc;
+} hlq_gemm_desc;
+
+/* n (1 or 2) independent products -- typically a layer's dX and dW GEMMs --
+ * with hlq_gemm_i8_grouped's contract each.  When both have long
+ * contractions they run as ONE CTA-pair launch whose clusters take a
+ * longest-first static schedule over both products' tiles (a layer's few long
+ * dW tiles and many short dX tiles then pack evenly across the SMs instead of
+ * running as two partially-filled waves); otherwise as separate launches. */
+HLQ_API int hlq_gemm_i8_multi(int n, const hlq_gemm_desc* descs, void* stream);
+
 /* ---------------------------------------------------------------------------
  * Reference-function equivalents (whole calls)
  * ------------------------------------------------------------------------- */

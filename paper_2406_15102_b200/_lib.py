@@ -46,6 +46,7 @@ SIGNATURES = {
     "hlq_gemm_i8_grouped": (_I, [_P, _I64, _I64, _P, _I64, _I64, _I64, _I64, _I64, _I64, _I, _I, _P,
                                  _P, _D, _I, _P, _I, _I64, _P, _I64, _P]),
     "hlq_gemm_i8_ws": (_SZ, [_I64, _I64, _I64, _I64]),
+    "hlq_gemm_i8_multi": (_I, [_I, _P, _P]),
     "hlq_gemm_i8_ex": (_I, [_P, _I64, _I64, _P, _I64, _I64, _I64, _I64, _I64, _I64, _I, _I, _P, _P,
                             _D, _I, _P, _I, _I64, _P, _I64, _P, _SZ, _P]),
     "hlq_quantize_weights_ws": (_SZ, [_I]),
@@ -65,6 +66,14 @@ SIGNATURES = {
     "hlq_grad_weight": (_I, [_P, _I64, _P, _P, _I, _I64, _I64, _I64, _I64, _I, _U32, _I, _D, _P, _I,
                              _I, _P, _SZ, _P]),
 }
+
+class GemmDesc(ctypes.Structure):
+    """hlq_gemm_desc (include/hlq_b200.h)."""
+    _fields_ = [("A", _P), ("lda", _I64), ("a_gstride", _I64), ("B", _P), ("ldb", _I64), ("b_gstride", _I64),
+                ("M", _I64), ("N", _I64), ("K", _I64), ("groups", _I64), ("bits_a", _I), ("bits_b", _I),
+                ("sa", _P), ("sb", _P), ("extra", _D), ("epilogue", _I), ("out", _P), ("out_dtype", _I),
+                ("ldo", _I64), ("acc_out", _P), ("ld_acc", _I64)]
+
 
 _lock = threading.Lock()
 _lib = None

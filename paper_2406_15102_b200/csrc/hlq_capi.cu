@@ -242,6 +242,53 @@ int hlq_gemm_i8_grouped(const int8_t* A, int64_t lda, int64_t a_gstride, const i
                         extra, epilogue, out, out_dtype, ldo, acc_out, ld_acc, nullptr, 0, stream);
 }
 
+int hlq_gemm_i8_multi(int n, const hlq_gemm_desc* d, void* stream) {
+  if (n < 1 || n > 2 || !d) return fail(HLQ_ERR_PARAMETER, "hlq_gemm_i8_multi takes 1 or 2 products, got %d", n);
+  bool fuse = n == 2;
+  for (int q = 0; q < n; ++q) {
+    const hlq_gemm_desc& g = d[q];
+    // validate each product exactly as the single call does (zero-sized products skip the launch)
+    if (g.M == 0 || g.N == 0 || (g.groups > 1) || g.acc_out || !g.out) fuse = false;
+  }
+  if (fuse) {
+    for (int q = 0; q < 2; ++q) {
+      const hlq_gemm_desc& g = d[q];
+      HLQ_TRY(check_bits(g.bits_a));
+      HLQ_TRY(check_bits(g.bits_b));
+      HLQ_TRY(check_dtype(g.out_dtype));
+      HLQ_TRY(check_ld16(g.lda, "A"));
+      HLQ_TRY(check_ld16(g.ldb, "B"));
+      if (g.M < 0 || g.N < 0 || g.K <= 0 || g.lda < g.K || g.ldb < g.K || g.ldo < g.N || g.M > INT32_MAX ||
+          g.N > INT32_MAX || g.K > INT32_MAX)
+        return fail(HLQ_ERR_DIMENSION, "bad GEMM shape M=%lld N=%lld K=%lld", (long long)g.M, (long long)g.N,
+                    (long long)g.K);
+      if ((long double)g.K * qmax_of(g.bits_a) * qmax_of(g.bits_b) >= 2147483648.0L)
+        return fail(HLQ_ERR_PARAMETER, "contraction extent %lld exceeds the int32-exact bound", (long long)g.K);
+      if (g.epilogue != HLQ_EPI_EXACT && g.epilogue != HLQ_EPI_FAST)
+        return fail(HLQ_ERR_PARAMETER, "unknown epilogue %d", g.epilogue);
+    }
+    hlq::GemmDesc gd[2];
+    for (int q = 0; q < 2; ++q) {
+      const hlq_gemm_desc& g = d[q];
+      gd[q] = hlq::GemmDesc{g.A, g.lda, g.lda * g.M, g.B, g.ldb, g.ldb * g.N, g.M, g.N, g.K, 1, g.sa, g.sb,
+                            g.extra, g.epilogue, g.out, g.out_dtype, g.ldo, nullptr, 0};
+    }
+    if (hlq::gemm_i8_pair2_eligible(gd)) {
+      int e = hlq::launch_gemm_i8_pair2(gd, static_cast<cudaStream_t>(stream));
+      if (e == -1) return fail(HLQ_ERR_CUDA, "cuTensorMapEncodeTiled rejected the operands");
+      if (e != 0) return fail(HLQ_ERR_CUDA, "hlq_gemm_i8_multi: %s", cudaGetErrorString(cudaError_t(e)));
+      return HLQ_OK;
+    }
+  }
+  for (int q = 0; q < n; ++q) {
+    const hlq_gemm_desc& g = d[q];
+    HLQ_TRY(hlq_gemm_i8_grouped(g.A, g.lda, g.a_gstride, g.B, g.ldb, g.b_gstride, g.M, g.N, g.K, g.groups,
+                                g.bits_a, g.bits_b, g.sa, g.sb, g.extra, g.epilogue, g.out, g.out_dtype, g.ldo,
+                                g.acc_out, g.ld_acc, stream));
+  }
+  return HLQ_OK;
+}
+
 size_t hlq_gemm_i8_ws(int64_t M, int64_t N, int64_t K, int64_t groups) {
   if (M <= 0 || N <= 0 || K <= 0 || groups < 1) return 0;
   return hlq::gemm_i8_ws_bytes(M, N, K, groups);

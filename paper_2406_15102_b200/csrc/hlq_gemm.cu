@@ -22,6 +22,9 @@
 #include <cstdio>
 #include <cstdlib>
 #include <mutex>
+#include <algorithm>
+#include <cstring>
+#include <vector>
 
 #include "hlq_internal.h"
 #include "hlq_ptx.cuh"
@@ -374,18 +377,39 @@ __global__ void __launch_bounds__(kThreads, 1)
 // its TMEM holds its 128 accumulator rows; only the leader (rank 0) issues the
 // MMAs.  Per SM that is 16 + BN/2*128/1024 KB of operands per 128-byte K block
 // for 128 x BN MACs -- a third less L2->SM traffic than the 128 x BN single-CTA
-// tile, which is what bounds the dX / dW products (~46 B/clk/SM measured).
-// Pipelines: both producers wait on their own `empty` (the leader's MMA commit
-// multicasts to both CTAs) and complete bytes on the LEADER's `full`; the MMA
-// commit multicasts `tfull` to both CTAs; every epilogue warp of both CTAs
-// arrives on the leader's `tempty`.
+// tile.  Pipelines: both producers wait on their own `empty` (the leader's MMA
+// commit multicasts to both CTAs) and complete bytes on the LEADER's `full`;
+// the MMA commit multicasts `tfull` to both CTAs; every epilogue warp of both
+// CTAs arrives on the leader's `tempty`.
+//
+// Up to two independent products share one launch (the dX and dW GEMMs of a
+// layer): units of problem 0 come first in the global unit numbering, and an
+// optional host-built schedule (longest-processing-time first, per cluster)
+// lists each cluster's units so long dW units and short dX units pack evenly.
+struct PairProb {
+  int M, N, K, groups, splits, tma_out, epilogue, out_dtype;
+  const float* sa;
+  const float* sb;
+  double extra;
+  void* out;
+  int64_t ldo;
+  int32_t* acc_out;
+  int64_t ld_acc;
+  int32_t* slabs;
+  int unit0, units;
+};
+constexpr int kMaxSched = 11000;
+struct alignas(64) PairParams {
+  CUtensorMap a[2], b[2], o[2];
+  PairProb p[2];
+  int nprob, nsched;
+  uint16_t off[129];
+  uint16_t ids[kMaxSched];
+};
+
 template <int BN, int STAGES>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
-    gemm_i8_2sm_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant__ CUtensorMap map_b,
-                       const __grid_constant__ CUtensorMap map_o, int tma_out, int M, int N, int K, int groups, const float* __restrict__ sa,
-                       const float* __restrict__ sb, double extra, int epilogue, void* out, int out_dtype,
-                       int64_t ldo, int32_t* acc_out, int64_t ld_acc, int splits,
-                       int32_t* __restrict__ slabs) {
+    gemm_i8_2sm_kernel(const __grid_constant__ PairParams P) {
   constexpr uint32_t kABytes = kBM * kBK;             // this CTA's 128 rows of A
   constexpr uint32_t kBBytes = (BN / 2) * kBK;        // this CTA's BN/2 rows of B
   constexpr uint32_t kStageBytes = kABytes + kBBytes;
@@ -408,8 +432,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
   const bool leader = rank == 0;
 
   if (warp == 0 && lane == 0) {
-    ptx::tma_prefetch_desc(&map_a);
-    ptx::tma_prefetch_desc(&map_b);
+    for (int q = 0; q < P.nprob; ++q) {
+      ptx::tma_prefetch_desc(&P.a[q]);
+      ptx::tma_prefetch_desc(&P.b[q]);
+    }
   }
   if (warp == 1 && lane == 0) {
     for (int s = 0; s < STAGES; ++s) {
@@ -428,32 +454,50 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
   ptx::tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
 
-  const int num_m = (M + 2 * kBM - 1) / (2 * kBM);
-  const int num_n = (N + BN - 1) / BN;
-  const int tiles = num_m * num_n;
-  const int units = tiles * splits;
-  const int nk_g = (K + kBK - 1) / kBK;
-  const int nk = nk_g * groups;
   const int cid = blockIdx.x >> 1, ncl = gridDim.x >> 1;
+  const int total = P.p[0].units + (P.nprob > 1 ? P.p[1].units : 0);
+  const int count = P.nsched ? int(P.off[cid + 1]) - int(P.off[cid]) : (total - cid + ncl - 1) / ncl;
   const uint32_t full_leader = ptx::mapa(ptx::smem_u32(full), 0);
   const uint32_t tempty_leader = ptx::mapa(ptx::smem_u32(tempty), 0);
+
+  // unit i of this cluster -> (problem, tile, split, K-block range)
+  struct U {
+    int q, mb, nb, sp, kb0, kb1, nk_g;
+  };
+  auto unit = [&](int i) {
+    const int u = P.nsched ? int(P.ids[P.off[cid] + i]) : cid + i * ncl;
+    U r;
+    r.q = (P.nprob > 1 && u >= P.p[1].unit0) ? 1 : 0;
+    const PairProb& pr = P.p[r.q];
+    const int local = u - pr.unit0;
+    const int t = local / pr.splits;
+    r.sp = local - t * pr.splits;
+    const int num_n = (pr.N + BN - 1) / BN;
+    r.mb = t / num_n;
+    r.nb = t - r.mb * num_n;
+    r.nk_g = (pr.K + kBK - 1) / kBK;
+    const int nk = r.nk_g * pr.groups;
+    r.kb0 = int(int64_t(r.sp) * nk / pr.splits);
+    r.kb1 = int(int64_t(r.sp + 1) * nk / pr.splits);
+    return r;
+  };
 
   if (warp == 0) {
     if (ptx::elect_one()) {
       int stage = 0;
       uint32_t phase = 0;
-      for (int u = cid; u < units; u += ncl) {
-        const int t = u / splits, sp = u - t * splits;
-        const int mb = t / num_n, nb = t - mb * num_n;
-        const int kb0 = int(int64_t(sp) * nk / splits), kb1 = int(int64_t(sp + 1) * nk / splits);
-        int g = kb0 / nk_g, kg = kb0 - g * nk_g;
-        for (int kb = kb0; kb < kb1; ++kb) {
+      for (int i = 0; i < count; ++i) {
+        const U w = unit(i);
+        const CUtensorMap* ma = &P.a[w.q];
+        const CUtensorMap* mb = &P.b[w.q];
+        int g = w.kb0 / w.nk_g, kg = w.kb0 - g * w.nk_g;
+        for (int kb = w.kb0; kb < w.kb1; ++kb) {
           ptx::mbar_wait_sleep(&empty[stage], phase ^ 1);
           if (leader) ptx::mbar_arrive_expect_tx(&full[stage], 2 * kStageBytes);
           const uint32_t fb = full_leader + uint32_t(stage) * 8u;
-          ptx::tma_load_3d_2sm(sA + stage * kABytes, &map_a, fb, kg * kBK, mb * 2 * kBM + int(rank) * kBM, g);
-          ptx::tma_load_3d_2sm(sB + stage * kBBytes, &map_b, fb, kg * kBK, nb * BN + int(rank) * (BN / 2), g);
-          if (++kg == nk_g) { kg = 0; ++g; }
+          ptx::tma_load_3d_2sm(sA + stage * kABytes, ma, fb, kg * kBK, w.mb * 2 * kBM + int(rank) * kBM, g);
+          ptx::tma_load_3d_2sm(sB + stage * kBBytes, mb, fb, kg * kBK, w.nb * BN + int(rank) * (BN / 2), g);
+          if (++kg == w.nk_g) { kg = 0; ++g; }
           if (++stage == STAGES) { stage = 0; phase ^= 1; }
         }
       }
@@ -465,13 +509,12 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
       uint32_t phase = 0;
       int acc = 0;
       uint32_t acc_phase = 0;
-      for (int u = cid; u < units; u += ncl) {
-        const int sp = u % splits;
-        const int kb0 = int(int64_t(sp) * nk / splits), kb1 = int(int64_t(sp + 1) * nk / splits);
+      for (int i = 0; i < count; ++i) {
+        const U w = unit(i);
         ptx::mbar_wait_sleep(&tempty[acc], acc_phase ^ 1);
         ptx::tc_fence_after();
         const uint32_t d_tmem = tmem_base + uint32_t(acc * BN);
-        for (int kb = kb0; kb < kb1; ++kb) {
+        for (int kb = w.kb0; kb < w.kb1; ++kb) {
           ptx::mbar_wait(&full[stage], phase);
           ptx::tc_fence_after();
           if (ptx::elect_one()) {
@@ -480,9 +523,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
 #pragma unroll
             for (int k = 0; k < kBK / 32; ++k)
               ptx::mma_i8_2sm(d_tmem, a_desc + uint64_t((k * 32) >> 4), b_desc + uint64_t((k * 32) >> 4), idesc,
-                              (kb != kb0 || k != 0) ? 1u : 0u);
+                              (kb != w.kb0 || k != 0) ? 1u : 0u);
             ptx::mma_commit_2sm(&empty[stage], 0x3);
-            if (kb == kb1 - 1) ptx::mma_commit_2sm(&tfull[acc], 0x3);
+            if (kb == w.kb1 - 1) ptx::mma_commit_2sm(&tfull[acc], 0x3);
           }
           __syncwarp();
           if (++stage == STAGES) { stage = 0; phase ^= 1; }
@@ -492,39 +535,39 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
     }
   } else if (warp >= 4) {
     const uint32_t quarter = warp & 3;
-    const float comb = __fmul_rn(*sa, *sb);
-    const double dscale = __dmul_rn(double(comb), extra);
-    const float fscale = float(dscale);
-    const bool vec_ok = (ldo % 8 == 0) && ((reinterpret_cast<uintptr_t>(out) & 15) == 0);
     int acc = 0;
     uint32_t acc_phase = 0;
-    for (int u = cid; u < units; u += ncl) {
-      const int t = u / splits, sp = u - t * splits;
-      const int mb = t / num_n, nb = t - mb * num_n;
+    for (int i = 0; i < count; ++i) {
+      const U w = unit(i);
+      const PairProb& pr = P.p[w.q];
+      const float comb = __fmul_rn(*pr.sa, *pr.sb);
+      const double dscale = __dmul_rn(double(comb), pr.extra);
+      const float fscale = float(dscale);
+      const bool vec_ok = (pr.ldo % 8 == 0) && ((reinterpret_cast<uintptr_t>(pr.out) & 15) == 0);
       ptx::mbar_wait_sleep(&tfull[acc], acc_phase);
       ptx::tc_fence_after();
-      const int64_t row = int64_t(mb) * 2 * kBM + int64_t(rank) * kBM + quarter * 32 + lane;
-      const int32_t row0 = mb * 2 * kBM + int32_t(rank) * kBM + int32_t(quarter) * 32;
+      const int64_t row = int64_t(w.mb) * 2 * kBM + int64_t(rank) * kBM + quarter * 32 + lane;
+      const int32_t row0 = w.mb * 2 * kBM + int32_t(rank) * kBM + int32_t(quarter) * 32;
       uint8_t* wbuf = stg + quarter * kStgBytes;
 #pragma unroll 1
       for (int c = 0; c < BN / 32; ++c) {
-        const int64_t col0 = int64_t(nb) * BN + c * 32;
+        const int64_t col0 = int64_t(w.nb) * BN + c * 32;
         uint32_t r[32];
         ptx::tmem_ld_32x32b_x32(tmem_base + ((quarter * 32) << 16) + uint32_t(acc * BN + c * 32), r);
         ptx::tmem_ld_wait();
-        if (splits == 1 && tma_out) {
+        if (pr.splits == 1 && pr.tma_out) {
           if (lane == 0) ptx::bulk_wait_read<1>();
           __syncwarp();
-          if (row0 < M && col0 < N)
-            store_chunk_tma(r, fscale, out_dtype, wbuf + (c & 1) * (kStgBytes / 2), lane, &map_o, int32_t(col0),
-                            row0);
-        } else if (row < M && col0 < N) {
-          if (splits == 1) {
-            store_row_chunk(r, row, col0, N, epilogue, dscale, fscale, out, out_dtype, ldo, vec_ok, acc_out,
-                            ld_acc);
+          if (row0 < pr.M && col0 < pr.N)
+            store_chunk_tma(r, fscale, pr.out_dtype, wbuf + (c & 1) * (kStgBytes / 2), lane, &P.o[w.q],
+                            int32_t(col0), row0);
+        } else if (row < pr.M && col0 < pr.N) {
+          if (pr.splits == 1) {
+            store_row_chunk(r, row, col0, pr.N, pr.epilogue, dscale, fscale, pr.out, pr.out_dtype, pr.ldo, vec_ok,
+                            pr.acc_out, pr.ld_acc);
           } else {
-            int32_t* d = slabs + int64_t(sp) * M * N + row * N + col0;
-            if (col0 + 32 <= N && (N & 3) == 0) {
+            int32_t* d = pr.slabs + int64_t(w.sp) * pr.M * pr.N + row * pr.N + col0;
+            if (col0 + 32 <= pr.N && (pr.N & 3) == 0) {
 #pragma unroll
               for (int j = 0; j < 32; j += 4)
                 __stcg(reinterpret_cast<int4*>(d + j),
@@ -532,7 +575,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
             } else {
 #pragma unroll
               for (int j = 0; j < 32; ++j)
-                if (col0 + j < N) d[j] = int(r[j]);
+                if (col0 + j < pr.N) d[j] = int(r[j]);
             }
           }
         }
@@ -717,16 +760,87 @@ int run(const int8_t* A, int64_t lda, const int8_t* B, int64_t ldb, int64_t M, i
                               ld_acc, splits, ws, geo, stream);
 }
 
+struct PairSpec {  // one product for the CTA-pair kernel
+  const int8_t* A;
+  int64_t lda;
+  const int8_t* B;
+  int64_t ldb;
+  int64_t M, N, K, groups, a_gstride, b_gstride;
+  const float* sa;
+  const float* sb;
+  double extra;
+  int epilogue;
+  void* out;
+  int out_dtype;
+  int64_t ldo;
+  int32_t* acc_out;
+  int64_t ld_acc;
+  int splits;
+  void* ws;
+};
+
+template <int BN>
+bool fill_prob(PairParams& P, int q, const PairSpec& s, int unit0) {
+  if (!make_map(&P.a[q], s.A, s.M, s.K, s.lda, s.groups, s.a_gstride, kBM) ||
+      !make_map(&P.b[q], s.B, s.N, s.K, s.ldb, s.groups, s.b_gstride, BN / 2))
+    return false;
+  PairProb& p = P.p[q];
+  p.M = int(s.M); p.N = int(s.N); p.K = int(s.K); p.groups = int(s.groups); p.splits = s.splits;
+  p.tma_out = make_out_map(&P.o[q], s.out, s.out_dtype, s.M, s.N, s.ldo, s.epilogue, s.acc_out, s.splits) ? 1 : 0;
+  if (!p.tma_out) P.o[q] = P.a[q];  // unused
+  p.epilogue = s.epilogue; p.out_dtype = s.out_dtype; p.sa = s.sa; p.sb = s.sb; p.extra = s.extra;
+  p.out = s.out; p.ldo = s.ldo; p.acc_out = s.acc_out; p.ld_acc = s.ld_acc;
+  p.slabs = s.splits > 1 ? static_cast<int32_t*>(s.ws) : nullptr;
+  p.unit0 = unit0;
+  p.units = int(((s.M + 2 * kBM - 1) / (2 * kBM)) * ((s.N + BN - 1) / BN) * s.splits);
+  return true;
+}
+
+// Longest-processing-time-first static schedule over the clusters (cost of a
+// unit = its K blocks + a fixed epilogue / pipeline-fill term).  false if the
+// table does not fit the kernel parameters (then: round-robin).
+bool lpt_schedule(PairParams& P, int ncl) {
+  const int total = P.p[0].units + (P.nprob > 1 ? P.p[1].units : 0);
+  if (total > kMaxSched || ncl > 128 || total > 65535) return false;
+  std::vector<std::pair<int, int>> cost(total);  // (cost, unit)
+  for (int u = 0; u < total; ++u) {
+    const PairProb& pr = P.p[(P.nprob > 1 && u >= P.p[1].unit0) ? 1 : 0];
+    const int nk = ((pr.K + kBK - 1) / kBK) * pr.groups / pr.splits;
+    cost[u] = {nk + 4, u};
+  }
+  std::stable_sort(cost.begin(), cost.end(), [](const auto& x, const auto& y) { return x.first > y.first; });
+  std::vector<int64_t> load(ncl, 0);
+  std::vector<std::vector<uint16_t>> lists(ncl);
+  for (const auto& cu : cost) {
+    int best = 0;
+    for (int c = 1; c < ncl; ++c)
+      if (load[c] < load[best]) best = c;
+    load[best] += cu.first;
+    lists[best].push_back(uint16_t(cu.second));
+  }
+  int o = 0;
+  for (int c = 0; c < ncl; ++c) {
+    P.off[c] = uint16_t(o);
+    for (uint16_t u : lists[c]) P.ids[o++] = u;
+  }
+  P.off[ncl] = uint16_t(o);
+  P.nsched = 1;
+  return true;
+}
+
 template <int BN, int STAGES>
-int run_2sm(const int8_t* A, int64_t lda, const int8_t* B, int64_t ldb, int64_t M, int64_t N, int64_t K,
-            int64_t groups, int64_t a_gstride, int64_t b_gstride, const float* sa, const float* sb, double extra,
-            int epilogue, void* out, int out_dtype, int64_t ldo, int32_t* acc_out, int64_t ld_acc, int splits,
-            void* ws, cudaStream_t stream) {
+int run_2sm_specs(const PairSpec* specs, int n, cudaStream_t stream) {
   constexpr size_t kSmem = size_t(STAGES) * (kBM * kBK + (BN / 2) * kBK) + kStgAll + 1024 + 256;
-  CUtensorMap ma, mb;
-  if (!make_map(&ma, A, M, K, lda, groups, a_gstride, kBM) ||
-      !make_map(&mb, B, N, K, ldb, groups, b_gstride, BN / 2))
-    return -1;
+  static PairParams P;  // host staging (large); launches copy it into the parameter buffer
+  static std::mutex mu;
+  std::lock_guard<std::mutex> lock(mu);
+  memset(&P, 0, sizeof(P));
+  P.nprob = n;
+  int unit0 = 0;
+  for (int q = 0; q < n; ++q) {
+    if (!fill_prob<BN>(P, q, specs[q], unit0)) return -1;
+    unit0 += P.p[q].units;
+  }
   static bool attr_set = false;
   if (!attr_set) {
     cudaError_t e = cudaFuncSetAttribute(gemm_i8_2sm_kernel<BN, STAGES>,
@@ -734,25 +848,32 @@ int run_2sm(const int8_t* A, int64_t lda, const int8_t* B, int64_t ldb, int64_t 
     if (e != cudaSuccess) return int(e);
     attr_set = true;
   }
-  const int64_t tiles = ((M + 2 * kBM - 1) / (2 * kBM)) * ((N + BN - 1) / BN);
-  const int64_t units = tiles * splits;
   const int64_t pairs = num_sms() / 2;
-  const int grid = 2 * int(units < pairs ? units : pairs);
-  int32_t* slabs = splits > 1 ? static_cast<int32_t*>(ws) : nullptr;
-  CUtensorMap mo;
-  const int tma_out = make_out_map(&mo, out, out_dtype, M, N, ldo, epilogue, acc_out, splits) ? 1 : 0;
-  if (!tma_out) mo = ma;  // unused
-  gemm_i8_2sm_kernel<BN, STAGES><<<grid, kThreads, kSmem, stream>>>(
-      ma, mb, mo, tma_out, int(M), int(N), int(K), int(groups), sa, sb, extra, epilogue, out, out_dtype, ldo,
-      acc_out, ld_acc, splits, slabs);
-  if (splits > 1) {
-    const int64_t nq = M * N / 4;
-    int fgrid = int((nq + 255) / 256);
-    if (fgrid > num_sms() * 8) fgrid = num_sms() * 8;
-    splitk_finalize<<<fgrid, 256, 0, stream>>>(slabs, splits, int(M), int(N), sa, sb, extra, epilogue, out,
-                                               out_dtype, ldo, acc_out, ld_acc);
+  const int ncl = int(unit0 < pairs ? unit0 : pairs);
+  if (n > 1) lpt_schedule(P, ncl);
+  gemm_i8_2sm_kernel<BN, STAGES><<<2 * ncl, kThreads, kSmem, stream>>>(P);
+  for (int q = 0; q < n; ++q) {
+    const PairSpec& s = specs[q];
+    if (s.splits > 1) {
+      const int64_t nq = s.M * s.N / 4;
+      int fgrid = int((nq + 255) / 256);
+      if (fgrid > num_sms() * 8) fgrid = num_sms() * 8;
+      splitk_finalize<<<fgrid, 256, 0, stream>>>(static_cast<int32_t*>(s.ws), s.splits, int(s.M), int(s.N), s.sa,
+                                                 s.sb, s.extra, s.epilogue, s.out, s.out_dtype, s.ldo, s.acc_out,
+                                                 s.ld_acc);
+    }
   }
   return int(cudaGetLastError());
+}
+
+template <int BN, int STAGES>
+int run_2sm(const int8_t* A, int64_t lda, const int8_t* B, int64_t ldb, int64_t M, int64_t N, int64_t K,
+            int64_t groups, int64_t a_gstride, int64_t b_gstride, const float* sa, const float* sb, double extra,
+            int epilogue, void* out, int out_dtype, int64_t ldo, int32_t* acc_out, int64_t ld_acc, int splits,
+            void* ws, cudaStream_t stream) {
+  const PairSpec s{A, lda, B, ldb, M, N, K, groups, a_gstride, b_gstride, sa, sb, extra, epilogue, out, out_dtype,
+                   ldo, acc_out, ld_acc, splits, ws};
+  return run_2sm_specs<BN, STAGES>(&s, 1, stream);
 }
 
 typedef CUresult (*EncodeIm2colFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
@@ -843,6 +964,28 @@ GemmPlan finish_plan(GemmPlan p, int64_t M, int64_t N, bool allow_split) {
 }
 
 }  // namespace
+
+int launch_gemm_i8_pair2(const GemmDesc* d, cudaStream_t stream) {
+  // both products as CTA-pair units of one launch (LPT-scheduled); the caller
+  // checked that both have long contractions (>= 16 K blocks) and >= 256 rows
+  const int bn = (d[0].N > 128 && d[1].N > 128) ? 256 : 128;
+  PairSpec s[2];
+  for (int q = 0; q < 2; ++q)
+    s[q] = PairSpec{d[q].A, d[q].lda, d[q].B, d[q].ldb, d[q].M, d[q].N, d[q].K, d[q].groups, d[q].a_gstride,
+                    d[q].b_gstride, d[q].sa, d[q].sb, d[q].extra, d[q].epilogue, d[q].out, d[q].out_dtype,
+                    d[q].ldo, d[q].acc_out, d[q].ld_acc, 1, nullptr};
+  if (bn == 256) return run_2sm_specs<256, 6>(s, 2, stream);
+  return run_2sm_specs<128, 8>(s, 2, stream);
+}
+
+bool gemm_i8_pair2_eligible(const GemmDesc* d) {
+  for (int q = 0; q < 2; ++q) {
+    const int64_t nk = ((d[q].K + kBK - 1) / kBK) * d[q].groups;
+    if (nk < 16 || d[q].M < 2 * kBM) return false;
+  }
+  if (const char* e = getenv("HLQ_GEMM_FUSE2")) return atoi(e) != 0;
+  return true;
+}
 
 size_t gemm_i8_ws_bytes(int64_t M, int64_t N, int64_t K, int64_t groups) {
   return plan_gemm(M, N, K, groups, true).ws;

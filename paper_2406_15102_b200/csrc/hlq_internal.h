@@ -83,6 +83,25 @@ constexpr int kMaxWeights = 128;
 int launch_weight_codes(int n, const float* const* w, const int64_t* O, const int64_t* I, int bits,
                         int8_t* const* codes, const int64_t* ld, float* const* scales, uint32_t* ws,
                         cudaStream_t stream);
+// Two products in one CTA-pair launch (hlq_gemm_i8_multi).
+struct GemmDesc {
+  const int8_t* A;
+  int64_t lda, a_gstride;
+  const int8_t* B;
+  int64_t ldb, b_gstride;
+  int64_t M, N, K, groups;
+  const float* sa;
+  const float* sb;
+  double extra;
+  int epilogue;
+  void* out;
+  int out_dtype;
+  int64_t ldo;
+  int32_t* acc_out;
+  int64_t ld_acc;
+};
+bool gemm_i8_pair2_eligible(const GemmDesc* d);
+int launch_gemm_i8_pair2(const GemmDesc* d, cudaStream_t stream);
 // Workspace bytes that let launch_gemm_i8 split K (0: no split planned).
 size_t gemm_i8_ws_bytes(int64_t M, int64_t N, int64_t K, int64_t groups);
 

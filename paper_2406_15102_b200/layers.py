@@ -125,10 +125,18 @@ class HLQLinearFunction(torch.autograd.Function):
             main = torch.cuda.current_stream()
             side = side_stream(gy.device)
             side.wait_stream(main)
-            with torch.cuda.stream(side):
-                gw, _ = ops.gemm_i8(cg, payload, O, I, k, bits_gw, bits_gw, sg, sx, 1.0, exact=False)
-            gx, _ = ops.gemm_i8(cgx, cw, B * L, I, ops.pad16(O), bits_gx, bits_gx, sgx, sw, 1.0,
-                                exact=False, out_dtype=out_dtype)
+            if side is main:
+                # dW and dX as one CTA-pair launch over both products' tiles when both
+                # contractions are long (otherwise hlq_gemm_i8_multi runs them back to back)
+                gw, gx = ops.gemm_i8_pair(
+                    dict(a=cg, b=payload, m=O, n=I, k=k, bits_a=bits_gw, bits_b=bits_gw, sa=sg, sb=sx),
+                    dict(a=cgx, b=cw, m=B * L, n=I, k=ops.pad16(O), bits_a=bits_gx, bits_b=bits_gx, sa=sgx,
+                         sb=sw, out_dtype=out_dtype))
+            else:
+                with torch.cuda.stream(side):
+                    gw, _ = ops.gemm_i8(cg, payload, O, I, k, bits_gw, bits_gw, sg, sx, 1.0, exact=False)
+                gx, _ = ops.gemm_i8(cgx, cw, B * L, I, ops.pad16(O), bits_gx, bits_gx, sgx, sw, 1.0,
+                                    exact=False, out_dtype=out_dtype)
             main.wait_stream(side)
             gw.record_stream(main)
             for t in (cg, sg, payload, sx):

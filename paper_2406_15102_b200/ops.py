@@ -280,6 +280,34 @@ def gemm_i8(a: torch.Tensor, b: torch.Tensor, m: int, n: int, k: int, bits_a: in
     return out, acc
 
 
+def gemm_i8_pair(p0: dict, p1: dict):
+    """Two independent products (typically a layer's dX and dW) in one call:
+    each dict holds gemm_i8's arguments (a, b, m, n, k, bits_a, bits_b, sa, sb,
+    extra, out_dtype; fast epilogue, single K group).  With long contractions
+    they run as one CTA-pair launch over both products' tiles
+    (hlq_gemm_i8_multi).  Returns (out0, out1)."""
+    outs, descs = [], []
+    for q in (p0, p1):
+        a, b = q["a"], q["b"]
+        if a.dtype != torch.int8 or b.dtype != torch.int8:
+            raise ParameterError("GEMM operands must be int8 codes")
+        m, n, k = q["m"], q["n"], q["k"]
+        od = q.get("out_dtype", torch.float32)
+        out = torch.empty((m, n), dtype=od, device=a.device)
+        outs.append(out)
+        descs.append(_lib.GemmDesc(a.data_ptr(), a.stride(0), a.stride(0) * m, b.data_ptr(), b.stride(0),
+                                   b.stride(0) * n, m, n, k, 1, q["bits_a"], q["bits_b"], q["sa"].data_ptr(),
+                                   q["sb"].data_ptr(), float(q.get("extra", 1.0)), _lib.HLQ_EPI_FAST,
+                                   out.data_ptr(), _lib.HLQ_BF16 if od == torch.bfloat16 else _lib.HLQ_F32, n, None,
+                                   0))
+    arr = (_lib.GemmDesc * 2)(*descs)
+    ops_ = 2 * sum(q["m"] * q["n"] * q["k"] for q in (p0, p1))
+    _traced("gemm", 0, ops_, 1, lambda: _lib.call("hlq_gemm_i8_multi", 2, ctypes.cast(arr, ctypes.c_void_p),
+                                                  _stream()),
+            key=f"gemm:pair:{p0['m']}x{p0['n']}x{p0['k']}+{p1['m']}x{p1['n']}x{p1['k']}")
+    return outs[0], outs[1]
+
+
 def conv_out_hw(H: int, W: int, k: int, stride: int, pad: int):
     return (H + 2 * pad - k) // stride + 1, (W + 2 * pad - k) // stride + 1
 

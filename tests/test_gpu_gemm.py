@@ -130,3 +130,23 @@ def test_linear_uses_refreshed_weight_codes(ops):
         net[2].weight.add_(1.0)
     assert net[0].cached_weight_codes() is not None and net[2].cached_weight_codes() is None
     assert refresh_weight_codes(net) == 1
+
+
+@pytest.mark.parametrize("fuse", ["1", "0"])
+def test_gemm_pair_matches_separate(ops, fuse, monkeypatch):
+    """A layer's dW and dX in one CTA-pair launch (LPT schedule over both
+    products' tiles) == two separate fast-epilogue GEMMs, bit for bit."""
+    monkeypatch.setenv("HLQ_GEMM_FUSE2", fuse)
+    torch.manual_seed(4)
+    O, I, T, K = 3072, 768, 4100, 2304
+    cg = torch.randint(-127, 128, (O, K), dtype=torch.int8, device="cuda")
+    xp = torch.randint(-127, 128, (I, K), dtype=torch.int8, device="cuda")
+    cgx = torch.randint(-7, 8, (T, O), dtype=torch.int8, device="cuda")
+    cw = torch.randint(-7, 8, (I, O), dtype=torch.int8, device="cuda")
+    s = [torch.tensor([v], device="cuda") for v in (0.013, 0.0021, 0.37, 0.0049)]
+    gw, gx = ops.gemm_i8_pair(dict(a=cg, b=xp, m=O, n=I, k=K, bits_a=8, bits_b=8, sa=s[0], sb=s[1]),
+                              dict(a=cgx, b=cw, m=T, n=I, k=O, bits_a=4, bits_b=4, sa=s[2], sb=s[3],
+                                   out_dtype=torch.bfloat16))
+    rw, _ = ops.gemm_i8(cg, xp, O, I, K, 8, 8, s[0], s[1], 1.0, exact=False)
+    rx, _ = ops.gemm_i8(cgx, cw, T, I, O, 4, 4, s[2], s[3], 1.0, exact=False, out_dtype=torch.bfloat16)
+    assert torch.equal(gw, rw) and torch.equal(gx, rx)
