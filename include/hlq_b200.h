@@ -227,6 +227,24 @@ HLQ_API int hlq_conv_acbp_compress(const void* x_nhwc, int dtype, int64_t B, int
                                    int bits, int8_t* payload, int64_t ld_payload, float* scale_out,
                                    uint32_t* stats_ws, void* stream);
 
+/* True stochastic rounding (quantize.py:114-125), bit-exact with the
+ * reference's RngState streams: codes of the transformed source with
+ * up = f64(q - floor(q)) > U, U = the element's draw from numpy's
+ * Philox4x64-10 keyed [seed, counter] (RngState(seed, counter).uniform over
+ * the array the reference quantizes, C order).  seed = RngState.split(tag) of
+ * the caller's state (tags backprop.py:42-43).  along_cols = 1: HT along cols
+ * (the gx operand of gy; codes (segs*rows, ld_dst)); 0: projection along rows
+ * keeping `bitmap` (gw operand / ACBP / W codes with bitmap 0xFFFF; codes
+ * K-major per column, as hlq_quantize_proj_rows).  index_kind (rows mode):
+ * 0 = the reference quantizes (cols, K) (gy's gw operand), 1 = (K, cols)
+ * (ACBP payload, W), 2 = batch-axis gy with L > 1, cols = l2 * o2.
+ * stats_ws: 32 bytes (the STATS pass runs inside). */
+HLQ_API int hlq_quantize_stochastic(const void* src, int dtype, int64_t segs, int64_t rows, int64_t cols,
+                                    int64_t ld_src, int64_t seg_src, int along_cols, uint32_t bitmap,
+                                    int bits, uint64_t seed, uint64_t counter, int index_kind, int64_t l2,
+                                    int64_t o2, uint32_t* stats_ws, int8_t* dst, int64_t ld_dst,
+                                    float* scale_out, void* stream);
+
 /* The dX right operand of many layers at once: codes_i = Q_bits(HT_O(W_i))
  * for n <= 128 fp32 weights W_i (O_i x I_i, row-major), written K-major as
  * (I_i rows of ld_i >= pad16(O_i) bytes), scale_i one fp32 each -- identical

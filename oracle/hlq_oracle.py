@@ -23,6 +23,8 @@ Reference anchors (paths relative to ``/root/reference/pkg/src/hlq``):
   backprop.py:212-234  block transform / low-rank projection along one axis
   quantize.py:94-100   per-tensor symmetric scale
   quantize.py:128-145  pseudo-stochastic rounding (low 11 bits as the draw)
+  quantize.py:26-59,114-125  RngState (splitmix64 splits, Philox4x64 draws) and
+                       true stochastic rounding; backprop.py:42-43,206-209 tags
   quantize.py:152-187  exact integer GEMM + fp64 dequant epilogue
   backprop.py:350-447  hq_grad_input / acbp_compress / hlq_grad_weight / hlq_backward
   harness/layers.py:96-158  conv lowering (im2col / col2im)
@@ -160,6 +162,62 @@ def quantize_with_amax(v: np.ndarray, bits: int, amax) -> tuple:
     return np.clip(lo + bump.astype(F32), -qmax, qmax).astype(np.int8), scale
 
 
+# ---------------------------------------------------------------------------
+# true stochastic rounding (quantize.py:26-59,114-125; backprop.py:42-43,206-209)
+# ---------------------------------------------------------------------------
+
+TAG_GX_LEFT, TAG_GX_RIGHT, TAG_GW_LEFT, TAG_GW_RIGHT = 11, 12, 21, 22
+_M64 = (1 << 64) - 1
+
+
+def splitmix64(x: int) -> int:
+    x = (x + 0x9E3779B97F4A7C15) & _M64
+    x = ((x ^ (x >> 30)) * 0xBF58476D1CE4E5B9) & _M64
+    x = ((x ^ (x >> 27)) * 0x94D049BB133111EB) & _M64
+    return (x ^ (x >> 31)) & _M64
+
+
+def split_seed(seed: int, *path: int) -> int:
+    """RngState(seed).split(*path).seed (quantize.py:48-52)."""
+    key = int(seed) & _M64
+    for p in path:
+        key = splitmix64(key ^ splitmix64(int(p) & _M64))
+    return key
+
+
+def uniform(seed: int, counter: int, shape) -> np.ndarray:
+    """RngState(seed, counter).uniform(shape): numpy's Philox4x64-10 keyed
+    [seed, counter], float64 draws in C order (quantize.py:54-59)."""
+    key = np.array([int(seed) & _M64, int(counter) & _M64], dtype=np.uint64)
+    return np.random.Generator(np.random.Philox(key=key)).random(size=shape)
+
+
+def quantize_stochastic(v: np.ndarray, bits: int, seed: int):
+    """quant_stochastic(v, bits, RngState(seed)) (quantize.py:114-125):
+    up = f64(q - floor(q)) > U.  -> (int8 codes, f32 scale)."""
+    qmax = QMAX[bits]
+    v = np.ascontiguousarray(v, dtype=F32)
+    if not np.isfinite(v).all():
+        raise OracleError("non-finite input")
+    amax = F32(np.abs(v).max()) if v.size else F32(0)
+    scale = F32(amax / F32(qmax))
+    if scale == 0:
+        scale = F32(1.0)
+    q = v / scale
+    lo = np.floor(q)
+    up = (q - lo) > uniform(seed, 0, v.shape)
+    codes = np.clip(lo + up.astype(F32), -qmax, qmax).astype(np.int8)
+    return codes, scale
+
+
+def _q(v: np.ndarray, bits: int, rng_seed, tag: int):
+    """_quant (backprop.py:206-209): pseudo when rng is None, else stochastic
+    on the tag's split stream."""
+    if rng_seed is None:
+        return quantize(v, bits)
+    return quantize_stochastic(v, bits, split_seed(rng_seed, tag))
+
+
 def int_gemm(a: np.ndarray, b: np.ndarray) -> np.ndarray:
     """Exact sum of int8 products; fp64 BLAS is exact below 2**53."""
     return (a.astype(np.float64) @ b.astype(np.float64)).astype(np.int64)
@@ -175,13 +233,14 @@ def dequant(acc: np.ndarray, sa, sb, extra: float = 1.0) -> np.ndarray:
 # ---------------------------------------------------------------------------
 
 def hq_grad_input(gy3: np.ndarray, w: np.ndarray, bits: int = 4, n: int = 16,
-                  stages: dict | None = None) -> np.ndarray:
+                  stages: dict | None = None, rng: int | None = None) -> np.ndarray:
+    """rng: the RngState seed (counter 0) for true stochastic rounding, or None."""
     B, L, O = gy3.shape
     I = w.shape[1]
     ghat = transform_axis(gy3, 2, n).reshape(B * L, -1)
     what = transform_axis(w, 0, n)
-    cg, sg = quantize(ghat, bits)
-    cw, sw = quantize(what, bits)
+    cg, sg = _q(ghat, bits, rng, TAG_GX_LEFT)
+    cw, sw = _q(what, bits, rng, TAG_GX_RIGHT)
     acc = int_gemm(cg, cw)
     out = dequant(acc, sg, sw).reshape(B, L, I)
     if stages is not None:
@@ -190,23 +249,23 @@ def hq_grad_input(gy3: np.ndarray, w: np.ndarray, bits: int = 4, n: int = 16,
 
 
 def acbp_compress(x3: np.ndarray, bases, bits: int = 8, n: int = 16,
-                  pad_small_axes: bool = False):
+                  pad_small_axes: bool = False, rng: int | None = None):
     """Forward-time projection + quantization of X -> (payload (K, I), scale, axis)."""
     B, L, I = x3.shape
     axis = proj_axis_rule(B, L, n, pad_small_axes)
     proj = transform_axis(x3, axis, n, bases)
-    codes, scale = quantize(proj, bits)
+    codes, scale = _q(proj, bits, rng, TAG_GW_RIGHT)
     return codes.reshape(-1, I), scale, axis
 
 
 def hlq_grad_weight(payload: np.ndarray, x_scale, axis: int, gy3: np.ndarray,
                     bases, bits: int = 8, n: int = 16, extra: float | None = None,
-                    stages: dict | None = None) -> np.ndarray:
+                    stages: dict | None = None, rng: int | None = None) -> np.ndarray:
     B, L, O = gy3.shape
     gproj = transform_axis(gy3, axis, n, bases).reshape(-1, O)
     if gproj.shape[0] != payload.shape[0]:
         raise OracleError("projected extents differ")
-    cg, sg = quantize(np.ascontiguousarray(gproj.T), bits)
+    cg, sg = _q(np.ascontiguousarray(gproj.T), bits, rng, TAG_GW_LEFT)
     acc = int_gemm(cg, payload)
     out = dequant(acc, sg, x_scale, 1.0 / B if extra is None else extra)
     if stages is not None:
@@ -217,14 +276,16 @@ def hlq_grad_weight(payload: np.ndarray, x_scale, axis: int, gy3: np.ndarray,
 def hlq_backward(x3: np.ndarray, w: np.ndarray, gy3: np.ndarray, rank: int = 8,
                  bits_gx: int = 4, bits_gw: int = 8, n: int = 16, bases=None,
                  pad_small_axes: bool = False, extra: float | None = None,
-                 stages: dict | None = None):
-    """ACBP branch of strategy_backward (backprop.py:416-430): gw then gx."""
+                 stages: dict | None = None, rng: int | None = None):
+    """ACBP branch of strategy_backward (backprop.py:416-430): gw then gx.
+    rng: RngState seed for true stochastic rounding (every site splits it by
+    its tag, so forward ACBP and backward draw independent streams)."""
     bases = lowest_sequency_bases(n, rank) if bases is None else tuple(bases)
-    payload, sx, axis = acbp_compress(x3, bases, bits_gw, n, pad_small_axes)
+    payload, sx, axis = acbp_compress(x3, bases, bits_gw, n, pad_small_axes, rng)
     if stages is not None:
         stages.update(x_codes=payload, x_scale=sx, axis=axis)
-    gw = hlq_grad_weight(payload, sx, axis, gy3, bases, bits_gw, n, extra, stages)
-    gx = hq_grad_input(gy3, w, bits_gx, n, stages)
+    gw = hlq_grad_weight(payload, sx, axis, gy3, bases, bits_gw, n, extra, stages, rng)
+    gx = hq_grad_input(gy3, w, bits_gx, n, stages, rng)
     return gx, gw
 
 

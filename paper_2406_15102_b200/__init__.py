@@ -18,6 +18,7 @@ from .backprop import (
     strategy_backward,
 )
 from .errors import DimensionError, ParameterError, StateError
+from .rng import RngState
 from .hadamard import DEFAULT_BLOCK, DEFAULT_RANK, HadamardPlan, lowest_sequency_bases, sequency_order
 
 __version__ = "0.1.0"

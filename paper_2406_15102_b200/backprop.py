@@ -16,8 +16,10 @@ int8 GEMM with the fused dequant epilogue.  Outputs are fp32 and, with the
 exact epilogue used here, bit-identical to the reference on the same inputs.
 
 Differences from the reference, by design:
-  * ``rng`` (true stochastic rounding, quantize.py:114-125) is not implemented
-    on the GPU yet: passing one raises ParameterError.
+  * ``rng`` (true stochastic rounding, quantize.py:114-125) runs on the GPU
+    (hlq_quantize_stochastic: numpy's Philox4x64-10 stream reproduced in CUDA),
+    bit-identical to the reference's RngState draws; the fused dual transform
+    of the pseudo mode is not used then (each operand has its own stream).
   * the ACBP payload is stored K-major ((I, K) instead of (K, I)), which is
     the tcgen05 operand layout; ``ACBPActivation.reference_payload()``
     returns the reference layout.
@@ -29,6 +31,7 @@ from dataclasses import dataclass, field, replace
 import torch
 
 from . import ops
+from .rng import TAG_GW_LEFT, TAG_GW_RIGHT, TAG_GX_LEFT, TAG_GX_RIGHT, site_key
 from .errors import DimensionError, ParameterError, StateError
 from .hadamard import DEFAULT_BLOCK, DEFAULT_RANK, HadamardPlan, lowest_sequency_bases
 
@@ -150,10 +153,9 @@ def ht_axis_for(B: int, L: int, block: int, pad_small_axes: bool = False) -> int
     return 1 if L >= B else 0
 
 
-def _no_rng(rng):
-    if rng is not None:
-        raise ParameterError("true stochastic rounding (rng) is not implemented on the B200 path; "
-                             "use the default pseudo-stochastic mode (rng=None)")
+def _check_rng(rng):
+    if rng is not None and not (hasattr(rng, "seed") and hasattr(rng, "counter")):
+        raise ParameterError("rng must be an RngState (seed, counter), e.g. paper_2406_15102_b200.RngState")
 
 
 def _as3(t: torch.Tensor, what: str) -> torch.Tensor:
@@ -173,13 +175,19 @@ def acbp_compress(x: torch.Tensor, plan: HadamardPlan, bits: int = 8, rng=None,
                   pad_small_axes: bool = False, check_finite: bool = True) -> ACBPActivation:
     """backprop.py:373-385 on the GPU: project X along ht_axis_for's axis,
     quantize (int8 by default), keep only the payload."""
-    _no_rng(rng)
+    _check_rng(rng)
     x = _as3(x, "x")
     B, L, I = x.shape
     axis = ht_axis_for(B, L, plan.block_size, pad_small_axes)
     segs, rows, cols, ld_src, seg_src = _proj_view(B, L, I, axis)
-    codes, k, scale, amax = ops.quant_proj_rows(x, segs, rows, cols, plan.gpu_bitmap(), bits,
-                                                ld_src, seg_src)
+    if rng is not None:
+        # reference quantizes proj (K, I) / (Kb, L, I) in C order: index k*cols + c
+        seed, ctr = site_key(rng, TAG_GW_RIGHT)
+        codes, scale, amax, k = ops.quant_stochastic(x, segs, rows, cols, ld_src, seg_src, False,
+                                                     plan.gpu_bitmap(), bits, seed, ctr, index_kind=1)
+    else:
+        codes, k, scale, amax = ops.quant_proj_rows(x, segs, rows, cols, plan.gpu_bitmap(), bits,
+                                                    ld_src, seg_src)
     if check_finite:
         ops.check_finite(amax)
     q = QuantizedTensor(payload=codes, bits=bits, scale=scale)
@@ -190,7 +198,7 @@ def hq_grad_input(gy: torch.Tensor, w: torch.Tensor, bits: int | None, rng=None,
                   block: int = DEFAULT_BLOCK, out_dtype=torch.float32, exact: bool = True,
                   check_finite: bool = True, stages: dict | None = None) -> torch.Tensor:
     """backprop.py:350-370: dX = deq(Q(HT_O(gy)) . Q(HT_O(W))), full rank, no inverse HT."""
-    _no_rng(rng)
+    _check_rng(rng)
     if gy.dim() != 3 or w.dim() != 2:
         raise DimensionError(f"expected gy (B,L,O) and w (O,I), got {tuple(gy.shape)}, {tuple(w.shape)}")
     if gy.shape[2] != w.shape[0]:
@@ -201,9 +209,17 @@ def hq_grad_input(gy: torch.Tensor, w: torch.Tensor, bits: int | None, rng=None,
         raise ParameterError(f"the B200 kernels implement block 16 only, got {block}")
     B, L, O = gy.shape
     I = w.shape[1]
-    cg, sg, ag = ops.quant_ht_cols(gy.reshape(B * L, O), bits)
     w32 = w if w.dtype == torch.float32 else w.float()
-    cw, kw, sw, aw = ops.quant_proj_rows(w32, 1, O, I, 0xFFFF, bits)
+    if rng is not None:
+        seed, ctr = site_key(rng, TAG_GX_LEFT)
+        g2 = gy.reshape(B * L, O).contiguous()
+        cg, sg, ag = ops.quant_stochastic(g2, 1, B * L, O, O, B * L * O, True, 0xFFFF, bits, seed, ctr)
+        seed, ctr = site_key(rng, TAG_GX_RIGHT)
+        cw, sw, aw, kw = ops.quant_stochastic(w32.contiguous(), 1, O, I, I, O * I, False, 0xFFFF, bits, seed,
+                                              ctr, index_kind=1)
+    else:
+        cg, sg, ag = ops.quant_ht_cols(gy.reshape(B * L, O), bits)
+        cw, kw, sw, aw = ops.quant_proj_rows(w32, 1, O, I, 0xFFFF, bits)
     if check_finite:
         ops.check_finite(ag, aw)
     out, acc = ops.gemm_i8(cg, cw, B * L, I, ops.pad16(O), bits, bits, sg, sw, 1.0, exact=exact,
@@ -225,14 +241,23 @@ def hlq_grad_weight(acbp: ACBPActivation, gy: torch.Tensor, bits: int = 8, rng=N
                     check_finite: bool = True, stages: dict | None = None) -> torch.Tensor:
     """backprop.py:388-410: project gy onto the ACBP bases, quantize, int8 GEMM
     against the stored payload, dequantize with s_g * s_x * extra (1/B by default)."""
-    _no_rng(rng)
+    _check_rng(rng)
     B, L, I = acbp.orig_shape
     if gy.dim() != 3 or gy.shape[0] != B or gy.shape[1] != L:
         raise StateError(f"gy shape {tuple(gy.shape)} does not match the compressed activation ({B}, {L}, ...)")
     if acbp.quantized.bits != bits:
         raise StateError(f"compressed activation is {acbp.quantized.bits}-bit but backward wants {bits}-bit")
     O = gy.shape[2]
-    cg, k, sg, ag = _gy_projection(gy, acbp.axis, acbp.plan, bits)
+    if rng is not None:
+        # the reference quantizes gy2.T: (O, K) for tokens / L == 1, (O, Kb*L) for the batch axis
+        seed, ctr = site_key(rng, TAG_GW_LEFT)
+        segs, rows, cols, ld_src, seg_src = _proj_view(B, L, O, acbp.axis)
+        kind = 2 if (acbp.axis == 0 and L > 1) else 0
+        cg, sg, ag, k = ops.quant_stochastic(gy.contiguous(), segs, rows, cols, ld_src, seg_src, False,
+                                             acbp.plan.gpu_bitmap(), bits, seed, ctr, index_kind=kind,
+                                             l2=L, o2=O)
+    else:
+        cg, k, sg, ag = _gy_projection(gy, acbp.axis, acbp.plan, bits)
     if k != acbp.k:
         raise StateError("projected extents differ between forward and backward; the plans do not match")
     if check_finite:

@@ -352,6 +352,37 @@ int hlq_quantize_weights(int n, const float* const* w, const int64_t* O, const i
   return cuda_status("hlq_quantize_weights");
 }
 
+int hlq_quantize_stochastic(const void* src, int dtype, int64_t segs, int64_t rows, int64_t cols,
+                            int64_t ld_src, int64_t seg_src, int along_cols, uint32_t bitmap, int bits,
+                            uint64_t seed, uint64_t counter, int index_kind, int64_t l2, int64_t o2,
+                            uint32_t* stats_ws, int8_t* dst, int64_t ld_dst, float* scale_out, void* stream) {
+  HLQ_TRY(check_dtype(dtype));
+  HLQ_TRY(check_bits(bits));
+  if (index_kind < 0 || index_kind > 2) return fail(HLQ_ERR_PARAMETER, "index_kind must be 0, 1 or 2");
+  if (along_cols) {
+    HLQ_TRY(check_ld16(ld_dst, "codes"));
+    if (segs < 0 || rows < 0 || cols < 0 || ld_src < cols || ld_dst < pad16(cols) ||
+        (segs > 1 && seg_src < rows * ld_src))
+      return fail(HLQ_ERR_DIMENSION, "bad stochastic view");
+  } else {
+    HLQ_TRY(proj_rows_checked(src, dtype, segs, rows, cols, ld_src, seg_src, bitmap, bits, dst, ld_dst));
+    if (index_kind == 2 && (l2 <= 0 || o2 <= 0 || l2 * o2 != cols))
+      return fail(HLQ_ERR_DIMENSION, "batch-axis index layout needs cols == l2 * o2");
+  }
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  hlq::TransformArgs t = proj_args(src, dtype, segs, rows, cols, ld_src, seg_src, along_cols ? 0xFFFFu : bitmap,
+                                   bits, stats_ws, nullptr, 0, nullptr);
+  t.do_gx = along_cols != 0;
+  t.do_gw = along_cols == 0;
+  t.bits_gx = bits;
+  cudaMemsetAsync(stats_ws, 0, HLQ_STATS_WS_BYTES, st);
+  hlq::launch_transform(t, hlq::kStats, st);  // statistics do not depend on the rounding
+  hlq::launch_stochastic_quant(src, dtype, segs, rows, cols, ld_src, seg_src, along_cols != 0, bitmap, bits,
+                               along_cols ? stats_ws : stats_ws + 2, dst, ld_dst, scale_out, seed, counter,
+                               index_kind, l2, o2, st);
+  return cuda_status("hlq_quantize_stochastic");
+}
+
 int hlq_conv_dgrad_i8(const int8_t* gcodes, int64_t ld_g, int64_t B, int64_t Ho, int64_t Wo, int64_t O,
                       const int8_t* wcodes, int64_t ld_w, int64_t C, int k, int stride, int pad,
                       int bits, const float* sg, const float* sw, int epilogue, void* dx_nhwc,

@@ -102,6 +102,15 @@ struct GemmDesc {
 };
 bool gemm_i8_pair2_eligible(const GemmDesc* d);
 int launch_gemm_i8_pair2(const GemmDesc* d, cudaStream_t stream);
+// True stochastic QUANT pass (hlq_stochastic.cu): along_cols = HT along the
+// contiguous axis (codes row-major, ld_dst), else the projection along rows
+// (codes K-major per column).  kind: the reference's C-order index of a gw
+// element -- 0: (cols, K) transposed, 1: (K, cols), 2: batch axis with
+// cols = l2 * o2.  stats from a prior STATS pass.
+void launch_stochastic_quant(const void* src, int dtype, int64_t segs, int64_t rows, int64_t cols, int64_t ld_src,
+                             int64_t seg_src, bool along_cols, uint32_t bitmap, int bits, const uint32_t* stats,
+                             int8_t* dst, int64_t ld_dst, float* scale_out, uint64_t k0, uint64_t k1, int kind,
+                             int64_t l2, int64_t o2, cudaStream_t st);
 // Workspace bytes that let launch_gemm_i8 split K (0: no split planned).
 size_t gemm_i8_ws_bytes(int64_t M, int64_t N, int64_t K, int64_t groups);
 

@@ -527,6 +527,10 @@ int choose_nb(int total_blocks, int cols, int rank) {
   int nb = rank >= 8 ? 4 : (rank >= 4 ? 8 : 16);
   const int ncol_tiles = (cols + kCols - 1) / kCols;
   while (nb > 1 && ((total_blocks + nb - 1) / nb) * ncol_tiles < num_sms() * 3) nb >>= 1;
+  if (const char* e = getenv("HLQ_TR_NB")) {  // development sweeps
+    const int v = atoi(e);
+    if (v >= 1 && v <= 16) nb = v;
+  }
   return nb;
 }
 

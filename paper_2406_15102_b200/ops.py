@@ -227,6 +227,36 @@ def quant_weights(weights, bits: int):
     return [(c, scales[i:i + 1]) for i, c in enumerate(codes)]
 
 
+def quant_stochastic(src: torch.Tensor, segs: int, rows: int, cols: int, ld_src: int, seg_src: int,
+                     along_cols: bool, bitmap: int, bits: int, seed: int, counter: int = 0,
+                     index_kind: int = 1, l2: int = 0, o2: int = 0):
+    """True stochastic rounding of the transformed source (hlq_quantize_stochastic).
+    along_cols: HT along cols -> (codes (segs*rows, pad16(cols)), scale, stats);
+    else the projection along rows -> (codes (cols, pad16(K)), scale, stats, K)."""
+    _check_bits(bits)
+    src = _cuda(src, "src")
+    dev = src.device
+    if along_cols:
+        ld = pad16(cols)
+        codes = torch.empty((segs * rows, ld), dtype=torch.int8, device=dev)
+        k = None
+    else:
+        k = proj_rows_k(segs, rows, bin(bitmap).count("1"))
+        ld = max(pad16(k), 16)
+        codes = torch.empty((cols, ld), dtype=torch.int8, device=dev)
+    scale = torch.empty(1, dtype=torch.float32, device=dev)
+    stats = torch.empty(8, dtype=torch.int32, device=dev)
+    _traced("transform", segs * rows * cols * src.element_size() + codes.numel(), 0, 2,
+            lambda: _lib.call("hlq_quantize_stochastic", _p(src), dtype_code(src), segs, rows, cols, ld_src,
+                              seg_src, int(along_cols), bitmap, bits, int(seed), int(counter), index_kind, l2, o2,
+                              _p(stats), _p(codes), ld, _p(scale), _stream()),
+            key=f"transform:stochastic:{segs * rows}x{cols}")
+    amax = stats[0:1] if along_cols else stats[2:3]
+    if along_cols:
+        return codes, scale, amax
+    return codes, scale, amax, k
+
+
 def proj_rows_amax(src: torch.Tensor, segs: int, rows: int, cols: int, bitmap: int,
                    stats: torch.Tensor, ld_src: int | None = None, seg_src: int | None = None):
     """Accumulate the transformed statistics (IEEE bits, atomic max) into stats[2:4]

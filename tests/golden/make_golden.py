@@ -96,6 +96,40 @@ def linear_case(name, seed, B, L, I, O, rank=8, bits_gx=4, bits_gw=8, pad_small=
     return name
 
 
+def stochastic_case(name, seed, B, L, I, O, rng_seed, rank=8, bits_gx=4, bits_gw=8):
+    """True stochastic rounding (quantize.py:114-125) through the reference's
+    own RngState / _quant tags, raw-x branch of hlq_backward."""
+    hlq, bp, qz, _ = _ref()
+    x, w, gy = _inputs(seed, B, L, I, O)
+    plan = hlq.HadamardPlan(block_size=16, basis_indices=hlq.hadamard.lowest_sequency_bases(16, rank))
+    strat = hlq.BackwardStrategy("hlq", hlq.PathSpec("ht_quant", bits_gx),
+                                 hlq.PathSpec("lowrank_quant", bits_gw), plan)
+    rng = qz.RngState(rng_seed)
+    X, Wt, G = hlq.Tensor(x), hlq.Tensor(w), hlq.Tensor(gy)
+    gp = hlq.hlq_backward(X, Wt, G, strategy=strat, rng=rng)
+    acbp = hlq.acbp_compress(X, plan, bits=bits_gw, rng=rng)
+    full = hlq.HadamardPlan(block_size=16, basis_indices=tuple(range(16)))
+    ghat = bp._block_axis(gy, 2, full)
+    what = bp._block_axis(w, 0, full)
+    qg = bp._quant(hlq.Tensor(ghat.reshape(-1, ghat.shape[-1])), bits_gx, rng, bp._TAG_GX_LEFT)
+    qw = bp._quant(hlq.Tensor(what), bits_gx, rng, bp._TAG_GX_RIGHT)
+    gproj = bp._project_axis(gy, acbp.axis, plan).reshape(-1, O)
+    qgw = bp._quant(hlq.Tensor(np.ascontiguousarray(gproj.T)), bits_gw, rng, bp._TAG_GW_LEFT)
+    out = dict(
+        x=x, w=w, gy=gy, rng_seed=np.uint64(rng_seed),
+        rank=np.int64(plan.rank), bases=np.array(plan.basis_indices, dtype=np.int64),
+        bits_gx=np.int64(bits_gx), bits_gw=np.int64(bits_gw), pad_small=np.int64(0),
+        gx_codes_g=qg.payload, gx_scale_g=np.float32(qg.scale),
+        gx_codes_w=qw.payload, gx_scale_w=np.float32(qw.scale),
+        x_codes=acbp.quantized.payload.reshape(-1, I), x_scale=np.float32(acbp.quantized.scale),
+        axis=np.int64(acbp.axis),
+        gw_codes_g=qgw.payload, gw_scale_g=np.float32(qgw.scale),
+        gx=gp.grad_input.data, gw=gp.grad_weight.data,
+    )
+    np.savez_compressed(os.path.join(HERE, f"{name}.npz"), **out)
+    return name
+
+
 def conv_case(name, seed, B, C, H, W, O, k, s, p, rank=8):
     hlq, bp, qz, layers = _ref()
     rng = np.random.default_rng(seed)
@@ -202,6 +236,9 @@ def main():
     made.append(conv_case("conv_k1s2p0", 22, 3, 16, 8, 8, 8, 1, 2, 0))
     made.append(conv_case("conv_k3s1p1_14", 23, 2, 16, 14, 14, 16, 3, 1, 1))
     made += known_answer_cases()
+    # true stochastic rounding (rng=RngState(seed)): tokens axis and batch axis
+    made.append(stochastic_case("stoch_lin3d", 40, 2, 37, 24, 40, rng_seed=0x1234ABCD))
+    made.append(stochastic_case("stoch_lin2d", 41, 48, 1, 32, 24, rng_seed=7))
     with open(os.path.join(HERE, "MANIFEST.json"), "w") as f:
         json.dump({"generated_by": "tests/golden/make_golden.py",
                    "reference": "/root/reference/pkg/src/hlq (read-only, build container)",

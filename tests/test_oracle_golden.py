@@ -90,3 +90,31 @@ def test_fwht_stage_order_matters():
 def test_non_finite_rejected():
     with pytest.raises(ValueError):
         orc.quantize(np.array([1.0, np.inf], dtype=np.float32), 8)
+
+
+STOCH = [c for c in MANIFEST["cases"] if c.startswith("stoch")]
+
+
+@pytest.mark.parametrize("case", STOCH)
+def test_stochastic_case_bit_exact(case):
+    """True stochastic rounding (RngState / Philox draws, quantize.py:114-125)."""
+    g = load(case)
+    st = {}
+    gx, gw = orc.hlq_backward(g["x"], g["w"], g["gy"], bases=tuple(g["bases"]),
+                              bits_gx=int(g["bits_gx"]), bits_gw=int(g["bits_gw"]), stages=st,
+                              rng=int(g["rng_seed"]))
+    for key in ("gx_codes_g", "gx_codes_w", "x_codes", "gw_codes_g"):
+        assert np.array_equal(st[key], g[key]), key
+    for key in ("gx_scale_g", "gx_scale_w", "x_scale", "gw_scale_g"):
+        assert np.float32(st[key]).tobytes() == np.float32(g[key]).tobytes(), key
+    assert np.array_equal(gx, g["gx"]) and np.array_equal(gw, g["gw"])
+
+
+def test_rng_split_matches_reference_values():
+    """splitmix64 splits (quantize.py:48-52): values taken from the reference's
+    RngState in the build container; the package mirror and the oracle agree."""
+    from paper_2406_15102_b200.rng import RngState, site_key
+    assert RngState(5).split(21).seed == 14007819075902455836
+    for seed in (0, 7, 0x1234ABCD, 2 ** 64 - 1):
+        for tag in (11, 12, 21, 22):
+            assert site_key(RngState(seed), tag) == (orc.split_seed(seed, tag), 0)
