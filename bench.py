@@ -426,6 +426,27 @@ def config_table(torch):
     fwd = graph_us(torch, lambda: conv_acbp_compress(xc, k, 1, 1, strat), flush)
     out["b_conv_256x256_3x3_14x14_b128"] = {"hlq_us": round(hc, 1), "dense_bf16_us": round(dc, 1),
                                             "speedup": round(dc / hc, 3), "fwd_acbp_us": round(fwd, 1)}
+    # ACBP container of the ViT-B/16 fc1 input: pack (transpose + CRC32) and
+    # unpack (header parse on the host, range / CRC checks, transpose back), GB/s of container bytes
+    from paper_2406_15102_b200 import acbp as acbp_mod
+    xa = torch.randn(128, 197, 768, device="cuda", dtype=torch.bfloat16)
+    from paper_2406_15102_b200.backprop import acbp_compress
+    from paper_2406_15102_b200.hadamard import HadamardPlan
+    act = acbp_compress(xa, HadamardPlan())
+    buf = acbp_mod.acbp_pack(act)
+    pk = graph_us(torch, lambda: acbp_mod.acbp_pack(act), flush)
+    acbp_mod.acbp_unpack(buf)
+    s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    s.record()
+    for _ in range(5):
+        acbp_mod.acbp_unpack(buf)
+    e.record()
+    e.synchronize()
+    up = s.elapsed_time(e) * 1e3 / 5
+    out["acbp_container_vit_fc1"] = {"bytes": buf.numel(), "pack_us": round(pk, 1),
+                                     "pack_GBps": round(buf.numel() / pk / 1e3, 1), "unpack_us": round(up, 1),
+                                     "unpack_GBps": round(buf.numel() / up / 1e3, 1),
+                                     "fp32_activation_bytes": 128 * 197 * 768 * 4}
     del flush
     return out
 

@@ -50,7 +50,8 @@ typedef enum {
   HLQ_ERR_PARAMETER = 2, /* errors.py:8  ParameterError */
   HLQ_ERR_STATE = 3,     /* errors.py:12 StateError */
   HLQ_ERR_NONFINITE = 4, /* quantize.py:138-139 ValueError */
-  HLQ_ERR_CUDA = 5
+  HLQ_ERR_CUDA = 5,
+  HLQ_ERR_FORMAT = 6 /* malformed ACBP container: FormatError; hlq_last_error_offset() = byte offset */
 } hlq_status;
 
 typedef enum { HLQ_F32 = 0, HLQ_BF16 = 1 } hlq_dtype;
@@ -258,6 +259,44 @@ HLQ_API size_t hlq_quantize_weights_ws(int n);
 HLQ_API int hlq_quantize_weights(int n, const float* const* w, const int64_t* O, const int64_t* I,
                                  int bits, int8_t* const* codes, const int64_t* ld,
                                  float* const* scales, uint32_t* ws, size_t ws_bytes, void* stream);
+
+/* ---------------------------------------------------------------------------
+ * ACBP container (acbp.py:3-212): the reference's bit-exact serialized form of
+ * a compressed activation -- header, per-tensor scale, payload in the
+ * reference's C order (int8, or int4 packed two per byte, low nibble first)
+ * and a zlib CRC32 -- built and verified on the GPU.  Our payload is K-major
+ * (rows = I, or L*I for the batch axis; K codes per row).
+ * ------------------------------------------------------------------------- */
+typedef struct {
+  int64_t B, L, I;            /* original activation shape */
+  int bits, block, rank;
+  uint32_t bitmap;
+  int axis;                   /* the container's axis rule (acbp.py:_container_axis) */
+  int64_t rows, K;            /* our K-major payload geometry */
+  int64_t payload_bytes, total_bytes;
+} hlq_acbp_info;
+
+/* Container size: 33-byte header + scale, payload, 4-byte CRC. */
+HLQ_API int64_t hlq_acbp_container_bytes(int64_t rows, int64_t k, int bits);
+/* Device scratch for hlq_acbp_pack / hlq_acbp_unpack of a container of that size. */
+HLQ_API size_t hlq_acbp_ws(int64_t total_bytes);
+/* acbp_pack (acbp.py:76-96): out (device, exactly hlq_acbp_container_bytes
+ * bytes) receives the container of the K-major payload (rows x k, ld), the
+ * device fp32 scale and the plan / shape fields.  Stream-ordered. */
+HLQ_API int hlq_acbp_pack(const int8_t* payload, int64_t ld, int64_t rows, int64_t k, int bits, int block,
+                          uint32_t bitmap, int64_t B, int64_t L, int64_t I, const float* scale,
+                          uint8_t* out, int64_t out_bytes, void* ws, size_t ws_bytes, void* stream);
+/* acbp_unpack, header half (acbp.py:127-185): validates every header field and
+ * the total length with the reference's rules; fills info.  Synchronous
+ * (copies the 33 header bytes back).  HLQ_ERR_FORMAT + offset on violation. */
+HLQ_API int hlq_acbp_parse(const uint8_t* buf, int64_t nbytes, hlq_acbp_info* info, void* stream);
+/* acbp_unpack, payload half (acbp.py:186-207): range / padding / CRC checks in
+ * the reference's order, then the payload back to K-major (rows x K, ld >= K)
+ * and the scale.  Synchronous.  HLQ_ERR_FORMAT + offset on violation. */
+HLQ_API int hlq_acbp_unpack(const uint8_t* buf, int64_t nbytes, const hlq_acbp_info* info, int8_t* payload,
+                            int64_t ld, float* scale_out, void* ws, size_t ws_bytes, void* stream);
+/* Byte offset of the last HLQ_ERR_FORMAT on this thread. */
+HLQ_API int64_t hlq_last_error_offset(void);
 
 /* Conv2d dX as ONE implicit GEMM (stride 1): dx[b, h, w, c] (channels-last)
  * = deq( sum over taps (i, j) and o of gcodes[b, h + pad - i, w + pad - j, o]

@@ -290,6 +290,35 @@ def hlq_backward(x3: np.ndarray, w: np.ndarray, gy3: np.ndarray, rank: int = 8,
 
 
 # ---------------------------------------------------------------------------
+# ACBP container (acbp.py:3-96); CRC32 = zlib's (stdlib), the same function
+# the reference calls
+# ---------------------------------------------------------------------------
+
+def acbp_container(payload_ref: np.ndarray, bits: int, block: int, bases, B: int, L: int, I: int,
+                   scale) -> bytes:
+    """acbp_pack: header, scale, payload (C order; int4 two per byte, low
+    nibble first, zero high nibble when odd), CRC32 of every prior byte."""
+    import struct
+    import zlib
+    bitmap = 0
+    for b in bases:
+        bitmap |= 1 << int(b)
+    out = bytearray(struct.pack("<4sHBBHHB", b"ACBP", 1, bits, block, len(bases), bitmap, 3))
+    out += struct.pack("<3I", B, L, I) + struct.pack("<I", 1) + struct.pack("<f", float(np.float32(scale)))
+    flat = np.ascontiguousarray(payload_ref).reshape(-1)
+    if bits == 8:
+        out += flat.astype(np.int8).tobytes()
+    else:
+        v = flat.astype(np.int64)
+        if v.size % 2:
+            v = np.concatenate([v, np.zeros(1, dtype=np.int64)])
+        nib = (v & 0xF).reshape(-1, 2)
+        out += (nib[:, 0] | (nib[:, 1] << 4)).astype(np.uint8).tobytes()
+    out += struct.pack("<I", zlib.crc32(bytes(out)) & 0xFFFFFFFF)
+    return bytes(out)
+
+
+# ---------------------------------------------------------------------------
 # conv lowering (harness/layers.py:96-158)
 # ---------------------------------------------------------------------------
 

@@ -10,12 +10,13 @@ import ctypes
 import os
 import threading
 
-from .errors import DimensionError, ParameterError, StateError
+from .errors import DimensionError, FormatError, ParameterError, StateError
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(_HERE, "libhlq_b200.so")
 
-HLQ_OK, HLQ_ERR_DIMENSION, HLQ_ERR_PARAMETER, HLQ_ERR_STATE, HLQ_ERR_NONFINITE, HLQ_ERR_CUDA = range(6)
+(HLQ_OK, HLQ_ERR_DIMENSION, HLQ_ERR_PARAMETER, HLQ_ERR_STATE, HLQ_ERR_NONFINITE, HLQ_ERR_CUDA,
+ HLQ_ERR_FORMAT) = range(7)
 HLQ_F32, HLQ_BF16 = 0, 1
 HLQ_EPI_EXACT, HLQ_EPI_FAST = 0, 1
 
@@ -46,6 +47,12 @@ SIGNATURES = {
     "hlq_gemm_i8_grouped": (_I, [_P, _I64, _I64, _P, _I64, _I64, _I64, _I64, _I64, _I64, _I, _I, _P,
                                  _P, _D, _I, _P, _I, _I64, _P, _I64, _P]),
     "hlq_gemm_i8_ws": (_SZ, [_I64, _I64, _I64, _I64]),
+    "hlq_acbp_container_bytes": (_I64, [_I64, _I64, _I]),
+    "hlq_acbp_ws": (_SZ, [_I64]),
+    "hlq_acbp_pack": (_I, [_P, _I64, _I64, _I64, _I, _I, _U32, _I64, _I64, _I64, _P, _P, _I64, _P, _SZ, _P]),
+    "hlq_acbp_parse": (_I, [_P, _I64, _P, _P]),
+    "hlq_acbp_unpack": (_I, [_P, _I64, _P, _P, _I64, _P, _P, _SZ, _P]),
+    "hlq_last_error_offset": (_I64, []),
     "hlq_gemm_i8_multi": (_I, [_I, _P, _P]),
     "hlq_gemm_i8_ex": (_I, [_P, _I64, _I64, _P, _I64, _I64, _I64, _I64, _I64, _I64, _I, _I, _P, _P,
                             _D, _I, _P, _I, _I64, _P, _I64, _P, _SZ, _P]),
@@ -68,6 +75,13 @@ SIGNATURES = {
     "hlq_grad_weight": (_I, [_P, _I64, _P, _P, _I, _I64, _I64, _I64, _I64, _I, _U32, _I, _D, _P, _I,
                              _I, _P, _SZ, _P]),
 }
+
+class AcbpInfo(ctypes.Structure):
+    """hlq_acbp_info (include/hlq_b200.h)."""
+    _fields_ = [("B", _I64), ("L", _I64), ("I", _I64), ("bits", _I), ("block", _I), ("rank", _I),
+                ("bitmap", _U32), ("axis", _I), ("rows", _I64), ("K", _I64), ("payload_bytes", _I64),
+                ("total_bytes", _I64)]
+
 
 class GemmDesc(ctypes.Structure):
     """hlq_gemm_desc (include/hlq_b200.h)."""
@@ -125,6 +139,8 @@ def check(status: int) -> None:
         raise StateError(msg)
     if status == HLQ_ERR_NONFINITE:
         raise ValueError(msg)
+    if status == HLQ_ERR_FORMAT:
+        raise FormatError(msg, int(load().hlq_last_error_offset()))
     raise HLQLibraryError(f"CUDA error in libhlq_b200: {msg}")
 
 

@@ -34,6 +34,7 @@ int num_sms() {
 namespace {
 
 thread_local char g_err[512] = {0};
+thread_local int64_t g_err_offset = -1;
 
 int fail(int code, const char* fmt, ...) {
   va_list ap;
@@ -381,6 +382,161 @@ int hlq_quantize_stochastic(const void* src, int dtype, int64_t segs, int64_t ro
                                along_cols ? stats_ws : stats_ws + 2, dst, ld_dst, scale_out, seed, counter,
                                index_kind, l2, o2, st);
   return cuda_status("hlq_quantize_stochastic");
+}
+
+int64_t hlq_acbp_container_bytes(int64_t rows, int64_t k, int bits) {
+  const int64_t count = rows * k;
+  return 33 + (bits == 8 ? count : (count + 1) / 2) + 4;
+}
+
+size_t hlq_acbp_ws(int64_t total_bytes) { return hlq::acbp_ws_bytes(total_bytes < 0 ? 0 : total_bytes); }
+
+int64_t hlq_last_error_offset(void) { return g_err_offset; }
+
+static int ffail(int64_t offset, const char* fmt, ...) {
+  char msg[400];
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(msg, sizeof(msg), fmt, ap);
+  va_end(ap);
+  g_err_offset = offset;
+  snprintf(g_err, sizeof(g_err), "%s", msg);
+  return HLQ_ERR_FORMAT;
+}
+
+// acbp.py:_container_axis + projected_shape, in our K-major terms
+static void container_geometry(int64_t B, int64_t L, int64_t I, int block, int rank, int* axis, int64_t* rows,
+                               int64_t* k) {
+  int ax;
+  if (L >= block || B >= block) ax = L >= block ? 1 : 0;
+  else ax = L >= B ? 1 : 0;
+  *axis = ax;
+  if (ax == 1) {
+    *rows = I;
+    *k = B * ((L + block - 1) / block) * rank;
+  } else {
+    *rows = L * I;
+    *k = ((B + block - 1) / block) * rank;
+  }
+}
+
+int hlq_acbp_pack(const int8_t* payload, int64_t ld, int64_t rows, int64_t k, int bits, int block,
+                  uint32_t bitmap, int64_t B, int64_t L, int64_t I, const float* scale, uint8_t* out,
+                  int64_t out_bytes, void* ws, size_t ws_bytes, void* stream) {
+  HLQ_TRY(check_bits(bits));
+  const int rank = __builtin_popcount(bitmap);
+  if (block != 2 && block != 4 && block != 8 && block != 16)
+    return fail(HLQ_ERR_PARAMETER, "container format supports block sizes 2..16, got %d", block);
+  if (bitmap == 0 || (bitmap >> block)) return fail(HLQ_ERR_PARAMETER, "bad basis bitmap 0x%x", bitmap);
+  if (B < 0 || L < 0 || I < 0 || B > UINT32_MAX || L > UINT32_MAX || I > UINT32_MAX)
+    return fail(HLQ_ERR_DIMENSION, "shape does not fit the container's u32 dims");
+  int axis;
+  int64_t rr, kk;
+  container_geometry(B, L, I, block, rank, &axis, &rr, &kk);
+  if (rr != rows || kk != k)
+    return fail(HLQ_ERR_PARAMETER, "payload geometry (%lld x %lld) is inconsistent with the container axis rule "
+                "(%lld x %lld)", (long long)rows, (long long)k, (long long)rr, (long long)kk);
+  if (rows * k > 0 && ld < k) return fail(HLQ_ERR_DIMENSION, "payload ld < K");
+  const int64_t total = hlq_acbp_container_bytes(rows, k, bits);
+  if (out_bytes != total) return fail(HLQ_ERR_DIMENSION, "container buffer must be %lld bytes", (long long)total);
+  if (ws_bytes < hlq_acbp_ws(total)) return fail(HLQ_ERR_PARAMETER, "workspace too small");
+  uint8_t h[29];
+  memcpy(h, "ACBP", 4);
+  const uint16_t ver = 1, rk = uint16_t(rank), bm = uint16_t(bitmap);
+  memcpy(h + 4, &ver, 2);
+  h[6] = uint8_t(bits);
+  h[7] = uint8_t(block);
+  memcpy(h + 8, &rk, 2);
+  memcpy(h + 10, &bm, 2);
+  h[12] = 3;
+  const uint32_t dims[3] = {uint32_t(B), uint32_t(L), uint32_t(I)}, ns = 1;
+  memcpy(h + 13, dims, 12);
+  memcpy(h + 25, &ns, 4);
+  const int e = hlq::acbp_pack(payload, ld, rows, k, bits, h, scale, out, total, ws, static_cast<cudaStream_t>(stream));
+  if (e) return fail(HLQ_ERR_CUDA, "hlq_acbp_pack: %s", cudaGetErrorString(cudaError_t(e)));
+  return HLQ_OK;
+}
+
+int hlq_acbp_parse(const uint8_t* buf, int64_t nbytes, hlq_acbp_info* info, void* stream) {
+  uint8_t h[33] = {0};
+  const int64_t n = nbytes < 33 ? nbytes : 33;
+  if (n > 0) {
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    cudaMemcpyAsync(h, buf, size_t(n), cudaMemcpyDeviceToHost, st);
+    if (cudaStreamSynchronize(st) != cudaSuccess) return cuda_status("hlq_acbp_parse");
+  }
+  // acbp.py:_Reader: a field that does not fit reports the position it starts at
+  auto need = [&](int64_t pos, int64_t len, const char* what) -> int {
+    if (pos + len > nbytes) return ffail(pos, "truncated container: missing %s", what);
+    return HLQ_OK;
+  };
+  HLQ_TRY(need(0, 4, "magic"));
+  if (memcmp(h, "ACBP", 4) != 0) return ffail(0, "bad magic");
+  HLQ_TRY(need(4, 2, "version"));
+  const uint16_t version = uint16_t(h[4] | (h[5] << 8));
+  if (version != 1) return ffail(4, "unsupported version %u", version);
+  HLQ_TRY(need(6, 1, "bits"));
+  const int bits = h[6];
+  if (bits != 4 && bits != 8) return ffail(6, "unsupported bit width %d", bits);
+  HLQ_TRY(need(7, 1, "block size"));
+  const int block = h[7];
+  if (block != 2 && block != 4 && block != 8 && block != 16) return ffail(7, "unsupported block size %d", block);
+  HLQ_TRY(need(8, 2, "rank"));
+  const int rank = h[8] | (h[9] << 8);
+  if (rank < 1 || rank > block) return ffail(8, "rank %d out of range for block size %d", rank, block);
+  HLQ_TRY(need(10, 2, "basis bitmap"));
+  const uint32_t bitmap = uint32_t(h[10] | (h[11] << 8));
+  if (bitmap >> block) return ffail(10, "basis bitmap 0x%04x has bits beyond the block", bitmap);
+  if (__builtin_popcount(bitmap) != rank) return ffail(10, "basis bitmap 0x%04x does not select %d bases", bitmap, rank);
+  HLQ_TRY(need(12, 1, "ndims"));
+  if (h[12] != 3) return ffail(12, "unsupported ndims %d", int(h[12]));
+  HLQ_TRY(need(13, 12, "dims"));
+  uint32_t dims[3];
+  memcpy(dims, h + 13, 12);
+  HLQ_TRY(need(25, 4, "scale count"));
+  uint32_t ns;
+  memcpy(&ns, h + 25, 4);
+  if (ns != 1) return ffail(25, "unsupported scale count %u", ns);
+  HLQ_TRY(need(29, 4, "scale"));
+  float scale;
+  memcpy(&scale, h + 29, 4);
+  if (!(scale > 0.0f) || scale == __builtin_inff()) return ffail(29, "scale must be positive and finite, got %g", double(scale));
+  hlq_acbp_info inf{};
+  inf.B = dims[0]; inf.L = dims[1]; inf.I = dims[2];
+  inf.bits = bits; inf.block = block; inf.rank = rank; inf.bitmap = bitmap;
+  container_geometry(inf.B, inf.L, inf.I, block, rank, &inf.axis, &inf.rows, &inf.K);
+  const int64_t count = inf.rows * inf.K;
+  inf.payload_bytes = bits == 8 ? count : (count + 1) / 2;
+  inf.total_bytes = 33 + inf.payload_bytes + 4;
+  if (nbytes != inf.total_bytes)
+    return ffail(33, "container length %lld does not match the declared shape (expected %lld)", (long long)nbytes,
+                 (long long)inf.total_bytes);
+  *info = inf;
+  return HLQ_OK;
+}
+
+int hlq_acbp_unpack(const uint8_t* buf, int64_t nbytes, const hlq_acbp_info* info, int8_t* payload, int64_t ld,
+                    float* scale_out, void* ws, size_t ws_bytes, void* stream) {
+  if (!info || nbytes != info->total_bytes) return fail(HLQ_ERR_PARAMETER, "info does not describe this buffer");
+  if (ws_bytes < hlq_acbp_ws(nbytes)) return fail(HLQ_ERR_PARAMETER, "workspace too small");
+  if (info->rows * info->K > 0 && (!payload || ld < info->K)) return fail(HLQ_ERR_DIMENSION, "payload ld < K");
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  int64_t bad = -1;
+  bool crc_ok = false;
+  const int e = hlq::acbp_check_and_unpack(buf, nbytes, info->rows, info->K, info->bits, payload, ld, scale_out, ws,
+                                           &bad, &crc_ok, st);
+  if (e) return fail(HLQ_ERR_CUDA, "hlq_acbp_unpack: %s", cudaGetErrorString(cudaError_t(e)));
+  if (bad >= 0)
+    return ffail(33 + bad, info->bits == 8 ? "payload value out of the symmetric int8 range"
+                                            : "payload value out of the symmetric int4 range");
+  const int64_t count = info->rows * info->K;
+  if (info->bits == 4 && (count % 2) && info->payload_bytes) {
+    uint8_t last = 0;
+    cudaMemcpy(&last, buf + 33 + info->payload_bytes - 1, 1, cudaMemcpyDeviceToHost);
+    if (last >> 4) return ffail(33 + info->payload_bytes - 1, "nonzero padding nibble");
+  }
+  if (!crc_ok) return ffail(33 + info->payload_bytes, "crc mismatch");
+  return HLQ_OK;
 }
 
 int hlq_conv_dgrad_i8(const int8_t* gcodes, int64_t ld_g, int64_t B, int64_t Ho, int64_t Wo, int64_t O,

@@ -111,6 +111,13 @@ void launch_stochastic_quant(const void* src, int dtype, int64_t segs, int64_t r
                              int64_t seg_src, bool along_cols, uint32_t bitmap, int bits, const uint32_t* stats,
                              int8_t* dst, int64_t ld_dst, float* scale_out, uint64_t k0, uint64_t k1, int kind,
                              int64_t l2, int64_t o2, cudaStream_t st);
+// ACBP container (hlq_acbp.cu)
+size_t acbp_ws_bytes(int64_t nbytes);
+int acbp_pack(const int8_t* codes, int64_t ld, int64_t R, int64_t K, int bits, const uint8_t* head29,
+              const float* scale, uint8_t* out, int64_t total, void* ws, cudaStream_t st);
+int acbp_check_and_unpack(const uint8_t* buf, int64_t total, int64_t R, int64_t K, int bits, int8_t* codes,
+                          int64_t ld, float* scale_out, void* ws, int64_t* bad_offset, bool* crc_ok,
+                          cudaStream_t st);
 // Workspace bytes that let launch_gemm_i8 split K (0: no split planned).
 size_t gemm_i8_ws_bytes(int64_t M, int64_t N, int64_t K, int64_t groups);
 

@@ -130,6 +130,24 @@ def stochastic_case(name, seed, B, L, I, O, rng_seed, rank=8, bits_gx=4, bits_gw
     return name
 
 
+def container_case(name, seed, B, L, I, bits=8, bases=(0, 2, 4, 6, 8, 10, 12, 14), pad_small=False):
+    """ACBP container bytes (acbp.py:76-96) of a reference-compressed activation."""
+    hlq, bp, qz, _ = _ref()
+    from hlq import acbp as acbp_mod
+    rng = np.random.default_rng(seed)
+    x = rng.standard_normal((B, L, I)).astype(np.float32)
+    plan = hlq.HadamardPlan(block_size=16, basis_indices=tuple(bases))
+    a = hlq.acbp_compress(hlq.Tensor(x), plan, bits=bits, pad_small_axes=pad_small)
+    buf = acbp_mod.acbp_pack(a)
+    back = acbp_mod.acbp_unpack(buf)
+    assert np.array_equal(back.quantized.payload, a.quantized.payload)
+    np.savez_compressed(os.path.join(HERE, f"{name}.npz"), x=x, bases=np.array(bases, dtype=np.int64),
+                        bits=np.int64(bits), pad_small=np.int64(pad_small), axis=np.int64(a.axis),
+                        payload=a.quantized.payload, scale=np.float32(a.quantized.scale),
+                        container=np.frombuffer(buf, dtype=np.uint8).copy())
+    return name
+
+
 def conv_case(name, seed, B, C, H, W, O, k, s, p, rank=8):
     hlq, bp, qz, layers = _ref()
     rng = np.random.default_rng(seed)
@@ -239,6 +257,15 @@ def main():
     # true stochastic rounding (rng=RngState(seed)): tokens axis and batch axis
     made.append(stochastic_case("stoch_lin3d", 40, 2, 37, 24, 40, rng_seed=0x1234ABCD))
     made.append(stochastic_case("stoch_lin2d", 41, 48, 1, 32, 24, rng_seed=7))
+    # ACBP containers (acbp.py): int8 / int4 (odd count -> padding nibble), batch axis,
+    # padded L, pad-small axes, empty batch
+    made.append(container_case("acbp_c8", 50, 4, 32, 12))
+    made.append(container_case("acbp_c4_odd", 51, 1, 16, 5, bits=4, bases=(0, 1, 2)))
+    made.append(container_case("acbp_c4", 52, 3, 40, 7, bits=4))
+    made.append(container_case("acbp_batchaxis", 53, 32, 4, 8))
+    made.append(container_case("acbp_padL", 54, 4, 20, 12))
+    made.append(container_case("acbp_padsmall", 55, 4, 8, 6, pad_small=True))
+    made.append(container_case("acbp_empty", 56, 0, 32, 8))
     with open(os.path.join(HERE, "MANIFEST.json"), "w") as f:
         json.dump({"generated_by": "tests/golden/make_golden.py",
                    "reference": "/root/reference/pkg/src/hlq (read-only, build container)",

@@ -118,3 +118,24 @@ def test_rng_split_matches_reference_values():
     for seed in (0, 7, 0x1234ABCD, 2 ** 64 - 1):
         for tag in (11, 12, 21, 22):
             assert site_key(RngState(seed), tag) == (orc.split_seed(seed, tag), 0)
+
+
+CONTAINERS = [c for c in MANIFEST["cases"] if c.startswith("acbp_")]
+
+
+@pytest.mark.parametrize("case", CONTAINERS)
+def test_container_bytes_match_reference(case):
+    """oracle.acbp_container == the reference's acbp_pack bytes."""
+    g = load(case)
+    x = g["x"]
+    B, L, I = x.shape
+    bits = int(g["bits"])
+    bases = tuple(int(b) for b in g["bases"])
+    if B == 0:
+        payload, scale = g["payload"], g["scale"]
+    else:
+        payload, scale, axis = orc.acbp_compress(x, bases, bits, pad_small_axes=bool(g["pad_small"]))
+        assert axis == int(g["axis"])
+        assert np.array_equal(payload.reshape(-1), g["payload"].reshape(-1))
+    buf = orc.acbp_container(payload, bits, 16, bases, B, L, I, scale)
+    assert buf == g["container"].tobytes()
