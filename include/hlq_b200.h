@@ -246,6 +246,14 @@ HLQ_API int hlq_quantize_stochastic(const void* src, int dtype, int64_t segs, in
                                     int64_t o2, uint32_t* stats_ws, int8_t* dst, int64_t ld_dst,
                                     float* scale_out, void* stream);
 
+/* Calibration energy (train.py:128-134 _basis_energy): energy16[i] = sum over
+ * every 16-row block (zero-padded) and column of the source view of |c_i|, c
+ * the orthonormal 16-point transform along rows -- the column sums of the
+ * reference's per-block |coefficient| matrix, in fp64.  select_bases
+ * (hadamard.py:174-188) keeps the `rank` largest means. */
+HLQ_API int hlq_basis_energy(const void* src, int dtype, int64_t segs, int64_t rows, int64_t cols,
+                             int64_t ld_src, int64_t seg_src, double* energy16, void* stream);
+
 /* The dX right operand of many layers at once: codes_i = Q_bits(HT_O(W_i))
  * for n <= 128 fp32 weights W_i (O_i x I_i, row-major), written K-major as
  * (I_i rows of ld_i >= pad16(O_i) bytes), scale_i one fp32 each -- identical

@@ -290,6 +290,24 @@ def hlq_backward(x3: np.ndarray, w: np.ndarray, gy3: np.ndarray, rank: int = 8,
 
 
 # ---------------------------------------------------------------------------
+# calibrated basis selection (harness/train.py:128-134, hadamard.py:174-188)
+# ---------------------------------------------------------------------------
+
+def basis_energy(gy3: np.ndarray, axis: int, n: int = 16) -> np.ndarray:
+    """_basis_energy: per-block |coefficient| matrix (num_blocks_total, n)."""
+    moved = np.moveaxis(pad_to(gy3, axis, n), axis, -1)
+    blocks = moved.shape[-1] // n
+    coeffs = fwht_blocks(np.ascontiguousarray(moved).reshape(*moved.shape[:-1], blocks, n))
+    return np.abs(coeffs).reshape(-1, n)
+
+
+def select_bases(energy: np.ndarray, rank: int) -> tuple:
+    means = np.abs(energy).mean(axis=0)
+    order = np.argsort(-means, kind="stable")
+    return tuple(sorted(int(i) for i in order[:rank]))
+
+
+# ---------------------------------------------------------------------------
 # ACBP container (acbp.py:3-96); CRC32 = zlib's (stdlib), the same function
 # the reference calls
 # ---------------------------------------------------------------------------

@@ -57,6 +57,7 @@ SIGNATURES = {
     "hlq_gemm_i8_ex": (_I, [_P, _I64, _I64, _P, _I64, _I64, _I64, _I64, _I64, _I64, _I, _I, _P, _P,
                             _D, _I, _P, _I, _I64, _P, _I64, _P, _SZ, _P]),
     "hlq_quantize_weights_ws": (_SZ, [_I]),
+    "hlq_basis_energy": (_I, [_P, _I, _I64, _I64, _I64, _I64, _I64, _P, _P]),
     "hlq_quantize_stochastic": (_I, [_P, _I, _I64, _I64, _I64, _I64, _I64, _I, _U32, _I, ctypes.c_uint64,
                                      ctypes.c_uint64, _I, _I64, _I64, _P, _P, _I64, _P, _P]),
     "hlq_quantize_weights": (_I, [_I, _P, _P, _P, _I, _P, _P, _P, _P, _SZ, _P]),

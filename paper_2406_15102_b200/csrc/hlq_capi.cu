@@ -384,6 +384,14 @@ int hlq_quantize_stochastic(const void* src, int dtype, int64_t segs, int64_t ro
   return cuda_status("hlq_quantize_stochastic");
 }
 
+int hlq_basis_energy(const void* src, int dtype, int64_t segs, int64_t rows, int64_t cols, int64_t ld_src,
+                     int64_t seg_src, double* energy16, void* stream) {
+  HLQ_TRY(proj_rows_checked(src, dtype, segs, rows, cols, ld_src, seg_src, 0xFFFFu, 8, nullptr, 0));
+  if (!energy16) return fail(HLQ_ERR_PARAMETER, "null energy output");
+  hlq::launch_basis_energy(src, dtype, segs, rows, cols, ld_src, seg_src, energy16, static_cast<cudaStream_t>(stream));
+  return cuda_status("hlq_basis_energy");
+}
+
 int64_t hlq_acbp_container_bytes(int64_t rows, int64_t k, int bits) {
   const int64_t count = rows * k;
   return 33 + (bits == 8 ? count : (count + 1) / 2) + 4;

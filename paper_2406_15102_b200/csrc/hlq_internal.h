@@ -111,6 +111,9 @@ void launch_stochastic_quant(const void* src, int dtype, int64_t segs, int64_t r
                              int64_t seg_src, bool along_cols, uint32_t bitmap, int bits, const uint32_t* stats,
                              int8_t* dst, int64_t ld_dst, float* scale_out, uint64_t k0, uint64_t k1, int kind,
                              int64_t l2, int64_t o2, cudaStream_t st);
+// Per-basis sum of |coefficient| of the block transform along rows (calibration).
+void launch_basis_energy(const void* src, int dtype, int64_t segs, int64_t rows, int64_t cols, int64_t ld_src,
+                         int64_t seg_src, double* energy, cudaStream_t st);
 // ACBP container (hlq_acbp.cu)
 size_t acbp_ws_bytes(int64_t nbytes);
 int acbp_pack(const int8_t* codes, int64_t ld, int64_t R, int64_t K, int bits, const uint8_t* head29,

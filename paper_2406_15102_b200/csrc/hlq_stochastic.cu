@@ -183,3 +183,64 @@ void launch_stochastic_quant(const void* src, int dtype, int64_t segs, int64_t r
 }
 
 }  // namespace hlq
+
+// ---------------------------------------------------------------------------
+// Basis energy for calibrated basis selection (train.py:128-134 _basis_energy,
+// hadamard.py:174-188 select_bases): sum over every 16-row block and column of
+// |coefficient i| of the orthonormal block transform along rows, i = 0..15,
+// accumulated in fp64 (the ordering of the per-basis means is what selection
+// uses).  energy (16 doubles) is zeroed by the caller's stream first.
+// ---------------------------------------------------------------------------
+namespace hlq {
+namespace {
+
+template <typename T>
+__global__ void __launch_bounds__(256) basis_energy_kernel(const void* src, int64_t segs, int64_t rows, int64_t cols,
+                                                           int64_t ld_src, int64_t seg_src, double* energy) {
+  const int64_t nblk = (rows + 15) / 16, units = cols * segs * nblk;
+  double acc[16];
+#pragma unroll
+  for (int i = 0; i < 16; ++i) acc[i] = 0.0;
+  for (int64_t u = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; u < units; u += int64_t(gridDim.x) * blockDim.x) {
+    const int64_t gb = u / cols, c = u - gb * cols;
+    const int64_t sg = gb / nblk, blk = gb - sg * nblk;
+    float v[16];
+#pragma unroll
+    for (int i = 0; i < 16; ++i) {
+      const int64_t r = blk * 16 + i;
+      float x = 0.0f;
+      if (r < rows) {
+        const T* p = static_cast<const T*>(src) + sg * seg_src + r * ld_src + c;
+        x = sizeof(T) == 2 ? __bfloat162float(*reinterpret_cast<const __nv_bfloat16*>(p))
+                           : *reinterpret_cast<const float*>(p);
+      }
+      v[i] = x;
+    }
+    dev::fwht16_raw(v);
+#pragma unroll
+    for (int i = 0; i < 16; ++i) acc[i] += double(fabsf(__fmul_rn(v[i], 0.25f)));
+  }
+#pragma unroll
+  for (int i = 0; i < 16; ++i) {
+    double a = acc[i];
+    for (int o = 16; o > 0; o >>= 1) a += __shfl_xor_sync(0xffffffffu, a, o);
+    if ((threadIdx.x & 31) == 0) atomicAdd(energy + i, a);
+  }
+}
+
+}  // namespace
+
+void launch_basis_energy(const void* src, int dtype, int64_t segs, int64_t rows, int64_t cols, int64_t ld_src,
+                         int64_t seg_src, double* energy, cudaStream_t st) {
+  cudaMemsetAsync(energy, 0, 16 * sizeof(double), st);
+  const int64_t units = cols * segs * ((rows + 15) / 16);
+  int64_t grid = (units + 255) / 256;
+  if (grid > num_sms() * 8) grid = num_sms() * 8;
+  if (grid < 1) grid = 1;
+  if (dtype == kBF16)
+    basis_energy_kernel<__nv_bfloat16><<<int(grid), 256, 0, st>>>(src, segs, rows, cols, ld_src, seg_src, energy);
+  else
+    basis_energy_kernel<float><<<int(grid), 256, 0, st>>>(src, segs, rows, cols, ld_src, seg_src, energy);
+}
+
+}  // namespace hlq

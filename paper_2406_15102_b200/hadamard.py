@@ -96,3 +96,15 @@ class HadamardPlan:
             raise ParameterError(
                 f"the B200 kernels implement block_size {GPU_BLOCK} only, got {self.block_size}")
         return self.basis_bitmap()
+
+
+def select_bases(means, rank: int) -> tuple:
+    """hadamard.py:174-188: the `rank` bases with the largest mean |coefficient|
+    (ties toward the lower index), returned ascending.  `means`: 16 values."""
+    import numpy as np
+    m = np.asarray(means, dtype=np.float64).reshape(-1)
+    n = m.size
+    if not 1 <= rank <= n:
+        raise ParameterError(f"rank must be in [1, {n}], got {rank}")
+    order = np.argsort(-m, kind="stable")
+    return tuple(sorted(int(i) for i in order[:rank]))

@@ -68,7 +68,7 @@ class HLQLinearFunction(torch.autograd.Function):
     weight)."""
 
     @staticmethod
-    def forward(ctx, x, weight, bias, strategy: BackwardStrategy, wcodes=None):
+    def forward(ctx, x, weight, bias, strategy: BackwardStrategy, wcodes=None, calib_layer=None):
         B, L, I = _blv(x.shape)
         O = weight.shape[0]
         plan = strategy.plan
@@ -99,6 +99,7 @@ class HLQLinearFunction(torch.autograd.Function):
         x.record_stream(side)
         ctx.save_for_backward(weight, payload, sx, cw, sw)
         ctx.meta = (B, L, I, axis, k, x.dtype, tuple(x.shape), bias is not None, strategy)
+        ctx.calib_layer = calib_layer
         return y
 
     @staticmethod
@@ -110,6 +111,8 @@ class HLQLinearFunction(torch.autograd.Function):
         if gy3.dtype not in (torch.float32, torch.bfloat16):
             gy3 = gy3.float()
         gy3 = gy3.contiguous()
+        if ctx.calib_layer is not None:  # calibrate_bases: the layer's gradient-energy hook (layers.py:61-62)
+            _calib_record(ctx.calib_layer, gy3, axis)
         gx = gw = gb = None
         bits_gx = strategy.grad_input_path.bits or 4
         bits_gw = strategy.grad_weight_path.bits or 8
@@ -146,7 +149,7 @@ class HLQLinearFunction(torch.autograd.Function):
             gx = gx.reshape(x_shape).to(x_dtype)
             if has_bias and ctx.needs_input_grad[2]:
                 gb = gy.reshape(-1, O).sum(0, dtype=torch.float32)
-            return gx, gw, gb, None, None
+            return gx, gw, gb, None, None, None
         if ctx.needs_input_grad[1]:
             bits = strategy.grad_weight_path.bits or 8
             segs, rows, cols, ld_src, seg_src = _proj_view(B, L, O, axis)
@@ -170,7 +173,7 @@ class HLQLinearFunction(torch.autograd.Function):
                 gx = gx.to(x_dtype)
         if has_bias and ctx.needs_input_grad[2]:
             gb = gy.reshape(-1, O).sum(0, dtype=torch.float32)
-        return gx, gw, gb, None, None
+        return gx, gw, gb, None, None, None
 
 
 class HLQLinear(nn.Linear):
@@ -200,7 +203,8 @@ class HLQLinear(nn.Linear):
         if torch.is_autocast_enabled("cuda"):
             x = x.to(torch.get_autocast_dtype("cuda"))
         with torch.autocast("cuda", enabled=False):
-            return HLQLinearFunction.apply(x, self.weight, self.bias, self.strategy, self.cached_weight_codes())
+            return HLQLinearFunction.apply(x, self.weight, self.bias, self.strategy, self.cached_weight_codes(),
+                                           self if _CALIB[0] is not None else None)
 
     @classmethod
     def from_linear(cls, lin: nn.Linear, strategy: BackwardStrategy | None = None) -> "HLQLinear":
@@ -211,6 +215,46 @@ class HLQLinear(nn.Linear):
             if lin.bias is not None:
                 m.bias.copy_(lin.bias)
         return m
+
+
+_CALIB = [None]  # {HLQLinear: [energy sums (16,) fp64, count]} while calibrate_bases runs
+
+
+def calibrate_bases(model: nn.Module, backward_pass) -> dict:
+    """One-batch L1 basis selection (harness/train.py:137-167): run
+    ``backward_pass()`` (a forward + backward of one calibration batch) while
+    every HLQLinear records the per-basis |coefficient| energy of its upstream
+    gradient along its projection axis (GPU, hlq_basis_energy), then give each
+    layer the `rank` bases carrying the most energy (select_bases).  Returns
+    {layer: basis tuple}; full-rank plans are left alone."""
+    from .hadamard import select_bases
+    layers = [m for m in model.modules() if isinstance(m, HLQLinear)]
+    _CALIB[0] = {m: None for m in layers}
+    try:
+        backward_pass()
+    finally:
+        sinks, _CALIB[0] = _CALIB[0], None
+    out = {}
+    for m in layers:
+        plan = m.strategy.plan
+        if plan.full_rank or sinks.get(m) is None:
+            continue
+        sums, count = sinks[m]
+        idx = select_bases((sums / max(count, 1)).cpu().numpy(), plan.rank)
+        m.strategy = m.strategy.with_plan(plan.with_bases(idx))
+        out[m] = idx
+    return out
+
+
+def _calib_record(layer, gy3, axis: int):
+    sinks = _CALIB[0]
+    if sinks is None or layer not in sinks:
+        return
+    B, L, O = gy3.shape
+    segs, rows, cols, ld_src, seg_src = _proj_view(B, L, O, axis)
+    e, n = ops.basis_energy(gy3, segs, rows, cols, ld_src, seg_src)
+    prev = sinks[layer]
+    sinks[layer] = (e, n) if prev is None else (prev[0] + e, prev[1] + n)
 
 
 def refresh_weight_codes(module: nn.Module) -> int:

@@ -257,6 +257,20 @@ def quant_stochastic(src: torch.Tensor, segs: int, rows: int, cols: int, ld_src:
     return codes, scale, amax, k
 
 
+def basis_energy(src: torch.Tensor, segs: int, rows: int, cols: int, ld_src: int | None = None,
+                 seg_src: int | None = None):
+    """Per-basis sums of |coefficient| of the block transform along rows
+    (hlq_basis_energy) -> (sums (16,) float64 tensor, number of blocks x columns)."""
+    src = _cuda(src, "src")
+    ld_src = cols if ld_src is None else ld_src
+    seg_src = rows * ld_src if seg_src is None else seg_src
+    energy = torch.empty(16, dtype=torch.float64, device=src.device)
+    _traced("transform", segs * rows * cols * src.element_size(), 0, 1,
+            lambda: _lib.call("hlq_basis_energy", _p(src), dtype_code(src), segs, rows, cols, ld_src, seg_src,
+                              _p(energy), _stream()))
+    return energy, segs * ((rows + 15) // 16) * cols
+
+
 def proj_rows_amax(src: torch.Tensor, segs: int, rows: int, cols: int, bitmap: int,
                    stats: torch.Tensor, ld_src: int | None = None, seg_src: int | None = None):
     """Accumulate the transformed statistics (IEEE bits, atomic max) into stats[2:4]

@@ -148,6 +148,24 @@ def container_case(name, seed, B, L, I, bits=8, bases=(0, 2, 4, 6, 8, 10, 12, 14
     return name
 
 
+def calib_case(name, seed, B, L, O, rank=8):
+    """Calibrated basis selection (train.py:128-134 _basis_energy, hadamard.py:174-188)."""
+    hlq, bp, qz, _ = _ref()
+    import importlib
+    tr = importlib.import_module("hlq.harness.train")
+    rng = np.random.default_rng(seed)
+    gy = (rng.lognormal(0.0, 1.4, size=(B, L, O)) * rng.choice([-1.0, 1.0], size=(B, L, O)) * 1e-3)
+    gy = gy.astype(np.float32)
+    # give the bases distinct energies: add a smooth (low-sequency) component along L
+    gy += (np.sin(np.arange(L) / 3.0)[None, :, None] * 2e-3).astype(np.float32)
+    axis = bp.ht_axis_for(B, L, 16)
+    energy = tr._basis_energy(gy, axis, 16)
+    bases = hlq.hadamard.select_bases(hlq.Tensor(energy), rank)
+    np.savez_compressed(os.path.join(HERE, f"{name}.npz"), gy=gy, axis=np.int64(axis), rank=np.int64(rank),
+                        means=np.abs(energy).mean(axis=0), bases=np.array(bases, dtype=np.int64))
+    return name
+
+
 def conv_case(name, seed, B, C, H, W, O, k, s, p, rank=8):
     hlq, bp, qz, layers = _ref()
     rng = np.random.default_rng(seed)
@@ -266,6 +284,9 @@ def main():
     made.append(container_case("acbp_padL", 54, 4, 20, 12))
     made.append(container_case("acbp_padsmall", 55, 4, 8, 6, pad_small=True))
     made.append(container_case("acbp_empty", 56, 0, 32, 8))
+    # calibrated basis selection
+    made.append(calib_case("calib_tokens", 60, 4, 48, 40))
+    made.append(calib_case("calib_batch", 61, 64, 1, 24, rank=4))
     with open(os.path.join(HERE, "MANIFEST.json"), "w") as f:
         json.dump({"generated_by": "tests/golden/make_golden.py",
                    "reference": "/root/reference/pkg/src/hlq (read-only, build container)",

@@ -139,3 +139,14 @@ def test_container_bytes_match_reference(case):
         assert np.array_equal(payload.reshape(-1), g["payload"].reshape(-1))
     buf = orc.acbp_container(payload, bits, 16, bases, B, L, I, scale)
     assert buf == g["container"].tobytes()
+
+
+CALIB = [c for c in MANIFEST["cases"] if c.startswith("calib_")]
+
+
+@pytest.mark.parametrize("case", CALIB)
+def test_calibration_matches_reference(case):
+    g = load(case)
+    e = orc.basis_energy(g["gy"], int(g["axis"]))
+    assert np.array_equal(np.abs(e).mean(axis=0), g["means"])
+    assert orc.select_bases(e, int(g["rank"])) == tuple(int(b) for b in g["bases"])
