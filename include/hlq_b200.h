@@ -254,6 +254,48 @@ HLQ_API int hlq_quantize_stochastic(const void* src, int dtype, int64_t segs, in
 HLQ_API int hlq_basis_energy(const void* src, int dtype, int64_t segs, int64_t rows, int64_t cols,
                              int64_t ld_src, int64_t seg_src, double* energy16, void* stream);
 
+/* ---- baseline strategies (backprop.py:91-155, 212-303) ----
+ * A strided view of a float32 / bfloat16 source: unit (segment s, 16-block b
+ * along rows, column c), element (s, r, c) at src + s*src_stride[0] +
+ * r*src_stride[1] + c*src_stride[2].  bitmap selects the kept bases of the
+ * orthonormal 16-point block transform along rows (0xFFFF: `_block_axis`,
+ * backprop.py:212-220; a subset: `_project_axis`, :223-234); bitmap 0 is the
+ * identity (no transform; r indexes the output).  Output element (s, k, c),
+ * k = b*rank + j for the j-th kept basis (identity: k = r), is written at
+ * dst + s*dst_stride[0] + k*dst_stride[1] + c*dst_stride[2]; idx_stride maps
+ * it to its C-order index in the array the reference quantizes (the Philox
+ * draw index of true stochastic rounding).  Rows past `rows` are zero padding
+ * (transform) or absent (identity). */
+typedef struct hlq_xform {
+  const void* src;
+  int32_t src_dtype;
+  int64_t segs, rows, cols;
+  int64_t src_stride[3];
+  uint32_t bitmap;
+  int64_t dst_stride[3];
+  int64_t idx_stride[3];
+} hlq_xform;
+
+/* Q_bits of the view's outputs with ONE per-tensor scale (quantize.py:94-100):
+ * rounding 0 = quant_pseudo_stochastic (quantize.py:128-145), 1 =
+ * quant_stochastic with RngState(seed, counter) draws (quantize.py:114-125).
+ * int8 codes at dst (positions the view does not write are left untouched:
+ * zero them first when they are GEMM padding), scale_out one fp32, stats_ws
+ * HLQ_STATS_WS_BYTES device bytes (word 0 = amax bits; >= 0x7F800000 flags a
+ * non-finite input).  Two launches (statistics, quantization). */
+HLQ_API int hlq_xform_quantize(const hlq_xform* view, int bits, int rounding, uint64_t seed, uint64_t counter,
+                               uint32_t* stats_ws, int8_t* dst, float* scale_out, void* stream);
+
+/* The view's outputs in float32 (the bits=None float pipelines and the
+ * LBP-WHT low-rank projection, backprop.py:223-234). */
+HLQ_API int hlq_xform_project_f32(const hlq_xform* view, float* dst, void* stream);
+
+/* `_unproject_axis` (backprop.py:237-249): the view's SOURCE (float32) holds
+ * kept coefficients (s, k, c); scatter them into full 16-blocks by bitmap,
+ * inverse (= forward, orthonormal) transform, write rows r < rows as
+ * (s, r, c) through dst_stride. */
+HLQ_API int hlq_xform_unproject_f32(const hlq_xform* view, float* dst, void* stream);
+
 /* The dX right operand of many layers at once: codes_i = Q_bits(HT_O(W_i))
  * for n <= 128 fp32 weights W_i (O_i x I_i, row-major), written K-major as
  * (I_i rows of ld_i >= pad16(O_i) bytes), scale_i one fp32 each -- identical

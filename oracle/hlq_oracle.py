@@ -27,6 +27,7 @@ Reference anchors (paths relative to ``/root/reference/pkg/src/hlq``):
                        true stochastic rounding; backprop.py:42-43,206-209 tags
   quantize.py:152-187  exact integer GEMM + fp64 dequant epilogue
   backprop.py:350-447  hq_grad_input / acbp_compress / hlq_grad_weight / hlq_backward
+  backprop.py:237-347  baseline strategies (naive quant, HQ, LBP-WHT, float pipelines)
   harness/layers.py:96-158  conv lowering (im2col / col2im)
 """
 from __future__ import annotations
@@ -287,6 +288,79 @@ def hlq_backward(x3: np.ndarray, w: np.ndarray, gy3: np.ndarray, rank: int = 8,
     gw = hlq_grad_weight(payload, sx, axis, gy3, bases, bits_gw, n, extra, stages, rng)
     gx = hq_grad_input(gy3, w, bits_gx, n, stages, rng)
     return gx, gw
+
+
+# ---------------------------------------------------------------------------
+# baseline strategies (backprop.py:91-155, 237-347)
+# ---------------------------------------------------------------------------
+
+def untransform_axis(c: np.ndarray, axis: int, n: int, bases, extent: int) -> np.ndarray:
+    """_unproject_axis (backprop.py:237-249): scatter the kept coefficients of
+    every block into n slots (zeros elsewhere), FWHT (orthonormal, its own
+    inverse), crop ``axis`` back to ``extent``."""
+    m = np.moveaxis(np.asarray(c, dtype=F32), axis, -1)
+    r = len(bases)
+    nb = m.shape[-1] // r
+    full = np.zeros((*m.shape[:-1], nb, n), dtype=F32)
+    full[..., list(bases)] = m.reshape(*m.shape[:-1], nb, r)
+    out = fwht_blocks(full).reshape(*m.shape[:-1], nb * n)[..., :extent]
+    return np.ascontiguousarray(np.moveaxis(out, -1, axis))
+
+
+def _float_gemm(a: np.ndarray, b: np.ndarray) -> np.ndarray:
+    return (a.astype(F32) @ b.astype(F32)).astype(F32)
+
+
+def strategy_backward(x3: np.ndarray, w: np.ndarray, gy3: np.ndarray, gx_mode: str, gx_bits,
+                      gw_mode: str, gw_bits, bases, n: int = 16, pad_small_axes: bool = False,
+                      rng: int | None = None):
+    """Raw-activation branch of strategy_backward (backprop.py:431-435) for every
+    gradient mode: fp, quant (direct), ht_quant (full-rank block transform),
+    lowrank (projection, float GEMM, dX unprojected), lowrank_quant (HLQ);
+    bits None = the float pipeline of a quantizing mode.  Returns (gx, gw)."""
+    B, L, I = x3.shape
+    O = w.shape[0]
+    bases = tuple(bases)
+    full = tuple(range(n))
+    # grad_input (backprop.py:294-316)
+    if gx_mode == "fp" or (gx_mode == "quant" and gx_bits is None):
+        gx = _float_gemm(gy3.reshape(-1, O), w).reshape(B, L, I)
+    elif gx_mode == "quant":
+        cg, sg = _q(gy3.reshape(-1, O), gx_bits, rng, TAG_GX_LEFT)
+        cw, sw = _q(w, gx_bits, rng, TAG_GX_RIGHT)
+        gx = dequant(int_gemm(cg, cw), sg, sw).reshape(B, L, I)
+    elif gx_mode == "ht_quant":
+        if gx_bits is None:
+            ghat = transform_axis(gy3, 2, n).reshape(B * L, -1)
+            gx = _float_gemm(ghat, transform_axis(w, 0, n)).reshape(B, L, I)
+        else:
+            gx = hq_grad_input(gy3, w, gx_bits, n, rng=rng)
+    elif gx_mode == "lowrank":
+        axis = proj_axis_rule(B, L, n, pad_small_axes)
+        ghat = transform_axis(gy3, axis, n, bases)
+        gxh = _float_gemm(ghat.reshape(-1, O), w).reshape(*ghat.shape[:-1], I)
+        gx = untransform_axis(gxh, axis, n, bases, gy3.shape[axis])
+    else:
+        raise OracleError(f"unknown grad_input mode {gx_mode!r}")
+    # grad_weight (backprop.py:256-291)
+    inv_b = F32(1.0 / B)
+    if gw_mode == "lowrank_quant" and gw_bits is not None:
+        payload, sx, axis = acbp_compress(x3, bases, gw_bits, n, pad_small_axes, rng)
+        return gx, hlq_grad_weight(payload, sx, axis, gy3, bases, gw_bits, n, rng=rng)
+    if gw_mode in ("ht_quant", "lowrank", "lowrank_quant"):
+        axis = proj_axis_rule(B, L, n, pad_small_axes)
+        keep = full if gw_mode == "ht_quant" else bases
+        x2 = transform_axis(x3, axis, n, keep).reshape(-1, I)
+        g2 = transform_axis(gy3, axis, n, keep).reshape(-1, O)
+    elif gw_mode in ("fp", "quant"):
+        x2, g2 = x3.reshape(-1, I), gy3.reshape(-1, O)
+    else:
+        raise OracleError(f"unknown grad_weight mode {gw_mode!r}")
+    if gw_mode in ("fp", "lowrank") or gw_bits is None:
+        return gx, (_float_gemm(np.ascontiguousarray(g2.T), x2) * inv_b).astype(F32)
+    cg, sg = _q(np.ascontiguousarray(g2.T), gw_bits, rng, TAG_GW_LEFT)
+    cx, sx = _q(np.ascontiguousarray(x2), gw_bits, rng, TAG_GW_RIGHT)
+    return gx, dequant(int_gemm(cg, cx), sg, sx, 1.0 / B)
 
 
 # ---------------------------------------------------------------------------

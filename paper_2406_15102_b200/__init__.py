@@ -15,7 +15,10 @@ from .backprop import (
     hlq_grad_weight,
     hq_grad_input,
     ht_axis_for,
+    lbp_wht_backward,
+    naive_quant_backward,
     strategy_backward,
+    vanilla_backward,
 )
 from .errors import DimensionError, ParameterError, StateError
 from .rng import RngState

@@ -58,6 +58,9 @@ SIGNATURES = {
                             _D, _I, _P, _I, _I64, _P, _I64, _P, _SZ, _P]),
     "hlq_quantize_weights_ws": (_SZ, [_I]),
     "hlq_basis_energy": (_I, [_P, _I, _I64, _I64, _I64, _I64, _I64, _P, _P]),
+    "hlq_xform_quantize": (_I, [_P, _I, _I, ctypes.c_uint64, ctypes.c_uint64, _P, _P, _P, _P]),
+    "hlq_xform_project_f32": (_I, [_P, _P, _P]),
+    "hlq_xform_unproject_f32": (_I, [_P, _P, _P]),
     "hlq_quantize_stochastic": (_I, [_P, _I, _I64, _I64, _I64, _I64, _I64, _I, _U32, _I, ctypes.c_uint64,
                                      ctypes.c_uint64, _I, _I64, _I64, _P, _P, _I64, _P, _P]),
     "hlq_quantize_weights": (_I, [_I, _P, _P, _P, _I, _P, _P, _P, _P, _SZ, _P]),
@@ -82,6 +85,12 @@ class AcbpInfo(ctypes.Structure):
     _fields_ = [("B", _I64), ("L", _I64), ("I", _I64), ("bits", _I), ("block", _I), ("rank", _I),
                 ("bitmap", _U32), ("axis", _I), ("rows", _I64), ("K", _I64), ("payload_bytes", _I64),
                 ("total_bytes", _I64)]
+
+
+class Xform(ctypes.Structure):
+    """hlq_xform (include/hlq_b200.h)."""
+    _fields_ = [("src", _P), ("src_dtype", ctypes.c_int32), ("segs", _I64), ("rows", _I64), ("cols", _I64),
+                ("src_stride", _I64 * 3), ("bitmap", _U32), ("dst_stride", _I64 * 3), ("idx_stride", _I64 * 3)]
 
 
 class GemmDesc(ctypes.Structure):

@@ -79,10 +79,41 @@ class BackwardStrategy:
         return cls("vanilla", PathSpec("fp"), PathSpec("fp"))
 
     @classmethod
+    def naive_quant(cls, bits: int = 4) -> "BackwardStrategy":
+        return cls(f"int{bits}", PathSpec("quant", bits), PathSpec("quant", bits))
+
+    @classmethod
+    def hq(cls, bits_gx: int = 4, bits_gw: int = 4, block: int = DEFAULT_BLOCK) -> "BackwardStrategy":
+        plan = HadamardPlan(block_size=block, basis_indices=tuple(range(block)))
+        return cls("hq", PathSpec("ht_quant", bits_gx), PathSpec("ht_quant", bits_gw), plan)
+
+    @classmethod
+    def lbp_wht(cls, rank: int = DEFAULT_RANK, block: int = DEFAULT_BLOCK) -> "BackwardStrategy":
+        plan = HadamardPlan(block_size=block, basis_indices=lowest_sequency_bases(block, rank))
+        return cls("lbp-wht", PathSpec("lowrank"), PathSpec("lowrank"), plan)
+
+    @classmethod
     def hlq(cls, bits_gx: int = 4, bits_gw: int = 8, rank: int = DEFAULT_RANK,
             block: int = DEFAULT_BLOCK) -> "BackwardStrategy":
         plan = HadamardPlan(block_size=block, basis_indices=lowest_sequency_bases(block, rank))
         return cls("hlq", PathSpec("ht_quant", bits_gx), PathSpec("lowrank_quant", bits_gw), plan)
+
+    def float_pipeline(self) -> "BackwardStrategy":
+        """Quantizers removed, transforms and rank kept (backprop.py:120-128)."""
+        return replace(self, name=f"{self.name}[float]",
+                       grad_input_path=replace(self.grad_input_path, bits=None),
+                       grad_weight_path=replace(self.grad_weight_path, bits=None))
+
+    def debug_exact(self) -> "BackwardStrategy":
+        """No quantization, full rank: reproduces the vanilla backward (backprop.py:130-137)."""
+        return replace(self.float_pipeline(), name=f"{self.name}[exact]",
+                       plan=self.plan.with_rank(self.plan.block_size))
+
+    @property
+    def is_hlq(self) -> bool:
+        """The combined scheme the fused training kernels implement."""
+        return (self.grad_input_path.mode == "ht_quant" and self.grad_input_path.bits is not None
+                and self.grad_weight_path.mode == "lowrank_quant" and self.grad_weight_path.bits is not None)
 
     def with_warmup_bits(self, bits: int = 8) -> "BackwardStrategy":
         def widen(spec: PathSpec) -> PathSpec:
@@ -203,12 +234,15 @@ def hq_grad_input(gy: torch.Tensor, w: torch.Tensor, bits: int | None, rng=None,
         raise DimensionError(f"expected gy (B,L,O) and w (O,I), got {tuple(gy.shape)}, {tuple(w.shape)}")
     if gy.shape[2] != w.shape[0]:
         raise DimensionError(f"output channels differ: gy {tuple(gy.shape)} vs w {tuple(w.shape)}")
-    if bits is None:
-        raise ParameterError("bits=None (float debug pipeline) is not implemented on the B200 path")
     if block != 16:
         raise ParameterError(f"the B200 kernels implement block 16 only, got {block}")
     B, L, O = gy.shape
     I = w.shape[1]
+    if bits is None:
+        # transforms only, float GEMM (backprop.py:364-366): ghat @ what == gy @ w up to roundoff
+        ghat = _block_f32(gy.reshape(B * L, O), along_cols=True)
+        what = _block_f32(w, along_cols=False)
+        return (ghat @ what).reshape(B, L, I)
     w32 = w if w.dtype == torch.float32 else w.float()
     if rng is not None:
         seed, ctr = site_key(rng, TAG_GX_LEFT)
@@ -315,24 +349,159 @@ def _vanilla_gx(gy, w):
     return (gy.reshape(-1, O).float() @ w.float()).reshape(B, L, -1)
 
 
-def _vanilla_gw(x, gy):
+def _vanilla_gw(x, gy, extra):
     B, L, I = x.shape
-    return (gy.reshape(-1, gy.shape[2]).float().t() @ x.reshape(-1, I).float()) * (1.0 / B)
+    return (gy.reshape(-1, gy.shape[2]).float().t() @ x.reshape(-1, I).float()) * extra
+
+
+# ---------------------------------------------------------------------------
+# baseline strategies: naive quant, HQ on dW, LBP-WHT and
+# the bits=None float pipelines, on the hlq_xform_* kernels; float GEMMs are
+# cuBLAS fp32 (torch matmul; TF32 stays off unless the caller enables it)
+# ---------------------------------------------------------------------------
+
+def _block_f32(m: torch.Tensor, along_cols: bool) -> torch.Tensor:
+    """_block_axis of a 2-D (R, C) matrix in float32: along its columns axis
+    (-> (R, pad16(C))) or its rows axis (-> (pad16(R), C))."""
+    R, C = m.shape
+    m = m.contiguous()
+    if along_cols:
+        out = torch.empty((R, ops.pad16(C)), dtype=torch.float32, device=m.device)
+        return ops.xform_project(m, 1, C, R, (0, 1, C), 0xFFFF, out, (0, 1, out.stride(0)))
+    out = torch.empty((ops.pad16(R), C), dtype=torch.float32, device=m.device)
+    return ops.xform_project(m, 1, R, C, (0, C, 1), 0xFFFF, out, (0, C, 1))
+
+
+def _project_f32(t: torch.Tensor, axis: int, bitmap: int) -> torch.Tensor:
+    """_project_axis (backprop.py:223-234) of (B, L, C) along `axis` in float32,
+    in the reference's shape: (B, K, C) for axis 1, (Kb, L, C) for axis 0."""
+    B, L, C = t.shape
+    segs, rows, cols, ld_src, seg_src = _proj_view(B, L, C, axis)
+    kps = ((rows + 15) // 16) * bin(bitmap).count("1")
+    out = torch.empty((segs, kps, cols), dtype=torch.float32, device=t.device)
+    ops.xform_project(t.contiguous(), segs, rows, cols, (seg_src, ld_src, 1), bitmap, out, (kps * cols, cols, 1))
+    return out if axis == 1 else out.reshape(kps, L, C)
+
+
+def _unproject_f32(coeff: torch.Tensor, axis: int, bitmap: int, B: int, L: int, C: int) -> torch.Tensor:
+    """_unproject_axis (backprop.py:237-249) back to (B, L, C)."""
+    segs, rows, cols, ld_src, seg_src = _proj_view(B, L, C, axis)
+    kps = ((rows + 15) // 16) * bin(bitmap).count("1")
+    out = torch.empty((B, L, C), dtype=torch.float32, device=coeff.device)
+    return ops.xform_unproject(coeff.contiguous(), segs, rows, cols, (kps * cols, cols, 1), bitmap, out,
+                               (seg_src, ld_src, 1))
+
+
+def _plain_codes(m: torch.Tensor, bits: int, rng, tag: int, contract_rows: bool, ref_transposed: bool = False):
+    """_quant of a 2-D (R, C) matrix with no transform (the "quant" mode) as a
+    K-major GEMM operand: contracted over C -> codes (R, pad16(C)); over R ->
+    codes (C, pad16(R)).  ref_transposed: the reference quantizes m.T (its
+    draw index is c*R + r).  Returns (codes, scale, amax_bits)."""
+    R, C = m.shape
+    m = m.contiguous()
+    if contract_rows:
+        codes = torch.zeros((C, max(ops.pad16(R), 16)), dtype=torch.int8, device=m.device)
+        dst = (0, 1, codes.stride(0))
+    else:
+        codes = torch.zeros((R, max(ops.pad16(C), 16)), dtype=torch.int8, device=m.device)
+        dst = (0, codes.stride(0), 1)
+    seed, ctr = site_key(rng, tag) if rng is not None else (None, 0)
+    idx = (0, 1, R) if ref_transposed else (0, C, 1)
+    scale, amax = ops.xform_quantize(m, 1, R, C, (0, C, 1), 0, codes, dst, bits, seed, ctr, idx)
+    return codes, scale, amax
+
+
+def _naive_gx(gy, w, bits, rng, check_finite=True):
+    """backprop.py:301-307: Q(gy (M, O)) . Q(W (O, I)), both quantized directly."""
+    B, L, O = gy.shape
+    I = w.shape[1]
+    cg, sg, ag = _plain_codes(gy.reshape(B * L, O), bits, rng, TAG_GX_LEFT, contract_rows=False)
+    cw, sw, aw = _plain_codes(w if w.dtype == torch.float32 else w.float(), bits, rng, TAG_GX_RIGHT,
+                              contract_rows=True)
+    if check_finite:
+        ops.check_finite(ag, aw)
+    out, _ = ops.gemm_i8(cg, cw, B * L, I, cg.shape[1], bits, bits, sg, sw, 1.0, exact=True)
+    return out.reshape(B, L, I)
+
+
+def _naive_gw(x, gy, bits, rng, extra, check_finite=True):
+    """backprop.py:256-291 with mode "quant": Q(gy2^T (O, K)) . Q(x2 (K, I)), K = B*L."""
+    B, L, I = x.shape
+    O = gy.shape[2]
+    K = B * L
+    cg, sg, ag = _plain_codes(gy.reshape(K, O), bits, rng, TAG_GW_LEFT, contract_rows=True, ref_transposed=True)
+    cx, sx, ax = _plain_codes(x.reshape(K, I), bits, rng, TAG_GW_RIGHT, contract_rows=True)
+    if check_finite:
+        ops.check_finite(ag, ax)
+    out, _ = ops.gemm_i8(cg, cx, O, I, cg.shape[1], bits, bits, sg, sx, extra, exact=True)
+    return out
+
+
+def _lowrank_gx(gy, w, strategy: BackwardStrategy):
+    """backprop.py:310-316: project gy, float GEMM, inverse projection."""
+    B, L, O = gy.shape
+    I = w.shape[1]
+    axis = ht_axis_for(B, L, strategy.plan.block_size, strategy.pad_small_axes)
+    bm = strategy.plan.gpu_bitmap()
+    ghat = _project_f32(gy, axis, bm)
+    gx_hat = (ghat.reshape(-1, O) @ w.float()).reshape(*ghat.shape[:-1], I)
+    return _unproject_f32(gx_hat, axis, bm, B, L, I)
+
+
+def _float_gw(x, gy, plan: HadamardPlan | None, strategy: BackwardStrategy, extra):
+    """_gw_operands + the bits=None branch of _gw_from_operands (backprop.py:256-276):
+    project x and gy along the token (or batch) axis, float GEMM."""
+    B, L, I = x.shape
+    O = gy.shape[2]
+    if plan is None:
+        return _vanilla_gw(x, gy, extra)
+    axis = ht_axis_for(B, L, plan.block_size, strategy.pad_small_axes)
+    bm = plan.gpu_bitmap()
+    x2 = _project_f32(x, axis, bm).reshape(-1, I)
+    gy2 = _project_f32(gy, axis, bm).reshape(-1, O)
+    return (gy2.t() @ x2) * extra
+
+
+def _full(plan: HadamardPlan) -> HadamardPlan:
+    return plan.with_rank(plan.block_size)
 
 
 def _grad_input(gy, w, strategy: BackwardStrategy, rng, stages=None):
+    """backprop.py:294-316."""
     spec = strategy.grad_input_path
-    if spec.mode == "fp":
+    if spec.mode == "fp" or (spec.mode == "quant" and spec.bits is None):
         return _vanilla_gx(gy, w)
+    if spec.mode == "quant":
+        return _naive_gx(gy, w, spec.bits, rng)
     if spec.mode == "ht_quant":
         return hq_grad_input(gy, w, spec.bits, rng=rng, block=strategy.plan.block_size, stages=stages)
-    raise ParameterError(f"grad_input mode {spec.mode!r} is a baseline without a B200 kernel "
-                         "(SURVEY.md 8(f) f4)")
+    return _lowrank_gx(gy, w, strategy)
+
+
+def _grad_weight(x, gy, strategy: BackwardStrategy, rng, extra):
+    """backprop.py:256-291 for the raw-activation modes."""
+    spec = strategy.grad_weight_path
+    if spec.mode == "fp" or (spec.mode == "quant" and spec.bits is None):
+        return _vanilla_gw(x, gy, extra)
+    if spec.mode == "quant":
+        return _naive_gw(x, gy, spec.bits, rng, extra)
+    if spec.bits is None:  # ht_quant / lowrank_quant float pipelines, lowrank
+        plan = _full(strategy.plan) if spec.mode == "ht_quant" else strategy.plan
+        return _float_gw(x, gy, plan, strategy, extra)
+    if spec.mode == "ht_quant":
+        # full-rank block transform along the token axis, quantized: the HLQ dW
+        # kernels with every basis kept (same tags, same C-order draw indices)
+        acbp = acbp_compress(x, _full(strategy.plan), bits=spec.bits, rng=rng,
+                             pad_small_axes=strategy.pad_small_axes)
+        return hlq_grad_weight(acbp, gy, bits=spec.bits, rng=rng, extra_scale=extra)
+    raise ParameterError(f"grad_weight mode {spec.mode!r} needs the compressed activation path")
 
 
 def strategy_backward(x_or_acbp, w: torch.Tensor, gy: torch.Tensor, strategy: BackwardStrategy,
-                      rng=None, stages: dict | None = None) -> GradPair:
-    """backprop.py:413-435."""
+                      rng=None, stages: dict | None = None, gw_scale: float | None = None) -> GradPair:
+    """backprop.py:413-435.  gw_scale replaces the 1/B mean factor of the
+    weight gradient (the torch modules pass 1: autograd's gy already has it)."""
+    _check_rng(rng)
     if isinstance(x_or_acbp, ACBPActivation):
         acbp = x_or_acbp
         if strategy.grad_weight_path.mode != "lowrank_quant":
@@ -344,12 +513,13 @@ def strategy_backward(x_or_acbp, w: torch.Tensor, gy: torch.Tensor, strategy: Ba
         if gy.dim() != 3 or tuple(gy.shape[:2]) != (B, L) or w.shape[1] != I:
             raise DimensionError(f"gy {tuple(gy.shape)} / w {tuple(w.shape)} do not match activation {acbp.orig_shape}")
         bits_gw = strategy.grad_weight_path.bits or 8
+        extra = 1.0 / B if gw_scale is None else gw_scale
         if (strategy.grad_input_path.mode == "ht_quant" and strategy.grad_input_path.bits
                 and rng is None and dual_ok(B, L, acbp.axis)):
-            gx, gw = hlq_pair(acbp, w, gy, strategy.grad_input_path.bits, bits_gw, 1.0 / B,
+            gx, gw = hlq_pair(acbp, w, gy, strategy.grad_input_path.bits, bits_gw, extra,
                               stages=stages)
             return GradPair(gx, gw)
-        gw = hlq_grad_weight(acbp, gy, bits=bits_gw, rng=rng, stages=stages)
+        gw = hlq_grad_weight(acbp, gy, bits=bits_gw, rng=rng, extra_scale=extra, stages=stages)
         gx = _grad_input(gy, w, strategy, rng, stages)
         return GradPair(gx, gw)
     x = x_or_acbp
@@ -363,20 +533,36 @@ def strategy_backward(x_or_acbp, w: torch.Tensor, gy: torch.Tensor, strategy: Ba
     if tuple(gy.shape) != (B, L, O):
         raise DimensionError(f"gy shape {tuple(gy.shape)} does not match ({B}, {L}, {O})")
     spec = strategy.grad_weight_path
-    if spec.mode == "lowrank_quant":
+    if spec.mode == "lowrank_quant" and spec.bits is not None:
         # raw branch == ACBP branch bit for bit in pseudo mode (test_backprop.py:338-345)
         acbp = acbp_compress(x, strategy.plan, bits=spec.bits or 8, rng=rng,
                              pad_small_axes=strategy.pad_small_axes)
         if stages is not None:
             stages.update(x_codes=acbp.reference_payload(), x_scale=acbp.quantized.scale, axis=acbp.axis)
-        return strategy_backward(acbp, w, gy, strategy, rng=rng, stages=stages)
+        return strategy_backward(acbp, w, gy, strategy, rng=rng, stages=stages, gw_scale=gw_scale)
     gx = _grad_input(gy, w, strategy, rng, stages)
-    if spec.mode == "fp":
-        gw = _vanilla_gw(x, gy)
-    else:
-        raise ParameterError(f"grad_weight mode {spec.mode!r} is a baseline without a B200 kernel "
-                             "(SURVEY.md 8(f) f4)")
+    gw = _grad_weight(x, gy, strategy, rng, 1.0 / B if gw_scale is None else gw_scale)
     return GradPair(gx, gw)
+
+
+def vanilla_backward(x: torch.Tensor, w: torch.Tensor, gy: torch.Tensor) -> GradPair:
+    """backprop.py:326-331: the exact chain rule (float32 GEMMs)."""
+    return strategy_backward(x, w, gy, BackwardStrategy.vanilla())
+
+
+def naive_quant_backward(x: torch.Tensor, w: torch.Tensor, gy: torch.Tensor, bits: int, rng=None) -> GradPair:
+    """backprop.py:334-337: both products on directly quantized operands."""
+    return strategy_backward(x, w, gy, BackwardStrategy.naive_quant(bits), rng=rng)
+
+
+def lbp_wht_backward(x: torch.Tensor, w: torch.Tensor, gy: torch.Tensor, plan: HadamardPlan,
+                     pad_small_axes: bool = False) -> GradPair:
+    """backprop.py:340-347: low-rank basis truncation on both paths (float GEMMs)."""
+    if plan.full_rank:
+        raise ParameterError("plan is full-rank; low-rank backward needs rank < block size")
+    strategy = BackwardStrategy("lbp-wht", PathSpec("lowrank"), PathSpec("lowrank"), plan=plan,
+                                pad_small_axes=pad_small_axes)
+    return strategy_backward(x, w, gy, strategy)
 
 
 def hlq_backward(x_or_acbp, w: torch.Tensor, gy: torch.Tensor,

@@ -20,8 +20,8 @@ ROOT = os.path.dirname(HERE)
 CSRC = os.path.join(HERE, "csrc")
 LIB = os.path.join(HERE, "libhlq_b200.so")
 SOURCES = ["hlq_transform.cu", "hlq_transform_fallback.cu", "hlq_conv.cu", "hlq_gemm.cu", "hlq_weights.cu",
-           "hlq_stochastic.cu", "hlq_acbp.cu", "hlq_capi.cu"]
-HEADERS = ["hlq_ptx.cuh", "hlq_quant.cuh", "hlq_internal.h", os.path.join("..", "..", "include", "hlq_b200.h")]
+           "hlq_stochastic.cu", "hlq_baselines.cu", "hlq_acbp.cu", "hlq_capi.cu"]
+HEADERS = ["hlq_ptx.cuh", "hlq_quant.cuh", "hlq_philox.cuh", "hlq_internal.h", os.path.join("..", "..", "include", "hlq_b200.h")]
 
 NVCC_FLAGS = [
     "-gencode", "arch=compute_100a,code=sm_100a",

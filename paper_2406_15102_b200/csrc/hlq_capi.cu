@@ -392,6 +392,53 @@ int hlq_basis_energy(const void* src, int dtype, int64_t segs, int64_t rows, int
   return cuda_status("hlq_basis_energy");
 }
 
+static int xform_view(const hlq_xform* v, bool quant_source_dtype, hlq::XformView* x) {
+  if (!v) return fail(HLQ_ERR_PARAMETER, "null view");
+  if (quant_source_dtype) HLQ_TRY(check_dtype(v->src_dtype));
+  if (v->segs < 0 || v->rows < 0 || v->cols < 0) return fail(HLQ_ERR_DIMENSION, "negative view extent");
+  if (!v->src && v->segs * v->rows * v->cols > 0) return fail(HLQ_ERR_PARAMETER, "null source");
+  if (v->bitmap > 0xFFFFu) return fail(HLQ_ERR_PARAMETER, "bitmap has bits above the 16-point block");
+  *x = hlq::XformView{};
+  x->src = v->src; x->dtype = quant_source_dtype ? v->src_dtype : HLQ_F32;
+  x->segs = v->segs; x->rows = v->rows; x->cols = v->cols; x->nblk = (v->rows + 15) / 16;
+  x->ss = v->src_stride[0]; x->sr = v->src_stride[1]; x->sc = v->src_stride[2];
+  x->bitmap = v->bitmap; x->rank = __builtin_popcount(v->bitmap);
+  x->ds = v->dst_stride[0]; x->dk = v->dst_stride[1]; x->dc = v->dst_stride[2];
+  x->is = v->idx_stride[0]; x->ik = v->idx_stride[1]; x->ic = v->idx_stride[2];
+  return HLQ_OK;
+}
+
+int hlq_xform_quantize(const hlq_xform* view, int bits, int rounding, uint64_t seed, uint64_t counter,
+                       uint32_t* stats_ws, int8_t* dst, float* scale_out, void* stream) {
+  hlq::XformView x;
+  HLQ_TRY(xform_view(view, true, &x));
+  HLQ_TRY(check_bits(bits));
+  if (rounding != 0 && rounding != 1) return fail(HLQ_ERR_PARAMETER, "rounding must be 0 (pseudo) or 1 (stochastic)");
+  if (!stats_ws || !scale_out) return fail(HLQ_ERR_PARAMETER, "null stats or scale");
+  if (!dst && x.segs * x.rows * x.cols > 0) return fail(HLQ_ERR_PARAMETER, "null codes");
+  hlq::launch_xform_quant(x, bits, rounding, seed, counter, stats_ws, dst, scale_out, static_cast<cudaStream_t>(stream));
+  return cuda_status("hlq_xform_quantize");
+}
+
+int hlq_xform_project_f32(const hlq_xform* view, float* dst, void* stream) {
+  hlq::XformView x;
+  HLQ_TRY(xform_view(view, true, &x));
+  if (!dst && x.segs * x.rows * x.cols > 0) return fail(HLQ_ERR_PARAMETER, "null output");
+  if (x.segs * x.rows * x.cols == 0) return HLQ_OK;
+  hlq::launch_xform_f32(x, dst, static_cast<cudaStream_t>(stream));
+  return cuda_status("hlq_xform_project_f32");
+}
+
+int hlq_xform_unproject_f32(const hlq_xform* view, float* dst, void* stream) {
+  hlq::XformView x;
+  HLQ_TRY(xform_view(view, false, &x));
+  if (x.bitmap == 0) return fail(HLQ_ERR_PARAMETER, "unproject needs at least one kept basis");
+  if (!dst && x.segs * x.rows * x.cols > 0) return fail(HLQ_ERR_PARAMETER, "null output");
+  if (x.segs * x.rows * x.cols == 0) return HLQ_OK;
+  hlq::launch_unproject_f32(x, dst, static_cast<cudaStream_t>(stream));
+  return cuda_status("hlq_xform_unproject_f32");
+}
+
 int64_t hlq_acbp_container_bytes(int64_t rows, int64_t k, int bits) {
   const int64_t count = rows * k;
   return 33 + (bits == 8 ? count : (count + 1) / 2) + 4;

@@ -121,6 +121,22 @@ int acbp_pack(const int8_t* codes, int64_t ld, int64_t R, int64_t K, int bits, c
 int acbp_check_and_unpack(const uint8_t* buf, int64_t total, int64_t R, int64_t K, int bits, int8_t* codes,
                           int64_t ld, float* scale_out, void* ws, int64_t* bad_offset, bool* crc_ok,
                           cudaStream_t st);
+// Baseline-strategy transforms (hlq_baselines.cu): strided view, block FWHT
+// along rows keeping `bitmap`'s bases (0 = identity), outputs (s, k, c).
+struct XformView {
+  const void* src;
+  int dtype;
+  int64_t segs, rows, cols, nblk;
+  int64_t ss, sr, sc;  // source strides (elements)
+  uint32_t bitmap;
+  int rank;
+  int64_t ds, dk, dc;  // destination strides (elements)
+  int64_t is, ik, ic;  // reference C-order index strides (stochastic draws)
+};
+void launch_xform_quant(const XformView& x, int bits, int rounding, uint64_t k0, uint64_t k1, uint32_t* stats,
+                        int8_t* dst, float* scale_out, cudaStream_t st);
+void launch_xform_f32(const XformView& x, float* dst, cudaStream_t st);
+void launch_unproject_f32(const XformView& x, float* dst, cudaStream_t st);
 // Workspace bytes that let launch_gemm_i8 split K (0: no split planned).
 size_t gemm_i8_ws_bytes(int64_t M, int64_t N, int64_t K, int64_t groups);
 

@@ -176,6 +176,33 @@ class HLQLinearFunction(torch.autograd.Function):
         return gx, gw, gb, None, None, None
 
 
+class BaselineLinearFunction(torch.autograd.Function):
+    """Linear layer under a baseline strategy (naive quant, HQ, LBP-WHT, float
+    pipelines; backprop.py:91-155): the raw input is saved and the backward is
+    backprop.strategy_backward on the hlq_xform / GEMM kernels -- the
+    reference's ablation-grid path (harness/layers.py:57-69 with
+    store_compressed off)."""
+
+    @staticmethod
+    def forward(ctx, x, weight, bias, strategy: BackwardStrategy, rng=None):
+        ctx.save_for_backward(x, weight)
+        ctx.meta = (tuple(x.shape), bias is not None, strategy, rng)
+        return F.linear(x, weight.to(x.dtype) if x.dtype != weight.dtype else weight,
+                        None if bias is None else bias.to(x.dtype))
+
+    @staticmethod
+    def backward(ctx, gy):
+        from .backprop import strategy_backward
+        x, weight = ctx.saved_tensors
+        x_shape, has_bias, strategy, rng = ctx.meta
+        B, L, I = _blv(x_shape)
+        O = weight.shape[0]
+        gp = strategy_backward(x.reshape(B, L, I).float(), weight.float(), gy.reshape(B, L, O).float(), strategy,
+                               rng=rng, gw_scale=1.0)
+        gb = gy.reshape(-1, O).sum(0, dtype=torch.float32) if has_bias and ctx.needs_input_grad[2] else None
+        return gp.grad_input.reshape(x_shape).to(x.dtype), gp.grad_weight.to(weight.dtype), gb, None, None
+
+
 class HLQLinear(nn.Linear):
     """nn.Linear with the HLQ backward (reference harness/layers.py:72-93)."""
 
@@ -203,6 +230,8 @@ class HLQLinear(nn.Linear):
         if torch.is_autocast_enabled("cuda"):
             x = x.to(torch.get_autocast_dtype("cuda"))
         with torch.autocast("cuda", enabled=False):
+            if not self.strategy.is_hlq:
+                return BaselineLinearFunction.apply(x, self.weight, self.bias, self.strategy)
             return HLQLinearFunction.apply(x, self.weight, self.bias, self.strategy, self.cached_weight_codes(),
                                            self if _CALIB[0] is not None else None)
 

@@ -271,6 +271,70 @@ def basis_energy(src: torch.Tensor, segs: int, rows: int, cols: int, ld_src: int
     return energy, segs * ((rows + 15) // 16) * cols
 
 
+# ---------------------------------------------------------------------------
+# baseline-strategy transforms (hlq_xform_*)
+# ---------------------------------------------------------------------------
+
+def _xview(src, segs, rows, cols, src_strides, bitmap, dst_strides, idx_strides=(0, 0, 0)):
+    v = _lib.Xform()
+    v.src = src.data_ptr()
+    v.src_dtype = dtype_code(src) if src.dtype != torch.float32 else _lib.HLQ_F32
+    v.segs, v.rows, v.cols = int(segs), int(rows), int(cols)
+    v.bitmap = int(bitmap)
+    for i in range(3):
+        v.src_stride[i] = int(src_strides[i])
+        v.dst_stride[i] = int(dst_strides[i])
+        v.idx_stride[i] = int(idx_strides[i])
+    return v
+
+
+def xform_quantize(src: torch.Tensor, segs: int, rows: int, cols: int, src_strides, bitmap: int,
+                   dst: torch.Tensor, dst_strides, bits: int, seed: int | None = None, counter: int = 0,
+                   idx_strides=(0, 0, 0)):
+    """Q_bits of the strided view's outputs into the int8 tensor dst (pseudo-
+    stochastic rounding, or Philox draws when seed is given).  Returns
+    (scale (1,) fp32, amax_bits (1,) int32)."""
+    _check_bits(bits)
+    src = _cuda(src, "src")
+    if dst.dtype != torch.int8:
+        raise ParameterError("codes must be int8")
+    v = _xview(src, segs, rows, cols, src_strides, bitmap, dst_strides, idx_strides)
+    scale = torch.empty(1, dtype=torch.float32, device=src.device)
+    stats = torch.empty(8, dtype=torch.int32, device=src.device)
+    rounding = 0 if seed is None else 1
+    _traced("transform", src.numel() * src.element_size() + dst.numel(), 0, 2,
+            lambda: _lib.call("hlq_xform_quantize", ctypes.byref(v), bits, rounding, int(seed or 0),
+                              int(counter), _p(stats), _p(dst), _p(scale), _stream()),
+            key=f"transform:xform_quant:{segs * rows}x{cols}")
+    return scale, stats[0:1]
+
+
+def xform_project(src: torch.Tensor, segs: int, rows: int, cols: int, src_strides, bitmap: int,
+                  dst: torch.Tensor, dst_strides) -> torch.Tensor:
+    """The strided view's (transformed) outputs in float32 into dst."""
+    src = _cuda(src, "src")
+    if dst.dtype != torch.float32:
+        raise ParameterError("projection output must be float32")
+    v = _xview(src, segs, rows, cols, src_strides, bitmap, dst_strides)
+    _traced("transform", src.numel() * src.element_size() + dst.numel() * 4, 0, 1,
+            lambda: _lib.call("hlq_xform_project_f32", ctypes.byref(v), _p(dst), _stream()),
+            key=f"transform:xform_f32:{segs * rows}x{cols}")
+    return dst
+
+
+def xform_unproject(coeffs: torch.Tensor, segs: int, rows: int, cols: int, src_strides, bitmap: int,
+                    dst: torch.Tensor, dst_strides) -> torch.Tensor:
+    """_unproject_axis: kept coefficients (s, k, c) -> float32 (s, r, c), r < rows."""
+    coeffs = _cuda(coeffs, "coefficients")
+    if coeffs.dtype != torch.float32 or dst.dtype != torch.float32:
+        raise ParameterError("unprojection runs in float32")
+    v = _xview(coeffs, segs, rows, cols, src_strides, bitmap, dst_strides)
+    _traced("transform", coeffs.numel() * 4 + dst.numel() * 4, 0, 1,
+            lambda: _lib.call("hlq_xform_unproject_f32", ctypes.byref(v), _p(dst), _stream()),
+            key=f"transform:unproject:{segs * rows}x{cols}")
+    return dst
+
+
 def proj_rows_amax(src: torch.Tensor, segs: int, rows: int, cols: int, bitmap: int,
                    stats: torch.Tensor, ld_src: int | None = None, seg_src: int | None = None):
     """Accumulate the transformed statistics (IEEE bits, atomic max) into stats[2:4]

@@ -242,6 +242,38 @@ def known_answer_cases():
     return names
 
 
+def baseline_case(name, seed, B, L, I, O, preset, rng_seed=None, pad_small=False, **kw):
+    """A baseline strategy (backprop.py:91-155: vanilla, naive int4/int8, HQ,
+    LBP-WHT, float pipelines, mixed modes) through the reference's
+    strategy_backward on the raw activation."""
+    hlq, bp, qz, _ = _ref()
+    x, w, gy = _inputs(seed, B, L, I, O)
+    S = hlq.BackwardStrategy
+    if preset == "custom":
+        strat = S("custom", hlq.PathSpec(*kw["gx"]), hlq.PathSpec(*kw["gw"]),
+                  hlq.HadamardPlan(block_size=16, basis_indices=hlq.hadamard.lowest_sequency_bases(
+                      16, kw.get("rank", 8))))
+    else:
+        base, _, variant = preset.partition(".")
+        strat = getattr(S, base)(**kw)
+        if variant:
+            strat = getattr(strat, variant)()
+    if pad_small:
+        import dataclasses
+        strat = dataclasses.replace(strat, pad_small_axes=True)
+    rng = qz.RngState(rng_seed) if rng_seed is not None else None
+    gp = hlq.strategy_backward(hlq.Tensor(x), hlq.Tensor(w), hlq.Tensor(gy), strat, rng=rng)
+    gx_spec, gw_spec = strat.grad_input_path, strat.grad_weight_path
+    out = dict(x=x, w=w, gy=gy, preset=np.array(preset),
+               gx_mode=np.array(gx_spec.mode), gx_bits=np.int64(gx_spec.bits or 0),
+               gw_mode=np.array(gw_spec.mode), gw_bits=np.int64(gw_spec.bits or 0),
+               bases=np.array(strat.plan.basis_indices, dtype=np.int64), pad_small=np.int64(pad_small),
+               rng_seed=np.int64(-1 if rng_seed is None else rng_seed),
+               gx=gp.grad_input.data, gw=gp.grad_weight.data)
+    np.savez_compressed(os.path.join(HERE, f"{name}.npz"), **out)
+    return name
+
+
 def main():
     made = []
     # 2-D Linear convention (layers.py:87): L = 1, projection along B.
@@ -277,6 +309,25 @@ def main():
     made.append(stochastic_case("stoch_lin2d", 41, 48, 1, 32, 24, rng_seed=7))
     # ACBP containers (acbp.py): int8 / int4 (odd count -> padding nibble), batch axis,
     # padded L, pad-small axes, empty batch
+    # baseline strategies
+    made.append(baseline_case("base_vanilla", 60, 4, 40, 48, 36, "vanilla"))
+    made.append(baseline_case("base_int4", 61, 4, 40, 48, 36, "naive_quant", bits=4))
+    made.append(baseline_case("base_int8", 62, 3, 37, 24, 20, "naive_quant", bits=8))
+    made.append(baseline_case("base_int4_rng", 63, 4, 40, 48, 36, "naive_quant", rng_seed=99, bits=4))
+    made.append(baseline_case("base_hq", 64, 4, 40, 48, 36, "hq"))
+    made.append(baseline_case("base_hq8", 65, 3, 37, 24, 20, "hq", bits_gx=8, bits_gw=8))
+    made.append(baseline_case("base_hq_rng", 66, 3, 37, 24, 20, "hq", rng_seed=5))
+    made.append(baseline_case("base_hq_batch", 67, 32, 5, 16, 24, "hq"))
+    made.append(baseline_case("base_lbp", 68, 3, 37, 24, 20, "lbp_wht"))
+    made.append(baseline_case("base_lbp_r4", 69, 4, 40, 48, 36, "lbp_wht", rank=4))
+    made.append(baseline_case("base_lbp_batch", 70, 20, 3, 16, 24, "lbp_wht"))
+    made.append(baseline_case("base_lbp_padsmall", 71, 5, 7, 16, 8, "lbp_wht", pad_small=True))
+    made.append(baseline_case("base_hlq_float", 72, 3, 37, 24, 20, "hlq.float_pipeline"))
+    made.append(baseline_case("base_hlq_exact", 73, 3, 37, 24, 20, "hlq.debug_exact"))
+    made.append(baseline_case("base_hq_float", 74, 4, 40, 48, 36, "hq.float_pipeline"))
+    made.append(baseline_case("base_mix_q8_hlq", 75, 3, 37, 24, 20, "custom", gx=("quant", 8),
+                              gw=("lowrank_quant", 8)))
+    made.append(baseline_case("base_mix_lr_fp", 76, 4, 40, 48, 36, "custom", gx=("lowrank",), gw=("fp",)))
     made.append(container_case("acbp_c8", 50, 4, 32, 12))
     made.append(container_case("acbp_c4_odd", 51, 1, 16, 5, bits=4, bases=(0, 1, 2)))
     made.append(container_case("acbp_c4", 52, 3, 40, 7, bits=4))

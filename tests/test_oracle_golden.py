@@ -150,3 +150,34 @@ def test_calibration_matches_reference(case):
     e = orc.basis_energy(g["gy"], int(g["axis"]))
     assert np.array_equal(np.abs(e).mean(axis=0), g["means"])
     assert orc.select_bases(e, int(g["rank"])) == tuple(int(b) for b in g["bases"])
+
+
+BASELINES = [c for c in MANIFEST["cases"] if c.startswith("base_")]
+
+
+def _baseline_args(g):
+    bits = lambda v: None if int(v) == 0 else int(v)  # noqa: E731
+    seed = int(g["rng_seed"])
+    return dict(gx_mode=str(g["gx_mode"]), gx_bits=bits(g["gx_bits"]), gw_mode=str(g["gw_mode"]),
+                gw_bits=bits(g["gw_bits"]), bases=tuple(int(b) for b in g["bases"]),
+                pad_small_axes=bool(g["pad_small"]), rng=None if seed < 0 else seed)
+
+
+def _is_int(mode, bits):
+    return mode in ("quant", "ht_quant", "lowrank_quant") and bits is not None
+
+
+@pytest.mark.parametrize("case", BASELINES)
+def test_baseline_strategies_match_reference(case):
+    """Oracle restatement of every baseline mode vs the reference's
+    strategy_backward: integer paths bit-exact, float paths to fp32 roundoff."""
+    g = load(case)
+    a = _baseline_args(g)
+    gx, gw = orc.strategy_backward(g["x"], g["w"], g["gy"], **a)
+    for got, ref, mode, bits in ((gx, g["gx"], a["gx_mode"], a["gx_bits"]),
+                                 (gw, g["gw"], a["gw_mode"], a["gw_bits"])):
+        assert got.shape == ref.shape and got.dtype == ref.dtype
+        if _is_int(mode, bits):
+            assert np.array_equal(got, ref)
+        else:
+            assert np.allclose(got, ref, rtol=1e-5, atol=1e-6 * float(np.abs(ref).max() + 1e-30))
