@@ -107,6 +107,19 @@ HLQ_API int hlq_quantize_dual(const void* src, int dtype, int64_t segs, int64_t 
                               int8_t* dst_gw, int64_t ld_gw, float* scale_gx, float* scale_gw,
                               void* stream);
 
+/* hlq_quantize_dual plus the fp32 column sums of the source (colsum_out, cols
+ * floats): the bias gradient gy.sum over tokens (harness/layers.py:67 before
+ * its /B), read from the same tiles as the STATS pass -- no separate pass
+ * over gy.  Deterministic: per-work-item partials in colsum_ws
+ * (hlq_quantize_dual_colsum_ws bytes), reduced in a fixed order inside the
+ * same launch. */
+HLQ_API size_t hlq_quantize_dual_colsum_ws(int64_t segs, int64_t rows, int64_t cols, uint32_t bitmap);
+HLQ_API int hlq_quantize_dual_colsum(const void* src, int dtype, int64_t segs, int64_t rows, int64_t cols,
+                                     int64_t ld_src, int64_t seg_src, uint32_t bitmap, int bits_gx,
+                                     int bits_gw, uint32_t* stats_ws, int8_t* dst_gx, int64_t ld_gx,
+                                     int8_t* dst_gw, int64_t ld_gw, float* scale_gx, float* scale_gw,
+                                     float* colsum_out, void* colsum_ws, size_t colsum_ws_bytes, void* stream);
+
 /* The two passes of hlq_quantize_proj_rows, separately, for the data-parallel
  * global-scale mode: _amax accumulates (atomic max, no reset) the transformed
  * statistics into stats[2..3] (stats: 4 x uint32, zero-initialised by the

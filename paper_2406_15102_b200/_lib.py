@@ -13,7 +13,8 @@ import threading
 from .errors import DimensionError, FormatError, ParameterError, StateError
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libhlq_b200.so")
+# HLQ_LIB_PATH: load an alternative in-tree build (A/B kernel experiments)
+LIB_PATH = os.environ.get("HLQ_LIB_PATH") or os.path.join(_HERE, "libhlq_b200.so")
 
 (HLQ_OK, HLQ_ERR_DIMENSION, HLQ_ERR_PARAMETER, HLQ_ERR_STATE, HLQ_ERR_NONFINITE, HLQ_ERR_CUDA,
  HLQ_ERR_FORMAT) = range(7)
@@ -58,6 +59,9 @@ SIGNATURES = {
                             _D, _I, _P, _I, _I64, _P, _I64, _P, _SZ, _P]),
     "hlq_quantize_weights_ws": (_SZ, [_I]),
     "hlq_basis_energy": (_I, [_P, _I, _I64, _I64, _I64, _I64, _I64, _P, _P]),
+    "hlq_quantize_dual_colsum_ws": (_SZ, [_I64, _I64, _I64, _U32]),
+    "hlq_quantize_dual_colsum": (_I, [_P, _I, _I64, _I64, _I64, _I64, _I64, _U32, _I, _I, _P, _P, _I64, _P,
+                                      _I64, _P, _P, _P, _P, _SZ, _P]),
     "hlq_xform_quantize": (_I, [_P, _I, _I, ctypes.c_uint64, ctypes.c_uint64, _P, _P, _P, _P]),
     "hlq_xform_project_f32": (_I, [_P, _P, _P]),
     "hlq_xform_unproject_f32": (_I, [_P, _P, _P]),

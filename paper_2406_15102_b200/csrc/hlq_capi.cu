@@ -226,6 +226,35 @@ int hlq_quantize_dual(const void* src, int dtype, int64_t segs, int64_t rows, in
   return cuda_status("hlq_quantize_dual");
 }
 
+size_t hlq_quantize_dual_colsum_ws(int64_t segs, int64_t rows, int64_t cols, uint32_t bitmap) {
+  return hlq::transform_colsum_ws(segs, rows, cols, bitmap);
+}
+
+int hlq_quantize_dual_colsum(const void* src, int dtype, int64_t segs, int64_t rows, int64_t cols,
+                             int64_t ld_src, int64_t seg_src, uint32_t bitmap, int bits_gx, int bits_gw,
+                             uint32_t* stats_ws, int8_t* dst_gx, int64_t ld_gx, int8_t* dst_gw, int64_t ld_gw,
+                             float* scale_gx, float* scale_gw, float* colsum_out, void* colsum_ws,
+                             size_t colsum_ws_bytes, void* stream) {
+  HLQ_TRY(check_bits(bits_gx));
+  HLQ_TRY(proj_rows_checked(src, dtype, segs, rows, cols, ld_src, seg_src, bitmap, bits_gw, dst_gw,
+                            ld_gw));
+  HLQ_TRY(check_ld16(ld_gx, "gx codes"));
+  if (ld_gx < pad16(cols)) return fail(HLQ_ERR_DIMENSION, "gx codes ld < pad16(cols)");
+  if (!colsum_out) return fail(HLQ_ERR_PARAMETER, "null column-sum output");
+  const size_t need = hlq::transform_colsum_ws(segs, rows, cols, bitmap);
+  if (colsum_ws_bytes < need || (need && !colsum_ws))
+    return fail(HLQ_ERR_PARAMETER, "column-sum workspace needs %zu bytes, got %zu", need, colsum_ws_bytes);
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  hlq::TransformArgs t = proj_args(src, dtype, segs, rows, cols, ld_src, seg_src, bitmap, bits_gw,
+                                   stats_ws, dst_gw, ld_gw, scale_gw);
+  t.do_gx = true; t.bits_gx = bits_gx; t.dst_gx = dst_gx; t.ld_gx = ld_gx; t.scale_gx = scale_gx;
+  t.colsum_out = colsum_out;
+  t.colsum_ws = static_cast<float*>(colsum_ws);
+  cudaMemsetAsync(stats_ws, 0, HLQ_STATS_WS_BYTES, st);
+  hlq::launch_transform(t, hlq::kBoth, st);
+  return cuda_status("hlq_quantize_dual_colsum");
+}
+
 int hlq_gemm_i8(const int8_t* A, int64_t lda, const int8_t* B, int64_t ldb, int64_t M, int64_t N,
                 int64_t K, int bits_a, int bits_b, const float* sa, const float* sb, double extra,
                 int epilogue, void* out, int out_dtype, int64_t ldo, int32_t* acc_out,

@@ -33,9 +33,14 @@ struct TransformArgs {
   int64_t ld_gw;
   float* scale_gx;
   float* scale_gw;
+  // optional (kBoth with do_gw): fp32 column sums of the source -> colsum_out,
+  // partials in colsum_ws (transform_colsum_ws bytes)
+  float* colsum_out = nullptr;
+  float* colsum_ws = nullptr;
 };
 
 void launch_transform(const TransformArgs& t, int mode, cudaStream_t stream);
+size_t transform_colsum_ws(int64_t segs, int64_t rows, int64_t cols, uint32_t bitmap);
 void launch_transform_fallback(const TransformArgs& t, int mode, cudaStream_t stream);
 
 // Conv lowering (hlq_conv.cu).  x is channels-last (B, H, W, C).

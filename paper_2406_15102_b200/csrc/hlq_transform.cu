@@ -62,6 +62,9 @@ constexpr int kCols = 256;       // columns per step
 constexpr int kConsumers = 128;  // 4 consumer warps
 constexpr int kThreads = kConsumers + 32;
 constexpr int kStages = 4;
+#ifndef HLQ_TR_MINB
+#define HLQ_TR_MINB 4  // CTAs per SM the register budget is sized for
+#endif
 
 template <typename T>
 struct Tr;
@@ -92,6 +95,12 @@ struct Args {
   // one 16-output-pixel block x 256 channels per step and tap; segments =
   // images, rows = output pixels l = ho*Wo + wo, payload row = c*taps + tap
   int taps, kconv, cstr, cpad, wo_n;
+  // column sums of the source (the bias gradient), fused into the STATS pass of
+  // kBoth: cs_part[g][c] = sum of column c over row group g (one work item's
+  // rows), then a fixed-order reduction over g after pass 2 -> cs_out[c]
+  float* cs_part;
+  float* cs_out;
+  int groups;
 };
 
 // (item, block) steps of this CTA with 32-bit counters; divisions once per item.
@@ -181,6 +190,7 @@ __device__ __forceinline__ void consume(const Args& a, const Quant& qx, const Qu
   constexpr int kFlushThreads = kConsumers;
   StepIter it;
   it.begin(a, reverse);
+  float2 csum = make_float2(0.0f, 0.0f);
   while (it.valid(a)) {
     {
       ptx::mbar_wait(&full[slot], phase);
@@ -240,6 +250,22 @@ __device__ __forceinline__ void consume(const Args& a, const Quant& qx, const Qu
 #pragma unroll
             for (int i = 0; i < 16; ++i)
               if (i >= rvalid) pv[i] = make_float2(0.0f, 0.0f);
+          }
+          if (MODE == kStats && a.cs_part) {
+            // column sums of the 16 rows (pairwise tree), accumulated over the item
+            float2 t[8];
+#pragma unroll
+            for (int i = 0; i < 8; ++i) t[i] = f2add(pv[2 * i], pv[2 * i + 1]);
+#pragma unroll
+            for (int i = 0; i < 4; ++i) t[i] = f2add(t[2 * i], t[2 * i + 1]);
+            t[0] = f2add(f2add(t[0], t[1]), f2add(t[2], t[3]));
+            csum = it.bl == 0 ? t[0] : f2add(csum, t[0]);
+            if (it.bl == it.nbl - 1) {
+              // column-major partials: a column's groups are contiguous for the final sum
+              float* o = a.cs_part + int64_t(it.col0 + c) * a.groups + it.gb0 / a.nb;
+              o[0] = csum.x;
+              if (it.col0 + c + 1 < a.cols) o[a.groups] = csum.y;
+            }
           }
           fwht16_pair(pv);
           if (MODE == kStats) {
@@ -370,7 +396,7 @@ __device__ __forceinline__ void consume_quant(const Args& a, uint8_t* tiles, uin
 // waits for the barrier: it keeps streaming pass-2 tiles into the ring while
 // the consumers wait for the scales.
 template <typename T, int MODE, bool GX, bool GW, int BM>
-__global__ void __launch_bounds__(kThreads) tma_tile_kernel(const __grid_constant__ CUtensorMap map,
+__global__ void __launch_bounds__(kThreads, HLQ_TR_MINB) tma_tile_kernel(const __grid_constant__ CUtensorMap map,
                                                            Args a) {
   constexpr int kRow = Tr<T>::kRow;
   extern __shared__ __align__(128) uint8_t smem_raw[];
@@ -454,6 +480,31 @@ __global__ void __launch_bounds__(kThreads) tma_tile_kernel(const __grid_constan
   }
   asm volatile("bar.sync 2, %0;" ::"n"(kConsumers) : "memory");
   consume_quant<T, GX, GW, BM>(a, tiles, full, empty, cbuf, slot, phase, true);
+  if (GW && a.cs_out) {
+    // column sums: one warp per column, lanes over the column's contiguous
+    // row-group partials (coalesced, 16 loads in flight per lane), fixed
+    // summation order and shuffle tree -> deterministic.  The partials were
+    // written before the grid barrier (L2 loads).
+    const int lane = threadIdx.x & 31;
+    for (int c = blockIdx.x * (kConsumers / 32) + (threadIdx.x >> 5); c < a.cols;
+         c += gridDim.x * (kConsumers / 32)) {
+      const float* p = a.cs_part + int64_t(c) * a.groups;
+      float acc = 0.0f;
+      for (int g0 = 0; g0 < a.groups; g0 += 16 * 32) {
+        float v[16];
+#pragma unroll
+        for (int j = 0; j < 16; ++j) {
+          const int g = g0 + 32 * j + lane;
+          v[j] = g < a.groups ? __ldcg(p + g) : 0.0f;
+        }
+#pragma unroll
+        for (int j = 0; j < 16; ++j) acc += v[j];
+      }
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+      if (lane == 0) a.cs_out[c] = acc;
+    }
+  }
 }
 
 template <typename T, int MODE, bool GX, bool GW, int BM>
@@ -532,6 +583,33 @@ int choose_nb(int total_blocks, int cols, int rank) {
     if (v >= 1 && v <= 16) nb = v;
   }
   return nb;
+}
+
+// Column sums without the fused path (sources the tensor map cannot describe):
+// one thread per column over every row, in row order (deterministic).
+template <typename T>
+__global__ void colsum_kernel(const T* src, int64_t segs, int64_t rows, int64_t cols, int64_t ld, int64_t seg,
+                              float* out) {
+  const int64_t c = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (c >= cols) return;
+  float acc = 0.0f;
+  for (int64_t s = 0; s < segs; ++s)
+    for (int64_t r = 0; r < rows; ++r) {
+      const T v = src[s * seg + r * ld + c];
+      acc += sizeof(T) == 2 ? __bfloat162float(*reinterpret_cast<const __nv_bfloat16*>(&v))
+                            : *reinterpret_cast<const float*>(&v);
+    }
+  out[c] = acc;
+}
+
+void launch_colsum(const TransformArgs& t, cudaStream_t st) {
+  const int grid = int((t.cols + 127) / 128);
+  if (t.dtype == kBF16)
+    colsum_kernel<<<grid, 128, 0, st>>>(static_cast<const __nv_bfloat16*>(t.src), t.segs, t.rows, t.cols,
+                                        t.ld_src, t.seg_src, t.colsum_out);
+  else
+    colsum_kernel<<<grid, 128, 0, st>>>(static_cast<const float*>(t.src), t.segs, t.rows, t.cols, t.ld_src,
+                                        t.seg_src, t.colsum_out);
 }
 
 }  // namespace
@@ -620,9 +698,12 @@ void launch_transform(const TransformArgs& t, int mode, cudaStream_t stream) {
   if (!ok) {
     if (mode == kBoth) {
       launch_transform_fallback(t, kStats, stream);
-      return launch_transform_fallback(t, kQuant, stream);
+      launch_transform_fallback(t, kQuant, stream);
+    } else {
+      launch_transform_fallback(t, mode, stream);
     }
-    return launch_transform_fallback(t, mode, stream);
+    if (t.colsum_out) launch_colsum(t, stream);
+    return;
   }
   Args a{};
   a.rows = int(t.rows);
@@ -644,10 +725,24 @@ void launch_transform(const TransformArgs& t, int mode, cudaStream_t stream) {
   a.scale_gx = t.scale_gx;
   a.scale_gw = t.scale_gw;
   a.cstride = a.nb * a.rank + 16;
+  if (t.colsum_out && mode == kBoth && t.do_gw) {
+    a.groups = (a.total_blocks + a.nb - 1) / a.nb;
+    a.cs_part = t.colsum_ws;
+    a.cs_out = t.colsum_out;
+  }
   if (t.dtype == kBF16)
     launch_modes<__nv_bfloat16>(map, a, mode, t.do_gx, t.do_gw, stream);
   else
     launch_modes<float>(map, a, mode, t.do_gx, t.do_gw, stream);
+  if (t.colsum_out && !a.cs_out) launch_colsum(t, stream);
+}
+
+size_t transform_colsum_ws(int64_t segs, int64_t rows, int64_t cols, uint32_t bitmap) {
+  if (segs <= 0 || rows <= 0 || cols <= 0) return 0;
+  const int64_t total_blocks = segs * ((rows + 15) / 16);
+  if (total_blocks >= (int64_t(1) << 30) || cols >= (int64_t(1) << 30)) return 0;
+  const int nb = choose_nb(int(total_blocks), int(cols), __builtin_popcount(bitmap));
+  return size_t((total_blocks + nb - 1) / nb) * size_t(cols) * sizeof(float);
 }
 
 }  // namespace hlq

@@ -120,9 +120,11 @@ class HLQLinearFunction(torch.autograd.Function):
         if ctx.needs_input_grad[0] and ctx.needs_input_grad[1] and dual_ok(B, L, axis):
             # one fused transform of gy feeds both products (2 reads of gy instead of 4)
             segs, rows, cols, ld_src, seg_src = _proj_view(B, L, O, axis)
-            cgx, sgx, cg, kg, sg, _ = ops.quant_dual(gy3, segs, rows, cols,
-                                                     strategy.plan.gpu_bitmap(), bits_gx, bits_gw,
-                                                     ld_src, seg_src)
+            want_gb = has_bias and ctx.needs_input_grad[2]
+            # the bias gradient (column sums of gy) comes out of the same kernel's STATS pass
+            cgx, sgx, cg, kg, sg, _, *cs = ops.quant_dual(gy3, segs, rows, cols,
+                                                          strategy.plan.gpu_bitmap(), bits_gx, bits_gw,
+                                                          ld_src, seg_src, colsum=want_gb)
             cw, sw = cw_saved, sw_saved
             # the two products are independent: dW on the side stream, dX here
             main = torch.cuda.current_stream()
@@ -147,8 +149,8 @@ class HLQLinearFunction(torch.autograd.Function):
             if weight.dtype != torch.float32:
                 gw = gw.to(weight.dtype)
             gx = gx.reshape(x_shape).to(x_dtype)
-            if has_bias and ctx.needs_input_grad[2]:
-                gb = gy.reshape(-1, O).sum(0, dtype=torch.float32)
+            if want_gb:
+                gb = cs[0]
             return gx, gw, gb, None, None, None
         if ctx.needs_input_grad[1]:
             bits = strategy.grad_weight_path.bits or 8

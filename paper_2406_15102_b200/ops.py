@@ -124,10 +124,12 @@ def quant_ht_cols(src: torch.Tensor, bits: int):
 
 
 def quant_dual(src: torch.Tensor, segs: int, rows: int, cols: int, bitmap: int, bits_gx: int,
-               bits_gw: int, ld_src: int | None = None, seg_src: int | None = None):
+               bits_gw: int, ld_src: int | None = None, seg_src: int | None = None, colsum: bool = False):
     """Both gy operands from one read per pass: HT along cols (gx) and the
     rank-r projection along rows (gw).  Returns
-    (gx_codes (segs*rows, pad16(cols)), gx_scale, gw_codes (cols, pad16(K)), K, gw_scale, stats)."""
+    (gx_codes (segs*rows, pad16(cols)), gx_scale, gw_codes (cols, pad16(K)), K, gw_scale, stats)
+    and, with colsum, a 7th item: the fp32 column sums of src (cols,) -- the
+    bias gradient -- computed from the same tiles (hlq_quantize_dual_colsum)."""
     _check_bits(bits_gx)
     _check_bits(bits_gw)
     src = _cuda(src, "src")
@@ -141,12 +143,24 @@ def quant_dual(src: torch.Tensor, segs: int, rows: int, cols: int, bitmap: int, 
     scales = torch.empty(2, dtype=torch.float32, device=dev)
     stats = torch.empty(8, dtype=torch.int32, device=dev)
     nbytes = segs * rows * cols * src.element_size() + cgx.numel() + cols * k
-    _traced("transform", nbytes, 0, 1,
-            lambda: _lib.call("hlq_quantize_dual", _p(src), dtype_code(src), segs, rows, cols,
+    key = f"transform:dual:{segs * rows}x{cols}:{src.dtype}".replace("torch.", "")
+    if not colsum:
+        _traced("transform", nbytes, 0, 1,
+                lambda: _lib.call("hlq_quantize_dual", _p(src), dtype_code(src), segs, rows, cols,
+                                  ld_src, seg_src, bitmap, bits_gx, bits_gw, _p(stats), _p(cgx),
+                                  cgx.stride(0), _p(cgw), ldk, _p(scales), _p(scales[1:]), _stream()),
+                key=key)
+        return cgx, scales[0:1], cgw, k, scales[1:2], stats
+    cs = torch.empty(cols, dtype=torch.float32, device=dev)
+    wsb = int(_lib.load().hlq_quantize_dual_colsum_ws(segs, rows, cols, bitmap))
+    ws = torch.empty(max(wsb, 4), dtype=torch.uint8, device=dev)
+    _traced("transform", nbytes + cols * 4, 0, 1,
+            lambda: _lib.call("hlq_quantize_dual_colsum", _p(src), dtype_code(src), segs, rows, cols,
                               ld_src, seg_src, bitmap, bits_gx, bits_gw, _p(stats), _p(cgx),
-                              cgx.stride(0), _p(cgw), ldk, _p(scales), _p(scales[1:]), _stream()),
-            key=f"transform:dual:{segs * rows}x{cols}:{src.dtype}".replace("torch.", ""))
-    return cgx, scales[0:1], cgw, k, scales[1:2], stats
+                              cgx.stride(0), _p(cgw), ldk, _p(scales), _p(scales[1:]), _p(cs), _p(ws), wsb,
+                              _stream()),
+            key=key)
+    return cgx, scales[0:1], cgw, k, scales[1:2], stats, cs
 
 
 def transform_pass(src: torch.Tensor, segs: int, rows: int, cols: int, ld_src: int, seg_src: int,

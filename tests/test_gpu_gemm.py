@@ -150,3 +150,24 @@ def test_gemm_pair_matches_separate(ops, fuse, monkeypatch):
     rw, _ = ops.gemm_i8(cg, xp, O, I, K, 8, 8, s[0], s[1], 1.0, exact=False)
     rx, _ = ops.gemm_i8(cgx, cw, T, I, O, 4, 4, s[2], s[3], 1.0, exact=False, out_dtype=torch.bfloat16)
     assert torch.equal(gw, rw) and torch.equal(gx, rx)
+
+
+@pytest.mark.parametrize("B,L,O,dt", [(128, 197, 768, torch.bfloat16), (4, 197, 3072, torch.bfloat16),
+                                      (64, 1, 72, torch.float32), (3, 37, 20, torch.float32),
+                                      (5, 40, 36, torch.bfloat16)])
+def test_dual_column_sums(ops, B, L, O, dt):
+    """The bias gradient fused into the dual transform's STATS pass: fp32 column
+    sums of gy (TMA path, and the plain kernel when no tensor map fits: O*2 % 16
+    != 0), deterministic, codes unchanged by the extra output."""
+    torch.manual_seed(0)
+    gy = torch.randn(B, L, O, device="cuda").to(dt)
+    segs, rows = (B, L) if L >= 16 else (1, B)
+    base = ops.quant_dual(gy, segs, rows, O, 0x5555, 4, 8, O, L * O)
+    r1 = ops.quant_dual(gy, segs, rows, O, 0x5555, 4, 8, O, L * O, colsum=True)
+    r2 = ops.quant_dual(gy, segs, rows, O, 0x5555, 4, 8, O, L * O, colsum=True)
+    ref = gy.double().reshape(-1, O).sum(0)
+    assert torch.allclose(r1[6].double(), ref, rtol=1e-5, atol=1e-5 * gy.abs().max().item())
+    assert torch.equal(r1[6], r2[6])  # fixed reduction order
+    k = r1[3]
+    assert torch.equal(r1[0], base[0]) and torch.equal(r1[2][:, :k], base[2][:, :k])
+    assert torch.equal(r1[1], base[1]) and torch.equal(r1[4], base[4])
