@@ -36,9 +36,10 @@
 #define HLQ_API
 #endif
 
-/* Device scratch the single-call quantizers need for their statistics and the
- * fused kernel's grid barrier (zeroed by the library on the caller's stream). */
-#define HLQ_STATS_WS_BYTES 32
+/* Device scratch the single-call quantizers need for their statistics, the
+ * fused kernel's grid barrier and its work-ticket counters, each on its own
+ * 128-byte line (zeroed by the library on the caller's stream). */
+#define HLQ_STATS_WS_BYTES 512
 
 #ifdef __cplusplus
 extern "C" {
@@ -76,8 +77,8 @@ HLQ_API int hlq_device_ok(void);
  * Replaces `_block_axis(gy, 2, plan)` + `quant_pseudo_stochastic` on the gx
  * left operand (backprop.py:212-220,362,367; quantize.py:128-145).
  * Writes codes (rows x pad16(cols), leading dim ld_dst >= pad16(cols), a
- * multiple of 16) and the fp32 scale.  stats_ws: HLQ_STATS_WS_BYTES (32-byte,
- * 8 x uint32) device scratch; on return stats_ws[0] holds the bits of max|4v| (>= 0x7F800000
+ * multiple of 16) and the fp32 scale.  stats_ws: HLQ_STATS_WS_BYTES device
+ * scratch; on return stats_ws[0] holds the bits of max|4v| (>= 0x7F800000
  * means a NaN/Inf was present, the reference's ValueError).  bits in {4, 8}. */
 HLQ_API int hlq_quantize_ht_cols(const void* src, int dtype, int64_t rows, int64_t cols, int64_t ld_src,
                          int bits, uint32_t* stats_ws, int8_t* dst, int64_t ld_dst,

@@ -17,7 +17,8 @@ int num_sms();
 // codes transposed into dst_gw[col * ld_gw + (seg * nblk + blk) * rank + j].
 // stats: {amax_gx, ~minnz_gx, amax_gw, ~minnz_gw} (uint32 bits, max-reduced;
 // zero-initialised by the caller before the STATS pass; kBoth also uses
-// stats[4] as its grid-barrier counter, zero-initialised likewise).  When only do_gw is
+// stats[32] as its grid-barrier counter and stats[64] / stats[96] as its
+// per-pass work tickets -- one 128-byte line each -- zero-initialised likewise).  When only do_gw is
 // set the gw statistics still live at stats[2..3].
 struct TransformArgs {
   const void* src;

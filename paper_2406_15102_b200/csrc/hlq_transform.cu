@@ -91,6 +91,9 @@ struct Args {
   float* scale_gx;
   float* scale_gw;
   int cstride;  // bytes per column in the code staging buffer
+#ifdef HLQ_TR_TRACE
+  unsigned long long* trace;  // per CTA: 8 globaltimer stamps (development timeline)
+#endif
   // conv ACBP (taps > 0): the source is channels-last x read by im2col-mode TMA,
   // one 16-output-pixel block x 256 channels per step and tap; segments =
   // images, rows = output pixels l = ho*Wo + wo, payload row = c*taps + tap
@@ -107,18 +110,24 @@ struct Args {
 // ord runs over this CTA's ordinals blockIdx.x, +gridDim.x, ...; item = ord, or
 // items-1-ord for the reversed second pass of the fused kernel (the last items
 // of pass 1 are the ones still in L2 when pass 2 starts).
+//
+// Dynamic mode (the fused kBoth kernel): the producer takes items from a
+// global ticket counter (ctr) instead -- CTAs sharing an SM, L2 hit rates and
+// the item count per CTA all vary, and a static split left the slowest CTA
+// 25 % behind the median in each pass -- and tells the consumers which
+// (item, block) each ring slot holds (at()).
 struct StepIter {
   int ord, item, bl, nbl, gb0, col0, s, blk, tap;
   bool rev;
-  __device__ __forceinline__ void begin(const Args& a, bool reverse) {
+  uint32_t* ctr;  // non-null: dynamic tickets
+  __device__ __forceinline__ void begin(const Args& a, bool reverse, uint32_t* ticket_ctr = nullptr) {
     rev = reverse;
-    ord = blockIdx.x;
+    ctr = ticket_ctr;
+    ord = ctr ? int(atomicAdd(ctr, 1u)) : int(blockIdx.x);
     start(a);
   }
-  __device__ __forceinline__ bool valid(const Args& a) const { return ord < a.items; }
-  __device__ __forceinline__ void start(const Args& a) {
-    if (ord >= a.items) return;
-    item = rev ? a.items - 1 - ord : ord;
+  __device__ __forceinline__ void setup(const Args& a, int i) {
+    item = i;
     int rest = item;
     tap = 0;
     if (a.taps) {  // taps innermost: concurrent CTAs reuse the same x pixels through L2
@@ -129,13 +138,26 @@ struct StepIter {
     col0 = (rest - g * a.ncol_tiles) * kCols;
     gb0 = g * a.nb;
     nbl = min(a.nb, a.total_blocks - gb0);
+  }
+  // consumer side of the dynamic mode: block `b` of item `i`
+  __device__ __forceinline__ void at(const Args& a, int i, int b) {
+    ord = 0;
+    setup(a, i);
+    bl = b;
+    s = (gb0 + b) / a.nblk;
+    blk = gb0 + b - s * a.nblk;
+  }
+  __device__ __forceinline__ bool valid(const Args& a) const { return ord < a.items; }
+  __device__ __forceinline__ void start(const Args& a) {
+    if (ord >= a.items) return;
+    setup(a, rev ? a.items - 1 - ord : ord);
     bl = 0;
     s = gb0 / a.nblk;
     blk = gb0 - s * a.nblk;
   }
   __device__ __forceinline__ void next(const Args& a) {
     if (++bl == nbl) {
-      ord += gridDim.x;
+      ord = ctr ? int(atomicAdd(ctr, 1u)) : ord + int(gridDim.x);
       start(a);
     } else if (++blk == a.nblk) {
       blk = 0;
@@ -175,11 +197,11 @@ __device__ __forceinline__ void read16x2(uint32_t pa, uint32_t pb, float2 (&p)[1
   }
 }
 
-template <typename T, int MODE, bool GX, bool GW, int BM, bool FX, bool FW>
+template <typename T, int MODE, bool GX, bool GW, int BM, bool FX, bool FW, bool DYN>
 __device__ __forceinline__ void consume(const Args& a, const Quant& qx, const Quant& qw,
                                         uint8_t* tiles, uint64_t* full, uint64_t* empty,
-                                        uint8_t* cbuf, Stat& sx, Stat& sw, int& slot,
-                                        uint32_t& phase, bool reverse) {
+                                        const volatile int* meta, uint8_t* cbuf, Stat& sx, Stat& sw,
+                                        int& slot, uint32_t& phase, bool reverse) {
   constexpr int kRow = Tr<T>::kRow;
   const uint32_t bitmap = BM ? uint32_t(BM) : a.bitmap;
   const int rank = BM ? __builtin_popcount(uint32_t(BM)) : a.rank;
@@ -189,11 +211,21 @@ __device__ __forceinline__ void consume(const Args& a, const Quant& qx, const Qu
   const int ftid = tid;
   constexpr int kFlushThreads = kConsumers;
   StepIter it;
-  it.begin(a, reverse);
+  if (!DYN) it.begin(a, reverse);
   float2 csum = make_float2(0.0f, 0.0f);
-  while (it.valid(a)) {
+  while (DYN || it.valid(a)) {
     {
       ptx::mbar_wait(&full[slot], phase);
+      if (DYN) {
+        const int m = meta[slot];
+        if (m < 0) {  // the producer found no more items for this pass
+          __syncwarp();
+          if (lane == 0) ptx::mbar_arrive(&empty[slot]);
+          if (++slot == kStages) { slot = 0; phase ^= 1; }
+          break;
+        }
+        it.at(a, m >> 5, m & 31);
+      }
       const uint32_t tile = ptx::smem_u32(tiles) + slot * (16 * kRow);
       const int rvalid = a.rows - it.blk * 16;  // rows of this block inside the segment
       // ---------------- phase 1: (row, 16-col block) pieces -> gx operand
@@ -362,15 +394,15 @@ __device__ __forceinline__ void consume(const Args& a, const Quant& qx, const Qu
       }
       asm volatile("bar.sync 1, %0;" ::"n"(kFlushThreads));
     }
-    it.next(a);
+    if (!DYN) it.next(a);
   }
 }
 
 // Quant-pass dispatch on the (grid-uniform) fast-division guard of each operand.
-template <typename T, bool GX, bool GW, int BM>
+template <typename T, bool GX, bool GW, int BM, bool DYN>
 __device__ __forceinline__ void consume_quant(const Args& a, uint8_t* tiles, uint64_t* full,
-                                              uint64_t* empty, uint8_t* cbuf, int& slot,
-                                              uint32_t& phase, bool reverse) {
+                                              uint64_t* empty, const volatile int* meta, uint8_t* cbuf,
+                                              int& slot, uint32_t& phase, bool reverse) {
   Quant qx{}, qw{};
   if (GX) qx = make_quant(a.stats, a.bits_gx);
   if (GW) qw = make_quant(a.stats + 2, a.bits_gw);
@@ -381,17 +413,21 @@ __device__ __forceinline__ void consume_quant(const Args& a, uint8_t* tiles, uin
   Stat sx, sw;
   const bool fx = !GX || qx.fast, fw = !GW || qw.fast;
   if (fx && fw)
-    consume<T, kQuant, GX, GW, BM, true, true>(a, qx, qw, tiles, full, empty, cbuf, sx, sw, slot, phase, reverse);
+    consume<T, kQuant, GX, GW, BM, true, true, DYN>(a, qx, qw, tiles, full, empty, meta, cbuf, sx, sw, slot, phase,
+                                                   reverse);
   else if (fx)
-    consume<T, kQuant, GX, GW, BM, true, false>(a, qx, qw, tiles, full, empty, cbuf, sx, sw, slot, phase, reverse);
+    consume<T, kQuant, GX, GW, BM, true, false, DYN>(a, qx, qw, tiles, full, empty, meta, cbuf, sx, sw, slot, phase,
+                                                   reverse);
   else if (fw)
-    consume<T, kQuant, GX, GW, BM, false, true>(a, qx, qw, tiles, full, empty, cbuf, sx, sw, slot, phase, reverse);
+    consume<T, kQuant, GX, GW, BM, false, true, DYN>(a, qx, qw, tiles, full, empty, meta, cbuf, sx, sw, slot, phase,
+                                                   reverse);
   else
-    consume<T, kQuant, GX, GW, BM, false, false>(a, qx, qw, tiles, full, empty, cbuf, sx, sw, slot, phase, reverse);
+    consume<T, kQuant, GX, GW, BM, false, false, DYN>(a, qx, qw, tiles, full, empty, meta, cbuf, sx, sw, slot, phase,
+                                                   reverse);
 }
 
 // MODE kStats / kQuant: one pass.  MODE kBoth: both passes in one cooperative
-// launch -- statistics, a grid-wide barrier (a counter in stats[4]), then the
+// launch -- statistics, a grid-wide barrier (a counter in stats[32]), then the
 // quantization pass over the items in reverse order.  The producer warp never
 // waits for the barrier: it keeps streaming pass-2 tiles into the ring while
 // the consumers wait for the scales.
@@ -408,8 +444,26 @@ __global__ void __launch_bounds__(kThreads, HLQ_TR_MINB) tma_tile_kernel(const _
   bars += (8u - (ptx::smem_u32(bars) & 7u)) & 7u;
   uint64_t* full = reinterpret_cast<uint64_t*>(bars);
   uint64_t* empty = full + kStages;
+  int* meta = reinterpret_cast<int*>(empty + kStages);  // dynamic mode: item << 5 | block
+#ifdef HLQ_TR_STATIC
+  constexpr bool kDyn = false;  // A/B builds
+#else
+  constexpr bool kDyn = MODE == kBoth;
+#endif
 
   const int warp = threadIdx.x >> 5;
+#ifdef HLQ_TR_TRACE
+  auto stamp = [&](int i) {
+    if (threadIdx.x == 0) {
+      unsigned long long t;
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+      a.trace[blockIdx.x * 8 + i] = t;
+    }
+  };
+#else
+  auto stamp = [](int) {};
+#endif
+  stamp(0);
   if (threadIdx.x == 0) {
     for (int s = 0; s < kStages; ++s) {
       ptx::mbar_init(&full[s], 1);
@@ -427,9 +481,10 @@ __global__ void __launch_bounds__(kThreads, HLQ_TR_MINB) tma_tile_kernel(const _
       uint32_t phase = 0;
       for (int pass = 0; pass < (MODE == kBoth ? 2 : 1); ++pass) {
         StepIter it;
-        it.begin(a, pass == 1);
+        it.begin(a, pass == 1, kDyn ? a.stats + 64 + 32 * pass : nullptr);
         while (it.valid(a)) {
           ptx::mbar_wait_sleep(&empty[slot], phase ^ 1);
+          if (kDyn) meta[slot] = (it.item << 5) | it.bl;
           ptx::mbar_arrive_expect_tx(&full[slot], 16 * kRow);
           if (a.taps) {
             const int l0 = it.blk * 16, ho = l0 / a.wo_n, wo = l0 - ho * a.wo_n;
@@ -443,6 +498,12 @@ __global__ void __launch_bounds__(kThreads, HLQ_TR_MINB) tma_tile_kernel(const _
           if (++slot == kStages) { slot = 0; phase ^= 1; }
           it.next(a);
         }
+        if (kDyn) {  // end-of-pass sentinel slot
+          ptx::mbar_wait_sleep(&empty[slot], phase ^ 1);
+          meta[slot] = -1;
+          ptx::mbar_arrive(&full[slot]);
+          if (++slot == kStages) { slot = 0; phase ^= 1; }
+        }
       }
     }
     return;
@@ -451,35 +512,58 @@ __global__ void __launch_bounds__(kThreads, HLQ_TR_MINB) tma_tile_kernel(const _
   int slot = 0;
   uint32_t phase = 0;
   if (MODE == kQuant) {
-    consume_quant<T, GX, GW, BM>(a, tiles, full, empty, cbuf, slot, phase, false);
+    consume_quant<T, GX, GW, BM, false>(a, tiles, full, empty, meta, cbuf, slot, phase, false);
     return;
   }
   Stat sx, sw;
   {
     Quant dummy{};
-    consume<T, kStats, GX, GW, BM, true, true>(a, dummy, dummy, tiles, full, empty, cbuf, sx, sw, slot,
-                                               phase, false);
+    consume<T, kStats, GX, GW, BM, true, true, kDyn>(a, dummy, dummy, tiles, full, empty, meta, cbuf, sx, sw,
+                                                     slot, phase, false);
   }
+  stamp(1);
   sx.warp_reduce();
   sw.warp_reduce();
+  // CTA-level reduction first: one atomic per statistic per CTA (same-line
+  // atomics from every warp of every CTA queued up in front of the barrier)
+  __shared__ float red[kConsumers / 32][4];
   if ((threadIdx.x & 31) == 0) {
+    red[threadIdx.x >> 5][0] = sx.amax;
+    red[threadIdx.x >> 5][1] = sx.mnz;
+    red[threadIdx.x >> 5][2] = sw.amax;
+    red[threadIdx.x >> 5][3] = sw.mnz;
+  }
+  asm volatile("bar.sync 2, %0;" ::"n"(kConsumers) : "memory");
+  if (threadIdx.x == 0) {
+#pragma unroll
+    for (int w = 1; w < kConsumers / 32; ++w) {
+      asm("max.NaN.f32 %0, %0, %1;" : "+f"(sx.amax) : "f"(red[w][0]));
+      asm("min.f32 %0, %0, %1;" : "+f"(sx.mnz) : "f"(red[w][1]));
+      asm("max.NaN.f32 %0, %0, %1;" : "+f"(sw.amax) : "f"(red[w][2]));
+      asm("min.f32 %0, %0, %1;" : "+f"(sw.mnz) : "f"(red[w][3]));
+    }
     if (GX) sx.commit(a.stats);
     if (GW) sw.commit(a.stats + 2);
   }
   if (MODE == kStats) return;
   // ---------------- grid barrier (consumer threads only; all CTAs co-resident)
-  asm volatile("bar.sync 2, %0;" ::"n"(kConsumers) : "memory");
   if (threadIdx.x == 0) {
-    __threadfence();
-    atomicAdd(a.stats + 4, 1u);
+    // release-add, relaxed L2 polling (no L1 invalidation per probe), one
+    // acquire fence once every CTA has arrived
     uint32_t seen;
-    do {
-      asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(seen) : "l"(a.stats + 4) : "memory");
-      if (seen < gridDim.x) __nanosleep(64);
-    } while (seen < gridDim.x);
+    asm volatile("fence.acq_rel.gpu;\n\tatom.relaxed.gpu.global.add.u32 %0, [%1], 1;"
+                 : "=r"(seen) : "l"(a.stats + 32) : "memory");
+    ++seen;
+    while (seen < gridDim.x) {
+      __nanosleep(32);
+      asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];" : "=r"(seen) : "l"(a.stats + 32) : "memory");
+    }
+    asm volatile("fence.acq_rel.gpu;" ::: "memory");
   }
   asm volatile("bar.sync 2, %0;" ::"n"(kConsumers) : "memory");
-  consume_quant<T, GX, GW, BM>(a, tiles, full, empty, cbuf, slot, phase, true);
+  stamp(2);
+  consume_quant<T, GX, GW, BM, kDyn>(a, tiles, full, empty, meta, cbuf, slot, phase, true);
+  stamp(3);
   if (GW && a.cs_out) {
     // column sums: one warp per column, lanes over the column's contiguous
     // row-group partials (coalesced, 16 loads in flight per lane), fixed
@@ -505,13 +589,14 @@ __global__ void __launch_bounds__(kThreads, HLQ_TR_MINB) tma_tile_kernel(const _
       if (lane == 0) a.cs_out[c] = acc;
     }
   }
+  stamp(4);
 }
 
 template <typename T, int MODE, bool GX, bool GW, int BM>
 void launch_one(const CUtensorMap& map, Args a, cudaStream_t stream) {
   constexpr int kRow = Tr<T>::kRow;
   const size_t smem = 128 + size_t(kStages) * 16 * kRow +
-                      (GW && MODE != kStats ? size_t(kCols) * a.cstride : 0) + 8 + 2 * kStages * 8;
+                      (GW && MODE != kStats ? size_t(kCols) * a.cstride : 0) + 8 + 2 * kStages * 8 + kStages * 4;
   auto kern = tma_tile_kernel<T, MODE, GX, GW, BM>;
   static bool attr = false;
   if (!attr) {
@@ -522,6 +607,7 @@ void launch_one(const CUtensorMap& map, Args a, cudaStream_t stream) {
   if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kThreads, smem) != cudaSuccess ||
       per_sm < 1)
     per_sm = 1;
+  if (per_sm > 4) per_sm = 4;  // 5 resident CTAs measured no faster (more tail per item)
   if (const char* e = getenv("HLQ_TR_CTAS_PER_SM")) {  // development sweeps
     const int v = atoi(e);
     if (v >= 1 && v < per_sm) per_sm = v;
@@ -679,6 +765,10 @@ bool launch_conv_acbp_tma(const void* x, int dtype, int B, int H, int W, int C, 
   return true;
 }
 
+#ifdef HLQ_TR_TRACE
+unsigned long long* g_tr_trace = nullptr;
+#endif
+
 void launch_transform(const TransformArgs& t, int mode, cudaStream_t stream) {
   const size_t esz = t.dtype == kBF16 ? 2 : 4;
   const bool fits32 = t.rows < (int64_t(1) << 30) && t.cols < (int64_t(1) << 30) &&
@@ -725,6 +815,9 @@ void launch_transform(const TransformArgs& t, int mode, cudaStream_t stream) {
   a.scale_gx = t.scale_gx;
   a.scale_gw = t.scale_gw;
   a.cstride = a.nb * a.rank + 16;
+#ifdef HLQ_TR_TRACE
+  a.trace = g_tr_trace;
+#endif
   if (t.colsum_out && mode == kBoth && t.do_gw) {
     a.groups = (a.total_blocks + a.nb - 1) / a.nb;
     a.cs_part = t.colsum_ws;
@@ -746,3 +839,9 @@ size_t transform_colsum_ws(int64_t segs, int64_t rows, int64_t cols, uint32_t bi
 }
 
 }  // namespace hlq
+
+#ifdef HLQ_TR_TRACE
+extern "C" __attribute__((visibility("default"))) void hlq_debug_set_trace(unsigned long long* p) {
+  hlq::g_tr_trace = p;
+}
+#endif

@@ -15,6 +15,7 @@ from . import _lib
 from .errors import DimensionError, ParameterError
 
 QMAX = {4: 7, 8: 127}
+STATS_WORDS = 128  # HLQ_STATS_WS_BYTES / 4
 
 # ---------------------------------------------------------------------------
 # launch accounting / tracing (bench.py's gpu_launches and roofline inputs)
@@ -116,7 +117,7 @@ def quant_ht_cols(src: torch.Tensor, bits: int):
     ld = pad16(cols)
     codes = torch.empty((rows, ld), dtype=torch.int8, device=src.device)
     scale = torch.empty(1, dtype=torch.float32, device=src.device)
-    stats = torch.empty(8, dtype=torch.int32, device=src.device)
+    stats = torch.empty(STATS_WORDS, dtype=torch.int32, device=src.device)
     _traced("transform", rows * cols * src.element_size() + rows * ld, 0, 1,
             lambda: _lib.call("hlq_quantize_ht_cols", _p(src), dtype_code(src), rows, cols, cols,
                               bits, _p(stats), _p(codes), ld, _p(scale), _stream()))
@@ -141,7 +142,7 @@ def quant_dual(src: torch.Tensor, segs: int, rows: int, cols: int, bitmap: int, 
     cgx = torch.empty((segs * rows, pad16(cols)), dtype=torch.int8, device=dev)
     cgw = torch.empty((cols, ldk), dtype=torch.int8, device=dev)
     scales = torch.empty(2, dtype=torch.float32, device=dev)
-    stats = torch.empty(8, dtype=torch.int32, device=dev)
+    stats = torch.empty(STATS_WORDS, dtype=torch.int32, device=dev)
     nbytes = segs * rows * cols * src.element_size() + cgx.numel() + cols * k
     key = f"transform:dual:{segs * rows}x{cols}:{src.dtype}".replace("torch.", "")
     if not colsum:
@@ -194,7 +195,7 @@ def quant_proj_rows(src: torch.Tensor, segs: int, rows: int, cols: int, bitmap: 
     ld = max(pad16(k), 16)
     codes = torch.empty((cols, ld), dtype=torch.int8, device=src.device)
     scale = torch.empty(1, dtype=torch.float32, device=src.device)
-    stats = torch.empty(8, dtype=torch.int32, device=src.device)
+    stats = torch.empty(STATS_WORDS, dtype=torch.int32, device=src.device)
     _traced("transform", segs * rows * cols * src.element_size() + cols * k, 0, 1,
             lambda: _lib.call("hlq_quantize_proj_rows", _p(src), dtype_code(src), segs, rows, cols,
                               ld_src, seg_src, bitmap, bits, _p(stats), _p(codes), ld, _p(scale),
@@ -259,7 +260,7 @@ def quant_stochastic(src: torch.Tensor, segs: int, rows: int, cols: int, ld_src:
         ld = max(pad16(k), 16)
         codes = torch.empty((cols, ld), dtype=torch.int8, device=dev)
     scale = torch.empty(1, dtype=torch.float32, device=dev)
-    stats = torch.empty(8, dtype=torch.int32, device=dev)
+    stats = torch.empty(STATS_WORDS, dtype=torch.int32, device=dev)
     _traced("transform", segs * rows * cols * src.element_size() + codes.numel(), 0, 2,
             lambda: _lib.call("hlq_quantize_stochastic", _p(src), dtype_code(src), segs, rows, cols, ld_src,
                               seg_src, int(along_cols), bitmap, bits, int(seed), int(counter), index_kind, l2, o2,
@@ -314,7 +315,7 @@ def xform_quantize(src: torch.Tensor, segs: int, rows: int, cols: int, src_strid
         raise ParameterError("codes must be int8")
     v = _xview(src, segs, rows, cols, src_strides, bitmap, dst_strides, idx_strides)
     scale = torch.empty(1, dtype=torch.float32, device=src.device)
-    stats = torch.empty(8, dtype=torch.int32, device=src.device)
+    stats = torch.empty(STATS_WORDS, dtype=torch.int32, device=src.device)
     rounding = 0 if seed is None else 1
     _traced("transform", src.numel() * src.element_size() + dst.numel(), 0, 2,
             lambda: _lib.call("hlq_xform_quantize", ctypes.byref(v), bits, rounding, int(seed or 0),
@@ -445,7 +446,7 @@ def conv_acbp(x_nhwc: torch.Tensor, k: int, stride: int, pad: int, bitmap: int, 
     ld = max(pad16(kk), 16)
     codes = torch.empty((C * k * k, ld), dtype=torch.int8, device=x_nhwc.device)
     scale = torch.empty(1, dtype=torch.float32, device=x_nhwc.device)
-    stats = torch.empty(8, dtype=torch.int32, device=x_nhwc.device)
+    stats = torch.empty(STATS_WORDS, dtype=torch.int32, device=x_nhwc.device)
     nbytes = x_nhwc.numel() * x_nhwc.element_size() + C * k * k * kk
     _traced("transform", nbytes, 0, 2,
             lambda: _lib.call("hlq_conv_acbp_compress", _p(x_nhwc), dtype_code(x_nhwc), B, H, W, C, k,
