@@ -340,6 +340,8 @@ __device__ __forceinline__ void consume(const Args& a, const Quant& qx, const Qu
               }
             }
             }
+            // staged in smem, flushed per item as K-major runs (direct 8-byte
+            // global stores measured slower: 94 vs 80 us on the fc2-input ACBP)
             uint8_t* ox = cbuf + c * a.cstride + it.bl * rank;
             uint8_t* oy = ox + a.cstride;
             if (rank == 16) {
