@@ -299,15 +299,20 @@ def timed(torch, dist, fn):
 
 def graph_us(torch, fn, flush, reps=10):
     """Median device time (us) of fn captured in a CUDA graph (no host
-    overhead), L2 flushed (a 256 MB write) before every replay."""
+    overhead), L2 flushed before every replay: a 256 MB write, then a 160 MB
+    read of its start so the dirty lines are written back before the timed
+    region instead of during it (that write-back had added ~10 us to small
+    kernels)."""
     fn()
     torch.cuda.synchronize()
     g = torch.cuda.CUDAGraph()
     with torch.cuda.graph(g):
         fn()
     ts = []
+    head = flush[: 40 * 1024 * 1024]
     for _ in range(reps):
         flush.zero_()
+        head.sum()
         s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         s.record()
         g.replay()
@@ -399,9 +404,11 @@ def config_table(torch):
         xp, k, sx, _ = ops.quant_proj_rows(x.reshape(T, I), 1, T, I, bm, 8)
 
         def hlq_bwd():
+            # as HLQLinearFunction.backward runs it: one fused gy transform, then dW and
+            # dX as one hlq_gemm_i8_multi call
             cgx, sgx, cg, kg, sg, _ = ops.quant_dual(gy.reshape(T, O), 1, T, O, bm, 4, 8)
-            ops.gemm_i8(cg, xp, O, I, k, 8, 8, sg, sx, 1.0, exact=False)
-            ops.gemm_i8(cgx, cw, T, I, ops.pad16(O), 4, 4, sgx, sw, 1.0, exact=False)
+            ops.gemm_i8_pair(dict(a=cg, b=xp, m=O, n=I, k=k, bits_a=8, bits_b=8, sa=sg, sb=sx),
+                             dict(a=cgx, b=cw, m=T, n=I, k=ops.pad16(O), bits_a=4, bits_b=4, sa=sgx, sb=sw))
         h = graph_us(torch, hlq_bwd, flush)
         out[f"a_linear_4096x1024_fp32_r{rank}"] = {"hlq_us": round(h, 1), "dense_bf16_us": round(dense, 1),
                                                    "speedup": round(dense / h, 3), "K": k}

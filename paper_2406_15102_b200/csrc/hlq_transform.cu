@@ -111,11 +111,12 @@ struct Args {
 // items-1-ord for the reversed second pass of the fused kernel (the last items
 // of pass 1 are the ones still in L2 when pass 2 starts).
 //
-// Dynamic mode (the fused kBoth kernel): the producer takes items from a
-// global ticket counter (ctr) instead -- CTAs sharing an SM, L2 hit rates and
-// the item count per CTA all vary, and a static split left the slowest CTA
-// 25 % behind the median in each pass -- and tells the consumers which
-// (item, block) each ring slot holds (at()).
+// Dynamic mode (the fused kBoth kernel): each CTA's first item is static
+// (blockIdx.x), later ones come from a global ticket counter (ctr) -- CTAs
+// sharing an SM, L2 hit rates and the item count per CTA all vary, and a
+// static split left the slowest CTA 25 % behind the median in each pass --
+// and the producer tells the consumers which (item, block) each ring slot
+// holds (at()).
 struct StepIter {
   int ord, item, bl, nbl, gb0, col0, s, blk, tap;
   bool rev;
@@ -123,7 +124,7 @@ struct StepIter {
   __device__ __forceinline__ void begin(const Args& a, bool reverse, uint32_t* ticket_ctr = nullptr) {
     rev = reverse;
     ctr = ticket_ctr;
-    ord = ctr ? int(atomicAdd(ctr, 1u)) : int(blockIdx.x);
+    ord = int(blockIdx.x);  // first item static (a greedy first grab let early CTAs queue two)
     start(a);
   }
   __device__ __forceinline__ void setup(const Args& a, int i) {
@@ -157,7 +158,7 @@ struct StepIter {
   }
   __device__ __forceinline__ void next(const Args& a) {
     if (++bl == nbl) {
-      ord = ctr ? int(atomicAdd(ctr, 1u)) : ord + int(gridDim.x);
+      ord = ctr ? int(gridDim.x + atomicAdd(ctr, 1u)) : ord + int(gridDim.x);
       start(a);
     } else if (++blk == a.nblk) {
       blk = 0;

@@ -35,6 +35,7 @@ def timeit(fn, iters=20, warmup=3, flush=None):
     for _ in range(iters):
         if flush is not None:
             flush.zero_()
+            flush[: 40 * 1024 * 1024].sum()  # evict the dirty lines before timing
         s = torch.cuda.Event(enable_timing=True)
         e = torch.cuda.Event(enable_timing=True)
         s.record()

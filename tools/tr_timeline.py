@@ -41,6 +41,14 @@ def main():
     buf = torch.zeros(148 * 8 * 8, dtype=torch.int64, device="cuda")
     lib.hlq_debug_set_trace.argtypes = [ctypes.c_void_p]
     lib.hlq_debug_set_trace(ctypes.c_void_p(buf.data_ptr()))
+    if len(sys.argv) > 1 and sys.argv[1] == "config_a":
+        T = 4096
+        for bm in (0x0101, 0x5555):
+            gy = torch.randn(T, 1024, device="cuda") * 1e-3
+            run(f"config (a) dual fp32 bitmap {bm:#x}", lambda: ops.quant_dual(gy, 1, T, 1024, bm, 4, 8), buf)
+            x = torch.randn(T, 1024, device="cuda")
+            run(f"config (a) proj fp32 bitmap {bm:#x}", lambda: ops.quant_proj_rows(x, 1, T, 1024, bm, 8), buf)
+        return
     B, L = 128, 197
     for I in (768, 3072):
         x = torch.randn(B, L, I, device="cuda").to(torch.bfloat16)
