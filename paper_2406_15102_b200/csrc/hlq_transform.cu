@@ -71,12 +71,10 @@ struct Tr;
 template <>
 struct Tr<float> {
   static constexpr int kRow = kCols * 4;
-  static constexpr int kDtype = 2;
 };
 template <>
 struct Tr<__nv_bfloat16> {
   static constexpr int kRow = kCols * 2;
-  static constexpr int kDtype = 1;
 };
 
 struct Args {
