@@ -238,21 +238,62 @@ def make_model(torch, hlq: bool):
     return m
 
 
+_COPY = {}
+
+
 def train_steps(torch, model, opt, x, y, n, host=None):
+    """n training steps.  host=(pinned images, pinned labels): every step's
+    inputs are copied host->device and its loss is read back to the host; the
+    input copies are double-buffered on a copy stream, so step i+1's H2D
+    transfer runs under step i's compute (what a prefetching data loader does),
+    and step i's loss lands in pinned memory and is read by the host once step
+    i+1 has been enqueued (one-step-delayed logging), so the host never leaves
+    the GPU idle waiting on it."""
     F = torch.nn.functional
     loss = None
-    for _ in range(n):
+    losses, pending = [], None
+    if host is not None:
+        key = ("buf", x.data_ptr())
+        if key not in _COPY:  # one copy stream and one second input buffer, made once
+            _COPY[key] = (torch.cuda.Stream(), torch.empty_like(x), torch.empty_like(y))
+        cs, x2, y2 = _COPY[key]
+        bufs = [(x, y), (x2, y2)]
+        ready = [torch.cuda.Event(), torch.cuda.Event()]
+
+        def fetch(j):
+            bx, by = bufs[j % 2]
+            cs.wait_stream(torch.cuda.current_stream())  # the buffer's previous step is done
+            with torch.cuda.stream(cs):
+                bx.copy_(host[0], non_blocking=True)
+                by.copy_(host[1], non_blocking=True)
+                ready[j % 2].record(cs)
+        fetch(0)
+    for i in range(n):
+        cx, cy = x, y
         if host is not None:
-            x.copy_(host[0], non_blocking=True)
-            y.copy_(host[1], non_blocking=True)
+            torch.cuda.current_stream().wait_event(ready[i % 2])
+            cx, cy = bufs[i % 2]
+            if i + 1 < n:
+                fetch(i + 1)
         with torch.autocast("cuda", dtype=torch.bfloat16):
-            logits = model(x)
-        loss = F.cross_entropy(logits.float(), y)
+            logits = model(cx)
+        loss = F.cross_entropy(logits.float(), cy)
         loss.backward()
         opt.step()
         opt.zero_grad(set_to_none=True)
         if host is not None:
-            loss.item()  # D2H of the step's result
+            # D2H of this step's result; the host reads it after enqueuing the next step
+            lh = _COPY.setdefault(("loss", x.data_ptr()), torch.empty(2, dtype=torch.float32).pin_memory())
+            lh[i % 2: i % 2 + 1].copy_(loss.detach().reshape(1), non_blocking=True)
+            done = torch.cuda.Event()
+            done.record()
+            if i > 0:
+                pending.synchronize()
+                losses.append(float(lh[(i - 1) % 2]))
+            pending = done
+    if host is not None and n > 0:
+        pending.synchronize()
+        losses.append(float(lh[(n - 1) % 2]))
     return loss
 
 
@@ -575,6 +616,7 @@ def run_ours(args):
     hx = x.cpu().pin_memory()
     hy = y.cpu().pin_memory()
     e2e_steps = max(3, min(args.steps, 10))
+    train_steps(torch, model, opt, x, y, 2, host=(hx, hy))  # copy stream + second buffer, untimed
     ms_e2e = timed(torch, dist, lambda: train_steps(torch, model, opt, x, y, e2e_steps, host=(hx, hy)))
     e2e_value = world * B * e2e_steps / (ms_e2e * 1e-3)
 
@@ -620,7 +662,10 @@ def run_ours(args):
             "config": workload_config(args, world),
             "e2e": {"value": round(e2e_value, 2), "unit": "img/s",
                     "h2d_bytes_per_step": int(hx.numel() * hx.element_size() + hy.numel() * hy.element_size()),
-                    "d2h_bytes_per_step": 4},
+                    "d2h_bytes_per_step": 4,
+                    "pipeline": "inputs double-buffered on a copy stream (step i+1's H2D under step i); "
+                                "each step's loss copied to pinned host memory and read by the host after "
+                                "the next step is enqueued"},
             "roofline": roof,
             "gpu_launches": int(launches),
             "warmup_steps_run": int(warm_steps),
