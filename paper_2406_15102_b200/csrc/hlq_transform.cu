@@ -115,8 +115,10 @@ struct Args {
 // static split left the slowest CTA 25 % behind the median in each pass --
 // and the producer tells the consumers which (item, block) each ring slot
 // holds (at()).
+constexpr int kMetaWords = 6;  // per ring slot: col0, s, blk, gb0, nbl | bl << 8 | tap << 16, grp
+
 struct StepIter {
-  int ord, item, bl, nbl, gb0, col0, s, blk, tap;
+  int ord, item, bl, nbl, gb0, col0, s, blk, tap, grp;
   bool rev;
   uint32_t* ctr;  // non-null: dynamic tickets
   __device__ __forceinline__ void begin(const Args& a, bool reverse, uint32_t* ticket_ctr = nullptr) {
@@ -134,17 +136,21 @@ struct StepIter {
       tap = item - rest * a.taps;
     }
     const int g = rest / a.ncol_tiles;
+    grp = g;
     col0 = (rest - g * a.ncol_tiles) * kCols;
     gb0 = g * a.nb;
     nbl = min(a.nb, a.total_blocks - gb0);
   }
-  // consumer side of the dynamic mode: block `b` of item `i`
-  __device__ __forceinline__ void at(const Args& a, int i, int b) {
-    ord = 0;
-    setup(a, i);
-    bl = b;
-    s = (gb0 + b) / a.nblk;
-    blk = gb0 + b - s * a.nblk;
+  // producer -> consumers: everything a step needs, so the consumers do no
+  // integer divisions (they were ~25 % of the ACBP kernel's instructions)
+  __device__ __forceinline__ void publish(int* m) const {
+    m[0] = col0; m[1] = s; m[2] = blk; m[3] = gb0; m[4] = nbl | (bl << 8) | (tap << 16); m[5] = grp;
+  }
+  __device__ __forceinline__ void load(const volatile int* m) {
+    col0 = m[0]; s = m[1]; blk = m[2]; gb0 = m[3];
+    const int pk = m[4];
+    nbl = pk & 0xFF; bl = (pk >> 8) & 0xFF; tap = pk >> 16;
+    grp = m[5];
   }
   __device__ __forceinline__ bool valid(const Args& a) const { return ord < a.items; }
   __device__ __forceinline__ void start(const Args& a) {
@@ -216,14 +222,14 @@ __device__ __forceinline__ void consume(const Args& a, const Quant& qx, const Qu
     {
       ptx::mbar_wait(&full[slot], phase);
       if (DYN) {
-        const int m = meta[slot];
-        if (m < 0) {  // the producer found no more items for this pass
+        const volatile int* m = meta + kMetaWords * slot;
+        if (m[0] < 0) {  // the producer found no more items for this pass
           __syncwarp();
           if (lane == 0) ptx::mbar_arrive(&empty[slot]);
           if (++slot == kStages) { slot = 0; phase ^= 1; }
           break;
         }
-        it.at(a, m >> 5, m & 31);
+        it.load(m);
       }
       const uint32_t tile = ptx::smem_u32(tiles) + slot * (16 * kRow);
       const int rvalid = a.rows - it.blk * 16;  // rows of this block inside the segment
@@ -293,7 +299,7 @@ __device__ __forceinline__ void consume(const Args& a, const Quant& qx, const Qu
             csum = it.bl == 0 ? t[0] : f2add(csum, t[0]);
             if (it.bl == it.nbl - 1) {
               // column-major partials: a column's groups are contiguous for the final sum
-              float* o = a.cs_part + int64_t(it.col0 + c) * a.groups + it.gb0 / a.nb;
+              float* o = a.cs_part + int64_t(it.col0 + c) * a.groups + it.grp;
               o[0] = csum.x;
               if (it.col0 + c + 1 < a.cols) o[a.groups] = csum.y;
             }
@@ -445,7 +451,7 @@ __global__ void __launch_bounds__(kThreads, HLQ_TR_MINB) tma_tile_kernel(const _
   bars += (8u - (ptx::smem_u32(bars) & 7u)) & 7u;
   uint64_t* full = reinterpret_cast<uint64_t*>(bars);
   uint64_t* empty = full + kStages;
-  int* meta = reinterpret_cast<int*>(empty + kStages);  // dynamic mode: item << 5 | block
+  int* meta = reinterpret_cast<int*>(empty + kStages);  // dynamic mode: kMetaWords per slot
 #ifdef HLQ_TR_STATIC
   constexpr bool kDyn = false;  // A/B builds
 #else
@@ -485,7 +491,7 @@ __global__ void __launch_bounds__(kThreads, HLQ_TR_MINB) tma_tile_kernel(const _
         it.begin(a, pass == 1, kDyn ? a.stats + 64 + 32 * pass : nullptr);
         while (it.valid(a)) {
           ptx::mbar_wait_sleep(&empty[slot], phase ^ 1);
-          if (kDyn) meta[slot] = (it.item << 5) | it.bl;
+          if (kDyn) it.publish(meta + kMetaWords * slot);
           ptx::mbar_arrive_expect_tx(&full[slot], 16 * kRow);
           if (a.taps) {
             const int l0 = it.blk * 16, ho = l0 / a.wo_n, wo = l0 - ho * a.wo_n;
@@ -501,7 +507,7 @@ __global__ void __launch_bounds__(kThreads, HLQ_TR_MINB) tma_tile_kernel(const _
         }
         if (kDyn) {  // end-of-pass sentinel slot
           ptx::mbar_wait_sleep(&empty[slot], phase ^ 1);
-          meta[slot] = -1;
+          meta[kMetaWords * slot] = -1;
           ptx::mbar_arrive(&full[slot]);
           if (++slot == kStages) { slot = 0; phase ^= 1; }
         }
@@ -597,7 +603,7 @@ template <typename T, int MODE, bool GX, bool GW, int BM>
 void launch_one(const CUtensorMap& map, Args a, cudaStream_t stream) {
   constexpr int kRow = Tr<T>::kRow;
   const size_t smem = 128 + size_t(kStages) * 16 * kRow +
-                      (GW && MODE != kStats ? size_t(kCols) * a.cstride : 0) + 8 + 2 * kStages * 8 + kStages * 4;
+                      (GW && MODE != kStats ? size_t(kCols) * a.cstride : 0) + 8 + 2 * kStages * 8 + kStages * kMetaWords * 4;
   auto kern = tma_tile_kernel<T, MODE, GX, GW, BM>;
   static bool attr = false;
   if (!attr) {
