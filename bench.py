@@ -682,7 +682,9 @@ def run_ours(args):
         dopt = torch.optim.SGD(dmodel.parameters(), lr=1e-3, momentum=0.9, foreach=True)
         warmup(torch, lambda n: train_steps(torch, dmodel, dopt, x, y, n), args.warmup, dist, 2.0)
         dsteps = max(3, min(args.steps, 10))
-        dms = timed(torch, dist, lambda: train_steps(torch, dmodel, dopt, x, y, dsteps))
+        # best of two windows: the comparison arm is informational, so give it the benefit
+        # of any clock / power transient (single windows varied 38.7 - 43.4 ms across runs)
+        dms = min(timed(torch, dist, lambda: train_steps(torch, dmodel, dopt, x, y, dsteps)) for _ in range(2))
         if rank == 0:
             line["dense_bf16_train"] = {"value": round(world * B * dsteps / (dms * 1e-3), 2),
                                         "unit": "img/s", "ms_per_step": round(dms / dsteps, 3)}
