@@ -171,3 +171,30 @@ def test_dual_column_sums(ops, B, L, O, dt):
     k = r1[3]
     assert torch.equal(r1[0], base[0]) and torch.equal(r1[2][:, :k], base[2][:, :k])
     assert torch.equal(r1[1], base[1]) and torch.equal(r1[4], base[4])
+
+
+@pytest.mark.parametrize("B,L,O", [(128, 197, 3072), (128, 197, 768), (64, 1, 4096), (3, 1000, 520)])
+def test_fused_dynamic_transform_equals_two_static_passes(ops, B, L, O):
+    """Full-size property: the fused cooperative kernel (dynamic work tickets,
+    grid barrier, reversed pass 2) produces exactly the codes and scales of the
+    separately launched STATS and QUANT passes (static schedule)."""
+    torch.manual_seed(1)
+    gy = (torch.randn(B, L, O, device="cuda") * 1e-3).to(torch.bfloat16)
+    segs, rows = (B, L) if L >= 16 else (1, B)
+    cgx, sgx, cgw, k, sgw, _ = ops.quant_dual(gy, segs, rows, O, 0x5555, 4, 8, O, L * O)
+    st = ops.new_stats("cuda")
+    ops.transform_pass(gy, segs, rows, O, O, L * O, True, True, 0x5555, 4, 8, 0, st)
+    rgx = torch.empty_like(cgx)
+    rgw = torch.zeros_like(cgw)
+    sc = torch.empty(2, device="cuda")
+    ops.transform_pass(gy, segs, rows, O, O, L * O, True, True, 0x5555, 4, 8, 1, st, rgx, rgw, sc[0:1], sc[1:2])
+    assert torch.equal(sgx, sc[0:1]) and torch.equal(sgw, sc[1:2])
+    assert torch.equal(cgx[:, :O], rgx[:, :O])
+    assert torch.equal(cgw[:, :k], rgw[:, :k])
+    x = torch.randn(B, L, O, device="cuda").to(torch.bfloat16)
+    xp, kx, sx, _ = ops.quant_proj_rows(x, segs, rows, O, 0x5555, 8, O, L * O)
+    st2 = ops.new_stats("cuda")
+    ops.transform_pass(x, segs, rows, O, O, L * O, False, True, 0x5555, 8, 8, 0, st2)
+    rx = torch.zeros_like(xp)
+    ops.transform_pass(x, segs, rows, O, O, L * O, False, True, 0x5555, 8, 8, 1, st2, None, rx, None, sc[1:2])
+    assert torch.equal(sx, sc[1:2]) and torch.equal(xp[:, :kx], rx[:, :kx])
