@@ -70,7 +70,7 @@ def conv_acbp_compress(x: torch.Tensor, k: int, stride: int, pad: int, strategy:
 def _conv_backward(acbp: ACBPActivation, w4: torch.Tensor, gy: torch.Tensor, x_shape, stride: int,
                    pad: int, strategy: BackwardStrategy, extra: float, exact: bool, dx_dtype,
                    need_dx: bool = True, need_dw: bool = True, stages: dict | None = None,
-                   implicit: bool | None = None):
+                   implicit: bool | None = None, wcodes=None):
     """implicit (default: stride 1 and not exact): dX as one implicit GEMM over
     the taps (hlq_conv_dgrad_i8; taps summed in int32, matches the reference to
     fp32 rounding); otherwise the reference's lowering, GEMM -> dcols -> col2im
@@ -108,10 +108,14 @@ def _conv_backward(acbp: ACBPActivation, w4: torch.Tensor, gy: torch.Tensor, x_s
             stages.update(gw_codes_g=cg[:, :kg], gw_scale_g=sg, gw_acc=accw)
     if implicit is None:
         implicit = stride == 1 and not exact and pad <= k - 1
-    if need_dx and implicit:
+    if need_dx and (wcodes is not None and not want):
+        cw, sw = wcodes  # batched refresh (layers.refresh_weight_codes) for this weight version
+        kw = O
+    elif need_dx:
         w2 = w4.detach().reshape(O, I)
         w2 = w2 if w2.dtype == torch.float32 else w2.float()
         cw, kw, sw, _ = ops.quant_proj_rows(w2.contiguous(), 1, O, I, 0xFFFF, bits_gx)
+    if need_dx and implicit:
         dx_nhwc, accx = ops.conv_dgrad_i8(cgx, B, Ho, Wo, O, cw, C, k, pad, bits_gx, sgx, sw, exact=exact,
                                           out_dtype=dx_dtype, want_acc=want)
         dx = dx_nhwc.permute(0, 3, 1, 2)  # NCHW shape, channels_last memory
@@ -119,9 +123,6 @@ def _conv_backward(acbp: ACBPActivation, w4: torch.Tensor, gy: torch.Tensor, x_s
             stages.update(gx_codes_g=cgx, gx_scale_g=sgx, gx_codes_w=cw[:, :kw].t(), gx_scale_w=sw,
                           dx_acc=accx)
     elif need_dx:
-        w2 = w4.detach().reshape(O, I)
-        w2 = w2 if w2.dtype == torch.float32 else w2.float()
-        cw, kw, sw, _ = ops.quant_proj_rows(w2.contiguous(), 1, O, I, 0xFFFF, bits_gx)
         # fp32 dcols even for training: rounding every tap's partial to bf16 before the
         # col2im sum costs ~1.6e-3 relative error on dX, over the 1e-3 contract
         cols_dtype = torch.float32
@@ -164,9 +165,10 @@ def conv2d_hlq_backward(x: torch.Tensor, w4: torch.Tensor, gy: torch.Tensor, str
 
 class HLQConv2dFunction(torch.autograd.Function):
     @staticmethod
-    def forward(ctx, x, weight, bias, stride, pad, strategy: BackwardStrategy):
+    def forward(ctx, x, weight, bias, stride, pad, strategy: BackwardStrategy, wcodes=None):
         y = F.conv2d(x, weight.to(x.dtype), None if bias is None else bias.to(x.dtype),
                      stride=stride, padding=pad)
+        ctx.wcodes = wcodes if ctx.needs_input_grad[0] else None
         acbp = None
         if ctx.needs_input_grad[1]:
             acbp, _ = conv_acbp_compress(x.detach(), weight.shape[2], stride, pad, strategy)
@@ -186,20 +188,20 @@ class HLQConv2dFunction(torch.autograd.Function):
             # no weight gradient requested: dX only (dense path is the stock op)
             dx = torch.nn.grad.conv2d_input(x_shape, weight.to(gy.dtype), gy, stride=stride,
                                             padding=pad)
-            return dx, None, None, None, None, None
+            return dx, None, None, None, None, None, None
         axis, kk, orig = am
         acbp = ACBPActivation(QuantizedTensor(payload, strategy.grad_weight_path.bits or 8, sx), orig,
                               axis, strategy.plan, kk)
         out_dtype = x_dtype if x_dtype in (torch.float32, torch.bfloat16) else torch.float32
         dx, dw = _conv_backward(acbp, weight, gy, x_shape, stride, pad, strategy, 1.0, False,
-                                out_dtype, need_dx=ctx.needs_input_grad[0])
+                                out_dtype, need_dx=ctx.needs_input_grad[0], wcodes=ctx.wcodes)
         if dx is not None and dx.dtype != x_dtype:
             dx = dx.to(x_dtype)
         if weight.dtype != torch.float32:
             dw = dw.to(weight.dtype)
         if has_bias and ctx.needs_input_grad[2]:
             db = gy.sum(dim=(0, 2, 3), dtype=torch.float32)
-        return dx, dw, db, None, None, None
+        return dx, dw, db, None, None, None, None
 
 
 class HLQConv2d(nn.Conv2d):
@@ -214,6 +216,18 @@ class HLQConv2d(nn.Conv2d):
             raise ParameterError("HLQConv2d supports square kernels, equal int stride/padding, "
                                  "no dilation / groups (the reference Conv2d surface)")
         self.strategy = strategy or BackwardStrategy.hlq()
+        self._wcodes = None  # (weight version, data_ptr, bits, codes, scale); see refresh_weight_codes
+        self._hlq_weight_codes = True
+
+    def bits_gx(self) -> int:
+        return self.strategy.grad_input_path.bits or 4
+
+    def cached_weight_codes(self):
+        c = self._wcodes
+        w = self.weight
+        if c is not None and c[0] == w._version and c[1] == w.data_ptr() and c[2] == self.bits_gx():
+            return c[3], c[4]
+        return None
 
     def forward(self, x):
         if not (self.training and torch.is_grad_enabled()):
@@ -222,7 +236,7 @@ class HLQConv2d(nn.Conv2d):
             x = x.to(torch.get_autocast_dtype("cuda"))
         with torch.autocast("cuda", enabled=False):
             return HLQConv2dFunction.apply(x, self.weight, self.bias, self.stride[0], self.padding[0],
-                                           self.strategy)
+                                           self.strategy, self.cached_weight_codes())
 
     @classmethod
     def from_conv(cls, conv: nn.Conv2d, strategy: BackwardStrategy | None = None) -> "HLQConv2d":

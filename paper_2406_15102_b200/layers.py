@@ -213,6 +213,7 @@ class HLQLinear(nn.Linear):
         super().__init__(in_features, out_features, bias=bias, device=device, dtype=dtype)
         self.strategy = strategy or BackwardStrategy.hlq()
         self._wcodes = None  # (weight version, data_ptr, bits, codes, scale)
+        self._hlq_weight_codes = True  # refreshed in batch by refresh_weight_codes
 
     def bits_gx(self) -> int:
         return self.strategy.grad_input_path.bits or 4
@@ -299,12 +300,14 @@ def refresh_weight_codes(module: nn.Module) -> int:
     # the cache says (replays re-run the kernels, not this Python check)
     force = torch.cuda.is_available() and torch.cuda.is_current_stream_capturing()
     for m in module.modules():
-        if isinstance(m, HLQLinear) and m.weight.is_cuda and (force or m.cached_weight_codes() is None):
+        # HLQLinear and HLQConv2d (its weight viewed as (O, C*k*k), the dX operand's layout)
+        if getattr(m, "_hlq_weight_codes", False) and m.weight.is_cuda and \
+                (force or m.cached_weight_codes() is None):
             stale.setdefault(m.bits_gx(), []).append(m)
     n = 0
     for bits, mods in stale.items():
-        ws = [m.weight.detach() if m.weight.dtype == torch.float32 else m.weight.detach().float()
-              for m in mods]
+        ws = [(m.weight.detach() if m.weight.dtype == torch.float32 else m.weight.detach().float())
+              .reshape(m.weight.shape[0], -1) for m in mods]
         for m, (codes, scale) in zip(mods, ops.quant_weights(ws, bits)):
             m._wcodes = (m.weight._version, m.weight.data_ptr(), bits, codes, scale)
         n += len(mods)
