@@ -175,3 +175,38 @@ def test_training_path_conv_matches_oracle(conv, B, C, H, O, k, s, p):
     rdx, rdw = orc.conv2d_hlq_backward(x, w, gy, s, p, extra=1.0)
     assert np.linalg.norm(n(dx) - rdx) / np.linalg.norm(rdx) < 1e-5
     assert np.linalg.norm(n(dw) - rdw) / np.linalg.norm(rdw) < 1e-5
+
+
+def test_conv_uses_batched_weight_codes(conv):
+    """HLQConv2d weight codes come from the model-wide batched refresh
+    (layers.refresh_weight_codes) and give the same gradients bit for bit as
+    the per-layer transform (stride 1: implicit dgrad; stride 2: GEMM + col2im)."""
+    from paper_2406_15102_b200.layers import convert_linears, refresh_weight_codes
+    torch.manual_seed(0)
+    net = torch.nn.Sequential(torch.nn.Conv2d(16, 32, 3, padding=1), torch.nn.ReLU(),
+                              torch.nn.Conv2d(32, 32, 3, stride=2, padding=1)).to(DEV)
+    net = convert_linears(conv.convert_convs(net).to(memory_format=torch.channels_last))
+    x = torch.randn(8, 16, 16, 16, device=DEV).to(memory_format=torch.channels_last).requires_grad_(True)
+
+    def grads(batched):
+        for m in net:
+            if isinstance(m, conv.HLQConv2d):
+                m._wcodes = None
+        net._hlq_wcodes_hook = batched
+        x.grad = None
+        for p in net.parameters():
+            p.grad = None
+        if batched:
+            assert refresh_weight_codes(net) == 2
+        y = net(x) if batched else torch.nn.Sequential(*net)(x)
+        y.float().square().sum().backward()
+        return [x.grad.clone()] + [p.grad.clone() for p in net.parameters()]
+
+    a = grads(True)
+    assert all(m._wcodes is not None for m in net if isinstance(m, conv.HLQConv2d))
+    for m in net:
+        if isinstance(m, conv.HLQConv2d):
+            m._wcodes = None
+    b = grads(False)
+    for u, v in zip(a, b):
+        assert torch.equal(u, v)
