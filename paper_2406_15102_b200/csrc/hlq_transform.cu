@@ -96,6 +96,10 @@ struct Args {
   // one 16-output-pixel block x 256 channels per step and tap; segments =
   // images, rows = output pixels l = ho*Wo + wo, payload row = c*taps + tap
   int taps, kconv, cstr, cpad, wo_n;
+  // narrow conv inputs (C = 32 / 64 / 128): tq = 256 / C taps share one step,
+  // tap q of the group in columns [q*C, q*C + C) of the tile, stored as tq
+  // dense 16 x C sub-tiles (im2col boxes of C channels); tq = 1 otherwise
+  int tq, cch;
   // column sums of the source (the bias gradient), fused into the STATS pass of
   // kBoth: cs_part[g][c] = sum of column c over row group g (one work item's
   // rows), then a fixed-order reduction over g after pass 2 -> cs_out[c]
@@ -118,7 +122,7 @@ struct Args {
 constexpr int kMetaWords = 6;  // per ring slot: col0, s, blk, gb0, nbl | bl << 8 | tap << 16, grp
 
 struct StepIter {
-  int ord, item, bl, nbl, gb0, col0, s, blk, tap, grp;
+  int ord, item, bl, nbl, gb0, col0, s, blk, tap, grp, ntq;
   bool rev;
   uint32_t* ctr;  // non-null: dynamic tickets
   __device__ __forceinline__ void begin(const Args& a, bool reverse, uint32_t* ticket_ctr = nullptr) {
@@ -131,9 +135,12 @@ struct StepIter {
     item = i;
     int rest = item;
     tap = 0;
-    if (a.taps) {  // taps innermost: concurrent CTAs reuse the same x pixels through L2
-      rest = item / a.taps;
-      tap = item - rest * a.taps;
+    ntq = 1;
+    if (a.taps) {  // tap groups innermost: concurrent CTAs reuse the same x pixels through L2
+      const int ntg = (a.taps + a.tq - 1) / a.tq;
+      rest = item / ntg;
+      tap = (item - rest * ntg) * a.tq;
+      ntq = min(a.tq, a.taps - tap);
     }
     const int g = rest / a.ncol_tiles;
     grp = g;
@@ -144,12 +151,12 @@ struct StepIter {
   // producer -> consumers: everything a step needs, so the consumers do no
   // integer divisions (they were ~25 % of the ACBP kernel's instructions)
   __device__ __forceinline__ void publish(int* m) const {
-    m[0] = col0; m[1] = s; m[2] = blk; m[3] = gb0; m[4] = nbl | (bl << 8) | (tap << 16); m[5] = grp;
+    m[0] = col0; m[1] = s; m[2] = blk; m[3] = gb0; m[4] = nbl | (bl << 8) | (tap << 16) | (ntq << 24); m[5] = grp;
   }
   __device__ __forceinline__ void load(const volatile int* m) {
     col0 = m[0]; s = m[1]; blk = m[2]; gb0 = m[3];
     const int pk = m[4];
-    nbl = pk & 0xFF; bl = (pk >> 8) & 0xFF; tap = pk >> 16;
+    nbl = pk & 0xFF; bl = (pk >> 8) & 0xFF; tap = (pk >> 16) & 0xFF; ntq = (pk >> 24) & 0xFF;
     grp = m[5];
   }
   __device__ __forceinline__ bool valid(const Args& a) const { return ord < a.items; }
@@ -269,15 +276,20 @@ __device__ __forceinline__ void consume(const Args& a, const Quant& qx, const Qu
       // ---------------- phase 2: column pair -> gw operand (projection along rows)
       if (GW && p2) {
         const int c = 2 * tid;
-        if (it.col0 + c < a.cols) {
+        // tap-grouped tiles: column c is channel c % cch of tap (tap + c / cch)
+        const int q = a.tq > 1 ? c / a.cch : 0;
+        const uint32_t pitch = a.tq > 1 ? uint32_t(a.cch) * sizeof(T) : uint32_t(kRow);
+        const uint32_t col_addr = tile + (a.tq > 1 ? q * 16 * pitch + uint32_t(c - q * a.cch) * sizeof(T)
+                                                   : uint32_t(c) * sizeof(T));
+        if (a.tq > 1 ? q < it.ntq : it.col0 + c < a.cols) {
           float2 pv[16];
 #pragma unroll
           for (int i = 0; i < 16; ++i) {
             if (sizeof(T) == 2) {
-              const uint32_t w = ptx::lds32(tile + i * kRow + 2 * c);
+              const uint32_t w = ptx::lds32(col_addr + i * pitch);
               pv[i] = make_float2(bf_lo(w), bf_hi(w));
             } else {
-              const uint2 w = ptx::lds64(tile + i * kRow + 4 * c);
+              const uint2 w = ptx::lds64(col_addr + i * pitch);
               pv[i] = make_float2(__uint_as_float(w.x), __uint_as_float(w.y));
             }
           }
@@ -378,25 +390,33 @@ __device__ __forceinline__ void consume(const Args& a, const Quant& qx, const Qu
       const int run = it.nbl * rank;
       const int64_t k0 = int64_t(it.gb0) * rank;
       const int orow = a.taps ? a.taps : 1;  // payload row of column c: c (Linear) or c*taps + tap (conv)
-      const int ncols = min(kCols, a.cols - it.col0);
+      const int ncols = a.tq > 1 ? it.ntq * a.cch : min(kCols, a.cols - it.col0);
+      // payload row of tile column c (tap-grouped: channel c % cch, tap + c / cch)
+      auto prow = [&](int c) -> int64_t {
+        if (a.tq > 1) {
+          const int qq = c / a.cch;
+          return int64_t(c - qq * a.cch) * orow + it.tap + qq;
+        }
+        return int64_t(it.col0 + c) * orow + it.tap;
+      };
       if ((run & 15) == 0 && (k0 & 15) == 0) {
         const int chunks = run >> 4;
         for (int i = ftid; i < ncols * chunks; i += kFlushThreads) {
           const int c = i / chunks, q = i - c * chunks;
-          *reinterpret_cast<uint4*>(a.dst_gw + int64_t((it.col0 + c) * orow + it.tap) * a.ld_gw + k0 + 16 * q) =
+          *reinterpret_cast<uint4*>(a.dst_gw + prow(c) * a.ld_gw + k0 + 16 * q) =
               *reinterpret_cast<const uint4*>(cbuf + c * a.cstride + 16 * q);
         }
       } else if ((run & 7) == 0 && (k0 & 7) == 0) {
         const int chunks = run >> 3;
         for (int i = ftid; i < ncols * chunks; i += kFlushThreads) {
           const int c = i / chunks, q = i - c * chunks;
-          *reinterpret_cast<uint2*>(a.dst_gw + int64_t((it.col0 + c) * orow + it.tap) * a.ld_gw + k0 + 8 * q) =
+          *reinterpret_cast<uint2*>(a.dst_gw + prow(c) * a.ld_gw + k0 + 8 * q) =
               *reinterpret_cast<const uint2*>(cbuf + c * a.cstride + 8 * q);
         }
       } else {
         for (int i = ftid; i < ncols * run; i += kFlushThreads) {
           const int c = i / run, q = i - c * run;
-          a.dst_gw[int64_t((it.col0 + c) * orow + it.tap) * a.ld_gw + k0 + q] = int8_t(cbuf[c * a.cstride + q]);
+          a.dst_gw[prow(c) * a.ld_gw + k0 + q] = int8_t(cbuf[c * a.cstride + q]);
         }
       }
       asm volatile("bar.sync 1, %0;" ::"n"(kFlushThreads));
@@ -492,14 +512,18 @@ __global__ void __launch_bounds__(kThreads, HLQ_TR_MINB) tma_tile_kernel(const _
         while (it.valid(a)) {
           ptx::mbar_wait_sleep(&empty[slot], phase ^ 1);
           if (kDyn) it.publish(meta + kMetaWords * slot);
-          ptx::mbar_arrive_expect_tx(&full[slot], 16 * kRow);
           if (a.taps) {
             const int l0 = it.blk * 16, ho = l0 / a.wo_n, wo = l0 - ho * a.wo_n;
-            const int ti = it.tap / a.kconv, tj = it.tap - ti * a.kconv;
-            ptx::tma_load_im2col_4d(tiles + slot * 16 * kRow, &map, &full[slot], it.col0,
-                                    wo * a.cstr - a.cpad, ho * a.cstr - a.cpad, it.s, uint16_t(tj),
-                                    uint16_t(ti));
+            const uint32_t sub = a.tq > 1 ? uint32_t(16 * a.cch * sizeof(T)) : uint32_t(16 * kRow);
+            ptx::mbar_arrive_expect_tx(&full[slot], sub * uint32_t(it.ntq));
+            for (int q = 0; q < it.ntq; ++q) {
+              const int tp = it.tap + q, ti = tp / a.kconv, tj = tp - ti * a.kconv;
+              ptx::tma_load_im2col_4d(tiles + slot * 16 * kRow + q * sub, &map, &full[slot], it.col0,
+                                      wo * a.cstr - a.cpad, ho * a.cstr - a.cpad, it.s, uint16_t(tj),
+                                      uint16_t(ti));
+            }
           } else {
+            ptx::mbar_arrive_expect_tx(&full[slot], 16 * kRow);
             ptx::tma_load_3d(tiles + slot * 16 * kRow, &map, &full[slot], it.col0, it.blk * 16, it.s);
           }
           if (++slot == kStages) { slot = 0; phase ^= 1; }
@@ -728,6 +752,8 @@ bool launch_conv_acbp_tma(const void* x, int dtype, int B, int H, int W, int C, 
   if (!enc || (reinterpret_cast<uintptr_t>(x) % 16) || (size_t(C) * esz) % 16 || stride > 8 || pad > 127 ||
       k - 1 - pad > 127 || k > 16 || Ho * Wo < 16)
     return false;
+  // narrow inputs: several taps per 256-column step, one C-channel im2col box each
+  const int tq = (C == 32 || C == 64 || C == 128) && getenv("HLQ_CONV_NOGROUP") == nullptr ? kCols / C : 1;
   CUtensorMap map;
   const cuuint64_t dims[4] = {cuuint64_t(C), cuuint64_t(W), cuuint64_t(H), cuuint64_t(B)};
   const cuuint64_t strides[3] = {cuuint64_t(C) * esz, cuuint64_t(C) * esz * W, cuuint64_t(C) * esz * W * H};
@@ -735,7 +761,7 @@ bool launch_conv_acbp_tma(const void* x, int dtype, int B, int H, int W, int C, 
   const int upper[2] = {pad - (k - 1), pad - (k - 1)};
   const cuuint32_t es[4] = {1, cuuint32_t(stride), cuuint32_t(stride), 1};
   if (enc(&map, dtype == kBF16 ? CU_TENSOR_MAP_DATA_TYPE_BFLOAT16 : CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4,
-          const_cast<void*>(x), dims, strides, lower, upper, cuuint32_t(kCols), 16, es,
+          const_cast<void*>(x), dims, strides, lower, upper, cuuint32_t(tq > 1 ? C : kCols), 16, es,
           CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
           CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
     return false;
@@ -751,12 +777,15 @@ bool launch_conv_acbp_tma(const void* x, int dtype, int B, int H, int W, int C, 
   a.cpad = pad;
   a.wo_n = Wo;
   a.ncol_tiles = (C + kCols - 1) / kCols;
+  a.tq = tq;
+  a.cch = C;
+  const int ntg = (a.taps + tq - 1) / tq;  // tap groups per (pixel block, column tile)
   {
     int nb = a.rank >= 8 ? 4 : (a.rank >= 4 ? 8 : 16);
-    while (nb > 1 && ((a.total_blocks + nb - 1) / nb) * a.ncol_tiles * a.taps < num_sms() * 3) nb >>= 1;
+    while (nb > 1 && ((a.total_blocks + nb - 1) / nb) * a.ncol_tiles * ntg < num_sms() * 3) nb >>= 1;
     a.nb = nb;
   }
-  a.items = ((a.total_blocks + a.nb - 1) / a.nb) * a.ncol_tiles * a.taps;
+  a.items = ((a.total_blocks + a.nb - 1) / a.nb) * a.ncol_tiles * ntg;
   a.bitmap = bitmap;
   a.bits_gx = bits;
   a.bits_gw = bits;
@@ -808,6 +837,8 @@ void launch_transform(const TransformArgs& t, int mode, cudaStream_t stream) {
   a.nblk = int((t.rows + 15) / 16);
   a.total_blocks = int(t.segs) * a.nblk;
   a.rank = t.do_gw ? __builtin_popcount(t.bitmap) : 0;
+  a.tq = 1;
+  a.cch = kCols;
   a.nb = t.do_gw ? choose_nb(a.total_blocks, a.cols, a.rank) : 4;
   a.ncol_tiles = (a.cols + kCols - 1) / kCols;
   a.items = ((a.total_blocks + a.nb - 1) / a.nb) * a.ncol_tiles;

@@ -451,7 +451,8 @@ def conv_acbp(x_nhwc: torch.Tensor, k: int, stride: int, pad: int, bitmap: int, 
     _traced("transform", nbytes, 0, 2,
             lambda: _lib.call("hlq_conv_acbp_compress", _p(x_nhwc), dtype_code(x_nhwc), B, H, W, C, k,
                               stride, pad, bitmap, bits, _p(codes), ld, _p(scale), _p(stats),
-                              _stream()))
+                              _stream()),
+            key=f"transform:conv_acbp:{B}x{H}x{W}x{C}:k{k}s{stride}")
     return codes, kk, scale, stats[2:3]
 
 
@@ -469,7 +470,8 @@ def conv_dgrad_i8(gcodes: torch.Tensor, B: int, Ho: int, Wo: int, O: int, wcodes
                               wcodes.stride(0), C, k, 1, pad, bits, _p(sg), _p(sw),
                               _lib.HLQ_EPI_EXACT if exact else _lib.HLQ_EPI_FAST, _p(dx),
                               _lib.HLQ_BF16 if out_dtype == torch.bfloat16 else _lib.HLQ_F32, _p(acc),
-                              _stream()))
+                              _stream()),
+            key=f"gemm:conv_dgrad:{B}x{Ho}x{Wo}x{O}->{C}:k{k}")
     return dx, acc
 
 
