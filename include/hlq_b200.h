@@ -323,6 +323,12 @@ HLQ_API size_t hlq_quantize_weights_ws(int n);
 HLQ_API int hlq_quantize_weights(int n, const float* const* w, const int64_t* O, const int64_t* I,
                                  int bits, int8_t* const* codes, const int64_t* ld,
                                  float* const* scales, uint32_t* ws, size_t ws_bytes, void* stream);
+/* The same, also writing wbf16[i] (device, O_i x I_i row-major, may be a null
+ * array) = RN-to-bf16 copy of W_i from the statistics pass's read: the forward
+ * GEMM operand under bf16 autocast, without a separate cast per layer. */
+HLQ_API int hlq_quantize_weights_ex(int n, const float* const* w, const int64_t* O, const int64_t* I,
+                                    int bits, int8_t* const* codes, const int64_t* ld, float* const* scales,
+                                    void* const* wbf16, uint32_t* ws, size_t ws_bytes, void* stream);
 
 /* ---------------------------------------------------------------------------
  * ACBP container (acbp.py:3-212): the reference's bit-exact serialized form of

@@ -363,6 +363,12 @@ size_t hlq_quantize_weights_ws(int n) { return n < 0 ? 0 : size_t(8 * n + 8) * s
 int hlq_quantize_weights(int n, const float* const* w, const int64_t* O, const int64_t* I, int bits,
                          int8_t* const* codes, const int64_t* ld, float* const* scales, uint32_t* ws,
                          size_t ws_bytes, void* stream) {
+  return hlq_quantize_weights_ex(n, w, O, I, bits, codes, ld, scales, nullptr, ws, ws_bytes, stream);
+}
+
+int hlq_quantize_weights_ex(int n, const float* const* w, const int64_t* O, const int64_t* I, int bits,
+                            int8_t* const* codes, const int64_t* ld, float* const* scales, void* const* wbf16,
+                            uint32_t* ws, size_t ws_bytes, void* stream) {
   HLQ_TRY(check_bits(bits));
   if (n < 0 || n > hlq::kMaxWeights)
     return fail(HLQ_ERR_PARAMETER, "batched weight codes take 0..%d tensors, got %d", hlq::kMaxWeights, n);
@@ -377,7 +383,8 @@ int hlq_quantize_weights(int n, const float* const* w, const int64_t* O, const i
                   (long long)pad16(O[i]));
     if (reinterpret_cast<uintptr_t>(codes[i]) % 16) return fail(HLQ_ERR_PARAMETER, "codes %d not 16-byte aligned", i);
   }
-  int e = hlq::launch_weight_codes(n, w, O, I, bits, codes, ld, scales, ws, static_cast<cudaStream_t>(stream));
+  int e = hlq::launch_weight_codes(n, w, O, I, bits, codes, ld, scales, ws, static_cast<cudaStream_t>(stream),
+                                   wbf16);
   if (e != 0) return fail(HLQ_ERR_CUDA, "hlq_quantize_weights: %s", cudaGetErrorString(cudaError_t(e)));
   return cuda_status("hlq_quantize_weights");
 }

@@ -88,7 +88,7 @@ int launch_conv_dgrad_i8(const int8_t* G, int64_t ldg, int64_t B, int64_t Ho, in
 constexpr int kMaxWeights = 128;
 int launch_weight_codes(int n, const float* const* w, const int64_t* O, const int64_t* I, int bits,
                         int8_t* const* codes, const int64_t* ld, float* const* scales, uint32_t* ws,
-                        cudaStream_t stream);
+                        cudaStream_t stream, void* const* wbf16 = nullptr);
 // Two products in one CTA-pair launch (hlq_gemm_i8_multi).
 struct GemmDesc {
   const int8_t* A;

@@ -17,6 +17,7 @@
 // loads, the 16-point butterfly on f32x2 lanes, then statistics (pass 1) or
 // codes (pass 2, two 16-byte stores).  Pass 1 -> per-tensor atomic max ->
 // grid barrier -> pass 2.
+#include <cuda_bf16.h>
 #include <cuda_runtime.h>
 #include <cstdint>
 
@@ -34,6 +35,7 @@ constexpr int kColsPerItem = 2 * kThr;
 
 struct WDesc {
   const float* w;
+  __nv_bfloat16* wbf;  // optional bf16 copy of W (the forward GEMM's operand under autocast)
   int8_t* codes;
   float* scale;
   uint32_t* stats;  // 8 words per tensor: {amax, ~minnz, ...}
@@ -109,6 +111,12 @@ __global__ void __launch_bounds__(kThr) weight_codes_kernel(const __grid_constan
           const float* src = d.w + int64_t(o) * d.I + c;
           if (two && (reinterpret_cast<uintptr_t>(src) & 7) == 0) p[r] = __ldg(reinterpret_cast<const float2*>(src));
           else { p[r].x = __ldg(src); if (two) p[r].y = __ldg(src + 1); }
+          if (d.wbf) {  // the bf16 cast of W rides on the statistics pass's read
+            __nv_bfloat16* dst = d.wbf + int64_t(o) * d.I + c;
+            if (two && (reinterpret_cast<uintptr_t>(dst) & 3) == 0)
+              *reinterpret_cast<__nv_bfloat162*>(dst) = __floats2bfloat162_rn(p[r].x, p[r].y);
+            else { dst[0] = __float2bfloat16_rn(p[r].x); if (two) dst[1] = __float2bfloat16_rn(p[r].y); }
+          }
         }
       }
       fwht16_pair(p);
@@ -153,7 +161,7 @@ __global__ void __launch_bounds__(kThr) weight_codes_kernel(const __grid_constan
 
 int launch_weight_codes(int n, const float* const* w, const int64_t* O, const int64_t* I, int bits,
                         int8_t* const* codes, const int64_t* ld, float* const* scales, uint32_t* ws,
-                        cudaStream_t stream) {
+                        cudaStream_t stream, void* const* wbf16) {
   WBatch b{};
   b.n = n;
   b.bits = bits;
@@ -161,6 +169,7 @@ int launch_weight_codes(int n, const float* const* w, const int64_t* O, const in
   for (int i = 0; i < n; ++i) {
     WDesc& d = b.t[i];
     d.w = w[i];
+    d.wbf = wbf16 ? static_cast<__nv_bfloat16*>(wbf16[i]) : nullptr;
     d.codes = codes[i];
     d.scale = scales[i];
     d.stats = ws + 8 * i;

@@ -86,12 +86,17 @@ class HLQLinearFunction(torch.autograd.Function):
                 payload, k, sx, _ = ops.quant_proj_rows(x.detach().contiguous(), segs, rows, cols,
                                                         plan.gpu_bitmap(), bits_gw, ld_src, seg_src)
             if ctx.needs_input_grad[0] and wcodes is not None:
-                cw, sw = wcodes  # refreshed for this weight version by refresh_weight_codes
+                cw, sw = wcodes[0], wcodes[1]  # refreshed for this weight version by refresh_weight_codes
             elif ctx.needs_input_grad[0]:
                 w32 = weight.detach() if weight.dtype == torch.float32 else weight.detach().float()
                 cw, _, sw, _ = ops.quant_proj_rows(w32, 1, O, I, 0xFFFF, bits_gx)
-        y = F.linear(x, weight.to(x.dtype) if x.dtype != weight.dtype else weight,
-                     None if bias is None else bias.to(x.dtype))
+        if x.dtype == weight.dtype:
+            wx = weight
+        elif wcodes is not None and len(wcodes) > 2 and wcodes[2] is not None and x.dtype == torch.bfloat16:
+            wx = wcodes[2]  # bf16 copy written by the batched codes refresh (no per-layer cast)
+        else:
+            wx = weight.to(x.dtype)
+        y = F.linear(x, wx, None if bias is None else bias.to(x.dtype))
         main.wait_stream(side)
         for t in (payload, sx, cw, sw):
             if t is not None:
@@ -224,7 +229,7 @@ class HLQLinear(nn.Linear):
         c = self._wcodes
         w = self.weight
         if c is not None and c[0] == w._version and c[1] == w.data_ptr() and c[2] == self.bits_gx():
-            return c[3], c[4]
+            return c[3:]
         return None
 
     def forward(self, x):
@@ -308,8 +313,12 @@ def refresh_weight_codes(module: nn.Module) -> int:
     for bits, mods in stale.items():
         ws = [(m.weight.detach() if m.weight.dtype == torch.float32 else m.weight.detach().float())
               .reshape(m.weight.shape[0], -1) for m in mods]
-        for m, (codes, scale) in zip(mods, ops.quant_weights(ws, bits)):
-            m._wcodes = (m.weight._version, m.weight.data_ptr(), bits, codes, scale)
+        # Linear layers under autocast also take the bf16 weight for their forward GEMM
+        want_bf16 = torch.is_autocast_enabled("cuda") and torch.get_autocast_dtype("cuda") == torch.bfloat16 \
+            and os.environ.get("HLQ_WCODES_BF16", "1") != "0"
+        for m, res in zip(mods, ops.quant_weights(ws, bits, bf16=want_bf16)):
+            wbf = res[2] if want_bf16 and isinstance(m, HLQLinear) else None
+            m._wcodes = (m.weight._version, m.weight.data_ptr(), bits, res[0], res[1], wbf)
         n += len(mods)
     return n
 

@@ -204,10 +204,11 @@ def quant_proj_rows(src: torch.Tensor, segs: int, rows: int, cols: int, bitmap: 
     return codes, k, scale, stats[2:3]
 
 
-def quant_weights(weights, bits: int):
+def quant_weights(weights, bits: int, bf16: bool = False):
     """Q_bits(HT_O(W)) for a list of fp32 CUDA weights (O, I) in one launch.
     Returns [(codes (I, pad16(O)) int8, scale (1,) fp32)] -- the same as
-    quant_proj_rows(W, 1, O, I, 0xFFFF, bits)[0, 2] per tensor."""
+    quant_proj_rows(W, 1, O, I, 0xFFFF, bits)[0, 2] per tensor -- or, with
+    bf16, [(codes, scale, W as bf16 (O, I))] (the cast rides on the same read)."""
     _check_bits(bits)
     n = len(weights)
     if n == 0:
@@ -215,7 +216,7 @@ def quant_weights(weights, bits: int):
     if n > 128:
         out = []
         for i in range(0, n, 128):
-            out += quant_weights(weights[i:i + 128], bits)
+            out += quant_weights(weights[i:i + 128], bits, bf16)
         return out
     dev = weights[0].device
     ws_ = [_cuda(w, "weight") for w in weights]
@@ -223,6 +224,7 @@ def quant_weights(weights, bits: int):
         if w.dtype != torch.float32 or w.dim() != 2:
             raise ParameterError("batched weight codes take 2-D float32 weights")
     codes = [torch.empty((w.shape[1], pad16(w.shape[0])), dtype=torch.int8, device=dev) for w in ws_]
+    wbf = [torch.empty(w.shape, dtype=torch.bfloat16, device=dev) for w in ws_] if bf16 else None
     scales = torch.empty(n, dtype=torch.float32, device=dev)
     wsb = int(_lib.load().hlq_quantize_weights_ws(n))
     scratch = torch.empty(wsb, dtype=torch.uint8, device=dev)
@@ -231,14 +233,17 @@ def quant_weights(weights, bits: int):
     wp = P(*[w.data_ptr() for w in ws_])
     cp = P(*[c.data_ptr() for c in codes])
     sp = P(*[scales.data_ptr() + 4 * i for i in range(n)])
+    bp = P(*[b.data_ptr() for b in wbf]) if bf16 else None
     Os = I64(*[w.shape[0] for w in ws_])
     Is = I64(*[w.shape[1] for w in ws_])
     lds = I64(*[c.stride(0) for c in codes])
-    nbytes = sum(w.numel() * 4 + c.numel() for w, c in zip(ws_, codes))
+    nbytes = sum(w.numel() * 4 + c.numel() + (w.numel() * 2 if bf16 else 0) for w, c in zip(ws_, codes))
     _traced("transform", nbytes, 0, 1,
-            lambda: _lib.call("hlq_quantize_weights", n, wp, Os, Is, bits, cp, lds, sp, _p(scratch), wsb,
+            lambda: _lib.call("hlq_quantize_weights_ex", n, wp, Os, Is, bits, cp, lds, sp, bp, _p(scratch), wsb,
                               _stream()),
             key=f"transform:weights:{n}")
+    if bf16:
+        return [(c, scales[i:i + 1], wbf[i]) for i, c in enumerate(codes)]
     return [(c, scales[i:i + 1]) for i, c in enumerate(codes)]
 
 

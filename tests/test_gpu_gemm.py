@@ -198,3 +198,26 @@ def test_fused_dynamic_transform_equals_two_static_passes(ops, B, L, O):
     rx = torch.zeros_like(xp)
     ops.transform_pass(x, segs, rows, O, O, L * O, False, True, 0x5555, 8, 8, 1, st2, None, rx, None, sc[1:2])
     assert torch.equal(sx, sc[1:2]) and torch.equal(xp[:, :kx], rx[:, :kx])
+
+
+def test_autocast_forward_uses_refreshed_bf16_weights(ops):
+    """Under bf16 autocast the batched refresh also writes each Linear's bf16
+    weight (hlq_quantize_weights_ex); the forward GEMM then uses it instead of
+    a per-layer cast -- outputs and gradients bit-identical to the cast path."""
+    from paper_2406_15102_b200.layers import convert_linears
+
+    def run(batch):
+        torch.manual_seed(3)
+        net = convert_linears(torch.nn.Sequential(torch.nn.Linear(64, 96), torch.nn.GELU(),
+                                                  torch.nn.Linear(96, 40)).cuda(), batch_weight_codes=batch)
+        x = torch.randn(4, 33, 64, device="cuda", requires_grad=True)
+        with torch.autocast("cuda", dtype=torch.bfloat16):
+            y = net(x)
+        y.float().square().sum().backward()
+        if batch:
+            assert net[0]._wcodes[5] is not None and net[0]._wcodes[5].dtype == torch.bfloat16
+            assert torch.equal(net[0]._wcodes[5], net[0].weight.detach().to(torch.bfloat16))
+        return [y.detach(), x.grad] + [p.grad for p in net.parameters()]
+
+    for a, b in zip(run(True), run(False)):
+        assert torch.equal(a, b)
