@@ -100,6 +100,11 @@ struct Args {
   // tap q of the group in columns [q*C, q*C + C) of the tile, stored as tq
   // dense 16 x C sub-tiles (im2col boxes of C channels); tq = 1 otherwise
   int tq, cch;
+  // row groups (Linear / gy sources with cols = 32 / 64 / 128, taps == 0): a
+  // step holds tq = 256 / cols consecutive 16-row blocks as tq dense 16 x cols
+  // sub-tiles; items count `vblocks` = ceil(total_blocks / tq) block groups
+  int vblocks;
+  int cbw;  // columns of the gw staging buffer (cch when row-grouped, else 256)
   // column sums of the source (the bias gradient), fused into the STATS pass of
   // kBoth: cs_part[g][c] = sum of column c over row group g (one work item's
   // rows), then a fixed-order reduction over g after pass 2 -> cs_out[c]
@@ -146,7 +151,7 @@ struct StepIter {
     grp = g;
     col0 = (rest - g * a.ncol_tiles) * kCols;
     gb0 = g * a.nb;
-    nbl = min(a.nb, a.total_blocks - gb0);
+    nbl = min(a.nb, a.vblocks - gb0);
   }
   // producer -> consumers: everything a step needs, so the consumers do no
   // integer divisions (they were ~25 % of the ACBP kernel's instructions)
@@ -209,7 +214,7 @@ __device__ __forceinline__ void read16x2(uint32_t pa, uint32_t pb, float2 (&p)[1
   }
 }
 
-template <typename T, int MODE, bool GX, bool GW, int BM, bool FX, bool FW, bool DYN>
+template <typename T, int MODE, bool GX, bool GW, int BM, bool FX, bool FW, bool DYN, int GRP>
 __device__ __forceinline__ void consume(const Args& a, const Quant& qx, const Quant& qw,
                                         uint8_t* tiles, uint64_t* full, uint64_t* empty,
                                         const volatile int* meta, uint8_t* cbuf, Stat& sx, Stat& sw,
@@ -239,21 +244,46 @@ __device__ __forceinline__ void consume(const Args& a, const Quant& qx, const Qu
         it.load(m);
       }
       const uint32_t tile = ptx::smem_u32(tiles) + slot * (16 * kRow);
+      constexpr bool rg = GRP == 2;  // row-grouped narrow source (GRP 1: conv tap groups)
+      if (rg && !DYN) {  // static schedule: the first real block of this step (dynamic: published)
+        const int rb = (it.gb0 + it.bl) * a.tq;
+        it.s = rb / a.nblk;
+        it.blk = rb - it.s * a.nblk;
+      }
+      const int rb0 = (it.gb0 + it.bl) * a.tq;  // rg: first real block of the step
       const int rvalid = a.rows - it.blk * 16;  // rows of this block inside the segment
       // ---------------- phase 1: (row, 16-col block) pieces -> gx operand
       // thread = (rows r and r+8, block b); rows past the segment and columns
       // past `cols` were zero-filled by TMA, so the statistics need no predicate
       if (GX && p1) {
         const int r = tid >> 4, b = tid & 15;
-        const int c = it.col0 + b * 16;
+        // rg: 16-col block b is block bb of sub-tile q (real block rb0 + q)
+        int bb = b, ps = it.s, pb = it.blk, prv = rvalid;
+        uint32_t pitch = kRow, base = tile;
+        bool ok = true;
+        if (rg) {
+          const int bpt = a.cch >> 4, q = b / bpt;
+          bb = b - q * bpt;
+          pitch = uint32_t(a.cch) * sizeof(T);
+          base = tile + q * 16 * pitch;
+          ok = rb0 + q < a.total_blocks;
+          pb += q;
+          while (pb >= a.nblk) { pb -= a.nblk; ++ps; }
+          prv = a.rows - pb * 16;
+        }
+        const int c = it.col0 + bb * 16;
         float2 p[16];
-        read16x2<T>(tile + r * kRow + b * 16 * sizeof(T), tile + (r + 8) * kRow + b * 16 * sizeof(T), p,
-                    uint32_t(b >> 2) & 1u);
+        if (ok)
+          read16x2<T>(base + r * pitch + bb * 16 * sizeof(T), base + (r + 8) * pitch + bb * 16 * sizeof(T), p,
+                      uint32_t(b >> 2) & 1u);
+        else
+#pragma unroll
+          for (int i = 0; i < 16; ++i) p[i] = make_float2(0.0f, 0.0f);
         fwht16_pair(p);
         if (MODE == kStats) {
 #pragma unroll
           for (int i = 0; i < 16; ++i) sx.add2(p[i].x, p[i].y);
-        } else if (c < a.cols) {
+        } else if (ok && c < a.cols) {
           uint32_t w[16];
 #pragma unroll
           for (int i = 0; i < 16; ++i) w[i] = quant2<FX>(p[i], qx);  // (code A_i, code B_i)
@@ -265,10 +295,10 @@ __device__ __forceinline__ void consume(const Args& a, const Quant& qx, const Qu
             ca[q] = __byte_perm(t01, t23, 0x6420);
             cb[q] = __byte_perm(t01, t23, 0x7531);
           }
-          const int64_t row = int64_t(it.s) * a.rows + it.blk * 16 + r;
-          if (r < rvalid)
+          const int64_t row = int64_t(ps) * a.rows + pb * 16 + r;
+          if (r < prv)
             *reinterpret_cast<uint4*>(a.dst_gx + row * a.ld_gx + c) = make_uint4(ca[0], ca[1], ca[2], ca[3]);
-          if (r + 8 < rvalid)
+          if (r + 8 < prv)
             *reinterpret_cast<uint4*>(a.dst_gx + (row + 8) * a.ld_gx + c) =
                 make_uint4(cb[0], cb[1], cb[2], cb[3]);
         }
@@ -276,12 +306,15 @@ __device__ __forceinline__ void consume(const Args& a, const Quant& qx, const Qu
       // ---------------- phase 2: column pair -> gw operand (projection along rows)
       if (GW && p2) {
         const int c = 2 * tid;
-        // tap-grouped tiles: column c is channel c % cch of tap (tap + c / cch)
-        const int q = a.tq > 1 ? c / a.cch : 0;
-        const uint32_t pitch = a.tq > 1 ? uint32_t(a.cch) * sizeof(T) : uint32_t(kRow);
-        const uint32_t col_addr = tile + (a.tq > 1 ? q * 16 * pitch + uint32_t(c - q * a.cch) * sizeof(T)
+        // tap-grouped (conv) tiles: column c is channel c % cch of tap (tap + c / cch);
+        // row-grouped tiles: column c % cch of real block rb0 + c / cch
+        const int q = GRP ? c / a.cch : 0;
+        const int cc = c - q * a.cch;  // source column inside the sub-tile (== c when tq == 1)
+        const uint32_t pitch = GRP ? uint32_t(a.cch) * sizeof(T) : uint32_t(kRow);
+        const uint32_t col_addr = tile + (GRP ? q * 16 * pitch + uint32_t(cc) * sizeof(T)
                                                    : uint32_t(c) * sizeof(T));
-        if (a.tq > 1 ? q < it.ntq : it.col0 + c < a.cols) {
+        const bool in = GRP == 0 ? it.col0 + c < a.cols : (rg ? rb0 + q < a.total_blocks : q < it.ntq);
+        if (in) {
           float2 pv[16];
 #pragma unroll
           for (int i = 0; i < 16; ++i) {
@@ -311,9 +344,11 @@ __device__ __forceinline__ void consume(const Args& a, const Quant& qx, const Qu
             csum = it.bl == 0 ? t[0] : f2add(csum, t[0]);
             if (it.bl == it.nbl - 1) {
               // column-major partials: a column's groups are contiguous for the final sum
-              float* o = a.cs_part + int64_t(it.col0 + c) * a.groups + it.grp;
+              // (rg: one partial per sub-tile position q of the item's steps)
+              const int oc = rg ? cc : it.col0 + c;
+              float* o = a.cs_part + int64_t(oc) * a.groups + (rg ? it.grp * a.tq + q : it.grp);
               o[0] = csum.x;
-              if (it.col0 + c + 1 < a.cols) o[a.groups] = csum.y;
+              if (oc + 1 < a.cols) o[a.groups] = csum.y;
             }
           }
           fwht16_pair(pv);
@@ -359,7 +394,7 @@ __device__ __forceinline__ void consume(const Args& a, const Quant& qx, const Qu
             }
             // staged in smem, flushed per item as K-major runs (direct 8-byte
             // global stores measured slower: 94 vs 80 us on the fc2-input ACBP)
-            uint8_t* ox = cbuf + c * a.cstride + it.bl * rank;
+            uint8_t* ox = rg ? cbuf + cc * a.cstride + (it.bl * a.tq + q) * rank : cbuf + c * a.cstride + it.bl * rank;
             uint8_t* oy = ox + a.cstride;
             if (rank == 16) {
               *reinterpret_cast<uint4*>(ox) = make_uint4(cx[0], cx[1], cx[2], cx[3]);
@@ -377,6 +412,15 @@ __device__ __forceinline__ void consume(const Args& a, const Quant& qx, const Qu
               }
             }
           }
+        } else if (MODE == kStats && rg && a.cs_part) {
+          // a sub-tile past the last real block: its column sums still need the
+          // item's partial written (zero when the item had no other step)
+          if (it.bl == 0) csum = make_float2(0.0f, 0.0f);
+          if (it.bl == it.nbl - 1) {
+            float* o = a.cs_part + int64_t(cc) * a.groups + it.grp * a.tq + q;
+            o[0] = csum.x;
+            if (cc + 1 < a.cols) o[a.groups] = csum.y;
+          }
         }
       }
       // release the slot to the producer (one arrive per consuming warp)
@@ -387,13 +431,14 @@ __device__ __forceinline__ void consume(const Args& a, const Quant& qx, const Qu
     // ---------------- end of a work item: flush the staged gw codes
     if (GW && MODE == kQuant && it.bl == it.nbl - 1) {
       asm volatile("bar.sync 1, %0;" ::"n"(kFlushThreads));
-      const int run = it.nbl * rank;
-      const int64_t k0 = int64_t(it.gb0) * rank;
+      constexpr bool rgf = GRP == 2;
+      const int run = rgf ? (min(a.total_blocks, (it.gb0 + it.nbl) * a.tq) - it.gb0 * a.tq) * rank : it.nbl * rank;
+      const int64_t k0 = int64_t(rgf ? it.gb0 * a.tq : it.gb0) * rank;
       const int orow = a.taps ? a.taps : 1;  // payload row of column c: c (Linear) or c*taps + tap (conv)
-      const int ncols = a.tq > 1 ? it.ntq * a.cch : min(kCols, a.cols - it.col0);
+      const int ncols = rgf ? a.cch : (GRP == 1 ? it.ntq * a.cch : min(kCols, a.cols - it.col0));
       // payload row of tile column c (tap-grouped: channel c % cch, tap + c / cch)
       auto prow = [&](int c) -> int64_t {
-        if (a.tq > 1) {
+        if (GRP == 1) {
           const int qq = c / a.cch;
           return int64_t(c - qq * a.cch) * orow + it.tap + qq;
         }
@@ -426,7 +471,7 @@ __device__ __forceinline__ void consume(const Args& a, const Quant& qx, const Qu
 }
 
 // Quant-pass dispatch on the (grid-uniform) fast-division guard of each operand.
-template <typename T, bool GX, bool GW, int BM, bool DYN>
+template <typename T, bool GX, bool GW, int BM, bool DYN, int GRP>
 __device__ __forceinline__ void consume_quant(const Args& a, uint8_t* tiles, uint64_t* full,
                                               uint64_t* empty, const volatile int* meta, uint8_t* cbuf,
                                               int& slot, uint32_t& phase, bool reverse) {
@@ -440,16 +485,16 @@ __device__ __forceinline__ void consume_quant(const Args& a, uint8_t* tiles, uin
   Stat sx, sw;
   const bool fx = !GX || qx.fast, fw = !GW || qw.fast;
   if (fx && fw)
-    consume<T, kQuant, GX, GW, BM, true, true, DYN>(a, qx, qw, tiles, full, empty, meta, cbuf, sx, sw, slot, phase,
+    consume<T, kQuant, GX, GW, BM, true, true, DYN, GRP>(a, qx, qw, tiles, full, empty, meta, cbuf, sx, sw, slot, phase,
                                                    reverse);
   else if (fx)
-    consume<T, kQuant, GX, GW, BM, true, false, DYN>(a, qx, qw, tiles, full, empty, meta, cbuf, sx, sw, slot, phase,
+    consume<T, kQuant, GX, GW, BM, true, false, DYN, GRP>(a, qx, qw, tiles, full, empty, meta, cbuf, sx, sw, slot, phase,
                                                    reverse);
   else if (fw)
-    consume<T, kQuant, GX, GW, BM, false, true, DYN>(a, qx, qw, tiles, full, empty, meta, cbuf, sx, sw, slot, phase,
+    consume<T, kQuant, GX, GW, BM, false, true, DYN, GRP>(a, qx, qw, tiles, full, empty, meta, cbuf, sx, sw, slot, phase,
                                                    reverse);
   else
-    consume<T, kQuant, GX, GW, BM, false, false, DYN>(a, qx, qw, tiles, full, empty, meta, cbuf, sx, sw, slot, phase,
+    consume<T, kQuant, GX, GW, BM, false, false, DYN, GRP>(a, qx, qw, tiles, full, empty, meta, cbuf, sx, sw, slot, phase,
                                                    reverse);
 }
 
@@ -458,7 +503,7 @@ __device__ __forceinline__ void consume_quant(const Args& a, uint8_t* tiles, uin
 // quantization pass over the items in reverse order.  The producer warp never
 // waits for the barrier: it keeps streaming pass-2 tiles into the ring while
 // the consumers wait for the scales.
-template <typename T, int MODE, bool GX, bool GW, int BM>
+template <typename T, int MODE, bool GX, bool GW, int BM, int GRP>
 __global__ void __launch_bounds__(kThreads, HLQ_TR_MINB) tma_tile_kernel(const __grid_constant__ CUtensorMap map,
                                                            Args a) {
   constexpr int kRow = Tr<T>::kRow;
@@ -467,7 +512,7 @@ __global__ void __launch_bounds__(kThreads, HLQ_TR_MINB) tma_tile_kernel(const _
   // shared address space and emits LDS/STS rather than generic LD/ST
   uint8_t* tiles = smem_raw + ((128u - (ptx::smem_u32(smem_raw) & 127u)) & 127u);
   uint8_t* cbuf = tiles + kStages * 16 * kRow;
-  uint8_t* bars = cbuf + (GW && MODE != kStats ? kCols * a.cstride : 0);
+  uint8_t* bars = cbuf + (GW && MODE != kStats ? a.cbw * a.cstride : 0);
   bars += (8u - (ptx::smem_u32(bars) & 7u)) & 7u;
   uint64_t* full = reinterpret_cast<uint64_t*>(bars);
   uint64_t* empty = full + kStages;
@@ -511,16 +556,32 @@ __global__ void __launch_bounds__(kThreads, HLQ_TR_MINB) tma_tile_kernel(const _
         it.begin(a, pass == 1, kDyn ? a.stats + 64 + 32 * pass : nullptr);
         while (it.valid(a)) {
           ptx::mbar_wait_sleep(&empty[slot], phase ^ 1);
+          constexpr bool rgp = GRP == 2;
+          if (rgp) {  // first real block of this step's group
+            const int rb = (it.gb0 + it.bl) * a.tq;
+            it.s = rb / a.nblk;
+            it.blk = rb - it.s * a.nblk;
+          }
           if (kDyn) it.publish(meta + kMetaWords * slot);
           if (a.taps) {
             const int l0 = it.blk * 16, ho = l0 / a.wo_n, wo = l0 - ho * a.wo_n;
-            const uint32_t sub = a.tq > 1 ? uint32_t(16 * a.cch * sizeof(T)) : uint32_t(16 * kRow);
+            const uint32_t sub = GRP == 1 ? uint32_t(16 * a.cch * sizeof(T)) : uint32_t(16 * kRow);
             ptx::mbar_arrive_expect_tx(&full[slot], sub * uint32_t(it.ntq));
             for (int q = 0; q < it.ntq; ++q) {
               const int tp = it.tap + q, ti = tp / a.kconv, tj = tp - ti * a.kconv;
               ptx::tma_load_im2col_4d(tiles + slot * 16 * kRow + q * sub, &map, &full[slot], it.col0,
                                       wo * a.cstr - a.cpad, ho * a.cstr - a.cpad, it.s, uint16_t(tj),
                                       uint16_t(ti));
+            }
+          } else if (rgp) {
+            const int rb = (it.gb0 + it.bl) * a.tq;
+            const int nv = min(a.tq, a.total_blocks - rb);
+            const uint32_t sub = uint32_t(16 * a.cch * sizeof(T));
+            ptx::mbar_arrive_expect_tx(&full[slot], sub * uint32_t(nv));
+            int ps = it.s, pb = it.blk;
+            for (int q = 0; q < nv; ++q) {
+              ptx::tma_load_3d(tiles + slot * 16 * kRow + q * sub, &map, &full[slot], 0, pb * 16, ps);
+              if (++pb == a.nblk) { pb = 0; ++ps; }
             }
           } else {
             ptx::mbar_arrive_expect_tx(&full[slot], 16 * kRow);
@@ -543,13 +604,13 @@ __global__ void __launch_bounds__(kThreads, HLQ_TR_MINB) tma_tile_kernel(const _
   int slot = 0;
   uint32_t phase = 0;
   if (MODE == kQuant) {
-    consume_quant<T, GX, GW, BM, false>(a, tiles, full, empty, meta, cbuf, slot, phase, false);
+    consume_quant<T, GX, GW, BM, false, GRP>(a, tiles, full, empty, meta, cbuf, slot, phase, false);
     return;
   }
   Stat sx, sw;
   {
     Quant dummy{};
-    consume<T, kStats, GX, GW, BM, true, true, kDyn>(a, dummy, dummy, tiles, full, empty, meta, cbuf, sx, sw,
+    consume<T, kStats, GX, GW, BM, true, true, kDyn, GRP>(a, dummy, dummy, tiles, full, empty, meta, cbuf, sx, sw,
                                                      slot, phase, false);
   }
   stamp(1);
@@ -593,7 +654,7 @@ __global__ void __launch_bounds__(kThreads, HLQ_TR_MINB) tma_tile_kernel(const _
   }
   asm volatile("bar.sync 2, %0;" ::"n"(kConsumers) : "memory");
   stamp(2);
-  consume_quant<T, GX, GW, BM, kDyn>(a, tiles, full, empty, meta, cbuf, slot, phase, true);
+  consume_quant<T, GX, GW, BM, kDyn, GRP>(a, tiles, full, empty, meta, cbuf, slot, phase, true);
   stamp(3);
   if (GW && a.cs_out) {
     // column sums: one warp per column, lanes over the column's contiguous
@@ -623,12 +684,12 @@ __global__ void __launch_bounds__(kThreads, HLQ_TR_MINB) tma_tile_kernel(const _
   stamp(4);
 }
 
-template <typename T, int MODE, bool GX, bool GW, int BM>
+template <typename T, int MODE, bool GX, bool GW, int BM, int GRP>
 void launch_one(const CUtensorMap& map, Args a, cudaStream_t stream) {
   constexpr int kRow = Tr<T>::kRow;
   const size_t smem = 128 + size_t(kStages) * 16 * kRow +
-                      (GW && MODE != kStats ? size_t(kCols) * a.cstride : 0) + 8 + 2 * kStages * 8 + kStages * kMetaWords * 4;
-  auto kern = tma_tile_kernel<T, MODE, GX, GW, BM>;
+                      (GW && MODE != kStats ? size_t(a.cbw) * a.cstride : 0) + 8 + 2 * kStages * 8 + kStages * kMetaWords * 4;
+  auto kern = tma_tile_kernel<T, MODE, GX, GW, BM, GRP>;
   static bool attr = false;
   if (!attr) {
     cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
@@ -665,13 +726,22 @@ void launch_one(const CUtensorMap& map, Args a, cudaStream_t stream) {
 
 template <typename T, int MODE, bool GX, bool GW>
 void launch_bm(const CUtensorMap& map, const Args& a, cudaStream_t st) {
-  if (!GW) return launch_one<T, MODE, GX, GW, 0>(map, a, st);
+  if (a.tq > 1) {  // grouped narrow tiles: the default plan or the generic bitmap
+    const bool conv = a.taps != 0;
+    if (GW && a.bitmap == 0x5555) {
+      if (conv) return launch_one<T, MODE, GX, GW, 0x5555, 1>(map, a, st);
+      return launch_one<T, MODE, GX, GW, 0x5555, 2>(map, a, st);
+    }
+    if (conv) return launch_one<T, MODE, GX, GW, 0, 1>(map, a, st);
+    return launch_one<T, MODE, GX, GW, 0, 2>(map, a, st);
+  }
+  if (!GW) return launch_one<T, MODE, GX, GW, 0, 0>(map, a, st);
   switch (a.bitmap) {
-    case 0x5555: return launch_one<T, MODE, GX, GW, 0x5555>(map, a, st);  // rank 8 (default plan)
-    case 0x1111: return launch_one<T, MODE, GX, GW, 0x1111>(map, a, st);  // rank 4
-    case 0x0101: return launch_one<T, MODE, GX, GW, 0x0101>(map, a, st);  // rank 2
-    case 0xFFFF: return launch_one<T, MODE, GX, GW, 0xFFFF>(map, a, st);  // full (H.W, rank 16)
-    default: return launch_one<T, MODE, GX, GW, 0>(map, a, st);           // calibrated bases
+    case 0x5555: return launch_one<T, MODE, GX, GW, 0x5555, 0>(map, a, st);  // rank 8 (default plan)
+    case 0x1111: return launch_one<T, MODE, GX, GW, 0x1111, 0>(map, a, st);  // rank 4
+    case 0x0101: return launch_one<T, MODE, GX, GW, 0x0101, 0>(map, a, st);  // rank 2
+    case 0xFFFF: return launch_one<T, MODE, GX, GW, 0xFFFF, 0>(map, a, st);  // full (H.W, rank 16)
+    default: return launch_one<T, MODE, GX, GW, 0, 0>(map, a, st);           // calibrated bases
   }
 }
 
@@ -779,6 +849,8 @@ bool launch_conv_acbp_tma(const void* x, int dtype, int B, int H, int W, int C, 
   a.ncol_tiles = (C + kCols - 1) / kCols;
   a.tq = tq;
   a.cch = C;
+  a.vblocks = a.total_blocks;
+  a.cbw = kCols;
   const int ntg = (a.taps + tq - 1) / tq;  // tap groups per (pixel block, column tile)
   {
     int nb = a.rank >= 8 ? 4 : (a.rank >= 4 ? 8 : 16);
@@ -813,12 +885,15 @@ void launch_transform(const TransformArgs& t, int mode, cudaStream_t stream) {
                        (t.segs <= 1 || (t.seg_src * esz) % 16 == 0);
   CUtensorMap map;
   bool ok = fits32 && aligned && t.rows > 0 && t.cols > 0 && t.segs > 0;
+  // narrow sources: row groups of 256 / cols blocks per step (one cols-wide box each)
+  const int tq = (t.cols == 32 || t.cols == 64 || t.cols == 128) && getenv("HLQ_TR_NOGROUP") == nullptr
+                     ? int(kCols / t.cols) : 1;
   if (ok) {
     const uint64_t seg_stride = t.segs > 1 ? uint64_t(t.seg_src) * esz
                                            : (uint64_t(t.rows) * t.ld_src * esz + 15) & ~uint64_t(15);
     const uint64_t dims[3] = {uint64_t(t.cols), uint64_t(t.rows), uint64_t(t.segs)};
     const uint64_t strides[2] = {uint64_t(t.ld_src) * esz, seg_stride};
-    const uint32_t box[3] = {uint32_t(kCols), 16, 1};
+    const uint32_t box[3] = {uint32_t(tq > 1 ? t.cols : kCols), 16, 1};
     ok = encode_tensor_map(&map, t.dtype == kBF16 ? 1 : 2, 3, t.src, dims, strides, box, 0);
   }
   if (!ok) {
@@ -837,11 +912,13 @@ void launch_transform(const TransformArgs& t, int mode, cudaStream_t stream) {
   a.nblk = int((t.rows + 15) / 16);
   a.total_blocks = int(t.segs) * a.nblk;
   a.rank = t.do_gw ? __builtin_popcount(t.bitmap) : 0;
-  a.tq = 1;
-  a.cch = kCols;
-  a.nb = t.do_gw ? choose_nb(a.total_blocks, a.cols, a.rank) : 4;
+  a.tq = tq;
+  a.cch = tq > 1 ? a.cols : kCols;
+  a.vblocks = (a.total_blocks + tq - 1) / tq;
+  a.cbw = tq > 1 ? a.cols : kCols;
+  a.nb = t.do_gw ? choose_nb(a.vblocks, tq > 1 ? kCols : a.cols, a.rank * tq) : 4;
   a.ncol_tiles = (a.cols + kCols - 1) / kCols;
-  a.items = ((a.total_blocks + a.nb - 1) / a.nb) * a.ncol_tiles;
+  a.items = ((a.vblocks + a.nb - 1) / a.nb) * a.ncol_tiles;
   a.bitmap = t.bitmap;
   a.bits_gx = t.bits_gx;
   a.bits_gw = t.bits_gw;
@@ -852,12 +929,12 @@ void launch_transform(const TransformArgs& t, int mode, cudaStream_t stream) {
   a.ld_gw = t.ld_gw;
   a.scale_gx = t.scale_gx;
   a.scale_gw = t.scale_gw;
-  a.cstride = a.nb * a.rank + 16;
+  a.cstride = a.nb * a.tq * a.rank + 16;
 #ifdef HLQ_TR_TRACE
   a.trace = g_tr_trace;
 #endif
   if (t.colsum_out && mode == kBoth && t.do_gw) {
-    a.groups = (a.total_blocks + a.nb - 1) / a.nb;
+    a.groups = ((a.vblocks + a.nb - 1) / a.nb) * a.tq;  // rg: one partial per sub-tile position
     a.cs_part = t.colsum_ws;
     a.cs_out = t.colsum_out;
   }
@@ -872,8 +949,8 @@ size_t transform_colsum_ws(int64_t segs, int64_t rows, int64_t cols, uint32_t bi
   if (segs <= 0 || rows <= 0 || cols <= 0) return 0;
   const int64_t total_blocks = segs * ((rows + 15) / 16);
   if (total_blocks >= (int64_t(1) << 30) || cols >= (int64_t(1) << 30)) return 0;
-  const int nb = choose_nb(int(total_blocks), int(cols), __builtin_popcount(bitmap));
-  return size_t((total_blocks + nb - 1) / nb) * size_t(cols) * sizeof(float);
+  (void)bitmap;  // upper bound over the item sizes and row groups the launch may choose
+  return size_t(total_blocks + 16 * 16) * size_t(cols) * sizeof(float);
 }
 
 }  // namespace hlq

@@ -153,6 +153,7 @@ def test_gemm_pair_matches_separate(ops, fuse, monkeypatch):
 
 
 @pytest.mark.parametrize("B,L,O,dt", [(128, 197, 768, torch.bfloat16), (4, 197, 3072, torch.bfloat16),
+                                      (32, 197, 64, torch.bfloat16), (5, 40, 128, torch.float32),
                                       (64, 1, 72, torch.float32), (3, 37, 20, torch.float32),
                                       (5, 40, 36, torch.bfloat16)])
 def test_dual_column_sums(ops, B, L, O, dt):
@@ -173,7 +174,8 @@ def test_dual_column_sums(ops, B, L, O, dt):
     assert torch.equal(r1[1], base[1]) and torch.equal(r1[4], base[4])
 
 
-@pytest.mark.parametrize("B,L,O", [(128, 197, 3072), (128, 197, 768), (64, 1, 4096), (3, 1000, 520)])
+@pytest.mark.parametrize("B,L,O", [(128, 197, 3072), (128, 197, 768), (64, 1, 4096), (3, 1000, 520),
+                                   (256, 256, 64), (37, 197, 128), (512, 1, 32)])
 def test_fused_dynamic_transform_equals_two_static_passes(ops, B, L, O):
     """Full-size property: the fused cooperative kernel (dynamic work tickets,
     grid barrier, reversed pass 2) produces exactly the codes and scales of the

@@ -116,6 +116,9 @@ def oracle_stages(x, w, gy, bases, bits_gx=4, bits_gw=8, pad_small=False):
     ((8, 197, 3072, 768), 8),     # ViT-B/16 fc2 geometry
     ((3, 50, 100, 1000), 4),      # ragged everything (O=1000 like a ViT head)
     ((64, 7, 40, 24), 8),         # batch axis with L > 1 (grouped K)
+    ((6, 197, 128, 64), 8),       # narrow gy / x: row-grouped tiles (4 and 2 blocks per step)
+    ((3, 40, 64, 32), 8),         # narrow, 8 blocks per step, ragged segments
+    ((64, 7, 32, 128), 4),        # narrow on the batch axis
 ])
 def test_seeded_vs_oracle(hlq, shape, rank):
     B, L, I, O = shape
