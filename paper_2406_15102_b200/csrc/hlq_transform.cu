@@ -61,7 +61,10 @@ using namespace dev;
 constexpr int kCols = 256;       // columns per step
 constexpr int kConsumers = 128;  // 4 consumer warps
 constexpr int kThreads = kConsumers + 32;
-constexpr int kStages = 4;
+#ifndef HLQ_TR_STAGES
+#define HLQ_TR_STAGES 4
+#endif
+constexpr int kStages = HLQ_TR_STAGES;
 #ifndef HLQ_TR_MINB
 #define HLQ_TR_MINB 4  // CTAs per SM the register budget is sized for
 #endif
