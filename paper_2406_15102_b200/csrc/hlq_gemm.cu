@@ -979,9 +979,13 @@ int launch_gemm_i8_pair2(const GemmDesc* d, cudaStream_t stream) {
 }
 
 bool gemm_i8_pair2_eligible(const GemmDesc* d) {
+  static const int min_nk = [] {
+    const char* e = getenv("HLQ_GEMM_PAIR_MINK");  // development sweeps
+    return e ? atoi(e) : 16;
+  }();
   for (int q = 0; q < 2; ++q) {
     const int64_t nk = ((d[q].K + kBK - 1) / kBK) * d[q].groups;
-    if (nk < 16 || d[q].M < 2 * kBM) return false;
+    if (nk < min_nk || d[q].M < 2 * kBM) return false;
   }
   if (const char* e = getenv("HLQ_GEMM_FUSE2")) return atoi(e) != 0;
   return true;
