@@ -136,3 +136,24 @@ def test_reference_payload_reindexing_matches_oracle_layout():
     acbp = h.ACBPActivation(h.QuantizedTensor(torch.from_numpy(kmajor), 8, torch.tensor([scale])),
                             (B, L, I), 0, h.HadamardPlan(), q)
     assert np.array_equal(acbp.reference_payload().numpy(), codes)
+
+
+def test_bench_reference_arm_contract():
+    """`bench.py --impl reference` (the reference algorithm on the host cores)
+    prints one JSON line with the bench contract's keys; it needs no GPU."""
+    import json
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    out = subprocess.run([sys.executable, os.path.join(root, "bench.py"), "--impl", "reference", "--steps", "1",
+                          "--warmup", "0"], capture_output=True, text=True, timeout=600, cwd=root)
+    assert out.returncode == 0, out.stderr[-2000:]
+    line = json.loads(out.stdout.strip().splitlines()[-1])
+    for k in ("impl", "metric", "value", "unit", "n_gpus", "steps", "warmup", "ms_per_step", "higher_is_better",
+              "scaling", "vs_baseline", "dtype", "data", "config", "cpu_baseline", "e2e"):
+        assert k in line, k
+    assert line["impl"] == "reference" and line["value"] > 0 and line["unit"] == "img/s"
+    assert line["cpu_baseline"]["kind"] == "port" and line["cpu_baseline"]["value"] == line["value"]
+    assert line["e2e"]["h2d_bytes_per_step"] == 0 and line["e2e"]["value"] == line["value"]
+    with open(os.path.join(root, "BASELINE.json")) as f:
+        assert line["metric"] == json.load(f)["metric"]
