@@ -179,6 +179,14 @@ HLQ_API int hlq_gemm_i8_grouped(const int8_t* A, int64_t lda, int64_t a_gstride,
  * contract and results as hlq_gemm_i8_grouped (int_matmul_dequant,
  * quantize.py:152-187). */
 HLQ_API size_t hlq_gemm_i8_ws(int64_t M, int64_t N, int64_t K, int64_t groups);
+/* Contractions longer than the int32-exact bound (K * groups * qmax_a * qmax_b
+ * >= 2^31, e.g. an 8-bit dW with K > 133,143) run as K chunks that each stay
+ * inside it, summed in int64 before the dequant -- the reference accumulates
+ * in int64 up to MAX_K = {8: 10^6, 4: 10^7} (quantize.py:19-21,166-170) and
+ * hlq_gemm_i8_ex fails with PARAMETER past that bound, as int_matmul does.
+ * Such products need ws of hlq_gemm_i8_ws_bits(...) bytes (they cannot run
+ * unsplit), N % 4 == 0, and acc_out == NULL (an int32 dump could overflow). */
+HLQ_API size_t hlq_gemm_i8_ws_bits(int64_t M, int64_t N, int64_t K, int64_t groups, int bits_a, int bits_b);
 HLQ_API int hlq_gemm_i8_ex(const int8_t* A, int64_t lda, int64_t a_gstride, const int8_t* B,
                            int64_t ldb, int64_t b_gstride, int64_t M, int64_t N, int64_t K,
                            int64_t groups, int bits_a, int bits_b, const float* sa, const float* sb,

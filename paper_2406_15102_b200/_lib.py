@@ -48,6 +48,7 @@ SIGNATURES = {
     "hlq_gemm_i8_grouped": (_I, [_P, _I64, _I64, _P, _I64, _I64, _I64, _I64, _I64, _I64, _I, _I, _P,
                                  _P, _D, _I, _P, _I, _I64, _P, _I64, _P]),
     "hlq_gemm_i8_ws": (_SZ, [_I64, _I64, _I64, _I64]),
+    "hlq_gemm_i8_ws_bits": (_SZ, [_I64, _I64, _I64, _I64, _I, _I]),
     "hlq_acbp_container_bytes": (_I64, [_I64, _I64, _I]),
     "hlq_acbp_ws": (_SZ, [_I64]),
     "hlq_acbp_pack": (_I, [_P, _I64, _I64, _I64, _I, _I, _U32, _I64, _I64, _I64, _P, _P, _I64, _P, _SZ, _P]),

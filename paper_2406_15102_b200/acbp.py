@@ -48,9 +48,10 @@ def acbp_pack(acbp: ACBPActivation) -> torch.Tensor:
     wsb = int(lib.hlq_acbp_ws(total))
     ws = torch.empty(wsb, dtype=torch.uint8, device=dev)
     scale = q.scale.reshape(1).to(torch.float32)
-    _lib.call("hlq_acbp_pack", ops._p(payload), payload.stride(0) if payload.dim() == 2 else max(k, 1), rows, k,
-              q.bits, plan.block_size, plan.basis_bitmap(), B, L, I, ops._p(scale), ops._p(out), total,
-              ops._p(ws), wsb, ops._stream())
+    with torch.cuda.device(dev):
+        _lib.call("hlq_acbp_pack", ops._p(payload), payload.stride(0) if payload.dim() == 2 else max(k, 1), rows,
+                  k, q.bits, plan.block_size, plan.basis_bitmap(), B, L, I, ops._p(scale), ops._p(out), total,
+                  ops._p(ws), wsb, ops._stream())
     return out
 
 
@@ -73,6 +74,9 @@ def acbp_unpack(buf: torch.Tensor) -> ACBPActivation:
     qt = QuantizedTensor(payload=payload, bits=info.bits, scale=scale)
     return ACBPActivation(quantized=qt, orig_shape=(int(info.B), int(info.L), int(info.I)), axis=int(info.axis),
                           plan=plan, k=int(info.K))
+
+
+acbp_unpack = ops.on_device(acbp_unpack)
 
 
 def to_bytes(buf: torch.Tensor) -> bytes:

@@ -324,6 +324,15 @@ size_t hlq_gemm_i8_ws(int64_t M, int64_t N, int64_t K, int64_t groups) {
   return hlq::gemm_i8_ws_bytes(M, N, K, groups);
 }
 
+size_t hlq_gemm_i8_ws_bits(int64_t M, int64_t N, int64_t K, int64_t groups, int bits_a, int bits_b) {
+  if (M <= 0 || N <= 0 || K <= 0 || groups < 1 || check_bits(bits_a) || check_bits(bits_b)) return 0;
+  return hlq::gemm_i8_ws_bytes(M, N, K, groups,
+                               hlq::gemm_min_splits(K, groups, qmax_of(bits_a), qmax_of(bits_b)));
+}
+
+// int_matmul's advertised bound (quantize.py:21,166-170): MAX_K = {8: 10^6, 4: 10^7}
+static int64_t max_k_of(int bits) { return bits == 8 ? 1000000 : 10000000; }
+
 int hlq_gemm_i8_ex(const int8_t* A, int64_t lda, int64_t a_gstride, const int8_t* B, int64_t ldb,
                    int64_t b_gstride, int64_t M, int64_t N, int64_t K, int64_t groups, int bits_a,
                    int bits_b, const float* sa, const float* sb, double extra, int epilogue, void* out,
@@ -342,17 +351,28 @@ int hlq_gemm_i8_ex(const int8_t* A, int64_t lda, int64_t a_gstride, const int8_t
                 (long long)K);
   if (M > INT32_MAX || N > INT32_MAX || K > INT32_MAX)
     return fail(HLQ_ERR_DIMENSION, "GEMM extent exceeds int32");
-  const long double worst = (long double)K * groups * qmax_of(bits_a) * qmax_of(bits_b);
-  if (worst >= 2147483648.0L)
-    return fail(HLQ_ERR_PARAMETER,
-                "contraction extent %lld exceeds the int32-exact bound for %dx%d-bit operands",
-                (long long)K, bits_a, bits_b);
+  const int64_t kbound = max_k_of(bits_a) < max_k_of(bits_b) ? max_k_of(bits_a) : max_k_of(bits_b);
+  if (K * groups > kbound)
+    return fail(HLQ_ERR_PARAMETER, "contraction extent %lld exceeds the overflow-safe bound %lld for %dx%d-bit operands",
+                (long long)(K * groups), (long long)kbound, bits_a, bits_b);
+  const int min_splits = hlq::gemm_min_splits(K, groups, qmax_of(bits_a), qmax_of(bits_b));
+  if (min_splits > 1) {
+    // past the int32-exact bound: int32 chunks summed in int64 (needs the chunk slabs)
+    if (acc_out)
+      return fail(HLQ_ERR_PARAMETER, "contraction extent %lld exceeds the int32 accumulator dump bound",
+                  (long long)(K * groups));
+    if (N % 4 || !ws || ws_bytes < hlq::gemm_i8_ws_bytes(M, N, K, groups, min_splits))
+      return fail(HLQ_ERR_PARAMETER,
+                  "contraction extent %lld needs K chunks: N %% 4 == 0 and hlq_gemm_i8_ws_bits bytes of workspace",
+                  (long long)(K * groups));
+  }
   if (epilogue != HLQ_EPI_EXACT && epilogue != HLQ_EPI_FAST)
     return fail(HLQ_ERR_PARAMETER, "unknown epilogue %d", epilogue);
   if (M == 0 || N == 0) return HLQ_OK;
   int e = hlq::launch_gemm_i8(A, lda, B, ldb, M, N, K, groups, a_gstride, b_gstride, sa, sb, extra,
                               epilogue, out, out_dtype, ldo, acc_out, ld_acc, ws, ws_bytes,
-                              static_cast<cudaStream_t>(stream));
+                              static_cast<cudaStream_t>(stream), min_splits);
+  if (e == -2) return fail(HLQ_ERR_PARAMETER, "long contraction: output / workspace not 16-byte aligned");
   if (e == -1) return fail(HLQ_ERR_CUDA, "cuTensorMapEncodeTiled unavailable or rejected the operands");
   if (e != 0) return fail(HLQ_ERR_CUDA, "hlq_gemm_i8: %s", cudaGetErrorString(cudaError_t(e)));
   return HLQ_OK;

@@ -595,6 +595,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
 }
 
 // out[m, n] = dequant(sum_s slab[s][m, n]) (+ the exact int32 sum into acc_out).
+// The slabs are summed in int64: a contraction longer than the int32-exact
+// bound is planned as >= 2 splits each inside it (the reference accumulates in
+// int64 up to MAX_K, quantize.py:21,167), and acc_out is then not requested.
 __global__ void __launch_bounds__(256) splitk_finalize(const int32_t* __restrict__ slabs, int splits,
                                                        int M, int N, const float* __restrict__ sa,
                                                        const float* __restrict__ sb, double extra,
@@ -606,21 +609,22 @@ __global__ void __launch_bounds__(256) splitk_finalize(const int32_t* __restrict
   const int64_t plane = int64_t(M) * N;
   const int64_t nq = plane >> 2;  // N % 4 == 0 is required by the launcher
   for (int64_t q = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; q < nq; q += int64_t(gridDim.x) * blockDim.x) {
-    int4 t = __ldcs(reinterpret_cast<const int4*>(slabs) + q);
+    const int4 t0 = __ldcs(reinterpret_cast<const int4*>(slabs) + q);
+    long long a[4] = {t0.x, t0.y, t0.z, t0.w};
     for (int s = 1; s < splits; ++s) {
       const int4 v = __ldcs(reinterpret_cast<const int4*>(slabs + s * plane) + q);
-      t.x += v.x; t.y += v.y; t.z += v.z; t.w += v.w;
+      a[0] += v.x; a[1] += v.y; a[2] += v.z; a[3] += v.w;
     }
     const int64_t e = q << 2;
     const int64_t m = e / N, n = e - m * N;
-    const int a[4] = {t.x, t.y, t.z, t.w};
-    if (acc_out) *reinterpret_cast<int4*>(acc_out + m * ld_acc + n) = t;
+    if (acc_out)
+      *reinterpret_cast<int4*>(acc_out + m * ld_acc + n) = make_int4(int(a[0]), int(a[1]), int(a[2]), int(a[3]));
     if (!out) continue;
     float v[4];
 #pragma unroll
     for (int j = 0; j < 4; ++j)
-      v[j] = epilogue == kEpiExact ? __double2float_rn(__dmul_rn(double(a[j]), dscale))
-                                   : __fmul_rn(__int2float_rn(a[j]), fscale);
+      v[j] = epilogue == kEpiExact ? __double2float_rn(__dmul_rn(__ll2double_rn(a[j]), dscale))
+                                   : __fmul_rn(__ll2float_rn(a[j]), fscale);
     if (out_dtype == kF32) {
       *reinterpret_cast<float4*>(static_cast<float*>(out) + m * ldo + n) = make_float4(v[0], v[1], v[2], v[3]);
     } else {
@@ -720,12 +724,11 @@ int run_maps(const CUtensorMap& ma, const CUtensorMap& mb, int64_t M, int64_t N,
              int64_t ldo, int32_t* acc_out, int64_t ld_acc, int splits, void* ws, const ConvGeo& geo,
              cudaStream_t stream) {
   using Cfg = GemmCfg<BN, STAGES>;
-  static bool attr_set = false;  // per template instance
-  if (!attr_set) {
-    cudaError_t e = cudaFuncSetAttribute(gemm_i8_kernel<BN, STAGES>,
-                                         cudaFuncAttributeMaxDynamicSharedMemorySize, int(Cfg::kSmem));
+  static std::atomic<unsigned long long> attr_set{0};  // per template instance and device
+  {
+    cudaError_t e = smem_attr_once(reinterpret_cast<const void*>(gemm_i8_kernel<BN, STAGES>), int(Cfg::kSmem),
+                                   attr_set);
     if (e != cudaSuccess) return int(e);
-    attr_set = true;
   }
   const int64_t tiles = ((M + kBM - 1) / kBM) * ((N + BN - 1) / BN);
   int32_t* slabs = splits > 1 ? static_cast<int32_t*>(ws) : nullptr;
@@ -841,12 +844,11 @@ int run_2sm_specs(const PairSpec* specs, int n, cudaStream_t stream) {
     if (!fill_prob<BN>(P, q, specs[q], unit0)) return -1;
     unit0 += P.p[q].units;
   }
-  static bool attr_set = false;
-  if (!attr_set) {
-    cudaError_t e = cudaFuncSetAttribute(gemm_i8_2sm_kernel<BN, STAGES>,
-                                         cudaFuncAttributeMaxDynamicSharedMemorySize, int(kSmem));
+  static std::atomic<unsigned long long> attr_set{0};  // per template instance and device
+  {
+    cudaError_t e = smem_attr_once(reinterpret_cast<const void*>(gemm_i8_2sm_kernel<BN, STAGES>), int(kSmem),
+                                   attr_set);
     if (e != cudaSuccess) return int(e);
-    attr_set = true;
   }
   const int64_t pairs = num_sms() / 2;
   const int ncl = int(unit0 < pairs ? unit0 : pairs);
@@ -904,8 +906,20 @@ struct GemmPlan {
 };
 
 GemmPlan finish_plan(GemmPlan p, int64_t M, int64_t N, bool allow_split);
+GemmPlan plan_gemm_base(int64_t M, int64_t N, int64_t K, int64_t groups, bool allow_split);
 
-GemmPlan plan_gemm(int64_t M, int64_t N, int64_t K, int64_t groups, bool allow_split) {
+// min_splits > 1: the contraction exceeds the int32-exact bound, so it must run
+// as at least that many K chunks (int32 partial slabs, int64 finalize).
+GemmPlan plan_gemm(int64_t M, int64_t N, int64_t K, int64_t groups, bool allow_split, int min_splits = 1) {
+  GemmPlan p = plan_gemm_base(M, N, K, groups, allow_split || min_splits > 1);
+  if (min_splits > p.splits) {
+    p.splits = min_splits;
+    p.ws = size_t(p.splits) * M * N * 4;
+  }
+  return p;
+}
+
+GemmPlan plan_gemm_base(int64_t M, int64_t N, int64_t K, int64_t groups, bool allow_split) {
   const int64_t m_tiles = (M + kBM - 1) / kBM;
   const int64_t wide_tiles = m_tiles * ((N + 255) / 256);
   const int64_t nk = ((K + kBK - 1) / kBK) * groups;
@@ -991,20 +1005,22 @@ bool gemm_i8_pair2_eligible(const GemmDesc* d) {
   return true;
 }
 
-size_t gemm_i8_ws_bytes(int64_t M, int64_t N, int64_t K, int64_t groups) {
-  return plan_gemm(M, N, K, groups, true).ws;
+size_t gemm_i8_ws_bytes(int64_t M, int64_t N, int64_t K, int64_t groups, int min_splits) {
+  return plan_gemm(M, N, K, groups, true, min_splits).ws;
 }
 
 int launch_gemm_i8(const int8_t* A, int64_t lda, const int8_t* B, int64_t ldb, int64_t M, int64_t N,
                    int64_t K, int64_t groups, int64_t a_gstride, int64_t b_gstride,
                    const float* sa, const float* sb, double extra, int epilogue,
                    void* out, int out_dtype, int64_t ldo, int32_t* acc_out, int64_t ld_acc,
-                   void* ws, size_t ws_bytes, cudaStream_t stream) {
-  GemmPlan p = plan_gemm(M, N, K, groups, true);
+                   void* ws, size_t ws_bytes, cudaStream_t stream, int min_splits) {
+  GemmPlan p = plan_gemm(M, N, K, groups, true, min_splits);
   const bool vec_out = (ldo % 4 == 0) && (reinterpret_cast<uintptr_t>(out) % 16 == 0) &&
                        (ld_acc % 4 == 0) && (reinterpret_cast<uintptr_t>(acc_out) % 16 == 0);
-  if (p.splits > 1 && (ws == nullptr || ws_bytes < p.ws || !vec_out || (reinterpret_cast<uintptr_t>(ws) % 16)))
+  if (p.splits > 1 && (ws == nullptr || ws_bytes < p.ws || !vec_out || (reinterpret_cast<uintptr_t>(ws) % 16))) {
+    if (min_splits > 1) return -2;  // a long contraction cannot run without its chunk slabs
     p = plan_gemm(M, N, K, groups, false);
+  }
   if (p.pair) {
     if (p.bn == 256)
       return run_2sm<256, 6>(A, lda, B, ldb, M, N, K, groups, a_gstride, b_gstride, sa, sb, extra, epilogue, out,

@@ -1,6 +1,7 @@
 // Internal launch declarations shared by the kernel translation units and the C-ABI.
 #pragma once
 #include <cuda_runtime.h>
+#include <atomic>
 #include <cstdint>
 
 namespace hlq {
@@ -10,6 +11,20 @@ enum : int { kStats = 0, kQuant = 1, kBoth = 2 };  // kBoth: one cooperative lau
 enum : int { kEpiExact = 0, kEpiFast = 1 };
 
 int num_sms();
+
+// cudaFuncSetAttribute(MaxDynamicSharedMemorySize) once per (kernel, device):
+// the attribute is per device, so a process driving several GPUs must set it
+// on each.  `done` is the call site's static per-device bitmask.
+inline cudaError_t smem_attr_once(const void* kern, int bytes, std::atomic<unsigned long long>& done) {
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= 64)
+    return cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
+  const unsigned long long bit = 1ull << dev;
+  if (done.load(std::memory_order_acquire) & bit) return cudaSuccess;
+  const cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
+  if (e == cudaSuccess) done.fetch_or(bit, std::memory_order_acq_rel);
+  return e;
+}
 
 // One pass (STATS or QUANT) of the transform kernels over a (segs x rows x cols)
 // view.  do_gx: 16-point HT along cols, codes row-major into dst_gx (row index
@@ -73,7 +88,7 @@ int launch_gemm_i8(const int8_t* A, int64_t lda, const int8_t* B, int64_t ldb, i
                    int64_t K, int64_t groups, int64_t a_gstride, int64_t b_gstride,
                    const float* sa, const float* sb, double extra, int epilogue,
                    void* out, int out_dtype, int64_t ldo, int32_t* acc_out, int64_t ld_acc,
-                   void* ws, size_t ws_bytes, cudaStream_t stream);
+                   void* ws, size_t ws_bytes, cudaStream_t stream, int min_splits = 1);
 // Implicit-GEMM dgrad of a stride-1 conv (k x k, padding pad): dX (B, H, W, C)
 // channels-last = sum over taps and o of G codes (B, Ho, Wo, O; pixel stride
 // ldg) at the shifted pixel x W codes (row c*k*k + tap, ld ldw), int32 in TMEM,
@@ -144,6 +159,13 @@ void launch_xform_quant(const XformView& x, int bits, int rounding, uint64_t k0,
 void launch_xform_f32(const XformView& x, float* dst, cudaStream_t st);
 void launch_unproject_f32(const XformView& x, float* dst, cudaStream_t st);
 // Workspace bytes that let launch_gemm_i8 split K (0: no split planned).
-size_t gemm_i8_ws_bytes(int64_t M, int64_t N, int64_t K, int64_t groups);
+size_t gemm_i8_ws_bytes(int64_t M, int64_t N, int64_t K, int64_t groups, int min_splits = 1);
+// K chunks needed to keep every int32 partial exact: 1 when K * groups * qa * qb < 2^31.
+inline int gemm_min_splits(int64_t K, int64_t groups, int qa, int qb) {
+  const int64_t kb = (K + 127) / 128 * groups;           // 128-byte K blocks
+  const int64_t per = (int64_t(2147483647) / (int64_t(128) * qa * qb));  // blocks per exact chunk
+  if (K * groups * int64_t(qa) * qb < int64_t(2147483648LL)) return 1;
+  return int((kb + per - 1) / per);
+}
 
 }  // namespace hlq

@@ -693,11 +693,8 @@ void launch_one(const CUtensorMap& map, Args a, cudaStream_t stream) {
   const size_t smem = 128 + size_t(kStages) * 16 * kRow +
                       (GW && MODE != kStats ? size_t(a.cbw) * a.cstride : 0) + 8 + 2 * kStages * 8 + kStages * kMetaWords * 4;
   auto kern = tma_tile_kernel<T, MODE, GX, GW, BM, GRP>;
-  static bool attr = false;
-  if (!attr) {
-    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
-    attr = true;
-  }
+  static std::atomic<unsigned long long> attr{0};  // per template instance and device
+  smem_attr_once(reinterpret_cast<const void*>(kern), 200 * 1024, attr);
   int per_sm = 0;
   if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kThreads, smem) != cudaSuccess ||
       per_sm < 1)

@@ -617,12 +617,8 @@ void launch_tile(const TileArgs& a, cudaStream_t stream) {
   const int64_t items = ngroups * ncol_tiles;
   const int rank = GW ? a.rank : 0;
   const size_t smem = GW ? size_t(2 * 16 * Traits<T>::kRowBytes) + size_t(kTileCols) * (a.nb * rank + 16) : 0;
-  static bool attr = false;
-  if (!attr) {
-    cudaFuncSetAttribute(tile_kernel<T, MODE, GX, GW, BM>,
-                         cudaFuncAttributeMaxDynamicSharedMemorySize, 96 * 1024);
-    attr = true;
-  }
+  static std::atomic<unsigned long long> attr{0};  // per template instance and device
+  smem_attr_once(reinterpret_cast<const void*>(tile_kernel<T, MODE, GX, GW, BM>), 96 * 1024, attr);
   // persistent grid: exactly the resident CTAs, each walking several steps so
   // the register prefetch always has the next two blocks in flight
   int per_sm = 0;

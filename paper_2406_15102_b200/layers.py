@@ -41,6 +41,22 @@ def _blv(shape):
 
 
 _SIDE = {}
+_STAGES = [None]  # list sink while capture_stages() is active
+
+
+class capture_stages:
+    """Record, per HLQLinearFunction.backward call, the codes and scales the
+    training path computed (parity tests of the path that actually trains).
+    The tensors are views, not copies; no extra kernels run."""
+
+    def __enter__(self):
+        self.records = []
+        _STAGES[0] = self.records
+        return self.records
+
+    def __exit__(self, *exc):
+        _STAGES[0] = None
+        return False
 
 
 def side_stream(device) -> torch.cuda.Stream:
@@ -135,9 +151,10 @@ class HLQLinearFunction(torch.autograd.Function):
             main = torch.cuda.current_stream()
             side = side_stream(gy.device)
             side.wait_stream(main)
-            if side is main:
+            # (torch.cuda.current_stream() returns a fresh wrapper per call: compare handles)
+            if side.cuda_stream == main.cuda_stream and ops.pair_eligible(O, B * L, k, ops.pad16(O)):
                 # dW and dX as one CTA-pair launch over both products' tiles when both
-                # contractions are long (otherwise hlq_gemm_i8_multi runs them back to back)
+                # contractions are long (otherwise two gemm_i8 calls, which keep the split-K planner)
                 gw, gx = ops.gemm_i8_pair(
                     dict(a=cg, b=payload, m=O, n=I, k=k, bits_a=bits_gw, bits_b=bits_gw, sa=sg, sb=sx),
                     dict(a=cgx, b=cw, m=B * L, n=I, k=ops.pad16(O), bits_a=bits_gx, bits_b=bits_gx, sa=sgx,
@@ -151,6 +168,13 @@ class HLQLinearFunction(torch.autograd.Function):
             gw.record_stream(main)
             for t in (cg, sg, payload, sx):
                 t.record_stream(side)
+            if _STAGES[0] is not None:
+                # parity capture of the training path, in the reference's layouts
+                # (backprop.py:350-410: codes (T, O_p), (O_p, I), (O, K), payload (K, I))
+                _STAGES[0].append(dict(gx_codes_g=cgx[:, :ops.pad16(O)], gx_scale_g=sgx,
+                                       gx_codes_w=cw[:, :ops.pad16(O)].t(), gx_scale_w=sw,
+                                       gw_codes_g=cg[:, :k], gw_scale_g=sg, x_codes=payload[:, :k].t(),
+                                       x_scale=sx, axis=axis))
             if weight.dtype != torch.float32:
                 gw = gw.to(weight.dtype)
             gx = gx.reshape(x_shape).to(x_dtype)
@@ -294,7 +318,7 @@ def _calib_record(layer, gy3, axis: int):
     sinks[layer] = (e, n) if prev is None else (prev[0] + e, prev[1] + n)
 
 
-def refresh_weight_codes(module: nn.Module) -> int:
+def refresh_weight_codes(module: nn.Module, force: bool = False) -> int:
     """Recompute, in ONE batched launch per bit width (hlq_quantize_weights),
     the dX weight codes Q(HT_O(W)) of every HLQLinear under `module` whose
     weight changed since its codes were made (training: every layer, once per
@@ -303,7 +327,7 @@ def refresh_weight_codes(module: nn.Module) -> int:
     stale = {}
     # under CUDA-graph capture the refresh must be part of the captured step whatever
     # the cache says (replays re-run the kernels, not this Python check)
-    force = torch.cuda.is_available() and torch.cuda.is_current_stream_capturing()
+    force = force or (torch.cuda.is_available() and torch.cuda.is_current_stream_capturing())
     for m in module.modules():
         # HLQLinear and HLQConv2d (its weight viewed as (O, C*k*k), the dX operand's layout)
         if getattr(m, "_hlq_weight_codes", False) and m.weight.is_cuda and \
@@ -324,8 +348,12 @@ def refresh_weight_codes(module: nn.Module) -> int:
 
 
 def _refresh_hook(module, args):
+    # always recompute: the (version, data_ptr) key cannot see in-place writes through
+    # `.data` (EMA, custom optimizers, storage swaps), and in training every step
+    # changes every weight anyway, so the cache would only skip work for extra
+    # forwards within one step
     if module.training and torch.is_grad_enabled():
-        refresh_weight_codes(module)
+        refresh_weight_codes(module, force=True)
 
 
 def convert_linears(module: nn.Module, strategy: BackwardStrategy | None = None,

@@ -80,6 +80,34 @@ def _stream():
     return ctypes.c_void_p(torch.cuda.current_stream().cuda_stream)
 
 
+def _first_tensor(args, kwargs):
+    for a in list(args) + list(kwargs.values()):
+        if torch.is_tensor(a):
+            return a
+        if isinstance(a, (list, tuple)) and a and torch.is_tensor(a[0]):
+            return a[0]
+        if isinstance(a, dict) and torch.is_tensor(a.get("a")):
+            return a["a"]
+    return None
+
+
+def on_device(fn):
+    """Run an op with its operands' device current: libhlq launches into the
+    current CUDA context on torch's current stream of the current device, so
+    a tensor on cuda:1 while cuda:0 is current must switch first (the check
+    costs one cudaGetDevice when the device already matches)."""
+    import functools
+
+    @functools.wraps(fn)
+    def wrapped(*args, **kwargs):
+        t = _first_tensor(args, kwargs)
+        if t is not None and t.is_cuda and t.device.index != torch.cuda.current_device():
+            with torch.cuda.device(t.device):
+                return fn(*args, **kwargs)
+        return fn(*args, **kwargs)
+    return wrapped
+
+
 def _p(t):
     return ctypes.c_void_p(0 if t is None else t.data_ptr())
 
@@ -396,7 +424,7 @@ def gemm_i8(a: torch.Tensor, b: torch.Tensor, m: int, n: int, k: int, bits_a: in
     b_gs = ldb * n if b_gstride is None else b_gstride
     # split-K workspace (the dW products: few output tiles, long K); stream-ordered
     # caching-allocator memory, no initialisation needed
-    wsb = int(_lib.load().hlq_gemm_i8_ws(m, n, k, groups)) if m > 0 and n > 0 else 0
+    wsb = int(_lib.load().hlq_gemm_i8_ws_bits(m, n, k, groups, bits_a, bits_b)) if m > 0 and n > 0 else 0
     ws = torch.empty(wsb, dtype=torch.uint8, device=dev) if wsb else None
     _traced("gemm", 0, 2 * m * n * k * groups, 1,
             lambda: _lib.call("hlq_gemm_i8_ex", _p(a), lda, a_gs, _p(b), ldb, b_gs, m, n, k,
@@ -406,6 +434,22 @@ def gemm_i8(a: torch.Tensor, b: torch.Tensor, m: int, n: int, k: int, bits_a: in
                               _p(acc), n, _p(ws), wsb, _stream()),
             key=f"gemm:{m}x{n}x{k * groups}")
     return out, acc
+
+
+PAIR_MIN_K = 16 * 128  # >= 16 K blocks of 128 bytes in BOTH products (hlq_gemm.cu gemm_i8_pair2_eligible)
+
+
+def pair_eligible(m0: int, m1: int, k0: int, k1: int) -> bool:
+    """True when hlq_gemm_i8_multi runs two products as ONE CTA-pair launch
+    (both contractions long, both >= 256 rows).  Otherwise the caller issues
+    two gemm_i8 calls, which keeps the split-K planner for short-M products
+    (the multi entry's sequential fallback runs without a split-K workspace).
+    HLQ_PAIR=0 disables the fused launch (A/B measurements)."""
+    import os
+    if os.environ.get("HLQ_PAIR", "1") == "0":
+        return False
+    # (contractions past the int32-exact bound run as K chunks through gemm_i8)
+    return PAIR_MIN_K - 128 < min(k0, k1) and max(k0, k1) * 127 * 127 < 2 ** 31 and min(m0, m1) >= 256
 
 
 def gemm_i8_pair(p0: dict, p1: dict):
@@ -509,3 +553,11 @@ def check_finite(*amax_bits: torch.Tensor) -> None:
 def require_dims(cond: bool, msg: str):
     if not cond:
         raise DimensionError(msg)
+
+
+for _name in ("quant_ht_cols", "quant_dual", "transform_pass", "quant_proj_rows", "quant_weights",
+              "quant_stochastic", "basis_energy", "xform_quantize", "xform_project", "xform_unproject",
+              "proj_rows_amax", "proj_rows_quant", "gemm_i8", "gemm_i8_pair", "conv_acbp", "conv_dgrad_i8",
+              "col2im"):
+    globals()[_name] = on_device(globals()[_name])
+del _name
