@@ -191,8 +191,23 @@ __device__ __forceinline__ Quant make_quant(const uint32_t* g, int bits) {
   return q;
 }
 
-// Unclamped codes of two values as two s16 lanes: code = ceil((Q - u) / 2048),
-// Q = RN(w / d) by reciprocal-FMA division, u = bits(w) & 0x7FF.
+// The reference rounds up iff RN(q - floor(q)) * 2048 > u (quantize.py:143-144).
+// q - floor(q) is exact except for q in (-0.5, 0), where it is RN(q + 1): in
+// the scaled domain (Q = 2048 q) the test is RN(Q + 2048) > u, i.e. (u integer,
+// ties to even) Q + 2048 > u + 2^-14 -- so those lanes use Qr = RU(Q - 2^-14)
+// (RU keeps the comparison with every integer boundary), all others Qr = Q.
+// RU(Q - 2^-14) == Q for Q <= -1024 (ulp >= 2^-13), and as int32 bit patterns
+// RU(Q - 2^-14) > Q exactly when Q < 0 (larger magnitude, sign set) while for
+// Q >= 0 it is below Q: one integer max selects Qr.  (Found by the batch-128
+// ViT qkv parity test: 1 of 58 M codes had Q + 2048 - u in (0, 2^-14].)
+__device__ __forceinline__ float2 ref_frac_adjust(float2 Q) {
+  const float2 t = f2add_rp(Q, f2(-0x1p-14f));
+  return make_float2(__int_as_float(max(__float_as_int(Q.x), __float_as_int(t.x))),
+                     __int_as_float(max(__float_as_int(Q.y), __float_as_int(t.y))));
+}
+
+// Unclamped codes of two values as two s16 lanes: code = ceil((Qr - u) / 2048),
+// Qr = ref_frac_adjust(Q), Q = RN(w / d) by reciprocal-FMA division, u = bits(w) & 0x7FF.
 //   U  = 2^23 + u as a float (one LOP3: OR the draw into 2^23's mantissa);
 //   z  = RU(Q - U) = RU(y - 2^23), y = Q - u in (-2^19, 2^19): a grid of
 //        spacing <= 1 around -2^23, so z + 2^23 = g is the smallest grid point
@@ -203,7 +218,7 @@ __device__ __forceinline__ Quant make_quant(const uint32_t* g, int bits) {
 __device__ __forceinline__ uint32_t quant_fast2(float2 w, const Quant& q) {
   const float2 Q0 = f2mul(w, f2(q.r));
   const float2 e = f2fma(Q0, f2(-q.d), w);
-  const float2 Q = f2fma(e, f2(q.r), Q0);
+  const float2 Q = ref_frac_adjust(f2fma(e, f2(q.r), Q0));
   uint32_t ux, uy;
   const uint32_t magic = 0x4B000000u;  // 2^23
   asm("lop3.b32 %0, %1, 0x7FF, %2, 0xEA;" : "=r"(ux) : "r"(__float_as_uint(w.x)), "r"(magic));

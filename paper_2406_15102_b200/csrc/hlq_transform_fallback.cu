@@ -96,6 +96,13 @@ __device__ __forceinline__ float2 f2add_rp(float2 a, float2 b) {
       : "=f"(d.x), "=f"(d.y) : "f"(a.x), "f"(a.y), "f"(b.x), "f"(b.y));
   return d;
 }
+// The reference's frac = RN(q - floor(q)) is RN(q + 1) for q in (-0.5, 0):
+// Qr = RU(Q - 2^-14) there, Q elsewhere (one int max; see hlq_quant.cuh).
+__device__ __forceinline__ float2 ref_frac_adjust(float2 Q) {
+  const float2 t = f2add_rp(Q, make_float2(-0x1p-14f, -0x1p-14f));
+  return make_float2(__int_as_float(max(__float_as_int(Q.x), __float_as_int(t.x))),
+                     __int_as_float(max(__float_as_int(Q.y), __float_as_int(t.y))));
+}
 __device__ __forceinline__ float2 f2fma_rp(float2 a, float2 b, float2 c) {
   float2 d;
   asm("{.reg .b64 ra, rb, rc, rd;\n\tmov.b64 ra, {%2, %3};\n\tmov.b64 rb, {%4, %5};\n\t"
@@ -275,7 +282,7 @@ __device__ __forceinline__ Quant make_quant(const uint32_t* g, int bits) {
 __device__ __forceinline__ uint2 quant_fast2(float2 w, const Quant& q) {
   float2 Q = f2mul(w, f2(q.r));
   const float2 e = f2fma(Q, f2(-q.d), w);
-  Q = f2fma(e, f2(q.r), Q);
+  Q = ref_frac_adjust(f2fma(e, f2(q.r), Q));  // hlq_quant.cuh: the reference's RN(q - floor(q))
   Q.x = fminf(fmaxf(Q.x, -q.lim), q.lim);
   Q.y = fminf(fmaxf(Q.y, -q.lim), q.lim);
   // -u as an exact float: (2^23) - (2^23 + u)
