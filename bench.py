@@ -423,159 +423,182 @@ def timed(torch, dist, fn):
     return ms
 
 
-def graph_us(torch, fn, flush, reps=10):
-    """Median device time (us) of fn captured in a CUDA graph (no host
-    overhead), L2 flushed before every replay: a 256 MB write, then a 160 MB
-    read of its start so the dirty lines are written back before the timed
-    region instead of during it (that write-back had added ~10 us to small
-    kernels)."""
-    fn()
-    torch.cuda.synchronize()
-    g = torch.cuda.CUDAGraph()
-    with torch.cuda.graph(g):
-        fn()
-    ts = []
+def event_us(torch, timed, flush, prep=None, reps=10):
+    """Median device time (us) of timed(prep()) through the product's own
+    Python entry points (autograd), L2 flushed before each repetition: the
+    flush is written, then read back so its dirty lines are not written back
+    inside the timed region; a GPU spin (torch.cuda._sleep, ~1.5 ms) lets the
+    host enqueue the whole call before the start event fires, so host-side
+    autograd / launch overhead is not counted -- CUDA events on the stream."""
     head = flush[: 40 * 1024 * 1024]
-    for _ in range(reps):
+    ts = []
+    for i in range(reps + 1):
+        st = prep() if prep is not None else None
         flush.zero_()
         head.sum()
+        torch.cuda._sleep(3_000_000)
         s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         s.record()
-        g.replay()
+        timed(st)
         e.record()
         e.synchronize()
-        ts.append(s.elapsed_time(e) * 1e3)
+        if i:
+            ts.append(s.elapsed_time(e) * 1e3)
     return sorted(ts)[len(ts) // 2]
 
 
+def _linear_pair(torch, I, O, strategy=None):
+    """(HLQ module under its model-wide hook, dense nn.Linear) with equal weights."""
+    from paper_2406_15102_b200.layers import convert_linears
+    torch.manual_seed(1)
+    dense = torch.nn.Linear(I, O).cuda()
+    hnet = convert_linears(torch.nn.Sequential(torch.nn.Linear(I, O)), strategy).cuda()
+    with torch.no_grad():
+        hnet[0].weight.copy_(dense.weight)
+        hnet[0].bias.copy_(dense.bias)
+    return hnet, dense
+
+
+def layer_autograd(torch, flush, mod_h, mod_d, x, gy, amp=True):
+    """One layer through autograd, HLQ module vs dense module:
+    fwd = the forward (HLQ: stock GEMM + ACBP; the W codes come from the
+    model-wide refresh, reported separately), bwd = loss.backward() of the
+    layer (HLQ: HLQLinearFunction / HLQConv2dFunction.backward; dense: the
+    cuBLAS / cuDNN bf16 dgrad + wgrad + bias reduction + fp32 grad casts),
+    libhlq_bwd_us = the libhlq calls inside that backward (ops.trace)."""
+    from paper_2406_15102_b200 import ops
+    from paper_2406_15102_b200.layers import refresh_weight_codes
+    ac = (lambda: torch.autocast("cuda", dtype=torch.bfloat16)) if amp else (lambda: torch.autocast("cuda",
+                                                                                                  enabled=False))
+    xr = x.detach().requires_grad_(True)
+
+    def fwd_h():
+        with ac():
+            return mod_h[0](xr) if isinstance(mod_h, torch.nn.Sequential) else mod_h(xr)
+
+    def fwd_d():
+        with ac():
+            return mod_d(xr)
+    with ac():
+        refresh_weight_codes(mod_h, force=True)
+    out = {}
+    out["hlq_fwd_us"] = event_us(torch, lambda _: fwd_h(), flush)
+    out["dense_fwd_us"] = event_us(torch, lambda _: fwd_d(), flush)
+    out["hlq_bwd_us"] = event_us(torch, lambda y: y.backward(gy), flush, prep=fwd_h)
+    out["dense_bwd_us"] = event_us(torch, lambda y: y.backward(gy), flush, prep=fwd_d)
+    y = fwd_h()
+    torch.cuda.synchronize()
+    with ops.trace() as tr:
+        y.backward(gy)
+    out["libhlq_bwd_us"] = round(sum(v["us"] for v in tr.summary().values()), 1)
+    out["libhlq_bwd_kernels"] = {k: {"us": round(v["us"], 1), "calls": v["calls"]}
+                                 for k, v in tr.summary(by="key").items()}
+    for k in ("hlq_fwd_us", "dense_fwd_us", "hlq_bwd_us", "dense_bwd_us"):
+        out[k] = round(out[k], 1)
+    out["bwd_speedup"] = round(out["dense_bwd_us"] / out["hlq_bwd_us"], 3)
+    out["fwd_overhead_us"] = round(out["hlq_fwd_us"] - out["dense_fwd_us"], 1)
+    return out
+
+
 def layer_bwd_table(torch):
-    """Per-layer backward (dX + dW) at the ViT-B/16 shapes, batch 128: the HLQ
-    kernels exactly as HLQLinearFunction.backward runs them vs the dense bf16
-    backward (two cuBLAS GEMMs).  CUDA-graph replays, L2 flushed before each."""
+    """Per-layer timing at the ViT-B/16 shapes (batch 128, L = 197, bf16
+    autocast), through the product's autograd modules (HLQLinear under
+    convert_linears, as the training step runs them) vs stock nn.Linear.
+    block_total adds the HLQ-only forward work (ACBP) and the amortised W
+    codes (one batched refresh of all 49 weights per step, / 49 per layer):
+    total_hlq_overhead compares HLQ fwd + bwd + W codes against dense fwd + bwd."""
     from paper_2406_15102_b200 import ops
     flush = torch.empty(64 * 1024 * 1024, device="cuda")
-
     out = {}
-    for name, B, L, I, O in [("qkv", BATCH, TOKENS, 768, 2304), ("proj", BATCH, TOKENS, 768, 768),
-                             ("fc1", BATCH, TOKENS, 768, 3072), ("fc2", BATCH, TOKENS, 3072, 768)]:
-        torch.manual_seed(1)
-        x = torch.randn(B, L, I, device="cuda", dtype=torch.bfloat16)
-        w = torch.randn(O, I, device="cuda") * (2.0 / I) ** 0.5
-        gy = (torch.randn(B, L, O, device="cuda") * 1e-3).to(torch.bfloat16)
-        xp, k, sx, _ = ops.quant_proj_rows(x, B, L, I, 0x5555, 8, I, L * I)
-        cw, _, sw, _ = ops.quant_proj_rows(w, 1, O, I, 0xFFFF, 4)
-        def hlq_bwd():
-            # exactly HLQLinearFunction.backward: fused gy transform, then dW and dX
-            # (one CTA-pair launch over both when both contractions are long)
-            cgx, sgx, cg, kg, sg, _ = ops.quant_dual(gy, B, L, O, 0x5555, 4, 8, O, L * O)
-            ops.gemm_i8_pair(dict(a=cg, b=xp, m=O, n=I, k=k, bits_a=8, bits_b=8, sa=sg, sb=sx),
-                             dict(a=cgx, b=cw, m=B * L, n=I, k=ops.pad16(O), bits_a=4, bits_b=4, sa=sgx, sb=sw,
-                                  out_dtype=torch.bfloat16))
-
-        def hlq_fwd_extra():
-            # forward-time work (on a side stream under the forward GEMM in training); the
-            # W codes come from the model-wide batched refresh (weight_codes_refresh below)
-            ops.quant_proj_rows(x, B, L, I, 0x5555, 8, I, L * I)
-
-        wb, xb, gb = w.to(torch.bfloat16), x.reshape(-1, I), gy.reshape(-1, O)
-
-        def dense_bwd():
-            gb @ wb
-            gb.t() @ xb
-
-        h, d, f = (graph_us(torch, hlq_bwd, flush), graph_us(torch, dense_bwd, flush),
-                   graph_us(torch, hlq_fwd_extra, flush))
-        out[name] = {"hlq_us": round(h, 1), "dense_bf16_us": round(d, 1), "speedup": round(d / h, 3),
-                     "fwd_overhead_us": round(f, 1)}
-    tot_h = sum(v["hlq_us"] for v in out.values())
-    tot_d = sum(v["dense_bf16_us"] for v in out.values())
-    tot_f = sum(v["fwd_overhead_us"] for v in out.values())
-    out["block_total"] = {"hlq_us": round(tot_h, 1), "dense_bf16_us": round(tot_d, 1),
-                          "speedup": round(tot_d / tot_h, 3), "fwd_overhead_us": round(tot_f, 1)}
-    # W codes of all 49 ViT-B/16 Linear weights, one batched launch per step
+    for name, I, O in (("qkv", 768, 2304), ("proj", 768, 768), ("fc1", 768, 3072), ("fc2", 3072, 768)):
+        hnet, dense = _linear_pair(torch, I, O)
+        torch.manual_seed(2)
+        x = torch.randn(BATCH, TOKENS, I, device="cuda", dtype=torch.bfloat16)
+        gy = (torch.randn(BATCH, TOKENS, O, device="cuda") * 1e-3).to(torch.bfloat16)
+        out[name] = layer_autograd(torch, flush, hnet, dense, x, gy)
+        del hnet, dense, x, gy
+    # W codes of all 49 ViT-B/16 Linear weights: one batched launch per step
     torch.manual_seed(3)
     shapes = [(2304, 768), (768, 768), (3072, 768), (768, 3072)] * 12 + [(1000, 768)]
     ws = [torch.randn(o, i, device="cuda") * (2.0 / i) ** 0.5 for o, i in shapes]
-    out["weight_codes_refresh"] = {"us_per_step": round(graph_us(torch, lambda: ops.quant_weights(ws, 4), flush), 1),
-                                   "layers": len(ws), "launches": 1}
+    wc = event_us(torch, lambda _: ops.quant_weights(ws, 4, bf16=True), flush)
     del ws
-    out["note"] = ("hlq_us = backward as run by HLQLinearFunction (fused gy transform, then dW + dX via "
-                   "hlq_gemm_i8_multi); fwd_overhead_us = ACBP(X) in the forward; "
-                   "weight_codes_refresh = the dX weight codes of every layer, batched once per step")
+    lay = [out[n] for n in ("qkv", "proj", "fc1", "fc2")]
+    tot = {k: round(sum(v[k] for v in lay), 1) for k in ("hlq_fwd_us", "dense_fwd_us", "hlq_bwd_us",
+                                                          "dense_bwd_us", "libhlq_bwd_us")}
+    tot["bwd_speedup"] = round(tot["dense_bwd_us"] / tot["hlq_bwd_us"], 3)
+    wc_block = wc * 4 / 49
+    hlq_all = tot["hlq_fwd_us"] + tot["hlq_bwd_us"] + wc_block
+    dense_all = tot["dense_fwd_us"] + tot["dense_bwd_us"]
+    tot["total_hlq_overhead"] = {"hlq_fwd_plus_bwd_plus_wcodes_us": round(hlq_all, 1),
+                                 "dense_fwd_plus_bwd_us": round(dense_all, 1),
+                                 "speedup": round(dense_all / hlq_all, 3),
+                                 "wcodes_us_per_block": round(wc_block, 1)}
+    out["block_total"] = tot
+    out["weight_codes_refresh"] = {"us_per_step": round(wc, 1), "layers": 49, "launches": 1,
+                                   "note": "fp32 master weights -> W codes + the bf16 forward copies"}
+    out["note"] = ("through autograd: HLQLinear (convert_linears) vs nn.Linear, bf16 autocast, batch 128 x 197 "
+                   "tokens; device time by CUDA events with the host enqueue hidden behind a GPU spin, L2 flushed; "
+                   "fwd_overhead_us = HLQ forward - dense forward (the ACBP of X)")
     del flush
     return out
 
 
 def config_table(torch):
-    """The other BASELINE single-layer configs, HLQ backward vs dense bf16
-    backward on the same GPU (CUDA graphs, L2 flushed):
-      (a) configs[0]: Linear 4096 tokens x 1024 -> 1024, fp32 I/O, HLA rank 2
-          (r = tokens/8: K = 512) and the paper-default rank 8;
+    """The other BASELINE single-layer configs through the autograd modules,
+    HLQ vs dense bf16 on the same GPU (L2 flushed, device time):
+      (a) configs[0]: Linear 4096 tokens x 1024 -> 1024, fp32 I/O (2-D input:
+          projection along the token axis), HLA rank 2 (r = tokens/8: K = 512)
+          and the paper-default rank 8, vs the dense bf16 layer;
       (b) configs[1]: Conv2d 256 -> 256, 3x3, 14x14, batch 128, rank 8 --
-          HLQConv2dFunction.backward's kernels (fused gy transform, W codes,
-          dW / dX int8 GEMMs, col2im) vs cuDNN dgrad + wgrad, channels_last bf16."""
-    from paper_2406_15102_b200 import ops
+          HLQConv2d (HLQConv2dFunction) vs nn.Conv2d (cuDNN), channels_last,
+          bf16 autocast."""
+    from paper_2406_15102_b200 import acbp as acbp_mod
+    from paper_2406_15102_b200.backprop import BackwardStrategy, acbp_compress
+    from paper_2406_15102_b200.conv import convert_convs
+    from paper_2406_15102_b200.hadamard import HadamardPlan, lowest_sequency_bases
+    from paper_2406_15102_b200.layers import convert_linears
     flush = torch.empty(64 * 1024 * 1024, device="cuda")
     out = {}
-    torch.manual_seed(2)
     T, I, O = 4096, 1024, 1024
-    x = torch.randn(T, 1, I, device="cuda")
-    w = torch.randn(O, I, device="cuda") * (2.0 / I) ** 0.5
-    gy = torch.randn(T, 1, O, device="cuda") * 1e-3
-    wb, xb, gb = w.to(torch.bfloat16), x.reshape(T, I).to(torch.bfloat16), gy.reshape(T, O).to(torch.bfloat16)
-    dense = graph_us(torch, lambda: (gb @ wb, gb.t() @ xb), flush)
-    cw, _, sw, _ = ops.quant_proj_rows(w, 1, O, I, 0xFFFF, 4)
-    for rank, bm in ((2, 0x0101), (8, 0x5555)):
-        # 2-D Linear convention: projection along the token (batch) axis, one segment
-        xp, k, sx, _ = ops.quant_proj_rows(x.reshape(T, I), 1, T, I, bm, 8)
-
-        def hlq_bwd():
-            # as HLQLinearFunction.backward runs it: one fused gy transform, then dW and
-            # dX as one hlq_gemm_i8_multi call
-            cgx, sgx, cg, kg, sg, _ = ops.quant_dual(gy.reshape(T, O), 1, T, O, bm, 4, 8)
-            ops.gemm_i8_pair(dict(a=cg, b=xp, m=O, n=I, k=k, bits_a=8, bits_b=8, sa=sg, sb=sx),
-                             dict(a=cgx, b=cw, m=T, n=I, k=ops.pad16(O), bits_a=4, bits_b=4, sa=sgx, sb=sw))
-        h = graph_us(torch, hlq_bwd, flush)
-        out[f"a_linear_4096x1024_fp32_r{rank}"] = {"hlq_us": round(h, 1), "dense_bf16_us": round(dense, 1),
-                                                   "speedup": round(dense / h, 3), "K": k}
+    torch.manual_seed(2)
+    x = torch.randn(T, I, device="cuda")
+    gy = torch.randn(T, O, device="cuda") * 1e-3
+    xb, gb = x.to(torch.bfloat16), gy.to(torch.bfloat16)
+    for rank in (2, 8):
+        strat = BackwardStrategy.hlq().with_plan(HadamardPlan(basis_indices=lowest_sequency_bases(16, rank)))
+        hnet, dense = _linear_pair(torch, I, O, strat)
+        # dense arm: the same layer in bf16 (autocast); HLQ arm: fp32 I/O as BASELINE configs[0] states
+        d = layer_autograd(torch, flush, hnet, dense, xb, gb, amp=True)
+        h = layer_autograd(torch, flush, hnet, dense, x, gy, amp=False)
+        out[f"a_linear_4096x1024_fp32_r{rank}"] = {
+            "hlq_bwd_us": h["hlq_bwd_us"], "hlq_fwd_us": h["hlq_fwd_us"], "libhlq_bwd_us": h["libhlq_bwd_us"],
+            "dense_bf16_bwd_us": d["dense_bwd_us"], "dense_bf16_fwd_us": d["dense_fwd_us"],
+            "bwd_speedup": round(d["dense_bwd_us"] / h["hlq_bwd_us"], 3),
+            "total_speedup": round((d["dense_bwd_us"] + d["dense_fwd_us"]) / (h["hlq_bwd_us"] + h["hlq_fwd_us"]), 3),
+            "K": T * rank // 16}
     # (b) conv
-    B, C, H, W, k = 128, 256, 14, 14, 3
-    xc = torch.randn(B, C, H, W, device="cuda").to(memory_format=torch.channels_last).to(torch.bfloat16)
-    w4 = torch.randn(C, C, k, k, device="cuda") * (2.0 / (C * k * k)) ** 0.5
-    gyc = (torch.randn(B, C, H, W, device="cuda") * 1e-3).to(torch.bfloat16).to(
-        memory_format=torch.channels_last)
-    from paper_2406_15102_b200.backprop import BackwardStrategy
-    from paper_2406_15102_b200.conv import _conv_backward, conv_acbp_compress
-    strat = BackwardStrategy.hlq()
-    acbp, _ = conv_acbp_compress(xc, k, 1, 1, strat)
-    hc = graph_us(torch, lambda: _conv_backward(acbp, w4, gyc, xc.shape, 1, 1, strat, 1.0, False,
-                                                torch.bfloat16), flush)
-    w4b = w4.to(torch.bfloat16).to(memory_format=torch.channels_last)
-
-    def dense_conv():
-        torch.nn.grad.conv2d_input(xc.shape, w4b, gyc, stride=1, padding=1)
-        torch.nn.grad.conv2d_weight(xc, w4b.shape, gyc, stride=1, padding=1)
-    dc = graph_us(torch, dense_conv, flush)
-    fwd = graph_us(torch, lambda: conv_acbp_compress(xc, k, 1, 1, strat), flush)
-    out["b_conv_256x256_3x3_14x14_b128"] = {"hlq_us": round(hc, 1), "dense_bf16_us": round(dc, 1),
-                                            "speedup": round(dc / hc, 3), "fwd_acbp_us": round(fwd, 1)}
+    B, C, H, k = 128, 256, 14, 3
+    torch.manual_seed(4)
+    xc = torch.randn(B, C, H, H, device="cuda").to(memory_format=torch.channels_last).to(torch.bfloat16)
+    gyc = (torch.randn(B, C, H, H, device="cuda") * 1e-3).to(torch.bfloat16).to(memory_format=torch.channels_last)
+    dconv = torch.nn.Conv2d(C, C, k, padding=1).cuda().to(memory_format=torch.channels_last)
+    hconv = convert_linears(convert_convs(torch.nn.Sequential(torch.nn.Conv2d(C, C, k, padding=1)))).cuda()
+    hconv = hconv.to(memory_format=torch.channels_last)
+    with torch.no_grad():
+        hconv[0].weight.copy_(dconv.weight)
+        hconv[0].bias.copy_(dconv.bias)
+    c = layer_autograd(torch, flush, hconv, dconv, xc, gyc, amp=True)
+    c["config"] = "B=128, 256->256, 3x3, 14x14, stride 1, pad 1, rank 8, channels_last bf16"
+    c["total_speedup"] = round((c["dense_bwd_us"] + c["dense_fwd_us"]) / (c["hlq_bwd_us"] + c["hlq_fwd_us"]), 3)
+    out["b_conv_256x256_3x3_14x14_b128"] = c
     # ACBP container (SURVEY 8(f) f1) of the ViT-B/16 fc1 input: pack (transpose + CRC32) and
     # unpack (header parse on the host, range / CRC checks, transpose back), GB/s of container bytes
-    from paper_2406_15102_b200 import acbp as acbp_mod
     xa = torch.randn(128, 197, 768, device="cuda", dtype=torch.bfloat16)
-    from paper_2406_15102_b200.backprop import acbp_compress
-    from paper_2406_15102_b200.hadamard import HadamardPlan
     act = acbp_compress(xa, HadamardPlan())
     buf = acbp_mod.acbp_pack(act)
-    pk = graph_us(torch, lambda: acbp_mod.acbp_pack(act), flush)
-    acbp_mod.acbp_unpack(buf)
-    s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    s.record()
-    for _ in range(5):
-        acbp_mod.acbp_unpack(buf)
-    e.record()
-    e.synchronize()
-    up = s.elapsed_time(e) * 1e3 / 5
+    pk = event_us(torch, lambda _: acbp_mod.acbp_pack(act), flush)
+    up = event_us(torch, lambda _: acbp_mod.acbp_unpack(buf), flush)
     out["acbp_container_vit_fc1"] = {"bytes": buf.numel(), "pack_us": round(pk, 1),
                                      "pack_GBps": round(buf.numel() / pk / 1e3, 1), "unpack_us": round(up, 1),
                                      "unpack_GBps": round(buf.numel() / up / 1e3, 1),
