@@ -487,7 +487,9 @@ def layer_autograd(torch, flush, mod_h, mod_d, x, gy, amp=True):
     out["hlq_bwd_us"] = event_us(torch, lambda y: y.backward(gy), flush, prep=fwd_h)
     out["dense_bwd_us"] = event_us(torch, lambda y: y.backward(gy), flush, prep=fwd_d)
     y = fwd_h()
-    torch.cuda.synchronize()
+    flush.zero_()
+    flush[: 40 * 1024 * 1024].sum()
+    torch.cuda._sleep(3_000_000)  # the whole backward is enqueued before its first kernel runs
     with ops.trace() as tr:
         y.backward(gy)
     out["libhlq_bwd_us"] = round(sum(v["us"] for v in tr.summary().values()), 1)

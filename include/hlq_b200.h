@@ -409,6 +409,10 @@ HLQ_API int hlq_col2im_ex(const void* dcols, int dtype, int64_t ld, int64_t B, i
 /* Workspace bytes needed by hlq_hq_grad_input / hlq_grad_weight. */
 HLQ_API size_t hlq_hq_grad_input_ws(int64_t T, int64_t O, int64_t I);
 HLQ_API size_t hlq_grad_weight_ws(int64_t B, int64_t L, int64_t O, int axis, int rank);
+/* hlq_grad_weight_ws plus the dW GEMM's split-K / K-chunk slabs: required for
+ * contractions past the int32-exact bound (e.g. an 8-bit K > 133,143), which
+ * then run as int64-summed chunks up to the reference's MAX_K (quantize.py:21). */
+HLQ_API size_t hlq_grad_weight_ws_ex(int64_t B, int64_t L, int64_t O, int64_t I, int axis, int rank, int bits);
 
 /* backprop.py:350-370  hq_grad_input(gy, w, bits): dX (T x I) from gy (T x O)
  * and the fp32 weight W (O x I).  dx_dtype HLQ_F32 with HLQ_EPI_EXACT
@@ -424,6 +428,13 @@ HLQ_API int hlq_grad_weight(const int8_t* payload, int64_t ld_payload, const flo
                     const void* gy, int gy_dtype, int64_t B, int64_t L, int64_t O, int64_t I,
                     int axis, uint32_t bitmap, int bits, double extra, void* dw, int dw_dtype,
                     int epilogue, void* ws, size_t ws_bytes, void* stream);
+
+/* Lazy non-finite check (quantize.py:119-120,138-139 raise ValueError on NaN/Inf):
+ * every transform entry point ORs 1 into a per-device sticky word when an
+ * operand's amax is non-finite.  This copies the word to dst (device or
+ * pinned host memory; may be NULL) on `stream` and, with reset, clears it --
+ * stream-ordered, no host synchronisation, CUDA-graph capturable. */
+HLQ_API int hlq_nonfinite_fetch(uint32_t* dst, int reset, void* stream);
 
 #ifdef __cplusplus
 }

@@ -32,4 +32,7 @@ def __getattr__(name):
     if name in ("HLQLinear", "HLQLinearFunction", "convert_linears", "refresh_weight_codes"):
         from . import layers
         return getattr(layers, name)
+    if name in ("NonFiniteGuard", "check_nonfinite", "install_nonfinite_check"):
+        from . import nonfinite
+        return getattr(nonfinite, name)
     raise AttributeError(name)

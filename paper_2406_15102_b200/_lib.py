@@ -49,6 +49,7 @@ SIGNATURES = {
                                  _P, _D, _I, _P, _I, _I64, _P, _I64, _P]),
     "hlq_gemm_i8_ws": (_SZ, [_I64, _I64, _I64, _I64]),
     "hlq_gemm_i8_ws_bits": (_SZ, [_I64, _I64, _I64, _I64, _I, _I]),
+    "hlq_nonfinite_fetch": (_I, [_P, _I, _P]),
     "hlq_acbp_container_bytes": (_I64, [_I64, _I64, _I]),
     "hlq_acbp_ws": (_SZ, [_I64]),
     "hlq_acbp_pack": (_I, [_P, _I64, _I64, _I64, _I, _I, _U32, _I64, _I64, _I64, _P, _P, _I64, _P, _SZ, _P]),
@@ -80,6 +81,7 @@ SIGNATURES = {
     "hlq_acbp_rows": (_I64, [_I64, _I64, _I]),
     "hlq_acbp_compress": (_I, [_P, _I, _I64, _I64, _I64, _I, _U32, _I, _P, _I64, _P, _P, _P]),
     "hlq_hq_grad_input_ws": (_SZ, [_I64, _I64, _I64]),
+    "hlq_grad_weight_ws_ex": (_SZ, [_I64, _I64, _I64, _I64, _I, _I, _I]),
     "hlq_grad_weight_ws": (_SZ, [_I64, _I64, _I64, _I, _I]),
     "hlq_hq_grad_input": (_I, [_P, _I, _I64, _I64, _P, _I64, _I, _P, _I, _I, _P, _SZ, _P]),
     "hlq_grad_weight": (_I, [_P, _I64, _P, _P, _I, _I64, _I64, _I64, _I64, _I, _U32, _I, _D, _P, _I,

@@ -319,6 +319,16 @@ int hlq_gemm_i8_multi(int n, const hlq_gemm_desc* d, void* stream) {
   return HLQ_OK;
 }
 
+int hlq_nonfinite_fetch(uint32_t* dst, int reset, void* stream) {
+  uint32_t* w = hlq::nonfinite_word();
+  if (!w) return fail(HLQ_ERR_CUDA, "non-finite flag unavailable on this device");
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  if (dst && cudaMemcpyAsync(dst, w, sizeof(uint32_t), cudaMemcpyDefault, st) != cudaSuccess)
+    return cuda_status("hlq_nonfinite_fetch");
+  if (reset && cudaMemsetAsync(w, 0, sizeof(uint32_t), st) != cudaSuccess) return cuda_status("hlq_nonfinite_fetch");
+  return HLQ_OK;
+}
+
 size_t hlq_gemm_i8_ws(int64_t M, int64_t N, int64_t K, int64_t groups) {
   if (M <= 0 || N <= 0 || K <= 0 || groups < 1) return 0;
   return hlq::gemm_i8_ws_bytes(M, N, K, groups);
@@ -786,6 +796,12 @@ size_t hlq_grad_weight_ws(int64_t B, int64_t L, int64_t O, int axis, int rank) {
   return align256(size_t(hlq_acbp_rows(L, O, axis) * pad16(k))) + 256;
 }
 
+size_t hlq_grad_weight_ws_ex(int64_t B, int64_t L, int64_t O, int64_t I, int axis, int rank, int bits) {
+  // + the K-chunk slabs of a contraction past the int32-exact bound (hlq_gemm_i8_ws_bits)
+  const int64_t k = hlq_acbp_k(B, L, axis, rank);
+  return hlq_grad_weight_ws(B, L, O, axis, rank) + hlq_gemm_i8_ws_bits(O, I, k, axis == 0 ? L : 1, bits, bits);
+}
+
 int hlq_grad_weight(const int8_t* payload, int64_t ld_payload, const float* x_scale,
                     const void* gy, int gy_dtype, int64_t B, int64_t L, int64_t O, int64_t I,
                     int axis, uint32_t bitmap, int bits, double extra, void* dw, int dw_dtype,
@@ -815,9 +831,12 @@ int hlq_grad_weight(const int8_t* payload, int64_t ld_payload, const float* x_sc
   // axis 0: the transposed projections have L*O rows (l, o) and L*I rows
   // (l, i); the reference's K index (blk, j, l) becomes L stacked K panels.
   const int64_t groups = axis == 0 ? L : 1;
-  return hlq_gemm_i8_grouped(cg, ldk, ldk * O, payload, ld_payload, ld_payload * I, O, I, k, groups,
-                             bits, bits, scale, x_scale, extra, epilogue, dw, dw_dtype, I, nullptr, 0,
-                             stream);
+  // a workspace of hlq_grad_weight_ws_ex bytes also carries the GEMM's split / K-chunk slabs
+  const size_t base = hlq_grad_weight_ws(B, L, O, axis, rank);
+  void* gws = ws_bytes > base ? static_cast<uint8_t*>(ws) + base : nullptr;
+  return hlq_gemm_i8_ex(cg, ldk, ldk * O, payload, ld_payload, ld_payload * I, O, I, k, groups, bits, bits, scale,
+                        x_scale, extra, epilogue, dw, dw_dtype, I, nullptr, 0, gws, gws ? ws_bytes - base : 0,
+                        stream);
 }
 
 }  // extern "C"

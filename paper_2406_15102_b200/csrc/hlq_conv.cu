@@ -39,6 +39,7 @@ struct ConvArgs {
   int8_t* dst;
   int64_t ld_dst;
   float* scale;
+  uint32_t* nonfinite;  // nonfinite_word()
   bool vec;
 };
 
@@ -180,6 +181,7 @@ __global__ void __launch_bounds__(kThreads) im2col_proj_kernel(ConvArgs a) {
   }
   const Quant q = make_quant(a.stats + 2, a.bits);
   if (blockIdx.x == 0 && threadIdx.x == 0 && a.scale) *a.scale = q.s;
+  if (blockIdx.x == 0 && threadIdx.x == 0) flag_nonfinite(q, a.nonfinite);
   if (q.fast)
     im2col_body<T, MODE, BM, true>(a, q, tile, cbuf, cstride, st);
   else
@@ -346,6 +348,7 @@ void launch_im2col_proj(const void* x, int dtype, int B, int H, int W, int C, in
                         int pad, uint32_t bitmap, int bits, int mode, uint32_t* stats, int8_t* dst,
                         int64_t ld_dst, float* scale, cudaStream_t st) {
   ConvArgs a{};
+  a.nonfinite = nonfinite_word();
   a.x = x;
   a.B = B; a.H = H; a.W = W; a.C = C; a.k = k; a.stride = stride; a.pad = pad;
   a.Ho = (H + 2 * pad - k) / stride + 1;

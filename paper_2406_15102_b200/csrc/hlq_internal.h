@@ -12,6 +12,12 @@ enum : int { kEpiExact = 0, kEpiFast = 1 };
 
 int num_sms();
 
+// This device's sticky "a quantized operand held NaN/Inf" word (hlq_transform.cu):
+// every transform kernel ORs 1 into it when an operand's amax bits are
+// non-finite; hlq_nonfinite_fetch copies and resets it (stream-ordered, no
+// host sync) so training can check once per step (quantize.py:119-120,138-139).
+uint32_t* nonfinite_word();
+
 // cudaFuncSetAttribute(MaxDynamicSharedMemorySize) once per (kernel, device):
 // the attribute is per device, so a process driving several GPUs must set it
 // on each.  `done` is the call site's static per-device bitmask.

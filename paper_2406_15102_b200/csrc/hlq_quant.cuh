@@ -163,7 +163,13 @@ struct Quant {
   uint32_t lim16;   // (qmax, qmax) as s16x2
   uint32_t nlim16;  // (-qmax, -qmax) as s16x2
   bool fast;
+  bool nonfinite;  // the operand's amax bits were NaN / Inf
 };
+
+// OR the operand's non-finite status into the device's sticky flag (one thread per operand)
+__device__ __forceinline__ void flag_nonfinite(const Quant& q, uint32_t* word) {
+  if (q.nonfinite && word) atomicOr(word, 1u);
+}
 
 // scale = f32(amax_v) / f32(qmax), 0 -> 1 (quantize.py:94-100), amax_v = RN(0.25 * max|w|)
 // (= max|RN(0.25 w)| because rounding is monotone).
@@ -176,6 +182,7 @@ __device__ __forceinline__ Quant make_quant(const uint32_t* g, int bits) {
   // L1-bypassing loads: in the fused kernel these words were written by other
   // CTAs' atomics just before the grid barrier
   const uint32_t g0 = __ldcg(g), g1 = __ldcg(g + 1);
+  q.nonfinite = g0 >= 0x7F800000u;
   const float amax_w = __uint_as_float(g0);
   const float amax_v = __fmul_rn(amax_w, 0.25f);
   float s = __fdiv_rn(amax_v, q.qmax);

@@ -91,6 +91,7 @@ struct Args {
   int64_t ld_gw;
   float* scale_gx;
   float* scale_gw;
+  uint32_t* nonfinite;  // nonfinite_word()
   int cstride;  // bytes per column in the code staging buffer
 #ifdef HLQ_TR_TRACE
   unsigned long long* trace;  // per CTA: 8 globaltimer stamps (development timeline)
@@ -484,6 +485,8 @@ __device__ __forceinline__ void consume_quant(const Args& a, uint8_t* tiles, uin
   if (blockIdx.x == 0 && threadIdx.x == 0) {
     if (GX && a.scale_gx) *a.scale_gx = qx.s;
     if (GW && a.scale_gw) *a.scale_gw = qw.s;
+    if (GX) flag_nonfinite(qx, a.nonfinite);
+    if (GW) flag_nonfinite(qw, a.nonfinite);
   }
   Stat sx, sw;
   const bool fx = !GX || qx.fast, fw = !GW || qw.fast;
@@ -801,6 +804,20 @@ void launch_colsum(const TransformArgs& t, cudaStream_t st) {
 
 }  // namespace
 
+__device__ uint32_t g_nonfinite_flag;
+
+uint32_t* nonfinite_word() {
+  static uint32_t* addr[64] = {nullptr};
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= 64) return nullptr;
+  if (!addr[dev]) {
+    void* p = nullptr;
+    if (cudaGetSymbolAddress(&p, g_nonfinite_flag) != cudaSuccess) return nullptr;
+    addr[dev] = static_cast<uint32_t*>(p);
+  }
+  return addr[dev];
+}
+
 typedef CUresult (*EncodeIm2colFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
                                    const cuuint64_t*, const int*, const int*, cuuint32_t, cuuint32_t,
                                    const cuuint32_t*, CUtensorMapInterleave, CUtensorMapSwizzle,
@@ -865,6 +882,7 @@ bool launch_conv_acbp_tma(const void* x, int dtype, int B, int H, int W, int C, 
   a.dst_gw = dst;
   a.ld_gw = ld_dst;
   a.scale_gw = scale;
+  a.nonfinite = nonfinite_word();
   a.cstride = a.nb * a.rank + 16;
   if (dtype == kBF16)
     launch_modes<__nv_bfloat16>(map, a, mode, false, true, stream);
@@ -929,6 +947,7 @@ void launch_transform(const TransformArgs& t, int mode, cudaStream_t stream) {
   a.ld_gw = t.ld_gw;
   a.scale_gx = t.scale_gx;
   a.scale_gw = t.scale_gw;
+  a.nonfinite = nonfinite_word();
   a.cstride = a.nb * a.tq * a.rank + 16;
 #ifdef HLQ_TR_TRACE
   a.trace = g_tr_trace;

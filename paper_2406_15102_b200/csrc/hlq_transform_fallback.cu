@@ -256,6 +256,7 @@ __device__ __forceinline__ void reduce_stat_to_global(Stat s, uint32_t* g) {
 struct Quant {
   float s, d, r, lim, qmax;
   bool fast;
+  bool nonfinite;
 };
 
 // scale = f32(amax_v) / f32(qmax), 0 -> 1 (quantize.py:94-100), amax_v = RN(0.25 * max|w|),
@@ -263,6 +264,7 @@ struct Quant {
 __device__ __forceinline__ Quant make_quant(const uint32_t* g, int bits) {
   Quant q;
   q.qmax = float((1 << (bits - 1)) - 1);
+  q.nonfinite = g[0] >= 0x7F800000u;
   const float amax_w = __uint_as_float(g[0]);
   const float amax_v = __fmul_rn(amax_w, 0.25f);
   float s = __fdiv_rn(amax_v, q.qmax);
@@ -337,6 +339,7 @@ struct TileArgs {
   int64_t ld_gw;
   float* scale_gx;
   float* scale_gw;
+  uint32_t* nonfinite;  // nonfinite_word()
   bool vec;
 };
 
@@ -605,6 +608,8 @@ __global__ void __launch_bounds__(kThreads) tile_kernel(TileArgs a) {
   if (blockIdx.x == 0 && threadIdx.x == 0) {
     if (GX && a.scale_gx) *a.scale_gx = qx.s;
     if (GW && a.scale_gw) *a.scale_gw = qw.s;
+    if (GX && qx.nonfinite && a.nonfinite) atomicOr(a.nonfinite, 1u);
+    if (GW && qw.nonfinite && a.nonfinite) atomicOr(a.nonfinite, 1u);
   }
   const bool fx = !GX || qx.fast, fw = !GW || qw.fast;  // uniform across the grid
   if (fx && fw)
@@ -694,6 +699,7 @@ void launch_transform_fallback(const TransformArgs& t, int mode, cudaStream_t st
   a.ld_gw = t.ld_gw;
   a.scale_gx = t.scale_gx;
   a.scale_gw = t.scale_gw;
+  a.nonfinite = nonfinite_word();
   const size_t esz = t.dtype == kBF16 ? 2 : 4;
   a.vec = (reinterpret_cast<uintptr_t>(t.src) % 16 == 0) && ((t.ld_src * esz) % 16 == 0) &&
           ((t.seg_src * esz) % 16 == 0);

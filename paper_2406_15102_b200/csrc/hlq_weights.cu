@@ -47,6 +47,7 @@ struct WBatch {
   WDesc t[kMaxWeights];
   int n, items, bits;
   uint32_t* barrier;
+  uint32_t* nonfinite;  // nonfinite_word()
 };
 
 __device__ __forceinline__ int find_tensor(const WBatch& b, int item) {
@@ -149,6 +150,7 @@ __global__ void __launch_bounds__(kThr) weight_codes_kernel(const __grid_constan
       q = make_quant(d.stats, b.bits);
       cur = ti;
       if (item == d.item0 && threadIdx.x == 0 && d.scale) *d.scale = q.s;
+      if (item == d.item0 && threadIdx.x == 0) flag_nonfinite(q, b.nonfinite);
     }
     const int local = item - d.item0;
     const int blk = local / d.nchunk, c0 = (local - blk * d.nchunk) * kColsPerItem;
@@ -183,6 +185,7 @@ int launch_weight_codes(int n, const float* const* w, const int64_t* O, const in
   }
   b.items = items;
   b.barrier = ws + 8 * n;
+  b.nonfinite = nonfinite_word();
   cudaError_t e = cudaMemsetAsync(ws, 0, size_t(8 * n + 8) * sizeof(uint32_t), stream);
   if (e != cudaSuccess) return int(e);
   int per_sm = 0;
