@@ -89,7 +89,7 @@ HLQ_API int hlq_quantize_ht_cols(const void* src, int dtype, int64_t rows, int64
  * src is `segs` segments of (rows x cols) with row stride ld_src and segment
  * stride seg_src.  Replaces `_project_axis` + `quant_pseudo_stochastic`
  * (backprop.py:223-234; acbp_compress :373-385; hlq_grad_weight :401-407) and,
- * with bitmap 0xFFFF, `_block_axis(w, 0, plan)` (:363).  stats_ws: 32-byte
+ * with bitmap 0xFFFF, `_block_axis(w, 0, plan)` (:363).  stats_ws: HLQ_STATS_WS_BYTES of
  * scratch, the amax bits land in stats_ws[2]. */
 HLQ_API int hlq_quantize_proj_rows(const void* src, int dtype, int64_t segs, int64_t rows, int64_t cols,
                            int64_t ld_src, int64_t seg_src, uint32_t bitmap, int bits,
@@ -101,7 +101,7 @@ HLQ_API int hlq_quantize_proj_rows(const void* src, int dtype, int64_t segs, int
  * the gw codes Q_bits_gw(projection along rows) exactly as
  * hlq_quantize_proj_rows, over the same (segs x rows x cols) view.  Valid when
  * the token axis is the projection axis (reference axis rule L >= 16, or
- * L == 1 with projection along the batch).  stats_ws: 32 bytes. */
+ * L == 1 with projection along the batch).  stats_ws: HLQ_STATS_WS_BYTES. */
 HLQ_API int hlq_quantize_dual(const void* src, int dtype, int64_t segs, int64_t rows, int64_t cols,
                               int64_t ld_src, int64_t seg_src, uint32_t bitmap, int bits_gx,
                               int bits_gw, uint32_t* stats_ws, int8_t* dst_gx, int64_t ld_gx,
@@ -235,7 +235,7 @@ HLQ_API int64_t hlq_acbp_rows(int64_t L, int64_t I, int axis);
 /* backprop.py:373-385  acbp_compress(x, plan, bits, pad_small_axes).
  * x is (B, L, I); axis from ht_axis_for (0 = batch, 1 = tokens).  Payload is
  * written K-major, payload[row * ld_payload + k] (the reference's (K, I)
- * payload, transposed; see hlq_acbp_k).  stats_ws: 32-byte scratch. */
+ * payload, transposed; see hlq_acbp_k).  stats_ws: HLQ_STATS_WS_BYTES of scratch. */
 HLQ_API int hlq_acbp_compress(const void* x, int dtype, int64_t B, int64_t L, int64_t I, int axis,
                       uint32_t bitmap, int bits, int8_t* payload, int64_t ld_payload,
                       float* scale_out, uint32_t* stats_ws, void* stream);
@@ -261,7 +261,7 @@ HLQ_API int hlq_conv_acbp_compress(const void* x_nhwc, int dtype, int64_t B, int
  * K-major per column, as hlq_quantize_proj_rows).  index_kind (rows mode):
  * 0 = the reference quantizes (cols, K) (gy's gw operand), 1 = (K, cols)
  * (ACBP payload, W), 2 = batch-axis gy with L > 1, cols = l2 * o2.
- * stats_ws: 32 bytes (the STATS pass runs inside). */
+ * stats_ws: HLQ_STATS_WS_BYTES (the STATS pass runs inside). */
 HLQ_API int hlq_quantize_stochastic(const void* src, int dtype, int64_t segs, int64_t rows, int64_t cols,
                                     int64_t ld_src, int64_t seg_src, int along_cols, uint32_t bitmap,
                                     int bits, uint64_t seed, uint64_t counter, int index_kind, int64_t l2,

@@ -765,7 +765,7 @@ int hlq_acbp_compress(const void* x, int dtype, int64_t B, int64_t L, int64_t I,
 
 size_t hlq_hq_grad_input_ws(int64_t T, int64_t O, int64_t I) {
   const int64_t op = pad16(O);
-  return align256(size_t(T * op)) + align256(size_t(I * op)) + 256;
+  return align256(size_t(T * op)) + align256(size_t(I * op)) + 2 * HLQ_STATS_WS_BYTES + 256;
 }
 
 int hlq_hq_grad_input(const void* gy, int gy_dtype, int64_t T, int64_t O, const float* w, int64_t I,
@@ -782,10 +782,12 @@ int hlq_hq_grad_input(const void* gy, int gy_dtype, int64_t T, int64_t O, const 
   p += align256(size_t(T * op));
   int8_t* cw = reinterpret_cast<int8_t*>(p);
   p += align256(size_t(I * op));
-  uint32_t* stats = reinterpret_cast<uint32_t*>(p);    // [0..7] gy, [8..15] w
-  float* scales = reinterpret_cast<float*>(p + 64);  // [0] gy, [1] w
+  // one HLQ_STATS_WS_BYTES scratch per transform (statistics, grid barrier, work tickets)
+  uint32_t* stats = reinterpret_cast<uint32_t*>(p);                             // gy
+  uint32_t* stats_w = reinterpret_cast<uint32_t*>(p + HLQ_STATS_WS_BYTES);      // w
+  float* scales = reinterpret_cast<float*>(p + 2 * HLQ_STATS_WS_BYTES);         // [0] gy, [1] w
   HLQ_TRY(hlq_quantize_ht_cols(gy, gy_dtype, T, O, O, bits, stats, cg, op, scales, stream));
-  HLQ_TRY(hlq_quantize_proj_rows(w, HLQ_F32, 1, O, I, I, O * I, 0xFFFFu, bits, stats + 8, cw, op,
+  HLQ_TRY(hlq_quantize_proj_rows(w, HLQ_F32, 1, O, I, I, O * I, 0xFFFFu, bits, stats_w, cw, op,
                                  scales + 1, stream));
   return hlq_gemm_i8(cg, op, cw, op, T, I, op, bits, bits, scales, scales + 1, 1.0, epilogue, dx,
                      dx_dtype, I, nullptr, 0, stream);
@@ -793,7 +795,7 @@ int hlq_hq_grad_input(const void* gy, int gy_dtype, int64_t T, int64_t O, const 
 
 size_t hlq_grad_weight_ws(int64_t B, int64_t L, int64_t O, int axis, int rank) {
   const int64_t k = hlq_acbp_k(B, L, axis, rank);
-  return align256(size_t(hlq_acbp_rows(L, O, axis) * pad16(k))) + 256;
+  return align256(size_t(hlq_acbp_rows(L, O, axis) * pad16(k))) + HLQ_STATS_WS_BYTES + 256;
 }
 
 size_t hlq_grad_weight_ws_ex(int64_t B, int64_t L, int64_t O, int64_t I, int axis, int rank, int bits) {
@@ -820,8 +822,8 @@ int hlq_grad_weight(const int8_t* payload, int64_t ld_payload, const float* x_sc
   uint8_t* p = static_cast<uint8_t*>(ws);
   int8_t* cg = reinterpret_cast<int8_t*>(p);
   p += align256(size_t(hlq_acbp_rows(L, O, axis) * ldk));
-  uint32_t* stats = reinterpret_cast<uint32_t*>(p);
-  float* scale = reinterpret_cast<float*>(p + 64);
+  uint32_t* stats = reinterpret_cast<uint32_t*>(p);                      // HLQ_STATS_WS_BYTES
+  float* scale = reinterpret_cast<float*>(p + HLQ_STATS_WS_BYTES);
   if (axis == 1)
     HLQ_TRY(hlq_quantize_proj_rows(gy, gy_dtype, B, L, O, O, L * O, bitmap, bits, stats, cg, ldk,
                                    scale, stream));

@@ -110,7 +110,7 @@ class Binding:
         k = self.lib.hlq_acbp_k(B, L, axis, rank)
         rows = self.lib.hlq_acbp_rows(L, I, axis)
         ld = max((k + 15) // 16 * 16, 16)
-        d_x, d_pay, d_s, d_st = self.put(x.astype(np.float32)), self.dev(rows * ld), self.dev(4), self.dev(64)
+        d_x, d_pay, d_s, d_st = self.put(x.astype(np.float32)), self.dev(rows * ld), self.dev(4), self.dev(512)  # HLQ_STATS_WS_BYTES
         self.check(self.lib.hlq_acbp_compress(d_x, 0, B, L, I, axis, bitmap, bits, d_pay, ld, d_s, d_st, None))
         return (d_pay, ld, d_s), self.get(d_pay, (rows, ld), np.int8)[:, :k], self.get(d_s, (1,), np.float32)[0], k
 
