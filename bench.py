@@ -46,6 +46,10 @@ def parse():
     ap.add_argument("--batch", type=int, default=BATCH, help="images per GPU")
     ap.add_argument("--no-extras", action="store_true", help="skip dense/layer/cpu side measurements")
     ap.add_argument("--dist-backend", default="nccl", choices=["nccl", "gloo"])
+    ap.add_argument("--dp-mode", default="replica", choices=["replica", "exact"],
+                    help="N > 1: replica = DDP fp32 dW all-reduce with shard-local scales; exact = global scales "
+                         "(all-reduce MAX of the statistics) and int32 dW accumulator all-reduce inside the HLQ "
+                         "layers, bit-equal to one process on the whole batch (dp.enable_exact_dp)")
     return ap.parse_args()
 
 
@@ -204,6 +208,7 @@ def workload_config(args, world):
     return {"workload": "vit_b16_finetune_step (BASELINE configs[3])", "model": "ViT-B/16",
             "global_batch": args.batch * world, "per_gpu_batch": args.batch, "seq_len": TOKENS,
             "image": IMG, "parallelism": f"dp{world}", "amp": "bf16",
+            "dp_mode": getattr(args, "dp_mode", "replica") if world > 1 else None,
             "hlq": "gx int4 HQ (block 16), gw int8 HLA rank 8, ACBP int8; 49 Linear layers",
             "l2": "per-step working set (activations, codes) >> 126 MB L2; no flush needed"}
 
@@ -700,6 +705,10 @@ def run_ours(args):
     B = args.batch
     model = make_model(torch, hlq=True)
     if dist is not None:
+        if args.dp_mode == "exact":
+            from paper_2406_15102_b200.dp import enable_exact_dp
+            ignore = enable_exact_dp(model)  # the HLQ weights' dW is all-reduced inside the layers
+            torch.nn.parallel.DistributedDataParallel._set_params_and_buffers_to_ignore_for_model(model, ignore)
         model = torch.nn.parallel.DistributedDataParallel(model, device_ids=[local],
                                                           gradient_as_bucket_view=True)
     opt = torch.optim.SGD(model.parameters(), lr=1e-3, momentum=0.9, foreach=True)

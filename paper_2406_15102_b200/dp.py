@@ -54,6 +54,102 @@ class Reducer:
         return acc
 
 
+class ExactDP:
+    """The exact (global-scale) data-parallel mode of the HLQ autograd modules.
+
+    Attached to every HLQLinear of a model by enable_exact_dp(); the layer's
+    forward ACBP and backward gy transform then run as STATS pass ->
+    all-reduce(MAX) of the 16-byte statistics -> QUANT pass, so every rank
+    quantizes with the scale the single-process reference computes over the
+    whole batch (quantize.py:94-100), and dW is the all-reduce(SUM) of the
+    exact int32 accumulators followed by one dequant (backprop.py:407-410).
+    The accumulator all-reduce is asynchronous: the layer's dX GEMM (local
+    rows, no communication) runs under it.  dW comes back already averaged
+    over ranks (torch's mean-loss convention), so the HLQ weights are excluded
+    from DDP; every other parameter stays with DDP."""
+
+    def __init__(self, group=None):
+        self.group = group
+        self.reducer = Reducer(group)
+        self.world = dist.get_world_size(group)
+
+    def quant_rows(self, src, segs, rows, cols, ld_src, seg_src, bitmap, bits):
+        """Global-scale projection along rows (the ACBP of X): codes (cols, pad16(K)), K, scale."""
+        dev = src.device
+        st = ops.new_stats(dev)
+        ops.transform_pass(src, segs, rows, cols, ld_src, seg_src, False, True, bitmap, bits, bits, 0, st)
+        self.reducer.max_stats(st)
+        k = ops.proj_rows_k(segs, rows, bin(bitmap).count("1"))
+        codes = torch.empty((cols, max(ops.pad16(k), 16)), dtype=torch.int8, device=dev)
+        scale = torch.empty(1, dtype=torch.float32, device=dev)
+        ops.transform_pass(src, segs, rows, cols, ld_src, seg_src, False, True, bitmap, bits, bits, 1, st,
+                           dst_gw=codes, scale_gw=scale)
+        return codes, k, scale
+
+    def quant_gy(self, gy3, axis, bitmap, bits_gx, bits_gw):
+        """Both gy operands with global scales: (gx codes (T, pad16(O)), gx scale,
+        gw codes (O, pad16(K)), K, gw scale)."""
+        B, L, O = gy3.shape
+        dev = gy3.device
+        segs, rows, cols, ld, sg = _proj_view(B, L, O, axis)
+        k = ops.proj_rows_k(segs, rows, bin(bitmap).count("1"))
+        cgx = torch.empty((B * L, ops.pad16(O)), dtype=torch.int8, device=dev)
+        cgw = torch.empty((cols, max(ops.pad16(k), 16)), dtype=torch.int8, device=dev)
+        scales = torch.empty(2, dtype=torch.float32, device=dev)
+        st = ops.new_stats(dev)
+        dual = dual_ok(B, L, axis)
+        if dual:
+            ops.transform_pass(gy3, segs, rows, cols, ld, sg, True, True, bitmap, bits_gx, bits_gw, 0, st)
+        else:
+            ops.transform_pass(gy3, 1, B * L, O, O, B * L * O, True, False, 0xFFFF, bits_gx, bits_gx, 0, st)
+            ops.transform_pass(gy3, segs, rows, cols, ld, sg, False, True, bitmap, bits_gw, bits_gw, 0, st)
+        self.reducer.max_stats(st)
+        if dual:
+            ops.transform_pass(gy3, segs, rows, cols, ld, sg, True, True, bitmap, bits_gx, bits_gw, 1, st,
+                               dst_gx=cgx, dst_gw=cgw, scale_gx=scales[0:1], scale_gw=scales[1:2])
+        else:
+            ops.transform_pass(gy3, 1, B * L, O, O, B * L * O, True, False, 0xFFFF, bits_gx, bits_gx, 1, st,
+                               dst_gx=cgx, scale_gx=scales[0:1])
+            ops.transform_pass(gy3, segs, rows, cols, ld, sg, False, True, bitmap, bits_gw, bits_gw, 1, st,
+                               dst_gw=cgw, scale_gw=scales[1:2])
+        return cgx, scales[0:1], cgw, k, scales[1:2]
+
+    def reduce_acc_async(self, acc: torch.Tensor, k_local: int, groups: int, bits: int):
+        """Start the all-reduce(SUM) of the int32 dW accumulator; widened to
+        int64 when the global contraction could overflow int32.  Returns
+        (tensor being reduced, work handle)."""
+        qmax = (1 << (bits - 1)) - 1
+        if k_local * groups * self.world * qmax * qmax >= 2 ** 31:
+            acc = acc.to(torch.int64)
+        work = dist.all_reduce(acc, op=dist.ReduceOp.SUM, group=self.group, async_op=True)
+        return acc, work
+
+    def dequant_fast(self, acc, sa, sb, out_dtype=torch.float32):
+        """The GEMM's fast epilogue on the summed accumulator:
+        f32(acc) * f32(f64(f32(sa*sb)) / world)  (1/world: torch's mean over ranks)."""
+        scale = ((sa.float() * sb.float()).to(torch.float64) * (1.0 / self.world)).to(torch.float32)
+        return (acc.to(torch.float32) * scale).to(out_dtype)
+
+
+def enable_exact_dp(model: torch.nn.Module, group=None):
+    """Switch every HLQLinear under `model` to the exact data-parallel mode
+    and return the parameter names DDP must ignore (their gradients are
+    all-reduced inside the layers):
+
+        names = enable_exact_dp(model)
+        DistributedDataParallel._set_params_and_buffers_to_ignore_for_model(model, names)
+        model = DistributedDataParallel(model, ...)
+    """
+    from .layers import HLQLinear
+    dp = ExactDP(group)
+    names = []
+    for name, m in model.named_modules():
+        if isinstance(m, HLQLinear):
+            m.dp = dp
+            names.append(f"{name}.weight" if name else "weight")
+    return names
+
+
 def dequant(acc: torch.Tensor, sa: torch.Tensor, sb: torch.Tensor, extra: float) -> torch.Tensor:
     """out = f32(f64(acc) * (f64(f32(sa * sb)) * extra)) -- quantize.py:181-187."""
     comb = (sa.float() * sb.float()).to(torch.float64)

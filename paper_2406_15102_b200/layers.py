@@ -84,7 +84,7 @@ class HLQLinearFunction(torch.autograd.Function):
     weight)."""
 
     @staticmethod
-    def forward(ctx, x, weight, bias, strategy: BackwardStrategy, wcodes=None, calib_layer=None):
+    def forward(ctx, x, weight, bias, strategy: BackwardStrategy, wcodes=None, calib_layer=None, dp=None):
         B, L, I = _blv(x.shape)
         O = weight.shape[0]
         plan = strategy.plan
@@ -98,7 +98,14 @@ class HLQLinearFunction(torch.autograd.Function):
         payload = sx = cw = sw = None
         k = 0
         with torch.cuda.stream(side):
-            if ctx.needs_input_grad[1]:
+            if ctx.needs_input_grad[1] and dp is not None:
+                # exact data-parallel mode: the scale of the WHOLE batch's projection (dp.ExactDP)
+                if axis == 0 and B % plan.block_size:
+                    raise ParameterError("exact DP with the batch-axis projection needs shards of a multiple "
+                                         f"of {plan.block_size} samples, got {B}")
+                payload, k, sx = dp.quant_rows(x.detach().contiguous(), segs, rows, cols, ld_src, seg_src,
+                                               plan.gpu_bitmap(), bits_gw)
+            elif ctx.needs_input_grad[1]:
                 payload, k, sx, _ = ops.quant_proj_rows(x.detach().contiguous(), segs, rows, cols,
                                                         plan.gpu_bitmap(), bits_gw, ld_src, seg_src)
             if ctx.needs_input_grad[0] and wcodes is not None:
@@ -121,6 +128,7 @@ class HLQLinearFunction(torch.autograd.Function):
         ctx.save_for_backward(weight, payload, sx, cw, sw)
         ctx.meta = (B, L, I, axis, k, x.dtype, tuple(x.shape), bias is not None, strategy)
         ctx.calib_layer = calib_layer
+        ctx.dp = dp
         return y
 
     @staticmethod
@@ -138,6 +146,8 @@ class HLQLinearFunction(torch.autograd.Function):
         bits_gx = strategy.grad_input_path.bits or 4
         bits_gw = strategy.grad_weight_path.bits or 8
         out_dtype = x_dtype if x_dtype in (torch.float32, torch.bfloat16) else torch.float32
+        if ctx.dp is not None and ctx.needs_input_grad[1]:
+            return _exact_dp_backward(ctx, gy, gy3, weight, payload, sx, cw_saved, sw_saved)
         if ctx.needs_input_grad[0] and ctx.needs_input_grad[1] and dual_ok(B, L, axis):
             # one fused transform of gy feeds both products (2 reads of gy instead of 4)
             segs, rows, cols, ld_src, seg_src = _proj_view(B, L, O, axis)
@@ -180,7 +190,7 @@ class HLQLinearFunction(torch.autograd.Function):
             gx = gx.reshape(x_shape).to(x_dtype)
             if want_gb:
                 gb = cs[0]
-            return gx, gw, gb, None, None, None
+            return gx, gw, gb, None, None, None, None
         if ctx.needs_input_grad[1]:
             bits = strategy.grad_weight_path.bits or 8
             segs, rows, cols, ld_src, seg_src = _proj_view(B, L, O, axis)
@@ -204,7 +214,33 @@ class HLQLinearFunction(torch.autograd.Function):
                 gx = gx.to(x_dtype)
         if has_bias and ctx.needs_input_grad[2]:
             gb = gy.reshape(-1, O).sum(0, dtype=torch.float32)
-        return gx, gw, gb, None, None, None
+        return gx, gw, gb, None, None, None, None
+
+
+def _exact_dp_backward(ctx, gy, gy3, weight, payload, sx, cw, sw):
+    """HLQLinearFunction.backward in the exact data-parallel mode (dp.ExactDP):
+    global-scale gy codes, dW = all-reduce(SUM) of the int32 accumulators
+    (asynchronous, overlapped with the local dX GEMM) + one dequant."""
+    B, L, I, axis, k, x_dtype, x_shape, has_bias, strategy = ctx.meta
+    dp = ctx.dp
+    O = weight.shape[0]
+    bits_gx = strategy.grad_input_path.bits or 4
+    bits_gw = strategy.grad_weight_path.bits or 8
+    cgx, sgx, cg, kg, sg = dp.quant_gy(gy3, axis, strategy.plan.gpu_bitmap(), bits_gx, bits_gw)
+    groups = L if axis == 0 else 1
+    _, acc = ops.gemm_i8(cg, payload, O, I, k, bits_gw, bits_gw, sg, sx, 1.0, want_acc=True, want_out=False,
+                         groups=groups, a_gstride=cg.stride(0) * O, b_gstride=payload.stride(0) * I)
+    acc, work = dp.reduce_acc_async(acc, k, groups, bits_gw)
+    gx = None
+    if ctx.needs_input_grad[0]:
+        out_dtype = x_dtype if x_dtype in (torch.float32, torch.bfloat16) else torch.float32
+        gx, _ = ops.gemm_i8(cgx, cw, B * L, I, ops.pad16(O), bits_gx, bits_gx, sgx, sw, 1.0, exact=False,
+                            out_dtype=out_dtype)
+        gx = gx.reshape(x_shape).to(x_dtype)
+    work.wait()
+    gw = dp.dequant_fast(acc, sg, sx, weight.dtype)
+    gb = gy.reshape(-1, O).sum(0, dtype=torch.float32) if has_bias and ctx.needs_input_grad[2] else None
+    return gx, gw, gb, None, None, None, None
 
 
 class BaselineLinearFunction(torch.autograd.Function):
@@ -243,6 +279,7 @@ class HLQLinear(nn.Linear):
         self.strategy = strategy or BackwardStrategy.hlq()
         self._wcodes = None  # (weight version, data_ptr, bits, codes, scale)
         self._hlq_weight_codes = True  # refreshed in batch by refresh_weight_codes
+        self.dp = None  # dp.ExactDP when the exact data-parallel mode is on (dp.enable_exact_dp)
 
     def bits_gx(self) -> int:
         return self.strategy.grad_input_path.bits or 4
@@ -265,7 +302,7 @@ class HLQLinear(nn.Linear):
             if not self.strategy.is_hlq:
                 return BaselineLinearFunction.apply(x, self.weight, self.bias, self.strategy)
             return HLQLinearFunction.apply(x, self.weight, self.bias, self.strategy, self.cached_weight_codes(),
-                                           self if _CALIB[0] is not None else None)
+                                           self if _CALIB[0] is not None else None, self.dp)
 
     @classmethod
     def from_linear(cls, lin: nn.Linear, strategy: BackwardStrategy | None = None) -> "HLQLinear":

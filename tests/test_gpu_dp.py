@@ -63,3 +63,88 @@ def test_global_scale_dp_world2(case):
         p.join(timeout=60)
     for r in res:
         assert r[0] == "ok", r
+
+
+# ---------------------------------------------------------------------------
+# the exact mode in the TRAINING path: HLQLinear modules under enable_exact_dp,
+# stepped by bench.py's train_steps loop, two ranks on one GPU (gloo)
+# ---------------------------------------------------------------------------
+
+def _tiny_vit():
+    from paper_2406_15102_b200.layers import convert_linears
+    from paper_2406_15102_b200.vit import ViT
+    torch.manual_seed(0)
+    m = ViT(image=32, patch=8, dim=64, depth=2, heads=2, mlp=256, classes=10).cuda()
+    convert_linears(m)
+    # only the HLQ weights train: every other gradient is a cross-sample
+    # reduction whose fp32 summation order differs between 1 and 2 ranks
+    for n, p in m.named_parameters():
+        p.requires_grad_(n.endswith("weight") and ("blocks" in n or n.startswith("head")) and p.dim() == 2)
+    return m
+
+
+def _run_steps(model, x, y, steps=2):
+    import bench
+    from torch.nn.attention import SDPBackend, sdpa_kernel
+    opt = torch.optim.SGD([p for p in model.parameters() if p.requires_grad], lr=0.5)
+    F = torch.nn.functional
+    with sdpa_kernel(SDPBackend.MATH):  # deterministic attention backward
+        with torch.autocast("cuda", dtype=torch.bfloat16):
+            loss = F.cross_entropy(model(x).float(), y)
+        loss.backward()
+        g1 = {n: p.grad.detach().clone() for n, p in model.named_parameters() if p.requires_grad}
+        opt.step()
+        opt.zero_grad(set_to_none=True)
+        bench.train_steps(torch, model, opt, x, y, steps - 1)  # the benchmark's own step loop
+    torch.cuda.synchronize()
+    w = {n: p.detach().clone() for n, p in model.named_parameters() if p.requires_grad}
+    return g1, w
+
+
+def _exact_worker(rank, world, port, q):
+    try:
+        import sys
+        import torch.distributed as dist
+        sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+        os.environ["MASTER_ADDR"] = "127.0.0.1"
+        os.environ["MASTER_PORT"] = str(port)
+        torch.cuda.set_device(0)
+        g = torch.Generator(device="cuda").manual_seed(7)
+        X = torch.randn(32, 3, 32, 32, device="cuda", generator=g)
+        Y = torch.randint(0, 10, (32,), device="cuda", generator=g)
+        # single-process reference run on the whole batch (the ordinary HLQ path)
+        ref_g, ref_w = _run_steps(_tiny_vit(), X, Y)
+        dist.init_process_group("gloo", rank=rank, world_size=world)
+        from paper_2406_15102_b200.dp import enable_exact_dp
+        model = _tiny_vit()
+        names = enable_exact_dp(model)
+        assert len(names) == 2 * 4 + 1
+        half = 32 // world
+        sl = slice(rank * half, (rank + 1) * half)
+        g1, w = _run_steps(model, X[sl].contiguous(), Y[sl].contiguous())
+        bad = [n for n in ref_g if not torch.equal(g1[n], ref_g[n])]
+        badw = [n for n in ref_w if not torch.equal(w[n], ref_w[n])]
+        q.put(("ok" if not bad and not badw else "mismatch", rank, bad[:4], badw[:4]))
+        dist.barrier()
+        dist.destroy_process_group()
+    except Exception as e:  # noqa: BLE001
+        import traceback
+        q.put(("err", rank, traceback.format_exc()[-1500:]))
+
+
+def test_exact_dp_training_steps_world2():
+    """Two ranks x 16 images == one process x 32 images, bit for bit: the
+    step-1 dW of every HLQ layer and the HLQ weights after 2 SGD steps."""
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_exact_worker, args=(r, 2, port, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    res = [q.get(timeout=600) for _ in range(2)]
+    for p in procs:
+        p.join(timeout=60)
+    for r in res:
+        assert r[0] == "ok", r
