@@ -289,6 +289,39 @@ def traffic_for(key: str):
     return None
 
 
+def sweep_summary():
+    """BASELINE configs[4] (shape sweep) summary from the committed
+    profiles/*_sweep.jsonl (tools/sweep_e.py on a B200: 240 points, tokens
+    2K-64K x hidden 768-8192 x r 1/2/4/8 x bf16/fp32 I/O, HLQLinear autograd vs
+    dense bf16 nn.Linear), or None."""
+    import glob
+    import math
+    paths = sorted(glob.glob(os.path.join(ROOT, "profiles", "*_sweep.jsonl")))
+    if not paths:
+        return None
+    rows = [json.loads(line) for line in open(paths[-1]) if line.strip()]
+    meta = next((r for r in rows if r.get("meta")), {})
+    pts = [r for r in rows if not r.get("meta")]
+    gm = lambda v: round(math.exp(sum(math.log(x) for x in v) / len(v)), 3)  # noqa: E731
+    out = {"file": os.path.relpath(paths[-1], ROOT), "points": len(pts), "gpu": meta.get("gpu"),
+           "int8_tops": meta.get("int8_tops"), "hbm_gbs": meta.get("hbm_gbs"), "by_io_rank": {}}
+    for io in ("bf16", "fp32"):
+        for r in (1, 2, 4, 8):
+            s = [p for p in pts if p["io"] == io and p["rank"] == r]
+            if s:
+                out["by_io_rank"][f"{io}_r{r}"] = {
+                    "bwd_speedup_geomean": gm([p["bwd_speedup"] for p in s]),
+                    "total_speedup_geomean": gm([p["total_speedup"] for p in s]),
+                    "roofline_frac_geomean": gm([p["roofline_frac"] for p in s]),
+                    "bwd_speedup_range": [min(p["bwd_speedup"] for p in s), max(p["bwd_speedup"] for p in s)]}
+    by_h = {}
+    for p in pts:
+        if p["io"] == "bf16" and p["rank"] == 8:
+            by_h.setdefault(p["hidden"], []).append(p["bwd_speedup"])
+    out["bf16_r8_bwd_speedup_geomean_by_hidden"] = {str(h): gm(v) for h, v in sorted(by_h.items())}
+    return out
+
+
 def measured_peaks():
     p = os.path.join(ROOT, "MEASURED_PEAKS.json")
     if os.path.exists(p):
@@ -477,21 +510,35 @@ def layer_autograd(torch, flush, mod_h, mod_d, x, gy, amp=True):
                                                                                                   enabled=False))
     xr = x.detach().requires_grad_(True)
 
+    def fresh(mod):
+        # a step's backward WRITES the gradients (no accumulation into a previous rep's)
+        xr.grad = None
+        for p in mod.parameters():
+            p.grad = None
+
     def fwd_h():
+        fresh(mod_h)
         with ac():
             return mod_h[0](xr) if isinstance(mod_h, torch.nn.Sequential) else mod_h(xr)
 
     def fwd_d():
+        fresh(mod_d)
         with ac():
             return mod_d(xr)
     with ac():
         refresh_weight_codes(mod_h, force=True)
     out = {}
     out["hlq_fwd_us"] = event_us(torch, lambda _: fwd_h(), flush)
-    out["dense_fwd_us"] = event_us(torch, lambda _: fwd_d(), flush)
     out["hlq_bwd_us"] = event_us(torch, lambda y: y.backward(gy), flush, prep=fwd_h)
-    out["dense_bwd_us"] = event_us(torch, lambda y: y.backward(gy), flush, prep=fwd_d)
-    y = fwd_h()
+    if mod_d is not None:
+        out["dense_fwd_us"] = event_us(torch, lambda _: fwd_d(), flush)
+        out["dense_bwd_us"] = event_us(torch, lambda y: y.backward(gy), flush, prep=fwd_d)
+    flush.zero_()
+    flush[: 40 * 1024 * 1024].sum()
+    torch.cuda._sleep(3_000_000)  # the whole forward is enqueued before its first kernel runs
+    with ops.trace() as trf:
+        y = fwd_h()
+    out["libhlq_fwd_us"] = round(sum(v["us"] for v in trf.summary().values()), 1)
     flush.zero_()
     flush[: 40 * 1024 * 1024].sum()
     torch.cuda._sleep(3_000_000)  # the whole backward is enqueued before its first kernel runs
@@ -501,9 +548,12 @@ def layer_autograd(torch, flush, mod_h, mod_d, x, gy, amp=True):
     out["libhlq_bwd_kernels"] = {k: {"us": round(v["us"], 1), "calls": v["calls"]}
                                  for k, v in tr.summary(by="key").items()}
     for k in ("hlq_fwd_us", "dense_fwd_us", "hlq_bwd_us", "dense_bwd_us"):
-        out[k] = round(out[k], 1)
-    out["bwd_speedup"] = round(out["dense_bwd_us"] / out["hlq_bwd_us"], 3)
-    out["fwd_overhead_us"] = round(out["hlq_fwd_us"] - out["dense_fwd_us"], 1)
+        if k in out:
+            out[k] = round(out[k], 1)
+    if mod_d is not None:
+        out["bwd_speedup"] = round(out["dense_bwd_us"] / out["hlq_bwd_us"], 3)
+        out["fwd_overhead_us"] = round(out["hlq_fwd_us"] - out["dense_fwd_us"], 1)
+    out["acbp_fwd_us"] = out.pop("libhlq_fwd_us")  # the HLQ-only forward kernels (ACBP of X)
     return out
 
 
@@ -812,6 +862,7 @@ def run_ours(args):
         torch.cuda.empty_cache()
         if rank == 0:
             line["layer_bwd"] = layer_bwd_table(torch)
+            line["sweep_e"] = sweep_summary()
             line["config_bwd"] = config_table(torch)
             try:
                 line["resnet18_cifar_train"] = resnet_table(torch)
