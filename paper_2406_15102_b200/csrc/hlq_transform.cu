@@ -337,15 +337,24 @@ __device__ __forceinline__ void consume(const Args& a, const Quant& qx, const Qu
             for (int i = 0; i < 16; ++i)
               if (i >= rvalid) pv[i] = make_float2(0.0f, 0.0f);
           }
-          if (MODE == kStats && a.cs_part) {
-            // column sums of the 16 rows (pairwise tree), accumulated over the item
+          // column sums of the 16 rows, accumulated over the item (the bias gradient):
+          // the un-normalised DC coefficient of the projection butterfly IS the pairwise
+          // tree ((x0+x1)+(x2+x3))+... in the same order (stages h = 1, 2, 4, 8), so
+          // when basis 0 is kept the sum comes for free from pv[0]; otherwise the tree
+          const bool dc_kept = (bitmap & 1u) != 0;
+          float2 blk_sum = make_float2(0.0f, 0.0f);
+          if (MODE == kStats && a.cs_part && !dc_kept) {
             float2 t[8];
 #pragma unroll
             for (int i = 0; i < 8; ++i) t[i] = f2add(pv[2 * i], pv[2 * i + 1]);
 #pragma unroll
             for (int i = 0; i < 4; ++i) t[i] = f2add(t[2 * i], t[2 * i + 1]);
-            t[0] = f2add(f2add(t[0], t[1]), f2add(t[2], t[3]));
-            csum = it.bl == 0 ? t[0] : f2add(csum, t[0]);
+            blk_sum = f2add(f2add(t[0], t[1]), f2add(t[2], t[3]));
+          }
+          fwht16_pair(pv);
+          if (MODE == kStats && a.cs_part) {
+            if (dc_kept) blk_sum = pv[0];
+            csum = it.bl == 0 ? blk_sum : f2add(csum, blk_sum);
             if (it.bl == it.nbl - 1) {
               // column-major partials: a column's groups are contiguous for the final sum
               // (rg: one partial per sub-tile position q of the item's steps)
@@ -355,7 +364,6 @@ __device__ __forceinline__ void consume(const Args& a, const Quant& qx, const Qu
               if (oc + 1 < a.cols) o[a.groups] = csum.y;
             }
           }
-          fwht16_pair(pv);
           if (MODE == kStats) {
 #pragma unroll
             for (int i = 0; i < 16; ++i)

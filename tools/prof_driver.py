@@ -29,6 +29,8 @@ def main():
     for _ in range(reps):
         if what == "dual":
             ops.quant_dual(gy, segs, rows, O, 0x5555, 4, 8, O, L * O)
+        elif what == "dualcs":  # as the training path runs it: with the bias-gradient column sums
+            ops.quant_dual(gy, segs, rows, O, 0x5555, 4, 8, O, L * O, colsum=True)
         elif what == "acbp":
             ops.quant_proj_rows(x, segs, rows, I, 0x5555, 8, I, L * I)
         elif what == "w":
