@@ -121,6 +121,17 @@ HLQ_API int hlq_quantize_dual_colsum(const void* src, int dtype, int64_t segs, i
                                      int8_t* dst_gw, int64_t ld_gw, float* scale_gx, float* scale_gw,
                                      float* colsum_out, void* colsum_ws, size_t colsum_ws_bytes, void* stream);
 
+/* hlq_quantize_dual_colsum with the gx codes optionally PACKED int4 (pack_gx = 1,
+ * bits_gx = 4): two codes per byte, low nibble first (acbp.py:56-61), row
+ * stride ld_gx bytes >= pad16(cols) / 2 (a multiple of 16) -- the A operand of
+ * hlq_gemm_i4a_ex / hlq_gemm_desc.a_packed.  colsum_out may be NULL (no column
+ * sums).  Same codes and scales as the int8 form. */
+HLQ_API int hlq_quantize_dual_ex(const void* src, int dtype, int64_t segs, int64_t rows, int64_t cols,
+                                 int64_t ld_src, int64_t seg_src, uint32_t bitmap, int bits_gx, int bits_gw,
+                                 uint32_t* stats_ws, void* dst_gx, int64_t ld_gx, int pack_gx, int8_t* dst_gw,
+                                 int64_t ld_gw, float* scale_gx, float* scale_gw, float* colsum_out,
+                                 void* colsum_ws, size_t colsum_ws_bytes, void* stream);
+
 /* The two passes of hlq_quantize_proj_rows, separately, for the data-parallel
  * global-scale mode: _amax accumulates (atomic max, no reset) the transformed
  * statistics into stats[2..3] (stats: 4 x uint32, zero-initialised by the
@@ -194,6 +205,18 @@ HLQ_API int hlq_gemm_i8_ex(const int8_t* A, int64_t lda, int64_t a_gstride, cons
                            int32_t* acc_out, int64_t ld_acc, void* ws, size_t ws_bytes,
                            void* stream);
 
+/* hlq_gemm_i8_ex with the A operand as PACKED int4 codes: two codes per byte,
+ * low nibble first (the ACBP container's nibble order, acbp.py:56-61), i.e.
+ * A[m, k] is the signed nibble (k & 1 ? high : low) of byte A[m * lda + k/2];
+ * lda (bytes, a multiple of 16) >= ceil(K/2).  bits_a must be 4.  The GEMM
+ * sign-extends the nibbles to int8 in shared memory ahead of the tcgen05
+ * kind::i8 MMAs (sm_100a has no int4 MMA): half the A bytes of the int8 form,
+ * same results bit for bit. */
+HLQ_API int hlq_gemm_i4a_ex(const uint8_t* A, int64_t lda, int64_t a_gstride, const int8_t* B, int64_t ldb,
+                            int64_t b_gstride, int64_t M, int64_t N, int64_t K, int64_t groups, int bits_b,
+                            const float* sa, const float* sb, double extra, int epilogue, void* out,
+                            int out_dtype, int64_t ldo, void* ws, size_t ws_bytes, void* stream);
+
 /* One product for hlq_gemm_i8_multi (fields as in hlq_gemm_i8_grouped). */
 typedef struct {
   const int8_t* A;
@@ -211,6 +234,7 @@ typedef struct {
   int64_t ldo;
   int32_t* acc_out;
   int64_t ld_acc;
+  int a_packed;  /* 1: A holds packed int4 codes (see hlq_gemm_i4a_ex); bits_a must be 4 */
 } hlq_gemm_desc;
 
 /* n (1 or 2) independent products -- typically a layer's dX and dW GEMMs --

@@ -57,6 +57,10 @@ SIGNATURES = {
     "hlq_acbp_unpack": (_I, [_P, _I64, _P, _P, _I64, _P, _P, _SZ, _P]),
     "hlq_last_error_offset": (_I64, []),
     "hlq_gemm_i8_multi": (_I, [_I, _P, _P]),
+    "hlq_gemm_i4a_ex": (_I, [_P, _I64, _I64, _P, _I64, _I64, _I64, _I64, _I64, _I64, _I, _P, _P, _D, _I, _P,
+                             _I, _I64, _P, _SZ, _P]),
+    "hlq_quantize_dual_ex": (_I, [_P, _I, _I64, _I64, _I64, _I64, _I64, _U32, _I, _I, _P, _P, _I64, _I, _P, _I64,
+                                  _P, _P, _P, _P, _SZ, _P]),
     "hlq_gemm_i8_ex": (_I, [_P, _I64, _I64, _P, _I64, _I64, _I64, _I64, _I64, _I64, _I, _I, _P, _P,
                             _D, _I, _P, _I, _I64, _P, _I64, _P, _SZ, _P]),
     "hlq_quantize_weights_ws": (_SZ, [_I]),
@@ -106,7 +110,7 @@ class GemmDesc(ctypes.Structure):
     _fields_ = [("A", _P), ("lda", _I64), ("a_gstride", _I64), ("B", _P), ("ldb", _I64), ("b_gstride", _I64),
                 ("M", _I64), ("N", _I64), ("K", _I64), ("groups", _I64), ("bits_a", _I), ("bits_b", _I),
                 ("sa", _P), ("sb", _P), ("extra", _D), ("epilogue", _I), ("out", _P), ("out_dtype", _I),
-                ("ldo", _I64), ("acc_out", _P), ("ld_acc", _I64)]
+                ("ldo", _I64), ("acc_out", _P), ("ld_acc", _I64), ("a_packed", _I)]
 
 
 _lock = threading.Lock()

@@ -255,6 +255,35 @@ int hlq_quantize_dual_colsum(const void* src, int dtype, int64_t segs, int64_t r
   return cuda_status("hlq_quantize_dual_colsum");
 }
 
+int hlq_quantize_dual_ex(const void* src, int dtype, int64_t segs, int64_t rows, int64_t cols, int64_t ld_src,
+                         int64_t seg_src, uint32_t bitmap, int bits_gx, int bits_gw, uint32_t* stats_ws,
+                         void* dst_gx, int64_t ld_gx, int pack_gx, int8_t* dst_gw, int64_t ld_gw, float* scale_gx,
+                         float* scale_gw, float* colsum_out, void* colsum_ws, size_t colsum_ws_bytes,
+                         void* stream) {
+  HLQ_TRY(check_bits(bits_gx));
+  HLQ_TRY(proj_rows_checked(src, dtype, segs, rows, cols, ld_src, seg_src, bitmap, bits_gw, dst_gw,
+                            ld_gw));
+  HLQ_TRY(check_ld16(ld_gx, "gx codes"));
+  if (pack_gx && bits_gx != 4) return fail(HLQ_ERR_PARAMETER, "packed gx codes are 4-bit, got bits_gx=%d", bits_gx);
+  if (ld_gx < (pack_gx ? pad16(cols) / 2 : pad16(cols)))
+    return fail(HLQ_ERR_DIMENSION, "gx codes ld %lld too small for %lld columns", (long long)ld_gx, (long long)cols);
+  if (colsum_out) {
+    const size_t need = hlq::transform_colsum_ws(segs, rows, cols, bitmap);
+    if (colsum_ws_bytes < need || (need && !colsum_ws))
+      return fail(HLQ_ERR_PARAMETER, "column-sum workspace needs %zu bytes, got %zu", need, colsum_ws_bytes);
+  }
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  hlq::TransformArgs t = proj_args(src, dtype, segs, rows, cols, ld_src, seg_src, bitmap, bits_gw,
+                                   stats_ws, dst_gw, ld_gw, scale_gw);
+  t.do_gx = true; t.bits_gx = bits_gx; t.dst_gx = static_cast<int8_t*>(dst_gx); t.ld_gx = ld_gx;
+  t.scale_gx = scale_gx; t.pack_gx = pack_gx != 0;
+  t.colsum_out = colsum_out;
+  t.colsum_ws = static_cast<float*>(colsum_ws);
+  cudaMemsetAsync(stats_ws, 0, HLQ_STATS_WS_BYTES, st);
+  hlq::launch_transform(t, hlq::kBoth, st);
+  return cuda_status("hlq_quantize_dual_ex");
+}
+
 int hlq_gemm_i8(const int8_t* A, int64_t lda, const int8_t* B, int64_t ldb, int64_t M, int64_t N,
                 int64_t K, int bits_a, int bits_b, const float* sa, const float* sb, double extra,
                 int epilogue, void* out, int out_dtype, int64_t ldo, int32_t* acc_out,
@@ -272,6 +301,12 @@ int hlq_gemm_i8_grouped(const int8_t* A, int64_t lda, int64_t a_gstride, const i
                         extra, epilogue, out, out_dtype, ldo, acc_out, ld_acc, nullptr, 0, stream);
 }
 
+static int gemm_ex_impl(const int8_t* A, int64_t lda, int64_t a_gstride, const int8_t* B, int64_t ldb,
+                   int64_t b_gstride, int64_t M, int64_t N, int64_t K, int64_t groups, int bits_a,
+                   int bits_b, const float* sa, const float* sb, double extra, int epilogue, void* out,
+                   int out_dtype, int64_t ldo, int32_t* acc_out, int64_t ld_acc, void* ws,
+                   size_t ws_bytes, void* stream, bool a4);
+
 int hlq_gemm_i8_multi(int n, const hlq_gemm_desc* d, void* stream) {
   if (n < 1 || n > 2 || !d) return fail(HLQ_ERR_PARAMETER, "hlq_gemm_i8_multi takes 1 or 2 products, got %d", n);
   bool fuse = n == 2;
@@ -288,7 +323,8 @@ int hlq_gemm_i8_multi(int n, const hlq_gemm_desc* d, void* stream) {
       HLQ_TRY(check_dtype(g.out_dtype));
       HLQ_TRY(check_ld16(g.lda, "A"));
       HLQ_TRY(check_ld16(g.ldb, "B"));
-      if (g.M < 0 || g.N < 0 || g.K <= 0 || g.lda < g.K || g.ldb < g.K || g.ldo < g.N || g.M > INT32_MAX ||
+      if (g.a_packed && g.bits_a != 4) return fail(HLQ_ERR_PARAMETER, "packed A holds 4-bit codes");
+      if (g.M < 0 || g.N < 0 || g.K <= 0 || g.lda < (g.a_packed ? (g.K + 1) / 2 : g.K) || g.ldb < g.K || g.ldo < g.N || g.M > INT32_MAX ||
           g.N > INT32_MAX || g.K > INT32_MAX)
         return fail(HLQ_ERR_DIMENSION, "bad GEMM shape M=%lld N=%lld K=%lld", (long long)g.M, (long long)g.N,
                     (long long)g.K);
@@ -301,7 +337,7 @@ int hlq_gemm_i8_multi(int n, const hlq_gemm_desc* d, void* stream) {
     for (int q = 0; q < 2; ++q) {
       const hlq_gemm_desc& g = d[q];
       gd[q] = hlq::GemmDesc{g.A, g.lda, g.lda * g.M, g.B, g.ldb, g.ldb * g.N, g.M, g.N, g.K, 1, g.sa, g.sb,
-                            g.extra, g.epilogue, g.out, g.out_dtype, g.ldo, nullptr, 0};
+                            g.extra, g.epilogue, g.out, g.out_dtype, g.ldo, nullptr, 0, g.a_packed ? 1 : 0};
     }
     if (hlq::gemm_i8_pair2_eligible(gd)) {
       int e = hlq::launch_gemm_i8_pair2(gd, static_cast<cudaStream_t>(stream));
@@ -312,9 +348,9 @@ int hlq_gemm_i8_multi(int n, const hlq_gemm_desc* d, void* stream) {
   }
   for (int q = 0; q < n; ++q) {
     const hlq_gemm_desc& g = d[q];
-    HLQ_TRY(hlq_gemm_i8_grouped(g.A, g.lda, g.a_gstride, g.B, g.ldb, g.b_gstride, g.M, g.N, g.K, g.groups,
-                                g.bits_a, g.bits_b, g.sa, g.sb, g.extra, g.epilogue, g.out, g.out_dtype, g.ldo,
-                                g.acc_out, g.ld_acc, stream));
+    HLQ_TRY(gemm_ex_impl(g.A, g.lda, g.a_gstride, g.B, g.ldb, g.b_gstride, g.M, g.N, g.K, g.groups, g.bits_a,
+                         g.bits_b, g.sa, g.sb, g.extra, g.epilogue, g.out, g.out_dtype, g.ldo, g.acc_out, g.ld_acc,
+                         nullptr, 0, stream, g.a_packed != 0));
   }
   return HLQ_OK;
 }
@@ -343,11 +379,11 @@ size_t hlq_gemm_i8_ws_bits(int64_t M, int64_t N, int64_t K, int64_t groups, int 
 // int_matmul's advertised bound (quantize.py:21,166-170): MAX_K = {8: 10^6, 4: 10^7}
 static int64_t max_k_of(int bits) { return bits == 8 ? 1000000 : 10000000; }
 
-int hlq_gemm_i8_ex(const int8_t* A, int64_t lda, int64_t a_gstride, const int8_t* B, int64_t ldb,
+static int gemm_ex_impl(const int8_t* A, int64_t lda, int64_t a_gstride, const int8_t* B, int64_t ldb,
                    int64_t b_gstride, int64_t M, int64_t N, int64_t K, int64_t groups, int bits_a,
                    int bits_b, const float* sa, const float* sb, double extra, int epilogue, void* out,
                    int out_dtype, int64_t ldo, int32_t* acc_out, int64_t ld_acc, void* ws,
-                   size_t ws_bytes, void* stream) {
+                   size_t ws_bytes, void* stream, bool a4) {
   if (groups < 1 || groups > 65535 || (groups > 1 && (a_gstride % 16 || b_gstride % 16 ||
                                                       a_gstride < lda * M || b_gstride < ldb * N)))
     return fail(HLQ_ERR_PARAMETER, "bad K-group layout groups=%lld", (long long)groups);
@@ -355,8 +391,10 @@ int hlq_gemm_i8_ex(const int8_t* A, int64_t lda, int64_t a_gstride, const int8_t
   HLQ_TRY(check_bits(bits_b));
   HLQ_TRY(check_dtype(out_dtype));
   HLQ_TRY(check_ld16(lda, "A"));
+  if (a4 && bits_a != 4) return fail(HLQ_ERR_PARAMETER, "packed A holds 4-bit codes, got bits_a=%d", bits_a);
+  const int64_t a_row = a4 ? (K + 1) / 2 : K;  // bytes of one A row
   HLQ_TRY(check_ld16(ldb, "B"));
-  if (M < 0 || N < 0 || K <= 0 || lda < K || ldb < K || (out && ldo < N) || (acc_out && ld_acc < N))
+  if (M < 0 || N < 0 || K <= 0 || lda < a_row || ldb < K || (out && ldo < N) || (acc_out && ld_acc < N))
     return fail(HLQ_ERR_DIMENSION, "bad GEMM shape M=%lld N=%lld K=%lld", (long long)M, (long long)N,
                 (long long)K);
   if (M > INT32_MAX || N > INT32_MAX || K > INT32_MAX)
@@ -381,11 +419,28 @@ int hlq_gemm_i8_ex(const int8_t* A, int64_t lda, int64_t a_gstride, const int8_t
   if (M == 0 || N == 0) return HLQ_OK;
   int e = hlq::launch_gemm_i8(A, lda, B, ldb, M, N, K, groups, a_gstride, b_gstride, sa, sb, extra,
                               epilogue, out, out_dtype, ldo, acc_out, ld_acc, ws, ws_bytes,
-                              static_cast<cudaStream_t>(stream), min_splits);
+                              static_cast<cudaStream_t>(stream), min_splits, a4);
   if (e == -2) return fail(HLQ_ERR_PARAMETER, "long contraction: output / workspace not 16-byte aligned");
   if (e == -1) return fail(HLQ_ERR_CUDA, "cuTensorMapEncodeTiled unavailable or rejected the operands");
   if (e != 0) return fail(HLQ_ERR_CUDA, "hlq_gemm_i8: %s", cudaGetErrorString(cudaError_t(e)));
   return HLQ_OK;
+}
+
+int hlq_gemm_i8_ex(const int8_t* A, int64_t lda, int64_t a_gstride, const int8_t* B, int64_t ldb,
+                   int64_t b_gstride, int64_t M, int64_t N, int64_t K, int64_t groups, int bits_a,
+                   int bits_b, const float* sa, const float* sb, double extra, int epilogue, void* out,
+                   int out_dtype, int64_t ldo, int32_t* acc_out, int64_t ld_acc, void* ws,
+                   size_t ws_bytes, void* stream) {
+  return gemm_ex_impl(A, lda, a_gstride, B, ldb, b_gstride, M, N, K, groups, bits_a, bits_b, sa, sb, extra,
+                      epilogue, out, out_dtype, ldo, acc_out, ld_acc, ws, ws_bytes, stream, false);
+}
+
+int hlq_gemm_i4a_ex(const uint8_t* A, int64_t lda, int64_t a_gstride, const int8_t* B, int64_t ldb,
+                    int64_t b_gstride, int64_t M, int64_t N, int64_t K, int64_t groups, int bits_b,
+                    const float* sa, const float* sb, double extra, int epilogue, void* out, int out_dtype,
+                    int64_t ldo, void* ws, size_t ws_bytes, void* stream) {
+  return gemm_ex_impl(reinterpret_cast<const int8_t*>(A), lda, a_gstride, B, ldb, b_gstride, M, N, K, groups, 4,
+                      bits_b, sa, sb, extra, epilogue, out, out_dtype, ldo, nullptr, 0, ws, ws_bytes, stream, true);
 }
 
 size_t hlq_quantize_weights_ws(int n) { return n < 0 ? 0 : size_t(8 * n + 8) * sizeof(uint32_t); }

@@ -36,6 +36,54 @@ namespace {
 constexpr int kBM = 128;
 constexpr int kBK = 128;  // bytes of K per stage = one 128B swizzle row
 constexpr int kThreads = 256;
+// Packed int4 A operand: + 4 converter warps (8..11)
+constexpr int kThreadsA4 = 384;
+constexpr uint32_t kPackedA = kBM * kBK / 2;  // one stage of packed A: 128 rows x 64 bytes
+
+// ---------------------------------------------------------------- packed int4 A
+// The gx codes Q4(H.gy) can live in HBM packed two per byte, low nibble first
+// (the ACBP container's nibble order, acbp.py:56-61) -- half the bytes of the
+// int8 form.  tcgen05 has no int4 MMA and TMA cannot sign-extend nibbles, so
+// the TMA loads each 128 x 64-byte packed tile into the UPPER half of the
+// stage's A slot and 4 converter warps sign-extend it in place into the
+// 128 x 128-byte SWIZZLE_128B K-major int8 tile kind::i8 reads (all packed
+// input is read into registers, then a named barrier, then the writes).
+__device__ __forceinline__ uint32_t sext_nibbles(uint32_t v) {
+  // v: one nibble in the low half of each byte -> the bytes' int8 values:
+  // (v ^ 8) + 0x78 stays below 0x88 per byte (no carries), ^ 0x80 = v - 16 [v >= 8]
+  return ((v ^ 0x08080808u) + 0x78787878u) ^ 0x80808080u;
+}
+__device__ __forceinline__ void unpack8(uint32_t x, uint32_t& o0, uint32_t& o1) {
+  const uint32_t lo = sext_nibbles(x & 0x0F0F0F0Fu);         // codes 0, 2, 4, 6
+  const uint32_t hi = sext_nibbles((x >> 4) & 0x0F0F0F0Fu);  // codes 1, 3, 5, 7
+  o0 = __byte_perm(lo, hi, 0x5140);
+  o1 = __byte_perm(lo, hi, 0x7362);
+}
+// ct = converter thread 0..127.  Unit u = (row u / 4, 16 packed bytes u % 4 =
+// K codes [32 q, 32 q + 32)) -> int8 chunks 2q and 2q+1 of the row, at chunk
+// position c ^ (row % 8) (the 128B swizzle of a 1024-byte aligned tile).
+__device__ __forceinline__ void convert_a4(uint8_t* slot, int ct) {
+  const uint32_t base = ptx::smem_u32(slot);
+  uint4 in[4];
+#pragma unroll
+  for (int j = 0; j < 4; ++j) in[j] = ptx::lds128(base + kPackedA + uint32_t(ct + 128 * j) * 16u);
+  asm volatile("bar.sync 3, 128;" ::: "memory");
+#pragma unroll
+  for (int j = 0; j < 4; ++j) {
+    const int u = ct + 128 * j, r = u >> 2, q = u & 3;
+    uint32_t o[8];
+    unpack8(in[j].x, o[0], o[1]);
+    unpack8(in[j].y, o[2], o[3]);
+    unpack8(in[j].z, o[4], o[5]);
+    unpack8(in[j].w, o[6], o[7]);
+    const uint32_t row = base + uint32_t(r) * 128u;
+    asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(row + ((uint32_t(2 * q) ^ (r & 7)) << 4)),
+                 "r"(o[0]), "r"(o[1]), "r"(o[2]), "r"(o[3]) : "memory");
+    asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(row + ((uint32_t(2 * q + 1) ^ (r & 7)) << 4)),
+                 "r"(o[4]), "r"(o[5]), "r"(o[6]), "r"(o[7]) : "memory");
+  }
+  ptx::fence_proxy_async_smem();  // generic-proxy writes -> visible to the tensor core (async proxy)
+}
 
 template <int BN, int STAGES>
 struct GemmCfg;
@@ -168,8 +216,8 @@ struct ConvGeo {
   int nkc;        // 128-byte channel chunks per tap
 };
 
-template <int BN, int STAGES>
-__global__ void __launch_bounds__(kThreads, 1)
+template <int BN, int STAGES, bool A4>
+__global__ void __launch_bounds__(A4 ? kThreadsA4 : kThreads, 1)
     gemm_i8_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant__ CUtensorMap map_b,
                    const __grid_constant__ CUtensorMap map_o, int tma_out,
                    int M, int N, int K, int groups, const float* __restrict__ sa, const float* __restrict__ sb,
@@ -187,7 +235,8 @@ __global__ void __launch_bounds__(kThreads, 1)
   uint64_t* empty = full + STAGES;
   uint64_t* tfull = empty + STAGES;
   uint64_t* tempty = tfull + 2;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+  uint64_t* aready = tempty + 2;  // A4: the stage's A tile is converted (4 converter warps)
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(aready + STAGES);
 
   const uint32_t warp = ptx::warp_id();
   const uint32_t lane = ptx::lane_id();
@@ -200,6 +249,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     for (int s = 0; s < STAGES; ++s) {
       ptx::mbar_init(&full[s], 1);
       ptx::mbar_init(&empty[s], 1);
+      ptx::mbar_init(&aready[s], 4);
     }
     for (int a = 0; a < 2; ++a) {
       ptx::mbar_init(&tfull[a], 1);
@@ -240,8 +290,13 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
         for (int kb = kb0; kb < kb1; ++kb) {
           ptx::mbar_wait_sleep(&empty[stage], phase ^ 1);
-          ptx::mbar_arrive_expect_tx(&full[stage], Cfg::kStageBytes);
-          if (geo.conv) {
+          ptx::mbar_arrive_expect_tx(&full[stage], A4 ? kPackedA + Cfg::kBBytes : Cfg::kStageBytes);
+          if (A4) {
+            // packed A (64 bytes of K per row) into the upper half of the A slot
+            ptx::tma_load_3d(sA + stage * Cfg::kABytes + kPackedA, &map_a, &full[stage], kg * (kBK / 2), mb * kBM,
+                             g);
+            ptx::tma_load_3d(sB + stage * Cfg::kBBytes, &map_b, &full[stage], kg * kBK, nb * BN, g);
+          } else if (geo.conv) {
             const int tap = kb / geo.nkc, oc = kb - tap * geo.nkc;
             const int ti = tap / geo.k, tj = tap - ti * geo.k;
             // flipped tap (k-1-i, k-1-j): dX[h, w] += G[h + pad - i, w + pad - j] W[i, j]
@@ -272,6 +327,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       const uint32_t d_tmem = tmem_base + uint32_t(acc * BN);
       for (int kb = kb0; kb < kb1; ++kb) {
         ptx::mbar_wait(&full[stage], phase);
+        if (A4) ptx::mbar_wait(&aready[stage], phase);
         ptx::tc_fence_after();
         if (ptx::elect_one()) {
           const uint64_t a_desc = ptx::desc_kmajor_sw128(ptx::smem_u32(sA + stage * Cfg::kABytes));
@@ -290,7 +346,23 @@ __global__ void __launch_bounds__(kThreads, 1)
       }
       if (++acc == 2) { acc = 0; acc_phase ^= 1; }
     }
-  } else if (warp >= 4) {
+  } else if (A4 && warp >= 8) {
+    // converters: the same (unit, K block) walk as the MMA issuer
+    const int ct = int(threadIdx.x) - 256;
+    int stage = 0;
+    uint32_t phase = 0;
+    for (int u = blockIdx.x; u < units; u += gridDim.x) {
+      const int sp = u % splits;
+      const int kb0 = int(int64_t(sp) * nk / splits), kb1 = int(int64_t(sp + 1) * nk / splits);
+      for (int kb = kb0; kb < kb1; ++kb) {
+        ptx::mbar_wait(&full[stage], phase);
+        convert_a4(sA + stage * Cfg::kABytes, ct);
+        __syncwarp();
+        if (lane == 0) ptx::mbar_arrive(&aready[stage]);
+        if (++stage == STAGES) { stage = 0; phase ^= 1; }
+      }
+    }
+  } else if (warp >= 4 && warp < 8) {
     const uint32_t quarter = warp & 3;  // TMEM lanes [32*quarter, 32*quarter+32)
     const float comb = __fmul_rn(*sa, *sb);
     const double dscale = __dmul_rn(double(comb), extra);
@@ -364,7 +436,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
   }
 
-  if (warp >= 4 && lane == 0) ptx::bulk_wait_read<0>();  // staging reads done before the CTA exits
+  if (warp >= 4 && warp < 8 && lane == 0) ptx::bulk_wait_read<0>();  // staging reads done before the CTA exits
   ptx::tc_fence_before();
   __syncthreads();
   ptx::tc_fence_after();
@@ -388,6 +460,7 @@ __global__ void __launch_bounds__(kThreads, 1)
 // lists each cluster's units so long dW units and short dX units pack evenly.
 struct PairProb {
   int M, N, K, groups, splits, tma_out, epilogue, out_dtype;
+  int a4;  // A is packed int4 (map a[] boxes 64 bytes x 128 rows; converted in smem)
   const float* sa;
   const float* sb;
   double extra;
@@ -407,8 +480,8 @@ struct alignas(64) PairParams {
   uint16_t ids[kMaxSched];
 };
 
-template <int BN, int STAGES>
-__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
+template <int BN, int STAGES, bool A4ANY>
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(A4ANY ? kThreadsA4 : kThreads, 1)
     gemm_i8_2sm_kernel(const __grid_constant__ PairParams P) {
   constexpr uint32_t kABytes = kBM * kBK;             // this CTA's 128 rows of A
   constexpr uint32_t kBBytes = (BN / 2) * kBK;        // this CTA's BN/2 rows of B
@@ -424,7 +497,13 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
   uint64_t* empty = full + STAGES;
   uint64_t* tfull = empty + STAGES;
   uint64_t* tempty = tfull + 2;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+  // packed-A units: each CTA's packed A completes on its own `pfull`; its
+  // converters then arrive on the LEADER's `aready` (4 warps x 2 CTAs).  These
+  // two complete only on packed rounds, so every role tracks their phases per
+  // stage (bit s of `pph`).
+  uint64_t* pfull = tempty + 2;
+  uint64_t* aready = pfull + STAGES;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(aready + STAGES);
 
   const uint32_t warp = ptx::warp_id();
   const uint32_t lane = ptx::lane_id();
@@ -446,6 +525,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
       ptx::mbar_init(&tfull[a], 1);
       ptx::mbar_init(&tempty[a], 8);  // 4 epilogue warps x 2 CTAs
     }
+    for (int s = 0; s < STAGES; ++s) {
+      ptx::mbar_init(&pfull[s], 1);
+      ptx::mbar_init(&aready[s], 8);  // 4 converter warps x 2 CTAs
+    }
     ptx::fence_mbar_init();
   }
   if (warp == 2) ptx::tmem_alloc_2sm(tmem_slot, kTmemCols);
@@ -459,6 +542,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
   const int count = P.nsched ? int(P.off[cid + 1]) - int(P.off[cid]) : (total - cid + ncl - 1) / ncl;
   const uint32_t full_leader = ptx::mapa(ptx::smem_u32(full), 0);
   const uint32_t tempty_leader = ptx::mapa(ptx::smem_u32(tempty), 0);
+  const uint32_t aready_leader = ptx::mapa(ptx::smem_u32(aready), 0);
 
   // unit i of this cluster -> (problem, tile, split, K-block range)
   struct U {
@@ -491,11 +575,19 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
         const CUtensorMap* ma = &P.a[w.q];
         const CUtensorMap* mb = &P.b[w.q];
         int g = w.kb0 / w.nk_g, kg = w.kb0 - g * w.nk_g;
+        const bool a4 = A4ANY && P.p[w.q].a4;
         for (int kb = w.kb0; kb < w.kb1; ++kb) {
           ptx::mbar_wait_sleep(&empty[stage], phase ^ 1);
-          if (leader) ptx::mbar_arrive_expect_tx(&full[stage], 2 * kStageBytes);
+          if (leader) ptx::mbar_arrive_expect_tx(&full[stage], a4 ? 2 * kBBytes : 2 * kStageBytes);
           const uint32_t fb = full_leader + uint32_t(stage) * 8u;
-          ptx::tma_load_3d_2sm(sA + stage * kABytes, ma, fb, kg * kBK, w.mb * 2 * kBM + int(rank) * kBM, g);
+          if (a4) {
+            // this CTA's packed A rows -> upper half of its A slot, completion on its own pfull
+            ptx::mbar_arrive_expect_tx(&pfull[stage], kPackedA);
+            ptx::tma_load_3d(sA + stage * kABytes + kPackedA, ma, &pfull[stage], kg * (kBK / 2),
+                             w.mb * 2 * kBM + int(rank) * kBM, g);
+          } else {
+            ptx::tma_load_3d_2sm(sA + stage * kABytes, ma, fb, kg * kBK, w.mb * 2 * kBM + int(rank) * kBM, g);
+          }
           ptx::tma_load_3d_2sm(sB + stage * kBBytes, mb, fb, kg * kBK, w.nb * BN + int(rank) * (BN / 2), g);
           if (++kg == w.nk_g) { kg = 0; ++g; }
           if (++stage == STAGES) { stage = 0; phase ^= 1; }
@@ -509,13 +601,19 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
       uint32_t phase = 0;
       int acc = 0;
       uint32_t acc_phase = 0;
+      uint32_t pph = 0;
       for (int i = 0; i < count; ++i) {
         const U w = unit(i);
+        const bool a4 = A4ANY && P.p[w.q].a4;
         ptx::mbar_wait_sleep(&tempty[acc], acc_phase ^ 1);
         ptx::tc_fence_after();
         const uint32_t d_tmem = tmem_base + uint32_t(acc * BN);
         for (int kb = w.kb0; kb < w.kb1; ++kb) {
           ptx::mbar_wait(&full[stage], phase);
+          if (a4) {
+            ptx::mbar_wait(&aready[stage], (pph >> stage) & 1u);  // both CTAs' A converted
+            pph ^= 1u << stage;
+          }
           ptx::tc_fence_after();
           if (ptx::elect_one()) {
             const uint64_t a_desc = ptx::desc_kmajor_sw128(ptx::smem_u32(sA + stage * kABytes));
@@ -533,7 +631,26 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
         if (++acc == 2) { acc = 0; acc_phase ^= 1; }
       }
     }
-  } else if (warp >= 4) {
+  } else if (A4ANY && warp >= 8) {
+    // converters (both CTAs): sign-extend this CTA's packed A rows in place
+    const int ct = int(threadIdx.x) - 256;
+    int stage = 0;
+    uint32_t pph = 0;
+    for (int i = 0; i < count; ++i) {
+      const U w = unit(i);
+      const bool a4 = P.p[w.q].a4 != 0;
+      for (int kb = w.kb0; kb < w.kb1; ++kb) {
+        if (a4) {
+          ptx::mbar_wait(&pfull[stage], (pph >> stage) & 1u);
+          pph ^= 1u << stage;
+          convert_a4(sA + stage * kABytes, ct);
+          __syncwarp();
+          if (lane == 0) ptx::mbar_arrive_cluster(aready_leader + uint32_t(stage) * 8u);
+        }
+        if (++stage == STAGES) stage = 0;
+      }
+    }
+  } else if (warp >= 4 && warp < 8) {
     const uint32_t quarter = warp & 3;
     int acc = 0;
     uint32_t acc_phase = 0;
@@ -587,7 +704,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
     }
   }
 
-  if (warp >= 4 && lane == 0) ptx::bulk_wait_read<0>();
+  if (warp >= 4 && warp < 8 && lane == 0) ptx::bulk_wait_read<0>();
   ptx::tc_fence_before();
   ptx::cluster_sync();
   ptx::tc_fence_after();
@@ -672,6 +789,21 @@ bool make_map(CUtensorMap* map, const int8_t* ptr, int64_t rows, int64_t k, int6
             CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
+// Packed int4 A: (ceil(K/2) bytes, rows, groups), 64-byte x 128-row boxes (one
+// stage of K = 128 codes), no swizzle -- the converter warps write the SW128 tile.
+bool make_map_a4(CUtensorMap* map, const int8_t* ptr, int64_t rows, int64_t k, int64_t ld, int64_t groups,
+                 int64_t gstride) {
+  EncodeTiledFn fn = encode_fn();
+  if (!fn) return false;
+  cuuint64_t dims[3] = {cuuint64_t((k + 1) / 2), cuuint64_t(rows), cuuint64_t(groups)};
+  cuuint64_t strides[2] = {cuuint64_t(ld), cuuint64_t(groups > 1 ? gstride : ld * rows)};
+  cuuint32_t box[3] = {uint32_t(kBK / 2), uint32_t(kBM), 1};
+  cuuint32_t estr[3] = {1, 1, 1};
+  return fn(map, CU_TENSOR_MAP_DATA_TYPE_UINT8, 3, const_cast<int8_t*>(ptr), dims, strides, box, estr,
+            CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+            CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
 // Store map of the output for the TMA epilogue: (N, M) with row stride ldo,
 // 32 x 32 boxes, swizzle matching store_chunk_tma.  False = use the direct
 // store epilogue (exact fp64 dequant, int32 accumulator dump, split-K slabs or
@@ -718,7 +850,7 @@ bool encode_tensor_map(void* map, int dtype, int rank, const void* ptr, const ui
 
 namespace {
 
-template <int BN, int STAGES>
+template <int BN, int STAGES, bool A4 = false>
 int run_maps(const CUtensorMap& ma, const CUtensorMap& mb, int64_t M, int64_t N, int64_t K, int64_t groups,
              const float* sa, const float* sb, double extra, int epilogue, void* out, int out_dtype,
              int64_t ldo, int32_t* acc_out, int64_t ld_acc, int splits, void* ws, const ConvGeo& geo,
@@ -726,7 +858,7 @@ int run_maps(const CUtensorMap& ma, const CUtensorMap& mb, int64_t M, int64_t N,
   using Cfg = GemmCfg<BN, STAGES>;
   static std::atomic<unsigned long long> attr_set{0};  // per template instance and device
   {
-    cudaError_t e = smem_attr_once(reinterpret_cast<const void*>(gemm_i8_kernel<BN, STAGES>), int(Cfg::kSmem),
+    cudaError_t e = smem_attr_once(reinterpret_cast<const void*>(gemm_i8_kernel<BN, STAGES, A4>), int(Cfg::kSmem),
                                    attr_set);
     if (e != cudaSuccess) return int(e);
   }
@@ -737,7 +869,7 @@ int run_maps(const CUtensorMap& ma, const CUtensorMap& mb, int64_t M, int64_t N,
   CUtensorMap mo;
   const int tma_out = make_out_map(&mo, out, out_dtype, M, N, ldo, epilogue, acc_out, splits) ? 1 : 0;
   if (!tma_out) mo = ma;  // unused
-  gemm_i8_kernel<BN, STAGES><<<grid, kThreads, Cfg::kSmem, stream>>>(
+  gemm_i8_kernel<BN, STAGES, A4><<<grid, A4 ? kThreadsA4 : kThreads, Cfg::kSmem, stream>>>(
       ma, mb, mo, tma_out, int(M), int(N), int(K), int(groups), sa, sb, extra, epilogue, out, out_dtype, ldo,
       acc_out, ld_acc, splits, slabs, geo);
   if (splits > 1) {
@@ -753,12 +885,15 @@ int run_maps(const CUtensorMap& ma, const CUtensorMap& mb, int64_t M, int64_t N,
 template <int BN, int STAGES>
 int run(const int8_t* A, int64_t lda, const int8_t* B, int64_t ldb, int64_t M, int64_t N, int64_t K,
         int64_t groups, int64_t a_gstride, int64_t b_gstride, const float* sa, const float* sb, double extra, int epilogue, void* out, int out_dtype,
-        int64_t ldo, int32_t* acc_out, int64_t ld_acc, int splits, void* ws, cudaStream_t stream) {
+        int64_t ldo, int32_t* acc_out, int64_t ld_acc, int splits, void* ws, cudaStream_t stream, bool a4) {
   CUtensorMap ma, mb;
-  if (!make_map(&ma, A, M, K, lda, groups, a_gstride, kBM) ||
-      !make_map(&mb, B, N, K, ldb, groups, b_gstride, BN))
-    return -1;
+  const bool okA = a4 ? make_map_a4(&ma, A, M, K, lda, groups, a_gstride)
+                      : make_map(&ma, A, M, K, lda, groups, a_gstride, kBM);
+  if (!okA || !make_map(&mb, B, N, K, ldb, groups, b_gstride, BN)) return -1;
   const ConvGeo geo{0, 0, 0, 0, 0, 0};
+  if (a4)
+    return run_maps<BN, STAGES, true>(ma, mb, M, N, K, groups, sa, sb, extra, epilogue, out, out_dtype, ldo,
+                                      acc_out, ld_acc, splits, ws, geo, stream);
   return run_maps<BN, STAGES>(ma, mb, M, N, K, groups, sa, sb, extra, epilogue, out, out_dtype, ldo, acc_out,
                               ld_acc, splits, ws, geo, stream);
 }
@@ -780,14 +915,16 @@ struct PairSpec {  // one product for the CTA-pair kernel
   int64_t ld_acc;
   int splits;
   void* ws;
+  int a4;  // A packed int4
 };
 
 template <int BN>
 bool fill_prob(PairParams& P, int q, const PairSpec& s, int unit0) {
-  if (!make_map(&P.a[q], s.A, s.M, s.K, s.lda, s.groups, s.a_gstride, kBM) ||
-      !make_map(&P.b[q], s.B, s.N, s.K, s.ldb, s.groups, s.b_gstride, BN / 2))
-    return false;
+  const bool okA = s.a4 ? make_map_a4(&P.a[q], s.A, s.M, s.K, s.lda, s.groups, s.a_gstride)
+                        : make_map(&P.a[q], s.A, s.M, s.K, s.lda, s.groups, s.a_gstride, kBM);
+  if (!okA || !make_map(&P.b[q], s.B, s.N, s.K, s.ldb, s.groups, s.b_gstride, BN / 2)) return false;
   PairProb& p = P.p[q];
+  p.a4 = s.a4;
   p.M = int(s.M); p.N = int(s.N); p.K = int(s.K); p.groups = int(s.groups); p.splits = s.splits;
   p.tma_out = make_out_map(&P.o[q], s.out, s.out_dtype, s.M, s.N, s.ldo, s.epilogue, s.acc_out, s.splits) ? 1 : 0;
   if (!p.tma_out) P.o[q] = P.a[q];  // unused
@@ -833,7 +970,7 @@ bool lpt_schedule(PairParams& P, int ncl) {
 
 template <int BN, int STAGES>
 int run_2sm_specs(const PairSpec* specs, int n, cudaStream_t stream) {
-  constexpr size_t kSmem = size_t(STAGES) * (kBM * kBK + (BN / 2) * kBK) + kStgAll + 1024 + 256;
+  constexpr size_t kSmem = size_t(STAGES) * (kBM * kBK + (BN / 2) * kBK) + kStgAll + 1024 + 512;
   static PairParams P;  // host staging (large); launches copy it into the parameter buffer
   static std::mutex mu;
   std::lock_guard<std::mutex> lock(mu);
@@ -844,16 +981,23 @@ int run_2sm_specs(const PairSpec* specs, int n, cudaStream_t stream) {
     if (!fill_prob<BN>(P, q, specs[q], unit0)) return -1;
     unit0 += P.p[q].units;
   }
-  static std::atomic<unsigned long long> attr_set{0};  // per template instance and device
+  bool any_a4 = false;
+  for (int q = 0; q < n; ++q) any_a4 = any_a4 || specs[q].a4;
+  static std::atomic<unsigned long long> attr_set{0}, attr_set4{0};  // per template instance and device
   {
-    cudaError_t e = smem_attr_once(reinterpret_cast<const void*>(gemm_i8_2sm_kernel<BN, STAGES>), int(kSmem),
-                                   attr_set);
+    cudaError_t e = any_a4 ? smem_attr_once(reinterpret_cast<const void*>(gemm_i8_2sm_kernel<BN, STAGES, true>),
+                                            int(kSmem), attr_set4)
+                           : smem_attr_once(reinterpret_cast<const void*>(gemm_i8_2sm_kernel<BN, STAGES, false>),
+                                            int(kSmem), attr_set);
     if (e != cudaSuccess) return int(e);
   }
   const int64_t pairs = num_sms() / 2;
   const int ncl = int(unit0 < pairs ? unit0 : pairs);
   if (n > 1) lpt_schedule(P, ncl);
-  gemm_i8_2sm_kernel<BN, STAGES><<<2 * ncl, kThreads, kSmem, stream>>>(P);
+  if (any_a4)
+    gemm_i8_2sm_kernel<BN, STAGES, true><<<2 * ncl, kThreadsA4, kSmem, stream>>>(P);
+  else
+    gemm_i8_2sm_kernel<BN, STAGES, false><<<2 * ncl, kThreads, kSmem, stream>>>(P);
   for (int q = 0; q < n; ++q) {
     const PairSpec& s = specs[q];
     if (s.splits > 1) {
@@ -872,9 +1016,9 @@ template <int BN, int STAGES>
 int run_2sm(const int8_t* A, int64_t lda, const int8_t* B, int64_t ldb, int64_t M, int64_t N, int64_t K,
             int64_t groups, int64_t a_gstride, int64_t b_gstride, const float* sa, const float* sb, double extra,
             int epilogue, void* out, int out_dtype, int64_t ldo, int32_t* acc_out, int64_t ld_acc, int splits,
-            void* ws, cudaStream_t stream) {
+            void* ws, cudaStream_t stream, bool a4) {
   const PairSpec s{A, lda, B, ldb, M, N, K, groups, a_gstride, b_gstride, sa, sb, extra, epilogue, out, out_dtype,
-                   ldo, acc_out, ld_acc, splits, ws};
+                   ldo, acc_out, ld_acc, splits, ws, a4 ? 1 : 0};
   return run_2sm_specs<BN, STAGES>(&s, 1, stream);
 }
 
@@ -987,7 +1131,7 @@ int launch_gemm_i8_pair2(const GemmDesc* d, cudaStream_t stream) {
   for (int q = 0; q < 2; ++q)
     s[q] = PairSpec{d[q].A, d[q].lda, d[q].B, d[q].ldb, d[q].M, d[q].N, d[q].K, d[q].groups, d[q].a_gstride,
                     d[q].b_gstride, d[q].sa, d[q].sb, d[q].extra, d[q].epilogue, d[q].out, d[q].out_dtype,
-                    d[q].ldo, d[q].acc_out, d[q].ld_acc, 1, nullptr};
+                    d[q].ldo, d[q].acc_out, d[q].ld_acc, 1, nullptr, d[q].a4};
   if (bn == 256) return run_2sm_specs<256, 6>(s, 2, stream);
   return run_2sm_specs<128, 8>(s, 2, stream);
 }
@@ -1013,7 +1157,7 @@ int launch_gemm_i8(const int8_t* A, int64_t lda, const int8_t* B, int64_t ldb, i
                    int64_t K, int64_t groups, int64_t a_gstride, int64_t b_gstride,
                    const float* sa, const float* sb, double extra, int epilogue,
                    void* out, int out_dtype, int64_t ldo, int32_t* acc_out, int64_t ld_acc,
-                   void* ws, size_t ws_bytes, cudaStream_t stream, int min_splits) {
+                   void* ws, size_t ws_bytes, cudaStream_t stream, int min_splits, bool a4) {
   GemmPlan p = plan_gemm(M, N, K, groups, true, min_splits);
   const bool vec_out = (ldo % 4 == 0) && (reinterpret_cast<uintptr_t>(out) % 16 == 0) &&
                        (ld_acc % 4 == 0) && (reinterpret_cast<uintptr_t>(acc_out) % 16 == 0);
@@ -1024,18 +1168,18 @@ int launch_gemm_i8(const int8_t* A, int64_t lda, const int8_t* B, int64_t ldb, i
   if (p.pair) {
     if (p.bn == 256)
       return run_2sm<256, 6>(A, lda, B, ldb, M, N, K, groups, a_gstride, b_gstride, sa, sb, extra, epilogue, out,
-                             out_dtype, ldo, acc_out, ld_acc, p.splits, ws, stream);
+                             out_dtype, ldo, acc_out, ld_acc, p.splits, ws, stream, a4);
     if (p.bn == 192)
       return run_2sm<192, 6>(A, lda, B, ldb, M, N, K, groups, a_gstride, b_gstride, sa, sb, extra, epilogue, out,
-                             out_dtype, ldo, acc_out, ld_acc, p.splits, ws, stream);
+                             out_dtype, ldo, acc_out, ld_acc, p.splits, ws, stream, a4);
     return run_2sm<128, 8>(A, lda, B, ldb, M, N, K, groups, a_gstride, b_gstride, sa, sb, extra, epilogue, out,
-                           out_dtype, ldo, acc_out, ld_acc, p.splits, ws, stream);
+                           out_dtype, ldo, acc_out, ld_acc, p.splits, ws, stream, a4);
   }
   if (p.bn == 256)
     return run<256, 4>(A, lda, B, ldb, M, N, K, groups, a_gstride, b_gstride, sa, sb, extra, epilogue, out,
-                       out_dtype, ldo, acc_out, ld_acc, p.splits, ws, stream);
+                       out_dtype, ldo, acc_out, ld_acc, p.splits, ws, stream, a4);
   return run<128, 6>(A, lda, B, ldb, M, N, K, groups, a_gstride, b_gstride, sa, sb, extra, epilogue, out,
-                     out_dtype, ldo, acc_out, ld_acc, p.splits, ws, stream);
+                     out_dtype, ldo, acc_out, ld_acc, p.splits, ws, stream, a4);
 }
 
 int launch_conv_dgrad_i8(const int8_t* G, int64_t ldg, int64_t B, int64_t Ho, int64_t Wo, int64_t O,

@@ -59,6 +59,8 @@ struct TransformArgs {
   // partials in colsum_ws (transform_colsum_ws bytes)
   float* colsum_out = nullptr;
   float* colsum_ws = nullptr;
+  // gx codes packed two per byte (low nibble first), ld_gx in bytes (4-bit codes only)
+  bool pack_gx = false;
 };
 
 void launch_transform(const TransformArgs& t, int mode, cudaStream_t stream);
@@ -94,7 +96,7 @@ int launch_gemm_i8(const int8_t* A, int64_t lda, const int8_t* B, int64_t ldb, i
                    int64_t K, int64_t groups, int64_t a_gstride, int64_t b_gstride,
                    const float* sa, const float* sb, double extra, int epilogue,
                    void* out, int out_dtype, int64_t ldo, int32_t* acc_out, int64_t ld_acc,
-                   void* ws, size_t ws_bytes, cudaStream_t stream, int min_splits = 1);
+                   void* ws, size_t ws_bytes, cudaStream_t stream, int min_splits = 1, bool a4 = false);
 // Implicit-GEMM dgrad of a stride-1 conv (k x k, padding pad): dX (B, H, W, C)
 // channels-last = sum over taps and o of G codes (B, Ho, Wo, O; pixel stride
 // ldg) at the shifted pixel x W codes (row c*k*k + tap, ld ldw), int32 in TMEM,
@@ -126,6 +128,7 @@ struct GemmDesc {
   int64_t ldo;
   int32_t* acc_out;
   int64_t ld_acc;
+  int a4 = 0;  // A packed int4 (lda in bytes of the packed rows)
 };
 bool gemm_i8_pair2_eligible(const GemmDesc* d);
 int launch_gemm_i8_pair2(const GemmDesc* d, cudaStream_t stream);

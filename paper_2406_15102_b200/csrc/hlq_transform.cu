@@ -92,6 +92,7 @@ struct Args {
   float* scale_gx;
   float* scale_gw;
   uint32_t* nonfinite;  // nonfinite_word()
+  int pack_gx;          // gx codes as packed int4 (two per byte, low nibble first; ld_gx in bytes)
   int cstride;  // bytes per column in the code staging buffer
 #ifdef HLQ_TR_TRACE
   unsigned long long* trace;  // per CTA: 8 globaltimer stamps (development timeline)
@@ -300,11 +301,33 @@ __device__ __forceinline__ void consume(const Args& a, const Quant& qx, const Qu
             cb[q] = __byte_perm(t01, t23, 0x7531);
           }
           const int64_t row = int64_t(ps) * a.rows + pb * 16 + r;
-          if (r < prv)
-            *reinterpret_cast<uint4*>(a.dst_gx + row * a.ld_gx + c) = make_uint4(ca[0], ca[1], ca[2], ca[3]);
-          if (r + 8 < prv)
-            *reinterpret_cast<uint4*>(a.dst_gx + (row + 8) * a.ld_gx + c) =
-                make_uint4(cb[0], cb[1], cb[2], cb[3]);
+          if (a.pack_gx) {
+            // nibble pairs: n_j = codes (2j, 2j+1) of row A in byte 0, of row B in byte 2
+            // (the ACBP container's nibble order, low nibble first, acbp.py:56-61)
+            uint32_t n[8];
+#pragma unroll
+            for (int j = 0; j < 8; ++j) {
+              const uint32_t hi = w[2 * j + 1] << 4;
+              asm("lop3.b32 %0, %1, %2, 0x000F000F, 0xE4;" : "=r"(n[j]) : "r"(w[2 * j]), "r"(hi));  // (a & c) | (b & ~c)
+            }
+            uint32_t pa[2], pb2[2];
+#pragma unroll
+            for (int q = 0; q < 2; ++q) {
+              const uint32_t t01 = __byte_perm(n[4 * q], n[4 * q + 1], 0x6420);
+              const uint32_t t23 = __byte_perm(n[4 * q + 2], n[4 * q + 3], 0x6420);
+              pa[q] = __byte_perm(t01, t23, 0x6420);
+              pb2[q] = __byte_perm(t01, t23, 0x7531);
+            }
+            if (r < prv) *reinterpret_cast<uint2*>(a.dst_gx + row * a.ld_gx + (c >> 1)) = make_uint2(pa[0], pa[1]);
+            if (r + 8 < prv)
+              *reinterpret_cast<uint2*>(a.dst_gx + (row + 8) * a.ld_gx + (c >> 1)) = make_uint2(pb2[0], pb2[1]);
+          } else {
+            if (r < prv)
+              *reinterpret_cast<uint4*>(a.dst_gx + row * a.ld_gx + c) = make_uint4(ca[0], ca[1], ca[2], ca[3]);
+            if (r + 8 < prv)
+              *reinterpret_cast<uint4*>(a.dst_gx + (row + 8) * a.ld_gx + c) =
+                  make_uint4(cb[0], cb[1], cb[2], cb[3]);
+          }
         }
       }
       // ---------------- phase 2: column pair -> gw operand (projection along rows)
@@ -956,6 +979,7 @@ void launch_transform(const TransformArgs& t, int mode, cudaStream_t stream) {
   a.scale_gx = t.scale_gx;
   a.scale_gw = t.scale_gw;
   a.nonfinite = nonfinite_word();
+  a.pack_gx = t.pack_gx ? 1 : 0;
   a.cstride = a.nb * a.tq * a.rank + 16;
 #ifdef HLQ_TR_TRACE
   a.trace = g_tr_trace;

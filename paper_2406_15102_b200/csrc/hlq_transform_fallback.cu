@@ -340,6 +340,7 @@ struct TileArgs {
   float* scale_gx;
   float* scale_gw;
   uint32_t* nonfinite;  // nonfinite_word()
+  bool pack_gx;         // gx codes packed int4 (two per byte, low nibble first)
   bool vec;
 };
 
@@ -465,12 +466,20 @@ __device__ __forceinline__ void run_tile(const TileArgs& a, const Quant& qx, con
           const uint2 cc = quant2<FAST_GX>(make_float2(v[i], v[i + 1]), qx);
           c[i] = cc.x; c[i + 1] = cc.y;
         }
-        uint4 out;
-        out.x = pack_bytes(c[0], c[1], c[2], c[3]);
-        out.y = pack_bytes(c[4], c[5], c[6], c[7]);
-        out.z = pack_bytes(c[8], c[9], c[10], c[11]);
-        out.w = pack_bytes(c[12], c[13], c[14], c[15]);
-        *reinterpret_cast<uint4*>(a.dst_gx + p.row * a.ld_gx + p.col0 + pb * 16) = out;
+        if (a.pack_gx) {
+          uint32_t nb[8];
+#pragma unroll
+          for (int j = 0; j < 8; ++j) nb[j] = (c[2 * j] & 0xFu) | ((c[2 * j + 1] & 0xFu) << 4);
+          const uint2 out = make_uint2(pack_bytes(nb[0], nb[1], nb[2], nb[3]), pack_bytes(nb[4], nb[5], nb[6], nb[7]));
+          *reinterpret_cast<uint2*>(a.dst_gx + p.row * a.ld_gx + ((p.col0 + pb * 16) >> 1)) = out;
+        } else {
+          uint4 out;
+          out.x = pack_bytes(c[0], c[1], c[2], c[3]);
+          out.y = pack_bytes(c[4], c[5], c[6], c[7]);
+          out.z = pack_bytes(c[8], c[9], c[10], c[11]);
+          out.w = pack_bytes(c[12], c[13], c[14], c[15]);
+          *reinterpret_cast<uint4*>(a.dst_gx + p.row * a.ld_gx + p.col0 + pb * 16) = out;
+        }
       }
     }
     if (!GW) return;
@@ -700,6 +709,7 @@ void launch_transform_fallback(const TransformArgs& t, int mode, cudaStream_t st
   a.scale_gx = t.scale_gx;
   a.scale_gw = t.scale_gw;
   a.nonfinite = nonfinite_word();
+  a.pack_gx = t.pack_gx;
   const size_t esz = t.dtype == kBF16 ? 2 : 4;
   a.vec = (reinterpret_cast<uintptr_t>(t.src) % 16 == 0) && ((t.ld_src * esz) % 16 == 0) &&
           ((t.seg_src * esz) % 16 == 0);

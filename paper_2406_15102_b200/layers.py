@@ -152,10 +152,12 @@ class HLQLinearFunction(torch.autograd.Function):
             # one fused transform of gy feeds both products (2 reads of gy instead of 4)
             segs, rows, cols, ld_src, seg_src = _proj_view(B, L, O, axis)
             want_gb = has_bias and ctx.needs_input_grad[2]
+            # 4-bit gx codes live in HBM packed two per byte (the dX GEMM sign-extends them in smem)
+            pack = bits_gx == 4 and os.environ.get("HLQ_PACK_GX", "1") != "0"
             # the bias gradient (column sums of gy) comes out of the same kernel's STATS pass
             cgx, sgx, cg, kg, sg, _, *cs = ops.quant_dual(gy3, segs, rows, cols,
                                                           strategy.plan.gpu_bitmap(), bits_gx, bits_gw,
-                                                          ld_src, seg_src, colsum=want_gb)
+                                                          ld_src, seg_src, colsum=want_gb, pack_gx=pack)
             cw, sw = cw_saved, sw_saved
             # the two products are independent: dW on the side stream, dX here
             main = torch.cuda.current_stream()
@@ -168,12 +170,12 @@ class HLQLinearFunction(torch.autograd.Function):
                 gw, gx = ops.gemm_i8_pair(
                     dict(a=cg, b=payload, m=O, n=I, k=k, bits_a=bits_gw, bits_b=bits_gw, sa=sg, sb=sx),
                     dict(a=cgx, b=cw, m=B * L, n=I, k=ops.pad16(O), bits_a=bits_gx, bits_b=bits_gx, sa=sgx,
-                         sb=sw, out_dtype=out_dtype))
+                         sb=sw, out_dtype=out_dtype, a_packed=pack))
             else:
                 with torch.cuda.stream(side):
                     gw, _ = ops.gemm_i8(cg, payload, O, I, k, bits_gw, bits_gw, sg, sx, 1.0, exact=False)
                 gx, _ = ops.gemm_i8(cgx, cw, B * L, I, ops.pad16(O), bits_gx, bits_gx, sgx, sw, 1.0,
-                                    exact=False, out_dtype=out_dtype)
+                                    exact=False, out_dtype=out_dtype, a_packed=pack)
             main.wait_stream(side)
             gw.record_stream(main)
             for t in (cg, sg, payload, sx):
@@ -181,7 +183,8 @@ class HLQLinearFunction(torch.autograd.Function):
             if _STAGES[0] is not None:
                 # parity capture of the training path, in the reference's layouts
                 # (backprop.py:350-410: codes (T, O_p), (O_p, I), (O, K), payload (K, I))
-                _STAGES[0].append(dict(gx_codes_g=cgx[:, :ops.pad16(O)], gx_scale_g=sgx,
+                _STAGES[0].append(dict(gx_codes_g=ops.unpack_int4(cgx, ops.pad16(O)) if pack else cgx[:, :ops.pad16(O)],
+                                       gx_scale_g=sgx, gx_packed=pack,
                                        gx_codes_w=cw[:, :ops.pad16(O)].t(), gx_scale_w=sw,
                                        gw_codes_g=cg[:, :k], gw_scale_g=sg, x_codes=payload[:, :k].t(),
                                        x_scale=sx, axis=axis))

@@ -152,44 +152,61 @@ def quant_ht_cols(src: torch.Tensor, bits: int):
     return codes, scale, stats[0:1]
 
 
+def packed_ld(cols: int) -> int:
+    """Row stride (bytes) of packed int4 codes for `cols` columns: pad16(cols) / 2
+    rounded up to 16 (TMA row strides are 16-byte multiples)."""
+    return (pad16(cols) // 2 + 15) & ~15
+
+
+def unpack_int4(packed: torch.Tensor, cols: int) -> torch.Tensor:
+    """int8 codes (rows, cols) from packed int4 rows (two per byte, low nibble
+    first).  Torch ops -- for parity checks / stage dumps, not the hot path."""
+    p = packed.view(torch.uint8).to(torch.int16)
+    lo, hi = p & 0xF, p >> 4
+    out = torch.stack([lo, hi], dim=-1).reshape(packed.shape[0], -1)[:, :cols]
+    return torch.where(out >= 8, out - 16, out).to(torch.int8)
+
+
 def quant_dual(src: torch.Tensor, segs: int, rows: int, cols: int, bitmap: int, bits_gx: int,
-               bits_gw: int, ld_src: int | None = None, seg_src: int | None = None, colsum: bool = False):
+               bits_gw: int, ld_src: int | None = None, seg_src: int | None = None, colsum: bool = False,
+               pack_gx: bool = False):
     """Both gy operands from one read per pass: HT along cols (gx) and the
     rank-r projection along rows (gw).  Returns
     (gx_codes (segs*rows, pad16(cols)), gx_scale, gw_codes (cols, pad16(K)), K, gw_scale, stats)
     and, with colsum, a 7th item: the fp32 column sums of src (cols,) -- the
-    bias gradient -- computed from the same tiles (hlq_quantize_dual_colsum)."""
+    bias gradient -- computed from the same tiles.  pack_gx (4-bit gx codes):
+    gx_codes is (segs*rows, packed_ld(cols)) uint8, two codes per byte, low
+    nibble first (hlq_quantize_dual_ex) -- the A operand of gemm_i8(a_packed=True)."""
     _check_bits(bits_gx)
     _check_bits(bits_gw)
+    if pack_gx and bits_gx != 4:
+        raise ParameterError("packed gx codes are 4-bit")
     src = _cuda(src, "src")
     ld_src = cols if ld_src is None else ld_src
     seg_src = rows * ld_src if seg_src is None else seg_src
     k = proj_rows_k(segs, rows, bin(bitmap).count("1"))
     ldk = max(pad16(k), 16)
     dev = src.device
-    cgx = torch.empty((segs * rows, pad16(cols)), dtype=torch.int8, device=dev)
+    if pack_gx:
+        cgx = torch.empty((segs * rows, packed_ld(cols)), dtype=torch.uint8, device=dev)
+    else:
+        cgx = torch.empty((segs * rows, pad16(cols)), dtype=torch.int8, device=dev)
     cgw = torch.empty((cols, ldk), dtype=torch.int8, device=dev)
     scales = torch.empty(2, dtype=torch.float32, device=dev)
     stats = torch.empty(STATS_WORDS, dtype=torch.int32, device=dev)
     nbytes = segs * rows * cols * src.element_size() + cgx.numel() + cols * k
     key = f"transform:dual:{segs * rows}x{cols}:{src.dtype}".replace("torch.", "")
-    if not colsum:
-        _traced("transform", nbytes, 0, 1,
-                lambda: _lib.call("hlq_quantize_dual", _p(src), dtype_code(src), segs, rows, cols,
-                                  ld_src, seg_src, bitmap, bits_gx, bits_gw, _p(stats), _p(cgx),
-                                  cgx.stride(0), _p(cgw), ldk, _p(scales), _p(scales[1:]), _stream()),
-                key=key)
-        return cgx, scales[0:1], cgw, k, scales[1:2], stats
-    cs = torch.empty(cols, dtype=torch.float32, device=dev)
-    wsb = int(_lib.load().hlq_quantize_dual_colsum_ws(segs, rows, cols, bitmap))
-    ws = torch.empty(max(wsb, 4), dtype=torch.uint8, device=dev)
-    _traced("transform", nbytes + cols * 4, 0, 1,
-            lambda: _lib.call("hlq_quantize_dual_colsum", _p(src), dtype_code(src), segs, rows, cols,
-                              ld_src, seg_src, bitmap, bits_gx, bits_gw, _p(stats), _p(cgx),
-                              cgx.stride(0), _p(cgw), ldk, _p(scales), _p(scales[1:]), _p(cs), _p(ws), wsb,
-                              _stream()),
+    cs = torch.empty(cols, dtype=torch.float32, device=dev) if colsum else None
+    wsb = int(_lib.load().hlq_quantize_dual_colsum_ws(segs, rows, cols, bitmap)) if colsum else 0
+    ws = torch.empty(max(wsb, 4), dtype=torch.uint8, device=dev) if colsum else None
+    _traced("transform", nbytes + (cols * 4 if colsum else 0), 0, 1,
+            lambda: _lib.call("hlq_quantize_dual_ex", _p(src), dtype_code(src), segs, rows, cols, ld_src, seg_src,
+                              bitmap, bits_gx, bits_gw, _p(stats), _p(cgx), cgx.stride(0), int(pack_gx), _p(cgw),
+                              ldk, _p(scales), _p(scales[1:]), _p(cs), _p(ws), wsb, _stream()),
             key=key)
-    return cgx, scales[0:1], cgw, k, scales[1:2], stats, cs
+    if colsum:
+        return cgx, scales[0:1], cgw, k, scales[1:2], stats, cs
+    return cgx, scales[0:1], cgw, k, scales[1:2], stats
 
 
 def transform_pass(src: torch.Tensor, segs: int, rows: int, cols: int, ld_src: int, seg_src: int,
@@ -411,9 +428,12 @@ def proj_rows_quant(src: torch.Tensor, segs: int, rows: int, cols: int, bitmap: 
 def gemm_i8(a: torch.Tensor, b: torch.Tensor, m: int, n: int, k: int, bits_a: int, bits_b: int,
             sa: torch.Tensor, sb: torch.Tensor, extra: float = 1.0, exact: bool = True,
             out_dtype=torch.float32, want_acc: bool = False, want_out: bool = True,
-            groups: int = 1, a_gstride: int | None = None, b_gstride: int | None = None):
+            groups: int = 1, a_gstride: int | None = None, b_gstride: int | None = None,
+            a_packed: bool = False):
     """D[m, n] = sum_(g,k) A[g][m, k] B[g][n, k] on K-major int8 codes, fused dequant.
     Returns (out or None, acc or None)."""
+    if a_packed:
+        return _gemm_i4a(a, b, m, n, k, bits_b, sa, sb, extra, exact, out_dtype)
     if a.dtype != torch.int8 or b.dtype != torch.int8:
         raise ParameterError("GEMM operands must be int8 codes")
     dev = a.device
@@ -434,6 +454,22 @@ def gemm_i8(a: torch.Tensor, b: torch.Tensor, m: int, n: int, k: int, bits_a: in
                               _p(acc), n, _p(ws), wsb, _stream()),
             key=f"gemm:{m}x{n}x{k * groups}")
     return out, acc
+
+
+def _gemm_i4a(a, b, m, n, k, bits_b, sa, sb, extra, exact, out_dtype):
+    """gemm_i8 with A as packed int4 codes (uint8 (m, >= ceil(k/2)), low nibble
+    first): hlq_gemm_i4a_ex sign-extends them to int8 in shared memory."""
+    if a.dtype != torch.uint8 or b.dtype != torch.int8:
+        raise ParameterError("packed GEMM: A uint8 (two int4 codes per byte), B int8 codes")
+    out = torch.empty((m, n), dtype=out_dtype, device=a.device)
+    _traced("gemm", 0, 2 * m * n * k, 1,
+            lambda: _lib.call("hlq_gemm_i4a_ex", _p(a), a.stride(0), a.stride(0) * m, _p(b), b.stride(0),
+                              b.stride(0) * n, m, n, k, 1, bits_b, _p(sa), _p(sb), float(extra),
+                              _lib.HLQ_EPI_EXACT if exact else _lib.HLQ_EPI_FAST, _p(out),
+                              _lib.HLQ_BF16 if out_dtype == torch.bfloat16 else _lib.HLQ_F32, n, None, 0,
+                              _stream()),
+            key=f"gemm:i4a:{m}x{n}x{k}")
+    return out, None
 
 
 PAIR_MIN_K = 16 * 128  # >= 16 K blocks of 128 bytes in BOTH products (hlq_gemm.cu gemm_i8_pair2_eligible)
@@ -461,8 +497,9 @@ def gemm_i8_pair(p0: dict, p1: dict):
     outs, descs = [], []
     for q in (p0, p1):
         a, b = q["a"], q["b"]
-        if a.dtype != torch.int8 or b.dtype != torch.int8:
-            raise ParameterError("GEMM operands must be int8 codes")
+        packed = bool(q.get("a_packed", False))
+        if a.dtype != (torch.uint8 if packed else torch.int8) or b.dtype != torch.int8:
+            raise ParameterError("GEMM operands must be int8 codes (A: uint8 packed int4 with a_packed)")
         m, n, k = q["m"], q["n"], q["k"]
         od = q.get("out_dtype", torch.float32)
         out = torch.empty((m, n), dtype=od, device=a.device)
@@ -471,7 +508,7 @@ def gemm_i8_pair(p0: dict, p1: dict):
                                    b.stride(0) * n, m, n, k, 1, q["bits_a"], q["bits_b"], q["sa"].data_ptr(),
                                    q["sb"].data_ptr(), float(q.get("extra", 1.0)), _lib.HLQ_EPI_FAST,
                                    out.data_ptr(), _lib.HLQ_BF16 if od == torch.bfloat16 else _lib.HLQ_F32, n, None,
-                                   0))
+                                   0, int(packed)))
     arr = (_lib.GemmDesc * 2)(*descs)
     ops_ = 2 * sum(q["m"] * q["n"] * q["k"] for q in (p0, p1))
     _traced("gemm", 0, ops_, 1, lambda: _lib.call("hlq_gemm_i8_multi", 2, ctypes.cast(arr, ctypes.c_void_p),

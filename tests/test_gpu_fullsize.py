@@ -95,6 +95,7 @@ def test_training_path_autocast_vs_oracle(hlq, name, I, O):
     assert lin._wcodes is not None, "batched weight-codes refresh did not run"
     assert len(recs) == 1
     st = {k: (to_np(v) if torch.is_tensor(v) else v) for k, v in recs[0].items()}
+    assert st["gx_packed"], "the training path keeps the 4-bit gx codes packed two per byte"
     # the oracle sees exactly the values the kernels read: bf16 X (autocast) and bf16 dY, upcast
     xb = xt.detach().to(torch.bfloat16).float().cpu().numpy()
     gb = gyb.float().cpu().numpy()
