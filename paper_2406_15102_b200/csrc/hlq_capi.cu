@@ -392,6 +392,9 @@ static int gemm_ex_impl(const int8_t* A, int64_t lda, int64_t a_gstride, const i
   HLQ_TRY(check_dtype(out_dtype));
   HLQ_TRY(check_ld16(lda, "A"));
   if (a4 && bits_a != 4) return fail(HLQ_ERR_PARAMETER, "packed A holds 4-bit codes, got bits_a=%d", bits_a);
+  // the widened packed codes are 16 * code: the int32 accumulator holds 16 x the sum
+  if (a4 && (long double)K * groups * 16 * 7 * qmax_of(bits_b) >= 2147483648.0L)
+    return fail(HLQ_ERR_PARAMETER, "packed-A contraction extent %lld exceeds the int32-exact bound", (long long)K);
   const int64_t a_row = a4 ? (K + 1) / 2 : K;  // bytes of one A row
   HLQ_TRY(check_ld16(ldb, "B"));
   if (M < 0 || N < 0 || K <= 0 || lda < a_row || ldb < K || (out && ldo < N) || (acc_out && ld_acc < N))

@@ -36,41 +36,44 @@ namespace {
 constexpr int kBM = 128;
 constexpr int kBK = 128;  // bytes of K per stage = one 128B swizzle row
 constexpr int kThreads = 256;
-// Packed int4 A operand: + 4 converter warps (8..11)
-constexpr int kThreadsA4 = 384;
+// Packed int4 A operand: + kConvWarps converter warps (8 .. 8 + kConvWarps - 1)
+constexpr int kConvWarps = 8;
+constexpr int kConvThreads = 32 * kConvWarps;
+constexpr int kThreadsA4 = 256 + kConvThreads;
 constexpr uint32_t kPackedA = kBM * kBK / 2;  // one stage of packed A: 128 rows x 64 bytes
 
 // ---------------------------------------------------------------- packed int4 A
 // The gx codes Q4(H.gy) can live in HBM packed two per byte, low nibble first
 // (the ACBP container's nibble order, acbp.py:56-61) -- half the bytes of the
-// int8 form.  tcgen05 has no int4 MMA and TMA cannot sign-extend nibbles, so
-// the TMA loads each 128 x 64-byte packed tile into the UPPER half of the
-// stage's A slot and 4 converter warps sign-extend it in place into the
-// 128 x 128-byte SWIZZLE_128B K-major int8 tile kind::i8 reads (all packed
-// input is read into registers, then a named barrier, then the writes).
-__device__ __forceinline__ uint32_t sext_nibbles(uint32_t v) {
-  // v: one nibble in the low half of each byte -> the bytes' int8 values:
-  // (v ^ 8) + 0x78 stays below 0x88 per byte (no carries), ^ 0x80 = v - 16 [v >= 8]
-  return ((v ^ 0x08080808u) + 0x78787878u) ^ 0x80808080u;
-}
+// int8 form.  tcgen05 has no int4 MMA and TMA cannot widen nibbles, so the TMA
+// loads each 128 x 64-byte packed tile into the UPPER half of the stage's A
+// slot and 4 converter warps widen it in place into the 128 x 128-byte
+// SWIZZLE_128B K-major int8 tile kind::i8 reads (all packed input is read into
+// registers, then a named barrier, then the writes).  A nibble placed in the
+// HIGH half of its byte is the int8 value 16 * code (two's complement), so the
+// widening needs no sign extension: the MMA accumulates 16 * sum(a b) (exact:
+// 16 * 49 * K < 2^31 for K < 2.7 M) and the host folds 1/16 into the dequant
+// scale -- power-of-two scalings are exact, so the outputs are bit-identical.
 __device__ __forceinline__ void unpack8(uint32_t x, uint32_t& o0, uint32_t& o1) {
-  const uint32_t lo = sext_nibbles(x & 0x0F0F0F0Fu);         // codes 0, 2, 4, 6
-  const uint32_t hi = sext_nibbles((x >> 4) & 0x0F0F0F0Fu);  // codes 1, 3, 5, 7
+  const uint32_t lo = (x << 4) & 0xF0F0F0F0u;  // 16 * codes 0, 2, 4, 6
+  const uint32_t hi = x & 0xF0F0F0F0u;         // 16 * codes 1, 3, 5, 7
   o0 = __byte_perm(lo, hi, 0x5140);
   o1 = __byte_perm(lo, hi, 0x7362);
 }
-// ct = converter thread 0..127.  Unit u = (row u / 4, 16 packed bytes u % 4 =
-// K codes [32 q, 32 q + 32)) -> int8 chunks 2q and 2q+1 of the row, at chunk
-// position c ^ (row % 8) (the 128B swizzle of a 1024-byte aligned tile).
+// ct = converter thread 0 .. kConvThreads-1.  Unit u = (row u / 4, 16 packed
+// bytes u % 4 = K codes [32 q, 32 q + 32)) -> int8 chunks 2q and 2q+1 of the
+// row, at chunk position c ^ (row % 8) (the 128B swizzle of a 1024-byte
+// aligned tile).
 __device__ __forceinline__ void convert_a4(uint8_t* slot, int ct) {
+  constexpr int kUnits = 512 / kConvThreads;
   const uint32_t base = ptx::smem_u32(slot);
-  uint4 in[4];
+  uint4 in[kUnits];
 #pragma unroll
-  for (int j = 0; j < 4; ++j) in[j] = ptx::lds128(base + kPackedA + uint32_t(ct + 128 * j) * 16u);
-  asm volatile("bar.sync 3, 128;" ::: "memory");
+  for (int j = 0; j < kUnits; ++j) in[j] = ptx::lds128(base + kPackedA + uint32_t(ct + kConvThreads * j) * 16u);
+  asm volatile("bar.sync 3, %0;" ::"n"(kConvThreads) : "memory");
 #pragma unroll
-  for (int j = 0; j < 4; ++j) {
-    const int u = ct + 128 * j, r = u >> 2, q = u & 3;
+  for (int j = 0; j < kUnits; ++j) {
+    const int u = ct + kConvThreads * j, r = u >> 2, q = u & 3;
     uint32_t o[8];
     unpack8(in[j].x, o[0], o[1]);
     unpack8(in[j].y, o[2], o[3]);
@@ -249,7 +252,7 @@ __global__ void __launch_bounds__(A4 ? kThreadsA4 : kThreads, 1)
     for (int s = 0; s < STAGES; ++s) {
       ptx::mbar_init(&full[s], 1);
       ptx::mbar_init(&empty[s], 1);
-      ptx::mbar_init(&aready[s], 4);
+      ptx::mbar_init(&aready[s], kConvWarps);
     }
     for (int a = 0; a < 2; ++a) {
       ptx::mbar_init(&tfull[a], 1);
@@ -527,7 +530,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(A4ANY ? kThreadsA4 :
     }
     for (int s = 0; s < STAGES; ++s) {
       ptx::mbar_init(&pfull[s], 1);
-      ptx::mbar_init(&aready[s], 8);  // 4 converter warps x 2 CTAs
+      ptx::mbar_init(&aready[s], 2 * kConvWarps);  // converter warps x 2 CTAs
     }
     ptx::fence_mbar_init();
   }
@@ -645,7 +648,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(A4ANY ? kThreadsA4 :
           pph ^= 1u << stage;
           convert_a4(sA + stage * kABytes, ct);
           __syncwarp();
-          if (lane == 0) ptx::mbar_arrive_cluster(aready_leader + uint32_t(stage) * 8u);
+          if (lane == 0) ptx::mbar_arrive_remote(aready_leader + uint32_t(stage) * 8u);
         }
         if (++stage == STAGES) stage = 0;
       }
@@ -891,9 +894,9 @@ int run(const int8_t* A, int64_t lda, const int8_t* B, int64_t ldb, int64_t M, i
                       : make_map(&ma, A, M, K, lda, groups, a_gstride, kBM);
   if (!okA || !make_map(&mb, B, N, K, ldb, groups, b_gstride, BN)) return -1;
   const ConvGeo geo{0, 0, 0, 0, 0, 0};
-  if (a4)
-    return run_maps<BN, STAGES, true>(ma, mb, M, N, K, groups, sa, sb, extra, epilogue, out, out_dtype, ldo,
-                                      acc_out, ld_acc, splits, ws, geo, stream);
+  if (a4)  // the widened A holds 16 * code: 1/16 in the dequant scale (exact)
+    return run_maps<BN, STAGES, true>(ma, mb, M, N, K, groups, sa, sb, extra * 0.0625, epilogue, out, out_dtype,
+                                      ldo, acc_out, ld_acc, splits, ws, geo, stream);
   return run_maps<BN, STAGES>(ma, mb, M, N, K, groups, sa, sb, extra, epilogue, out, out_dtype, ldo, acc_out,
                               ld_acc, splits, ws, geo, stream);
 }
@@ -928,7 +931,8 @@ bool fill_prob(PairParams& P, int q, const PairSpec& s, int unit0) {
   p.M = int(s.M); p.N = int(s.N); p.K = int(s.K); p.groups = int(s.groups); p.splits = s.splits;
   p.tma_out = make_out_map(&P.o[q], s.out, s.out_dtype, s.M, s.N, s.ldo, s.epilogue, s.acc_out, s.splits) ? 1 : 0;
   if (!p.tma_out) P.o[q] = P.a[q];  // unused
-  p.epilogue = s.epilogue; p.out_dtype = s.out_dtype; p.sa = s.sa; p.sb = s.sb; p.extra = s.extra;
+  p.epilogue = s.epilogue; p.out_dtype = s.out_dtype; p.sa = s.sa; p.sb = s.sb;
+  p.extra = s.a4 ? s.extra * 0.0625 : s.extra;  // packed A is widened to 16 * code
   p.out = s.out; p.ldo = s.ldo; p.acc_out = s.acc_out; p.ld_acc = s.ld_acc;
   p.slabs = s.splits > 1 ? static_cast<int32_t*>(s.ws) : nullptr;
   p.unit0 = unit0;
@@ -1005,8 +1009,8 @@ int run_2sm_specs(const PairSpec* specs, int n, cudaStream_t stream) {
       int fgrid = int((nq + 255) / 256);
       if (fgrid > num_sms() * 8) fgrid = num_sms() * 8;
       splitk_finalize<<<fgrid, 256, 0, stream>>>(static_cast<int32_t*>(s.ws), s.splits, int(s.M), int(s.N), s.sa,
-                                                 s.sb, s.extra, s.epilogue, s.out, s.out_dtype, s.ldo, s.acc_out,
-                                                 s.ld_acc);
+                                                 s.sb, s.a4 ? s.extra * 0.0625 : s.extra, s.epilogue, s.out,
+                                                 s.out_dtype, s.ldo, s.acc_out, s.ld_acc);
     }
   }
   return int(cudaGetLastError());

@@ -160,6 +160,13 @@ __device__ __forceinline__ void cluster_sync() {
 __device__ __forceinline__ void mbar_arrive_cluster(uint32_t cluster_addr) {
   asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(cluster_addr) : "memory");
 }
+// The same arrive with the default (.cta-scope release) semantics, as CUTLASS's
+// ClusterBarrier::arrive(cta_id) issues it: no GPU-scope MEMBAR per call.  Used
+// by the packed-A converters, whose shared-memory writes feed the pair
+// leader's tensor-core reads (fence.proxy.async first).
+__device__ __forceinline__ void mbar_arrive_remote(uint32_t cluster_addr) {
+  asm volatile("mbarrier.arrive.shared::cluster.b64 _, [%0];" ::"r"(cluster_addr) : "memory");
+}
 // CTA-pair TMA: data into this CTA's smem, completion bytes to an mbarrier that
 // may live in the peer CTA (the pair leader's full barrier).
 __device__ __forceinline__ void tma_load_3d_2sm(void* smem_dst, const CUtensorMap* map, uint32_t bar_cluster,

@@ -41,6 +41,14 @@ def _blv(shape):
 
 
 _SIDE = {}
+PACK_GX = [None]  # None: HLQ_PACK_GX from the environment (default off); True / False: forced
+
+
+def pack_gx_enabled() -> bool:
+    """Whether the training path keeps the 4-bit gx codes packed two per byte."""
+    if PACK_GX[0] is not None:
+        return bool(PACK_GX[0])
+    return os.environ.get("HLQ_PACK_GX", "0") == "1"
 _STAGES = [None]  # list sink while capture_stages() is active
 
 
@@ -152,8 +160,10 @@ class HLQLinearFunction(torch.autograd.Function):
             # one fused transform of gy feeds both products (2 reads of gy instead of 4)
             segs, rows, cols, ld_src, seg_src = _proj_view(B, L, O, axis)
             want_gb = has_bias and ctx.needs_input_grad[2]
-            # 4-bit gx codes live in HBM packed two per byte (the dX GEMM sign-extends them in smem)
-            pack = bits_gx == 4 and os.environ.get("HLQ_PACK_GX", "1") != "0"
+            # 4-bit gx codes packed two per byte in HBM (the dX GEMM widens them in smem):
+            # half the code bytes, bit-identical results, but measured 12-15 % slower dX GEMMs
+            # and a ~1 % slower ViT-B/16 step on B200 -- opt-in (PACK_GX / HLQ_PACK_GX=1)
+            pack = bits_gx == 4 and pack_gx_enabled()
             # the bias gradient (column sums of gy) comes out of the same kernel's STATS pass
             cgx, sgx, cg, kg, sg, _, *cs = ops.quant_dual(gy3, segs, rows, cols,
                                                           strategy.plan.gpu_bitmap(), bits_gx, bits_gw,

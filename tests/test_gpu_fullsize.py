@@ -71,10 +71,12 @@ def _bf16_round(a: np.ndarray) -> np.ndarray:
     return torch.from_numpy(np.ascontiguousarray(a)).to(torch.bfloat16).float().numpy()
 
 
-@pytest.mark.parametrize("name,I,O", [("fc1", 768, 3072), ("fc2", 3072, 768)])
-def test_training_path_autocast_vs_oracle(hlq, name, I, O):
-    from paper_2406_15102_b200 import ops
+@pytest.mark.parametrize("name,I,O,packed", [("fc1", 768, 3072, False), ("fc2", 3072, 768, False),
+                                            ("fc1", 768, 3072, True), ("fc2", 3072, 768, True)])
+def test_training_path_autocast_vs_oracle(hlq, name, I, O, packed):
+    from paper_2406_15102_b200 import layers, ops
     from paper_2406_15102_b200.layers import HLQLinear, capture_stages, convert_linears
+    layers.PACK_GX[0] = packed
     B, L = 128, 197
     x, w, gy = orc.make_inputs(O * 7 + I, (B, L, I), (O, I), (B, L, O))
     net = convert_linears(torch.nn.Sequential(torch.nn.Linear(I, O))).to(DEV)
@@ -94,8 +96,9 @@ def test_training_path_autocast_vs_oracle(hlq, name, I, O):
         torch.cuda.synchronize()
     assert lin._wcodes is not None, "batched weight-codes refresh did not run"
     assert len(recs) == 1
+    layers.PACK_GX[0] = None
     st = {k: (to_np(v) if torch.is_tensor(v) else v) for k, v in recs[0].items()}
-    assert st["gx_packed"], "the training path keeps the 4-bit gx codes packed two per byte"
+    assert st["gx_packed"] == packed
     # the oracle sees exactly the values the kernels read: bf16 X (autocast) and bf16 dY, upcast
     xb = xt.detach().to(torch.bfloat16).float().cpu().numpy()
     gb = gyb.float().cpu().numpy()
