@@ -8,7 +8,7 @@ HLQ_BENCH_MIN_WARMUP_S=0 timeout 900 ncu --metrics gpu__time_duration.sum --cloc
   --csv --log-file gpurun_out/launches.csv python bench.py --steps 1 --warmup 1 --no-extras > gpurun_out/launches_bench.log 2>&1
 # 2. the dominant kernel class: the fused transform (fc1 gy, dual, one cooperative launch)
 timeout 300 ncu --set full --clock-control none --import-source on -k regex:tma_tile_kernel -s 1 -c 1 \
-  -o gpurun_out/prof_dual python tools/prof_driver.py dual 128,197,768,3072 2 > /dev/null 2>&1
+  -o gpurun_out/prof_dual python tools/prof_driver.py dualcs 128,197,768,3072 2 > /dev/null 2>&1
 # (acbp: launches 0-2 are the driver's setup transforms; -s 3 = the first ACBP of the loop)
 timeout 300 ncu --set full --clock-control none --import-source on -k regex:tma_tile_kernel -s 3 -c 1 \
   -o gpurun_out/prof_acbp python tools/prof_driver.py acbp 128,197,3072,768 2 > /dev/null 2>&1
