@@ -196,7 +196,7 @@ HLQ_API size_t hlq_gemm_i8_ws(int64_t M, int64_t N, int64_t K, int64_t groups);
  * in int64 up to MAX_K = {8: 10^6, 4: 10^7} (quantize.py:19-21,166-170) and
  * hlq_gemm_i8_ex fails with PARAMETER past that bound, as int_matmul does.
  * Such products need ws of hlq_gemm_i8_ws_bits(...) bytes (they cannot run
- * unsplit), N % 4 == 0, and acc_out == NULL (an int32 dump could overflow). */
+ * unsplit) and acc_out == NULL (an int32 dump could overflow). */
 HLQ_API size_t hlq_gemm_i8_ws_bits(int64_t M, int64_t N, int64_t K, int64_t groups, int bits_a, int bits_b);
 HLQ_API int hlq_gemm_i8_ex(const int8_t* A, int64_t lda, int64_t a_gstride, const int8_t* B,
                            int64_t ldb, int64_t b_gstride, int64_t M, int64_t N, int64_t K,

@@ -412,9 +412,8 @@ static int gemm_ex_impl(const int8_t* A, int64_t lda, int64_t a_gstride, const i
     if (acc_out)
       return fail(HLQ_ERR_PARAMETER, "contraction extent %lld exceeds the int32 accumulator dump bound",
                   (long long)(K * groups));
-    if (N % 4 || !ws || ws_bytes < hlq::gemm_i8_ws_bytes(M, N, K, groups, min_splits))
-      return fail(HLQ_ERR_PARAMETER,
-                  "contraction extent %lld needs K chunks: N %% 4 == 0 and hlq_gemm_i8_ws_bits bytes of workspace",
+    if (!ws || ws_bytes < hlq::gemm_i8_ws_bytes(M, N, K, groups, min_splits))
+      return fail(HLQ_ERR_PARAMETER, "contraction extent %lld needs K chunks: hlq_gemm_i8_ws_bits bytes of workspace",
                   (long long)(K * groups));
   }
   if (epilogue != HLQ_EPI_EXACT && epilogue != HLQ_EPI_FAST)

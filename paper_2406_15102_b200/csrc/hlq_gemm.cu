@@ -722,12 +722,29 @@ __global__ void __launch_bounds__(256) splitk_finalize(const int32_t* __restrict
                                                        int M, int N, const float* __restrict__ sa,
                                                        const float* __restrict__ sb, double extra,
                                                        int epilogue, void* out, int out_dtype, int64_t ldo,
-                                                       int32_t* acc_out, int64_t ld_acc) {
+                                                       int32_t* acc_out, int64_t ld_acc, int vec) {
   const float comb = __fmul_rn(*sa, *sb);
   const double dscale = __dmul_rn(double(comb), extra);
   const float fscale = float(dscale);
   const int64_t plane = int64_t(M) * N;
-  const int64_t nq = plane >> 2;  // N % 4 == 0 is required by the launcher
+  if (!vec) {
+    // any N / output alignment (e.g. the 27 columns of an RGB stem's conv dW): one element per thread
+    for (int64_t e = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; e < plane; e += int64_t(gridDim.x) * blockDim.x) {
+      long long a = __ldcs(slabs + e);
+      for (int s = 1; s < splits; ++s) a += __ldcs(slabs + s * plane + e);
+      const int64_t m = e / N, n = e - m * N;
+      if (acc_out) acc_out[m * ld_acc + n] = int(a);
+      if (!out) continue;
+      const float v = epilogue == kEpiExact ? __double2float_rn(__dmul_rn(__ll2double_rn(a), dscale))
+                                            : __fmul_rn(__ll2float_rn(a), fscale);
+      if (out_dtype == kF32)
+        static_cast<float*>(out)[m * ldo + n] = v;
+      else
+        static_cast<__nv_bfloat16*>(out)[m * ldo + n] = __float2bfloat16_rn(v);
+    }
+    return;
+  }
+  const int64_t nq = plane >> 2;  // vec: N % 4 == 0 and 16-byte aligned rows
   for (int64_t q = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; q < nq; q += int64_t(gridDim.x) * blockDim.x) {
     const int4 t0 = __ldcs(reinterpret_cast<const int4*>(slabs) + q);
     long long a[4] = {t0.x, t0.y, t0.z, t0.w};
@@ -879,8 +896,10 @@ int run_maps(const CUtensorMap& ma, const CUtensorMap& mb, int64_t M, int64_t N,
     const int64_t nq = M * N / 4;
     int fgrid = int((nq + 255) / 256);
     if (fgrid > num_sms() * 8) fgrid = num_sms() * 8;
+    const int vec = (N % 4 == 0) && (ldo % 4 == 0) && (reinterpret_cast<uintptr_t>(out) % 16 == 0) &&
+                    (ld_acc % 4 == 0) && (reinterpret_cast<uintptr_t>(acc_out) % 16 == 0);
     splitk_finalize<<<fgrid, 256, 0, stream>>>(slabs, splits, int(M), int(N), sa, sb, extra, epilogue, out,
-                                               out_dtype, ldo, acc_out, ld_acc);
+                                               out_dtype, ldo, acc_out, ld_acc, vec);
   }
   return int(cudaGetLastError());
 }
@@ -1008,9 +1027,11 @@ int run_2sm_specs(const PairSpec* specs, int n, cudaStream_t stream) {
       const int64_t nq = s.M * s.N / 4;
       int fgrid = int((nq + 255) / 256);
       if (fgrid > num_sms() * 8) fgrid = num_sms() * 8;
+      const int vec = (s.N % 4 == 0) && (s.ldo % 4 == 0) && (reinterpret_cast<uintptr_t>(s.out) % 16 == 0) &&
+                      (s.ld_acc % 4 == 0) && (reinterpret_cast<uintptr_t>(s.acc_out) % 16 == 0);
       splitk_finalize<<<fgrid, 256, 0, stream>>>(static_cast<int32_t*>(s.ws), s.splits, int(s.M), int(s.N), s.sa,
                                                  s.sb, s.a4 ? s.extra * 0.0625 : s.extra, s.epilogue, s.out,
-                                                 s.out_dtype, s.ldo, s.acc_out, s.ld_acc);
+                                                 s.out_dtype, s.ldo, s.acc_out, s.ld_acc, vec);
     }
   }
   return int(cudaGetLastError());
@@ -1082,7 +1103,7 @@ GemmPlan plan_gemm_base(int64_t M, int64_t N, int64_t K, int64_t groups, bool al
   // fc2 dX, K = 768) stays single-CTA: its epilogue, not the operand stream,
   // dominates.
   const int64_t tiles128 = m_tiles * ((N + 127) / 128);
-  const bool split_case = allow_split && 2 * tiles128 <= sms && nk >= 16 && N % 4 == 0;
+  const bool split_case = allow_split && 2 * tiles128 <= sms && nk >= 16;
   if (!split_case && nk >= 16 && M >= 2 * kBM && sms >= 2) {
     const int64_t pairs = sms / 2, pm = (M + 2 * kBM - 1) / (2 * kBM);
     const int64_t u256 = pm * ((N + 255) / 256), u192 = pm * ((N + 191) / 192), u128 = pm * ((N + 127) / 128);
@@ -1100,9 +1121,15 @@ GemmPlan plan_gemm_base(int64_t M, int64_t N, int64_t K, int64_t groups, bool al
   // at fc1 size, which outweighs the wave gain once >= half the SMs are busy
   // (tools/gemm_sweep.py, B200).  (the finalize pass reads 16-byte int32 quads:
   // N % 4 == 0)
-  if (allow_split && 2 * tiles <= sms && nk >= 16 && N % 4 == 0) {
+  if (allow_split && 2 * tiles <= sms && nk >= 16) {
     int64_t sp = sms / tiles;
-    if (sp > 4) sp = 4;
+    // the cap is the int32 slab round trip (splits x M x N x 4 bytes written and
+    // re-read): 4 splits at ViT dW sizes (9.4 MB per slab), up to 64 for the
+    // small-output, very long-K products of conv wgrad (ResNet CIFAR stem dW:
+    // 64 x 27 outputs, K = 131072 -- one tile, 4 splits left 144 SMs idle)
+    int64_t cap = (int64_t(64) << 20) / (M * N * 4);
+    cap = cap < 4 ? 4 : (cap > 64 ? 64 : cap);
+    if (sp > cap) sp = cap;
     while (sp > 1 && nk / sp < 8) --sp;
     p.splits = int(sp);
   }
@@ -1118,7 +1145,7 @@ GemmPlan finish_plan(GemmPlan p, int64_t M, int64_t N, bool allow_split) {
   }
   if (const char* e = getenv("HLQ_GEMM_SPLITS")) {
     const int s = atoi(e);
-    if (s >= 1 && s <= 64 && allow_split && N % 4 == 0) p.splits = s;
+    if (s >= 1 && s <= 64 && allow_split) p.splits = s;
   }
   if (const char* e = getenv("HLQ_GEMM_PAIR")) p.pair = atoi(e) != 0;
   if (p.splits > 1) p.ws = size_t(p.splits) * M * N * 4;
@@ -1165,7 +1192,8 @@ int launch_gemm_i8(const int8_t* A, int64_t lda, const int8_t* B, int64_t ldb, i
   GemmPlan p = plan_gemm(M, N, K, groups, true, min_splits);
   const bool vec_out = (ldo % 4 == 0) && (reinterpret_cast<uintptr_t>(out) % 16 == 0) &&
                        (ld_acc % 4 == 0) && (reinterpret_cast<uintptr_t>(acc_out) % 16 == 0);
-  if (p.splits > 1 && (ws == nullptr || ws_bytes < p.ws || !vec_out || (reinterpret_cast<uintptr_t>(ws) % 16))) {
+  (void)vec_out;  // splitk_finalize has a scalar path for any N / output alignment
+  if (p.splits > 1 && (ws == nullptr || ws_bytes < p.ws || (reinterpret_cast<uintptr_t>(ws) % 16))) {
     if (min_splits > 1) return -2;  // a long contraction cannot run without its chunk slabs
     p = plan_gemm(M, N, K, groups, false);
   }

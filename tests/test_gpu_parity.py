@@ -320,3 +320,29 @@ def test_reference_frac_rounding_ties(hlq):
     assert np.array_equal(to_np(cgx)[:, :ref_gx.shape[1]], ref_gx)
     ref_gw, _ = orc.quantize(np.ascontiguousarray(orc.transform_axis(g3, 1, 16).reshape(16, -1).T), 8)
     assert np.array_equal(to_np(cg)[:, :kg], ref_gw)
+
+
+@pytest.mark.parametrize("m,n,k", [(64, 27, 131072),   # ResNet CIFAR stem conv dW: split-K, N % 4 != 0
+                                   (64, 27, 140000),   # ... past the int32 bound (int64 chunk sum)
+                                   (100, 9, 40000)])
+def test_split_k_any_n(hlq, m, n, k):
+    from paper_2406_15102_b200 import ops
+    rng = np.random.default_rng(m + n)
+    ld = ops.pad16(k)
+    a = rng.integers(-127, 128, size=(m, k)).astype(np.int8)
+    b = rng.integers(-127, 128, size=(n, k)).astype(np.int8)
+    A = torch.zeros((m, ld), dtype=torch.int8, device=DEV)
+    Bm = torch.zeros((n, ld), dtype=torch.int8, device=DEV)
+    A[:, :k] = torch.from_numpy(a).to(DEV)
+    Bm[:, :k] = torch.from_numpy(b).to(DEV)
+    sa = torch.tensor([0.5], device=DEV)
+    sb = torch.tensor([2.0 ** -18], device=DEV)
+    ref = (a.astype(np.float64) @ b.astype(np.float64).T).astype(np.int64)
+    out, _ = ops.gemm_i8(A, Bm, m, n, k, 8, 8, sa, sb, 1.0, exact=True)
+    assert np.array_equal(to_np(out), orc.dequant(ref, np.float32(0.5), np.float32(2.0 ** -18)))
+    assert int(_lib_ws(m, n, k)) > 0  # the planner splits these long contractions
+
+
+def _lib_ws(m, n, k):
+    from paper_2406_15102_b200 import _lib
+    return _lib.load().hlq_gemm_i8_ws_bits(m, n, k, 1, 8, 8)
