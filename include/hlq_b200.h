@@ -415,6 +415,18 @@ HLQ_API int hlq_conv_dgrad_i8(const int8_t* gcodes, int64_t ld_g, int64_t B, int
                               int epilogue, void* dx_nhwc, int dx_dtype, int32_t* acc_out,
                               void* stream);
 
+/* Implicit-GEMM dgrad for any stride: dX (B, H, W, C) channels-last, H / W the
+ * forward input extent ((H + 2 pad - k) / stride + 1 == Ho).  Stride s > 1 runs
+ * as s^2 output phases (h = s h' + ph): phase (ph, pw) is a stride-1
+ * correlation of the gy codes with the taps i = (ph + pad) mod s + s t -- no
+ * zero-inserted gy, no dcols tensor -- and its rows are scattered to dX by the
+ * epilogue (harness/layers.py:153-158 lowers this to GEMM + col2im).  Taps are
+ * summed in int32 before the dequant, as at stride 1. */
+HLQ_API int hlq_conv_dgrad_i8_ex(const int8_t* gcodes, int64_t ld_g, int64_t B, int64_t Ho, int64_t Wo, int64_t O,
+                                 const int8_t* wcodes, int64_t ld_w, int64_t C, int k, int stride, int pad,
+                                 int64_t H, int64_t W, int bits, const float* sg, const float* sw, int epilogue,
+                                 void* dx_nhwc, int dx_dtype, int32_t* acc_out, void* stream);
+
 /* col2im (layers.py:109-121): dx[b, h, w, c] (channels-last) = sum over taps
  * in the reference's (i, j) order of dcols[b*L + l, c*k*k + i*k + j]
  * (fp32 accumulation; bit-exact vs the reference for fp32 dcols). */

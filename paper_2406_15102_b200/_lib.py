@@ -75,6 +75,8 @@ SIGNATURES = {
                                      ctypes.c_uint64, _I, _I64, _I64, _P, _P, _I64, _P, _P]),
     "hlq_quantize_weights": (_I, [_I, _P, _P, _P, _I, _P, _P, _P, _P, _SZ, _P]),
     "hlq_quantize_weights_ex": (_I, [_I, _P, _P, _P, _I, _P, _P, _P, _P, _P, _SZ, _P]),
+    "hlq_conv_dgrad_i8_ex": (_I, [_P, _I64, _I64, _I64, _I64, _I64, _P, _I64, _I64, _I, _I, _I, _I64, _I64, _I,
+                                  _P, _P, _I, _P, _I, _P, _P]),
     "hlq_conv_dgrad_i8": (_I, [_P, _I64, _I64, _I64, _I64, _I64, _P, _I64, _I64, _I, _I, _I, _I, _P, _P,
                                _I, _P, _I, _P, _P]),
     "hlq_conv_acbp_compress": (_I, [_P, _I, _I64, _I64, _I64, _I64, _I, _I, _I, _U32, _I, _P, _I64,

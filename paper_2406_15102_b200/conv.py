@@ -71,10 +71,11 @@ def _conv_backward(acbp: ACBPActivation, w4: torch.Tensor, gy: torch.Tensor, x_s
                    pad: int, strategy: BackwardStrategy, extra: float, exact: bool, dx_dtype,
                    need_dx: bool = True, need_dw: bool = True, stages: dict | None = None,
                    implicit: bool | None = None, wcodes=None):
-    """implicit (default: stride 1 and not exact): dX as one implicit GEMM over
-    the taps (hlq_conv_dgrad_i8; taps summed in int32, matches the reference to
-    fp32 rounding); otherwise the reference's lowering, GEMM -> dcols -> col2im
-    in tap order (bit-exact with the exact epilogue)."""
+    """implicit (default: not exact): dX as implicit GEMMs over the taps
+    (hlq_conv_dgrad_i8_ex -- one launch, or stride^2 output phases; taps summed
+    in int32, matches the reference to fp32 rounding); otherwise the
+    reference's lowering, GEMM -> dcols -> col2im in tap order (bit-exact with
+    the exact epilogue)."""
     B, C, H, W = x_shape
     O, _, k, _ = w4.shape
     Ho, Wo = gy.shape[2], gy.shape[3]
@@ -107,7 +108,7 @@ def _conv_backward(acbp: ACBPActivation, w4: torch.Tensor, gy: torch.Tensor, x_s
         if want:
             stages.update(gw_codes_g=cg[:, :kg], gw_scale_g=sg, gw_acc=accw)
     if implicit is None:
-        implicit = stride == 1 and not exact and pad <= k - 1
+        implicit = not exact and pad <= k - 1
     if need_dx and (wcodes is not None and not want):
         cw, sw = wcodes  # batched refresh (layers.refresh_weight_codes) for this weight version
         kw = O
@@ -117,7 +118,7 @@ def _conv_backward(acbp: ACBPActivation, w4: torch.Tensor, gy: torch.Tensor, x_s
         cw, kw, sw, _ = ops.quant_proj_rows(w2.contiguous(), 1, O, I, 0xFFFF, bits_gx)
     if need_dx and implicit:
         dx_nhwc, accx = ops.conv_dgrad_i8(cgx, B, Ho, Wo, O, cw, C, k, pad, bits_gx, sgx, sw, exact=exact,
-                                          out_dtype=dx_dtype, want_acc=want)
+                                          out_dtype=dx_dtype, want_acc=want, stride=stride, H=H, W=W)
         dx = dx_nhwc.permute(0, 3, 1, 2)  # NCHW shape, channels_last memory
         if want:
             stages.update(gx_codes_g=cgx, gx_scale_g=sgx, gx_codes_w=cw[:, :kw].t(), gx_scale_w=sw,

@@ -717,32 +717,40 @@ int hlq_acbp_unpack(const uint8_t* buf, int64_t nbytes, const hlq_acbp_info* inf
   return HLQ_OK;
 }
 
-int hlq_conv_dgrad_i8(const int8_t* gcodes, int64_t ld_g, int64_t B, int64_t Ho, int64_t Wo, int64_t O,
-                      const int8_t* wcodes, int64_t ld_w, int64_t C, int k, int stride, int pad,
-                      int bits, const float* sg, const float* sw, int epilogue, void* dx_nhwc,
-                      int dx_dtype, int32_t* acc_out, void* stream) {
+int hlq_conv_dgrad_i8_ex(const int8_t* gcodes, int64_t ld_g, int64_t B, int64_t Ho, int64_t Wo, int64_t O,
+                         const int8_t* wcodes, int64_t ld_w, int64_t C, int k, int stride, int pad, int64_t H,
+                         int64_t W, int bits, const float* sg, const float* sw, int epilogue, void* dx_nhwc,
+                         int dx_dtype, int32_t* acc_out, void* stream) {
   HLQ_TRY(check_bits(bits));
   HLQ_TRY(check_dtype(dx_dtype));
   HLQ_TRY(check_ld16(ld_g, "gy codes"));
   HLQ_TRY(check_ld16(ld_w, "W codes"));
-  if (stride != 1)
-    return fail(HLQ_ERR_PARAMETER, "implicit-GEMM dgrad needs stride 1 (use the GEMM + col2im path)");
-  if (B <= 0 || Ho <= 0 || Wo <= 0 || O <= 0 || C <= 0 || k <= 0 || pad < 0 || pad > k - 1 ||
-      ld_g < pad16(O) || ld_w < pad16(O) || k > 15)
-    return fail(HLQ_ERR_DIMENSION, "bad conv dgrad geometry");
-  const int64_t H = Ho + k - 1 - 2 * pad, W = Wo + k - 1 - 2 * pad;
-  if (H <= 0 || W <= 0 || B * H * W > INT32_MAX)
+  if (B <= 0 || Ho <= 0 || Wo <= 0 || O <= 0 || C <= 0 || k <= 0 || stride <= 0 || stride > 8 || pad < 0 ||
+      pad > k - 1 || ld_g < pad16(O) || ld_w < pad16(O) || k > 15 || H <= 0 || W <= 0 ||
+      (H + 2 * pad - k) / stride + 1 != Ho || (W + 2 * pad - k) / stride + 1 != Wo || H + 2 * pad < k ||
+      W + 2 * pad < k || B * H * W > INT32_MAX)
     return fail(HLQ_ERR_DIMENSION, "bad conv dgrad geometry");
   const long double worst = (long double)k * k * pad16(O) * qmax_of(bits) * qmax_of(bits);
   if (worst >= 2147483648.0L)
     return fail(HLQ_ERR_PARAMETER, "contraction k*k*O exceeds the int32-exact bound");
   if (epilogue != HLQ_EPI_EXACT && epilogue != HLQ_EPI_FAST)
     return fail(HLQ_ERR_PARAMETER, "unknown epilogue %d", epilogue);
-  int e = hlq::launch_conv_dgrad_i8(gcodes, ld_g, B, Ho, Wo, O, wcodes, ld_w, C, k, pad, sg, sw, epilogue,
-                                    dx_nhwc, dx_dtype, C, acc_out, C, static_cast<cudaStream_t>(stream));
+  int e = hlq::launch_conv_dgrad_i8(gcodes, ld_g, B, Ho, Wo, O, wcodes, ld_w, C, k, stride, pad, H, W, sg, sw,
+                                    epilogue, dx_nhwc, dx_dtype, C, acc_out, C, static_cast<cudaStream_t>(stream));
   if (e == -1) return fail(HLQ_ERR_CUDA, "im2col tensor map rejected");
   if (e != 0) return fail(HLQ_ERR_CUDA, "hlq_conv_dgrad_i8: %s", cudaGetErrorString(cudaError_t(e)));
   return HLQ_OK;
+}
+
+int hlq_conv_dgrad_i8(const int8_t* gcodes, int64_t ld_g, int64_t B, int64_t Ho, int64_t Wo, int64_t O,
+                      const int8_t* wcodes, int64_t ld_w, int64_t C, int k, int stride, int pad,
+                      int bits, const float* sg, const float* sw, int epilogue, void* dx_nhwc,
+                      int dx_dtype, int32_t* acc_out, void* stream) {
+  // stride 1 determines dX's extent; strided convs name it (hlq_conv_dgrad_i8_ex)
+  if (stride != 1)
+    return fail(HLQ_ERR_PARAMETER, "strided dgrad needs the dX extent: use hlq_conv_dgrad_i8_ex");
+  return hlq_conv_dgrad_i8_ex(gcodes, ld_g, B, Ho, Wo, O, wcodes, ld_w, C, k, 1, pad, Ho + k - 1 - 2 * pad,
+                              Wo + k - 1 - 2 * pad, bits, sg, sw, epilogue, dx_nhwc, dx_dtype, acc_out, stream);
 }
 
 int hlq_conv_acbp_compress(const void* x_nhwc, int dtype, int64_t B, int64_t H, int64_t W,

@@ -208,15 +208,22 @@ __device__ __forceinline__ void store_row_chunk(const uint32_t (&acc)[32], int64
 // covers K blocks [split*nk/splits, (split+1)*nk/splits) and stores its int32
 // partial tile to workspace slab `split`; splitk_finalize then sums the slabs
 // (integers: exact in any order) and runs the same dequant epilogue.
-// Implicit-GEMM conv dgrad (stride 1): A[m, (tap, o)] = G codes at output pixel
-// m shifted by the flipped tap, read by im2col-mode TMA (zero padding from the
-// map's bounding box); B[c, (tap, o)] = W codes row c*k*k + tap, a 3-D tiled
-// map (o, tap, c).  K loop = taps x channel chunks of 128.
+// Implicit-GEMM conv dgrad: A[m, (tap, o)] = G codes at output pixel m shifted
+// by the flipped tap, read by im2col-mode TMA (zero padding from the map's
+// bounding box); B[c, (tap, o)] = W codes of the tap, a 4-D tiled map
+// (o, tap_j, tap_i, c).  K loop = taps x channel chunks of 128.
+// Stride s > 1 runs as s^2 output phases (h = s h' + ph, w = s w' + pw): phase
+// (ph, pw) is a stride-1 correlation of G with the taps i = i0 + s t
+// (i0 = (ph + pad) mod s), G row h' + (ph + pad - i0)/s - t -- no zero-inserted
+// G and no dcols tensor; its rows are scattered to dX by the epilogue.
 struct ConvGeo {
-  int conv;       // 0: plain GEMM
-  int Ho, Wo;     // gy spatial extent (= the im2col box traversal)
-  int k, padp;    // kernel size, im2col padding k-1-pad
-  int nkc;        // 128-byte channel chunks per tap
+  int conv;        // 0: plain GEMM
+  int Ho, Wo;      // the output grid this launch walks (a phase grid for s > 1)
+  int kh, kw;      // taps of this phase along h / w
+  int lo_h, lo_w;  // im2col base offset of the flipped-tap traversal (-(k-1-pad) at stride 1)
+  int nkc;         // 128-byte channel chunks per tap
+  int s, ph, pw;   // output remap: row (b, h', w') -> dX pixel (b, s h' + ph, s w' + pw)
+  int H, W;        // dX spatial extent
 };
 
 template <int BN, int STAGES, bool A4>
@@ -271,7 +278,7 @@ __global__ void __launch_bounds__(A4 ? kThreadsA4 : kThreads, 1)
   const int tiles = num_m * num_n;
   const int units = tiles * splits;
   const int nk_g = (K + kBK - 1) / kBK;  // K blocks per group
-  const int nk = geo.conv ? geo.k * geo.k * geo.nkc : nk_g * groups;  // groups / taps accumulate
+  const int nk = geo.conv ? geo.kh * geo.kw * geo.nkc : nk_g * groups;  // groups / taps accumulate
 
   if (warp == 0) {
     if (ptx::elect_one()) {
@@ -301,12 +308,11 @@ __global__ void __launch_bounds__(A4 ? kThreadsA4 : kThreads, 1)
             ptx::tma_load_3d(sB + stage * Cfg::kBBytes, &map_b, &full[stage], kg * kBK, nb * BN, g);
           } else if (geo.conv) {
             const int tap = kb / geo.nkc, oc = kb - tap * geo.nkc;
-            const int ti = tap / geo.k, tj = tap - ti * geo.k;
-            // flipped tap (k-1-i, k-1-j): dX[h, w] += G[h + pad - i, w + pad - j] W[i, j]
-            ptx::tma_load_im2col_4d(sA + stage * Cfg::kABytes, &map_a, &full[stage], oc * kBK,
-                                    pw - geo.padp, ph - geo.padp, pn, uint16_t(geo.k - 1 - tj),
-                                    uint16_t(geo.k - 1 - ti));
-            ptx::tma_load_3d(sB + stage * Cfg::kBBytes, &map_b, &full[stage], oc * kBK, tap, nb * BN);
+            const int ti = tap / geo.kw, tj = tap - ti * geo.kw;
+            // flipped tap: dX[h, w] += G[h + pad - i, w + pad - j] W[i, j] (per phase: t = tap index)
+            ptx::tma_load_im2col_4d(sA + stage * Cfg::kABytes, &map_a, &full[stage], oc * kBK, pw + geo.lo_w,
+                                    ph + geo.lo_h, pn, uint16_t(geo.kw - 1 - tj), uint16_t(geo.kh - 1 - ti));
+            ptx::tma_load_4d(sB + stage * Cfg::kBBytes, &map_b, &full[stage], oc * kBK, tj, ti, nb * BN);
           } else {
             ptx::tma_load_3d(sA + stage * Cfg::kABytes, &map_a, &full[stage], kg * kBK, mb * kBM, g);
             ptx::tma_load_3d(sB + stage * Cfg::kBBytes, &map_b, &full[stage], kg * kBK, nb * BN, g);
@@ -403,9 +409,16 @@ __global__ void __launch_bounds__(A4 ? kThreadsA4 : kThreads, 1)
           uint32_t r[32];
           ptx::tmem_ld_32x32b_x32(tmem_base + ((quarter * 32) << 16) + uint32_t(acc * BN + c * 32), r);
           ptx::tmem_ld_wait();
-          if (row < M && col0 < N)
-            store_row_chunk(r, row, col0, N, epilogue, dscale, fscale, out, out_dtype, ldo, vec_ok,
+          if (row < M && col0 < N) {
+            int64_t orow = row;
+            if (geo.conv && geo.s > 1) {  // phase row (b, h', w') -> dX pixel (b, s h' + ph, s w' + pw)
+              const int64_t hw = int64_t(geo.Ho) * geo.Wo;
+              const int64_t b = row / hw, r2 = row - b * hw, hp = r2 / geo.Wo, wp = r2 - hp * geo.Wo;
+              orow = (b * geo.H + geo.s * hp + geo.ph) * geo.W + geo.s * wp + geo.pw;
+            }
+            store_row_chunk(r, orow, col0, N, epilogue, dscale, fscale, out, out_dtype, ldo, vec_ok,
                             acc_out, ld_acc);
+          }
         }
         ptx::tc_fence_before();
         ptx::mbar_arrive(&tempty[acc]);
@@ -887,7 +900,9 @@ int run_maps(const CUtensorMap& ma, const CUtensorMap& mb, int64_t M, int64_t N,
   const int64_t units = tiles * splits;
   const int grid = int(units < num_sms() ? units : num_sms());
   CUtensorMap mo;
-  const int tma_out = make_out_map(&mo, out, out_dtype, M, N, ldo, epilogue, acc_out, splits) ? 1 : 0;
+  // strided conv phases scatter their rows: the direct-store epilogue
+  const int tma_out =
+      (geo.conv && geo.s > 1) ? 0 : (make_out_map(&mo, out, out_dtype, M, N, ldo, epilogue, acc_out, splits) ? 1 : 0);
   if (!tma_out) mo = ma;  // unused
   gemm_i8_kernel<BN, STAGES, A4><<<grid, A4 ? kThreadsA4 : kThreads, Cfg::kSmem, stream>>>(
       ma, mb, mo, tma_out, int(M), int(N), int(K), int(groups), sa, sb, extra, epilogue, out, out_dtype, ldo,
@@ -912,7 +927,7 @@ int run(const int8_t* A, int64_t lda, const int8_t* B, int64_t ldb, int64_t M, i
   const bool okA = a4 ? make_map_a4(&ma, A, M, K, lda, groups, a_gstride)
                       : make_map(&ma, A, M, K, lda, groups, a_gstride, kBM);
   if (!okA || !make_map(&mb, B, N, K, ldb, groups, b_gstride, BN)) return -1;
-  const ConvGeo geo{0, 0, 0, 0, 0, 0};
+  const ConvGeo geo{0, 0, 0, 0, 0, 0, 0, 0, 1, 0, 0, 0, 0};
   if (a4)  // the widened A holds 16 * code: 1/16 in the dequant scale (exact)
     return run_maps<BN, STAGES, true>(ma, mb, M, N, K, groups, sa, sb, extra * 0.0625, epilogue, out, out_dtype,
                                       ldo, acc_out, ld_acc, splits, ws, geo, stream);
@@ -1215,49 +1230,71 @@ int launch_gemm_i8(const int8_t* A, int64_t lda, const int8_t* B, int64_t ldb, i
 }
 
 int launch_conv_dgrad_i8(const int8_t* G, int64_t ldg, int64_t B, int64_t Ho, int64_t Wo, int64_t O,
-                         const int8_t* Wc, int64_t ldw, int64_t C, int k, int pad, const float* sa,
-                         const float* sb, int epilogue, void* out, int out_dtype, int64_t ldo,
-                         int32_t* acc_out, int64_t ld_acc, cudaStream_t stream) {
+                         const int8_t* Wc, int64_t ldw, int64_t C, int k, int stride, int pad, int64_t H,
+                         int64_t W, const float* sa, const float* sb, int epilogue, void* out, int out_dtype,
+                         int64_t ldo, int32_t* acc_out, int64_t ld_acc, cudaStream_t stream) {
   EncodeIm2colFn enc = encode_im2col_fn();
   EncodeTiledFn tenc = encode_fn();
   if (!enc || !tenc) return -1;
-  const int padp = k - 1 - pad;  // dgrad of a stride-1 conv = conv of gy, flipped taps, padding k-1-pad
-  O = (O + 15) & ~int64_t(15);    // the contraction runs over the padded HT blocks (codes of pad16(O))
-  const int64_t H = Ho + 2 * padp - k + 1, W = Wo + 2 * padp - k + 1;
-  CUtensorMap ma, mb;
-  {
-    // gy codes as NHWC int8: dims (O, Wo, Ho, B), pixel stride ldg bytes
-    cuuint64_t dims[4] = {cuuint64_t(O), cuuint64_t(Wo), cuuint64_t(Ho), cuuint64_t(B)};
-    cuuint64_t strides[3] = {cuuint64_t(ldg), cuuint64_t(ldg * Wo), cuuint64_t(ldg * Wo * Ho)};
-    const int lower[2] = {-padp, -padp};
-    const int upper[2] = {padp - (k - 1), padp - (k - 1)};
-    cuuint32_t es[4] = {1, 1, 1, 1};
-    if (enc(&ma, CU_TENSOR_MAP_DATA_TYPE_UINT8, 4, const_cast<int8_t*>(G), dims, strides, lower, upper,
-            cuuint32_t(kBK), cuuint32_t(kBM), es, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
-            CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
-      return -1;
+  const int s = stride;
+  O = (O + 15) & ~int64_t(15);  // the contraction runs over the padded HT blocks (codes of pad16(O))
+  const int nkc = int((O + kBK - 1) / kBK);
+  // phases with output pixels but no tap get no contribution: zero dX (and the acc dump) first
+  bool empty_phase = false;
+  for (int ph = 0; ph < s; ++ph)
+    for (int pw = 0; pw < s; ++pw) {
+      const int i0 = (ph + pad) % s, j0 = (pw + pad) % s;
+      if ((i0 >= k || j0 >= k) && ph < H && pw < W) empty_phase = true;
+    }
+  if (empty_phase) {
+    const size_t esz = out_dtype == kBF16 ? 2 : 4;
+    if (out && cudaMemsetAsync(out, 0, size_t(B * H * W) * ldo * esz, stream) != cudaSuccess) return -1;
+    if (acc_out && cudaMemsetAsync(acc_out, 0, size_t(B * H * W) * ld_acc * 4, stream) != cudaSuccess) return -1;
   }
-  const int64_t taps = int64_t(k) * k;
-  const int bn = (C > 128 && ((B * H * W + kBM - 1) / kBM) * ((C + 255) / 256) >= num_sms()) ? 256 : 128;
-  {
-    // W codes (C*k*k rows of ldw bytes, K = o): dims (O, taps, C)
-    cuuint64_t dims[3] = {cuuint64_t(O), cuuint64_t(taps), cuuint64_t(C)};
-    cuuint64_t strides[2] = {cuuint64_t(ldw), cuuint64_t(ldw * taps)};
-    cuuint32_t box[3] = {cuuint32_t(kBK), 1, cuuint32_t(bn)};
-    cuuint32_t es[3] = {1, 1, 1};
-    if (tenc(&mb, CU_TENSOR_MAP_DATA_TYPE_UINT8, 3, const_cast<int8_t*>(Wc), dims, strides, box, es,
-             CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
-             CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
-      return -1;
-  }
-  const ConvGeo geo{1, int(H), int(W), k, padp, int((O + kBK - 1) / kBK)};
-  // the im2col box walks the OUTPUT (dX) pixel grid H x W of every image
-  const int64_t M = B * H * W;
-  if (bn == 256)
-    return run_maps<256, 4>(ma, mb, M, C, O, 1, sa, sb, 1.0, epilogue, out, out_dtype, ldo, acc_out, ld_acc, 1,
-                            nullptr, geo, stream);
-  return run_maps<128, 6>(ma, mb, M, C, O, 1, sa, sb, 1.0, epilogue, out, out_dtype, ldo, acc_out, ld_acc, 1,
-                          nullptr, geo, stream);
+  for (int ph = 0; ph < s; ++ph)
+    for (int pw = 0; pw < s; ++pw) {
+      const int i0 = (ph + pad) % s, j0 = (pw + pad) % s;
+      const int64_t Hp = (H - ph + s - 1) / s, Wp = (W - pw + s - 1) / s;
+      if (i0 >= k || j0 >= k || Hp <= 0 || Wp <= 0) continue;
+      const int kh = (k - i0 + s - 1) / s, kw = (k - j0 + s - 1) / s;
+      const int dh = (ph + pad - i0) / s, dw = (pw + pad - j0) / s;
+      const int lo_h = dh - kh + 1, lo_w = dw - kw + 1;
+      CUtensorMap ma, mb;
+      {
+        // gy codes as NHWC int8: dims (O, Wo, Ho, B), pixel stride ldg bytes; the traversal
+        // walks the Hp x Wp phase grid: upper corner = lower + (phase extent - gy extent)
+        cuuint64_t dims[4] = {cuuint64_t(O), cuuint64_t(Wo), cuuint64_t(Ho), cuuint64_t(B)};
+        cuuint64_t strides[3] = {cuuint64_t(ldg), cuuint64_t(ldg * Wo), cuuint64_t(ldg * Wo * Ho)};
+        const int lower[2] = {lo_w, lo_h};
+        const int upper[2] = {int(lo_w + Wp - Wo), int(lo_h + Hp - Ho)};
+        cuuint32_t es[4] = {1, 1, 1, 1};
+        if (enc(&ma, CU_TENSOR_MAP_DATA_TYPE_UINT8, 4, const_cast<int8_t*>(G), dims, strides, lower, upper,
+                cuuint32_t(kBK), cuuint32_t(kBM), es, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
+          return -1;
+      }
+      const int64_t M = B * Hp * Wp;
+      const int bn = (C > 128 && ((M + kBM - 1) / kBM) * ((C + 255) / 256) >= num_sms()) ? 256 : 128;
+      {
+        // W codes (C*k*k rows of ldw bytes, K = o), this phase's taps (i0 + s ti, j0 + s tj):
+        // dims (O, kw, kh, C), strides (s ldw, s k ldw, k^2 ldw)
+        cuuint64_t dims[4] = {cuuint64_t(O), cuuint64_t(kw), cuuint64_t(kh), cuuint64_t(C)};
+        cuuint64_t strides[3] = {cuuint64_t(ldw * s), cuuint64_t(ldw * s * k), cuuint64_t(ldw * k * k)};
+        cuuint32_t box[4] = {cuuint32_t(kBK), 1, 1, cuuint32_t(bn)};
+        cuuint32_t es[4] = {1, 1, 1, 1};
+        if (tenc(&mb, CU_TENSOR_MAP_DATA_TYPE_UINT8, 4, const_cast<int8_t*>(Wc + (int64_t(i0) * k + j0) * ldw), dims,
+                 strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                 CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
+          return -1;
+      }
+      const ConvGeo geo{1, int(Hp), int(Wp), kh, kw, lo_h, lo_w, nkc, s, ph, pw, int(H), int(W)};
+      const int e = bn == 256 ? run_maps<256, 4>(ma, mb, M, C, O, 1, sa, sb, 1.0, epilogue, out, out_dtype, ldo,
+                                                 acc_out, ld_acc, 1, nullptr, geo, stream)
+                              : run_maps<128, 6>(ma, mb, M, C, O, 1, sa, sb, 1.0, epilogue, out, out_dtype, ldo,
+                                                 acc_out, ld_acc, 1, nullptr, geo, stream);
+      if (e != 0) return e;
+    }
+  return 0;
 }
 
 }  // namespace hlq

@@ -97,14 +97,14 @@ int launch_gemm_i8(const int8_t* A, int64_t lda, const int8_t* B, int64_t ldb, i
                    const float* sa, const float* sb, double extra, int epilogue,
                    void* out, int out_dtype, int64_t ldo, int32_t* acc_out, int64_t ld_acc,
                    void* ws, size_t ws_bytes, cudaStream_t stream, int min_splits = 1, bool a4 = false);
-// Implicit-GEMM dgrad of a stride-1 conv (k x k, padding pad): dX (B, H, W, C)
+// Implicit-GEMM dgrad of a k x k conv with stride s and padding pad: dX (B, H, W, C)
 // channels-last = sum over taps and o of G codes (B, Ho, Wo, O; pixel stride
 // ldg) at the shifted pixel x W codes (row c*k*k + tap, ld ldw), int32 in TMEM,
-// then the dequant epilogue.
+// then the dequant epilogue.  s > 1: one launch per output phase (s^2).
 int launch_conv_dgrad_i8(const int8_t* G, int64_t ldg, int64_t B, int64_t Ho, int64_t Wo, int64_t O,
-                         const int8_t* Wc, int64_t ldw, int64_t C, int k, int pad, const float* sa,
-                         const float* sb, int epilogue, void* out, int out_dtype, int64_t ldo,
-                         int32_t* acc_out, int64_t ld_acc, cudaStream_t stream);
+                         const int8_t* Wc, int64_t ldw, int64_t C, int k, int stride, int pad, int64_t H,
+                         int64_t W, const float* sa, const float* sb, int epilogue, void* out, int out_dtype,
+                         int64_t ldo, int32_t* acc_out, int64_t ld_acc, cudaStream_t stream);
 // Batched W codes (hlq_weights.cu): Q_bits(HT_O(W_i)) of up to kMaxWeights fp32
 // (O_i, I_i) matrices in one cooperative launch; codes_i is (I_i, ld_i) K-major,
 // scales_i one fp32.  ws: 8 * n + 8 uint32 (statistics + grid barrier).

@@ -544,20 +544,25 @@ def conv_acbp(x_nhwc: torch.Tensor, k: int, stride: int, pad: int, bitmap: int, 
 
 def conv_dgrad_i8(gcodes: torch.Tensor, B: int, Ho: int, Wo: int, O: int, wcodes: torch.Tensor, C: int,
                   k: int, pad: int, bits: int, sg: torch.Tensor, sw: torch.Tensor, exact: bool = False,
-                  out_dtype=torch.bfloat16, want_acc: bool = False):
-    """Implicit-GEMM dX (B, H, W, C) channels-last of a stride-1 conv from the
-    gx codes (B*Ho*Wo, >= O) and the W codes (C*k*k, >= O) -- no dcols tensor,
-    no col2im.  Returns (dx, acc or None)."""
-    H, W = Ho + k - 1 - 2 * pad, Wo + k - 1 - 2 * pad
+                  out_dtype=torch.bfloat16, want_acc: bool = False, stride: int = 1, H: int | None = None,
+                  W: int | None = None):
+    """Implicit-GEMM dX (B, H, W, C) channels-last from the gx codes
+    (B*Ho*Wo, >= O) and the W codes (C*k*k, >= O) -- no dcols tensor, no
+    col2im; stride > 1 runs as stride^2 output phases (hlq_conv_dgrad_i8_ex).
+    H / W: the forward input extent (default: the stride-1 one).  Returns (dx, acc or None)."""
+    if H is None:
+        H = (Ho - 1) * stride + k - 2 * pad
+    if W is None:
+        W = (Wo - 1) * stride + k - 2 * pad
     dx = torch.empty((B, H, W, C), dtype=out_dtype, device=gcodes.device)
     acc = torch.empty((B * H * W, C), dtype=torch.int32, device=gcodes.device) if want_acc else None
-    _traced("gemm", 0, 2 * B * H * W * C * k * k * pad16(O), 1,
-            lambda: _lib.call("hlq_conv_dgrad_i8", _p(gcodes), gcodes.stride(0), B, Ho, Wo, O, _p(wcodes),
-                              wcodes.stride(0), C, k, 1, pad, bits, _p(sg), _p(sw),
+    _traced("gemm", 0, 2 * B * Ho * Wo * C * k * k * pad16(O), 1 if stride == 1 else stride * stride,
+            lambda: _lib.call("hlq_conv_dgrad_i8_ex", _p(gcodes), gcodes.stride(0), B, Ho, Wo, O, _p(wcodes),
+                              wcodes.stride(0), C, k, stride, pad, H, W, bits, _p(sg), _p(sw),
                               _lib.HLQ_EPI_EXACT if exact else _lib.HLQ_EPI_FAST, _p(dx),
                               _lib.HLQ_BF16 if out_dtype == torch.bfloat16 else _lib.HLQ_F32, _p(acc),
                               _stream()),
-            key=f"gemm:conv_dgrad:{B}x{Ho}x{Wo}x{O}->{C}:k{k}")
+            key=f"gemm:conv_dgrad:{B}x{Ho}x{Wo}x{O}->{C}:k{k}s{stride}")
     return dx, acc
 
 

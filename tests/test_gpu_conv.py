@@ -105,50 +105,56 @@ def test_hlq_conv2d_module_autograd(conv):
     assert np.allclose(n(m.bias.grad), gy.sum(axis=(0, 2, 3)), rtol=1e-4, atol=1e-5)
 
 
-def _col2im_int(acc, B, H, W, C, k, p, Ho, Wo):
+def _col2im_int(acc, B, H, W, C, k, p, Ho, Wo, s=1):
     """Integer col2im of per-tap accumulators (B*Ho*Wo, C*k*k) -> (B*H*W, C)."""
     a = acc.astype(np.int64).reshape(B, Ho, Wo, C, k, k)
-    out = np.zeros((B, H + 2 * p + k, W + 2 * p + k, C), dtype=np.int64)
+    out = np.zeros((B, H + 2 * p + k * s, W + 2 * p + k * s, C), dtype=np.int64)
     for i in range(k):
         for j in range(k):
-            out[:, i:i + Ho, j:j + Wo, :] += a[:, :, :, :, i, j]
+            out[:, i:i + s * (Ho - 1) + 1:s, j:j + s * (Wo - 1) + 1:s, :] += a[:, :, :, :, i, j]
     return out[:, p:p + H, p:p + W, :].reshape(B * H * W, C)
 
 
 # (B, C, H, O, k, pad): 3x3 same, 1x1, valid 3x3, 5x5, O < 128 (one partial
 # channel chunk), ragged O and C, M not a multiple of the 128-row tile
 IMPLICIT = [
-    (4, 64, 14, 256, 3, 1),
-    (3, 96, 9, 128, 1, 0),
-    (2, 48, 12, 64, 3, 0),
-    (2, 32, 11, 72, 5, 2),
-    (5, 40, 7, 200, 3, 1),
+    (4, 64, 14, 256, 3, 1, 1),
+    (3, 96, 9, 128, 1, 0, 1),
+    (2, 48, 12, 64, 3, 0, 1),
+    (2, 32, 11, 72, 5, 2, 1),
+    (5, 40, 7, 200, 3, 1, 1),
+    # strided: output phases (north_star item 4; ResNet downsampling convs and shortcuts)
+    (4, 64, 32, 128, 3, 1, 2),   # ResNet-18 CIFAR stage-2 conv
+    (4, 64, 32, 128, 1, 0, 2),   # 1x1 shortcut: three of the four phases have no tap (zero)
+    (3, 48, 15, 64, 3, 1, 2),    # odd extent: phases of different sizes
+    (2, 32, 13, 72, 5, 2, 2),
+    (2, 40, 12, 64, 3, 0, 3),    # stride 3
 ]
 
 
-@pytest.mark.parametrize("B,C,H,O,k,p", IMPLICIT)
-def test_implicit_gemm_dgrad_matches_col2im(conv, B, C, H, O, k, p):
+@pytest.mark.parametrize("B,C,H,O,k,p,s", IMPLICIT)
+def test_implicit_gemm_dgrad_matches_col2im(conv, B, C, H, O, k, p, s):
     from paper_2406_15102_b200.backprop import BackwardStrategy
-    x, w, gy = orc.make_inputs(11 + k + p, (B, C, H, H), (O, C, k, k), (1,))
-    Ho, _ = orc.conv_out_hw(H, H, k, 1, p)
+    x, w, gy = orc.make_inputs(11 + k + p + s, (B, C, H, H), (O, C, k, k), (1,))
+    Ho, _ = orc.conv_out_hw(H, H, k, s, p)
     rng = np.random.default_rng(5)
     gy = (rng.lognormal(0.0, 1.4, (B, O, Ho, Ho)) * rng.choice([-1.0, 1.0], (B, O, Ho, Ho)) * 1e-3)
     gy = gy.astype(np.float32)
     strat = BackwardStrategy.hlq()
     xt, wt, gt = t(x), t(w), t(gy)
-    acbp, _ = conv.conv_acbp_compress(xt, k, 1, p, strat)
+    acbp, _ = conv.conv_acbp_compress(xt, k, s, p, strat)
     st_ref, st_imp = {}, {}
-    dx_ref, _ = conv._conv_backward(acbp, wt, gt, xt.shape, 1, p, strat, 1.0, True, torch.float32,
+    dx_ref, _ = conv._conv_backward(acbp, wt, gt, xt.shape, s, p, strat, 1.0, True, torch.float32,
                                     need_dw=False, stages=st_ref, implicit=False)
-    dx_imp, _ = conv._conv_backward(acbp, wt, gt, xt.shape, 1, p, strat, 1.0, True, torch.float32,
+    dx_imp, _ = conv._conv_backward(acbp, wt, gt, xt.shape, s, p, strat, 1.0, True, torch.float32,
                                     need_dw=False, stages=st_imp, implicit=True)
     torch.cuda.synchronize()
-    want = _col2im_int(n(st_ref["gx_acc"]), B, H, H, C, k, p, Ho, Ho)
+    want = _col2im_int(n(st_ref["gx_acc"]), B, H, H, C, k, p, Ho, Ho, s)
     assert np.array_equal(n(st_imp["dx_acc"]).astype(np.int64), want)
     a, b = n(dx_imp), n(dx_ref)
     assert np.linalg.norm(a - b) / np.linalg.norm(b) < 1e-6
     # and against the CPU oracle (reference Conv2d.backward, 1/B not applied to dX)
-    rdx, _ = orc.conv2d_hlq_backward(x, w, gy, 1, p)
+    rdx, _ = orc.conv2d_hlq_backward(x, w, gy, s, p)
     assert np.linalg.norm(a - rdx) / np.linalg.norm(rdx) < 1e-6
 
 
