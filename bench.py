@@ -209,6 +209,7 @@ def workload_config(args, world):
             "global_batch": args.batch * world, "per_gpu_batch": args.batch, "seq_len": TOKENS,
             "image": IMG, "parallelism": f"dp{world}", "amp": "bf16",
             "dp_mode": getattr(args, "dp_mode", "replica") if world > 1 else None,
+            "hlq_reserved_sms": int(os.environ.get("HLQ_DP_RESERVED_SMS", "8")) if world > 1 else 0,
             "hlq": "gx int4 HQ (block 16), gw int8 HLA rank 8, ACBP int8; 49 Linear layers",
             "l2": "per-step working set (activations, codes) >> 126 MB L2; no flush needed"}
 
@@ -741,14 +742,22 @@ def run_ours(args):
     local = int(os.environ.get("LOCAL_RANK", "0")) % max(1, torch.cuda.device_count())
     torch.cuda.set_device(local)
     dist = None
+    reserve = 0
     if world > 1:
         if args.dist_backend == "nccl":
+            # DDP's gradient all-reduce runs beside the HLQ kernels: cap NCCL's CTAs and keep
+            # that many SMs out of libhlq's persistent / cooperative grids, so a cooperative
+            # transform never waits for an all-reduce at its grid barrier (HLQ_DP_RESERVED_SMS)
+            reserve = int(os.environ.get("HLQ_DP_RESERVED_SMS", "8"))
+            if reserve > 0:
+                os.environ.setdefault("NCCL_MAX_CTAS", str(reserve))
             dist_mod.init_process_group("nccl", device_id=torch.device("cuda", local))
         else:
             dist_mod.init_process_group(args.dist_backend)
         dist = dist_mod
     if _lib.load().hlq_device_ok() != 1:
         raise RuntimeError("libhlq_b200 needs an sm_100 device")
+    _lib.load().hlq_set_reserved_sms(reserve)
     torch.backends.cuda.matmul.allow_tf32 = True
     torch.backends.cudnn.allow_tf32 = True
 

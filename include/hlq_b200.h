@@ -472,6 +472,12 @@ HLQ_API int hlq_grad_weight(const int8_t* payload, int64_t ld_payload, const flo
  * stream-ordered, no host synchronisation, CUDA-graph capturable. */
 HLQ_API int hlq_nonfinite_fetch(uint32_t* dst, int reset, void* stream);
 
+/* Keep n SMs free of libhlq's grids (persistent GEMMs, cooperative transforms);
+ * returns the previous value.  For data parallelism: the gradient all-reduce's
+ * NCCL kernels (limit them with NCCL_MAX_CTAS) then run beside the HLQ kernels
+ * instead of delaying a cooperative transform at its grid barrier. */
+HLQ_API int hlq_set_reserved_sms(int n);
+
 #ifdef __cplusplus
 }
 #endif

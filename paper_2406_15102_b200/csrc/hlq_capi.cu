@@ -16,6 +16,12 @@
 
 namespace hlq {
 
+// SMs kept free of libhlq's persistent / cooperative grids (hlq_set_reserved_sms):
+// under data parallelism the NCCL kernels of the gradient all-reduce run
+// concurrently, and a cooperative transform grid sized to every SM would wait
+// for them at its grid barrier.
+static std::atomic<int> g_reserved_sms{0};
+
 int num_sms() {
   static thread_local int dev_cached = -1;
   static thread_local int sms = 148;
@@ -26,10 +32,16 @@ int num_sms() {
     if (cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev) == cudaSuccess && v > 0) sms = v;
     dev_cached = dev;
   }
-  return sms;
+  const int avail = sms - g_reserved_sms.load(std::memory_order_relaxed);
+  return avail < 2 ? 2 : avail;
 }
 
 }  // namespace hlq
+
+extern "C" int hlq_set_reserved_sms(int n) {
+  if (n < 0) n = 0;
+  return hlq::g_reserved_sms.exchange(n);
+}
 
 namespace {
 

@@ -223,3 +223,31 @@ def test_autocast_forward_uses_refreshed_bf16_weights(ops):
 
     for a, b in zip(run(True), run(False)):
         assert torch.equal(a, b)
+
+
+def test_reserved_sms_same_results():
+    """hlq_set_reserved_sms (data-parallel runs keep SMs free for NCCL): smaller
+    persistent / cooperative grids, identical results."""
+    import torch
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    from paper_2406_15102_b200 import _lib, ops
+    lib = _lib.load()
+    torch.manual_seed(0)
+    gy = (torch.randn(16, 197, 3072, device="cuda") * 1e-3).to(torch.bfloat16)
+    x = torch.randint(-127, 128, (768, 6656), dtype=torch.int8, device="cuda")
+
+    def run():
+        cgx, sgx, cg, k, sg, _, cs = ops.quant_dual(gy, 16, 197, 3072, 0x5555, 4, 8, 3072, 197 * 3072, colsum=True)
+        w = torch.randint(-7, 8, (768, 3072), dtype=torch.int8, device="cuda")
+        torch.manual_seed(1)
+        dw, _ = ops.gemm_i8(cg, x, 3072, 768, k, 8, 8, sg, sg, 1.0, exact=True)
+        return [cgx, sgx, cg, sg, cs, dw]
+    ref = run()
+    prev = lib.hlq_set_reserved_sms(40)
+    try:
+        got = run()
+    finally:
+        lib.hlq_set_reserved_sms(prev)
+    for a, b in zip(ref, got):
+        assert torch.equal(a, b)
