@@ -1154,15 +1154,11 @@ GemmPlan plan_gemm_base(int64_t M, int64_t N, int64_t K, int64_t groups, bool al
 // tuning knobs (development sweeps): HLQ_GEMM_SPLITS=s forces s splits (1 = off),
 // HLQ_GEMM_BN=128|256 forces the tile width, HLQ_GEMM_PAIR=0|1 the CTA-pair kernel
 GemmPlan finish_plan(GemmPlan p, int64_t M, int64_t N, bool allow_split) {
-  if (const char* e = getenv("HLQ_GEMM_BN")) {
-    const int bn = atoi(e);
-    if (bn == 128 || ((bn == 256 || bn == 192) && N > 128)) p.bn = bn;
-  }
-  if (const char* e = getenv("HLQ_GEMM_SPLITS")) {
-    const int s = atoi(e);
-    if (s >= 1 && s <= 64 && allow_split) p.splits = s;
-  }
-  if (const char* e = getenv("HLQ_GEMM_PAIR")) p.pair = atoi(e) != 0;
+  static const int knob_bn = env_knob("HLQ_GEMM_BN"), knob_splits = env_knob("HLQ_GEMM_SPLITS"),
+                   knob_pair = env_knob("HLQ_GEMM_PAIR");
+  if (knob_bn == 128 || ((knob_bn == 256 || knob_bn == 192) && N > 128)) p.bn = knob_bn;
+  if (knob_splits >= 1 && knob_splits <= 64 && allow_split) p.splits = knob_splits;
+  if (knob_pair >= 0) p.pair = knob_pair != 0;
   if (p.splits > 1) p.ws = size_t(p.splits) * M * N * 4;
   return p;
 }
@@ -1183,15 +1179,13 @@ int launch_gemm_i8_pair2(const GemmDesc* d, cudaStream_t stream) {
 }
 
 bool gemm_i8_pair2_eligible(const GemmDesc* d) {
-  static const int min_nk = [] {
-    const char* e = getenv("HLQ_GEMM_PAIR_MINK");  // development sweeps
-    return e ? atoi(e) : 16;
-  }();
+  static const int min_nk = env_knob("HLQ_GEMM_PAIR_MINK") >= 0 ? env_knob("HLQ_GEMM_PAIR_MINK") : 16;  // sweeps
+  static const int knob_fuse2 = env_knob("HLQ_GEMM_FUSE2");
   for (int q = 0; q < 2; ++q) {
     const int64_t nk = ((d[q].K + kBK - 1) / kBK) * d[q].groups;
     if (nk < min_nk || d[q].M < 2 * kBM) return false;
   }
-  if (const char* e = getenv("HLQ_GEMM_FUSE2")) return atoi(e) != 0;
+  if (knob_fuse2 >= 0) return knob_fuse2 != 0;
   return true;
 }
 

@@ -2,6 +2,7 @@
 #pragma once
 #include <cuda_runtime.h>
 #include <atomic>
+#include <cstdlib>
 #include <cstdint>
 
 namespace hlq {
@@ -11,6 +12,10 @@ enum : int { kStats = 0, kQuant = 1, kBoth = 2 };  // kBoth: one cooperative lau
 enum : int { kEpiExact = 0, kEpiFast = 1 };
 
 int num_sms();
+
+// Development knob from the environment, read once per process (-1 when unset).
+// Launch paths must not call getenv per launch (it scans the environment).
+inline int env_knob(const char* name);
 
 // This device's sticky "a quantized operand held NaN/Inf" word (hlq_transform.cu):
 // every transform kernel ORs 1 into it when an operand's amax bits are
@@ -175,6 +180,11 @@ inline int gemm_min_splits(int64_t K, int64_t groups, int qa, int qb) {
   const int64_t per = (int64_t(2147483647) / (int64_t(128) * qa * qb));  // blocks per exact chunk
   if (K * groups * int64_t(qa) * qb < int64_t(2147483648LL)) return 1;
   return int((kb + per - 1) / per);
+}
+
+inline int env_knob(const char* name) {
+  const char* e = std::getenv(name);
+  return e ? std::atoi(e) : -1;
 }
 
 }  // namespace hlq

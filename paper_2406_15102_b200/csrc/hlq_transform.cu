@@ -734,10 +734,9 @@ void launch_one(const CUtensorMap& map, Args a, cudaStream_t stream) {
       per_sm < 1)
     per_sm = 1;
   if (per_sm > 4) per_sm = 4;  // 5 resident CTAs measured no faster (more tail per item)
-  if (const char* e = getenv("HLQ_TR_CTAS_PER_SM")) {  // development sweeps
-    const int v = atoi(e);
-    if (v >= 1 && v < per_sm) per_sm = v;
-  }
+  static const int knob_cps = env_knob("HLQ_TR_CTAS_PER_SM");  // development sweeps
+  if (knob_cps >= 1 && knob_cps < per_sm) per_sm = knob_cps;
+
   const int cap = num_sms() * per_sm;
   const int grid = a.items < 1 ? 1 : (a.items > cap ? cap : a.items);
   if (MODE != kBoth) {
@@ -799,10 +798,8 @@ int choose_nb(int total_blocks, int cols, int rank) {
   int nb = rank >= 8 ? 4 : (rank >= 4 ? 8 : 16);
   const int ncol_tiles = (cols + kCols - 1) / kCols;
   while (nb > 1 && ((total_blocks + nb - 1) / nb) * ncol_tiles < num_sms() * 3) nb >>= 1;
-  if (const char* e = getenv("HLQ_TR_NB")) {  // development sweeps
-    const int v = atoi(e);
-    if (v >= 1 && v <= 16) nb = v;
-  }
+  static const int knob_nb = env_knob("HLQ_TR_NB");  // development sweeps
+  if (knob_nb >= 1 && knob_nb <= 16) nb = knob_nb;
   return nb;
 }
 
@@ -871,7 +868,8 @@ bool launch_conv_acbp_tma(const void* x, int dtype, int B, int H, int W, int C, 
       k - 1 - pad > 127 || k > 16 || Ho * Wo < 16)
     return false;
   // narrow inputs: several taps per 256-column step, one C-channel im2col box each
-  const int tq = (C == 32 || C == 64 || C == 128) && getenv("HLQ_CONV_NOGROUP") == nullptr ? kCols / C : 1;
+  static const bool nogroup_conv = env_knob("HLQ_CONV_NOGROUP") != -1;
+  const int tq = (C == 32 || C == 64 || C == 128) && !nogroup_conv ? kCols / C : 1;
   CUtensorMap map;
   const cuuint64_t dims[4] = {cuuint64_t(C), cuuint64_t(W), cuuint64_t(H), cuuint64_t(B)};
   const cuuint64_t strides[3] = {cuuint64_t(C) * esz, cuuint64_t(C) * esz * W, cuuint64_t(C) * esz * W * H};
@@ -935,7 +933,8 @@ void launch_transform(const TransformArgs& t, int mode, cudaStream_t stream) {
   CUtensorMap map;
   bool ok = fits32 && aligned && t.rows > 0 && t.cols > 0 && t.segs > 0;
   // narrow sources: row groups of 256 / cols blocks per step (one cols-wide box each)
-  const int tq = (t.cols == 32 || t.cols == 64 || t.cols == 128) && getenv("HLQ_TR_NOGROUP") == nullptr
+  static const bool nogroup = env_knob("HLQ_TR_NOGROUP") != -1;
+  const int tq = (t.cols == 32 || t.cols == 64 || t.cols == 128) && !nogroup
                      ? int(kCols / t.cols) : 1;
   if (ok) {
     const uint64_t seg_stride = t.segs > 1 ? uint64_t(t.seg_src) * esz
