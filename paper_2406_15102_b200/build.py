@@ -82,10 +82,32 @@ def build(force: bool = False, verbose: bool = False) -> str:
     return LIB
 
 
+def build_trace() -> str:
+    """Development build with -DHLQ_TR_TRACE (per-CTA globaltimer stamps of the
+    fused transform, tools/tr_timeline.py) into libhlq_b200_trace.so."""
+    objdir = os.path.join(HERE, "build_trace")
+    os.makedirs(objdir, exist_ok=True)
+    out = os.path.join(HERE, "libhlq_b200_trace.so")
+    objs, procs = [], []
+    for src in SOURCES:
+        obj = os.path.join(objdir, src.replace(".cu", ".o"))
+        objs.append(obj)
+        procs.append(subprocess.Popen([nvcc(), *NVCC_FLAGS, "-DHLQ_TR_TRACE", "-I", os.path.join(ROOT, "include"),
+                                       "-c", os.path.join(CSRC, src), "-o", obj]))
+    for p in procs:
+        if p.wait() != 0:
+            raise subprocess.CalledProcessError(p.returncode, "nvcc (trace build)")
+    subprocess.run([nvcc(), *NVCC_FLAGS, "-shared", *objs, "-o", out], check=True)
+    return out
+
+
 if __name__ == "__main__":
     ap = argparse.ArgumentParser()
     ap.add_argument("--verbose", action="store_true")
     ap.add_argument("--force", action="store_true")
+    ap.add_argument("--trace", action="store_true", help="also build libhlq_b200_trace.so (-DHLQ_TR_TRACE)")
     a = ap.parse_args()
     print(build(force=a.force or a.verbose, verbose=a.verbose))
+    if a.trace:
+        print(build_trace())
     sys.exit(0)

@@ -149,11 +149,14 @@ struct Stat {
   }
   // global layout {amax bits, ~(minnz bits - 1)}, both max-reduced so a zero
   // memset is the identity (NaN from max.NaN is 0x7FFFFFFF: flagged non-finite)
+  // Fire-and-forget reductions (RED, no returned value): the committing thread
+  // does not wait for an L2 round trip per word before it arrives at the grid
+  // barrier, whose release orders them.
   __device__ __forceinline__ void commit(uint32_t* g) const {
     const uint32_t ab = __float_as_uint(amax) & 0x7FFFFFFFu;
-    if (ab) atomicMax(g, ab);
+    if (ab) asm volatile("red.relaxed.gpu.global.max.u32 [%0], %1;" ::"l"(g), "r"(ab) : "memory");
     const uint32_t mb = __float_as_uint(mnz);
-    if (mb < 0x7F800000u) atomicMax(g + 1, ~mb);
+    if (mb < 0x7F800000u) asm volatile("red.relaxed.gpu.global.max.u32 [%0], %1;" ::"l"(g + 1), "r"(~mb) : "memory");
   }
 };
 

@@ -677,17 +677,15 @@ __global__ void __launch_bounds__(kThreads, HLQ_TR_MINB) tma_tile_kernel(const _
   if (MODE == kStats) return;
   // ---------------- grid barrier (consumer threads only; all CTAs co-resident)
   if (threadIdx.x == 0) {
-    // release-add, relaxed L2 polling (no L1 invalidation per probe), one
-    // acquire fence once every CTA has arrived
-    uint32_t seen;
-    asm volatile("fence.acq_rel.gpu;\n\tatom.relaxed.gpu.global.add.u32 %0, [%1], 1;"
-                 : "=r"(seen) : "l"(a.stats + 32) : "memory");
-    ++seen;
+    // release-reduction (no returned value to wait for) orders this CTA's
+    // statistics; acquire loads poll until every CTA has arrived
+    uint32_t seen = 0;
+    asm volatile("red.release.gpu.global.add.u32 [%0], 1;" ::"l"(a.stats + 32) : "memory");
+    asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(seen) : "l"(a.stats + 32) : "memory");
     while (seen < gridDim.x) {
       __nanosleep(32);
-      asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];" : "=r"(seen) : "l"(a.stats + 32) : "memory");
+      asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(seen) : "l"(a.stats + 32) : "memory");
     }
-    asm volatile("fence.acq_rel.gpu;" ::: "memory");
   }
   asm volatile("bar.sync 2, %0;" ::"n"(kConsumers) : "memory");
   stamp(2);

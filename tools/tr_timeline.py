@@ -41,6 +41,11 @@ def main():
     buf = torch.zeros(148 * 8 * 8, dtype=torch.int64, device="cuda")
     lib.hlq_debug_set_trace.argtypes = [ctypes.c_void_p]
     lib.hlq_debug_set_trace(ctypes.c_void_p(buf.data_ptr()))
+    if len(sys.argv) > 1 and sys.argv[1] == "small":
+        for B, L, O in [(256, 16, 512), (256, 64, 256), (256, 256, 128), (256, 1024, 64)]:
+            gy = (torch.randn(B, L, O, device="cuda") * 1e-3).to(torch.bfloat16)
+            run(f"dual {B}x{L}x{O}", lambda: ops.quant_dual(gy, B, L, O, 0x5555, 4, 8, O, L * O, colsum=True), buf)
+        return
     if len(sys.argv) > 1 and sys.argv[1] == "config_a":
         T = 4096
         for bm in (0x0101, 0x5555):
