@@ -274,6 +274,14 @@ HLQ_API int hlq_conv_acbp_compress(const void* x_nhwc, int dtype, int64_t B, int
                                    int bits, int8_t* payload, int64_t ld_payload, float* scale_out,
                                    uint32_t* stats_ws, void* stream);
 
+/* One pass of hlq_conv_acbp_compress: mode 0 = STATS (max-accumulates into
+ * stats_ws[2..3]; zero them first, or all-reduce(MAX) them across ranks
+ * after), mode 1 = QUANT with the scale those statistics imply -- the exact
+ * data-parallel mode's global-scale ACBP of a conv input (dp.ExactDP). */
+HLQ_API int hlq_conv_acbp_pass(const void* x_nhwc, int dtype, int64_t B, int64_t H, int64_t W, int64_t C, int k,
+                               int stride, int pad, uint32_t bitmap, int bits, int mode, uint32_t* stats_ws,
+                               int8_t* payload, int64_t ld_payload, float* scale_out, void* stream);
+
 /* True stochastic rounding (quantize.py:114-125), bit-exact with the
  * reference's RngState streams: codes of the transformed source with
  * up = f64(q - floor(q)) > U, U = the element's draw from numpy's

@@ -49,6 +49,7 @@ SIGNATURES = {
                                  _P, _D, _I, _P, _I, _I64, _P, _I64, _P]),
     "hlq_gemm_i8_ws": (_SZ, [_I64, _I64, _I64, _I64]),
     "hlq_gemm_i8_ws_bits": (_SZ, [_I64, _I64, _I64, _I64, _I, _I]),
+    "hlq_conv_acbp_pass": (_I, [_P, _I, _I64, _I64, _I64, _I64, _I, _I, _I, _U32, _I, _I, _P, _P, _I64, _P, _P]),
     "hlq_set_reserved_sms": (_I, [_I]),
     "hlq_nonfinite_fetch": (_I, [_P, _I, _P]),
     "hlq_acbp_container_bytes": (_I64, [_I64, _I64, _I]),

@@ -31,9 +31,10 @@ def _to_nhwc(x: torch.Tensor) -> torch.Tensor:
     return x.permute(0, 2, 3, 1).contiguous()
 
 
-def conv_acbp_compress(x: torch.Tensor, k: int, stride: int, pad: int, strategy: BackwardStrategy):
+def conv_acbp_compress(x: torch.Tensor, k: int, stride: int, pad: int, strategy: BackwardStrategy, dp=None):
     """ACBP of im2col(x) (layers.py:141-151 + backprop.py:373-385).  Returns an
-    ACBPActivation whose orig_shape is the lowered (B, L, C*k*k)."""
+    ACBPActivation whose orig_shape is the lowered (B, L, C*k*k).  dp
+    (dp.ExactDP): the scale of the whole data-parallel batch (amax is then None)."""
     B, C, H, W = x.shape
     Ho, Wo = ops.conv_out_hw(H, W, k, stride, pad)
     L = Ho * Wo
@@ -54,15 +55,29 @@ def conv_acbp_compress(x: torch.Tensor, k: int, stride: int, pad: int, strategy:
         win = xp.as_strided((B, Ho, Wo, C, k, k), (sb, stride * sh, stride * sw, sc, sh, sw))
         cols = torch.zeros((B, L, ldc), dtype=x.dtype, device=x.device)
         cols[:, :, :I] = win.reshape(B, L, I)
-        codes, kk, scale, amax = ops.quant_proj_rows(cols, B, L, I, plan.gpu_bitmap(), bits, ldc, L * ldc)
+        if dp is not None:
+            codes, kk, scale = dp.quant_rows(cols, B, L, I, ldc, L * ldc, plan.gpu_bitmap(), bits)
+            amax = None
+        else:
+            codes, kk, scale, amax = ops.quant_proj_rows(cols, B, L, I, plan.gpu_bitmap(), bits, ldc, L * ldc)
+    elif axis == 1 and dp is not None:
+        codes, kk, scale = dp.quant_conv(_to_nhwc(x), k, stride, pad, plan.gpu_bitmap(), bits)
+        amax = None
     elif axis == 1:
         codes, kk, scale, amax = ops.conv_acbp(_to_nhwc(x), k, stride, pad, plan.gpu_bitmap(), bits)
     else:
         # L < 16: projection along the batch axis needs the lowered tensor itself
         cols = F.unfold(x, k, padding=pad, stride=stride).transpose(1, 2).contiguous()
         segs, rows, cols_, ld, sg = _proj_view(B, L, C * k * k, axis)
-        codes, kk, scale, amax = ops.quant_proj_rows(cols, segs, rows, cols_, plan.gpu_bitmap(), bits,
-                                                     ld, sg)
+        if dp is not None:
+            if B % plan.block_size:
+                raise ParameterError("exact DP with the batch-axis projection needs shards of a multiple "
+                                     f"of {plan.block_size} images, got {B}")
+            codes, kk, scale = dp.quant_rows(cols, segs, rows, cols_, ld, sg, plan.gpu_bitmap(), bits)
+            amax = None
+        else:
+            codes, kk, scale, amax = ops.quant_proj_rows(cols, segs, rows, cols_, plan.gpu_bitmap(), bits,
+                                                         ld, sg)
     q = QuantizedTensor(payload=codes, bits=bits, scale=scale)
     return ACBPActivation(quantized=q, orig_shape=(B, L, C * k * k), axis=axis, plan=plan, k=kk), amax
 
@@ -70,7 +85,7 @@ def conv_acbp_compress(x: torch.Tensor, k: int, stride: int, pad: int, strategy:
 def _conv_backward(acbp: ACBPActivation, w4: torch.Tensor, gy: torch.Tensor, x_shape, stride: int,
                    pad: int, strategy: BackwardStrategy, extra: float, exact: bool, dx_dtype,
                    need_dx: bool = True, need_dw: bool = True, stages: dict | None = None,
-                   implicit: bool | None = None, wcodes=None):
+                   implicit: bool | None = None, wcodes=None, dp=None):
     """implicit (default: not exact): dX as implicit GEMMs over the taps
     (hlq_conv_dgrad_i8_ex -- one launch, or stride^2 output phases; taps summed
     in int32, matches the reference to fp32 rounding); otherwise the
@@ -89,7 +104,11 @@ def _conv_backward(acbp: ACBPActivation, w4: torch.Tensor, gy: torch.Tensor, x_s
     segs, rows, cols, ld_src, seg_src = _proj_view(B, L, O, acbp.axis)
     dx = dw = None
     want = stages is not None
-    if acbp.axis == 1:
+    if dp is not None:
+        # exact data-parallel mode: both gy operands with the whole batch's scales
+        cgx, sgx, cg, kg, sg = dp.quant_gy(gy3.reshape(B, L, O), acbp.axis, acbp.plan.gpu_bitmap(), bits_gx,
+                                           bits_gw)
+    elif acbp.axis == 1:
         cgx, sgx, cg, kg, sg, st = ops.quant_dual(gy3, segs, rows, cols, acbp.plan.gpu_bitmap(),
                                                   bits_gx, bits_gw, ld_src, seg_src)
     else:
@@ -98,15 +117,23 @@ def _conv_backward(acbp: ACBPActivation, w4: torch.Tensor, gy: torch.Tensor, x_s
         cgx, sgx, _ = ops.quant_ht_cols(gy3.reshape(B * L, O), bits_gx)
     if kg != acbp.k:
         raise DimensionError("projected extents differ between forward and backward")
+    pending = None
     if need_dw:
         groups = L if acbp.axis == 0 else 1
         xp = acbp.quantized.payload
-        dw2, accw = ops.gemm_i8(cg, xp, O, I, kg, bits_gw, bits_gw, sg, acbp.quantized.scale, extra,
-                                exact=exact, want_acc=want, groups=groups,
-                                a_gstride=cg.stride(0) * O, b_gstride=xp.stride(0) * I)
-        dw = dw2.reshape(O, C, k, k)
-        if want:
-            stages.update(gw_codes_g=cg[:, :kg], gw_scale_g=sg, gw_acc=accw)
+        if dp is not None:
+            # exact int32 partial sums, all-reduced under the dX GEMM, one dequant
+            _, accw = ops.gemm_i8(cg, xp, O, I, kg, bits_gw, bits_gw, sg, acbp.quantized.scale, 1.0,
+                                  want_acc=True, want_out=False, groups=groups,
+                                  a_gstride=cg.stride(0) * O, b_gstride=xp.stride(0) * I)
+            pending = dp.reduce_acc_async(accw, kg, groups, bits_gw)
+        else:
+            dw2, accw = ops.gemm_i8(cg, xp, O, I, kg, bits_gw, bits_gw, sg, acbp.quantized.scale, extra,
+                                    exact=exact, want_acc=want, groups=groups,
+                                    a_gstride=cg.stride(0) * O, b_gstride=xp.stride(0) * I)
+            dw = dw2.reshape(O, C, k, k)
+            if want:
+                stages.update(gw_codes_g=cg[:, :kg], gw_scale_g=sg, gw_acc=accw)
     if implicit is None:
         implicit = not exact and pad <= k - 1
     if need_dx and (wcodes is not None and not want):
@@ -139,6 +166,10 @@ def _conv_backward(acbp: ACBPActivation, w4: torch.Tensor, gy: torch.Tensor, x_s
         if want:
             stages.update(gx_codes_g=cgx, gx_scale_g=sgx, gx_codes_w=cw[:, :kw].t(), gx_scale_w=sw,
                           gx_acc=accx, dcols=dcols)
+    if pending is not None:
+        acc, work = pending
+        work.wait()
+        dw = dp.dequant_fast(acc, sg, acbp.quantized.scale).reshape(O, C, k, k)
     return dx, dw
 
 
@@ -166,18 +197,19 @@ def conv2d_hlq_backward(x: torch.Tensor, w4: torch.Tensor, gy: torch.Tensor, str
 
 class HLQConv2dFunction(torch.autograd.Function):
     @staticmethod
-    def forward(ctx, x, weight, bias, stride, pad, strategy: BackwardStrategy, wcodes=None):
+    def forward(ctx, x, weight, bias, stride, pad, strategy: BackwardStrategy, wcodes=None, dp=None):
         y = F.conv2d(x, weight.to(x.dtype), None if bias is None else bias.to(x.dtype),
                      stride=stride, padding=pad)
         ctx.wcodes = wcodes if ctx.needs_input_grad[0] else None
         acbp = None
         if ctx.needs_input_grad[1]:
-            acbp, _ = conv_acbp_compress(x.detach(), weight.shape[2], stride, pad, strategy)
+            acbp, _ = conv_acbp_compress(x.detach(), weight.shape[2], stride, pad, strategy, dp=dp)
             ctx.save_for_backward(weight, acbp.quantized.payload, acbp.quantized.scale)
         else:
             ctx.save_for_backward(weight, None, None)
         ctx.meta = (tuple(x.shape), x.dtype, stride, pad, strategy, bias is not None,
                     None if acbp is None else (acbp.axis, acbp.k, acbp.orig_shape))
+        ctx.dp = dp
         return y
 
     @staticmethod
@@ -189,20 +221,20 @@ class HLQConv2dFunction(torch.autograd.Function):
             # no weight gradient requested: dX only (dense path is the stock op)
             dx = torch.nn.grad.conv2d_input(x_shape, weight.to(gy.dtype), gy, stride=stride,
                                             padding=pad)
-            return dx, None, None, None, None, None, None
+            return dx, None, None, None, None, None, None, None
         axis, kk, orig = am
         acbp = ACBPActivation(QuantizedTensor(payload, strategy.grad_weight_path.bits or 8, sx), orig,
                               axis, strategy.plan, kk)
         out_dtype = x_dtype if x_dtype in (torch.float32, torch.bfloat16) else torch.float32
         dx, dw = _conv_backward(acbp, weight, gy, x_shape, stride, pad, strategy, 1.0, False,
-                                out_dtype, need_dx=ctx.needs_input_grad[0], wcodes=ctx.wcodes)
+                                out_dtype, need_dx=ctx.needs_input_grad[0], wcodes=ctx.wcodes, dp=ctx.dp)
         if dx is not None and dx.dtype != x_dtype:
             dx = dx.to(x_dtype)
         if weight.dtype != torch.float32:
             dw = dw.to(weight.dtype)
         if has_bias and ctx.needs_input_grad[2]:
             db = gy.sum(dim=(0, 2, 3), dtype=torch.float32)
-        return dx, dw, db, None, None, None, None
+        return dx, dw, db, None, None, None, None, None
 
 
 class HLQConv2d(nn.Conv2d):
@@ -219,6 +251,7 @@ class HLQConv2d(nn.Conv2d):
         self.strategy = strategy or BackwardStrategy.hlq()
         self._wcodes = None  # (weight version, data_ptr, bits, codes, scale); see refresh_weight_codes
         self._hlq_weight_codes = True
+        self.dp = None  # dp.ExactDP when the exact data-parallel mode is on (dp.enable_exact_dp)
 
     def bits_gx(self) -> int:
         return self.strategy.grad_input_path.bits or 4
@@ -237,7 +270,7 @@ class HLQConv2d(nn.Conv2d):
             x = x.to(torch.get_autocast_dtype("cuda"))
         with torch.autocast("cuda", enabled=False):
             return HLQConv2dFunction.apply(x, self.weight, self.bias, self.stride[0], self.padding[0],
-                                           self.strategy, self.cached_weight_codes())
+                                           self.strategy, self.cached_weight_codes(), self.dp)
 
     @classmethod
     def from_conv(cls, conv: nn.Conv2d, strategy: BackwardStrategy | None = None) -> "HLQConv2d":

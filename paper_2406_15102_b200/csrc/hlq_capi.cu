@@ -795,6 +795,33 @@ int hlq_conv_acbp_compress(const void* x_nhwc, int dtype, int64_t B, int64_t H, 
   return cuda_status("hlq_conv_acbp_compress");
 }
 
+int hlq_conv_acbp_pass(const void* x_nhwc, int dtype, int64_t B, int64_t H, int64_t W, int64_t C, int k,
+                       int stride, int pad, uint32_t bitmap, int bits, int mode, uint32_t* stats_ws,
+                       int8_t* payload, int64_t ld_payload, float* scale_out, void* stream) {
+  HLQ_TRY(check_dtype(dtype));
+  HLQ_TRY(check_bits(bits));
+  HLQ_TRY(check_bitmap(bitmap));
+  if (mode != 0 && mode != 1) return fail(HLQ_ERR_PARAMETER, "mode must be 0 (STATS) or 1 (QUANT)");
+  if (mode == 1) HLQ_TRY(check_ld16(ld_payload, "payload"));
+  if (B <= 0 || H <= 0 || W <= 0 || C <= 0 || k <= 0 || stride <= 0 || pad < 0 ||
+      H + 2 * pad < k || W + 2 * pad < k || B * H * W * C >= (int64_t(1) << 40))
+    return fail(HLQ_ERR_DIMENSION, "bad conv geometry");
+  const int64_t Ho = (H + 2 * pad - k) / stride + 1, Wo = (W + 2 * pad - k) / stride + 1;
+  if (Ho * Wo < 16)
+    return fail(HLQ_ERR_DIMENSION, "conv output has L=Ho*Wo=%lld < 16", (long long)(Ho * Wo));
+  const int64_t kk = B * ((Ho * Wo + 15) / 16) * __builtin_popcount(bitmap);
+  if (mode == 1 && ld_payload < kk)
+    return fail(HLQ_ERR_DIMENSION, "payload ld %lld < K %lld", (long long)ld_payload, (long long)kk);
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  const int m = mode == 0 ? hlq::kStats : hlq::kQuant;
+  if (hlq::launch_conv_acbp_tma(x_nhwc, dtype, int(B), int(H), int(W), int(C), k, stride, pad, bitmap, bits, m,
+                                stats_ws, payload, ld_payload, scale_out, st))
+    return cuda_status("hlq_conv_acbp_pass");
+  hlq::launch_im2col_proj(x_nhwc, dtype, int(B), int(H), int(W), int(C), k, stride, pad, bitmap, bits, m, stats_ws,
+                          payload, ld_payload, scale_out, st);
+  return cuda_status("hlq_conv_acbp_pass");
+}
+
 int hlq_col2im(const void* dcols, int dtype, int64_t ld, int64_t B, int64_t H, int64_t W, int64_t C,
                int k, int stride, int pad, void* dx_nhwc, int out_dtype, void* stream) {
   HLQ_TRY(check_dtype(dtype));

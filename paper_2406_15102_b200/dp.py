@@ -86,6 +86,20 @@ class ExactDP:
                            dst_gw=codes, scale_gw=scale)
         return codes, k, scale
 
+    def quant_conv(self, x_nhwc, k, stride, pad, bitmap, bits):
+        """Global-scale ACBP of im2col(x) (the conv input, channels-last):
+        codes (C*k*k, pad16(K)), K, scale."""
+        B, H, W, C = x_nhwc.shape
+        Ho, Wo = ops.conv_out_hw(H, W, k, stride, pad)
+        kk = B * ((Ho * Wo + 15) // 16) * bin(bitmap).count("1")
+        st = ops.new_stats(x_nhwc.device)
+        ops.conv_acbp_pass(x_nhwc, k, stride, pad, bitmap, bits, 0, st)
+        self.reducer.max_stats(st)
+        codes = torch.empty((C * k * k, max(ops.pad16(kk), 16)), dtype=torch.int8, device=x_nhwc.device)
+        scale = torch.empty(1, dtype=torch.float32, device=x_nhwc.device)
+        ops.conv_acbp_pass(x_nhwc, k, stride, pad, bitmap, bits, 1, st, codes, scale)
+        return codes, kk, scale
+
     def quant_gy(self, gy3, axis, bitmap, bits_gx, bits_gw):
         """Both gy operands with global scales: (gx codes (T, pad16(O)), gx scale,
         gw codes (O, pad16(K)), K, gw scale)."""
@@ -132,7 +146,7 @@ class ExactDP:
 
 
 def enable_exact_dp(model: torch.nn.Module, group=None):
-    """Switch every HLQLinear under `model` to the exact data-parallel mode
+    """Switch every HLQLinear / HLQConv2d under `model` to the exact data-parallel mode
     and return the parameter names DDP must ignore (their gradients are
     all-reduced inside the layers):
 
@@ -140,11 +154,12 @@ def enable_exact_dp(model: torch.nn.Module, group=None):
         DistributedDataParallel._set_params_and_buffers_to_ignore_for_model(model, names)
         model = DistributedDataParallel(model, ...)
     """
+    from .conv import HLQConv2d
     from .layers import HLQLinear
     dp = ExactDP(group)
     names = []
     for name, m in model.named_modules():
-        if isinstance(m, HLQLinear):
+        if isinstance(m, (HLQLinear, HLQConv2d)):
             m.dp = dp
             names.append(f"{name}.weight" if name else "weight")
     return names

@@ -542,6 +542,17 @@ def conv_acbp(x_nhwc: torch.Tensor, k: int, stride: int, pad: int, bitmap: int, 
     return codes, kk, scale, stats[2:3]
 
 
+def conv_acbp_pass(x_nhwc: torch.Tensor, k: int, stride: int, pad: int, bitmap: int, bits: int, mode: int,
+                   stats: torch.Tensor, codes: torch.Tensor | None = None, scale: torch.Tensor | None = None):
+    """One pass of the conv ACBP (hlq_conv_acbp_pass): mode 0 accumulates the
+    statistics into stats[2:4], mode 1 writes the codes with the scale they imply."""
+    x_nhwc = _cuda(x_nhwc, "x")
+    B, H, W, C = x_nhwc.shape
+    _lib.call("hlq_conv_acbp_pass", _p(x_nhwc), dtype_code(x_nhwc), B, H, W, C, k, stride, pad, bitmap, bits, mode,
+              _p(stats), _p(codes), 0 if codes is None else codes.stride(0), _p(scale), _stream())
+    LAUNCHES[0] += 1
+
+
 def conv_dgrad_i8(gcodes: torch.Tensor, B: int, Ho: int, Wo: int, O: int, wcodes: torch.Tensor, C: int,
                   k: int, pad: int, bits: int, sg: torch.Tensor, sw: torch.Tensor, exact: bool = False,
                   out_dtype=torch.bfloat16, want_acc: bool = False, stride: int = 1, H: int | None = None,
@@ -599,7 +610,8 @@ def require_dims(cond: bool, msg: str):
 
 for _name in ("quant_ht_cols", "quant_dual", "transform_pass", "quant_proj_rows", "quant_weights",
               "quant_stochastic", "basis_energy", "xform_quantize", "xform_project", "xform_unproject",
-              "proj_rows_amax", "proj_rows_quant", "gemm_i8", "gemm_i8_pair", "conv_acbp", "conv_dgrad_i8",
+              "proj_rows_amax", "proj_rows_quant", "gemm_i8", "gemm_i8_pair", "conv_acbp", "conv_acbp_pass",
+              "conv_dgrad_i8",
               "col2im"):
     globals()[_name] = on_device(globals()[_name])
 del _name

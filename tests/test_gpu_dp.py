@@ -148,3 +148,71 @@ def test_exact_dp_training_steps_world2():
         p.join(timeout=60)
     for r in res:
         assert r[0] == "ok", r
+
+
+def _conv_exact_worker(rank, world, port, q):
+    try:
+        import sys
+        import torch.distributed as dist
+        sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+        os.environ["MASTER_ADDR"] = "127.0.0.1"
+        os.environ["MASTER_PORT"] = str(port)
+        torch.cuda.set_device(0)
+        from paper_2406_15102_b200.conv import HLQConv2d
+        from paper_2406_15102_b200.dp import enable_exact_dp
+        bad = []
+        cases = [(3, 16, 3, 1, 1), (16, 32, 3, 2, 1), (32, 64, 3, 1, 1), (16, 16, 1, 2, 0)]
+        results = {}
+        for ci, (C, O, k, s, p) in enumerate(cases):
+            g = torch.Generator(device="cuda").manual_seed(100 + ci)
+            X = torch.randn(32, C, 16, 16, device="cuda", generator=g).to(memory_format=torch.channels_last)
+            Ho = (16 + 2 * p - k) // s + 1
+            G = (torch.randn(32, O, Ho, Ho, device="cuda", generator=g) * 1e-3).to(memory_format=torch.channels_last)
+            torch.manual_seed(7)
+            m = HLQConv2d(C, O, k, stride=s, padding=p, bias=False).cuda()
+            x = X.clone().requires_grad_(True)
+            m(x).backward(G)
+            results[ci] = (m.weight.grad.clone(), x.grad.clone())
+        dist.init_process_group("gloo", rank=rank, world_size=world)
+        half = 32 // world
+        sl = slice(rank * half, (rank + 1) * half)
+        for ci, (C, O, k, s, p) in enumerate(cases):
+            g = torch.Generator(device="cuda").manual_seed(100 + ci)
+            X = torch.randn(32, C, 16, 16, device="cuda", generator=g).to(memory_format=torch.channels_last)
+            Ho = (16 + 2 * p - k) // s + 1
+            G = (torch.randn(32, O, Ho, Ho, device="cuda", generator=g) * 1e-3).to(memory_format=torch.channels_last)
+            torch.manual_seed(7)
+            m = torch.nn.Sequential(HLQConv2d(C, O, k, stride=s, padding=p, bias=False).cuda())
+            enable_exact_dp(m)
+            x = X[sl].contiguous(memory_format=torch.channels_last).requires_grad_(True)
+            # torch mean-loss semantics: a rank's dY is world x its slice of the global one
+            m(x).backward(G[sl] * world)
+            dw_ref, dx_ref = results[ci]
+            if not torch.equal(m[0].weight.grad, dw_ref):
+                bad.append(("dW", ci))
+            if not torch.equal(x.grad, dx_ref[sl] * world):
+                bad.append(("dX", ci))
+        q.put(("ok" if not bad else "mismatch", rank, bad))
+        dist.barrier()
+        dist.destroy_process_group()
+    except Exception:  # noqa: BLE001
+        import traceback
+        q.put(("err", rank, traceback.format_exc()[-1500:]))
+
+
+def test_exact_dp_conv_world2():
+    """HLQConv2d in the exact mode: two ranks x 16 images give the one-process
+    dW bit for bit (small-C, im2col-TMA, strided and 1x1 convs), dX rows exact."""
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_conv_exact_worker, args=(r, 2, port, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    res = [q.get(timeout=600) for _ in range(2)]
+    for p in procs:
+        p.join(timeout=60)
+    for r in res:
+        assert r[0] == "ok", r
