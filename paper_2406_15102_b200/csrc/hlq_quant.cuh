@@ -138,6 +138,11 @@ struct Stat {
         "min.f32 %0, %0, t0, t1;}" : "+f"(mnz) : "f"(dec(a)), "f"(dec(b)));
   }
   __device__ __forceinline__ void add(float a) { add2(a, 0.0f); }
+  // amax only (the bound-test STATS pass takes min nonzero from the inputs)
+  __device__ __forceinline__ void amax2(float a, float b) {
+    asm("{.reg .f32 t0, t1;\n\tabs.f32 t0, %1;\n\tabs.f32 t1, %2;\n\t"
+        "max.NaN.f32 %0, %0, t0, t1;}" : "+f"(amax) : "f"(a), "f"(b));
+  }
   __device__ __forceinline__ void warp_reduce() {
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) {
@@ -159,6 +164,70 @@ struct Stat {
     if (mb < 0x7F800000u) asm volatile("red.relaxed.gpu.global.max.u32 [%0], %1;" ::"l"(g + 1), "r"(~mb) : "memory");
   }
 };
+
+// ------------------------------------------------------------------ bound statistics (bf16 sources)
+// The STATS pass needs max |w| over the transformed values exactly, but a block
+// can only raise the running maximum if its L1 norm can reach it: every
+// butterfly output satisfies |RN(a +- b)| <= RN(|a| + |b|) (RN is monotone),
+// so by induction each computed output of a block is <= the fp32 pairwise
+// tree sum of the block's |x|, which is <= L1 * (1 + 2^-24)^4.  The test sums
+// the |x| words as bf16x2 (4 tree levels, each RN step loses at most a factor
+// (1 - 2^-8)): a block whose bf16 sum is <= RD(0.96875 * m) for an exact
+// running maximum m of other blocks has every output < m and is skipped; the
+// others run the exact fp32 butterflies.  NaN / Inf sums never pass the test.
+//
+// Min nonzero guard of the fast division (make_quant), from the INPUTS: every
+// bf16 value is a multiple of g = 2^(E_min - 7) (E_min the exponent of the
+// smallest nonzero |x|, -126 for subnormals), so is every fp32 butterfly
+// output (an inexact RN result is a multiple of its ulp, itself >= g), hence
+// a nonzero |w| >= g >= min|x| * 2^-8.  The minimum runs on s16x2 lanes of
+// (|x| bits + 0x7FFF): 0 maps to 0x7FFF (the s16 maximum, never selected
+// while a nonzero lane exists), |x| bits a >= 1 to -32769 + a (monotone).
+__device__ __forceinline__ uint32_t bf2_add(uint32_t a, uint32_t b) {
+  uint32_t d;
+  asm("add.rn.bf16x2 %0, %1, %2;" : "=r"(d) : "r"(a), "r"(b));
+  return d;
+}
+__device__ __forceinline__ uint32_t s16x2_min3(uint32_t a, uint32_t b, uint32_t c) {
+  uint32_t d;
+  asm("min.s16x2 %0, %1, %2;" : "=r"(d) : "r"(a), "r"(b));  // ptxas fuses the pair into VIMNMX3
+  asm("min.s16x2 %0, %0, %1;" : "+r"(d) : "r"(c));
+  return d;
+}
+constexpr uint32_t kAbs2 = 0x7FFF7FFFu;
+// Pairwise bf16x2 tree over n |x| words (n = 8 or 16, 3 / 4 levels).
+template <int N>
+__device__ __forceinline__ uint32_t bf2_tree(const uint32_t (&a)[N]) {
+  uint32_t t[N / 2];
+#pragma unroll
+  for (int i = 0; i < N / 2; ++i) t[i] = bf2_add(a[2 * i], a[2 * i + 1]);
+#pragma unroll
+  for (int h = N / 4; h >= 1; h >>= 1)
+#pragma unroll
+    for (int i = 0; i < h; ++i) t[i] = bf2_add(t[2 * i], t[2 * i + 1]);
+  return t[0];
+}
+// skip threshold from an exact running maximum (0: only all-zero blocks skip;
+// tiny maxima never skip, so subnormal bf16 sums stay inside the margin)
+__device__ __forceinline__ float bound_thr(float m) {
+  return m >= 0x1p-100f ? __fmul_rd(m, 0.96875f) : 0.0f;
+}
+// the two bf16 lanes as fp32 and their NaN-propagating max
+__device__ __forceinline__ float bf2_lane_max(uint32_t s) {
+  float r;
+  asm("max.NaN.f32 %0, %1, %2;" : "=f"(r) : "f"(__uint_as_float(s << 16)), "f"(__uint_as_float(s & 0xFFFF0000u)));
+  return r;
+}
+// running s16x2 minimum -> the Stat::mnz encoding (bits - 1 of the lower bound
+// min|x| * 2^-8 of every nonzero transformed |w|); +inf when no nonzero input
+__device__ __forceinline__ float mz_to_mnz(uint32_t mz) {
+  const int lo = int(int16_t(mz & 0xFFFFu)), hi = int(int16_t(mz >> 16));
+  const int v = lo < hi ? lo : hi;
+  if (v == 0x7FFF) return __builtin_huge_valf();
+  const uint32_t a = uint32_t(v + 32769);                 // |x| bf16 bits of the smallest nonzero input
+  const float lb = __fmul_rn(__uint_as_float(a << 16), 0x1p-8f);  // exact (8 significant bits)
+  return __uint_as_float(__float_as_uint(lb) - 1u);
+}
 
 // ------------------------------------------------------------------ quantizer
 struct Quant {

@@ -110,6 +110,9 @@ struct Args {
   // sub-tiles; items count `vblocks` = ceil(total_blocks / tq) block groups
   int vblocks;
   int cbw;  // columns of the gw staging buffer (cch when row-grouped, else 256)
+  int poll_ns;    // grid-barrier polling back-off (HLQ_TR_POLL_NS, development)
+  int dev_flags;  // development A/B (HLQ_TR_FLAGS): 1 = no ticket prefetch, 2 = no grid maxima exchange,
+                 // 4 = bias column sums in the QUANT pass (+ a second grid barrier) instead of the STATS pass
   // column sums of the source (the bias gradient), fused into the STATS pass of
   // kBoth: cs_part[g][c] = sum of column c over row group g (one work item's
   // rows), then a fixed-order reduction over g after pass 2 -> cs_out[c]
@@ -133,12 +136,17 @@ constexpr int kMetaWords = 6;  // per ring slot: col0, s, blk, gb0, nbl | bl << 
 
 struct StepIter {
   int ord, item, bl, nbl, gb0, col0, s, blk, tap, grp, ntq;
-  bool rev;
+  int nxt;  // dynamic: the ticket already taken for the next item (fetched one item ahead,
+            // so the producer never waits on the atomic's round trip between items)
+  bool rev, pf;
   uint32_t* ctr;  // non-null: dynamic tickets
   __device__ __forceinline__ void begin(const Args& a, bool reverse, uint32_t* ticket_ctr = nullptr) {
     rev = reverse;
     ctr = ticket_ctr;
     ord = int(blockIdx.x);  // first item static (a greedy first grab let early CTAs queue two)
+    // prefetching pays with many items per CTA; with ~2 it lengthens the tail
+    pf = ctr && a.items >= 4 * int(gridDim.x) && !(a.dev_flags & 1);
+    if (pf && ord < a.items) nxt = int(gridDim.x + atomicAdd(ctr, 1u));
     start(a);
   }
   __device__ __forceinline__ void setup(const Args& a, int i) {
@@ -179,7 +187,14 @@ struct StepIter {
   }
   __device__ __forceinline__ void next(const Args& a) {
     if (++bl == nbl) {
-      ord = ctr ? int(gridDim.x + atomicAdd(ctr, 1u)) : ord + int(gridDim.x);
+      if (pf) {
+        ord = nxt;
+        if (ord < a.items) nxt = int(gridDim.x + atomicAdd(ctr, 1u));
+      } else if (ctr) {
+        ord = int(gridDim.x + atomicAdd(ctr, 1u));
+      } else {
+        ord += int(gridDim.x);
+      }
       start(a);
     } else if (++blk == a.nblk) {
       blk = 0;
@@ -188,6 +203,24 @@ struct StepIter {
   }
 };
 
+// bf16 row pieces: the 8 words (2 columns each) of rows A and B
+__device__ __forceinline__ void load16x2_bf16(uint32_t pa, uint32_t pb, uint32_t (&wa)[8], uint32_t (&wb)[8]) {
+  const uint4 ta[2] = {ptx::lds128(pa), ptx::lds128(pa + 16)};
+  const uint4 tb[2] = {ptx::lds128(pb), ptx::lds128(pb + 16)};
+#pragma unroll
+  for (int q = 0; q < 2; ++q) {
+    wa[4 * q] = ta[q].x; wa[4 * q + 1] = ta[q].y; wa[4 * q + 2] = ta[q].z; wa[4 * q + 3] = ta[q].w;
+    wb[4 * q] = tb[q].x; wb[4 * q + 1] = tb[q].y; wb[4 * q + 2] = tb[q].z; wb[4 * q + 3] = tb[q].w;
+  }
+}
+__device__ __forceinline__ void unpack16x2_bf16(const uint32_t (&wa)[8], const uint32_t (&wb)[8], float2 (&p)[16]) {
+#pragma unroll
+  for (int k = 0; k < 8; ++k) {
+    p[2 * k] = make_float2(bf_lo(wa[k]), bf_lo(wb[k]));
+    p[2 * k + 1] = make_float2(bf_hi(wa[k]), bf_hi(wb[k]));
+  }
+}
+
 // Two 16-element row pieces (rows r and r+8 of the staged tile, same column
 // block) as 16 f32x2 lanes: p[i] = (A[i], B[i]).  All four butterfly stages
 // then run on packed pairs.
@@ -195,18 +228,9 @@ template <typename T>
 __device__ __forceinline__ void read16x2(uint32_t pa, uint32_t pb, float2 (&p)[16], uint32_t flip) {
   if (sizeof(T) == 2) {
     (void)flip;  // swapping the halves per thread costs more SELs than the 2-way conflict
-    const uint4 ta[2] = {ptx::lds128(pa), ptx::lds128(pa + 16)};
-    const uint4 tb[2] = {ptx::lds128(pb), ptx::lds128(pb + 16)};
-#pragma unroll
-    for (int q = 0; q < 2; ++q) {
-      const uint32_t wa[4] = {ta[q].x, ta[q].y, ta[q].z, ta[q].w};
-      const uint32_t wb[4] = {tb[q].x, tb[q].y, tb[q].z, tb[q].w};
-#pragma unroll
-      for (int k = 0; k < 4; ++k) {
-        p[8 * q + 2 * k] = make_float2(bf_lo(wa[k]), bf_lo(wb[k]));
-        p[8 * q + 2 * k + 1] = make_float2(bf_hi(wa[k]), bf_hi(wb[k]));
-      }
-    }
+    uint32_t wa[8], wb[8];
+    load16x2_bf16(pa, pb, wa, wb);
+    unpack16x2_bf16(wa, wb, p);
   } else {
 #pragma unroll
     for (int q = 0; q < 4; ++q) {
@@ -223,7 +247,7 @@ template <typename T, int MODE, bool GX, bool GW, int BM, bool FX, bool FW, bool
 __device__ __forceinline__ void consume(const Args& a, const Quant& qx, const Quant& qw,
                                         uint8_t* tiles, uint64_t* full, uint64_t* empty,
                                         const volatile int* meta, uint8_t* cbuf, Stat& sx, Stat& sw,
-                                        int& slot, uint32_t& phase, bool reverse) {
+                                        int& slot, uint32_t& phase, bool reverse, uint32_t* shmax = nullptr) {
   constexpr int kRow = Tr<T>::kRow;
   const uint32_t bitmap = BM ? uint32_t(BM) : a.bitmap;
   const int rank = BM ? __builtin_popcount(uint32_t(BM)) : a.rank;
@@ -235,6 +259,18 @@ __device__ __forceinline__ void consume(const Args& a, const Quant& qx, const Qu
   StepIter it;
   if (!DYN) it.begin(a, reverse);
   float2 csum = make_float2(0.0f, 0.0f);
+  // bf16 STATS pass: L1-bound block skipping + min nonzero from the inputs
+  // (hlq_quant.cuh, "bound statistics"); fp32 sources keep the exact pass
+#ifdef HLQ_TR_EXACT_STATS
+  constexpr bool kBound = false;
+#else
+  constexpr bool kBound = MODE == kStats && sizeof(T) == 2;
+#endif
+  // the bias column sums run in the STATS pass (partials ready at the grid
+  // barrier) unless dev flag 4 moves them to the QUANT pass
+  const bool cs_here = a.cs_part && (MODE == ((a.dev_flags & 4) ? kQuant : kStats));
+  uint32_t mz = 0x7FFF7FFFu;      // running s16x2 min of |x| bits + 0x7FFF
+  float thr_x = 0.0f, thr_w = 0.0f;  // skip thresholds from the running exact maxima
   while (DYN || it.valid(a)) {
     {
       ptx::mbar_wait(&full[slot], phase);
@@ -250,6 +286,10 @@ __device__ __forceinline__ void consume(const Args& a, const Quant& qx, const Qu
       }
       const uint32_t tile = ptx::smem_u32(tiles) + slot * (16 * kRow);
       constexpr bool rg = GRP == 2;  // row-grouped narrow source (GRP 1: conv tap groups)
+      // running maxima shared by the CTA's warps and, through the producer
+      // (once per work item), with the grid (hlq_quant.cuh bound statistics)
+      uint2 gmax = make_uint2(0u, 0u);
+      if (kBound) gmax = ptx::lds64(ptx::smem_u32(shmax));
       if (rg && !DYN) {  // static schedule: the first real block of this step (dynamic: published)
         const int rb = (it.gb0 + it.bl) * a.tq;
         it.s = rb / a.nblk;
@@ -277,6 +317,41 @@ __device__ __forceinline__ void consume(const Args& a, const Quant& qx, const Qu
           prv = a.rows - pb * 16;
         }
         const int c = it.col0 + bb * 16;
+        if (kBound) {
+          uint32_t wa[8], wb[8];
+          if (ok) {
+            load16x2_bf16(base + r * pitch + bb * 16 * sizeof(T), base + (r + 8) * pitch + bb * 16 * sizeof(T), wa,
+                          wb);
+          } else {
+#pragma unroll
+            for (int k = 0; k < 8; ++k) wa[k] = wb[k] = 0u;
+          }
+          uint32_t aa[8], ab[8];
+#pragma unroll
+          for (int k = 0; k < 8; ++k) {
+            aa[k] = wa[k] & kAbs2;
+            ab[k] = wb[k] & kAbs2;
+            mz = s16x2_min3(mz, aa[k] + kAbs2, ab[k] + kAbs2);
+          }
+          const uint32_t sA = bf2_tree<8>(aa), sB = bf2_tree<8>(ab);
+          const uint32_t l1 = bf2_add(__byte_perm(sA, sB, 0x5410), __byte_perm(sA, sB, 0x7632));  // (L1 A, L1 B)
+          const bool need = !(bf2_lane_max(l1) <= thr_x);
+          if (need) {
+            float2 p[16];
+            unpack16x2_bf16(wa, wb, p);
+            fwht16_pair(p);
+#pragma unroll
+            for (int i = 0; i < 16; ++i) sx.amax2(p[i].x, p[i].y);
+          }
+          // share the best maximum across the warp and the grid (any exact block
+          // maximum bounds the result; NaN bits 0x7FFFFFFF win the max and stop skipping)
+          if (__any_sync(0xffffffffu, need)) {
+            const uint32_t wm = __reduce_max_sync(0xffffffffu, __float_as_uint(sx.amax) & 0x7FFFFFFFu);
+            if (lane == 0 && wm > gmax.x) atomicMax(shmax, wm);
+            thr_x = fmaxf(thr_x, bound_thr(__uint_as_float(wm)));
+          }
+          thr_x = fmaxf(thr_x, bound_thr(__uint_as_float(gmax.x)));
+        } else {
         float2 p[16];
         if (ok)
           read16x2<T>(base + r * pitch + bb * 16 * sizeof(T), base + (r + 8) * pitch + bb * 16 * sizeof(T), p,
@@ -329,6 +404,7 @@ __device__ __forceinline__ void consume(const Args& a, const Quant& qx, const Qu
                   make_uint4(cb[0], cb[1], cb[2], cb[3]);
           }
         }
+        }  // !kBound
       }
       // ---------------- phase 2: column pair -> gw operand (projection along rows)
       if (GW && p2) {
@@ -341,7 +417,54 @@ __device__ __forceinline__ void consume(const Args& a, const Quant& qx, const Qu
         const uint32_t col_addr = tile + (GRP ? q * 16 * pitch + uint32_t(cc) * sizeof(T)
                                                    : uint32_t(c) * sizeof(T));
         const bool in = GRP == 0 ? it.col0 + c < a.cols : (rg ? rb0 + q < a.total_blocks : q < it.ntq);
-        if (in) {
+        bool need_w = false;
+        if (kBound && in) {
+          uint32_t w[16], av[16];
+#pragma unroll
+          for (int i = 0; i < 16; ++i) {
+            w[i] = ptx::lds32(col_addr + i * pitch);
+            av[i] = w[i] & kAbs2;
+          }
+          if (!GX) {  // no phase 1 to take the input minimum
+#pragma unroll
+            for (int i = 0; i < 8; ++i) mz = s16x2_min3(mz, av[2 * i] + kAbs2, av[2 * i + 1] + kAbs2);
+          }
+          // (conv rows past the image, zeroed below, only loosen the bound)
+          need_w = !(bf2_lane_max(bf2_tree<16>(av)) <= thr_w);
+          if (cs_here) {
+            // bias column sums: the pairwise tree in the butterfly's DC order (stages
+            // h = 1, 2, 4, 8), accumulated over the item's blocks
+            float2 t[8];
+#pragma unroll
+            for (int i = 0; i < 8; ++i)
+              t[i] = f2add(make_float2(bf_lo(w[2 * i]), bf_hi(w[2 * i])),
+                           make_float2(bf_lo(w[2 * i + 1]), bf_hi(w[2 * i + 1])));
+#pragma unroll
+            for (int i = 0; i < 4; ++i) t[i] = f2add(t[2 * i], t[2 * i + 1]);
+            const float2 blk_sum = f2add(f2add(t[0], t[1]), f2add(t[2], t[3]));
+            csum = it.bl == 0 ? blk_sum : f2add(csum, blk_sum);
+            if (it.bl == it.nbl - 1) {
+              const int oc = rg ? cc : it.col0 + c;
+              float* o = a.cs_part + int64_t(oc) * a.groups + (rg ? it.grp * a.tq + q : it.grp);
+              o[0] = csum.x;
+              if (oc + 1 < a.cols) o[a.groups] = csum.y;
+            }
+          }
+          if (need_w) {
+            float2 pv[16];
+#pragma unroll
+            for (int i = 0; i < 16; ++i) pv[i] = make_float2(bf_lo(w[i]), bf_hi(w[i]));
+            if (a.taps && rvalid < 16) {
+#pragma unroll
+              for (int i = 0; i < 16; ++i)
+                if (i >= rvalid) pv[i] = make_float2(0.0f, 0.0f);
+            }
+            fwht16_pair(pv);
+#pragma unroll
+            for (int i = 0; i < 16; ++i)
+              if ((bitmap >> i) & 1u) sw.amax2(pv[i].x, pv[i].y);
+          }
+        } else if (in) {
           float2 pv[16];
 #pragma unroll
           for (int i = 0; i < 16; ++i) {
@@ -366,7 +489,7 @@ __device__ __forceinline__ void consume(const Args& a, const Quant& qx, const Qu
           // when basis 0 is kept the sum comes for free from pv[0]; otherwise the tree
           const bool dc_kept = (bitmap & 1u) != 0;
           float2 blk_sum = make_float2(0.0f, 0.0f);
-          if (MODE == kStats && a.cs_part && !dc_kept) {
+          if (cs_here && !dc_kept) {
             float2 t[8];
 #pragma unroll
             for (int i = 0; i < 8; ++i) t[i] = f2add(pv[2 * i], pv[2 * i + 1]);
@@ -375,7 +498,9 @@ __device__ __forceinline__ void consume(const Args& a, const Quant& qx, const Qu
             blk_sum = f2add(f2add(t[0], t[1]), f2add(t[2], t[3]));
           }
           fwht16_pair(pv);
-          if (MODE == kStats && a.cs_part) {
+          // (kQuant: the fused kernel's second pass; its partials are reduced
+          // after a second grid barrier)
+          if (cs_here) {
             if (dc_kept) blk_sum = pv[0];
             csum = it.bl == 0 ? blk_sum : f2add(csum, blk_sum);
             if (it.bl == it.nbl - 1) {
@@ -447,7 +572,7 @@ __device__ __forceinline__ void consume(const Args& a, const Quant& qx, const Qu
               }
             }
           }
-        } else if (MODE == kStats && rg && a.cs_part) {
+        } else if (cs_here && rg) {
           // a sub-tile past the last real block: its column sums still need the
           // item's partial written (zero when the item had no other step)
           if (it.bl == 0) csum = make_float2(0.0f, 0.0f);
@@ -456,6 +581,14 @@ __device__ __forceinline__ void consume(const Args& a, const Quant& qx, const Qu
             o[0] = csum.x;
             if (cc + 1 < a.cols) o[a.groups] = csum.y;
           }
+        }
+        if (kBound) {
+          if (__any_sync(0xffffffffu, need_w)) {
+            const uint32_t wm = __reduce_max_sync(0xffffffffu, __float_as_uint(sw.amax) & 0x7FFFFFFFu);
+            if (lane == 0 && wm > gmax.y) atomicMax(shmax + 1, wm);
+            thr_w = fmaxf(thr_w, bound_thr(__uint_as_float(wm)));
+          }
+          thr_w = fmaxf(thr_w, bound_thr(__uint_as_float(gmax.y)));
         }
       }
       // release the slot to the producer (one arrive per consuming warp)
@@ -503,6 +636,11 @@ __device__ __forceinline__ void consume(const Args& a, const Quant& qx, const Qu
     }
     if (!DYN) it.next(a);
   }
+  if (kBound) {  // both operands are transforms of the same inputs: one lower bound
+    const float mnz = mz_to_mnz(mz);
+    sx.mnz = mnz;
+    sw.mnz = mnz;
+  }
 }
 
 // Quant-pass dispatch on the (grid-uniform) fast-division guard of each operand.
@@ -535,6 +673,25 @@ __device__ __forceinline__ void consume_quant(const Args& a, uint8_t* tiles, uin
                                                    reverse);
 }
 
+// Grid-wide barrier among the consumer warps of co-resident CTAs (cooperative
+// launch): thread 0 publishes this CTA's arrival with a release reduction (no
+// returned value to wait for), after the CTA's prior writes were collected by
+// the named barrier, and polls with acquire loads until `target` arrivals.
+__device__ __forceinline__ void grid_barrier(uint32_t* ctr, uint32_t target, int poll_ns) {
+  if (threadIdx.x == 0) {
+    uint32_t seen = 0;
+    asm volatile("red.release.gpu.global.add.u32 [%0], 1;" ::"l"(ctr) : "memory");
+    asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(seen) : "l"(ctr) : "memory");
+    while (seen < target) {
+      // every CTA polls the same L2 line: back off so the arrivals and the
+      // statistics reductions queued on that slice are not delayed
+      __nanosleep(poll_ns);
+      asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(seen) : "l"(ctr) : "memory");
+    }
+  }
+  asm volatile("bar.sync 2, %0;" ::"n"(kConsumers) : "memory");
+}
+
 // MODE kStats / kQuant: one pass.  MODE kBoth: both passes in one cooperative
 // launch -- statistics, a grid-wide barrier (a counter in stats[32]), then the
 // quantization pass over the items in reverse order.  The producer warp never
@@ -554,6 +711,8 @@ __global__ void __launch_bounds__(kThreads, HLQ_TR_MINB) tma_tile_kernel(const _
   uint64_t* full = reinterpret_cast<uint64_t*>(bars);
   uint64_t* empty = full + kStages;
   int* meta = reinterpret_cast<int*>(empty + kStages);  // dynamic mode: kMetaWords per slot
+  uint32_t* shmax = reinterpret_cast<uint32_t*>(meta + kStages * kMetaWords);  // bound stats: CTA maxima (x, w)
+  constexpr bool kBoundK = (MODE == kStats || MODE == kBoth) && sizeof(T) == 2;
 #ifdef HLQ_TR_STATIC
   constexpr bool kDyn = false;  // A/B builds
 #else
@@ -578,6 +737,7 @@ __global__ void __launch_bounds__(kThreads, HLQ_TR_MINB) tma_tile_kernel(const _
       ptx::mbar_init(&full[s], 1);
       ptx::mbar_init(&empty[s], kConsumers / 32);
     }
+    shmax[0] = shmax[1] = 0u;
     ptx::fence_mbar_init();
   }
   __syncthreads();
@@ -591,7 +751,20 @@ __global__ void __launch_bounds__(kThreads, HLQ_TR_MINB) tma_tile_kernel(const _
       for (int pass = 0; pass < (MODE == kBoth ? 2 : 1); ++pass) {
         StepIter it;
         it.begin(a, pass == 1, kDyn ? a.stats + 64 + 32 * pass : nullptr);
+        uint4 gpend = make_uint4(0u, 0u, 0u, 0u);  // the grid maxima loaded at the previous item
         while (it.valid(a)) {
+          if (kBoundK && pass == 0 && it.bl == 0 && !(a.dev_flags & 2)) {
+            // fold the grid's maxima into the CTA's, publish the CTA's (one relaxed
+            // load and at most two reductions per item: no same-line hot spot)
+            const uint32_t cx = *reinterpret_cast<volatile uint32_t*>(shmax);
+            const uint32_t cw = *reinterpret_cast<volatile uint32_t*>(shmax + 1);
+            if (GX && cx > gpend.x) asm volatile("red.relaxed.gpu.global.max.u32 [%0], %1;" ::"l"(a.stats), "r"(cx) : "memory");
+            if (GW && cw > gpend.z) asm volatile("red.relaxed.gpu.global.max.u32 [%0], %1;" ::"l"(a.stats + 2), "r"(cw) : "memory");
+            if (gpend.x > cx) atomicMax(shmax, gpend.x);
+            if (gpend.z > cw) atomicMax(shmax + 1, gpend.z);
+            asm volatile("ld.relaxed.gpu.global.v4.u32 {%0, %1, %2, %3}, [%4];"
+                         : "=r"(gpend.x), "=r"(gpend.y), "=r"(gpend.z), "=r"(gpend.w) : "l"(a.stats));
+          }
           ptx::mbar_wait_sleep(&empty[slot], phase ^ 1);
           constexpr bool rgp = GRP == 2;
           if (rgp) {  // first real block of this step's group
@@ -648,7 +821,7 @@ __global__ void __launch_bounds__(kThreads, HLQ_TR_MINB) tma_tile_kernel(const _
   {
     Quant dummy{};
     consume<T, kStats, GX, GW, BM, true, true, kDyn, GRP>(a, dummy, dummy, tiles, full, empty, meta, cbuf, sx, sw,
-                                                     slot, phase, false);
+                                                     slot, phase, false, shmax);
   }
   stamp(1);
   sx.warp_reduce();
@@ -676,18 +849,7 @@ __global__ void __launch_bounds__(kThreads, HLQ_TR_MINB) tma_tile_kernel(const _
   }
   if (MODE == kStats) return;
   // ---------------- grid barrier (consumer threads only; all CTAs co-resident)
-  if (threadIdx.x == 0) {
-    // release-reduction (no returned value to wait for) orders this CTA's
-    // statistics; acquire loads poll until every CTA has arrived
-    uint32_t seen = 0;
-    asm volatile("red.release.gpu.global.add.u32 [%0], 1;" ::"l"(a.stats + 32) : "memory");
-    asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(seen) : "l"(a.stats + 32) : "memory");
-    while (seen < gridDim.x) {
-      __nanosleep(32);
-      asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(seen) : "l"(a.stats + 32) : "memory");
-    }
-  }
-  asm volatile("bar.sync 2, %0;" ::"n"(kConsumers) : "memory");
+  grid_barrier(a.stats + 32, gridDim.x, a.poll_ns);
   stamp(2);
   consume_quant<T, GX, GW, BM, kDyn, GRP>(a, tiles, full, empty, meta, cbuf, slot, phase, true);
   stamp(3);
@@ -696,6 +858,10 @@ __global__ void __launch_bounds__(kThreads, HLQ_TR_MINB) tma_tile_kernel(const _
     // row-group partials (coalesced, 16 loads in flight per lane), fixed
     // summation order and shuffle tree -> deterministic.  The partials were
     // written before the grid barrier (L2 loads).
+    if (a.dev_flags & 4) {  // partials written by the QUANT pass
+      asm volatile("bar.sync 2, %0;" ::"n"(kConsumers) : "memory");
+      grid_barrier(a.stats + 32, 2 * gridDim.x, a.poll_ns);
+    }
     const int lane = threadIdx.x & 31;
     for (int c = blockIdx.x * (kConsumers / 32) + (threadIdx.x >> 5); c < a.cols;
          c += gridDim.x * (kConsumers / 32)) {
@@ -723,7 +889,7 @@ template <typename T, int MODE, bool GX, bool GW, int BM, int GRP>
 void launch_one(const CUtensorMap& map, Args a, cudaStream_t stream) {
   constexpr int kRow = Tr<T>::kRow;
   const size_t smem = 128 + size_t(kStages) * 16 * kRow +
-                      (GW && MODE != kStats ? size_t(a.cbw) * a.cstride : 0) + 8 + 2 * kStages * 8 + kStages * kMetaWords * 4;
+                      (GW && MODE != kStats ? size_t(a.cbw) * a.cstride : 0) + 8 + 2 * kStages * 8 + kStages * kMetaWords * 4 + 8;
   auto kern = tma_tile_kernel<T, MODE, GX, GW, BM, GRP>;
   static std::atomic<unsigned long long> attr{0};  // per template instance and device
   smem_attr_once(reinterpret_cast<const void*>(kern), 200 * 1024, attr);
@@ -788,6 +954,16 @@ void launch_modes(const CUtensorMap& map, const Args& a, int mode, bool gx, bool
   if (mode == kStats) launch_ops<T, kStats>(map, a, gx, gw, st);
   else if (mode == kQuant) launch_ops<T, kQuant>(map, a, gx, gw, st);
   else launch_ops<T, kBoth>(map, a, gx, gw, st);
+}
+
+int tr_poll_ns() {
+  static const int f = env_knob("HLQ_TR_POLL_NS");
+  return f > 0 ? f : 128;
+}
+
+int tr_dev_flags() {
+  static const int f = env_knob("HLQ_TR_FLAGS");
+  return f > 0 ? f : 0;
 }
 
 // Blocks per work item: >= 32-byte output runs per column when the problem is
@@ -911,6 +1087,8 @@ bool launch_conv_acbp_tma(const void* x, int dtype, int B, int H, int W, int C, 
   a.scale_gw = scale;
   a.nonfinite = nonfinite_word();
   a.cstride = a.nb * a.rank + 16;
+  a.dev_flags = tr_dev_flags();
+  a.poll_ns = tr_poll_ns();
   if (dtype == kBF16)
     launch_modes<__nv_bfloat16>(map, a, mode, false, true, stream);
   else
@@ -978,6 +1156,8 @@ void launch_transform(const TransformArgs& t, int mode, cudaStream_t stream) {
   a.nonfinite = nonfinite_word();
   a.pack_gx = t.pack_gx ? 1 : 0;
   a.cstride = a.nb * a.tq * a.rank + 16;
+  a.dev_flags = tr_dev_flags();
+  a.poll_ns = tr_poll_ns();
 #ifdef HLQ_TR_TRACE
   a.trace = g_tr_trace;
 #endif

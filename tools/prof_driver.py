@@ -26,8 +26,16 @@ def main():
     xp, k, sx, _ = ops.quant_proj_rows(x, segs, rows, I, 0x5555, 8, I, L * I)
     cgx, sgx, cg, kg, sg, _ = ops.quant_dual(gy, segs, rows, O, 0x5555, 4, 8, O, L * O)
     cw, _, sw, _ = ops.quant_proj_rows(w, 1, O, I, 0xFFFF, 4)
+    st = ops.new_stats("cuda")
+    sc = torch.empty(2, device="cuda")
     for _ in range(reps):
-        if what == "dual":
+        if what == "statspass":  # the fused kernel's two passes launched alone (dev A/B)
+            st.zero_()
+            ops.transform_pass(gy, segs, rows, O, O, L * O, True, True, 0x5555, 4, 8, 0, st)
+        elif what == "quantpass":
+            ops.transform_pass(gy, segs, rows, O, O, L * O, True, True, 0x5555, 4, 8, 1, st, cgx, cg,
+                               sc[0:1], sc[1:2])
+        elif what == "dual":
             ops.quant_dual(gy, segs, rows, O, 0x5555, 4, 8, O, L * O)
         elif what == "dualcs":  # as the training path runs it: with the bias-gradient column sums
             ops.quant_dual(gy, segs, rows, O, 0x5555, 4, 8, O, L * O, colsum=True)

@@ -34,12 +34,18 @@ def dev_us(fn, flush, reps):
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--reps", type=int, default=20)
+    ap.add_argument("--dist", default="normal", choices=["normal", "lognormal"],
+                    help="gy distribution: N(0,1)*1e-3 or SURVEY 8(d)'s lognormal(0,1.4)*sign*1e-3")
     a = ap.parse_args()
     flush = torch.empty(64 * 1024 * 1024, device="cuda")
     B, L = 128, 197
     out = {}
     for O in (768, 2304, 3072):
-        gy = (torch.randn(B, L, O, device="cuda") * 1e-3).to(torch.bfloat16)
+        if a.dist == "normal":
+            gy = (torch.randn(B, L, O, device="cuda") * 1e-3).to(torch.bfloat16)
+        else:
+            z = torch.randn(B, L, O, device="cuda")
+            gy = (torch.exp(1.4 * torch.randn_like(z)) * torch.sign(z) * 1e-3).to(torch.bfloat16)
         out[f"dual_cs_{O}"] = round(dev_us(lambda: ops.quant_dual(gy, B, L, O, 0x5555, 4, 8, O, L * O, colsum=True),
                                            flush, a.reps), 1)
     for I in (768, 3072):
@@ -48,6 +54,7 @@ def main():
     ws = [torch.randn(o, i, device="cuda") * (2.0 / i) ** 0.5
           for o, i in [(2304, 768), (768, 768), (3072, 768), (768, 3072)] * 12 + [(1000, 768)]]
     out["wcodes_49"] = round(dev_us(lambda: ops.quant_weights(ws, 4, bf16=True), flush, a.reps), 1)
+    out["dist"] = a.dist
     print(json.dumps(out))
 
 

@@ -18,16 +18,21 @@ from tools.stage_bench import timeit  # noqa: E402
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--shape", default="128,197,768,3072")
+    ap.add_argument("--dist", default="normal", choices=["normal", "lognormal"])
     a = ap.parse_args()
     B, L, I, O = (int(v) for v in a.shape.split(","))
     flush = torch.empty(64 * 1024 * 1024, device="cuda")
-    gy = (torch.randn(B, L, O, device="cuda") * 1e-3).to(torch.bfloat16)
+    if a.dist == "normal":
+        gy = (torch.randn(B, L, O, device="cuda") * 1e-3).to(torch.bfloat16)
+    else:
+        z = torch.randn(B, L, O, device="cuda")
+        gy = (torch.exp(1.4 * torch.randn_like(z)) * torch.sign(z) * 1e-3).to(torch.bfloat16)
     k = ops.proj_rows_k(B, L, 8)
     cgx = torch.empty(B * L, ops.pad16(O), dtype=torch.int8, device="cuda")
     cgw = torch.empty(O, max(ops.pad16(k), 16), dtype=torch.int8, device="cuda")
     sc = torch.empty(2, device="cuda")
     st = ops.new_stats("cuda")
-    res = {"shape": [B, L, I, O]}
+    res = {"shape": [B, L, I, O], "dist": a.dist}
     res["dual_fused"] = timeit(lambda: ops.quant_dual(gy, B, L, O, 0x5555, 4, 8, O, L * O), flush=flush)
     res["dual_fused_noflush"] = timeit(lambda: ops.quant_dual(gy, B, L, O, 0x5555, 4, 8, O, L * O))
 
