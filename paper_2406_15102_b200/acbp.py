@@ -64,7 +64,9 @@ def acbp_unpack(buf: torch.Tensor) -> ACBPActivation:
     _lib.call("hlq_acbp_parse", ops._p(buf), n, ctypes.byref(info), ops._stream())
     dev = buf.device
     ld = max(ops.pad16(info.K), 16)
-    payload = torch.zeros((info.rows, ld), dtype=torch.int8, device=dev)
+    # int8: the unpack transpose writes every byte (padding columns zeroed); int4 leaves them
+    alloc = torch.empty if info.bits == 8 else torch.zeros
+    payload = alloc((info.rows, ld), dtype=torch.int8, device=dev)
     scale = torch.empty(1, dtype=torch.float32, device=dev)
     wsb = int(_lib.load().hlq_acbp_ws(n))
     ws = torch.empty(wsb, dtype=torch.uint8, device=dev)
