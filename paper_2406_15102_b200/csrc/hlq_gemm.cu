@@ -36,6 +36,10 @@ namespace {
 constexpr int kBM = 128;
 constexpr int kBK = 128;  // bytes of K per stage = one 128B swizzle row
 constexpr int kThreads = 256;
+// single-CTA int8-A kernel: two epilogue warps per TMEM lane quarter (warps 4-7
+// and 8-11) splitting each tile's columns -- one warp per SMSP could not keep up
+// with the MMAs (fc2 dX: the MMA warp waited on TMEM-empty, tensor pipe 54 %)
+constexpr int kThreadsE2 = 384;
 // Packed int4 A operand: + kConvWarps converter warps (8 .. 8 + kConvWarps - 1)
 constexpr int kConvWarps = 8;
 constexpr int kConvThreads = 32 * kConvWarps;
@@ -124,6 +128,37 @@ __device__ __forceinline__ void store_chunk_tma(const uint32_t (&acc)[32], float
 #pragma unroll
     for (int q = 0; q < 8; ++q)
       *reinterpret_cast<float4*>(rowp + 16 * (q ^ sw)) = make_float4(v[4 * q], v[4 * q + 1], v[4 * q + 2], v[4 * q + 3]);
+  }
+  ptx::fence_proxy_async_smem();
+  __syncwarp();
+  if (lane == 0) {
+    ptx::tma_store_2d(map_o, buf, col0, row0);
+    ptx::bulk_commit();
+  }
+}
+
+// bf16 fast epilogue of two adjacent 32 x 32 chunks as ONE 32 x 64 tile store:
+// 128-byte rows (SW128, conflict-free row-per-thread 16-byte writes).  The
+// 64-byte rows of single-chunk bf16 stores held the TMA store path to ~4 TB/s
+// (fc2 dX: the output write, not the tensor pipe, set the kernel time).
+__device__ __forceinline__ void store_pair_tma_bf16(const uint32_t (&a0)[32], const uint32_t (&a1)[32], float fscale,
+                                                    uint8_t* buf, uint32_t lane, const CUtensorMap* map_o,
+                                                    int32_t col0, int32_t row0) {
+  uint8_t* rowp = buf + lane * 128;
+  const uint32_t sw = lane & 7;
+#pragma unroll
+  for (int q = 0; q < 8; ++q) {
+    const uint32_t(&a)[32] = q < 4 ? a0 : a1;
+    const int j0 = 8 * (q & 3);
+    uint32_t w[4];
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      const float x = __fmul_rn(__int2float_rn(int(a[j0 + 2 * k])), fscale);
+      const float y = __fmul_rn(__int2float_rn(int(a[j0 + 2 * k + 1])), fscale);
+      __nv_bfloat162 t = __floats2bfloat162_rn(x, y);
+      w[k] = *reinterpret_cast<uint32_t*>(&t);
+    }
+    *reinterpret_cast<uint4*>(rowp + 16 * (q ^ sw)) = make_uint4(w[0], w[1], w[2], w[3]);
   }
   ptx::fence_proxy_async_smem();
   __syncwarp();
@@ -227,7 +262,7 @@ struct ConvGeo {
 };
 
 template <int BN, int STAGES, bool A4>
-__global__ void __launch_bounds__(A4 ? kThreadsA4 : kThreads, 1)
+__global__ void __launch_bounds__(A4 ? kThreadsA4 : kThreadsE2, 1)
     gemm_i8_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant__ CUtensorMap map_b,
                    const __grid_constant__ CUtensorMap map_o, int tma_out,
                    int M, int N, int K, int groups, const float* __restrict__ sa, const float* __restrict__ sb,
@@ -263,7 +298,7 @@ __global__ void __launch_bounds__(A4 ? kThreadsA4 : kThreads, 1)
     }
     for (int a = 0; a < 2; ++a) {
       ptx::mbar_init(&tfull[a], 1);
-      ptx::mbar_init(&tempty[a], 128);
+      ptx::mbar_init(&tempty[a], A4 ? 128 : 256);
     }
     ptx::fence_mbar_init();
   }
@@ -371,8 +406,10 @@ __global__ void __launch_bounds__(A4 ? kThreadsA4 : kThreads, 1)
         if (++stage == STAGES) { stage = 0; phase ^= 1; }
       }
     }
-  } else if (warp >= 4 && warp < 8) {
+  } else if ((warp >= 4 && warp < 8) || (!A4 && warp >= 8 && warp < 12)) {
     const uint32_t quarter = warp & 3;  // TMEM lanes [32*quarter, 32*quarter+32)
+    constexpr int kGroups = A4 ? 1 : 2;  // epilogue warps per quarter: chunk c belongs to group c % kGroups
+    const int grp = warp >= 8 ? 1 : 0;
     const float comb = __fmul_rn(*sa, *sb);
     const double dscale = __dmul_rn(double(comb), extra);
     const float fscale = float(dscale);
@@ -387,24 +424,47 @@ __global__ void __launch_bounds__(A4 ? kThreadsA4 : kThreads, 1)
       const int rl = quarter * 32 + lane;  // row inside the tile
       const int64_t row = int64_t(mb) * kBM + rl;
       if (splits == 1 && tma_out) {
-        uint8_t* wbuf = stg + quarter * kStgBytes;
+        // staging: A4 -- 2 buffers of 4 KB per warp (warps 4-7); otherwise one 4 KB
+        // buffer per warp (warps 4-11), the other warp of the quarter hides the wait
+        uint8_t* wbuf = A4 ? stg + quarter * kStgBytes : stg + (quarter + 4 * grp) * (kStgBytes / 2);
         const int32_t row0 = mb * kBM + int32_t(quarter) * 32;
+        if (out_dtype == kBF16) {
 #pragma unroll 1
-        for (int c = 0; c < BN / 32; ++c) {
+          for (int c = 2 * grp; c < BN / 32; c += 2 * kGroups) {  // 32 x 64 tiles (128-byte rows)
+            const int32_t col0 = nb * BN + c * 32;
+            uint32_t r0[32], r1[32];
+            ptx::tmem_ld_32x32b_x32(tmem_base + ((quarter * 32) << 16) + uint32_t(acc * BN + c * 32), r0);
+            ptx::tmem_ld_32x32b_x32(tmem_base + ((quarter * 32) << 16) + uint32_t(acc * BN + c * 32 + 32), r1);
+            ptx::tmem_ld_wait();
+            if (lane == 0) {  // the store that last used this buffer has read it
+              if (A4) ptx::bulk_wait_read<1>(); else ptx::bulk_wait_read<0>();
+            }
+            __syncwarp();
+            if (row0 < M && col0 < N)
+              store_pair_tma_bf16(r0, r1, fscale, A4 ? wbuf + ((c >> 1) & 1) * (kStgBytes / 2) : wbuf, lane, &map_o,
+                                  col0, row0);
+          }
+        } else {
+#pragma unroll 1
+        for (int c = grp; c < BN / 32; c += kGroups) {
           const int32_t col0 = nb * BN + c * 32;
           uint32_t r[32];
           ptx::tmem_ld_32x32b_x32(tmem_base + ((quarter * 32) << 16) + uint32_t(acc * BN + c * 32), r);
           ptx::tmem_ld_wait();
-          if (lane == 0) ptx::bulk_wait_read<1>();  // the store that used this buffer 2 chunks ago
+          if (lane == 0) {
+            if (A4) ptx::bulk_wait_read<1>(); else ptx::bulk_wait_read<0>();
+          }
           __syncwarp();
           if (row0 < M && col0 < N)
-            store_chunk_tma(r, fscale, out_dtype, wbuf + (c & 1) * (kStgBytes / 2), lane, &map_o, col0, row0);
+            store_chunk_tma(r, fscale, out_dtype, A4 ? wbuf + (c & 1) * (kStgBytes / 2) : wbuf, lane, &map_o, col0,
+                            row0);
+        }
         }
         ptx::tc_fence_before();
         ptx::mbar_arrive(&tempty[acc]);
       } else if (splits == 1) {
 #pragma unroll 1
-        for (int c = 0; c < BN / 32; ++c) {
+        for (int c = grp; c < BN / 32; c += kGroups) {
           const int64_t col0 = int64_t(nb) * BN + c * 32;
           uint32_t r[32];
           ptx::tmem_ld_32x32b_x32(tmem_base + ((quarter * 32) << 16) + uint32_t(acc * BN + c * 32), r);
@@ -426,7 +486,7 @@ __global__ void __launch_bounds__(A4 ? kThreadsA4 : kThreads, 1)
         // partial tile -> slab sp (row-major M x N int32); summed by splitk_finalize
         int32_t* slab = slabs + int64_t(sp) * M * N;
 #pragma unroll 1
-        for (int c = 0; c < BN / 32; ++c) {
+        for (int c = grp; c < BN / 32; c += kGroups) {
           const int64_t col0 = int64_t(nb) * BN + c * 32;
           uint32_t r[32];
           ptx::tmem_ld_32x32b_x32(tmem_base + ((quarter * 32) << 16) + uint32_t(acc * BN + c * 32), r);
@@ -452,7 +512,8 @@ __global__ void __launch_bounds__(A4 ? kThreadsA4 : kThreads, 1)
     }
   }
 
-  if (warp >= 4 && warp < 8 && lane == 0) ptx::bulk_wait_read<0>();  // staging reads done before the CTA exits
+  if (((warp >= 4 && warp < 8) || (!A4 && warp >= 8 && warp < 12)) && lane == 0)
+    ptx::bulk_wait_read<0>();  // staging reads done before the CTA exits
   ptx::tc_fence_before();
   __syncthreads();
   ptx::tc_fence_after();
@@ -682,6 +743,21 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(A4ANY ? kThreadsA4 :
       const int64_t row = int64_t(w.mb) * 2 * kBM + int64_t(rank) * kBM + quarter * 32 + lane;
       const int32_t row0 = w.mb * 2 * kBM + int32_t(rank) * kBM + int32_t(quarter) * 32;
       uint8_t* wbuf = stg + quarter * kStgBytes;
+      if (pr.splits == 1 && pr.tma_out && pr.out_dtype == kBF16) {
+#pragma unroll 1
+        for (int c = 0; c < BN / 32; c += 2) {  // 32 x 64 tiles (128-byte rows)
+          const int32_t col0 = w.nb * BN + c * 32;
+          uint32_t r0[32], r1[32];
+          ptx::tmem_ld_32x32b_x32(tmem_base + ((quarter * 32) << 16) + uint32_t(acc * BN + c * 32), r0);
+          ptx::tmem_ld_32x32b_x32(tmem_base + ((quarter * 32) << 16) + uint32_t(acc * BN + c * 32 + 32), r1);
+          ptx::tmem_ld_wait();
+          if (lane == 0) ptx::bulk_wait_read<1>();
+          __syncwarp();
+          if (row0 < pr.M && col0 < pr.N)
+            store_pair_tma_bf16(r0, r1, fscale, wbuf + ((c >> 1) & 1) * (kStgBytes / 2), lane, &P.o[w.q], col0,
+                                row0);
+        }
+      } else
 #pragma unroll 1
       for (int c = 0; c < BN / 32; ++c) {
         const int64_t col0 = int64_t(w.nb) * BN + c * 32;
@@ -715,7 +791,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(A4ANY ? kThreadsA4 :
       }
       ptx::tc_fence_before();
       __syncwarp();
-      if (lane == 0) ptx::mbar_arrive_cluster(tempty_leader + uint32_t(acc) * 8u);
+      // default-semantics remote arrive (as CUTLASS's 2-SM TMEM-empty arrive): the
+      // release.cluster form compiled to a MEMBAR + ERRBAR per tile and warp
+      if (lane == 0) ptx::mbar_arrive_remote(tempty_leader + uint32_t(acc) * 8u);
       if (++acc == 2) { acc = 0; acc_phase ^= 1; }
     }
   }
@@ -838,23 +916,25 @@ bool make_map_a4(CUtensorMap* map, const int8_t* ptr, int64_t rows, int64_t k, i
 }
 
 // Store map of the output for the TMA epilogue: (N, M) with row stride ldo,
-// 32 x 32 boxes, swizzle matching store_chunk_tma.  False = use the direct
+// 32-row boxes of 128-byte rows (32 fp32 / 64 bf16 columns), SW128 as
+// store_chunk_tma / store_pair_tma_bf16 write them.  False = use the direct
 // store epilogue (exact fp64 dequant, int32 accumulator dump, split-K slabs or
 // an output TMA cannot describe).
 bool make_out_map(CUtensorMap* map, void* out, int out_dtype, int64_t M, int64_t N, int64_t ldo, int epilogue,
                   const int32_t* acc_out, int splits) {
   if (!out || acc_out || splits != 1 || epilogue != kEpiFast) return false;
+  static const int knob_direct = env_knob("HLQ_GEMM_DIRECT_OUT");  // development A/B
+  if (knob_direct == 1) return false;
   const int64_t esz = out_dtype == kBF16 ? 2 : 4;
   if ((reinterpret_cast<uintptr_t>(out) % 16) || (ldo * esz) % 16 || M <= 0 || N <= 0) return false;
   EncodeTiledFn fn = encode_fn();
   if (!fn) return false;
   cuuint64_t dims[2] = {cuuint64_t(N), cuuint64_t(M)};
   cuuint64_t strides[1] = {cuuint64_t(ldo * esz)};
-  cuuint32_t box[2] = {32, 32};
+  cuuint32_t box[2] = {out_dtype == kBF16 ? 64u : 32u, 32};  // 128-byte rows either way
   cuuint32_t es[2] = {1, 1};
   return fn(map, out_dtype == kBF16 ? CU_TENSOR_MAP_DATA_TYPE_BFLOAT16 : CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, out,
-            dims, strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
-            out_dtype == kBF16 ? CU_TENSOR_MAP_SWIZZLE_64B : CU_TENSOR_MAP_SWIZZLE_128B,
+            dims, strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
             CU_TENSOR_MAP_L2_PROMOTION_NONE, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
@@ -904,7 +984,7 @@ int run_maps(const CUtensorMap& ma, const CUtensorMap& mb, int64_t M, int64_t N,
   const int tma_out =
       (geo.conv && geo.s > 1) ? 0 : (make_out_map(&mo, out, out_dtype, M, N, ldo, epilogue, acc_out, splits) ? 1 : 0);
   if (!tma_out) mo = ma;  // unused
-  gemm_i8_kernel<BN, STAGES, A4><<<grid, A4 ? kThreadsA4 : kThreads, Cfg::kSmem, stream>>>(
+  gemm_i8_kernel<BN, STAGES, A4><<<grid, A4 ? kThreadsA4 : kThreadsE2, Cfg::kSmem, stream>>>(
       ma, mb, mo, tma_out, int(M), int(N), int(K), int(groups), sa, sb, extra, epilogue, out, out_dtype, ldo,
       acc_out, ld_acc, splits, slabs, geo);
   if (splits > 1) {
@@ -1114,12 +1194,14 @@ GemmPlan plan_gemm_base(int64_t M, int64_t N, int64_t K, int64_t groups, bool al
   // Long contractions with enough rows run as CTA pairs (cta_group::2, 256-row
   // tiles: a third less operand traffic per MAC).  Tile width by a makespan
   // model: rounds of pair units x relative unit cost (a 256 x 128 unit costs
-  // ~0.6 of a 256 x 256 one; tools/gemm_sweep.py, B200).  Short K (e.g. the
-  // fc2 dX, K = 768) stays single-CTA: its epilogue, not the operand stream,
-  // dominates.
+  // ~0.6 of a 256 x 256 one; tools/gemm_sweep.py, B200).  Wide outputs (N >=
+  // 2048) take pairs at any K: a single CTA's 128 x 256 tile moves ~117 KB of
+  // shared memory per 128-byte K block (TMA in, MMA operand reads, epilogue
+  // staging) against ~545 cycles of MMA -- shared-memory bound at ~55 % tensor
+  // (ncu, fc2 dX); the pair halves the B traffic per SM (fc2 dX 63.5 -> 55 us).
   const int64_t tiles128 = m_tiles * ((N + 127) / 128);
   const bool split_case = allow_split && 2 * tiles128 <= sms && nk >= 16;
-  if (!split_case && nk >= 16 && M >= 2 * kBM && sms >= 2) {
+  if (!split_case && (nk >= 16 || (N >= 2048 && nk >= 2)) && M >= 2 * kBM && sms >= 2) {
     const int64_t pairs = sms / 2, pm = (M + 2 * kBM - 1) / (2 * kBM);
     const int64_t u256 = pm * ((N + 255) / 256), u192 = pm * ((N + 191) / 192), u128 = pm * ((N + 127) / 128);
     const double t256 = double((u256 + pairs - 1) / pairs), t192 = 0.9 * double((u192 + pairs - 1) / pairs),
