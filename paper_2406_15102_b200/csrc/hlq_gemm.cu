@@ -1263,9 +1263,13 @@ int launch_gemm_i8_pair2(const GemmDesc* d, cudaStream_t stream) {
 bool gemm_i8_pair2_eligible(const GemmDesc* d) {
   static const int min_nk = env_knob("HLQ_GEMM_PAIR_MINK") >= 0 ? env_knob("HLQ_GEMM_PAIR_MINK") : 16;  // sweeps
   static const int knob_fuse2 = env_knob("HLQ_GEMM_FUSE2");
+  // both products run as 256-row pair units; a short contraction qualifies when
+  // its output is wide (N >= 2048: the pair's halved B traffic pays at any K,
+  // plan_gemm_base) -- the ViT fc2 dX (K = 768, N = 3072) with its dW: 78 us
+  // fused vs 91 us as two launches
   for (int q = 0; q < 2; ++q) {
     const int64_t nk = ((d[q].K + kBK - 1) / kBK) * d[q].groups;
-    if (nk < min_nk || d[q].M < 2 * kBM) return false;
+    if ((nk < min_nk && !(d[q].N >= 2048 && nk >= 2)) || d[q].M < 2 * kBM) return false;
   }
   if (knob_fuse2 >= 0) return knob_fuse2 != 0;
   return true;

@@ -174,9 +174,10 @@ class HLQLinearFunction(torch.autograd.Function):
             side = side_stream(gy.device)
             side.wait_stream(main)
             # (torch.cuda.current_stream() returns a fresh wrapper per call: compare handles)
-            if side.cuda_stream == main.cuda_stream and ops.pair_eligible(O, B * L, k, ops.pad16(O)):
-                # dW and dX as one CTA-pair launch over both products' tiles when both
-                # contractions are long (otherwise two gemm_i8 calls, which keep the split-K planner)
+            if side.cuda_stream == main.cuda_stream and ops.pair_eligible(O, B * L, k, ops.pad16(O), I, I):
+                # dW and dX as one CTA-pair launch over both products' tiles when each
+                # contraction is long or its output wide (ops.pair_eligible; otherwise two
+                # gemm_i8 calls, which keep the split-K planner)
                 gw, gx = ops.gemm_i8_pair(
                     dict(a=cg, b=payload, m=O, n=I, k=k, bits_a=bits_gw, bits_b=bits_gw, sa=sg, sb=sx),
                     dict(a=cgx, b=cw, m=B * L, n=I, k=ops.pad16(O), bits_a=bits_gx, bits_b=bits_gx, sa=sgx,

@@ -8,6 +8,7 @@ HLQLibraryError.
 from __future__ import annotations
 
 import ctypes
+import os
 
 import torch
 
@@ -472,20 +473,27 @@ def _gemm_i4a(a, b, m, n, k, bits_b, sa, sb, extra, exact, out_dtype):
     return out, None
 
 
-PAIR_MIN_K = 16 * 128  # >= 16 K blocks of 128 bytes in BOTH products (hlq_gemm.cu gemm_i8_pair2_eligible)
+# >= 16 K blocks of 128 bytes in BOTH products (hlq_gemm.cu gemm_i8_pair2_eligible;
+# HLQ_GEMM_PAIR_MINK overrides both sides for A/B measurements)
+PAIR_MIN_K = int(os.environ.get("HLQ_GEMM_PAIR_MINK", "16")) * 128
 
 
-def pair_eligible(m0: int, m1: int, k0: int, k1: int) -> bool:
+def pair_eligible(m0: int, m1: int, k0: int, k1: int, n0: int = 0, n1: int = 0) -> bool:
     """True when hlq_gemm_i8_multi runs two products as ONE CTA-pair launch
-    (both contractions long, both >= 256 rows).  Otherwise the caller issues
-    two gemm_i8 calls, which keeps the split-K planner for short-M products
-    (the multi entry's sequential fallback runs without a split-K workspace).
-    HLQ_PAIR=0 disables the fused launch (A/B measurements)."""
-    import os
+    (mirror of hlq_gemm.cu gemm_i8_pair2_eligible): both >= 256 rows, each
+    contraction long (>= 16 K blocks) or its output wide (N >= 2048, e.g. the
+    ViT fc2 dX).  Otherwise the caller issues two gemm_i8 calls, which keeps the
+    split-K planner for short-M products (the multi entry's sequential fallback
+    runs without a split-K workspace).  HLQ_PAIR=0 disables the fused launch
+    (A/B measurements)."""
     if os.environ.get("HLQ_PAIR", "1") == "0":
         return False
+    for k, n in ((k0, n0), (k1, n1)):
+        nk = (k + 127) // 128
+        if not (k > PAIR_MIN_K - 128 or (n >= 2048 and nk >= 2)):
+            return False
     # (contractions past the int32-exact bound run as K chunks through gemm_i8)
-    return PAIR_MIN_K - 128 < min(k0, k1) and max(k0, k1) * 127 * 127 < 2 ** 31 and min(m0, m1) >= 256
+    return max(k0, k1) * 127 * 127 < 2 ** 31 and min(m0, m1) >= 256
 
 
 def gemm_i8_pair(p0: dict, p1: dict):
