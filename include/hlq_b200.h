@@ -38,7 +38,12 @@
 
 /* Device scratch the single-call quantizers need for their statistics, the
  * fused kernel's grid barrier and its work-ticket counters, each on its own
- * 128-byte line (zeroed by the library on the caller's stream). */
+ * 128-byte line (zeroed by the library on the caller's stream).  The
+ * single-call quantizers (hlq_quantize_ht_cols / _proj_rows / _dual* and
+ * hlq_conv_acbp_compress) also accept stats_ws = NULL: the statistics then
+ * live in one of 64 library-owned per-device slots that the fused launch
+ * zeroes again when it finishes (no memset launch; fewer than 64 such calls
+ * may execute concurrently on a device), and are not returned. */
 #define HLQ_STATS_WS_BYTES 512
 
 #ifdef __cplusplus

@@ -31,7 +31,8 @@ def _to_nhwc(x: torch.Tensor) -> torch.Tensor:
     return x.permute(0, 2, 3, 1).contiguous()
 
 
-def conv_acbp_compress(x: torch.Tensor, k: int, stride: int, pad: int, strategy: BackwardStrategy, dp=None):
+def conv_acbp_compress(x: torch.Tensor, k: int, stride: int, pad: int, strategy: BackwardStrategy, dp=None,
+                       want_stats: bool = True):
     """ACBP of im2col(x) (layers.py:141-151 + backprop.py:373-385).  Returns an
     ACBPActivation whose orig_shape is the lowered (B, L, C*k*k).  dp
     (dp.ExactDP): the scale of the whole data-parallel batch (amax is then None)."""
@@ -64,7 +65,8 @@ def conv_acbp_compress(x: torch.Tensor, k: int, stride: int, pad: int, strategy:
         codes, kk, scale = dp.quant_conv(_to_nhwc(x), k, stride, pad, plan.gpu_bitmap(), bits)
         amax = None
     elif axis == 1:
-        codes, kk, scale, amax = ops.conv_acbp(_to_nhwc(x), k, stride, pad, plan.gpu_bitmap(), bits)
+        codes, kk, scale, amax = ops.conv_acbp(_to_nhwc(x), k, stride, pad, plan.gpu_bitmap(), bits,
+                                               want_stats=want_stats)
     else:
         # L < 16: projection along the batch axis needs the lowered tensor itself
         cols = F.unfold(x, k, padding=pad, stride=stride).transpose(1, 2).contiguous()
@@ -109,8 +111,8 @@ def _conv_backward(acbp: ACBPActivation, w4: torch.Tensor, gy: torch.Tensor, x_s
         cgx, sgx, cg, kg, sg = dp.quant_gy(gy3.reshape(B, L, O), acbp.axis, acbp.plan.gpu_bitmap(), bits_gx,
                                            bits_gw)
     elif acbp.axis == 1:
-        cgx, sgx, cg, kg, sg, st = ops.quant_dual(gy3, segs, rows, cols, acbp.plan.gpu_bitmap(),
-                                                  bits_gx, bits_gw, ld_src, seg_src)
+        cgx, sgx, cg, kg, sg, _ = ops.quant_dual(gy3, segs, rows, cols, acbp.plan.gpu_bitmap(),
+                                                 bits_gx, bits_gw, ld_src, seg_src, want_stats=False)
     else:
         cg, kg, sg, _ = ops.quant_proj_rows(gy3, segs, rows, cols, acbp.plan.gpu_bitmap(), bits_gw,
                                             ld_src, seg_src)
@@ -203,7 +205,8 @@ class HLQConv2dFunction(torch.autograd.Function):
         ctx.wcodes = wcodes if ctx.needs_input_grad[0] else None
         acbp = None
         if ctx.needs_input_grad[1]:
-            acbp, _ = conv_acbp_compress(x.detach(), weight.shape[2], stride, pad, strategy, dp=dp)
+            acbp, _ = conv_acbp_compress(x.detach(), weight.shape[2], stride, pad, strategy, dp=dp,
+                                         want_stats=False)
             ctx.save_for_backward(weight, acbp.quantized.payload, acbp.quantized.scale)
         else:
             ctx.save_for_backward(weight, None, None)

@@ -132,6 +132,18 @@ int hlq_device_ok(void) {
   return major == 10 ? 1 : 0;
 }
 
+// stats_ws == NULL: a library-owned, self-cleaning statistics slot (no memset
+// launch); otherwise the caller's scratch, zeroed here
+static void prepare_stats(hlq::TransformArgs& t, uint32_t* stats_ws, cudaStream_t st) {
+  if (stats_ws) {
+    t.stats = stats_ws;
+    cudaMemsetAsync(stats_ws, 0, HLQ_STATS_WS_BYTES, st);
+  } else {
+    t.stats = hlq::stats_slot();
+    t.pooled = true;
+  }
+}
+
 int hlq_quantize_ht_cols(const void* src, int dtype, int64_t rows, int64_t cols, int64_t ld_src,
                          int bits, uint32_t* stats_ws, int8_t* dst, int64_t ld_dst,
                          float* scale_out, void* stream) {
@@ -148,7 +160,7 @@ int hlq_quantize_ht_cols(const void* src, int dtype, int64_t rows, int64_t cols,
   t.seg_src = rows * ld_src; t.do_gx = true; t.do_gw = false; t.bitmap = 0xFFFF;
   t.bits_gx = bits; t.bits_gw = bits; t.stats = stats_ws; t.dst_gx = dst; t.ld_gx = ld_dst;
   t.scale_gx = scale_out;
-  cudaMemsetAsync(stats_ws, 0, HLQ_STATS_WS_BYTES, st);
+  prepare_stats(t, stats_ws, st);
   hlq::launch_transform(t, hlq::kBoth, st);
   return cuda_status("hlq_quantize_ht_cols");
 }
@@ -191,9 +203,9 @@ int hlq_quantize_proj_rows(const void* src, int dtype, int64_t segs, int64_t row
                            void* stream) {
   HLQ_TRY(proj_rows_checked(src, dtype, segs, rows, cols, ld_src, seg_src, bitmap, bits, dst, ld_dst));
   cudaStream_t st = static_cast<cudaStream_t>(stream);
-  const hlq::TransformArgs t = proj_args(src, dtype, segs, rows, cols, ld_src, seg_src, bitmap, bits,
-                                         stats_ws, dst, ld_dst, scale_out);
-  cudaMemsetAsync(stats_ws, 0, HLQ_STATS_WS_BYTES, st);
+  hlq::TransformArgs t = proj_args(src, dtype, segs, rows, cols, ld_src, seg_src, bitmap, bits,
+                                   stats_ws, dst, ld_dst, scale_out);
+  prepare_stats(t, stats_ws, st);
   hlq::launch_transform(t, hlq::kBoth, st);
   return cuda_status("hlq_quantize_proj_rows");
 }
@@ -233,7 +245,7 @@ int hlq_quantize_dual(const void* src, int dtype, int64_t segs, int64_t rows, in
   hlq::TransformArgs t = proj_args(src, dtype, segs, rows, cols, ld_src, seg_src, bitmap, bits_gw,
                                    stats_ws, dst_gw, ld_gw, scale_gw);
   t.do_gx = true; t.bits_gx = bits_gx; t.dst_gx = dst_gx; t.ld_gx = ld_gx; t.scale_gx = scale_gx;
-  cudaMemsetAsync(stats_ws, 0, HLQ_STATS_WS_BYTES, st);
+  prepare_stats(t, stats_ws, st);
   hlq::launch_transform(t, hlq::kBoth, st);
   return cuda_status("hlq_quantize_dual");
 }
@@ -262,7 +274,7 @@ int hlq_quantize_dual_colsum(const void* src, int dtype, int64_t segs, int64_t r
   t.do_gx = true; t.bits_gx = bits_gx; t.dst_gx = dst_gx; t.ld_gx = ld_gx; t.scale_gx = scale_gx;
   t.colsum_out = colsum_out;
   t.colsum_ws = static_cast<float*>(colsum_ws);
-  cudaMemsetAsync(stats_ws, 0, HLQ_STATS_WS_BYTES, st);
+  prepare_stats(t, stats_ws, st);
   hlq::launch_transform(t, hlq::kBoth, st);
   return cuda_status("hlq_quantize_dual_colsum");
 }
@@ -291,7 +303,7 @@ int hlq_quantize_dual_ex(const void* src, int dtype, int64_t segs, int64_t rows,
   t.scale_gx = scale_gx; t.pack_gx = pack_gx != 0;
   t.colsum_out = colsum_out;
   t.colsum_ws = static_cast<float*>(colsum_ws);
-  cudaMemsetAsync(stats_ws, 0, HLQ_STATS_WS_BYTES, st);
+  prepare_stats(t, stats_ws, st);
   hlq::launch_transform(t, hlq::kBoth, st);
   return cuda_status("hlq_quantize_dual_ex");
 }
@@ -784,10 +796,13 @@ int hlq_conv_acbp_compress(const void* x_nhwc, int dtype, int64_t B, int64_t H, 
   const int64_t kk = B * ((Ho * Wo + 15) / 16) * __builtin_popcount(bitmap);
   if (ld_payload < kk) return fail(HLQ_ERR_DIMENSION, "payload ld %lld < K %lld", (long long)ld_payload, (long long)kk);
   cudaStream_t st = static_cast<cudaStream_t>(stream);
-  cudaMemsetAsync(stats_ws, 0, HLQ_STATS_WS_BYTES, st);
+  const bool pooled = stats_ws == nullptr;  // library slot: the fused launch zeroes it again
+  if (pooled) stats_ws = hlq::stats_slot();
+  else cudaMemsetAsync(stats_ws, 0, HLQ_STATS_WS_BYTES, st);
   if (hlq::launch_conv_acbp_tma(x_nhwc, dtype, int(B), int(H), int(W), int(C), k, stride, pad, bitmap, bits,
-                                hlq::kBoth, stats_ws, payload, ld_payload, scale_out, st))
+                                hlq::kBoth, stats_ws, payload, ld_payload, scale_out, st, pooled))
     return cuda_status("hlq_conv_acbp_compress");
+  if (pooled) cudaMemsetAsync(stats_ws, 0, HLQ_STATS_WS_BYTES, st);
   hlq::launch_im2col_proj(x_nhwc, dtype, int(B), int(H), int(W), int(C), k, stride, pad, bitmap, bits,
                           hlq::kStats, stats_ws, nullptr, 0, nullptr, st);
   hlq::launch_im2col_proj(x_nhwc, dtype, int(B), int(H), int(W), int(C), k, stride, pad, bitmap, bits,

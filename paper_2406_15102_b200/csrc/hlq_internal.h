@@ -66,9 +66,18 @@ struct TransformArgs {
   float* colsum_ws = nullptr;
   // gx codes packed two per byte (low nibble first), ld_gx in bytes (4-bit codes only)
   bool pack_gx = false;
+  // stats is a library-owned slot (stats_slot): the fused TMA launch zeroes it
+  // again when its last CTA finishes; other launches are preceded by a memset
+  bool pooled = false;
 };
 
 void launch_transform(const TransformArgs& t, int mode, cudaStream_t stream);
+// A fused transform's statistics scratch from the library's per-device ring of
+// kStatSlots zero-initialised HLQ_STATS_WS_BYTES slots, for callers that pass
+// stats_ws = NULL (no per-launch memset).  A slot is reused kStatSlots fused
+// launches later, so fewer than that many may run concurrently on a device.
+constexpr int kStatSlots = 64;
+uint32_t* stats_slot();
 size_t transform_colsum_ws(int64_t segs, int64_t rows, int64_t cols, uint32_t bitmap);
 void launch_transform_fallback(const TransformArgs& t, int mode, cudaStream_t stream);
 
@@ -81,7 +90,7 @@ void launch_im2col_proj(const void* x, int dtype, int B, int H, int W, int C, in
 // launched) when a tensor map cannot describe x; mode may be kBoth.
 bool launch_conv_acbp_tma(const void* x, int dtype, int B, int H, int W, int C, int k, int stride, int pad,
                           uint32_t bitmap, int bits, int mode, uint32_t* stats, int8_t* dst, int64_t ld_dst,
-                          float* scale, cudaStream_t stream);
+                          float* scale, cudaStream_t stream, bool pooled = false);
 // col2im for dcols with (tap, c) column order; false if C % 8 or alignment
 // rule out its 16-byte accesses (nothing launched).
 bool launch_col2im_tapmajor(const void* dcols, int in_dtype, int64_t ld, int B, int H, int W, int C, int k,

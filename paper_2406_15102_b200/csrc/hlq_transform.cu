@@ -47,7 +47,9 @@
 #include <cuda_bf16.h>
 #include <cstdint>
 #include <cstdlib>
+#include <atomic>
 
+#include "hlq_b200.h"
 #include "hlq_internal.h"
 #include "hlq_ptx.cuh"
 #include "hlq_quant.cuh"
@@ -111,6 +113,7 @@ struct Args {
   int vblocks;
   int cbw;  // columns of the gw staging buffer (cch when row-grouped, else 256)
   int poll_ns;    // grid-barrier polling back-off (HLQ_TR_POLL_NS, development)
+  int self_reset; // stats is a library slot: the last CTA to finish zeroes it (kBoth)
   int dev_flags;  // development A/B (HLQ_TR_FLAGS): 1 = no ticket prefetch, 2 = no grid maxima exchange,
                  // 4 = bias column sums in the QUANT pass (+ a second grid barrier) instead of the STATS pass
   // column sums of the source (the bias gradient), fused into the STATS pass of
@@ -808,6 +811,11 @@ __global__ void __launch_bounds__(kThreads, HLQ_TR_MINB) tma_tile_kernel(const _
         }
       }
     }
+    if (MODE == kBoth && a.self_reset) {
+      // join the final CTA barrier: this warp's ticket / maxima atomics are then
+      // ordered before the CTA's arrival at the slot's done counter
+      __syncthreads();
+    }
     return;
   }
 
@@ -883,6 +891,19 @@ __global__ void __launch_bounds__(kThreads, HLQ_TR_MINB) tma_tile_kernel(const _
     }
   }
   stamp(4);
+  if (MODE == kBoth && a.self_reset) {
+    // library-owned statistics slot: the last CTA to get here (every other CTA
+    // is past both passes and every barrier) zeroes it for its next launch
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      uint32_t old;
+      asm volatile("atom.acq_rel.gpu.global.add.u32 %0, [%1], 1;" : "=r"(old) : "l"(a.stats + 33) : "memory");
+      if (old == gridDim.x - 1) {
+        for (int i = 0; i < HLQ_STATS_WS_BYTES / 4; ++i)
+          asm volatile("st.relaxed.gpu.global.u32 [%0], %1;" ::"l"(a.stats + i), "r"(0u) : "memory");
+      }
+    }
+  }
 }
 
 template <typename T, int MODE, bool GX, bool GW, int BM, int GRP>
@@ -1007,6 +1028,21 @@ void launch_colsum(const TransformArgs& t, cudaStream_t st) {
 }  // namespace
 
 __device__ uint32_t g_nonfinite_flag;
+__device__ uint32_t g_stat_slots[kStatSlots][HLQ_STATS_WS_BYTES / 4];  // zero-initialised
+
+uint32_t* stats_slot() {
+  static uint32_t* base[64] = {nullptr};
+  static std::atomic<uint32_t> next[64];
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= 64) return nullptr;
+  if (!base[dev]) {
+    void* p = nullptr;
+    if (cudaGetSymbolAddress(&p, g_stat_slots) != cudaSuccess) return nullptr;
+    base[dev] = static_cast<uint32_t*>(p);
+  }
+  const uint32_t i = next[dev].fetch_add(1u, std::memory_order_relaxed) % kStatSlots;
+  return base[dev] + size_t(i) * (HLQ_STATS_WS_BYTES / 4);
+}
 
 uint32_t* nonfinite_word() {
   static uint32_t* addr[64] = {nullptr};
@@ -1027,7 +1063,7 @@ typedef CUresult (*EncodeIm2colFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t
 
 bool launch_conv_acbp_tma(const void* x, int dtype, int B, int H, int W, int C, int k, int stride, int pad,
                           uint32_t bitmap, int bits, int mode, uint32_t* stats, int8_t* dst, int64_t ld_dst,
-                          float* scale, cudaStream_t stream) {
+                          float* scale, cudaStream_t stream, bool pooled) {
   static EncodeIm2colFn enc = [] {
     void* p = nullptr;
     cudaDriverEntryPointQueryResult q;
@@ -1087,6 +1123,7 @@ bool launch_conv_acbp_tma(const void* x, int dtype, int B, int H, int W, int C, 
   a.scale_gw = scale;
   a.nonfinite = nonfinite_word();
   a.cstride = a.nb * a.rank + 16;
+  a.self_reset = pooled && mode == kBoth ? 1 : 0;
   a.dev_flags = tr_dev_flags();
   a.poll_ns = tr_poll_ns();
   if (dtype == kBF16)
@@ -1121,6 +1158,7 @@ void launch_transform(const TransformArgs& t, int mode, cudaStream_t stream) {
     ok = encode_tensor_map(&map, t.dtype == kBF16 ? 1 : 2, 3, t.src, dims, strides, box, 0);
   }
   if (!ok) {
+    if (t.pooled) cudaMemsetAsync(t.stats, 0, HLQ_STATS_WS_BYTES, stream);  // not self-cleaning
     if (mode == kBoth) {
       launch_transform_fallback(t, kStats, stream);
       launch_transform_fallback(t, kQuant, stream);
@@ -1158,6 +1196,8 @@ void launch_transform(const TransformArgs& t, int mode, cudaStream_t stream) {
   a.cstride = a.nb * a.tq * a.rank + 16;
   a.dev_flags = tr_dev_flags();
   a.poll_ns = tr_poll_ns();
+  a.self_reset = t.pooled && mode == kBoth ? 1 : 0;
+  if (t.pooled && mode != kBoth) cudaMemsetAsync(t.stats, 0, HLQ_STATS_WS_BYTES, stream);
 #ifdef HLQ_TR_TRACE
   a.trace = g_tr_trace;
 #endif

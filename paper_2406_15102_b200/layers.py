@@ -115,7 +115,8 @@ class HLQLinearFunction(torch.autograd.Function):
                                                plan.gpu_bitmap(), bits_gw)
             elif ctx.needs_input_grad[1]:
                 payload, k, sx, _ = ops.quant_proj_rows(x.detach().contiguous(), segs, rows, cols,
-                                                        plan.gpu_bitmap(), bits_gw, ld_src, seg_src)
+                                                        plan.gpu_bitmap(), bits_gw, ld_src, seg_src,
+                                                        want_stats=False)
             if ctx.needs_input_grad[0] and wcodes is not None:
                 cw, sw = wcodes[0], wcodes[1]  # refreshed for this weight version by refresh_weight_codes
             elif ctx.needs_input_grad[0]:
@@ -167,7 +168,8 @@ class HLQLinearFunction(torch.autograd.Function):
             # the bias gradient (column sums of gy) comes out of the same kernel's STATS pass
             cgx, sgx, cg, kg, sg, _, *cs = ops.quant_dual(gy3, segs, rows, cols,
                                                           strategy.plan.gpu_bitmap(), bits_gx, bits_gw,
-                                                          ld_src, seg_src, colsum=want_gb, pack_gx=pack)
+                                                          ld_src, seg_src, colsum=want_gb, pack_gx=pack,
+                                                          want_stats=False)
             cw, sw = cw_saved, sw_saved
             # the two products are independent: dW on the side stream, dX here
             main = torch.cuda.current_stream()

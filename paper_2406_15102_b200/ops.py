@@ -137,20 +137,22 @@ def new_stats(device) -> torch.Tensor:
     return torch.zeros(4, dtype=torch.int32, device=device)
 
 
-def quant_ht_cols(src: torch.Tensor, bits: int):
+def quant_ht_cols(src: torch.Tensor, bits: int, want_stats: bool = True):
     """Q_bits(block-FWHT of every row of a (rows, cols) matrix along cols).
-    Returns (codes (rows, pad16(cols)) int8, scale (1,) fp32, amax_bits (1,) int32)."""
+    Returns (codes (rows, pad16(cols)) int8, scale (1,) fp32, amax_bits (1,) int32);
+    want_stats=False: the statistics stay in a library slot (no memset launch)
+    and amax_bits is None."""
     _check_bits(bits)
     src = _cuda(src, "src")
     rows, cols = src.shape
     ld = pad16(cols)
     codes = torch.empty((rows, ld), dtype=torch.int8, device=src.device)
     scale = torch.empty(1, dtype=torch.float32, device=src.device)
-    stats = torch.empty(STATS_WORDS, dtype=torch.int32, device=src.device)
+    stats = torch.empty(STATS_WORDS, dtype=torch.int32, device=src.device) if want_stats else None
     _traced("transform", rows * cols * src.element_size() + rows * ld, 0, 1,
             lambda: _lib.call("hlq_quantize_ht_cols", _p(src), dtype_code(src), rows, cols, cols,
                               bits, _p(stats), _p(codes), ld, _p(scale), _stream()))
-    return codes, scale, stats[0:1]
+    return codes, scale, None if stats is None else stats[0:1]
 
 
 def packed_ld(cols: int) -> int:
@@ -170,14 +172,15 @@ def unpack_int4(packed: torch.Tensor, cols: int) -> torch.Tensor:
 
 def quant_dual(src: torch.Tensor, segs: int, rows: int, cols: int, bitmap: int, bits_gx: int,
                bits_gw: int, ld_src: int | None = None, seg_src: int | None = None, colsum: bool = False,
-               pack_gx: bool = False):
+               pack_gx: bool = False, want_stats: bool = True):
     """Both gy operands from one read per pass: HT along cols (gx) and the
     rank-r projection along rows (gw).  Returns
     (gx_codes (segs*rows, pad16(cols)), gx_scale, gw_codes (cols, pad16(K)), K, gw_scale, stats)
     and, with colsum, a 7th item: the fp32 column sums of src (cols,) -- the
     bias gradient -- computed from the same tiles.  pack_gx (4-bit gx codes):
     gx_codes is (segs*rows, packed_ld(cols)) uint8, two codes per byte, low
-    nibble first (hlq_quantize_dual_ex) -- the A operand of gemm_i8(a_packed=True)."""
+    nibble first (hlq_quantize_dual_ex) -- the A operand of gemm_i8(a_packed=True).
+    want_stats=False: the statistics stay in a library slot (no memset launch), stats is None."""
     _check_bits(bits_gx)
     _check_bits(bits_gw)
     if pack_gx and bits_gx != 4:
@@ -194,7 +197,7 @@ def quant_dual(src: torch.Tensor, segs: int, rows: int, cols: int, bitmap: int, 
         cgx = torch.empty((segs * rows, pad16(cols)), dtype=torch.int8, device=dev)
     cgw = torch.empty((cols, ldk), dtype=torch.int8, device=dev)
     scales = torch.empty(2, dtype=torch.float32, device=dev)
-    stats = torch.empty(STATS_WORDS, dtype=torch.int32, device=dev)
+    stats = torch.empty(STATS_WORDS, dtype=torch.int32, device=dev) if want_stats else None
     nbytes = segs * rows * cols * src.element_size() + cgx.numel() + cols * k
     key = f"transform:dual:{segs * rows}x{cols}:{src.dtype}".replace("torch.", "")
     cs = torch.empty(cols, dtype=torch.float32, device=dev) if colsum else None
@@ -230,9 +233,10 @@ def proj_rows_k(segs: int, rows: int, rank: int) -> int:
 
 
 def quant_proj_rows(src: torch.Tensor, segs: int, rows: int, cols: int, bitmap: int, bits: int,
-                    ld_src: int | None = None, seg_src: int | None = None):
+                    ld_src: int | None = None, seg_src: int | None = None, want_stats: bool = True):
     """Q_bits(rank-r block projection along rows), written transposed.
-    Returns (codes (cols, pad16(K)) int8, K, scale (1,), amax_bits (1,))."""
+    Returns (codes (cols, pad16(K)) int8, K, scale (1,), amax_bits (1,));
+    want_stats=False: library statistics slot, amax_bits None."""
     _check_bits(bits)
     src = _cuda(src, "src")
     ld_src = cols if ld_src is None else ld_src
@@ -241,13 +245,13 @@ def quant_proj_rows(src: torch.Tensor, segs: int, rows: int, cols: int, bitmap: 
     ld = max(pad16(k), 16)
     codes = torch.empty((cols, ld), dtype=torch.int8, device=src.device)
     scale = torch.empty(1, dtype=torch.float32, device=src.device)
-    stats = torch.empty(STATS_WORDS, dtype=torch.int32, device=src.device)
+    stats = torch.empty(STATS_WORDS, dtype=torch.int32, device=src.device) if want_stats else None
     _traced("transform", segs * rows * cols * src.element_size() + cols * k, 0, 1,
             lambda: _lib.call("hlq_quantize_proj_rows", _p(src), dtype_code(src), segs, rows, cols,
                               ld_src, seg_src, bitmap, bits, _p(stats), _p(codes), ld, _p(scale),
                               _stream()),
             key=f"transform:proj:{segs * rows}x{cols}:{src.dtype}".replace("torch.", ""))
-    return codes, k, scale, stats[2:3]
+    return codes, k, scale, None if stats is None else stats[2:3]
 
 
 def quant_weights(weights, bits: int, bf16: bool = False):
@@ -529,7 +533,7 @@ def conv_out_hw(H: int, W: int, k: int, stride: int, pad: int):
     return (H + 2 * pad - k) // stride + 1, (W + 2 * pad - k) // stride + 1
 
 
-def conv_acbp(x_nhwc: torch.Tensor, k: int, stride: int, pad: int, bitmap: int, bits: int):
+def conv_acbp(x_nhwc: torch.Tensor, k: int, stride: int, pad: int, bitmap: int, bits: int, want_stats: bool = True):
     """ACBP of im2col(x) along the output-pixel axis, from channels-last x
     (B, H, W, C) viewed as a contiguous tensor.  Returns (codes (C*k*k, pad16(K)), K, scale, amax)."""
     _check_bits(bits)
@@ -540,14 +544,14 @@ def conv_acbp(x_nhwc: torch.Tensor, k: int, stride: int, pad: int, bitmap: int, 
     ld = max(pad16(kk), 16)
     codes = torch.empty((C * k * k, ld), dtype=torch.int8, device=x_nhwc.device)
     scale = torch.empty(1, dtype=torch.float32, device=x_nhwc.device)
-    stats = torch.empty(STATS_WORDS, dtype=torch.int32, device=x_nhwc.device)
+    stats = torch.empty(STATS_WORDS, dtype=torch.int32, device=x_nhwc.device) if want_stats else None
     nbytes = x_nhwc.numel() * x_nhwc.element_size() + C * k * k * kk
     _traced("transform", nbytes, 0, 2,
             lambda: _lib.call("hlq_conv_acbp_compress", _p(x_nhwc), dtype_code(x_nhwc), B, H, W, C, k,
                               stride, pad, bitmap, bits, _p(codes), ld, _p(scale), _p(stats),
                               _stream()),
             key=f"transform:conv_acbp:{B}x{H}x{W}x{C}:k{k}s{stride}")
-    return codes, kk, scale, stats[2:3]
+    return codes, kk, scale, None if stats is None else stats[2:3]
 
 
 def conv_acbp_pass(x_nhwc: torch.Tensor, k: int, stride: int, pad: int, bitmap: int, bits: int, mode: int,
