@@ -114,6 +114,7 @@ struct Args {
   int cbw;  // columns of the gw staging buffer (cch when row-grouped, else 256)
   int poll_ns;    // grid-barrier polling back-off (HLQ_TR_POLL_NS, development)
   int self_reset; // stats is a library slot: the last CTA to finish zeroes it (kBoth)
+  int keep_items; // kBoth: first-pass items loaded evict_last (the second pass's first ones); 0 = no hints
   int dev_flags;  // development A/B (HLQ_TR_FLAGS): 1 = no ticket prefetch, 2 = no grid maxima exchange,
                  // 4 = bias column sums in the QUANT pass (+ a second grid barrier) instead of the STATS pass
   // column sums of the source (the bias gradient), fused into the STATS pass of
@@ -749,6 +750,7 @@ __global__ void __launch_bounds__(kThreads, HLQ_TR_MINB) tma_tile_kernel(const _
     // ---------------- producer
     if (ptx::elect_one()) {
       ptx::tma_prefetch_desc(&map);
+      const uint64_t pol_last = ptx::createpolicy_evict_last(), pol_first = ptx::createpolicy_evict_first();
       int slot = 0;
       uint32_t phase = 0;
       for (int pass = 0; pass < (MODE == kBoth ? 2 : 1); ++pass) {
@@ -798,7 +800,16 @@ __global__ void __launch_bounds__(kThreads, HLQ_TR_MINB) tma_tile_kernel(const _
             }
           } else {
             ptx::mbar_arrive_expect_tx(&full[slot], 16 * kRow);
-            ptx::tma_load_3d(tiles + slot * 16 * kRow, &map, &full[slot], it.col0, it.blk * 16, it.s);
+            if (MODE == kBoth && a.keep_items > 0) {
+              // L2 residency for the second pass (which walks the items in reverse):
+              // the last keep_items of the first pass stay (evict_last), everything
+              // else streams through (evict_first)
+              const bool keep = pass == 0 && it.ord >= a.items - a.keep_items;
+              ptx::tma_load_3d_hint(tiles + slot * 16 * kRow, &map, &full[slot], it.col0, it.blk * 16, it.s,
+                                    keep ? pol_last : pol_first);
+            } else {
+              ptx::tma_load_3d(tiles + slot * 16 * kRow, &map, &full[slot], it.col0, it.blk * 16, it.s);
+            }
           }
           if (++slot == kStages) { slot = 0; phase ^= 1; }
           it.next(a);
@@ -1197,6 +1208,14 @@ void launch_transform(const TransformArgs& t, int mode, cudaStream_t stream) {
   a.dev_flags = tr_dev_flags();
   a.poll_ns = tr_poll_ns();
   a.self_reset = t.pooled && mode == kBoth ? 1 : 0;
+  {
+    // keep ~HLQ_TR_KEEP_MB (default 32) MB of the source resident between the passes
+    // (fc2-input ACBP 75.8 -> 71.7 us, fc1 gy dual 120.7 -> 118.8 us; 64 / 96 MB no better)
+    static const int knob_keep = env_knob("HLQ_TR_KEEP_MB");
+    const double keep_mb = knob_keep >= 0 ? double(knob_keep) : 32.0;
+    const double src_mb = double(t.segs) * double(t.rows) * double(t.cols) * double(esz) / 1048576.0;
+    a.keep_items = keep_mb <= 0.0 ? 0 : (src_mb <= keep_mb ? a.items : int(double(a.items) * keep_mb / src_mb));
+  }
   if (t.pooled && mode != kBoth) cudaMemsetAsync(t.stats, 0, HLQ_STATS_WS_BYTES, stream);
 #ifdef HLQ_TR_TRACE
   a.trace = g_tr_trace;

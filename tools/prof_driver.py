@@ -47,6 +47,10 @@ def main():
             ops.gemm_i8(cgx, cw, T, I, ops.pad16(O), 4, 4, sgx, sw, 1.0, exact=False, out_dtype=dt)
         elif what == "gemm_dw":
             ops.gemm_i8(cg, xp, O, I, k, 8, 8, sg, sx, 1.0, exact=False)
+        elif what == "gemm_pair":  # dW + dX as the training path issues them (one CTA-pair launch)
+            ops.gemm_i8_pair(dict(a=cg, b=xp, m=O, n=I, k=k, bits_a=8, bits_b=8, sa=sg, sb=sx),
+                             dict(a=cgx, b=cw, m=T, n=I, k=ops.pad16(O), bits_a=4, bits_b=4, sa=sgx, sb=sw,
+                                  out_dtype=dt))
     torch.cuda.synchronize()
 
 
