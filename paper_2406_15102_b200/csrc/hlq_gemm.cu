@@ -307,6 +307,9 @@ __global__ void __launch_bounds__(A4 ? kThreadsA4 : kThreadsE2, 1)
   __syncthreads();
   ptx::tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
+  // programmatic dependent launch: the prologue above overlapped the previous
+  // kernel's tail; its outputs (codes, scales) are read only from here on
+  asm volatile("griddepcontrol.wait;" ::: "memory");
 
   const int num_m = (M + kBM - 1) / kBM;
   const int num_n = (N + BN - 1) / BN;
@@ -613,6 +616,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(A4ANY ? kThreadsA4 :
   ptx::cluster_sync();  // barrier inits visible to the peer before any remote arrive / TMA
   ptx::tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
+  asm volatile("griddepcontrol.wait;" ::: "memory");  // programmatic dependent launch (see gemm_i8_kernel)
 
   const int cid = blockIdx.x >> 1, ncl = gridDim.x >> 1;
   const int total = P.p[0].units + (P.nprob > 1 ? P.p[1].units : 0);
@@ -963,6 +967,16 @@ bool encode_tensor_map(void* map, int dtype, int rank, const void* ptr, const ui
 
 namespace {
 
+// Programmatic dependent launch (HLQ_PDL=0 disables): the GEMM's CTAs may start
+// their prologue (barriers, TMEM, descriptor prefetch) while the previous
+// kernel on the stream drains, and griddepcontrol.wait before touching its
+// outputs; the fused transforms trigger their dependents as each CTA finishes.
+void pdl_attr(cudaLaunchAttribute& a) {
+  static const int off = env_knob("HLQ_PDL");
+  a.id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  a.val.programmaticStreamSerializationAllowed = off == 0 ? 0 : 1;
+}
+
 template <int BN, int STAGES, bool A4 = false>
 int run_maps(const CUtensorMap& ma, const CUtensorMap& mb, int64_t M, int64_t N, int64_t K, int64_t groups,
              const float* sa, const float* sb, double extra, int epilogue, void* out, int out_dtype,
@@ -984,9 +998,20 @@ int run_maps(const CUtensorMap& ma, const CUtensorMap& mb, int64_t M, int64_t N,
   const int tma_out =
       (geo.conv && geo.s > 1) ? 0 : (make_out_map(&mo, out, out_dtype, M, N, ldo, epilogue, acc_out, splits) ? 1 : 0);
   if (!tma_out) mo = ma;  // unused
-  gemm_i8_kernel<BN, STAGES, A4><<<grid, A4 ? kThreadsA4 : kThreadsE2, Cfg::kSmem, stream>>>(
-      ma, mb, mo, tma_out, int(M), int(N), int(K), int(groups), sa, sb, extra, epilogue, out, out_dtype, ldo,
-      acc_out, ld_acc, splits, slabs, geo);
+  {
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(grid);
+    cfg.blockDim = dim3(A4 ? kThreadsA4 : kThreadsE2);
+    cfg.dynamicSmemBytes = Cfg::kSmem;
+    cfg.stream = stream;
+    cudaLaunchAttribute at[1];
+    pdl_attr(at[0]);
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    cudaLaunchKernelEx(&cfg, gemm_i8_kernel<BN, STAGES, A4>, ma, mb, mo, tma_out, int(M), int(N), int(K),
+                       int(groups), sa, sb, extra, epilogue, out, out_dtype, ldo, acc_out, ld_acc, splits, slabs,
+                       geo);
+  }
   if (splits > 1) {
     const int64_t nq = M * N / 4;
     int fgrid = int((nq + 255) / 256);
@@ -1112,10 +1137,21 @@ int run_2sm_specs(const PairSpec* specs, int n, cudaStream_t stream) {
   const int64_t pairs = num_sms() / 2;
   const int ncl = int(unit0 < pairs ? unit0 : pairs);
   if (n > 1) lpt_schedule(P, ncl);
-  if (any_a4)
-    gemm_i8_2sm_kernel<BN, STAGES, true><<<2 * ncl, kThreadsA4, kSmem, stream>>>(P);
-  else
-    gemm_i8_2sm_kernel<BN, STAGES, false><<<2 * ncl, kThreads, kSmem, stream>>>(P);
+  {
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(2 * ncl);
+    cfg.blockDim = dim3(any_a4 ? kThreadsA4 : kThreads);
+    cfg.dynamicSmemBytes = kSmem;
+    cfg.stream = stream;
+    cudaLaunchAttribute at[1];
+    pdl_attr(at[0]);
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    if (any_a4)
+      cudaLaunchKernelEx(&cfg, gemm_i8_2sm_kernel<BN, STAGES, true>, P);
+    else
+      cudaLaunchKernelEx(&cfg, gemm_i8_2sm_kernel<BN, STAGES, false>, P);
+  }
   for (int q = 0; q < n; ++q) {
     const PairSpec& s = specs[q];
     if (s.splits > 1) {

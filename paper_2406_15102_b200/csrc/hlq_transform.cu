@@ -902,6 +902,9 @@ __global__ void __launch_bounds__(kThreads, HLQ_TR_MINB) tma_tile_kernel(const _
     }
   }
   stamp(4);
+  // this CTA's outputs are written: a dependent GEMM launched with programmatic
+  // serialization may start its prologue (it waits for the whole grid before reading)
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
   if (MODE == kBoth && a.self_reset) {
     // library-owned statistics slot: the last CTA to get here (every other CTA
     // is past both passes and every barrier) zeroes it for its next launch
