@@ -807,6 +807,7 @@ int hlq_conv_acbp_compress(const void* x_nhwc, int dtype, int64_t B, int64_t H, 
                           hlq::kStats, stats_ws, nullptr, 0, nullptr, st);
   hlq::launch_im2col_proj(x_nhwc, dtype, int(B), int(H), int(W), int(C), k, stride, pad, bitmap, bits,
                           hlq::kQuant, stats_ws, payload, ld_payload, scale_out, st);
+  if (pooled) cudaMemsetAsync(stats_ws, 0, HLQ_STATS_WS_BYTES, st);  // leave the library slot zeroed
   return cuda_status("hlq_conv_acbp_compress");
 }
 

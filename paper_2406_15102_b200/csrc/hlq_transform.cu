@@ -745,6 +745,9 @@ __global__ void __launch_bounds__(kThreads, HLQ_TR_MINB) tma_tile_kernel(const _
     ptx::fence_mbar_init();
   }
   __syncthreads();
+  // programmatic dependent launch: the source (and everything else) is read
+  // only after the previous kernel on the stream has completed
+  asm volatile("griddepcontrol.wait;" ::: "memory");
 
   if (warp == kConsumers / 32) {
     // ---------------- producer
@@ -948,12 +951,21 @@ void launch_one(const CUtensorMap& map, Args a, cudaStream_t stream) {
   cfg.blockDim = dim3(kThreads);
   cfg.dynamicSmemBytes = smem;
   cfg.stream = stream;
-  cudaLaunchAttribute attr_coop[1];
+  cudaLaunchAttribute attr_coop[2];
   attr_coop[0].id = cudaLaunchAttributeCooperative;
   attr_coop[0].val.cooperative = 1;
+  // programmatic dependent launch (the kernel waits on griddepcontrol before its
+  // first read); HLQ_PDL=0 or a runtime that rejects the combination: plain
+  static const int pdl_off = env_knob("HLQ_PDL");
+  attr_coop[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr_coop[1].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = attr_coop;
-  cfg.numAttrs = 1;
-  cudaLaunchKernelEx(&cfg, kern, map, a);
+  cfg.numAttrs = pdl_off == 0 ? 1 : 2;
+  if (cudaLaunchKernelEx(&cfg, kern, map, a) != cudaSuccess && cfg.numAttrs == 2) {
+    (void)cudaGetLastError();
+    cfg.numAttrs = 1;
+    cudaLaunchKernelEx(&cfg, kern, map, a);
+  }
 }
 
 template <typename T, int MODE, bool GX, bool GW>
@@ -1180,6 +1192,8 @@ void launch_transform(const TransformArgs& t, int mode, cudaStream_t stream) {
       launch_transform_fallback(t, mode, stream);
     }
     if (t.colsum_out) launch_colsum(t, stream);
+    // the fallback kernels do not clean up after themselves: leave the slot zeroed
+    if (t.pooled) cudaMemsetAsync(t.stats, 0, HLQ_STATS_WS_BYTES, stream);
     return;
   }
   Args a{};
@@ -1233,6 +1247,7 @@ void launch_transform(const TransformArgs& t, int mode, cudaStream_t stream) {
   else
     launch_modes<float>(map, a, mode, t.do_gx, t.do_gw, stream);
   if (t.colsum_out && !a.cs_out) launch_colsum(t, stream);
+  if (t.pooled && mode != kBoth) cudaMemsetAsync(t.stats, 0, HLQ_STATS_WS_BYTES, stream);  // leave it zeroed
 }
 
 size_t transform_colsum_ws(int64_t segs, int64_t rows, int64_t cols, uint32_t bitmap) {

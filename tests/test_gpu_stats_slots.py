@@ -64,3 +64,9 @@ def test_slots_fallback_source(ops):
         b = ops.quant_dual(src, 4, 197, 768, 0x5555, 4, 8, 771, 197 * 771)
         assert torch.isfinite(b[1]).all()
         assert torch.equal(a[0], b[0]) and torch.equal(a[2], b[2]) and torch.equal(a[1], b[1])
+    # ... and leave their slots zeroed: the next 130 fused launches (every slot twice) are unaffected
+    g = src[:, :, :768].contiguous()
+    ref = ops.quant_dual(g, 4, 197, 768, 0x5555, 4, 8)
+    for _ in range(130):
+        a = ops.quant_dual(g, 4, 197, 768, 0x5555, 4, 8, want_stats=False)
+        assert torch.equal(a[0], ref[0]) and torch.equal(a[1], ref[1]) and torch.equal(a[4], ref[4])
