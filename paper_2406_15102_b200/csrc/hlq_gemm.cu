@@ -1089,7 +1089,10 @@ bool lpt_schedule(PairParams& P, int ncl) {
   for (int u = 0; u < total; ++u) {
     const PairProb& pr = P.p[(P.nprob > 1 && u >= P.p[1].unit0) ? 1 : 0];
     const int nk = ((pr.K + kBK - 1) / kBK) * pr.groups / pr.splits;
-    cost[u] = {nk + 4, u};
+    // fixed per-unit term (epilogue, pipeline fill): 2 measured best for the fc2
+    // dW + dX mix (74 us vs 78 us at 4 and 0; fc1 / qkv unchanged)
+    static const int knob_epi = env_knob("HLQ_GEMM_LPT_EPI");  // development sweeps
+    cost[u] = {nk + (knob_epi >= 0 ? knob_epi : 2), u};
   }
   std::stable_sort(cost.begin(), cost.end(), [](const auto& x, const auto& y) { return x.first > y.first; });
   std::vector<int64_t> load(ncl, 0);

@@ -19,6 +19,12 @@ for g in gemm_dx gemm_dw; do
 done
 timeout 300 ncu --set full --clock-control none --import-source on -k regex:gemm_i8 -s 1 -c 1 \
   -o gpurun_out/prof_fc2_gemm_dx python tools/prof_driver.py gemm_dx 128,197,3072,768 2 > /dev/null 2>&1
+# the fused dW + dX CTA-pair launch the training path issues for fc2 (and fc1)
+for s in 128,197,3072,768 128,197,768,3072; do
+  tag=$( [ $s = 128,197,3072,768 ] && echo fc2 || echo fc1 )
+  timeout 300 ncu --set full --clock-control none --import-source on -k regex:gemm_i8_2sm -s 1 -c 1 \
+    -o gpurun_out/prof_${tag}_gemm_pair python tools/prof_driver.py gemm_pair $s 2 > /dev/null 2>&1
+done
 # 4. conv (BASELINE config b): implicit-GEMM dgrad and the im2col ACBP
 timeout 300 ncu --set full --clock-control none -k regex:"gemm_i8|tma_tile" -s 0 -c 4 \
   -o gpurun_out/prof_conv python tools/conv_profile.py > /dev/null 2>&1
