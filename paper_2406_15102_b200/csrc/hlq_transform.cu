@@ -275,6 +275,15 @@ __device__ __forceinline__ void consume(const Args& a, const Quant& qx, const Qu
   const bool cs_here = a.cs_part && (MODE == ((a.dev_flags & 4) ? kQuant : kStats));
   uint32_t mz = 0x7FFF7FFFu;      // running s16x2 min of |x| bits + 0x7FFF
   float thr_x = 0.0f, thr_w = 0.0f;  // skip thresholds from the running exact maxima
+  // per-thread tile geometry, fixed for the whole launch (hoisted: the grouped
+  // variants had spent a signed integer division per thread and step on it)
+  const int g1_q = GRP == 2 ? (tid & 15) / (a.cch >> 4) : 0;    // phase 1, row groups: sub-tile
+  const int g1_bb = GRP == 2 ? (tid & 15) - g1_q * (a.cch >> 4) : (tid & 15);
+  const int g2_q = GRP ? (2 * tid) / a.cch : 0;                  // phase 2: sub-tile of column 2*tid
+  const int g2_cc = 2 * tid - g2_q * (GRP ? a.cch : 0);
+  const uint32_t g2_pitch = GRP ? uint32_t(a.cch) * sizeof(T) : uint32_t(kRow);
+  const uint32_t g2_off = GRP ? uint32_t(g2_q) * 16u * g2_pitch + uint32_t(g2_cc) * sizeof(T)
+                              : uint32_t(2 * tid) * sizeof(T);
   while (DYN || it.valid(a)) {
     {
       ptx::mbar_wait(&full[slot], phase);
@@ -311,8 +320,8 @@ __device__ __forceinline__ void consume(const Args& a, const Quant& qx, const Qu
         uint32_t pitch = kRow, base = tile;
         bool ok = true;
         if (rg) {
-          const int bpt = a.cch >> 4, q = b / bpt;
-          bb = b - q * bpt;
+          const int q = g1_q;
+          bb = g1_bb;
           pitch = uint32_t(a.cch) * sizeof(T);
           base = tile + q * 16 * pitch;
           ok = rb0 + q < a.total_blocks;
@@ -415,11 +424,10 @@ __device__ __forceinline__ void consume(const Args& a, const Quant& qx, const Qu
         const int c = 2 * tid;
         // tap-grouped (conv) tiles: column c is channel c % cch of tap (tap + c / cch);
         // row-grouped tiles: column c % cch of real block rb0 + c / cch
-        const int q = GRP ? c / a.cch : 0;
-        const int cc = c - q * a.cch;  // source column inside the sub-tile (== c when tq == 1)
-        const uint32_t pitch = GRP ? uint32_t(a.cch) * sizeof(T) : uint32_t(kRow);
-        const uint32_t col_addr = tile + (GRP ? q * 16 * pitch + uint32_t(cc) * sizeof(T)
-                                                   : uint32_t(c) * sizeof(T));
+        const int q = g2_q;
+        const int cc = g2_cc;  // source column inside the sub-tile (== c when tq == 1)
+        const uint32_t pitch = g2_pitch;
+        const uint32_t col_addr = tile + g2_off;
         const bool in = GRP == 0 ? it.col0 + c < a.cols : (rg ? rb0 + q < a.total_blocks : q < it.ntq);
         bool need_w = false;
         if (kBound && in) {
@@ -609,17 +617,21 @@ __device__ __forceinline__ void consume(const Args& a, const Quant& qx, const Qu
       const int orow = a.taps ? a.taps : 1;  // payload row of column c: c (Linear) or c*taps + tap (conv)
       const int ncols = rgf ? a.cch : (GRP == 1 ? it.ntq * a.cch : min(kCols, a.cols - it.col0));
       // payload row of tile column c (tap-grouped: channel c % cch, tap + c / cch)
+      // (cch of a tap-grouped tile is 32 / 64 / 128: shifts, not divisions)
+      const int csh = __ffs(GRP == 1 ? a.cch : 1) - 1;
       auto prow = [&](int c) -> int64_t {
         if (GRP == 1) {
-          const int qq = c / a.cch;
-          return int64_t(c - qq * a.cch) * orow + it.tap + qq;
+          const int qq = c >> csh;
+          return int64_t(c - (qq << csh)) * orow + it.tap + qq;
         }
         return int64_t(it.col0 + c) * orow + it.tap;
       };
       if ((run & 15) == 0 && (k0 & 15) == 0) {
         const int chunks = run >> 4;
+        const int chsh = __ffs(chunks) - 1;  // chunks = nbl * rank / 16 (rank 8 / 16, nbl a power of two)
+        const bool chpow2 = (chunks & (chunks - 1)) == 0;
         for (int i = ftid; i < ncols * chunks; i += kFlushThreads) {
-          const int c = i / chunks, q = i - c * chunks;
+          const int c = chpow2 ? (i >> chsh) : i / chunks, q = i - c * chunks;
           *reinterpret_cast<uint4*>(a.dst_gw + prow(c) * a.ld_gw + k0 + 16 * q) =
               *reinterpret_cast<const uint4*>(cbuf + c * a.cstride + 16 * q);
         }
@@ -785,11 +797,12 @@ __global__ void __launch_bounds__(kThreads, HLQ_TR_MINB) tma_tile_kernel(const _
             const int l0 = it.blk * 16, ho = l0 / a.wo_n, wo = l0 - ho * a.wo_n;
             const uint32_t sub = GRP == 1 ? uint32_t(16 * a.cch * sizeof(T)) : uint32_t(16 * kRow);
             ptx::mbar_arrive_expect_tx(&full[slot], sub * uint32_t(it.ntq));
+            int ti = it.tap / a.kconv, tj = it.tap - ti * a.kconv;  // one division per step
             for (int q = 0; q < it.ntq; ++q) {
-              const int tp = it.tap + q, ti = tp / a.kconv, tj = tp - ti * a.kconv;
               ptx::tma_load_im2col_4d(tiles + slot * 16 * kRow + q * sub, &map, &full[slot], it.col0,
                                       wo * a.cstr - a.cpad, ho * a.cstr - a.cpad, it.s, uint16_t(tj),
                                       uint16_t(ti));
+              if (++tj == a.kconv) { tj = 0; ++ti; }
             }
           } else if (rgp) {
             const int rb = (it.gb0 + it.bl) * a.tq;
@@ -935,7 +948,7 @@ void launch_one(const CUtensorMap& map, Args a, cudaStream_t stream) {
   if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kThreads, smem) != cudaSuccess ||
       per_sm < 1)
     per_sm = 1;
-  if (per_sm > 4) per_sm = 4;  // 5 resident CTAs measured no faster (more tail per item)
+  if (per_sm > HLQ_TR_MINB) per_sm = HLQ_TR_MINB;  // 5 resident CTAs measured no faster (more tail per item)
   static const int knob_cps = env_knob("HLQ_TR_CTAS_PER_SM");  // development sweeps
   if (knob_cps >= 1 && knob_cps < per_sm) per_sm = knob_cps;
 
