@@ -107,6 +107,13 @@ struct Args {
   // tap q of the group in columns [q*C, q*C + C) of the tile, stored as tq
   // dense 16 x C sub-tiles (im2col boxes of C channels); tq = 1 otherwise
   int tq, cch;
+  // conv ACBP row sharing (stride 1, pad (k-1)/2, Wo % 16 == 0, rank 8): a block of
+  // 16 output pixels of row ho and tap (i, j) holds input row ho + i - pad, so tap
+  // row i's vectors are tap row `pad`'s vectors shifted by (pad - i) output rows.
+  // Only taps [tap0, tap0 + ntap_c) (the middle row) are transformed; the flush
+  // writes each block's codes to the other tap rows at the shifted block (zeros
+  // where the shifted row falls in the padding).  sh_blk = Wo / 16.
+  int tap0, ntap_c, share, sh_blk;
   // row groups (Linear / gy sources with cols = 32 / 64 / 128, taps == 0): a
   // step holds tq = 256 / cols consecutive 16-row blocks as tq dense 16 x cols
   // sub-tiles; items count `vblocks` = ceil(total_blocks / tq) block groups
@@ -159,10 +166,10 @@ struct StepIter {
     tap = 0;
     ntq = 1;
     if (a.taps) {  // tap groups innermost: concurrent CTAs reuse the same x pixels through L2
-      const int ntg = (a.taps + a.tq - 1) / a.tq;
+      const int ntg = (a.ntap_c + a.tq - 1) / a.tq;
       rest = item / ntg;
-      tap = (item - rest * ntg) * a.tq;
-      ntq = min(a.tq, a.taps - tap);
+      tap = a.tap0 + (item - rest * ntg) * a.tq;
+      ntq = min(a.tq, a.tap0 + a.ntap_c - tap);
     }
     const int g = rest / a.ncol_tiles;
     grp = g;
@@ -244,6 +251,27 @@ __device__ __forceinline__ void read16x2(uint32_t pa, uint32_t pb, float2 (&p)[1
       p[4 * q + 2] = make_float2(__uint_as_float(ta.z), __uint_as_float(tb.z));
       p[4 * q + 3] = make_float2(__uint_as_float(ta.w), __uint_as_float(tb.w));
     }
+  }
+}
+
+// Conv ACBP row sharing (Args::share): the rank-8 codes of block gb of payload
+// row pr (tap (pad, j), channel c) are also the codes of tap (i, j) at the block
+// (pad - i) output rows further (same image); rows whose source would be the
+// padding get zeros, written by the block of the same output row.
+__device__ __forceinline__ void share_copy(const Args& a, int64_t pr, int gb, uint2 v) {
+  const int img = gb / a.nblk, lb = gb - img * a.nblk;
+  const int ho = lb / a.sh_blk, ho_n = a.rows / (16 * a.sh_blk);  // output rows per image
+  const int pad = a.tap0 / a.kconv;
+  for (int i = 0; i < a.kconv; ++i) {
+    if (i == pad) continue;
+    const int64_t row = pr + int64_t(i - pad) * a.kconv;
+    const int hd = ho + (pad - i);  // destination output row holding this vector
+    if (hd >= 0 && hd < ho_n)
+      *reinterpret_cast<uint2*>(a.dst_gw + row * a.ld_gw + int64_t(gb + (pad - i) * a.sh_blk) * 8) = v;
+    // the destination row ho of tap row i whose source row lies in the padding
+    const int src = ho + i - pad;
+    if (src < 0 || src >= ho_n)
+      *reinterpret_cast<uint2*>(a.dst_gw + row * a.ld_gw + int64_t(gb) * 8) = make_uint2(0u, 0u);
   }
 }
 
@@ -632,15 +660,22 @@ __device__ __forceinline__ void consume(const Args& a, const Quant& qx, const Qu
         const bool chpow2 = (chunks & (chunks - 1)) == 0;
         for (int i = ftid; i < ncols * chunks; i += kFlushThreads) {
           const int c = chpow2 ? (i >> chsh) : i / chunks, q = i - c * chunks;
-          *reinterpret_cast<uint4*>(a.dst_gw + prow(c) * a.ld_gw + k0 + 16 * q) =
-              *reinterpret_cast<const uint4*>(cbuf + c * a.cstride + 16 * q);
+          const uint4 v = *reinterpret_cast<const uint4*>(cbuf + c * a.cstride + 16 * q);
+          const int64_t pr = prow(c);
+          *reinterpret_cast<uint4*>(a.dst_gw + pr * a.ld_gw + k0 + 16 * q) = v;
+          if (a.share) {
+            share_copy(a, pr, it.gb0 + 2 * q, make_uint2(v.x, v.y));
+            share_copy(a, pr, it.gb0 + 2 * q + 1, make_uint2(v.z, v.w));
+          }
         }
       } else if ((run & 7) == 0 && (k0 & 7) == 0) {
         const int chunks = run >> 3;
         for (int i = ftid; i < ncols * chunks; i += kFlushThreads) {
           const int c = i / chunks, q = i - c * chunks;
-          *reinterpret_cast<uint2*>(a.dst_gw + prow(c) * a.ld_gw + k0 + 8 * q) =
-              *reinterpret_cast<const uint2*>(cbuf + c * a.cstride + 8 * q);
+          const uint2 v = *reinterpret_cast<const uint2*>(cbuf + c * a.cstride + 8 * q);
+          const int64_t pr = prow(c);
+          *reinterpret_cast<uint2*>(a.dst_gw + pr * a.ld_gw + k0 + 8 * q) = v;
+          if (a.share) share_copy(a, pr, it.gb0 + q, v);
         }
       } else {
         for (int i = ftid; i < ncols * run; i += kFlushThreads) {
@@ -1146,13 +1181,26 @@ bool launch_conv_acbp_tma(const void* x, int dtype, int B, int H, int W, int C, 
   a.cch = C;
   a.vblocks = a.total_blocks;
   a.cbw = kCols;
-  const int ntg = (a.taps + tq - 1) / tq;  // tap groups per (pixel block, column tile)
+  // row sharing (see Args): only the middle tap row is transformed
+  static const bool noshare = env_knob("HLQ_CONV_NOSHARE") == 1;
+  const bool share = !noshare && stride == 1 && (k & 1) && pad == (k - 1) / 2 && k > 1 && Ho == H &&
+                     Wo % 16 == 0 && a.rank == 8;
+  a.tap0 = share ? pad * k : 0;
+  a.ntap_c = share ? k : a.taps;
+  a.sh_blk = Wo / 16;
+  const int ntg = (a.ntap_c + tq - 1) / tq;  // tap groups per (pixel block, column tile)
   {
     int nb = a.rank >= 8 ? 4 : (a.rank >= 4 ? 8 : 16);
     while (nb > 1 && ((a.total_blocks + nb - 1) / nb) * a.ncol_tiles * ntg < num_sms() * 3) nb >>= 1;
     a.nb = nb;
   }
-  a.items = ((a.total_blocks + a.nb - 1) / a.nb) * a.ncol_tiles * ntg;
+  // the flush addresses whole items inside one image (blocks per image a multiple of nb)
+  a.share = share && a.nblk % a.nb == 0 ? 1 : 0;
+  if (share && !a.share) {
+    a.tap0 = 0;
+    a.ntap_c = a.taps;
+  }
+  a.items = ((a.total_blocks + a.nb - 1) / a.nb) * a.ncol_tiles * ((a.ntap_c + tq - 1) / tq);
   a.bitmap = bitmap;
   a.bits_gx = bits;
   a.bits_gw = bits;

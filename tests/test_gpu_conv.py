@@ -58,7 +58,10 @@ def test_golden_conv(conv, case):
 
 @pytest.mark.parametrize("B,C,H,O,k,s,p", [
     (16, 256, 14, 256, 3, 1, 1),   # BASELINE config (b) geometry, 16 of its 128 images
-    (8, 64, 32, 64, 3, 1, 1),      # ResNet-18 CIFAR stage 1
+    (8, 64, 32, 64, 3, 1, 1),      # ResNet-18 CIFAR stage 1 (ACBP row sharing: Wo % 16 == 0)
+    (4, 128, 16, 128, 3, 1, 1),    # row sharing, 2 taps per step, one block per output row
+    (2, 256, 16, 256, 3, 1, 1),    # row sharing, one tap per 256-channel step
+    (2, 32, 32, 32, 5, 1, 2),      # row sharing, 5x5 (8 taps per step)
     (8, 64, 32, 128, 3, 2, 1),     # stage-2 downsampling conv
     (8, 64, 32, 128, 1, 2, 0),     # 1x1 shortcut
     (4, 3, 32, 64, 3, 1, 1),       # stem (C = 3: unaligned channel rows)
