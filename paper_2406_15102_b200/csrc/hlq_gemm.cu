@@ -1393,7 +1393,10 @@ int launch_conv_dgrad_i8(const int8_t* G, int64_t ldg, int64_t B, int64_t Ho, in
           return -1;
       }
       const int64_t M = B * Hp * Wp;
-      const int bn = (C > 128 && ((M + kBM - 1) / kBM) * ((C + 255) / 256) >= num_sms()) ? 256 : 128;
+      // narrow outputs (C <= 64, the ResNet CIFAR stage 1): 128 x 64 tiles, no half-empty N
+      static const int knob_bn64 = env_knob("HLQ_GEMM_DGRAD_BN64");  // development A/B
+      const int bn = (C > 128 && ((M + kBM - 1) / kBM) * ((C + 255) / 256) >= num_sms()) ? 256
+                     : (C <= 64 && knob_bn64 != 0) ? 64 : 128;
       {
         // W codes (C*k*k rows of ldw bytes, K = o), this phase's taps (i0 + s ti, j0 + s tj):
         // dims (O, kw, kh, C), strides (s ldw, s k ldw, k^2 ldw)
@@ -1409,8 +1412,10 @@ int launch_conv_dgrad_i8(const int8_t* G, int64_t ldg, int64_t B, int64_t Ho, in
       const ConvGeo geo{1, int(Hp), int(Wp), kh, kw, lo_h, lo_w, nkc, s, ph, pw, int(H), int(W)};
       const int e = bn == 256 ? run_maps<256, 4>(ma, mb, M, C, O, 1, sa, sb, 1.0, epilogue, out, out_dtype, ldo,
                                                  acc_out, ld_acc, 1, nullptr, geo, stream)
-                              : run_maps<128, 6>(ma, mb, M, C, O, 1, sa, sb, 1.0, epilogue, out, out_dtype, ldo,
-                                                 acc_out, ld_acc, 1, nullptr, geo, stream);
+                    : bn == 64  ? run_maps<64, 8>(ma, mb, M, C, O, 1, sa, sb, 1.0, epilogue, out, out_dtype, ldo,
+                                                  acc_out, ld_acc, 1, nullptr, geo, stream)
+                                : run_maps<128, 6>(ma, mb, M, C, O, 1, sa, sb, 1.0, epilogue, out, out_dtype, ldo,
+                                                   acc_out, ld_acc, 1, nullptr, geo, stream);
       if (e != 0) return e;
     }
   return 0;
